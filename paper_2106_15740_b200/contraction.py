@@ -1,0 +1,225 @@
+"""Bucket-elimination contraction on B200 — the drop-in boundary.
+
+`contract(network, order, rank_cap=DEFAULT_RANK_CAP)` keeps the signature,
+return type (Python complex) and error behaviour of the reference entry
+point /root/reference/pkg/src/qtnsim/contraction.py:114-123:
+
+  * ValueError if `order` is not a permutation of the unfixed variables
+    (contraction.py:60-62);
+  * RankCapExceeded(rank, cap) — a RuntimeError — raised while compiling the
+    plan, i.e. before any device allocation (contraction.py:32-39, 85-87);
+  * `_contract_with_ranks` returns (value, step_ranks) whose peak equals the
+    CostReport width of the same order.
+
+Evaluation differs from the reference only in *how* each bucket runs: the
+plan compiler (csrc/qtn_plan.cpp) turns the order into a bucket program and
+one of two sm_100a executors runs it — a warp-per-network shared-memory
+interpreter for networks whose whole live set fits on chip, or fused
+per-bucket kernels over an HBM arena.  There is no CPU fallback: without a
+CUDA device these functions raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .network import TensorNetwork, sliced_tensors
+from .ordering import ContractionOrder
+
+__all__ = [
+    "DEFAULT_RANK_CAP",
+    "DEFAULT_MIXED_RANK",
+    "DEFAULT_SMEM_BUDGET",
+    "RankCapExceeded",
+    "ContractionPlan",
+    "contract",
+    "contract_many",
+]
+
+DEFAULT_RANK_CAP = 30
+# complex64 storage applies to intermediates of rank >= this (SURVEY §7:
+# all-complex64 fails 1e-5 on config 4; rank >= 10..14 keeps ~1e-8)
+DEFAULT_MIXED_RANK = 12
+# shared memory one network may use in the warp-resident executor
+DEFAULT_SMEM_BUDGET = 100 * 1024
+
+
+class RankCapExceeded(RuntimeError):
+    """An intermediate tensor would exceed the rank cap; contraction aborted
+    before allocation."""
+
+    def __init__(self, rank: int, cap: int):
+        super().__init__(f"intermediate of rank {rank} exceeds rank cap {cap}")
+        self.rank = rank
+        self.cap = cap
+
+
+def _dtype_code(dtype) -> int:
+    name = str(dtype).replace("torch.", "").replace("numpy.", "")
+    if name in ("complex64", "c64", "cfloat", "<class 'numpy.complex64'>"):
+        return N.DTYPE_C64
+    if name in ("complex128", "c128", "cdouble", "complex", "<class 'numpy.complex128'>",
+                "<class 'complex'>"):
+        return N.DTYPE_C128
+    raise ValueError(f"unsupported dtype {dtype!r}; use complex64 or complex128")
+
+
+class ContractionPlan:
+    """A compiled (sliced-network structure, elimination order) pair.
+
+    The structure is the list of variable tuples of `sliced_tensors` in
+    network order; data is supplied at execution time as one packed
+    complex128 buffer (tensor k at `input_offsets[k]`).
+    """
+
+    def __init__(self, structure, variable_count, fixed, sequence, rank_cap=DEFAULT_RANK_CAP,
+                 dtype="complex128", mixed_rank=DEFAULT_MIXED_RANK,
+                 smem_budget=DEFAULT_SMEM_BUDGET):
+        self._h = None
+        ranks = np.asarray([len(s) for s in structure] or [0], dtype=np.int32)
+        offs = np.zeros(len(structure) + 1, dtype=np.int32)
+        offs[1:] = np.cumsum([len(s) for s in structure])
+        flat = np.asarray([v for s in structure for v in s] or [0], dtype=np.int32)
+        is_fixed = np.zeros(max(variable_count, 1), dtype=np.uint8)
+        for v in fixed:
+            is_fixed[v] = 1
+        seq = np.asarray(list(sequence) or [0], dtype=np.int32)
+        desc = N.NetworkDesc(len(structure), N.i32(ranks), N.i32(offs), N.i32(flat),
+                             variable_count, N.u8(is_fixed))
+        h = C.c_void_p()
+        bad = C.c_int32(0)
+        rc = N.lib.qtn_plan_create(C.byref(desc), N.i32(seq), len(sequence), int(rank_cap),
+                                   _dtype_code(dtype), int(mixed_rank), int(smem_budget),
+                                   C.byref(h), C.byref(bad))
+        if rc == N.QTN_ERANKCAP:
+            raise RankCapExceeded(int(bad.value), int(rank_cap))
+        N.check(rc, "plan compile")
+        self._h = h
+        info = N.PlanInfo()
+        N.check(N.lib.qtn_plan_info(h, C.byref(info)))
+        self.executor = int(info.executor)
+        self.n_buckets = int(info.n_buckets)
+        self.n_empty_buckets = int(info.n_empty_buckets)
+        self.width = int(info.width)
+        self.input_elems = int(info.input_elems)
+        self.workspace_bytes = int(info.workspace_bytes)
+        self.smem_bytes = int(info.smem_bytes)
+        self.program_bytes = int(info.program_bytes)
+        self.alg_bytes = float(info.alg_bytes)
+        self.flops_sum = float(info.flops_sum)
+        sr = np.zeros(max(len(sequence), 1), dtype=np.int32)
+        N.check(N.lib.qtn_plan_step_ranks(h, N.i32(sr)))
+        self.step_ranks = tuple(int(x) for x in sr[: len(sequence)])
+        io = np.zeros(max(len(structure), 1), dtype=np.int64)
+        N.check(N.lib.qtn_plan_input_offsets(h, N.i64(io)))
+        self.input_offsets = io[: len(structure)].copy()
+        self.n_inputs = len(structure)
+
+    @classmethod
+    def from_network(cls, network: TensorNetwork, order: ContractionOrder, **kw):
+        sl = sliced_tensors(network)
+        plan = cls([t.variables for t in sl], network.variable_count, network.fixed,
+                   order.sequence, **kw)
+        return plan, sl
+
+    @property
+    def handle(self):
+        return self._h
+
+    def pack(self, datas, out: np.ndarray | None = None) -> np.ndarray:
+        """Pack sliced tensor data (network order) into the input layout."""
+        buf = out if out is not None else np.empty(self.input_elems, dtype=np.complex128)
+        for off, d in zip(self.input_offsets, datas):
+            flat = np.asarray(d, dtype=np.complex128).reshape(-1)
+            buf[off: off + flat.size] = flat
+        return buf
+
+    def execute(self, inputs_ptr: int, workspace_ptr: int, result_ptr: int, stream: int) -> None:
+        N.check(N.lib.qtn_plan_execute(self._h, inputs_ptr, workspace_ptr or None, result_ptr,
+                                       stream), "plan execute")
+
+    def __del__(self):
+        if self._h is not None and N is not None and N.lib is not None:
+            N.lib.qtn_plan_destroy(self._h)
+            self._h = None
+
+
+def _torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("a CUDA device is required: the B200 backend has no CPU fallback")
+    return torch
+
+
+def _run_plans(plans, datas_list):
+    """Execute plans (SMEM ones batched in one launch); returns complex list."""
+    torch = _torch_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream(dev)
+    results = torch.zeros(len(plans), dtype=torch.complex128, device=dev)
+    smem = [i for i, p in enumerate(plans) if p.executor == N.EXEC_SMEM]
+    hbm = [i for i, p in enumerate(plans) if p.executor == N.EXEC_HBM]
+    if smem:
+        arr = (C.c_void_p * len(smem))(*[plans[i].handle for i in smem])
+        b = C.c_void_p()
+        N.check(N.lib.qtn_batch_create(arr, len(smem), C.byref(b)), "batch create")
+        try:
+            nel = C.c_int64()
+            N.check(N.lib.qtn_batch_input_elems(b, C.byref(nel)))
+            offs = np.zeros(len(smem), dtype=np.int64)
+            N.check(N.lib.qtn_batch_input_offsets(b, N.i64(offs)))
+            host = np.zeros(max(nel.value, 1), dtype=np.complex128)
+            for k, i in enumerate(smem):
+                plans[i].pack(datas_list[i], host[offs[k]: offs[k] + plans[i].input_elems])
+            inp = torch.from_numpy(host).pin_memory().to(dev, non_blocking=True)
+            res = torch.empty(len(smem), dtype=torch.complex128, device=dev)
+            N.check(N.lib.qtn_batch_execute(b, inp.data_ptr(), 0, 1, res.data_ptr(),
+                                            stream.cuda_stream), "batch execute")
+            results[smem] = res
+            torch.cuda.current_stream(dev).synchronize()
+        finally:
+            N.lib.qtn_batch_destroy(b)
+    for i in hbm:
+        p = plans[i]
+        host = p.pack(datas_list[i])
+        inp = torch.from_numpy(host).pin_memory().to(dev, non_blocking=True)
+        ws = torch.empty(max(p.workspace_bytes, 16), dtype=torch.uint8, device=dev)
+        res = torch.empty(1, dtype=torch.complex128, device=dev)
+        p.execute(inp.data_ptr(), ws.data_ptr(), res.data_ptr(), stream.cuda_stream)
+        results[i] = res[0]
+    out = results.cpu().numpy()
+    return [complex(x) for x in out]
+
+
+def _contract_with_ranks(network: TensorNetwork, order: ContractionOrder, rank_cap: int,
+                         dtype="complex128", **kw):
+    unfixed = network.unfixed_variables()
+    if sorted(order.sequence) != list(unfixed):
+        raise ValueError("order is not a permutation of the network's unfixed variables")
+    plan, sl = ContractionPlan.from_network(network, order, rank_cap=rank_cap, dtype=dtype, **kw)
+    (value,) = _run_plans([plan], [[t.data for t in sl]])
+    return value, list(plan.step_ranks)
+
+
+def contract(network: TensorNetwork, order: ContractionOrder, rank_cap: int = DEFAULT_RANK_CAP,
+             dtype="complex128", **kw) -> complex:
+    """Contract all unfixed variables along `order` on the GPU; returns the
+    amplitude.  Raises RankCapExceeded before allocating any intermediate
+    whose rank would exceed `rank_cap`."""
+    value, _ = _contract_with_ranks(network, order, rank_cap, dtype=dtype, **kw)
+    return value
+
+
+def contract_many(networks, orders, rank_cap: int = DEFAULT_RANK_CAP, dtype="complex128", **kw):
+    """Contract independent networks; shared-memory-resident ones run as one
+    batched launch (one warp per network)."""
+    plans, datas = [], []
+    for net, order in zip(networks, orders):
+        plan, sl = ContractionPlan.from_network(net, order, rank_cap=rank_cap, dtype=dtype, **kw)
+        plans.append(plan)
+        datas.append([t.data for t in sl])
+    return _run_plans(plans, datas)

@@ -1,0 +1,165 @@
+// Internal structures shared by the host plan compiler (qtn_plan.cpp) and the
+// sm_100a kernels (qtn_kernels.cu).  Not part of the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/qtn_b200.h"
+
+namespace qtn {
+
+// ---------------------------------------------------------------- bit runs
+// An operand's flat index is a bit-gather of the output index o:
+//   idx(o, v) = sum_k ((o >> src_k) & (2^len_k - 1)) << dst_k  +  v << vshift
+// Consecutive variables that sit on consecutive bits of both o and the
+// operand collapse into one run, so an operand aligned with the output
+// (the primary operand) costs two runs.  Packed as src | dst<<8 | len<<16.
+inline uint32_t pack_run(uint32_t src, uint32_t dst, uint32_t len) {
+  return src | (dst << 8) | (len << 16);
+}
+
+constexpr int kMaxRuns = 32;   // >= max rank handled (w <= 32)
+constexpr int kMaxG = 8;       // streamed/gathered operands per bucket
+constexpr int kMaxT = 4;       // smem lookup tables per bucket
+constexpr int kMaxTOps = 24;   // small operands folded into tables
+constexpr int kTBits = 8;      // non-v bits per lookup table
+constexpr int kTileBits = 12;  // output elements per tile = 2^kTileBits
+
+struct GOpArg {                // operand read from global memory
+  const void* ptr;
+  uint32_t vshift;             // bit of v in the operand index
+  uint32_t c64;
+  uint32_t n_lo, n_hi;         // runs on tile-local bits / on tile bits
+  uint32_t lo[kMaxRuns];
+  uint32_t hi[kMaxRuns];
+};
+
+struct TOpArg {                // small operand folded into a table
+  const void* ptr;
+  uint32_t vshift;
+  uint32_t c64;
+  uint32_t n_runs;
+  uint32_t runs[kTBits];       // table-index bits -> operand index bits
+};
+
+struct TableArg {
+  uint32_t nbits;              // table has 2^(nbits+1) entries (v is the LSB)
+  uint32_t n_lo, n_hi;
+  uint32_t lo[kTBits];         // output bits -> table index (tile-local part)
+  uint32_t hi[kTBits];
+  uint32_t first_op, n_ops;
+  uint32_t smem_off;           // in complex128 entries
+};
+
+struct BucketArgs {
+  void* out;
+  uint64_t n_out;              // 2^R
+  uint32_t R;
+  uint32_t out_c64;
+  uint32_t primary;            // op 0 is aligned with the output low bits
+  uint32_t p_k;                // bit position of v in the primary operand
+  uint32_t ng, nt, ntop;
+  uint32_t table_entries;      // total smem table entries
+  GOpArg g[kMaxG];
+  TableArg t[kMaxT];
+  TOpArg top[kMaxTOps];
+};
+
+// ---------------------------------------------------- SMEM executor program
+// One network = one warp.  Program blob, 16-byte aligned sections:
+//   SmemHeader | SmemBucket[n_buckets] | SmemOp[n_ops] | u16 scalars[n_scalars]
+// All offsets are complex128-element offsets into the warp's data region
+// (packed inputs first, then the intermediate arena).
+struct SmemHeader {
+  uint32_t n_buckets;
+  uint32_t n_ops;
+  uint32_t n_scalars;
+  uint32_t pow2;               // number of empty buckets (factor 2 each)
+  uint32_t in_elems;           // packed input elements (complex128)
+  uint32_t data_elems;         // inputs + arena
+  uint32_t prog_bytes;         // whole blob, multiple of 16
+  uint32_t pad;
+};
+struct SmemBucket {
+  uint16_t out_off;
+  uint8_t R;
+  uint8_t n_ops;
+  uint16_t first_op;
+  uint16_t pad;
+};
+constexpr int kSmemOpRuns = 14;
+struct SmemOp {
+  uint16_t off;
+  uint8_t vshift;
+  uint8_t n_runs;
+  uint16_t runs[kSmemOpRuns];  // src | dst<<5 | len<<10
+};
+static_assert(sizeof(SmemHeader) == 32, "header");
+static_assert(sizeof(SmemBucket) == 8, "bucket");
+static_assert(sizeof(SmemOp) == 32, "op");
+
+// ------------------------------------------------------------- host plan
+struct TensorRec {
+  std::vector<int32_t> vars;   // layout, most significant first
+  bool input = false;
+  int64_t in_off = 0;          // packed-input element offset (inputs)
+  int64_t ws_off = -1;         // workspace byte offset (HBM intermediates)
+  int64_t sm_off = -1;         // SMEM data-region element offset
+  bool c64 = false;            // storage type (HBM intermediates)
+  int32_t born = -1;           // bucket index that produces it (-1: input)
+  int32_t last_use = -1;       // bucket index that consumes it (n: final fold)
+  int rank() const { return (int)vars.size(); }
+};
+
+struct BucketRec {
+  int32_t v;
+  std::vector<int32_t> ops;    // tensor ids, ascending (reference order)
+  int32_t primary;             // index into ops
+  int32_t out;                 // tensor id of the result
+  int32_t rank;                // output rank
+};
+
+}  // namespace qtn
+
+struct qtn_plan {
+  std::vector<qtn::TensorRec> tensors;   // inputs, then intermediates
+  std::vector<qtn::BucketRec> buckets;
+  std::vector<int32_t> step_ranks;       // per order entry
+  std::vector<int32_t> scalars;          // rank-0 tensors folded at the end
+  int32_t n_inputs = 0;
+  int32_t n_empty = 0;
+  int32_t width = 0;
+  int32_t executor = QTN_EXEC_HBM;
+  int64_t input_elems = 0;
+  int64_t workspace_bytes = 0;
+  int64_t smem_bytes = 0;
+  double alg_bytes = 0.0;
+  double flops_sum = 0.0;
+  std::vector<uint8_t> program;          // SMEM executor blob
+  std::vector<qtn::BucketArgs> hbm_args; // HBM executor launch templates
+                                         // (pointers hold offsets; patched
+                                         // at execute time)
+  qtn_batch* self_batch = nullptr;       // device copy of `program` for
+                                         // single-plan SMEM execution
+  ~qtn_plan();
+};
+
+namespace qtn {
+void set_error(const std::string& msg);
+// device-side launchers (qtn_kernels.cu)
+int launch_bucket(const BucketArgs& a, void* stream);
+int launch_fold(const void* const* ptrs, const uint8_t* c64, int n, int pow2,
+                void* result, bool accumulate, void* stream);
+int launch_smem_batch(const void* programs, const uint64_t* prog_offsets,
+                      const uint64_t* in_offsets, int n_nets, const void* inputs,
+                      int64_t set_elems, int n_sets, void* results, int64_t max_smem,
+                      void* stream);
+int device_alloc(void** p, size_t bytes);
+int device_free(void* p);
+int h2d(void* dst, const void* src, size_t bytes);
+int device_check();
+// pure host helpers (qtn_plan.cpp)
+void make_runs(const std::vector<std::pair<int, int>>& src_dst, std::vector<uint32_t>& runs);
+}  // namespace qtn

@@ -1,0 +1,560 @@
+// sm_100a kernels of the bucket-elimination backend.
+//
+//  * bucket_kernel     — one fused bucket over HBM: out[o] = sum_v prod_t T_t[idx_t(o,v)]
+//                        (replaces the `_product` einsum chain + `.sum`,
+//                        /root/reference/pkg/src/qtnsim/contraction.py:42-54, 90-96).
+//                        The primary operand streams aligned with the output
+//                        (16-byte vector loads), small operands are pre-multiplied
+//                        into shared-memory lookup tables, the v-sum happens in
+//                        registers, arithmetic in float64.
+//  * smem_net_kernel   — a whole small network per warp, resident in shared
+//                        memory: program, packed inputs and intermediates; one
+//                        launch for many networks x many angle sets.
+//  * tensorgen_kernel  — gate tensors generated on device from the angles
+//                        (circuit.py:186-205 conventions, network.py:153-165 slicing).
+//  * fold / energy     — scalar fold (contraction.py:77-81, 108-110) and the
+//                        MaxCut energy sum.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "qtn_internal.h"
+
+using namespace qtn;
+
+namespace {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 ld_c(const void* p, uint64_t i, uint32_t c64) {
+  if (c64) {
+    float2 f = __ldg(reinterpret_cast<const float2*>(p) + i);
+    return make_double2(f.x, f.y);
+  }
+  return __ldg(reinterpret_cast<const double2*>(p) + i);
+}
+__device__ __forceinline__ void st_c(void* p, uint64_t i, uint32_t c64, double2 v) {
+  if (c64)
+    reinterpret_cast<float2*>(p)[i] = make_float2((float)v.x, (float)v.y);
+  else
+    reinterpret_cast<double2*>(p)[i] = v;
+}
+__device__ __forceinline__ uint64_t gather64(uint64_t o, const uint32_t* runs, uint32_t n) {
+  uint64_t idx = 0;
+  for (uint32_t r = 0; r < n; ++r) {
+    const uint32_t w = runs[r];
+    const uint32_t s = w & 0xff, d = (w >> 8) & 0xff, l = (w >> 16) & 0xff;
+    idx |= ((o >> s) & ((1ull << l) - 1)) << d;
+  }
+  return idx;
+}
+__device__ __forceinline__ uint64_t gather_lo(uint32_t e, const uint32_t* runs, uint32_t n) {
+  uint64_t idx = 0;
+  for (uint32_t r = 0; r < n; ++r) {
+    const uint32_t w = runs[r];
+    const uint32_t s = w & 0xff, d = (w >> 8) & 0xff, l = (w >> 16) & 0xff;
+    idx |= (uint64_t)((e >> s) & ((1u << l) - 1)) << d;
+  }
+  return idx;
+}
+
+constexpr int kThreads = 256;
+
+// Element-wise body shared by both kernel variants: accumulate every
+// non-primary operand (gathered or tabulated) for output o = obase + e.
+__device__ __forceinline__ void accumulate_rest(const BucketArgs& a, uint32_t g_first, uint32_t e,
+                                                const uint64_t* gbase, const uint32_t* tbase,
+                                                const double2* tab, double2& a0, double2& a1) {
+#pragma unroll
+  for (int i = 0; i < kMaxG; ++i) {
+    if (i < (int)g_first || i >= (int)a.ng) continue;
+    const GOpArg& g = a.g[i];
+    const uint64_t idx = gbase[i] + gather_lo(e, g.lo, g.n_lo);
+    a0 = cmul(a0, ld_c(g.ptr, idx, g.c64));
+    a1 = cmul(a1, ld_c(g.ptr, idx + (1ull << g.vshift), g.c64));
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxT; ++j) {
+    if (j >= (int)a.nt) continue;
+    const TableArg& t = a.t[j];
+    const uint32_t ti = (tbase[j] | (uint32_t)gather_lo(e, t.lo, t.n_lo)) << 1;
+    const double2* tp = tab + t.smem_off + ti;
+    a0 = cmul(a0, tp[0]);
+    a1 = cmul(a1, tp[1]);
+  }
+}
+
+template <bool kFast>
+__global__ void __launch_bounds__(kThreads) bucket_kernel(const __grid_constant__ BucketArgs a) {
+  extern __shared__ double2 tab[];
+  // ---- lookup tables: T_j[bits, v] = prod over the folded small operands
+  for (uint32_t j = 0; j < a.nt; ++j) {
+    const TableArg& t = a.t[j];
+    const uint32_t n = 2u << t.nbits;
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+      const uint32_t bits = e >> 1, v = e & 1;
+      double2 acc = make_double2(1.0, 0.0);
+      for (uint32_t k = 0; k < t.n_ops; ++k) {
+        const TOpArg& op = a.top[t.first_op + k];
+        const uint64_t idx = gather_lo(bits, op.runs, op.n_runs) | ((uint64_t)v << op.vshift);
+        acc = cmul(acc, ld_c(op.ptr, idx, op.c64));
+      }
+      tab[t.smem_off + e] = acc;
+    }
+  }
+  __syncthreads();
+
+  const uint32_t tile_bits = a.R < (uint32_t)kTileBits ? a.R : (uint32_t)kTileBits;
+  const uint64_t n_tiles = a.n_out >> tile_bits;
+  const uint32_t tile_elems = 1u << tile_bits;
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint64_t obase = tile << tile_bits;
+    uint64_t gbase[kMaxG];
+    uint32_t tbase[kMaxT];
+#pragma unroll
+    for (int i = 0; i < kMaxG; ++i)
+      gbase[i] = i < (int)a.ng ? gather64(obase, a.g[i].hi, a.g[i].n_hi) : 0;
+#pragma unroll
+    for (int j = 0; j < kMaxT; ++j)
+      tbase[j] = j < (int)a.nt ? (uint32_t)gather64(obase, a.t[j].hi, a.t[j].n_hi) : 0;
+
+    if constexpr (kFast) {
+      // primary complex64, aligned, output complex64: two outputs per thread,
+      // 16-byte loads/stores.  tile_elems >= 2 here.
+      const GOpArg& p = a.g[0];
+      const float* P = reinterpret_cast<const float*>(p.ptr);
+      float* O = reinterpret_cast<float*>(a.out);
+      const uint64_t vstep = 1ull << a.p_k;
+#pragma unroll 4
+      for (uint32_t e = 2 * threadIdx.x; e < tile_elems; e += 2 * kThreads) {
+        const uint64_t idx = gbase[0] + gather_lo(e, p.lo, p.n_lo);
+        float4 x, y;
+        double2 a0, a1, b0, b1;  // (o,v=0) (o,v=1) (o+1,v=0) (o+1,v=1)
+        if (a.p_k == 0) {
+          x = __ldg(reinterpret_cast<const float4*>(P + 2 * idx));
+          y = __ldg(reinterpret_cast<const float4*>(P + 2 * (idx + 2)));
+          a0 = make_double2(x.x, x.y); a1 = make_double2(x.z, x.w);
+          b0 = make_double2(y.x, y.y); b1 = make_double2(y.z, y.w);
+        } else {
+          x = __ldg(reinterpret_cast<const float4*>(P + 2 * idx));
+          y = __ldg(reinterpret_cast<const float4*>(P + 2 * (idx + vstep)));
+          a0 = make_double2(x.x, x.y); b0 = make_double2(x.z, x.w);
+          a1 = make_double2(y.x, y.y); b1 = make_double2(y.z, y.w);
+        }
+        accumulate_rest(a, 1, e, gbase, tbase, tab, a0, a1);
+        accumulate_rest(a, 1, e + 1, gbase, tbase, tab, b0, b1);
+        const double2 r0 = cadd(a0, a1), r1 = cadd(b0, b1);
+        float4 r = make_float4((float)r0.x, (float)r0.y, (float)r1.x, (float)r1.y);
+        *reinterpret_cast<float4*>(O + 2 * (obase + e)) = r;
+      }
+    } else {
+      for (uint32_t e = threadIdx.x; e < tile_elems; e += kThreads) {
+        double2 a0 = make_double2(1.0, 0.0), a1 = a0;
+        accumulate_rest(a, 0, e, gbase, tbase, tab, a0, a1);
+        st_c(a.out, obase + e, a.out_c64, cadd(a0, a1));
+      }
+    }
+  }
+}
+
+int g_num_sms = 0;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
+  set_error(buf);
+  return QTN_ECUDA;
+}
+
+// ------------------------------------------------------- SMEM executor
+
+__device__ __forceinline__ uint32_t sgather(uint32_t e, const SmemOp& o) {
+  uint32_t idx = 0;
+  for (uint32_t r = 0; r < o.n_runs; ++r) {
+    const uint32_t w = o.runs[r];
+    const uint32_t s = w & 31, d = (w >> 5) & 31, l = (w >> 10) & 31;
+    idx |= ((e >> s) & ((1u << l) - 1)) << d;
+  }
+  return idx;
+}
+
+__device__ __forceinline__ void copy16(void* dst, const void* src, uint32_t bytes, int lane) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  const uint32_t n = bytes / 16;
+  uint32_t i = lane;
+  for (; i + 96 < n; i += 128) {
+    uint4 x0 = __ldg(s + i), x1 = __ldg(s + i + 32), x2 = __ldg(s + i + 64), x3 = __ldg(s + i + 96);
+    d[i] = x0; d[i + 32] = x1; d[i + 64] = x2; d[i + 96] = x3;
+  }
+  for (; i < n; i += 32) d[i] = __ldg(s + i);
+}
+
+// One warp executes one network's bucket program for one input set.
+__global__ void __launch_bounds__(32) smem_net_kernel(const uint8_t* __restrict__ progs,
+                                                      const uint64_t* __restrict__ prog_off,
+                                                      const uint64_t* __restrict__ in_off,
+                                                      int n_nets, const double2* __restrict__ inputs,
+                                                      int64_t set_elems, double2* __restrict__ results) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int net = blockIdx.x, set = blockIdx.y, lane = threadIdx.x;
+  const uint8_t* gp = progs + prog_off[net];
+  const SmemHeader h = *reinterpret_cast<const SmemHeader*>(gp);
+  copy16(sm, gp, h.prog_bytes, lane);
+  double2* D = reinterpret_cast<double2*>(sm + h.prog_bytes);
+  copy16(D, inputs + (int64_t)set * set_elems + in_off[net], h.in_elems * 16u, lane);
+  __syncwarp();
+  const SmemBucket* bk = reinterpret_cast<const SmemBucket*>(sm + sizeof(SmemHeader));
+  const SmemOp* ops = reinterpret_cast<const SmemOp*>(sm + sizeof(SmemHeader) +
+                                                      sizeof(SmemBucket) * h.n_buckets);
+  for (uint32_t bi = 0; bi < h.n_buckets; ++bi) {
+    const SmemBucket b = bk[bi];
+    const SmemOp* bo = ops + b.first_op;
+    const uint32_t n = 1u << b.R;
+    for (uint32_t e = lane; e < n; e += 32) {
+      const SmemOp& o0 = bo[0];
+      uint32_t idx = o0.off + sgather(e, o0);
+      double2 a0 = D[idx], a1 = D[idx + (1u << o0.vshift)];
+      for (uint32_t k = 1; k < b.n_ops; ++k) {
+        const SmemOp& o = bo[k];
+        idx = o.off + sgather(e, o);
+        a0 = cmul(a0, D[idx]);
+        a1 = cmul(a1, D[idx + (1u << o.vshift)]);
+      }
+      D[b.out_off + e] = cadd(a0, a1);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    const uint16_t* sc = reinterpret_cast<const uint16_t*>(
+        sm + sizeof(SmemHeader) + sizeof(SmemBucket) * h.n_buckets + sizeof(SmemOp) * h.n_ops);
+    double2 r = make_double2(ldexp(1.0, (int)h.pow2), 0.0);
+    for (uint32_t i = 0; i < h.n_scalars; ++i) r = cmul(r, D[sc[i]]);
+    results[(int64_t)set * n_nets + net] = r;
+  }
+}
+
+struct FoldArgs {
+  const void* ptrs[32];
+  uint8_t c64[32];
+};
+__global__ void fold_kernel_p(const __grid_constant__ FoldArgs f, int n, int pow2,
+                              double2* result, int accumulate) {
+  double2 r = accumulate ? *result : make_double2(ldexp(1.0, pow2), 0.0);
+  for (int i = 0; i < n; ++i) r = cmul(r, ld_c(f.ptrs[i], 0, f.c64[i]));
+  *result = r;
+}
+
+// ------------------------------------------------------- tensor generation
+
+__device__ double2 gate_entry(int kind, double t, uint32_t i, double sre, double sim) {
+  const double s = 0.70710678118654757;  // 1/sqrt(2), circuit.py:179
+  double sn, cs;
+  switch (kind) {
+    case QTN_GATE_INIT:
+      return make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+    case QTN_GATE_H:
+      return make_double2(i == 3 ? -s : s, 0.0);
+    case QTN_GATE_ZPOW:  // diag(1, e^{-it})
+      if (i == 0) return make_double2(1.0, 0.0);
+      if (i == 3) { sincos(t, &sn, &cs); return make_double2(cs, -sn); }
+      return make_double2(0.0, 0.0);
+    case QTN_GATE_ZPOW_DIAG:
+      if (i == 0) return make_double2(1.0, 0.0);
+      sincos(t, &sn, &cs);
+      return make_double2(cs, -sn);
+    case QTN_GATE_XPOW: {  // H diag(1, e) H = 1/2 [[1+e, 1-e], [1-e, 1+e]]
+      sincos(t, &sn, &cs);
+      const bool diag = (i == 0 || i == 3);
+      return diag ? make_double2(0.5 * (1.0 + cs), -0.5 * sn)
+                  : make_double2(0.5 * (1.0 - cs), 0.5 * sn);
+    }
+    case QTN_GATE_CNOT: {  // row = i >> 2, col = i & 3
+      const uint32_t row = i >> 2, col = i & 3;
+      const uint32_t img = row < 2 ? row : (row ^ 1);
+      return make_double2(col == img ? 1.0 : 0.0, 0.0);
+    }
+    case QTN_GATE_ZZ: {  // diag(r, r*, r*, r), r = e^{i g}
+      const uint32_t row = i >> 2, col = i & 3;
+      if (row != col) return make_double2(0.0, 0.0);
+      sincos(t, &sn, &cs);
+      return (row == 0 || row == 3) ? make_double2(cs, sn) : make_double2(cs, -sn);
+    }
+    case QTN_GATE_ZZ_DIAG: {
+      sincos(t, &sn, &cs);
+      return (i == 0 || i == 3) ? make_double2(cs, sn) : make_double2(cs, -sn);
+    }
+    case QTN_GATE_SCALAR:
+      return make_double2(sre, sim);
+  }
+  return make_double2(0.0, 0.0);
+}
+
+__global__ void tensorgen_kernel(const qtn_tensor_recipe* __restrict__ rec, int64_t n,
+                                 const double* __restrict__ angles, int n_angles,
+                                 int64_t set_elems, double2* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int set = blockIdx.y;
+  const qtn_tensor_recipe r = rec[k];
+  const double t = r.angle >= 0 ? r.scale * angles[(int64_t)set * n_angles + r.angle] + r.offset
+                                : r.offset;
+  const int fr = r.full_rank;
+  int kept = 0;
+  for (int q = 0; q < fr; ++q) kept += (r.keep_mask >> q) & 1;
+  double2* dst = out + (int64_t)set * set_elems + r.out_offset;
+  for (uint32_t e = 0; e < (1u << kept); ++e) {
+    uint32_t full = 0;
+    int kb = kept - 1;
+    for (int q = 0; q < fr; ++q) {  // position q is the (fr-1-q)th bit, MSB first
+      uint32_t bit;
+      if ((r.keep_mask >> q) & 1) bit = (e >> kb--) & 1;
+      else bit = (r.fixed_bits >> q) & 1;
+      full = (full << 1) | bit;
+    }
+    dst[e] = gate_entry(r.kind, t, full, r.scale, r.offset);
+  }
+}
+
+__global__ void energy_kernel(const double2* __restrict__ vals, int n, double* energies,
+                              double2* zz) {
+  const int s = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  double e = 0.0, zr = 0.0, zi = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double2 v = vals[(int64_t)s * n + i];
+    e += (1.0 - v.x) / 2.0;
+    zr += v.x;
+    zi += v.y;
+  }
+  if (energies) energies[s] = e;
+  if (zz) zz[s] = make_double2(zr, zi);
+}
+
+}  // namespace
+
+namespace qtn {
+
+int device_check() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    set_error("no CUDA device: the B200 backend has no CPU fallback");
+    return QTN_ENODEV;
+  }
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return QTN_OK;
+}
+
+int launch_bucket(const BucketArgs& a, void* stream) {
+  int rc = device_check();
+  if (rc) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint32_t tile_bits = a.R < (uint32_t)kTileBits ? a.R : (uint32_t)kTileBits;
+  const uint64_t n_tiles = a.n_out >> tile_bits;
+  const size_t smem = (size_t)a.table_entries * sizeof(double2);
+  const bool fast = a.primary && a.ng >= 1 && a.g[0].c64 && a.out_c64 && a.R >= 1;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(bucket_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(bucket_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr_set = true;
+  }
+  const uint64_t max_blocks = (uint64_t)g_num_sms * 8;
+  const unsigned blocks = (unsigned)std::min<uint64_t>(n_tiles, max_blocks);
+  if (fast)
+    bucket_kernel<true><<<blocks, kThreads, smem, st>>>(a);
+  else
+    bucket_kernel<false><<<blocks, kThreads, smem, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bucket_kernel launch");
+  return QTN_OK;
+}
+
+int launch_fold(const void* const* ptrs, const uint8_t* c64, int n, int pow2, void* result,
+                bool accumulate, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int done = 0;
+  bool acc = accumulate;
+  do {
+    FoldArgs f;
+    std::memset(&f, 0, sizeof(f));
+    const int m = std::min(32, n - done);
+    for (int i = 0; i < m; ++i) {
+      f.ptrs[i] = ptrs[done + i];
+      f.c64[i] = c64[done + i];
+    }
+    fold_kernel_p<<<1, 1, 0, st>>>(f, m, pow2, reinterpret_cast<double2*>(result), acc ? 1 : 0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "fold_kernel launch");
+    done += m;
+    acc = true;
+  } while (done < n);
+  return QTN_OK;
+}
+
+int device_alloc(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 16));
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaMalloc");
+    return QTN_ENOMEM;
+  }
+  return QTN_OK;
+}
+int device_free(void* p) {
+  if (p) cudaFree(p);
+  return QTN_OK;
+}
+int h2d(void* dst, const void* src, size_t bytes) {
+  cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy H2D");
+  return QTN_OK;
+}
+
+}  // namespace qtn
+
+// ------------------------------------------------------------- batches
+
+struct qtn_batch {
+  int n = 0;
+  uint8_t* d_prog = nullptr;
+  uint64_t* d_prog_off = nullptr;
+  uint64_t* d_in_off = nullptr;
+  int64_t set_elems = 0;
+  int64_t max_smem = 0;
+  std::vector<int64_t> in_offsets;
+};
+
+extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** out) {
+  if (!plans || n < 1 || !out) {
+    set_error("qtn_batch_create: bad arguments");
+    return QTN_EINVAL;
+  }
+  int rc = device_check();
+  if (rc) return rc;
+  std::vector<uint8_t> blob;
+  std::vector<uint64_t> poff(n), ioff(n);
+  qtn_batch* B = new qtn_batch();
+  B->n = n;
+  int64_t in = 0;
+  for (int i = 0; i < n; ++i) {
+    const qtn_plan* P = plans[i];
+    if (!P || P->executor != QTN_EXEC_SMEM) {
+      delete B;
+      set_error("qtn_batch_create: every plan must use the SMEM executor");
+      return QTN_EINVAL;
+    }
+    poff[i] = blob.size();
+    blob.insert(blob.end(), P->program.begin(), P->program.end());
+    ioff[i] = (uint64_t)in;
+    B->in_offsets.push_back(in);
+    in += (P->input_elems + 1) & ~1ll;  // keep every network 32-byte aligned
+    B->max_smem = std::max(B->max_smem, P->smem_bytes);
+  }
+  B->set_elems = in;
+  if ((rc = device_alloc((void**)&B->d_prog, blob.size())) ||
+      (rc = device_alloc((void**)&B->d_prog_off, n * sizeof(uint64_t))) ||
+      (rc = device_alloc((void**)&B->d_in_off, n * sizeof(uint64_t))) ||
+      (rc = h2d(B->d_prog, blob.data(), blob.size())) ||
+      (rc = h2d(B->d_prog_off, poff.data(), n * sizeof(uint64_t))) ||
+      (rc = h2d(B->d_in_off, ioff.data(), n * sizeof(uint64_t)))) {
+    qtn_batch_destroy(B);
+    return rc;
+  }
+  *out = B;
+  return QTN_OK;
+}
+
+extern "C" int qtn_batch_input_elems(const qtn_batch* B, int64_t* out) {
+  if (!B || !out) return QTN_EINVAL;
+  *out = B->set_elems;
+  return QTN_OK;
+}
+
+extern "C" int qtn_batch_input_offsets(const qtn_batch* B, int64_t* out) {
+  if (!B || !out) return QTN_EINVAL;
+  std::copy(B->in_offsets.begin(), B->in_offsets.end(), out);
+  return QTN_OK;
+}
+
+extern "C" int qtn_batch_execute(qtn_batch* B, const void* inputs, int64_t set_stride,
+                                 int32_t n_sets, void* results, void* stream) {
+  if (set_stride <= 0) set_stride = B ? B->set_elems : 0;
+  if (!B || !results || n_sets < 1 || n_sets > 65535) {
+    set_error("qtn_batch_execute: bad arguments");
+    return QTN_EINVAL;
+  }
+  int rc = device_check();
+  if (rc) return rc;
+  static int64_t attr = 0;
+  if (B->max_smem > 48 * 1024 && B->max_smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(smem_net_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)B->max_smem);
+    if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel attribute");
+    attr = B->max_smem;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  dim3 grid(B->n, n_sets);
+  smem_net_kernel<<<grid, 32, B->max_smem, st>>>(B->d_prog, B->d_prog_off, B->d_in_off, B->n,
+                                                 reinterpret_cast<const double2*>(inputs),
+                                                 set_stride, reinterpret_cast<double2*>(results));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel launch");
+  return QTN_OK;
+}
+
+extern "C" int qtn_batch_destroy(qtn_batch* B) {
+  if (!B) return QTN_OK;
+  device_free(B->d_prog);
+  device_free(B->d_prog_off);
+  device_free(B->d_in_off);
+  delete B;
+  return QTN_OK;
+}
+
+extern "C" int qtn_tensorgen(const qtn_tensor_recipe* recipes, int64_t n, const double* angles,
+                             int32_t n_angles, int32_t n_sets, int64_t set_elems, void* out,
+                             void* stream) {
+  if (n < 0 || n_sets < 1 || n_sets > 65535 || (n > 0 && (!recipes || !out))) {
+    set_error("qtn_tensorgen: bad arguments");
+    return QTN_EINVAL;
+  }
+  int rc = device_check();
+  if (rc) return rc;
+  if (n == 0) return QTN_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  dim3 grid((unsigned)((n + 127) / 128), n_sets);
+  tensorgen_kernel<<<grid, 128, 0, st>>>(recipes, n, angles, n_angles, set_elems,
+                                         reinterpret_cast<double2*>(out));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "tensorgen launch");
+  return QTN_OK;
+}
+
+extern "C" int qtn_energy_reduce(const void* values, int32_t n, int32_t n_sets, double* energies,
+                                 void* zz_sum, void* stream) {
+  if (!values || n < 0 || n_sets < 1) {
+    set_error("qtn_energy_reduce: bad arguments");
+    return QTN_EINVAL;
+  }
+  int rc = device_check();
+  if (rc) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  energy_kernel<<<n_sets, 32, 0, st>>>(reinterpret_cast<const double2*>(values), n, energies,
+                                       reinterpret_cast<double2*>(zz_sum));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "energy launch");
+  return QTN_OK;
+}

@@ -1,0 +1,714 @@
+// Plan compiler: (sliced network structure, elimination order) -> bucket
+// program for the sm_100a executors.  Pure host code (no GPU needed), so the
+// reference's argument errors and the rank cap fire before any allocation.
+//
+// Semantics follow the reference bucket loop
+//   _contract_with_ranks  /root/reference/pkg/src/qtnsim/contraction.py:57-111
+// step by step: the order must be a permutation of the unfixed variables
+// (60-62); bucket = ascending ids of the live tensors holding v (76); an empty
+// bucket multiplies by 2 (77-81); the union rank is checked against the cap
+// before anything is materialised (82-88); consumed tensors leave the live
+// set and the result enters it with a fresh id (98-106); rank-0 tensors fold
+// into the scalar at the end (108-110).  What differs is only HOW a bucket is
+// evaluated: one fused pass (product of all operands and the v-sum) instead
+// of the pairwise `_product` chain, with an output layout chosen so that the
+// largest operand streams contiguously.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "qtn_internal.h"
+
+namespace qtn {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+void make_runs(const std::vector<std::pair<int, int>>& src_dst, std::vector<uint32_t>& runs) {
+  // src_dst: (bit in source index, bit in destination index); merge runs
+  // where both advance by one.
+  std::vector<std::pair<int, int>> p = src_dst;
+  std::sort(p.begin(), p.end(), [](auto a, auto b) { return a.second < b.second; });
+  runs.clear();
+  size_t i = 0;
+  while (i < p.size()) {
+    int s = p[i].first, d = p[i].second, len = 1;
+    while (i + len < p.size() && p[i + len].first == s + len && p[i + len].second == d + len) ++len;
+    runs.push_back(pack_run((uint32_t)s, (uint32_t)d, (uint32_t)len));
+    i += len;
+  }
+}
+
+namespace {
+
+// Split runs of the output index into the tile-local part (bits < tile_bits)
+// and the per-tile part (bits >= tile_bits).
+void split_runs(const std::vector<std::pair<int, int>>& src_dst, int tile_bits,
+                std::vector<uint32_t>& lo, std::vector<uint32_t>& hi) {
+  std::vector<std::pair<int, int>> a, b;
+  for (auto& x : src_dst) (x.first < tile_bits ? a : b).push_back(x);
+  make_runs(a, lo);
+  make_runs(b, hi);
+}
+
+struct Block {
+  int64_t off, size;
+  int32_t start, end;  // inclusive lifetime in bucket steps
+};
+
+// First-fit placement on a (time x address) plane.
+int64_t place(std::vector<Block>& blocks, int64_t size, int32_t start, int32_t end,
+              int64_t align) {
+  std::vector<std::pair<int64_t, int64_t>> busy;
+  for (auto& b : blocks)
+    if (!(b.end < start || b.start > end)) busy.push_back({b.off, b.off + b.size});
+  std::sort(busy.begin(), busy.end());
+  int64_t off = 0;
+  for (auto& iv : busy) {
+    if (iv.first >= off + size) break;
+    off = std::max(off, (iv.second + align - 1) / align * align);
+  }
+  blocks.push_back({off, size, start, end});
+  return off;
+}
+
+int64_t elem_bytes(bool c64) { return c64 ? 8 : 16; }
+
+}  // namespace
+
+// Output layout rule: primary = first operand of maximal rank; variables
+// the primary lacks go on the most significant bits (union order), then the
+// primary's own variables minus v in the primary's order on the low bits.
+static void choose_layout(const std::vector<std::vector<int32_t>>& opvars, int32_t v,
+                          int32_t& primary, std::vector<int32_t>& out_vars) {
+  primary = 0;
+  for (size_t i = 1; i < opvars.size(); ++i)
+    if (opvars[i].size() > opvars[primary].size()) primary = (int32_t)i;
+  const auto& pv = opvars[primary];
+  std::vector<int32_t> uni;
+  for (auto& vs : opvars)
+    for (int32_t u : vs)
+      if (std::find(uni.begin(), uni.end(), u) == uni.end()) uni.push_back(u);
+  out_vars.clear();
+  for (int32_t u : uni)
+    if (u != v && std::find(pv.begin(), pv.end(), u) == pv.end()) out_vars.push_back(u);
+  for (int32_t u : pv)
+    if (u != v) out_vars.push_back(u);
+}
+
+// Operand index as (src bit in o, dst bit in operand) pairs + v's bit.
+static void operand_map(const std::vector<int32_t>& vars, const std::vector<int32_t>& out_vars,
+                        int32_t v, std::vector<std::pair<int, int>>& sd, int& vshift) {
+  const int R = (int)out_vars.size(), r = (int)vars.size();
+  sd.clear();
+  vshift = -1;
+  for (int k = 0; k < r; ++k) {
+    int dst = r - 1 - k;
+    if (vars[k] == v) {
+      vshift = dst;
+      continue;
+    }
+    int idx = (int)(std::find(out_vars.begin(), out_vars.end(), vars[k]) - out_vars.begin());
+    sd.push_back({R - 1 - idx, dst});
+  }
+}
+
+// Build the HBM-executor launch template of one bucket.  Operands: the
+// primary first (streamed), small ones folded into shared-memory lookup
+// tables, the rest gathered from global memory.
+static int build_bucket_args(const std::vector<std::vector<int32_t>>& opvars,
+                             const std::vector<uint8_t>& opc64, int32_t primary, int32_t v,
+                             const std::vector<int32_t>& out_vars, bool out_c64,
+                             bool primary_aligned, BucketArgs& a,
+                             std::vector<int32_t>& g_ops, std::vector<int32_t>& t_ops) {
+  std::memset(&a, 0, sizeof(a));
+  const int R = (int)out_vars.size();
+  a.R = (uint32_t)R;
+  a.n_out = 1ull << R;
+  a.out_c64 = out_c64;
+  a.primary = primary_aligned ? 1u : 0u;
+  g_ops.clear();
+  t_ops.clear();
+  std::vector<std::pair<int, int>> sd;
+  int vshift;
+  std::vector<uint32_t> lo, hi;
+  auto add_g = [&](int i) -> bool {
+    if ((int)a.ng >= kMaxG) return false;
+    operand_map(opvars[i], out_vars, v, sd, vshift);
+    split_runs(sd, kTileBits, lo, hi);
+    if ((int)lo.size() > kMaxRuns || (int)hi.size() > kMaxRuns) return false;
+    GOpArg& g = a.g[a.ng++];
+    g.vshift = (uint32_t)vshift;
+    g.c64 = opc64[i];
+    g.n_lo = (uint32_t)lo.size();
+    g.n_hi = (uint32_t)hi.size();
+    std::copy(lo.begin(), lo.end(), g.lo);
+    std::copy(hi.begin(), hi.end(), g.hi);
+    g_ops.push_back(i);
+    return true;
+  };
+  if (primary_aligned) {
+    add_g(primary);
+    // v's bit inside the primary operand
+    const auto& pv = opvars[primary];
+    a.p_k = (uint32_t)(pv.size() - 1 - (std::find(pv.begin(), pv.end(), v) - pv.begin()));
+  }
+  // candidates for tables: non-primary operands with <= kTBits non-v bits
+  std::vector<int> cand, rest;
+  for (int i = 0; i < (int)opvars.size(); ++i) {
+    if (primary_aligned && i == primary) continue;
+    if ((int)opvars[i].size() - 1 <= kTBits) cand.push_back(i);
+    else rest.push_back(i);
+  }
+  std::stable_sort(cand.begin(), cand.end(),
+                   [&](int x, int y) { return opvars[x].size() > opvars[y].size(); });
+  // bits of o per candidate
+  auto obits = [&](int i) {
+    std::vector<int> b;
+    for (int32_t u : opvars[i]) {
+      if (u == v) continue;
+      int idx = (int)(std::find(out_vars.begin(), out_vars.end(), u) - out_vars.begin());
+      b.push_back(R - 1 - idx);
+    }
+    return b;
+  };
+  std::vector<std::vector<int>> tbits;       // o bits per table
+  std::vector<std::vector<int>> tmembers;    // operand indices per table
+  for (int i : cand) {
+    auto b = obits(i);
+    int best = -1, best_overlap = -1;
+    for (int t = 0; t < (int)tbits.size(); ++t) {
+      std::vector<int> u = tbits[t];
+      int overlap = 0;
+      for (int x : b) {
+        if (std::find(u.begin(), u.end(), x) == u.end()) u.push_back(x);
+        else ++overlap;
+      }
+      if ((int)u.size() <= kTBits && overlap > best_overlap) {
+        best = t;
+        best_overlap = overlap;
+      }
+    }
+    int total_members = 0;
+    for (auto& m : tmembers) total_members += (int)m.size();
+    if (total_members >= kMaxTOps) {
+      rest.push_back(i);
+      continue;
+    }
+    if (best < 0) {
+      if ((int)tbits.size() >= kMaxT) {
+        rest.push_back(i);
+        continue;
+      }
+      tbits.push_back({});
+      tmembers.push_back({});
+      best = (int)tbits.size() - 1;
+    }
+    for (int x : b)
+      if (std::find(tbits[best].begin(), tbits[best].end(), x) == tbits[best].end())
+        tbits[best].push_back(x);
+    tmembers[best].push_back(i);
+  }
+  uint32_t smem_off = 0;
+  for (int t = 0; t < (int)tbits.size(); ++t) {
+    auto& bits = tbits[t];
+    std::sort(bits.begin(), bits.end());
+    TableArg& ta = a.t[a.nt++];
+    ta.nbits = (uint32_t)bits.size();
+    std::vector<std::pair<int, int>> osd;
+    for (int b = 0; b < (int)bits.size(); ++b) osd.push_back({bits[b], b});
+    split_runs(osd, kTileBits, lo, hi);
+    ta.n_lo = (uint32_t)lo.size();
+    ta.n_hi = (uint32_t)hi.size();
+    std::copy(lo.begin(), lo.end(), ta.lo);
+    std::copy(hi.begin(), hi.end(), ta.hi);
+    ta.first_op = a.ntop;
+    ta.n_ops = (uint32_t)tmembers[t].size();
+    ta.smem_off = smem_off;
+    smem_off += 2u << bits.size();
+    for (int i : tmembers[t]) {
+      TOpArg& to = a.top[a.ntop++];
+      to.c64 = opc64[i];
+      std::vector<std::pair<int, int>> tsd;
+      int vs = -1;
+      const auto& vars = opvars[i];
+      const int r = (int)vars.size();
+      for (int k = 0; k < r; ++k) {
+        int dst = r - 1 - k;
+        if (vars[k] == v) {
+          vs = dst;
+          continue;
+        }
+        int idx = (int)(std::find(out_vars.begin(), out_vars.end(), vars[k]) - out_vars.begin());
+        int ob = R - 1 - idx;
+        int tb = (int)(std::find(bits.begin(), bits.end(), ob) - bits.begin());
+        tsd.push_back({tb, dst});
+      }
+      std::vector<uint32_t> runs;
+      make_runs(tsd, runs);
+      to.vshift = (uint32_t)vs;
+      to.n_runs = (uint32_t)runs.size();
+      std::copy(runs.begin(), runs.end(), to.runs);
+      t_ops.push_back(i);
+    }
+  }
+  a.table_entries = smem_off;
+  for (int i : rest)
+    if (!add_g(i)) {
+      set_error("bucket has too many wide operands for one fused pass");
+      return QTN_EINVAL;
+    }
+  return QTN_OK;
+}
+
+}  // namespace qtn
+
+using namespace qtn;
+
+extern "C" const char* qtn_last_error(void) { return g_last_error.c_str(); }
+extern "C" int qtn_version(void) { return 1; }
+
+extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order,
+                               int32_t n_order, int32_t rank_cap, int32_t dtype,
+                               int32_t mixed_rank, int64_t smem_budget, qtn_plan** out_plan,
+                               int32_t* out_bad_rank) {
+  if (!net || !out_plan || n_order < 0 || (n_order > 0 && !order) || net->n_tensors < 0 ||
+      net->n_vars < 0) {
+    set_error("qtn_plan_create: bad arguments");
+    return QTN_EINVAL;
+  }
+  if (dtype != QTN_DTYPE_C128 && dtype != QTN_DTYPE_C64) {
+    set_error("unknown dtype");
+    return QTN_EINVAL;
+  }
+  *out_plan = nullptr;
+  const int nvar = net->n_vars;
+  // ---- validate: order is a permutation of the unfixed variables (60-62)
+  std::vector<int32_t> unfixed;
+  for (int v = 0; v < nvar; ++v)
+    if (!net->is_fixed[v]) unfixed.push_back(v);
+  {
+    std::vector<int32_t> s(order, order + n_order);
+    std::sort(s.begin(), s.end());
+    if (s != unfixed) {
+      set_error("order is not a permutation of the network's unfixed variables");
+      return QTN_EINVAL;
+    }
+  }
+  qtn_plan* P = new (std::nothrow) qtn_plan();
+  if (!P) {
+    set_error("out of host memory");
+    return QTN_ENOMEM;
+  }
+  // ---- inputs (sliced tensors, network order)
+  std::vector<std::vector<int32_t>> by_var(nvar);
+  int64_t in_off = 0;
+  for (int k = 0; k < net->n_tensors; ++k) {
+    TensorRec t;
+    t.input = true;
+    const int r = net->ranks[k];
+    if (r < 0 || r > 40) {
+      delete P;
+      set_error("tensor rank out of range");
+      return QTN_EINVAL;
+    }
+    for (int j = 0; j < r; ++j) {
+      int32_t u = net->vars[net->var_offsets[k] + j];
+      if (u < 0 || u >= nvar || net->is_fixed[u]) {
+        delete P;
+        set_error("tensor references a fixed or out-of-range variable");
+        return QTN_EINVAL;
+      }
+      if (std::find(t.vars.begin(), t.vars.end(), u) != t.vars.end()) {
+        delete P;
+        set_error("repeated variable in tensor");
+        return QTN_EINVAL;
+      }
+      t.vars.push_back(u);
+      by_var[u].push_back(k);
+    }
+    t.in_off = in_off;
+    in_off += 1ll << r;
+    P->tensors.push_back(std::move(t));
+  }
+  P->n_inputs = net->n_tensors;
+  P->input_elems = in_off;
+  // ---- symbolic elimination (75-106)
+  std::vector<char> alive(P->tensors.size(), 1);
+  for (int idx = 0; idx < n_order; ++idx) {
+    const int32_t v = order[idx];
+    std::vector<int32_t> ids = by_var[v];
+    by_var[v].clear();
+    std::sort(ids.begin(), ids.end());
+    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    if (ids.empty()) {
+      P->n_empty++;
+      P->step_ranks.push_back(0);
+      continue;
+    }
+    std::vector<std::vector<int32_t>> opvars;
+    std::vector<int32_t> uni;
+    for (int32_t id : ids) {
+      opvars.push_back(P->tensors[id].vars);
+      for (int32_t u : P->tensors[id].vars)
+        if (std::find(uni.begin(), uni.end(), u) == uni.end()) uni.push_back(u);
+    }
+    const int rank = (int)uni.size() - 1;
+    if (rank > rank_cap) {
+      if (out_bad_rank) *out_bad_rank = rank;
+      delete P;
+      set_error("intermediate of rank " + std::to_string(rank) + " exceeds rank cap " +
+                std::to_string(rank_cap));
+      return QTN_ERANKCAP;
+    }
+    P->step_ranks.push_back(rank);
+    P->width = std::max(P->width, rank);
+    BucketRec b;
+    b.v = v;
+    b.ops = ids;
+    b.rank = rank;
+    std::vector<int32_t> out_vars;
+    choose_layout(opvars, v, b.primary, out_vars);
+    const int32_t bi = (int32_t)P->buckets.size();
+    for (int32_t id : ids) {
+      alive[id] = 0;
+      P->tensors[id].last_use = bi;
+      for (int32_t u : P->tensors[id].vars) {
+        if (u == v) continue;
+        auto& lst = by_var[u];
+        lst.erase(std::remove(lst.begin(), lst.end(), id), lst.end());
+      }
+    }
+    TensorRec res;
+    res.vars = out_vars;
+    res.born = bi;
+    b.out = (int32_t)P->tensors.size();
+    for (int32_t u : out_vars) by_var[u].push_back(b.out);
+    P->tensors.push_back(std::move(res));
+    alive.push_back(1);
+    P->buckets.push_back(std::move(b));
+  }
+  const int32_t nb = (int32_t)P->buckets.size();
+  for (size_t id = 0; id < P->tensors.size(); ++id) {
+    if (!alive[id]) continue;
+    if (P->tensors[id].rank() != 0) {  // cannot happen after a full permutation
+      delete P;
+      set_error("non-scalar tensor survived a full elimination");
+      return QTN_EINVAL;
+    }
+    P->scalars.push_back((int32_t)id);
+    P->tensors[id].last_use = nb;
+  }
+  // ---- storage types and cost figures
+  for (auto& t : P->tensors)
+    if (!t.input) t.c64 = (dtype == QTN_DTYPE_C64) && t.rank() >= mixed_rank;
+  for (auto& b : P->buckets) P->flops_sum += std::ldexp(1.0, b.rank + 1);
+  P->flops_sum += 2.0 * P->n_empty;
+
+  // ---- SMEM executor feasibility: everything complex128 in shared memory
+  bool smem_ok = smem_budget > 0 && nb < 65535;
+  int64_t data_elems = 0;
+  std::vector<Block> sblocks;
+  if (smem_ok) {
+    for (int k = 0; k < P->n_inputs; ++k) {
+      auto& t = P->tensors[k];
+      sblocks.push_back({t.in_off, 1ll << t.rank(), -1, t.last_use});
+      t.sm_off = t.in_off;
+    }
+    data_elems = P->input_elems;
+    for (size_t id = P->n_inputs; id < P->tensors.size(); ++id) {
+      auto& t = P->tensors[id];
+      t.sm_off = place(sblocks, 1ll << t.rank(), t.born, t.last_use, 1);
+      data_elems = std::max<int64_t>(data_elems, t.sm_off + ((int64_t)1 << t.rank()));
+    }
+    size_t n_ops = 0;
+    for (auto& b : P->buckets) n_ops += b.ops.size();
+    int64_t prog = sizeof(SmemHeader) + sizeof(SmemBucket) * nb + sizeof(SmemOp) * n_ops +
+                   2 * (int64_t)P->scalars.size();
+    prog = (prog + 15) / 16 * 16;
+    const int64_t smem = prog + 16 * data_elems;
+    if (data_elems > 65535 || n_ops > 65535 || smem > smem_budget) smem_ok = false;
+    // every operand must fit the packed run encoding
+    std::vector<std::pair<int, int>> sd;
+    std::vector<uint32_t> runs;
+    std::vector<uint8_t> blob;
+    if (smem_ok) {
+      blob.assign(prog, 0);
+      SmemHeader* h = reinterpret_cast<SmemHeader*>(blob.data());
+      h->n_buckets = nb;
+      h->n_ops = (uint32_t)n_ops;
+      h->n_scalars = (uint32_t)P->scalars.size();
+      h->pow2 = (uint32_t)P->n_empty;
+      h->in_elems = (uint32_t)P->input_elems;
+      h->data_elems = (uint32_t)data_elems;
+      h->prog_bytes = (uint32_t)prog;
+      SmemBucket* sb = reinterpret_cast<SmemBucket*>(blob.data() + sizeof(SmemHeader));
+      SmemOp* so = reinterpret_cast<SmemOp*>(blob.data() + sizeof(SmemHeader) +
+                                            sizeof(SmemBucket) * nb);
+      uint32_t op_i = 0;
+      for (int bi = 0; bi < nb && smem_ok; ++bi) {
+        const auto& b = P->buckets[bi];
+        const auto& out = P->tensors[b.out];
+        sb[bi].out_off = (uint16_t)out.sm_off;
+        sb[bi].R = (uint8_t)b.rank;
+        sb[bi].n_ops = (uint8_t)b.ops.size();
+        sb[bi].first_op = (uint16_t)op_i;
+        // primary first: its product seeds the accumulator
+        std::vector<int32_t> ord = b.ops;
+        std::swap(ord[0], ord[b.primary]);
+        for (int32_t id : ord) {
+          int vs;
+          operand_map(P->tensors[id].vars, out.vars, b.v, sd, vs);
+          make_runs(sd, runs);
+          if ((int)runs.size() > kSmemOpRuns || b.rank > 31) {
+            smem_ok = false;
+            break;
+          }
+          SmemOp& o = so[op_i++];
+          o.off = (uint16_t)P->tensors[id].sm_off;
+          o.vshift = (uint8_t)vs;
+          o.n_runs = (uint8_t)runs.size();
+          for (size_t r = 0; r < runs.size(); ++r) {
+            uint32_t s = runs[r] & 0xff, d = (runs[r] >> 8) & 0xff, l = (runs[r] >> 16) & 0xff;
+            o.runs[r] = (uint16_t)(s | (d << 5) | (l << 10));
+          }
+        }
+      }
+      uint16_t* sc = reinterpret_cast<uint16_t*>(blob.data() + sizeof(SmemHeader) +
+                                                 sizeof(SmemBucket) * nb +
+                                                 sizeof(SmemOp) * n_ops);
+      for (size_t i = 0; i < P->scalars.size(); ++i)
+        sc[i] = (uint16_t)P->tensors[P->scalars[i]].sm_off;
+      if (smem_ok) {
+        P->program = std::move(blob);
+        P->smem_bytes = smem;
+      }
+    }
+  }
+  if (smem_ok) {
+    P->executor = QTN_EXEC_SMEM;
+    for (auto& t : P->tensors) t.c64 = false;
+  } else {
+    P->executor = QTN_EXEC_HBM;
+    // device arena for intermediates
+    std::vector<Block> hblocks;
+    int64_t ws = 0;
+    for (size_t id = P->n_inputs; id < P->tensors.size(); ++id) {
+      auto& t = P->tensors[id];
+      int64_t bytes = elem_bytes(t.c64) << t.rank();
+      bytes = std::max<int64_t>(bytes, 256);
+      t.ws_off = place(hblocks, bytes, t.born, t.last_use, 256);
+      ws = std::max(ws, t.ws_off + bytes);
+    }
+    P->workspace_bytes = ws;
+    // launch templates
+    for (int bi = 0; bi < nb; ++bi) {
+      const auto& b = P->buckets[bi];
+      std::vector<std::vector<int32_t>> opvars;
+      std::vector<uint8_t> opc64;
+      for (int32_t id : b.ops) {
+        opvars.push_back(P->tensors[id].vars);
+        opc64.push_back(P->tensors[id].c64 ? 1 : 0);
+      }
+      BucketArgs a;
+      std::vector<int32_t> g_ops, t_ops;
+      int rc = build_bucket_args(opvars, opc64, b.primary, b.v, P->tensors[b.out].vars,
+                                 P->tensors[b.out].c64, true, a, g_ops, t_ops);
+      if (rc) {
+        delete P;
+        return rc;
+      }
+      // remember which tensor each pointer slot refers to (patched at execute)
+      for (int i = 0; i < (int)a.ng; ++i)
+        a.g[i].ptr = reinterpret_cast<const void*>((uintptr_t)b.ops[g_ops[i]]);
+      for (int i = 0; i < (int)a.ntop; ++i)
+        a.top[i].ptr = reinterpret_cast<const void*>((uintptr_t)b.ops[t_ops[i]]);
+      a.out = reinterpret_cast<void*>((uintptr_t)b.out);
+      P->hbm_args.push_back(a);
+    }
+  }
+  // algorithmic bytes: e * (operand entries + output entries) per bucket
+  for (auto& b : P->buckets) {
+    double bytes = 0.0;
+    for (int32_t id : b.ops) {
+      const auto& t = P->tensors[id];
+      bytes += std::ldexp((double)elem_bytes(t.c64), t.rank());
+    }
+    const auto& o = P->tensors[b.out];
+    bytes += std::ldexp((double)elem_bytes(o.c64), o.rank());
+    P->alg_bytes += bytes;
+  }
+  *out_plan = P;
+  return QTN_OK;
+}
+
+extern "C" int qtn_plan_info(const qtn_plan* P, qtn_plan_info_t* info) {
+  if (!P || !info) {
+    set_error("null argument");
+    return QTN_EINVAL;
+  }
+  info->executor = P->executor;
+  info->n_buckets = (int32_t)P->buckets.size();
+  info->n_empty_buckets = P->n_empty;
+  info->width = P->width;
+  info->input_elems = P->input_elems;
+  info->workspace_bytes = P->workspace_bytes;
+  info->smem_bytes = P->smem_bytes;
+  info->program_bytes = (int64_t)P->program.size();
+  info->alg_bytes = P->alg_bytes;
+  info->flops_sum = P->flops_sum;
+  return QTN_OK;
+}
+
+extern "C" int qtn_plan_step_ranks(const qtn_plan* P, int32_t* out) {
+  if (!P || !out) {
+    set_error("null argument");
+    return QTN_EINVAL;
+  }
+  std::copy(P->step_ranks.begin(), P->step_ranks.end(), out);
+  return QTN_OK;
+}
+
+extern "C" int qtn_plan_input_offsets(const qtn_plan* P, int64_t* out) {
+  if (!P || !out) {
+    set_error("null argument");
+    return QTN_EINVAL;
+  }
+  for (int k = 0; k < P->n_inputs; ++k) out[k] = P->tensors[k].in_off;
+  return QTN_OK;
+}
+
+qtn_plan::~qtn_plan() {
+  if (self_batch) qtn_batch_destroy(self_batch);
+}
+
+extern "C" int qtn_plan_destroy(qtn_plan* P) {
+  delete P;
+  return QTN_OK;
+}
+
+extern "C" int qtn_bucket_layout(int32_t n_ops, const int32_t* ranks, const int32_t* var_offsets,
+                                 const int32_t* vars, int32_t elim_var, int32_t* out_rank,
+                                 int32_t* out_vars) {
+  if (n_ops < 1) {
+    set_error("bucket needs at least one operand");
+    return QTN_EINVAL;
+  }
+  std::vector<std::vector<int32_t>> opvars(n_ops);
+  for (int i = 0; i < n_ops; ++i) opvars[i].assign(vars + var_offsets[i], vars + var_offsets[i] + ranks[i]);
+  int32_t primary;
+  std::vector<int32_t> ov;
+  choose_layout(opvars, elim_var, primary, ov);
+  *out_rank = (int32_t)ov.size();
+  std::copy(ov.begin(), ov.end(), out_vars);
+  return QTN_OK;
+}
+
+extern "C" int qtn_bucket_contract(int32_t n_ops, const int32_t* ranks, const int32_t* var_offsets,
+                                   const int32_t* vars, const void* const* ptrs,
+                                   const uint8_t* c64, int32_t elim_var, int32_t out_rank,
+                                   const int32_t* out_vars, int32_t out_c64, void* out,
+                                   void* stream) {
+  if (n_ops < 1 || out_rank < 0 || out_rank > 34) {
+    set_error("qtn_bucket_contract: bad arguments");
+    return QTN_EINVAL;
+  }
+  std::vector<std::vector<int32_t>> opvars(n_ops);
+  std::vector<uint8_t> opc64(n_ops);
+  std::vector<int32_t> uni;
+  for (int i = 0; i < n_ops; ++i) {
+    opvars[i].assign(vars + var_offsets[i], vars + var_offsets[i] + ranks[i]);
+    opc64[i] = c64[i] ? 1 : 0;
+    if (std::find(opvars[i].begin(), opvars[i].end(), elim_var) == opvars[i].end()) {
+      set_error("every bucket operand must contain the eliminated variable");
+      return QTN_EINVAL;
+    }
+    for (int32_t u : opvars[i])
+      if (std::find(uni.begin(), uni.end(), u) == uni.end()) uni.push_back(u);
+  }
+  std::vector<int32_t> ov(out_vars, out_vars + out_rank);
+  {
+    std::vector<int32_t> a = ov, b;
+    for (int32_t u : uni)
+      if (u != elim_var) b.push_back(u);
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    if (a != b) {
+      set_error("out_vars must be the union of operand variables minus elim_var");
+      return QTN_EINVAL;
+    }
+  }
+  // the primary streams aligned only if the requested layout matches the rule
+  int32_t primary;
+  std::vector<int32_t> pref;
+  choose_layout(opvars, elim_var, primary, pref);
+  bool aligned = true;
+  {
+    const auto& pv = opvars[primary];
+    std::vector<int32_t> low;
+    for (int32_t u : pv)
+      if (u != elim_var) low.push_back(u);
+    aligned = ov.size() >= low.size() &&
+              std::equal(low.begin(), low.end(), ov.end() - low.size());
+  }
+  BucketArgs a;
+  std::vector<int32_t> g_ops, t_ops;
+  int rc = build_bucket_args(opvars, opc64, primary, elim_var, ov, out_c64 != 0, aligned, a,
+                             g_ops, t_ops);
+  if (rc) return rc;
+  for (int i = 0; i < (int)a.ng; ++i) a.g[i].ptr = ptrs[g_ops[i]];
+  for (int i = 0; i < (int)a.ntop; ++i) a.top[i].ptr = ptrs[t_ops[i]];
+  a.out = out;
+  return launch_bucket(a, stream);
+}
+
+// ------------------------------------------------------------- execution
+
+extern "C" int qtn_plan_execute(qtn_plan* P, const void* inputs, void* workspace, void* result,
+                                void* stream) {
+  if (!P || !result || (P->input_elems > 0 && !inputs)) {
+    set_error("qtn_plan_execute: null argument");
+    return QTN_EINVAL;
+  }
+  int rc = device_check();
+  if (rc) return rc;
+  if (P->executor == QTN_EXEC_SMEM) {
+    if (!P->self_batch) {
+      qtn_plan* one[1] = {P};
+      rc = qtn_batch_create(one, 1, &P->self_batch);
+      if (rc) return rc;
+    }
+    return qtn_batch_execute(P->self_batch, inputs, 0, 1, result, stream);
+  }
+  if (P->workspace_bytes > 0 && !workspace) {
+    set_error("HBM executor needs a workspace of workspace_bytes");
+    return QTN_EINVAL;
+  }
+  auto addr = [&](int32_t id) -> char* {
+    const auto& t = P->tensors[id];
+    if (t.input) return (char*)inputs + 16 * t.in_off;
+    return (char*)workspace + t.ws_off;
+  };
+  for (size_t bi = 0; bi < P->buckets.size(); ++bi) {
+    BucketArgs a = P->hbm_args[bi];
+    for (uint32_t i = 0; i < a.ng; ++i) a.g[i].ptr = addr((int32_t)(uintptr_t)a.g[i].ptr);
+    for (uint32_t i = 0; i < a.ntop; ++i) a.top[i].ptr = addr((int32_t)(uintptr_t)a.top[i].ptr);
+    a.out = addr((int32_t)(uintptr_t)a.out);
+    rc = launch_bucket(a, stream);
+    if (rc) return rc;
+  }
+  // scalar fold: 2^n_empty * prod(rank-0 tensors)  (contraction.py:77-81, 108-110)
+  std::vector<const void*> ptrs;
+  std::vector<uint8_t> c64;
+  for (int32_t id : P->scalars) {
+    ptrs.push_back(addr(id));
+    c64.push_back(P->tensors[id].c64 ? 1 : 0);
+  }
+  return launch_fold(ptrs.data(), c64.data(), (int)ptrs.size(), P->n_empty, result, false,
+                     stream);
+}

@@ -1,0 +1,185 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle and
+the golden vectors produced by the real reference (tests/golden)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2106_15740_b200 as Q
+import qtn_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _net_from_oracle(tensors, nv, fixed):
+    ts = [Q.Tensor(k, vs, d) for k, (vs, d) in enumerate(tensors)]
+    return Q.TensorNetwork(tuple(ts), nv, fixed)
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+@pytest.mark.parametrize("mode", list(Q.MODE_ORDER))
+def test_config1_contract_all_modes_c128(golden, mode):
+    G = golden("config1.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    nets, orders, want = [], [], []
+    for r in G["modes"][mode]:
+        net = Q.build_energy_network(graph, graph.edges[r["edge_index"]], params, mode)
+        order = Q.ContractionOrder(r["order"])
+        nets.append(net)
+        orders.append(order)
+        want.append(complex(*r["value"]))
+    got = Q.contract_many(nets, orders, dtype="complex128")
+    for g, w in zip(got, want):
+        assert abs(g - w) < 1e-12
+    # and single-network entry point, with step ranks
+    v, ranks = Q.contraction._contract_with_ranks(nets[0], orders[0], 30)
+    assert abs(v - want[0]) < 1e-12
+    assert max(ranks) == G["modes"][mode][0]["width"]
+
+
+def test_config1_energy_matches_statevector(golden):
+    G = golden("config1.json")
+    kat = golden("kat.json")
+    graph = Q.random_regular_graph(20, 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    want = sum((1 - z) / 2 for z in kat["config1_statevector_zz"])
+    for mode in Q.MODE_ORDER:
+        e = Q.energy_expectation(graph, params, mode=mode, dtype="complex128")
+        assert abs(e - want) < 1e-10, (mode, e, want)
+
+
+def test_config2_energy_and_edges(golden):
+    G = golden("config2.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    plan = Q.EnergyPlan(graph, G["p"], "zz+diagonal", dtype="complex64")
+    zz = plan.zz_values(params)
+    recs = G["modes"]["zz+diagonal"]
+    for r in recs:
+        w = complex(*r["value"])
+        assert abs(zz[r["edge_index"]] - w) < 1e-10
+    want = sum((1 - r["value"][0]) / 2 for r in recs)
+    e = plan.energies(params)[0]
+    assert abs(e - want) / abs(want) < 1e-12
+
+
+def test_config2_angle_batch_vs_oracle(golden):
+    """Several angle sets in one launch, each against the oracle at its angles."""
+    G = golden("config2.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    edges = [tuple(e) for e in G["edges"]]
+    plan = Q.EnergyPlan(graph, 2, "zz+diagonal", edge_ids=list(range(0, 150, 15)))
+    rng = np.random.default_rng(7)
+    sets = rng.uniform(0, math.pi, (5, 4))
+    got = plan.energies(sets)
+    for s in range(5):
+        g, b = list(sets[s, :2]), list(sets[s, 2:])
+        zz = [O.edge_zz(100, edges, edges[e], g, b, "zz+diagonal") for e in plan.edge_ids]
+        assert abs(got[s] - O.energy_from_zz(zz)) < 1e-10
+
+
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-11), ("complex64", 1e-5)])
+def test_config3_default_hbm_path(golden, dtype, tol):
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    recs = G["modes"]["default"][:6]
+    plan = Q.EnergyPlan(graph, G["p"], "default", dtype=dtype,
+                        edge_ids=[r["edge_index"] for r in recs])
+    assert plan.hbm_jobs, "config 3 default networks must take the HBM executor"
+    zz = plan.zz_values(params)
+    for r in recs:
+        w = complex(*r["value"])
+        assert abs(zz[r["edge_index"]] - w) <= tol * abs(w) + 1e-12
+
+
+def test_config3_zzdiag_energy(golden):
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    recs = G["modes"]["zz+diagonal"]
+    plan = Q.EnergyPlan(graph, G["p"], "zz+diagonal", dtype="complex64")
+    want = sum((1 - r["value"][0]) / 2 for r in recs)
+    e = plan.energies(params)[0]
+    assert abs(e - want) / abs(want) < 1e-10
+
+
+@pytest.mark.parametrize("edge_index,tol", [(16, 1e-5), (1058, 1e-5)])
+def test_config4_single_edge_c64(golden, edge_index, tol):
+    G = golden("config4.json")
+    rec = [r for r in G["modes"]["zz+diagonal"] if r["edge_index"] == edge_index][0]
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    plan = Q.EnergyPlan(graph, G["p"], "zz+diagonal", dtype="complex64", edge_ids=[edge_index])
+    zz = plan.zz_values(params)[edge_index]
+    w = complex(*rec["value"])
+    assert abs(zz - w) / abs(w) < tol
+
+
+def test_config4_edge16_c128(golden):
+    G = golden("config4.json")
+    rec = [r for r in G["modes"]["zz+diagonal"] if r["edge_index"] == 16][0]
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    plan = Q.EnergyPlan(graph, G["p"], "zz+diagonal", dtype="complex128", edge_ids=[16])
+    zz = plan.zz_values(params)[16]
+    w = complex(*rec["value"])
+    assert abs(zz - w) / abs(w) < 1e-11
+
+
+def test_synthetic_buckets_c_abi(golden):
+    """qtn_bucket_contract on config-5-shaped buckets vs the reference bucket ops."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2106_15740_b200 import _native as N
+
+    for case in golden("synthetic_buckets.json"):
+        ops = case["operands"]
+        datas = [np.asarray(o["re"]) + 1j * np.asarray(o["im"]) for o in ops]
+        for c64 in (False, True):
+            dt = torch.complex64 if c64 else torch.complex128
+            dev = [torch.from_numpy(d).to(dt).cuda() for d in datas]
+            ranks = np.asarray([len(o["vars"]) for o in ops], dtype=np.int32)
+            offs = np.zeros(len(ops) + 1, dtype=np.int32)
+            offs[1:] = np.cumsum(ranks)
+            flat = np.asarray([v for o in ops for v in o["vars"]], dtype=np.int32)
+            ptrs = (C.c_void_p * len(ops))(*[d.data_ptr() for d in dev])
+            flags = np.full(len(ops), 1 if c64 else 0, dtype=np.uint8)
+            ov = np.asarray(case["out_vars"], dtype=np.int32)
+            out = torch.empty(1 << len(ov), dtype=dt, device="cuda")
+            N.check(N.lib.qtn_bucket_contract(len(ops), N.i32(ranks), N.i32(offs), N.i32(flat),
+                                              ptrs, N.u8(flags), 0, len(ov), N.i32(ov),
+                                              1 if c64 else 0, out.data_ptr(),
+                                              torch.cuda.current_stream().cuda_stream))
+            got = out.cpu().numpy().astype(np.complex128)
+            want = np.asarray(case["out_re"]) + 1j * np.asarray(case["out_im"])
+            if c64:
+                # operands rounded to complex64 first: compare against that
+                ref_ops = [(tuple(o["vars"]), d.astype(np.complex64).astype(np.complex128))
+                           for o, d in zip(ops, datas)]
+                vs, ref = O.bucket_eliminate(
+                    [(v, d.reshape((2,) * len(v))) for v, d in ref_ops], 0)
+                assert list(vs) == case["out_vars"]
+                want = ref.reshape(-1)
+                tol = 1e-5
+            else:
+                tol = 1e-12
+            err = np.abs(got - want).max() / np.abs(want).max()
+            assert err < tol, (case["w"], case["m"], c64, err)
+
+
+def test_rank_cap_raised_before_execution():
+    graph = Q.random_regular_graph(100, 3, 0)
+    tpl = Q.energy_template(graph, graph.edges[0], 2, "default")
+    order, rep = Q.rgreedy_order(tpl.line_graph())
+    with pytest.raises(Q.RankCapExceeded) as ei:
+        Q.ContractionPlan(tpl.structure, tpl.variable_count, tpl.fixed, order.sequence,
+                          rank_cap=rep.width - 1)
+    assert ei.value.cap == rep.width - 1
