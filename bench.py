@@ -1,0 +1,549 @@
+#!/usr/bin/env python
+"""Benchmark: QAOA edge-energy contractions/sec and bucket-kernel HBM GB/s.
+
+Default workload (BASELINE.json configs[1], "config 2"): QAOA p=2 MaxCut
+energy on the seeded random 3-regular graph N=100 (graph seed 0), all 150
+per-edge light-cone networks in zz+diagonal mode, orders from the reference
+rgreedy(10, 0.02, seed 0), plans cached.  One step evaluates the energy for
+a batch of A angle sets (set 0 is the config's seeded angles, the rest are
+seeded U[0, pi) draws — the parameter batch a QAOA optimiser evaluates),
+i.e. 150*A edge contractions: on-device tensor generation, the batched
+shared-memory executor, and the energy reduction.  With --gpus N the edges
+are LPT-sharded over N ranks (strong scaling) and the per-set partial
+energies are all-reduced over NCCL once per step.
+
+Other workloads for development (`--workload`): config3 / config3-default
+(N=244, p=3), config4 (N=1000, p=5, edge #1058), config5 (synthetic bucket
+sweep).  `--impl reference` times the CPU oracle (the restated reference
+bucket elimination, oracle/qtn_oracle.py) on all host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:  # first sample before timing
+                time.sleep(0.05)
+            self.rows.clear()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# -------------------------------------------------------------- distributed
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def angle_sets(p, n_sets, seed=0):
+    from paper_2106_15740_b200 import seeded_angles
+
+    a = np.empty((n_sets, 2 * p), dtype=np.float64)
+    a[0] = seeded_angles(p, seed).as_vector()
+    if n_sets > 1:
+        rng = np.random.default_rng(1000 + seed)
+        a[1:] = rng.uniform(0.0, math.pi, (n_sets - 1, 2 * p))
+    return a
+
+
+WORKLOADS = {
+    "config2": dict(n=100, p=2, mode="zz+diagonal", edges=None, dtype="complex64"),
+    "config3": dict(n=244, p=3, mode="zz+diagonal", edges=None, dtype="complex64"),
+    "config3-default": dict(n=244, p=3, mode="default", edges=None, dtype="complex64"),
+    "config4": dict(n=1000, p=5, mode="zz+diagonal", edges=[1058], dtype="complex64"),
+}
+
+
+def profile_traffic(kernel_key):
+    """dram bytes per launch of the dominant kernel from a committed
+    `ncu --set full` summary (profiles/ncu_full_*.json), or None."""
+    prof = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(prof):
+        return None
+    for name in sorted(os.listdir(prof), reverse=True):
+        if name.startswith("ncu_full") and name.endswith(".json"):
+            try:
+                with open(os.path.join(prof, name)) as f:
+                    d = json.load(f)
+                k = d.get("kernels", {}).get(kernel_key)
+                if k and k.get("dram_bytes_per_launch"):
+                    return float(k["dram_bytes_per_launch"])
+            except Exception:
+                pass
+    return None
+
+
+# ------------------------------------------------------------ CPU baseline
+def _cpu_worker_init(n, edges, p, mode, orders):
+    global _W
+    _W = (n, edges, p, mode, orders)
+
+
+def _cpu_worker(job):
+    import qtn_oracle as O
+
+    n, edges, p, mode, orders = _W
+    e_idx, angles = job
+    g, b = list(angles[:p]), list(angles[p:])
+    tens, nv, fixed = O.edge_network(n, edges, edges[e_idx], g, b, mode)
+    val, _ = O.contract(tens, nv, fixed, orders[e_idx])
+    return e_idx, val.real
+
+
+def cpu_orders(graph, p, mode, edge_ids):
+    """Reference rgreedy orders (identical to the oracle's; computed once)."""
+    from paper_2106_15740_b200 import plan_edges
+
+    jobs = plan_edges(graph, p, mode, edge_ids, compile_plans=False)
+    return {j.index: list(j.order.sequence) for j in jobs}
+
+
+def cpu_baseline(wl, graph, sets, seconds=10.0, cores=1):
+    """Oracle (restated reference bucket elimination, complex128) on a
+    bounded sample: network build + contract per (edge, angle set), orders
+    cached, for ~`seconds` of wall time on `cores` processes."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import multiprocessing as mp
+
+    edge_ids = wl["edges"] if wl["edges"] is not None else list(range(graph.edge_count))
+    orders = cpu_orders(graph, wl["p"], wl["mode"], edge_ids)
+    edges = [tuple(e) for e in graph.edges]
+    def job(k):
+        return (edge_ids[k % len(edge_ids)], sets[(k // len(edge_ids)) % len(sets)])
+
+    init = (graph.node_count, edges, wl["p"], wl["mode"], orders)
+    done = 0
+    if cores <= 1:
+        _cpu_worker_init(*init)
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            _cpu_worker(job(done))
+            done += 1
+        dt = time.perf_counter() - t0
+    else:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(cores, initializer=_cpu_worker_init, initargs=init) as pool:
+            pool.map(_cpu_worker, [job(k) for k in range(cores)])  # warm
+            t0 = time.perf_counter()
+            chunk = max(cores * 4, len(edge_ids))
+            while time.perf_counter() - t0 < seconds:
+                pool.map(_cpu_worker, [job(k) for k in range(done, done + chunk)], chunksize=1)
+                done += chunk
+            dt = time.perf_counter() - t0
+    return done / dt, done, dt
+
+
+# -------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2106_15740_b200 import random_regular_graph
+
+    wl = WORKLOADS[args.workload]
+    graph = random_regular_graph(wl["n"], 3, 0)
+    sets = angle_sets(wl["p"], max(args.angle_sets, 1))
+    cores = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import multiprocessing as mp
+
+    edge_ids = wl["edges"] if wl["edges"] is not None else list(range(graph.edge_count))
+    orders = cpu_orders(graph, wl["p"], wl["mode"], edge_ids)
+    edges = [tuple(e) for e in graph.edges]
+    init = (graph.node_count, edges, wl["p"], wl["mode"], orders)
+    # one step = the energy of ONE angle set over all edges (a bounded sample
+    # of the GPU step, which evaluates A sets)
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores, initializer=_cpu_worker_init, initargs=init) as pool:
+        for it in range(args.warmup + args.steps):
+            s = sets[it % len(sets)]
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_worker, [(e, s) for e in edge_ids], chunksize=1)
+            dt = time.perf_counter() - t0
+            if it >= args.warmup:
+                times.append(dt)
+    per_step = len(edge_ids)
+    total = sum(times)
+    value = per_step * len(times) / total
+    line = {
+        "impl": "reference",
+        "metric": "QAOA edge-energy contractions/sec",
+        "value": value,
+        "unit": "contractions/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic (seeded graph and angles)",
+        "config": {"workload": args.workload, "edges_per_step": per_step, "angle_sets_per_step": 1,
+                   "mode": wl["mode"]},
+        "cpu_baseline": {"value": value, "unit": "contractions/s", "cores": cores, "kind": "port",
+                         "sample": f"1 angle set x {per_step} edge networks per step "
+                                   "(oracle network build + bucket elimination, complex128)"},
+        "e2e": {"value": value, "unit": "contractions/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def config5_roofline(torch, w=30, m=16, reps=5, seed=0):
+    """Synthetic bucket (config 5): rank-(w+1) complex64 operand + m small
+    rank-1/2 operands, output rank w, through qtn_bucket_contract."""
+    import ctypes as C
+
+    from paper_2106_15740_b200 import _native as N
+
+    rng = np.random.default_rng(seed)
+    perm = [int(x) for x in rng.permutation(w + 1)]
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    # rank w+1 complex64 operand: 2^(w+1) complex = 2^(w+2) floats
+    big = torch.randn(4 << w, dtype=torch.float32, device=dev, generator=g).view(torch.complex64)
+    ops_vars = [perm]
+    datas = [big]
+    for _ in range(m):
+        if rng.random() < 0.5:
+            ops_vars.append([0])
+        else:
+            ops_vars.append([0, int(rng.integers(1, w + 1))])
+        datas.append(torch.randn(2 << (len(ops_vars[-1])), dtype=torch.float32, device=dev,
+                                 generator=g).view(torch.complex64))
+    ranks = np.asarray([len(v) for v in ops_vars], dtype=np.int32)
+    offs = np.zeros(len(ranks) + 1, dtype=np.int32)
+    offs[1:] = np.cumsum(ranks)
+    flat = np.asarray([x for v in ops_vars for x in v], dtype=np.int32)
+    ov = np.zeros(w, dtype=np.int32)
+    r = C.c_int32()
+    N.check(N.lib.qtn_bucket_layout(len(ranks), N.i32(ranks), N.i32(offs), N.i32(flat), 0,
+                                    C.byref(r), N.i32(ov)))
+    out = torch.empty(1 << w, dtype=torch.complex64, device=dev)
+    ptrs = (C.c_void_p * len(datas))(*[d.data_ptr() for d in datas])
+    flags = np.ones(len(datas), dtype=np.uint8)
+    st = torch.cuda.current_stream()
+
+    def run():
+        N.check(N.lib.qtn_bucket_contract(len(ranks), N.i32(ranks), N.i32(offs), N.i32(flat), ptrs,
+                                          N.u8(flags), 0, w, N.i32(ov), 1, out.data_ptr(),
+                                          st.cuda_stream))
+
+    for _ in range(2):
+        run()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        run()
+        e1.record(st)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    alg = 8.0 * ((2 << w) + sum(1 << len(v) for v in ops_vars[1:]) + (1 << w))
+    t = statistics.median(ts)
+    del big, out, datas
+    torch.cuda.empty_cache()
+    return {"w": w, "m": m, "alg_bytes": alg, "seconds": t, "gbs": alg / t / 1e9}
+
+
+def run_gpu(args):
+    import torch
+
+    import paper_2106_15740_b200 as Q
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    wl = WORKLOADS[args.workload]
+    graph = Q.random_regular_graph(wl["n"], 3, 0)
+    edge_ids = wl["edges"] if wl["edges"] is not None else list(range(graph.edge_count))
+    t0 = time.perf_counter()
+    if world > 1:
+        allj = Q.plan_edges(graph, wl["p"], wl["mode"], edge_ids, compile_plans=False)
+        shard = Q.shard_edges([j.report.flops_sum for j in allj], world)[rank]
+        my_edges = [edge_ids[k] for k in shard]
+    else:
+        my_edges = edge_ids
+    plan = Q.EnergyPlan(graph, wl["p"], wl["mode"], dtype=args.dtype or wl["dtype"],
+                        edge_ids=my_edges)
+    plan_s = time.perf_counter() - t0
+    A = args.angle_sets
+    sets = angle_sets(wl["p"], A)
+    ang = torch.from_numpy(sets).to(dev)
+    st = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        b = plan.launch(ang, st)
+        if world > 1:
+            e = (b["e_smem"] if plan.smem_jobs else 0) + (b["e_hbm"] if plan.hbm_jobs else 0)
+            if not torch.is_tensor(e):
+                e = torch.zeros(A, dtype=torch.float64, device=dev)
+            dist.all_reduce(e)
+        return b
+
+    # dominant-kernel timing: the SMEM batch launch alone, events on its stream
+    def kernel_only():
+        import ctypes as C  # noqa: F401
+
+        from paper_2106_15740_b200 import _native as N
+
+        b = plan._buffers(A)
+        N.check(N.lib.qtn_batch_execute(plan._batch, b["inputs"].data_ptr(), plan.set_elems, A,
+                                        b["res_smem"].data_ptr(), st.cuda_stream))
+
+    clk = ClockSampler(local).__enter__()  # sampled through warm-up, timed and e2e loops
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    step_times = []
+    kern_times = []
+    launches = 0
+    if True:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            step()
+            e1.record(st)
+            e1.synchronize()
+            step_times.append(e0.elapsed_time(e1) / 1e3)
+            launches += plan.launches
+            if plan._batch is not None:
+                flush.zero_()
+                k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                k0.record(st)
+                kernel_only()
+                k1.record(st)
+                k1.synchronize()
+                kern_times.append(k0.elapsed_time(k1) / 1e3)
+    total = sum(step_times)
+    if dist is not None:
+        t = torch.tensor([total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    n_contr = len(edge_ids) * A * args.steps
+    value = n_contr / total
+
+    # end to end through the public API: host angles -> energies on host
+    e2e_times = []
+    for it in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t1 = time.perf_counter()
+        if world > 1:
+            en = plan.energies(sets)
+            buf = torch.from_numpy(en).to(dev)
+            dist.all_reduce(buf)
+            en = buf.cpu().numpy()
+        else:
+            en = plan.energies(sets)
+        dt = time.perf_counter() - t1
+        if it >= args.warmup:
+            e2e_times.append(dt)
+    e2e_total = sum(e2e_times)
+    if dist is not None:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = n_contr / e2e_total
+    clk.__exit__(None, None, None)
+
+    # sanity: set-0 energy is the config's energy
+    energy0 = float(en[0])
+
+    peak, peak_kind = hbm_peak()
+    if kern_times:
+        kt = sum(kern_times) / len(kern_times)
+        alg = sum(j.plan.alg_bytes for j in plan.smem_jobs) * A
+        kname = "smem_net_kernel"
+    else:
+        kt = total / args.steps
+        alg = plan.alg_bytes * A
+        kname = "bucket_kernel"
+    achieved = alg / kt / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": profile_traffic(kname), "kernel": kname,
+            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+            "alg_bytes_per_launch": alg, "avg_launch_s": kt}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            v, n, dt = cpu_baseline(wl, graph, sets[:1], seconds=args.cpu_seconds, cores=1)
+            cpu = {"value": v, "unit": "contractions/s", "cores": 1, "kind": "port",
+                   "sample": f"{n} edge networks (angle set 0) in {dt:.1f}s: oracle network build "
+                             "+ bucket elimination, complex128, orders cached"}
+        b5 = None
+        if not args.no_config5 and world == 1:
+            try:
+                b5 = config5_roofline(torch, w=args.c5_w, m=args.c5_m)
+                b5["frac"] = b5["gbs"] / peak
+            except Exception as ex:  # report, do not hide
+                b5 = {"error": repr(ex)}
+        out = {
+            "metric": "QAOA edge-energy contractions/sec",
+            "value": value,
+            "unit": "contractions/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "c128" if not plan.hbm_jobs else "c128 (c64 storage for rank>=12)",
+            "data": "synthetic (seeded random 3-regular graph, seeded angles)",
+            "config": {"workload": args.workload, "n": wl["n"], "p": wl["p"], "mode": wl["mode"],
+                       "edges": len(edge_ids), "angle_sets_per_step": A,
+                       "contractions_per_step": len(edge_ids) * A,
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"edges LPT-sharded over {world} GPU(s)",
+                       "energy_set0": energy0, "plan_seconds": plan_s},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "contractions/s",
+                    "h2d_bytes_per_step": int(sets.nbytes), "d2h_bytes_per_step": 8 * A,
+                    "api": "EnergyPlan.energies(host angle array) -> host energies"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "bucket_roofline_config5": b5,
+        }
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS) + ["config5"])
+    ap.add_argument("--angle-sets", type=int, default=1024)
+    ap.add_argument("--dtype", default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config5", action="store_true")
+    ap.add_argument("--c5-w", type=int, default=30)
+    ap.add_argument("--c5-m", type=int, default=16)
+    ap.add_argument("--c5-ws", default="20,22,24,26,28,30,31,32")
+    ap.add_argument("--c5-ms", default="4,8,16")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.workload == "config5":
+        return run_config5(args)
+    return run_gpu(args)
+
+
+def run_config5(args):
+    """Config-5 roofline sweep: one JSON line per (w, m)."""
+    import torch
+
+    peak, kind = hbm_peak()
+    for w in [int(x) for x in args.c5_ws.split(",")]:
+        for m in [int(x) for x in args.c5_ms.split(",")]:
+            r = config5_roofline(torch, w=w, m=m, reps=args.steps)
+            r.update({"workload": "config5", "frac": r["gbs"] / peak, "peak_gbs": peak,
+                      "peak_source": kind})
+            print(json.dumps(r), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -343,6 +343,7 @@ __global__ void energy_kernel(const double2* __restrict__ vals, int n, double* e
 namespace qtn {
 
 int device_check() {
+  if (g_num_sms > 0) return QTN_OK;
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess || n == 0) {

@@ -35,7 +35,8 @@ from .contraction import (DEFAULT_MIXED_RANK, DEFAULT_RANK_CAP, DEFAULT_SMEM_BUD
 from .lightcone import EnergyTemplate, energy_template
 from .ordering import ContractionOrder, CostReport, rgreedy_order
 
-__all__ = ["EdgeJob", "EnergyPlan", "plan_edges", "shard_edges", "energy_expectation"]
+__all__ = ["EdgeJob", "EnergyPlan", "plan_edges", "shard_edges", "rank_shard", "reduce_partials",
+           "energy_expectation"]
 
 
 class EdgeJob:
@@ -246,6 +247,29 @@ class EnergyPlan:
             self._batch = None
 
 
+def rank_shard(graph: ProblemGraph, p: int, mode: str, rank: int, world: int,
+               n_repeats=10, temp=0.02, seed=0):
+    """This rank's edges: LPT over the reference cost model.  Every rank
+    computes the same (deterministic) orders, so no exchange is needed."""
+    allj = plan_edges(graph, p, mode, range(graph.edge_count), compile_plans=False,
+                      n_repeats=n_repeats, temp=temp, seed=seed)
+    return shard_edges([j.report.flops_sum for j in allj], world)[rank]
+
+
+def reduce_partials(partial: np.ndarray, group=None, device=None) -> np.ndarray:
+    """Sum per-angle-set partial energies over the ranks (one all_reduce;
+    NCCL on GPUs, gloo on CPU)."""
+    import torch
+
+    dist = torch.distributed
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return partial
+    buf = torch.tensor(np.asarray(partial, dtype=np.float64),
+                       device=device if device is not None else "cpu")
+    dist.all_reduce(buf, group=group)
+    return buf.cpu().numpy()
+
+
 def energy_expectation(graph: ProblemGraph, params: QaoaParams, mode: str = "zz+diagonal",
                        dtype="complex64", plan: EnergyPlan | None = None, group=None,
                        **kw) -> float:
@@ -257,19 +281,12 @@ def energy_expectation(graph: ProblemGraph, params: QaoaParams, mode: str = "zz+
     dist = torch.distributed
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     if plan is None:
+        edge_ids = None
         if world > 1:
-            rank = dist.get_rank(group)
-            allj = plan_edges(graph, params.p, mode, range(graph.edge_count), dtype=dtype,
-                              compile_plans=False, **{k: v for k, v in kw.items()
-                                                      if k in ("n_repeats", "temp", "seed")})
-            shard = shard_edges([j.report.flops_sum for j in allj], world)[rank]
-            plan = EnergyPlan(graph, params.p, mode, dtype, edge_ids=shard, **kw)
-        else:
-            plan = EnergyPlan(graph, params.p, mode, dtype, **kw)
+            edge_ids = rank_shard(graph, params.p, mode, dist.get_rank(group), world,
+                                  **{k: v for k, v in kw.items()
+                                     if k in ("n_repeats", "temp", "seed")})
+        plan = EnergyPlan(graph, params.p, mode, dtype, edge_ids=edge_ids, **kw)
     e = plan.energies(params)
-    if world > 1:
-        dev = torch.device("cuda", torch.cuda.current_device())
-        buf = torch.tensor(e, dtype=torch.float64, device=dev)
-        dist.all_reduce(buf, group=group)
-        e = buf.cpu().numpy()
-    return float(e[0])
+    dev = torch.device("cuda", torch.cuda.current_device()) if world > 1 else None
+    return float(reduce_partials(e, group, dev)[0])
