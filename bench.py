@@ -360,21 +360,16 @@ def run_gpu(args):
     def step():
         b = plan.launch(ang, st)
         if world > 1:
-            e = (b["e_smem"] if plan.smem_jobs else 0) + (b["e_hbm"] if plan.hbm_jobs else 0)
-            if not torch.is_tensor(e):
-                e = torch.zeros(A, dtype=torch.float64, device=dev)
-            dist.all_reduce(e)
+            dist.all_reduce(b["energy"])
         return b
 
-    # dominant-kernel timing: the SMEM batch launch alone, events on its stream
+    # dominant-kernel timing: the contraction executors alone (SMEM batch
+    # launch, or the level launches of the streaming kernel), events on the
+    # launching stream
     def kernel_only():
-        import ctypes as C  # noqa: F401
-
-        from paper_2106_15740_b200 import _native as N
-
         b = plan._buffers(A)
-        N.check(N.lib.qtn_batch_execute(plan._batch, b["inputs"].data_ptr(), plan.set_elems, A,
-                                        b["res_smem"].data_ptr(), st.cuda_stream))
+        plan._batch.execute(b["inputs"].data_ptr(), A, b["ws"].data_ptr(), b["res"].data_ptr(),
+                            st.cuda_stream, set_stride=plan.set_elems)
 
     clk = ClockSampler(local).__enter__()  # sampled through warm-up, timed and e2e loops
     for _ in range(args.warmup):
@@ -396,7 +391,7 @@ def run_gpu(args):
             e1.synchronize()
             step_times.append(e0.elapsed_time(e1) / 1e3)
             launches += plan.launches
-            if plan._batch is not None:
+            if True:
                 flush.zero_()
                 k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 k0.record(st)
@@ -441,14 +436,9 @@ def run_gpu(args):
     energy0 = float(en[0])
 
     peak, peak_kind = hbm_peak()
-    if kern_times:
-        kt = sum(kern_times) / len(kern_times)
-        alg = sum(j.plan.alg_bytes for j in plan.smem_jobs) * A
-        kname = "smem_net_kernel"
-    else:
-        kt = total / args.steps
-        alg = plan.alg_bytes * A
-        kname = "bucket_kernel"
+    kt = sum(kern_times) / len(kern_times)
+    alg = plan.alg_bytes * A
+    kname = "stream_kernel" if plan.hbm_jobs else "smem_net_kernel"
     achieved = alg / kt / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": profile_traffic(kname), "kernel": kname,

@@ -132,18 +132,24 @@ int qtn_plan_execute(qtn_plan* plan, const void* inputs, void* workspace,
 
 /* ----------------------------------------------------- batched execution */
 
-/* Pack the programs of n SMEM-executor plans into one device program (one
- * warp per network per input set).  Network i's packed inputs start at
- * element offset qtn_batch_input_offset(i) inside one input set; sets are
- * input_set_elems apart. */
+/* Upload n plans as one device program.  SMEM-executor networks run one
+ * warp per (network, input set) in a single launch; HBM-executor networks
+ * run level-synchronously: one streaming-kernel launch per level of the
+ * elimination trees, covering every network and input set at once, then one
+ * scalar-fold launch.  Network i's packed inputs start at element offset
+ * qtn_batch_input_offsets()[i] inside one input set. */
 int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** out_batch);
 int qtn_batch_input_elems(const qtn_batch* batch, int64_t* out_elems);
 int qtn_batch_input_offsets(const qtn_batch* batch, int64_t* out_offsets);
+/* device workspace needed by qtn_batch_execute for n_sets input sets */
+int qtn_batch_workspace_bytes(const qtn_batch* batch, int32_t n_sets, int64_t* out_bytes);
+/* number of kernel launches one qtn_batch_execute issues */
+int qtn_batch_launches(const qtn_batch* batch, int32_t* out_launches);
 /* results[s*n + i] = value of network i under input set s (complex128).
  * Input set s starts at inputs + s*set_stride elements (0: the batch's own
  * qtn_batch_input_elems). */
 int qtn_batch_execute(qtn_batch* batch, const void* inputs, int64_t set_stride,
-                      int32_t n_sets, void* results, void* stream);
+                      int32_t n_sets, void* workspace, void* results, void* stream);
 int qtn_batch_destroy(qtn_batch* batch);
 
 /* ------------------------------------------ parametric tensor generation */

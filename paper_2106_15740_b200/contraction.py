@@ -35,6 +35,7 @@ __all__ = [
     "DEFAULT_SMEM_BUDGET",
     "RankCapExceeded",
     "ContractionPlan",
+    "PlanBatch",
     "contract",
     "contract_many",
 ]
@@ -138,6 +139,8 @@ class ContractionPlan:
         return buf
 
     def execute(self, inputs_ptr: int, workspace_ptr: int, result_ptr: int, stream: int) -> None:
+        """Run on device buffers: packed inputs, >= workspace_bytes of
+        workspace (HBM executor), one complex128 result."""
         N.check(N.lib.qtn_plan_execute(self._h, inputs_ptr, workspace_ptr or None, result_ptr,
                                        stream), "plan execute")
 
@@ -155,43 +158,63 @@ def _torch_cuda():
     return torch
 
 
+class PlanBatch:
+    """Device program for many plans (qtn_batch): SMEM-executor networks in
+    one warp-per-network launch, HBM-executor networks level-synchronously
+    (one streaming launch per elimination-tree level for all of them)."""
+
+    def __init__(self, plans):
+        _torch_cuda()
+        self.plans = list(plans)
+        arr = (C.c_void_p * len(self.plans))(*[p.handle for p in self.plans])
+        h = C.c_void_p()
+        N.check(N.lib.qtn_batch_create(arr, len(self.plans), C.byref(h)), "batch create")
+        self._h = h
+        nel = C.c_int64()
+        N.check(N.lib.qtn_batch_input_elems(h, C.byref(nel)))
+        self.set_elems = int(nel.value)
+        offs = np.zeros(len(self.plans), dtype=np.int64)
+        N.check(N.lib.qtn_batch_input_offsets(h, N.i64(offs)))
+        self.input_offsets = offs
+        nl = C.c_int32()
+        N.check(N.lib.qtn_batch_launches(h, C.byref(nl)))
+        self.launches = int(nl.value)
+
+    def workspace_bytes(self, n_sets: int) -> int:
+        w = C.c_int64()
+        N.check(N.lib.qtn_batch_workspace_bytes(self._h, int(n_sets), C.byref(w)))
+        return int(w.value)
+
+    def pack(self, datas_list) -> np.ndarray:
+        host = np.zeros(max(self.set_elems, 1), dtype=np.complex128)
+        for p, off, datas in zip(self.plans, self.input_offsets, datas_list):
+            p.pack(datas, host[off: off + p.input_elems])
+        return host
+
+    def execute(self, inputs_ptr, n_sets, workspace_ptr, results_ptr, stream, set_stride=0):
+        N.check(N.lib.qtn_batch_execute(self._h, inputs_ptr, int(set_stride), int(n_sets),
+                                        workspace_ptr or None, results_ptr, stream),
+                "batch execute")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and N is not None and N.lib is not None:
+            N.lib.qtn_batch_destroy(h)
+            self._h = None
+
+
 def _run_plans(plans, datas_list):
-    """Execute plans (SMEM ones batched in one launch); returns complex list."""
+    """Execute plans as one batch on the current device; returns complex list."""
     torch = _torch_cuda()
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream(dev)
-    results = torch.zeros(len(plans), dtype=torch.complex128, device=dev)
-    smem = [i for i, p in enumerate(plans) if p.executor == N.EXEC_SMEM]
-    hbm = [i for i, p in enumerate(plans) if p.executor == N.EXEC_HBM]
-    if smem:
-        arr = (C.c_void_p * len(smem))(*[plans[i].handle for i in smem])
-        b = C.c_void_p()
-        N.check(N.lib.qtn_batch_create(arr, len(smem), C.byref(b)), "batch create")
-        try:
-            nel = C.c_int64()
-            N.check(N.lib.qtn_batch_input_elems(b, C.byref(nel)))
-            offs = np.zeros(len(smem), dtype=np.int64)
-            N.check(N.lib.qtn_batch_input_offsets(b, N.i64(offs)))
-            host = np.zeros(max(nel.value, 1), dtype=np.complex128)
-            for k, i in enumerate(smem):
-                plans[i].pack(datas_list[i], host[offs[k]: offs[k] + plans[i].input_elems])
-            inp = torch.from_numpy(host).pin_memory().to(dev, non_blocking=True)
-            res = torch.empty(len(smem), dtype=torch.complex128, device=dev)
-            N.check(N.lib.qtn_batch_execute(b, inp.data_ptr(), 0, 1, res.data_ptr(),
-                                            stream.cuda_stream), "batch execute")
-            results[smem] = res
-            torch.cuda.current_stream(dev).synchronize()
-        finally:
-            N.lib.qtn_batch_destroy(b)
-    for i in hbm:
-        p = plans[i]
-        host = p.pack(datas_list[i])
-        inp = torch.from_numpy(host).pin_memory().to(dev, non_blocking=True)
-        ws = torch.empty(max(p.workspace_bytes, 16), dtype=torch.uint8, device=dev)
-        res = torch.empty(1, dtype=torch.complex128, device=dev)
-        p.execute(inp.data_ptr(), ws.data_ptr(), res.data_ptr(), stream.cuda_stream)
-        results[i] = res[0]
-    out = results.cpu().numpy()
+    batch = PlanBatch(plans)
+    inp = torch.from_numpy(batch.pack(datas_list)).pin_memory().to(dev, non_blocking=True)
+    ws = torch.empty(max(batch.workspace_bytes(1), 16), dtype=torch.uint8, device=dev)
+    res = torch.empty(len(plans), dtype=torch.complex128, device=dev)
+    batch.execute(inp.data_ptr(), 1, ws.data_ptr(), res.data_ptr(), stream.cuda_stream)
+    out = res.cpu().numpy()
+    del batch
     return [complex(x) for x in out]
 
 

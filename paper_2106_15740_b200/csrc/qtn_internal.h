@@ -138,11 +138,15 @@ struct qtn_plan {
   double alg_bytes = 0.0;
   double flops_sum = 0.0;
   std::vector<uint8_t> program;          // SMEM executor blob
-  std::vector<qtn::BucketArgs> hbm_args; // HBM executor launch templates
-                                         // (pointers hold offsets; patched
-                                         // at execute time)
-  qtn_batch* self_batch = nullptr;       // device copy of `program` for
-                                         // single-plan SMEM execution
+  // HBM executor: one streaming descriptor per bucket (tagged pointers
+  // relative to the network's input block / workspace), its level in the
+  // elimination tree (level-synchronous execution) and its tile count.
+  std::vector<uint8_t> hbm_desc;
+  std::vector<uint64_t> hbm_desc_off;
+  std::vector<int32_t> hbm_level;
+  std::vector<uint64_t> hbm_tiles;
+  int32_t n_levels = 0;
+  qtn_batch* self_batch = nullptr;       // device copy for single-plan runs
   ~qtn_plan();
 };
 
@@ -152,10 +156,6 @@ void set_error(const std::string& msg);
 int launch_bucket(const BucketArgs& a, void* stream);
 int launch_fold(const void* const* ptrs, const uint8_t* c64, int n, int pow2,
                 void* result, bool accumulate, void* stream);
-int launch_smem_batch(const void* programs, const uint64_t* prog_offsets,
-                      const uint64_t* in_offsets, int n_nets, const void* inputs,
-                      int64_t set_elems, int n_sets, void* results, int64_t max_smem,
-                      void* stream);
 int device_alloc(void** p, size_t bytes);
 int device_free(void* p);
 int h2d(void* dst, const void* src, size_t bytes);

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "qtn_internal.h"
+#include "qtn_stream.h"
 
 using namespace qtn;
 
@@ -201,7 +202,8 @@ __device__ __forceinline__ void copy16(void* dst, const void* src, uint32_t byte
 __global__ void __launch_bounds__(32) smem_net_kernel(const uint8_t* __restrict__ progs,
                                                       const uint64_t* __restrict__ prog_off,
                                                       const uint64_t* __restrict__ in_off,
-                                                      int n_nets, const double2* __restrict__ inputs,
+                                                      const int32_t* __restrict__ out_index,
+                                                      int n_total, const double2* __restrict__ inputs,
                                                       int64_t set_elems, double2* __restrict__ results) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int net = blockIdx.x, set = blockIdx.y, lane = threadIdx.x;
@@ -237,8 +239,32 @@ __global__ void __launch_bounds__(32) smem_net_kernel(const uint8_t* __restrict_
         sm + sizeof(SmemHeader) + sizeof(SmemBucket) * h.n_buckets + sizeof(SmemOp) * h.n_ops);
     double2 r = make_double2(ldexp(1.0, (int)h.pow2), 0.0);
     for (uint32_t i = 0; i < h.n_scalars; ++i) r = cmul(r, D[sc[i]]);
-    results[(int64_t)set * n_nets + net] = r;
+    results[(int64_t)set * n_total + out_index[net]] = r;
   }
+}
+
+// Final scalar fold of the HBM-executor networks: 2^n_empty times every
+// rank-0 tensor (contraction.py:77-81, 108-110), one thread per (network, set).
+__global__ void hbm_fold_kernel(const uint64_t* __restrict__ tags, const uint8_t* __restrict__ c64,
+                                const uint32_t* __restrict__ first, const int32_t* __restrict__ pow2,
+                                const int32_t* __restrict__ out_index, int n_hbm, int n_total,
+                                const char* in_base, int64_t in_set_stride,
+                                const int64_t* __restrict__ net_in_off, const char* ws_base,
+                                int64_t ws_set_stride, const int64_t* __restrict__ net_ws_off,
+                                double2* __restrict__ results) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_hbm) return;
+  const int set = blockIdx.y;
+  const char* in = in_base + (int64_t)set * in_set_stride + net_in_off[i];
+  const char* ws = ws_base + (int64_t)set * ws_set_stride + net_ws_off[i];
+  double2 r = make_double2(ldexp(1.0, pow2[i]), 0.0);
+  for (uint32_t k = first[i]; k < first[i + 1]; ++k) {
+    const uint64_t t = tags[k];
+    const uint64_t sel = t >> kSelShift, off = t & kOffMask;
+    const char* p = sel == 1 ? in + off : (sel == 2 ? ws + off : reinterpret_cast<const char*>(off));
+    r = cmul(r, ld_c(p, 0, c64[k]));
+  }
+  results[(int64_t)set * n_total + out_index[i]] = r;
 }
 
 struct FoldArgs {
@@ -428,15 +454,55 @@ int h2d(void* dst, const void* src, size_t bytes) {
 
 // ------------------------------------------------------------- batches
 
+template <typename T>
+static int upload(T** dst, const std::vector<T>& v) {
+  int rc = device_alloc((void**)dst, std::max<size_t>(v.size(), 1) * sizeof(T));
+  if (rc) return rc;
+  if (!v.empty()) rc = h2d(*dst, v.data(), v.size() * sizeof(T));
+  return rc;
+}
+
 struct qtn_batch {
   int n = 0;
+  int64_t set_elems = 0;
+  std::vector<int64_t> in_offsets;
+  // SMEM executor part
+  int n_smem = 0;
+  int64_t max_smem = 0;
   uint8_t* d_prog = nullptr;
   uint64_t* d_prog_off = nullptr;
   uint64_t* d_in_off = nullptr;
-  int64_t set_elems = 0;
-  int64_t max_smem = 0;
-  std::vector<int64_t> in_offsets;
+  int32_t* d_smem_index = nullptr;
+  // HBM executor part (level-synchronous)
+  int n_hbm = 0;
+  int64_t ws_per_set = 0;
+  uint8_t* d_desc = nullptr;
+  uint64_t* d_item_desc = nullptr;
+  uint32_t* d_item_net = nullptr;
+  uint64_t* d_tile_prefix = nullptr;
+  int64_t* d_net_in_off = nullptr;
+  int64_t* d_net_ws_off = nullptr;
+  std::vector<uint32_t> level_item0;    // first item of each level (+ end)
+  std::vector<uint64_t> level_prefix0;  // first prefix entry of each level
+  std::vector<uint64_t> level_tiles;    // tiles of one set per level
+  uint64_t* d_fold_tags = nullptr;
+  uint8_t* d_fold_c64 = nullptr;
+  uint32_t* d_fold_first = nullptr;
+  int32_t* d_fold_pow2 = nullptr;
+  int32_t* d_hbm_index = nullptr;
 };
+
+extern "C" int qtn_batch_destroy(qtn_batch* B) {
+  if (!B) return QTN_OK;
+  for (void* p : {(void*)B->d_prog, (void*)B->d_prog_off, (void*)B->d_in_off,
+                  (void*)B->d_smem_index, (void*)B->d_desc, (void*)B->d_item_desc,
+                  (void*)B->d_item_net, (void*)B->d_tile_prefix, (void*)B->d_net_in_off,
+                  (void*)B->d_net_ws_off, (void*)B->d_fold_tags, (void*)B->d_fold_c64,
+                  (void*)B->d_fold_first, (void*)B->d_fold_pow2, (void*)B->d_hbm_index})
+    device_free(p);
+  delete B;
+  return QTN_OK;
+}
 
 extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** out) {
   if (!plans || n < 1 || !out) {
@@ -445,32 +511,98 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   }
   int rc = device_check();
   if (rc) return rc;
-  std::vector<uint8_t> blob;
-  std::vector<uint64_t> poff(n), ioff(n);
   qtn_batch* B = new qtn_batch();
   B->n = n;
+  // input layout shared by both executors: networks in order, 32-byte aligned
   int64_t in = 0;
   for (int i = 0; i < n; ++i) {
-    const qtn_plan* P = plans[i];
-    if (!P || P->executor != QTN_EXEC_SMEM) {
+    if (!plans[i]) {
       delete B;
-      set_error("qtn_batch_create: every plan must use the SMEM executor");
+      set_error("qtn_batch_create: null plan");
       return QTN_EINVAL;
     }
-    poff[i] = blob.size();
-    blob.insert(blob.end(), P->program.begin(), P->program.end());
-    ioff[i] = (uint64_t)in;
     B->in_offsets.push_back(in);
-    in += (P->input_elems + 1) & ~1ll;  // keep every network 32-byte aligned
-    B->max_smem = std::max(B->max_smem, P->smem_bytes);
+    in += (plans[i]->input_elems + 1) & ~1ll;
   }
-  B->set_elems = in;
-  if ((rc = device_alloc((void**)&B->d_prog, blob.size())) ||
-      (rc = device_alloc((void**)&B->d_prog_off, n * sizeof(uint64_t))) ||
-      (rc = device_alloc((void**)&B->d_in_off, n * sizeof(uint64_t))) ||
-      (rc = h2d(B->d_prog, blob.data(), blob.size())) ||
-      (rc = h2d(B->d_prog_off, poff.data(), n * sizeof(uint64_t))) ||
-      (rc = h2d(B->d_in_off, ioff.data(), n * sizeof(uint64_t)))) {
+  B->set_elems = std::max<int64_t>(in, 2);
+  // ---- SMEM networks
+  std::vector<uint8_t> blob;
+  std::vector<uint64_t> poff, ioff;
+  std::vector<int32_t> sidx;
+  // ---- HBM networks
+  std::vector<uint8_t> desc;
+  std::vector<int32_t> hidx;
+  std::vector<int64_t> net_in, net_ws;
+  int32_t max_lev = 0;
+  for (int i = 0; i < n; ++i) {
+    const qtn_plan* P = plans[i];
+    if (P->executor == QTN_EXEC_SMEM) {
+      poff.push_back(blob.size());
+      blob.insert(blob.end(), P->program.begin(), P->program.end());
+      ioff.push_back((uint64_t)B->in_offsets[i]);
+      sidx.push_back(i);
+      B->max_smem = std::max(B->max_smem, P->smem_bytes);
+    } else {
+      hidx.push_back(i);
+      net_in.push_back(16 * B->in_offsets[i]);
+      net_ws.push_back(B->ws_per_set);
+      B->ws_per_set += (P->workspace_bytes + 255) & ~255ll;
+      max_lev = std::max(max_lev, P->n_levels);
+    }
+  }
+  B->n_smem = (int)sidx.size();
+  B->n_hbm = (int)hidx.size();
+  // level-major item lists over all HBM networks
+  std::vector<uint64_t> item_desc, prefix;
+  std::vector<uint32_t> item_net;
+  std::vector<uint64_t> desc_base(B->n_hbm);
+  for (int h = 0; h < B->n_hbm; ++h) {
+    const qtn_plan* P = plans[hidx[h]];
+    desc_base[h] = desc.size();
+    desc.insert(desc.end(), P->hbm_desc.begin(), P->hbm_desc.end());
+  }
+  for (int32_t lev = 0; lev < max_lev; ++lev) {
+    B->level_item0.push_back((uint32_t)item_desc.size());
+    B->level_prefix0.push_back(prefix.size());
+    uint64_t acc = 0;
+    prefix.push_back(0);
+    for (int h = 0; h < B->n_hbm; ++h) {
+      const qtn_plan* P = plans[hidx[h]];
+      for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
+        if (P->hbm_level[bi] != lev) continue;
+        item_desc.push_back(desc_base[h] + P->hbm_desc_off[bi]);
+        item_net.push_back((uint32_t)h);
+        acc += P->hbm_tiles[bi];
+        prefix.push_back(acc);
+      }
+    }
+    B->level_tiles.push_back(acc);
+  }
+  B->level_item0.push_back((uint32_t)item_desc.size());
+  // scalar folds
+  std::vector<uint64_t> ftags;
+  std::vector<uint8_t> fc64;
+  std::vector<uint32_t> ffirst;
+  std::vector<int32_t> fpow2;
+  for (int h = 0; h < B->n_hbm; ++h) {
+    const qtn_plan* P = plans[hidx[h]];
+    ffirst.push_back((uint32_t)ftags.size());
+    fpow2.push_back(P->n_empty);
+    for (int32_t id : P->scalars) {
+      const auto& t = P->tensors[id];
+      ftags.push_back(t.input ? tag_in(16ull * (uint64_t)t.in_off) : tag_ws((uint64_t)t.ws_off));
+      fc64.push_back(t.c64 ? 1 : 0);
+    }
+  }
+  ffirst.push_back((uint32_t)ftags.size());
+  if ((rc = upload(&B->d_prog, blob)) || (rc = upload(&B->d_prog_off, poff)) ||
+      (rc = upload(&B->d_in_off, ioff)) || (rc = upload(&B->d_smem_index, sidx)) ||
+      (rc = upload(&B->d_desc, desc)) || (rc = upload(&B->d_item_desc, item_desc)) ||
+      (rc = upload(&B->d_item_net, item_net)) || (rc = upload(&B->d_tile_prefix, prefix)) ||
+      (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
+      (rc = upload(&B->d_fold_tags, ftags)) || (rc = upload(&B->d_fold_c64, fc64)) ||
+      (rc = upload(&B->d_fold_first, ffirst)) || (rc = upload(&B->d_fold_pow2, fpow2)) ||
+      (rc = upload(&B->d_hbm_index, hidx))) {
     qtn_batch_destroy(B);
     return rc;
   }
@@ -490,38 +622,82 @@ extern "C" int qtn_batch_input_offsets(const qtn_batch* B, int64_t* out) {
   return QTN_OK;
 }
 
+extern "C" int qtn_batch_workspace_bytes(const qtn_batch* B, int32_t n_sets, int64_t* out) {
+  if (!B || !out || n_sets < 1) return QTN_EINVAL;
+  *out = B->ws_per_set * n_sets;
+  return QTN_OK;
+}
+
+extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t* out) {
+  if (!B || !out) return QTN_EINVAL;
+  int c = B->n_smem ? 1 : 0;
+  if (B->n_hbm) {
+    for (uint64_t t : B->level_tiles) c += t ? 1 : 0;
+    c += 1;
+  }
+  *out = c;
+  return QTN_OK;
+}
+
 extern "C" int qtn_batch_execute(qtn_batch* B, const void* inputs, int64_t set_stride,
-                                 int32_t n_sets, void* results, void* stream) {
-  if (set_stride <= 0) set_stride = B ? B->set_elems : 0;
+                                 int32_t n_sets, void* workspace, void* results, void* stream) {
   if (!B || !results || n_sets < 1 || n_sets > 65535) {
     set_error("qtn_batch_execute: bad arguments");
     return QTN_EINVAL;
   }
+  if (set_stride <= 0) set_stride = B->set_elems;
+  if (B->n_hbm && B->ws_per_set > 0 && !workspace) {
+    set_error("qtn_batch_execute: HBM networks need a workspace (qtn_batch_workspace_bytes)");
+    return QTN_EINVAL;
+  }
   int rc = device_check();
   if (rc) return rc;
-  static int64_t attr = 0;
-  if (B->max_smem > 48 * 1024 && B->max_smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(smem_net_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)B->max_smem);
-    if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel attribute");
-    attr = B->max_smem;
-  }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  dim3 grid(B->n, n_sets);
-  smem_net_kernel<<<grid, 32, B->max_smem, st>>>(B->d_prog, B->d_prog_off, B->d_in_off, B->n,
-                                                 reinterpret_cast<const double2*>(inputs),
-                                                 set_stride, reinterpret_cast<double2*>(results));
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel launch");
-  return QTN_OK;
-}
-
-extern "C" int qtn_batch_destroy(qtn_batch* B) {
-  if (!B) return QTN_OK;
-  device_free(B->d_prog);
-  device_free(B->d_prog_off);
-  device_free(B->d_in_off);
-  delete B;
+  if (B->n_smem) {
+    static int64_t attr = 0;
+    if (B->max_smem > 48 * 1024 && B->max_smem > attr) {
+      cudaError_t e = cudaFuncSetAttribute(smem_net_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)B->max_smem);
+      if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel attribute");
+      attr = B->max_smem;
+    }
+    dim3 grid(B->n_smem, n_sets);
+    smem_net_kernel<<<grid, 32, B->max_smem, st>>>(
+        B->d_prog, B->d_prog_off, B->d_in_off, B->d_smem_index, B->n,
+        reinterpret_cast<const double2*>(inputs), set_stride, reinterpret_cast<double2*>(results));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel launch");
+  }
+  if (B->n_hbm) {
+    for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
+      if (!B->level_tiles[lev]) continue;
+      StreamLaunch L;
+      std::memset(&L, 0, sizeof(L));
+      L.descs = B->d_desc;
+      L.item_desc = B->d_item_desc + B->level_item0[lev];
+      L.item_net = B->d_item_net + B->level_item0[lev];
+      L.tile_prefix = B->d_tile_prefix + B->level_prefix0[lev];
+      L.n_items = B->level_item0[lev + 1] - B->level_item0[lev];
+      L.n_sets = (uint32_t)n_sets;
+      L.total_tiles = B->level_tiles[lev];
+      L.in_base = reinterpret_cast<const char*>(inputs);
+      L.in_set_stride = 16 * set_stride;
+      L.net_in_off = B->d_net_in_off;
+      L.ws_base = reinterpret_cast<char*>(workspace);
+      L.ws_set_stride = B->ws_per_set;
+      L.net_ws_off = B->d_net_ws_off;
+      if ((rc = launch_stream(L, stream))) return rc;
+    }
+    dim3 grid((B->n_hbm + 127) / 128, n_sets);
+    hbm_fold_kernel<<<grid, 128, 0, st>>>(
+        B->d_fold_tags, B->d_fold_c64, B->d_fold_first, B->d_fold_pow2, B->d_hbm_index, B->n_hbm,
+        B->n, reinterpret_cast<const char*>(inputs), 16 * set_stride, B->d_net_in_off,
+        reinterpret_cast<const char*>(workspace), B->ws_per_set, B->d_net_ws_off,
+        reinterpret_cast<double2*>(results));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "hbm_fold_kernel launch");
+  }
   return QTN_OK;
 }
 

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "qtn_internal.h"
+#include "qtn_stream.h"
 
 namespace qtn {
 
@@ -266,6 +267,78 @@ static int build_bucket_args(const std::vector<std::vector<int32_t>>& opvars,
   return QTN_OK;
 }
 
+// Streaming descriptor of one bucket (qtn_stream.h): the same operand split
+// as build_bucket_args (primary streamed, small operands tabulated, the rest
+// gathered), runs stored whole (gathers are OR-linear over output bits, so
+// the kernel splits tile-base and tile-local parts itself), tile size chosen
+// so that a tile's primary slice is <= 32 KiB.
+int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
+  BucketArgs a;
+  std::vector<int32_t> g_ops, t_ops;
+  int rc = build_bucket_args(s.opvars, s.opc64, s.primary, s.v, s.out_vars, s.out_c64, true, a,
+                             g_ops, t_ops);
+  if (rc) return rc;
+  if ((int)a.ng - 1 > kSMaxG || (int)a.nt > kSMaxT || (int)a.ntop > kSMaxTOps) {
+    set_error("bucket has too many operands for the streaming kernel");
+    return QTN_EINVAL;
+  }
+  const size_t base = blob.size();
+  const int ng = (int)a.ng - 1;
+  const size_t bytes = sizeof(SHdr) + ng * sizeof(SGRec) + a.nt * sizeof(STRec) +
+                       a.ntop * sizeof(SORec);
+  blob.resize(base + bytes, 0);
+  SHdr* h = reinterpret_cast<SHdr*>(blob.data() + base);
+  const int R = (int)s.out_vars.size();
+  const bool pc64 = s.opc64[s.primary] != 0;
+  const int tb = std::min(R, pc64 ? 11 : 10);
+  h->out = s.out_tag;
+  h->p = s.optag[s.primary];
+  h->R = (uint8_t)R;
+  h->out_c64 = s.out_c64 ? 1 : 0;
+  h->p_c64 = pc64 ? 1 : 0;
+  h->p_k = (uint8_t)a.p_k;
+  h->p_rank = (uint8_t)s.opvars[s.primary].size();
+  h->ng = (uint8_t)ng;
+  h->nt = (uint8_t)a.nt;
+  h->ntop = (uint8_t)a.ntop;
+  h->tb = (uint8_t)tb;
+  h->table_entries = (uint16_t)a.table_entries;
+  h->desc_bytes = (uint16_t)bytes;
+  h->n_tiles = 1ull << (R - tb);
+  SGRec* g = reinterpret_cast<SGRec*>(blob.data() + base + sizeof(SHdr));
+  for (int i = 0; i < ng; ++i) {
+    const GOpArg& src = a.g[i + 1];
+    g[i].ptr = s.optag[g_ops[i + 1]];
+    g[i].vshift = (uint8_t)src.vshift;
+    g[i].c64 = (uint8_t)src.c64;
+    g[i].n_runs = (uint8_t)(src.n_lo + src.n_hi);
+    std::copy(src.lo, src.lo + src.n_lo, g[i].runs);
+    std::copy(src.hi, src.hi + src.n_hi, g[i].runs + src.n_lo);
+  }
+  STRec* t = reinterpret_cast<STRec*>(blob.data() + base + sizeof(SHdr) + ng * sizeof(SGRec));
+  for (uint32_t j = 0; j < a.nt; ++j) {
+    const TableArg& src = a.t[j];
+    t[j].nbits = (uint8_t)src.nbits;
+    t[j].n_runs = (uint8_t)(src.n_lo + src.n_hi);
+    t[j].first_op = (uint8_t)src.first_op;
+    t[j].n_ops = (uint8_t)src.n_ops;
+    t[j].smem_off = (uint16_t)src.smem_off;
+    std::copy(src.lo, src.lo + src.n_lo, t[j].runs);
+    std::copy(src.hi, src.hi + src.n_hi, t[j].runs + src.n_lo);
+  }
+  SORec* o = reinterpret_cast<SORec*>(blob.data() + base + sizeof(SHdr) + ng * sizeof(SGRec) +
+                                      a.nt * sizeof(STRec));
+  for (uint32_t k = 0; k < a.ntop; ++k) {
+    const TOpArg& src = a.top[k];
+    o[k].ptr = s.optag[t_ops[k]];
+    o[k].vshift = (uint8_t)src.vshift;
+    o[k].c64 = (uint8_t)src.c64;
+    o[k].n_runs = (uint8_t)src.n_runs;
+    std::copy(src.runs, src.runs + src.n_runs, o[k].runs);
+  }
+  return QTN_OK;
+}
+
 }  // namespace qtn
 
 using namespace qtn;
@@ -495,41 +568,58 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     for (auto& t : P->tensors) t.c64 = false;
   } else {
     P->executor = QTN_EXEC_HBM;
-    // device arena for intermediates
+    // levels of the elimination tree: a bucket runs after the buckets that
+    // produce its intermediate operands (level-synchronous execution)
+    std::vector<int32_t> tlevel(P->tensors.size(), 0);
+    int32_t nlev = 0;
+    P->hbm_level.assign(nb, 0);
+    for (int bi = 0; bi < nb; ++bi) {
+      int32_t lv = 0;
+      for (int32_t id : P->buckets[bi].ops) lv = std::max(lv, tlevel[id]);
+      P->hbm_level[bi] = lv;  // 0-based level index
+      tlevel[P->buckets[bi].out] = lv + 1;
+      nlev = std::max(nlev, lv + 1);
+    }
+    P->n_levels = nlev;
+    // device arena: lifetimes in levels (concurrent buckets never alias)
     std::vector<Block> hblocks;
     int64_t ws = 0;
     for (size_t id = P->n_inputs; id < P->tensors.size(); ++id) {
       auto& t = P->tensors[id];
       int64_t bytes = elem_bytes(t.c64) << t.rank();
       bytes = std::max<int64_t>(bytes, 256);
-      t.ws_off = place(hblocks, bytes, t.born, t.last_use, 256);
+      const int32_t s = P->hbm_level[t.born];
+      const int32_t e = t.last_use >= nb ? nlev + 1 : P->hbm_level[t.last_use];
+      t.ws_off = place(hblocks, bytes, s, e, 256);
       ws = std::max(ws, t.ws_off + bytes);
     }
     P->workspace_bytes = ws;
-    // launch templates
+    // one streaming descriptor per bucket
+    auto tag_of = [&](int32_t id) -> uint64_t {
+      const auto& t = P->tensors[id];
+      return t.input ? tag_in(16ull * (uint64_t)t.in_off) : tag_ws((uint64_t)t.ws_off);
+    };
     for (int bi = 0; bi < nb; ++bi) {
       const auto& b = P->buckets[bi];
-      std::vector<std::vector<int32_t>> opvars;
-      std::vector<uint8_t> opc64;
+      BucketSpec spec;
       for (int32_t id : b.ops) {
-        opvars.push_back(P->tensors[id].vars);
-        opc64.push_back(P->tensors[id].c64 ? 1 : 0);
+        spec.opvars.push_back(P->tensors[id].vars);
+        spec.opc64.push_back(P->tensors[id].c64 ? 1 : 0);
+        spec.optag.push_back(tag_of(id));
       }
-      BucketArgs a;
-      std::vector<int32_t> g_ops, t_ops;
-      int rc = build_bucket_args(opvars, opc64, b.primary, b.v, P->tensors[b.out].vars,
-                                 P->tensors[b.out].c64, true, a, g_ops, t_ops);
+      spec.primary = b.primary;
+      spec.v = b.v;
+      spec.out_vars = P->tensors[b.out].vars;
+      spec.out_c64 = P->tensors[b.out].c64;
+      spec.out_tag = tag_of(b.out);
+      P->hbm_desc_off.push_back(P->hbm_desc.size());
+      int rc = encode_stream_desc(spec, P->hbm_desc);
       if (rc) {
         delete P;
         return rc;
       }
-      // remember which tensor each pointer slot refers to (patched at execute)
-      for (int i = 0; i < (int)a.ng; ++i)
-        a.g[i].ptr = reinterpret_cast<const void*>((uintptr_t)b.ops[g_ops[i]]);
-      for (int i = 0; i < (int)a.ntop; ++i)
-        a.top[i].ptr = reinterpret_cast<const void*>((uintptr_t)b.ops[t_ops[i]]);
-      a.out = reinterpret_cast<void*>((uintptr_t)b.out);
-      P->hbm_args.push_back(a);
+      const SHdr* h = reinterpret_cast<const SHdr*>(P->hbm_desc.data() + P->hbm_desc_off.back());
+      P->hbm_tiles.push_back(h->n_tiles);
     }
   }
   // algorithmic bytes: e * (operand entries + output entries) per bucket
@@ -656,9 +746,25 @@ extern "C" int qtn_bucket_contract(int32_t n_ops, const int32_t* ranks, const in
     aligned = ov.size() >= low.size() &&
               std::equal(low.begin(), low.end(), ov.end() - low.size());
   }
+  if (aligned) {
+    // the streaming kernel (bulk-copy pipeline, lookup tables)
+    BucketSpec spec;
+    spec.opvars = opvars;
+    spec.opc64 = opc64;
+    for (int i = 0; i < n_ops; ++i) spec.optag.push_back(tag_abs(ptrs[i]));
+    spec.primary = primary;
+    spec.v = elim_var;
+    spec.out_vars = ov;
+    spec.out_c64 = out_c64 != 0;
+    spec.out_tag = tag_abs(out);
+    std::vector<uint8_t> desc;
+    int rc = encode_stream_desc(spec, desc);
+    if (rc == QTN_OK) return launch_stream_single(desc, stream);
+  }
+  // any other layout: generic fused kernel, every operand gathered
   BucketArgs a;
   std::vector<int32_t> g_ops, t_ops;
-  int rc = build_bucket_args(opvars, opc64, primary, elim_var, ov, out_c64 != 0, aligned, a,
+  int rc = build_bucket_args(opvars, opc64, primary, elim_var, ov, out_c64 != 0, false, a,
                              g_ops, t_ops);
   if (rc) return rc;
   for (int i = 0; i < (int)a.ng; ++i) a.g[i].ptr = ptrs[g_ops[i]];
@@ -677,38 +783,14 @@ extern "C" int qtn_plan_execute(qtn_plan* P, const void* inputs, void* workspace
   }
   int rc = device_check();
   if (rc) return rc;
-  if (P->executor == QTN_EXEC_SMEM) {
-    if (!P->self_batch) {
-      qtn_plan* one[1] = {P};
-      rc = qtn_batch_create(one, 1, &P->self_batch);
-      if (rc) return rc;
-    }
-    return qtn_batch_execute(P->self_batch, inputs, 0, 1, result, stream);
-  }
-  if (P->workspace_bytes > 0 && !workspace) {
+  if (P->executor == QTN_EXEC_HBM && P->workspace_bytes > 0 && !workspace) {
     set_error("HBM executor needs a workspace of workspace_bytes");
     return QTN_EINVAL;
   }
-  auto addr = [&](int32_t id) -> char* {
-    const auto& t = P->tensors[id];
-    if (t.input) return (char*)inputs + 16 * t.in_off;
-    return (char*)workspace + t.ws_off;
-  };
-  for (size_t bi = 0; bi < P->buckets.size(); ++bi) {
-    BucketArgs a = P->hbm_args[bi];
-    for (uint32_t i = 0; i < a.ng; ++i) a.g[i].ptr = addr((int32_t)(uintptr_t)a.g[i].ptr);
-    for (uint32_t i = 0; i < a.ntop; ++i) a.top[i].ptr = addr((int32_t)(uintptr_t)a.top[i].ptr);
-    a.out = addr((int32_t)(uintptr_t)a.out);
-    rc = launch_bucket(a, stream);
+  if (!P->self_batch) {
+    qtn_plan* one[1] = {P};
+    rc = qtn_batch_create(one, 1, &P->self_batch);
     if (rc) return rc;
   }
-  // scalar fold: 2^n_empty * prod(rank-0 tensors)  (contraction.py:77-81, 108-110)
-  std::vector<const void*> ptrs;
-  std::vector<uint8_t> c64;
-  for (int32_t id : P->scalars) {
-    ptrs.push_back(addr(id));
-    c64.push_back(P->tensors[id].c64 ? 1 : 0);
-  }
-  return launch_fold(ptrs.data(), c64.data(), (int)ptrs.size(), P->n_empty, result, false,
-                     stream);
+  return qtn_batch_execute(P->self_batch, inputs, 0, 1, workspace, result, stream);
 }

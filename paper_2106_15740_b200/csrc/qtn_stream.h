@@ -1,0 +1,103 @@
+// Streaming bucket executor: descriptors, work lists, launch entry points.
+// Shared by the host encoder (qtn_plan.cpp) and the kernel (qtn_stream.cu).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace qtn {
+
+// Tagged pointer: bits 62-63 select the base, the rest is a byte offset.
+//   0: absolute address   1: network input block   2: network workspace
+constexpr uint64_t kSelShift = 62;
+constexpr uint64_t kOffMask = (1ull << kSelShift) - 1;
+inline uint64_t tag_abs(const void* p) { return (uint64_t)(uintptr_t)p; }
+inline uint64_t tag_in(uint64_t byte_off) { return (1ull << kSelShift) | byte_off; }
+inline uint64_t tag_ws(uint64_t byte_off) { return (2ull << kSelShift) | byte_off; }
+
+constexpr int kSMaxG = 3;        // gathered operands besides the primary
+constexpr int kSMaxT = 4;        // lookup tables
+constexpr int kSMaxTOps = 16;    // small operands folded into tables
+constexpr int kSGRuns = 33;
+constexpr int kSTRuns = 8;
+
+// Descriptor of one bucket (16-byte aligned, variable length:
+// header, ng GRec, nt TRec, ntop ORec).
+struct SHdr {
+  uint64_t out;          // tagged
+  uint64_t p;            // tagged primary operand
+  uint8_t R;             // output rank
+  uint8_t out_c64;
+  uint8_t p_c64;
+  uint8_t p_k;           // bit of v inside the primary
+  uint8_t p_rank;
+  uint8_t ng, nt, ntop;
+  uint8_t tb;            // tile bits
+  uint8_t pad0[3];
+  uint16_t table_entries;
+  uint16_t desc_bytes;
+  uint64_t n_tiles;
+  uint8_t pad1[24];
+};
+struct SGRec {
+  uint64_t ptr;          // tagged
+  uint8_t vshift, c64, n_runs, pad;
+  uint32_t runs[kSGRuns];  // output bits -> operand bits (src | dst<<8 | len<<16)
+};
+struct STRec {
+  uint8_t nbits, n_runs, first_op, n_ops;
+  uint16_t smem_off;
+  uint16_t pad;
+  uint32_t runs[kSTRuns];  // output bits -> table index bits
+  uint32_t pad2[2];
+};
+struct SORec {
+  uint64_t ptr;          // tagged
+  uint8_t vshift, c64, n_runs, pad;
+  uint32_t runs[kSTRuns];  // table index bits -> operand bits
+};
+static_assert(sizeof(SHdr) == 64, "SHdr");
+static_assert(sizeof(SGRec) == 144, "SGRec");
+static_assert(sizeof(STRec) == 48, "STRec");
+static_assert(sizeof(SORec) == 48, "SORec");
+constexpr int kSDescMax = sizeof(SHdr) + kSMaxG * sizeof(SGRec) + kSMaxT * sizeof(STRec) +
+                          kSMaxTOps * sizeof(SORec);
+
+// A bucket in "operand form" before encoding.
+struct BucketSpec {
+  std::vector<std::vector<int32_t>> opvars;  // operand variable lists (MSB first)
+  std::vector<uint8_t> opc64;
+  std::vector<uint64_t> optag;               // tagged pointers
+  int32_t primary;                           // index of the aligned primary operand
+  int32_t v;
+  std::vector<int32_t> out_vars;
+  bool out_c64;
+  uint64_t out_tag;
+};
+
+// Host encoder: appends the descriptor bytes; returns QTN_OK or QTN_EINVAL
+// (bucket not expressible: too many wide operands).
+int encode_stream_desc(const BucketSpec& b, std::vector<uint8_t>& blob);
+
+// Work list of one launch: items = (descriptor, network), tiles flattened.
+struct StreamLaunch {
+  const uint8_t* descs;         // device blob
+  const uint64_t* item_desc;    // device: descriptor byte offset per item
+  const uint32_t* item_net;     // device: network index per item
+  const uint64_t* tile_prefix;  // device: n_items + 1
+  uint32_t n_items;
+  uint32_t n_sets;
+  uint64_t total_tiles;         // tiles of one set
+  const char* in_base;          // inputs
+  int64_t in_set_stride;        // bytes
+  const int64_t* net_in_off;    // device, bytes
+  char* ws_base;
+  int64_t ws_set_stride;        // bytes
+  const int64_t* net_ws_off;    // device, bytes
+};
+
+int launch_stream(const StreamLaunch& L, void* stream);
+// single descriptor with absolute pointers, descriptor passed by value
+int launch_stream_single(const std::vector<uint8_t>& desc, void* stream);
+
+}  // namespace qtn

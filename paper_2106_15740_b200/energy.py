@@ -12,7 +12,8 @@ computed once; every evaluation then runs, for any number of angle sets:
 
     tensorgen (angles -> gate tensors, on device)
       -> SMEM executor: one launch, one warp per (edge network, angle set)
-      -> HBM executor: fused per-bucket kernels for the wide networks
+      -> HBM executor: one streaming launch per elimination-tree level for
+         all wide networks and angle sets, then one scalar-fold launch
       -> energy reduction
 
 Multi-GPU: `shard_edges` splits the edges by longest-processing-time on
@@ -31,7 +32,7 @@ import numpy as np
 from . import _native as N
 from .circuit import ProblemGraph, QaoaParams
 from .contraction import (DEFAULT_MIXED_RANK, DEFAULT_RANK_CAP, DEFAULT_SMEM_BUDGET,
-                          ContractionPlan)
+                          ContractionPlan, PlanBatch)
 from .lightcone import EnergyTemplate, energy_template
 from .ordering import ContractionOrder, CostReport, rgreedy_order
 
@@ -128,38 +129,17 @@ class EnergyPlan:
         dev = torch.device("cuda", torch.cuda.current_device())
         self._torch = torch
         self._device = dev
-        # input-set layout: [SMEM batch inputs | HBM network 0 | HBM network 1 | ...]
-        self._batch = None
-        base = 0
+        # one device program for every edge network; input set layout from it
+        self._batch = PlanBatch([j.plan for j in self.jobs])
+        self.set_elems = self._batch.set_elems
         recs = []
-        if self.smem_jobs:
-            arr = (C.c_void_p * len(self.smem_jobs))(*[j.plan.handle for j in self.smem_jobs])
-            b = C.c_void_p()
-            N.check(N.lib.qtn_batch_create(arr, len(self.smem_jobs), C.byref(b)), "batch create")
-            self._batch = b
-            nel = C.c_int64()
-            N.check(N.lib.qtn_batch_input_elems(b, C.byref(nel)))
-            offs = np.zeros(len(self.smem_jobs), dtype=np.int64)
-            N.check(N.lib.qtn_batch_input_offsets(b, N.i64(offs)))
-            for j, o in zip(self.smem_jobs, offs):
-                r = j.template.recipes.copy()
-                r["out_offset"] = j.plan.input_offsets + o
-                recs.append(r)
-            base = int(nel.value)
-        self._hbm_offsets = []
-        for j in self.hbm_jobs:
-            base = (base + 1) & ~1
+        for j, off in zip(self.jobs, self._batch.input_offsets):
             r = j.template.recipes.copy()
-            r["out_offset"] = j.plan.input_offsets + base
+            r["out_offset"] = j.plan.input_offsets + off
             recs.append(r)
-            self._hbm_offsets.append(base)
-            base += j.plan.input_elems
-        self.set_elems = max(base, 2)
         allrec = np.concatenate(recs) if recs else np.zeros(0, dtype=N.RECIPE_DTYPE)
         self._n_recipes = len(allrec)
         self._recipes = torch.from_numpy(allrec.view(np.uint8).copy()).to(dev)
-        ws = max([j.plan.workspace_bytes for j in self.hbm_jobs] or [16])
-        self._ws = torch.empty(ws, dtype=torch.uint8, device=dev)
 
     def _buffers(self, n_sets):
         if n_sets not in self._bufs:
@@ -167,18 +147,23 @@ class EnergyPlan:
             dev = self._device
             self._bufs[n_sets] = dict(
                 inputs=t.zeros(n_sets * self.set_elems, dtype=t.complex128, device=dev),
-                res_smem=t.zeros((n_sets, max(len(self.smem_jobs), 1)), dtype=t.complex128, device=dev),
-                res_hbm=t.zeros((n_sets, max(len(self.hbm_jobs), 1)), dtype=t.complex128, device=dev),
-                e_smem=t.zeros(n_sets, dtype=t.float64, device=dev),
-                e_hbm=t.zeros(n_sets, dtype=t.float64, device=dev),
+                ws=t.empty(max(self._batch.workspace_bytes(n_sets), 16), dtype=t.uint8,
+                           device=dev),
+                res=t.zeros((n_sets, len(self.jobs)), dtype=t.complex128, device=dev),
+                energy=t.zeros(n_sets, dtype=t.float64, device=dev),
             )
         return self._bufs[n_sets]
 
+    @property
+    def launches_per_eval(self) -> int:
+        """Kernel launches of one evaluation: tensorgen + executors + energy."""
+        self._prepare()
+        return 2 + self._batch.launches
+
     def launch(self, angles_dev, stream=None):
         """Enqueue one evaluation for every angle set in `angles_dev`
-        ([n_sets, 2p] float64 on the device).  Returns the buffer dict; the
-        energies are bufs['e_smem'] + bufs['e_hbm'] once the stream is done.
-        Kernel launches: 1 tensorgen + 1 SMEM batch + per-bucket HBM + reductions."""
+        ([n_sets, 2p] float64 on the device); returns the buffer dict
+        (bufs['energy'][s], bufs['res'][s, job]) valid once the stream is done."""
         self._prepare()
         t = self._torch
         n_sets = int(angles_dev.shape[0])
@@ -188,26 +173,11 @@ class EnergyPlan:
         N.check(N.lib.qtn_tensorgen(self._recipes.data_ptr(), self._n_recipes,
                                     angles_dev.data_ptr(), 2 * self.p, n_sets, self.set_elems,
                                     b["inputs"].data_ptr(), sp), "tensorgen")
-        self.launches = 1
-        if self._batch is not None:
-            N.check(N.lib.qtn_batch_execute(self._batch, b["inputs"].data_ptr(), self.set_elems,
-                                            n_sets, b["res_smem"].data_ptr(), sp), "batch")
-            N.check(N.lib.qtn_energy_reduce(b["res_smem"].data_ptr(), len(self.smem_jobs), n_sets,
-                                            b["e_smem"].data_ptr(), None, sp), "energy")
-            self.launches += 2
-        if self.hbm_jobs:
-            esz = 16
-            ip = b["inputs"].data_ptr()
-            rp = b["res_hbm"].data_ptr()
-            nh = len(self.hbm_jobs)
-            for s in range(n_sets):
-                for k, (j, off) in enumerate(zip(self.hbm_jobs, self._hbm_offsets)):
-                    j.plan.execute(ip + esz * (s * self.set_elems + off), self._ws.data_ptr(),
-                                   rp + esz * (s * nh + k), sp)
-                    self.launches += j.plan.n_buckets + 1
-            N.check(N.lib.qtn_energy_reduce(rp, nh, n_sets, b["e_hbm"].data_ptr(), None, sp),
-                    "energy")
-            self.launches += 1
+        self._batch.execute(b["inputs"].data_ptr(), n_sets, b["ws"].data_ptr(),
+                            b["res"].data_ptr(), sp, set_stride=self.set_elems)
+        N.check(N.lib.qtn_energy_reduce(b["res"].data_ptr(), len(self.jobs), n_sets,
+                                        b["energy"].data_ptr(), None, sp), "energy")
+        self.launches = 2 + self._batch.launches
         return b
 
     def energies(self, angle_sets) -> np.ndarray:
@@ -222,8 +192,7 @@ class EnergyPlan:
             raise ValueError(f"expected {2 * self.p} angles per set, got {a.shape[1]}")
         dev_a = t.from_numpy(a).pin_memory().to(self._device, non_blocking=True)
         b = self.launch(dev_a)
-        out = (b["e_smem"] if self.smem_jobs else 0) + (b["e_hbm"] if self.hbm_jobs else 0)
-        return out.cpu().numpy().copy()
+        return b["energy"].cpu().numpy().copy()
 
     def zz_values(self, params: QaoaParams) -> dict:
         """Per-edge <Z_iZ_j> (complex) for one angle set, keyed by edge index."""
@@ -231,20 +200,8 @@ class EnergyPlan:
         t = self._torch
         a = t.from_numpy(np.atleast_2d(params.as_vector())).to(self._device)
         b = self.launch(a)
-        out = {}
-        rs = b["res_smem"][0].cpu().numpy()
-        rh = b["res_hbm"][0].cpu().numpy()
-        for k, j in enumerate(self.smem_jobs):
-            out[j.index] = complex(rs[k])
-        for k, j in enumerate(self.hbm_jobs):
-            out[j.index] = complex(rh[k])
-        return out
-
-    def __del__(self):
-        b = getattr(self, "_batch", None)
-        if b is not None and N is not None and N.lib is not None:
-            N.lib.qtn_batch_destroy(b)
-            self._batch = None
+        r = b["res"][0].cpu().numpy()
+        return {j.index: complex(r[k]) for k, j in enumerate(self.jobs)}
 
 
 def rank_shard(graph: ProblemGraph, p: int, mode: str, rank: int, world: int,

@@ -173,6 +173,18 @@ def test_synthetic_buckets_c_abi(golden):
                 tol = 1e-12
             err = np.abs(got - want).max() / np.abs(want).max()
             assert err < tol, (case["w"], case["m"], c64, err)
+            if not c64:
+                # a non-preferred output layout (reversed) takes the generic
+                # gather kernel; compare against the transposed golden
+                rv = ov[::-1].copy()
+                out2 = torch.empty(1 << len(ov), dtype=dt, device="cuda")
+                N.check(N.lib.qtn_bucket_contract(len(ops), N.i32(ranks), N.i32(offs),
+                                                  N.i32(flat), ptrs, N.u8(flags), 0, len(rv),
+                                                  N.i32(rv), 0, out2.data_ptr(),
+                                                  torch.cuda.current_stream().cuda_stream))
+                got2 = out2.cpu().numpy().reshape((2,) * len(ov))
+                want2 = want.reshape((2,) * len(ov)).transpose(list(range(len(ov)))[::-1])
+                assert np.abs(got2 - want2).max() / np.abs(want2).max() < 1e-12
 
 
 def test_rank_cap_raised_before_execution():
