@@ -342,14 +342,14 @@ def run_gpu(args):
     graph = Q.random_regular_graph(wl["n"], 3, 0)
     edge_ids = wl["edges"] if wl["edges"] is not None else list(range(graph.edge_count))
     t0 = time.perf_counter()
+    dtype = args.dtype or wl["dtype"]
+    # every rank plans all jobs (edges, or 2^k slices of them) identically and
+    # keeps its LPT shard: no exchange before the final all-reduce
+    jobs = Q.plan_edges(graph, wl["p"], wl["mode"], edge_ids, dtype=dtype, slice_k=args.slices)
     if world > 1:
-        allj = Q.plan_edges(graph, wl["p"], wl["mode"], edge_ids, compile_plans=False)
-        shard = Q.shard_edges([j.report.flops_sum for j in allj], world)[rank]
-        my_edges = [edge_ids[k] for k in shard]
-    else:
-        my_edges = edge_ids
-    plan = Q.EnergyPlan(graph, wl["p"], wl["mode"], dtype=args.dtype or wl["dtype"],
-                        edge_ids=my_edges)
+        keep = Q.shard_edges([j.cost for j in jobs], world)[rank]
+        jobs = [jobs[k] for k in keep]
+    plan = Q.EnergyPlan(graph, wl["p"], wl["mode"], dtype=dtype, jobs=jobs)
     plan_s = time.perf_counter() - t0
     A = args.angle_sets
     sets = angle_sets(wl["p"], A)
@@ -368,8 +368,8 @@ def run_gpu(args):
     # launching stream
     def kernel_only():
         b = plan._buffers(A)
-        plan._batch.execute(b["inputs"].data_ptr(), A, b["ws"].data_ptr(), b["res"].data_ptr(),
-                            st.cuda_stream, set_stride=plan.set_elems)
+        plan._batch.execute_angles(ang.data_ptr(), 2 * wl["p"], A, b["inputs"].data_ptr(),
+                                   b["ws"].data_ptr(), b["res"].data_ptr(), st.cuda_stream)
 
     clk = ClockSampler(local).__enter__()  # sampled through warm-up, timed and e2e loops
     for _ in range(args.warmup):
@@ -475,6 +475,8 @@ def run_gpu(args):
             "data": "synthetic (seeded random 3-regular graph, seeded angles)",
             "config": {"workload": args.workload, "n": wl["n"], "p": wl["p"], "mode": wl["mode"],
                        "edges": len(edge_ids), "angle_sets_per_step": A,
+                       "slices_per_edge": 2 ** args.slices,
+                       "width_max": max(j.report.width for j in plan.jobs),
                        "contractions_per_step": len(edge_ids) * A,
                        "l2": "flushed between timed steps (256 MiB write)",
                        "parallelism": f"edges LPT-sharded over {world} GPU(s)",
@@ -504,6 +506,8 @@ def main():
     ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS) + ["config5"])
     ap.add_argument("--angle-sets", type=int, default=1024)
     ap.add_argument("--dtype", default=None)
+    ap.add_argument("--slices", type=int, default=0,
+                    help="split every edge network into 2^k slices (config 4)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-config5", action="store_true")

@@ -184,10 +184,26 @@ int qtn_tensorgen(const qtn_tensor_recipe* recipes_dev, int64_t n_recipes,
                   const double* angles_dev, int32_t n_angles, int32_t n_sets,
                   int64_t set_elems, void* out_dev, void* stream);
 
-/* energies[s] = sum_i (1 - Re values[s*n + i]) / 2 and
- * zz_sum[s] = sum_i values[s*n+i] (complex128); deterministic order. */
-int qtn_energy_reduce(const void* values_dev, int32_t n, int32_t n_sets,
-                      double* energies_dev, void* zz_sum_dev, void* stream);
+/* Attach per-network tensor recipes (host array; network i owns
+ * recipes[offsets[i] .. offsets[i+1]), out_offset relative to the network's
+ * packed input).  Afterwards qtn_batch_execute_angles builds every input on
+ * device: SMEM-executor networks generate their tensors inside the executor
+ * kernel (no input buffer at all), HBM networks through qtn_tensorgen. */
+int qtn_batch_set_recipes(qtn_batch* batch, const qtn_tensor_recipe* recipes,
+                          const int64_t* offsets);
+/* One evaluation for n_sets angle vectors (angles_dev: n_sets x n_angles
+ * float64).  inputs_scratch: >= n_sets * qtn_batch_input_elems complex128
+ * (only touched when the batch has HBM networks; may be NULL otherwise). */
+int qtn_batch_execute_angles(qtn_batch* batch, const double* angles_dev, int32_t n_angles,
+                             int32_t n_sets, void* inputs_scratch, void* workspace,
+                             void* results, void* stream);
+
+/* energies[s] = sum_i (w_i - Re values[s*n + i]) / 2 and
+ * zz_sum[s] = sum_i values[s*n+i] (complex128); deterministic order.
+ * w_i = weights[i] (NULL: 1); an edge split into S slices has S networks of
+ * weight 1/S whose values sum to <Z_iZ_j>. */
+int qtn_energy_reduce(const void* values_dev, const double* weights_dev, int32_t n,
+                      int32_t n_sets, double* energies_dev, void* zz_sum_dev, void* stream);
 
 /* --------------------------------------------------- single-bucket entry */
 

@@ -92,8 +92,10 @@ _SIGNATURES = {
     "qtn_batch_launches": [_p, _i32p],
     "qtn_batch_execute": [_p, _p, C.c_int64, C.c_int32, _p, _p, _p],
     "qtn_batch_destroy": [_p],
+    "qtn_batch_set_recipes": [_p, _p, _i64p],
+    "qtn_batch_execute_angles": [_p, _p, C.c_int32, C.c_int32, _p, _p, _p, _p],
     "qtn_tensorgen": [_p, C.c_int64, _p, C.c_int32, C.c_int32, C.c_int64, _p, _p],
-    "qtn_energy_reduce": [_p, C.c_int32, C.c_int32, _p, _p, _p],
+    "qtn_energy_reduce": [_p, _p, C.c_int32, C.c_int32, _p, _p, _p],
     "qtn_bucket_contract": [C.c_int32, _i32p, _i32p, _i32p, C.POINTER(_p), _u8p, C.c_int32,
                             C.c_int32, _i32p, C.c_int32, _p, _p],
     "qtn_bucket_layout": [C.c_int32, _i32p, _i32p, _i32p, C.c_int32, _i32p, _i32p],

@@ -196,6 +196,31 @@ class PlanBatch:
                                         workspace_ptr or None, results_ptr, stream),
                 "batch execute")
 
+    @property
+    def has_hbm(self) -> bool:
+        return any(p.executor == N.EXEC_HBM for p in self.plans)
+
+    def set_recipes(self, recipes_per_plan):
+        """Tensor recipes (RECIPE_DTYPE arrays, offsets relative to each
+        network's packed input); enables execute_angles."""
+        allrec = np.concatenate(recipes_per_plan) if recipes_per_plan else np.zeros(
+            0, dtype=N.RECIPE_DTYPE)
+        allrec = np.ascontiguousarray(allrec)
+        offs = np.zeros(len(recipes_per_plan) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum([len(r) for r in recipes_per_plan])
+        N.check(N.lib.qtn_batch_set_recipes(self._h, allrec.ctypes.data, N.i64(offs)),
+                "set recipes")
+        nl = C.c_int32()
+        N.check(N.lib.qtn_batch_launches(self._h, C.byref(nl)))
+        # + tensorgen for HBM networks
+        self.launches = int(nl.value) + (1 if self.has_hbm else 0)
+
+    def execute_angles(self, angles_ptr, n_angles, n_sets, scratch_ptr, workspace_ptr,
+                       results_ptr, stream):
+        N.check(N.lib.qtn_batch_execute_angles(self._h, angles_ptr, int(n_angles), int(n_sets),
+                                               scratch_ptr or None, workspace_ptr or None,
+                                               results_ptr, stream), "batch execute (angles)")
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and N is not None and N.lib is not None:

@@ -80,8 +80,29 @@ struct SmemHeader {
   uint32_t in_elems;           // packed input elements (complex128)
   uint32_t data_elems;         // inputs + arena
   uint32_t prog_bytes;         // whole blob, multiple of 16
-  uint32_t pad;
+  uint32_t gen_off;            // byte offset of the generator section (0: none)
+  uint32_t n_params;           // generator: distinct gate parameters
+  uint32_t n_recs;             // generator: one record per input tensor
+  uint32_t pad[2];
 };
+// Generator section (appended by qtn_batch_set_recipes): the warp builds its
+// own input tensors in shared memory from the angles of its set — the
+// on-device form of gate_matrix + slicing (circuit.py:186-205,
+// network.py:153-165) fused into the executor.
+struct SmemGenParam {          // phase e^{-i t}, t = scale*angles[angle] + offset
+  double scale;
+  double offset;
+  int32_t angle;               // -1: constant t = offset; -2: literal value (scale + i*offset)
+  int32_t pad;
+};
+struct SmemGenRec {
+  uint8_t kind, full_rank, keep_mask, fixed_bits;
+  uint8_t param;
+  uint8_t pad;
+  uint16_t out_off;            // element offset in the warp's data region
+};
+static_assert(sizeof(SmemGenParam) == 24, "gen param");
+static_assert(sizeof(SmemGenRec) == 8, "gen rec");
 struct SmemBucket {
   uint16_t out_off;
   uint8_t R;
@@ -96,7 +117,7 @@ struct SmemOp {
   uint8_t n_runs;
   uint16_t runs[kSmemOpRuns];  // src | dst<<5 | len<<10
 };
-static_assert(sizeof(SmemHeader) == 32, "header");
+static_assert(sizeof(SmemHeader) == 48, "header");
 static_assert(sizeof(SmemBucket) == 8, "bucket");
 static_assert(sizeof(SmemOp) == 32, "op");
 

@@ -186,32 +186,113 @@ __device__ __forceinline__ uint32_t sgather(uint32_t e, const SmemOp& o) {
   return idx;
 }
 
-__device__ __forceinline__ void copy16(void* dst, const void* src, uint32_t bytes, int lane) {
+__device__ __forceinline__ void copy16(void* dst, const void* src, uint32_t bytes, uint32_t t,
+                                       uint32_t nt) {
   const uint4* s = reinterpret_cast<const uint4*>(src);
   uint4* d = reinterpret_cast<uint4*>(dst);
   const uint32_t n = bytes / 16;
-  uint32_t i = lane;
-  for (; i + 96 < n; i += 128) {
-    uint4 x0 = __ldg(s + i), x1 = __ldg(s + i + 32), x2 = __ldg(s + i + 64), x3 = __ldg(s + i + 96);
-    d[i] = x0; d[i + 32] = x1; d[i + 64] = x2; d[i + 96] = x3;
+  uint32_t i = t;
+  for (; i + 3 * nt < n; i += 4 * nt) {
+    uint4 x0 = __ldg(s + i), x1 = __ldg(s + i + nt), x2 = __ldg(s + i + 2 * nt),
+          x3 = __ldg(s + i + 3 * nt);
+    d[i] = x0; d[i + nt] = x1; d[i + 2 * nt] = x2; d[i + 3 * nt] = x3;
   }
-  for (; i < n; i += 32) d[i] = __ldg(s + i);
+  for (; i < n; i += nt) d[i] = __ldg(s + i);
 }
 
-// One warp executes one network's bucket program for one input set.
-__global__ void __launch_bounds__(32) smem_net_kernel(const uint8_t* __restrict__ progs,
-                                                      const uint64_t* __restrict__ prog_off,
-                                                      const uint64_t* __restrict__ in_off,
-                                                      const int32_t* __restrict__ out_index,
-                                                      int n_total, const double2* __restrict__ inputs,
-                                                      int64_t set_elems, double2* __restrict__ results) {
+// Gate tensor entry from the parameter phase ph = e^{-it} (or a literal).
+__device__ __forceinline__ double2 gen_entry(uint32_t kind, uint32_t i, double2 ph) {
+  const double s = 0.70710678118654757;  // 1/sqrt(2), circuit.py:179
+  switch (kind) {
+    case QTN_GATE_INIT: return make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+    case QTN_GATE_H: return make_double2(i == 3 ? -s : s, 0.0);
+    case QTN_GATE_ZPOW: return i == 0 ? make_double2(1.0, 0.0) : (i == 3 ? ph : make_double2(0.0, 0.0));
+    case QTN_GATE_ZPOW_DIAG: return i == 0 ? make_double2(1.0, 0.0) : ph;
+    case QTN_GATE_XPOW: {
+      const bool d = (i == 0 || i == 3);
+      return d ? make_double2(0.5 * (1.0 + ph.x), 0.5 * ph.y) : make_double2(0.5 * (1.0 - ph.x), -0.5 * ph.y);
+    }
+    case QTN_GATE_CNOT: {
+      const uint32_t row = i >> 2, col = i & 3;
+      return make_double2(col == (row < 2 ? row : (row ^ 1)) ? 1.0 : 0.0, 0.0);
+    }
+    case QTN_GATE_ZZ: {  // diag(r, r*, r*, r), r = e^{i g} = conj(ph)
+      const uint32_t row = i >> 2, col = i & 3;
+      if (row != col) return make_double2(0.0, 0.0);
+      return (row == 0 || row == 3) ? make_double2(ph.x, -ph.y) : ph;
+    }
+    case QTN_GATE_ZZ_DIAG: return (i == 0 || i == 3) ? make_double2(ph.x, -ph.y) : ph;
+    case QTN_GATE_SCALAR: return ph;
+  }
+  return make_double2(0.0, 0.0);
+}
+
+struct SmemArgs {
+  const uint8_t* progs;
+  const uint64_t* prog_off;
+  const uint64_t* in_off;
+  const int32_t* out_index;
+  const double2* inputs;       // packed inputs (NULL when generating from angles)
+  int64_t set_elems;
+  double2* results;
+  const double* angles;        // n_sets x n_angles (NULL: copy inputs)
+  int32_t n_angles;
+  int32_t n_sets;
+  int32_t n_total;
+  uint32_t prog_max;           // bytes reserved for the program (CTA-shared)
+  uint32_t warp_bytes;         // bytes of one warp's data region
+};
+
+constexpr int kNetWarps = 4;   // angle sets per CTA (one warp each)
+
+// One CTA = one network x kNetWarps angle sets.  The bucket program is
+// staged once per CTA; each warp owns a data region (inputs + intermediates)
+// and either generates its inputs from its angle vector or copies them.
+__global__ void __launch_bounds__(32 * kNetWarps) smem_net_kernel(const __grid_constant__ SmemArgs A) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const int net = blockIdx.x, set = blockIdx.y, lane = threadIdx.x;
-  const uint8_t* gp = progs + prog_off[net];
+  const int net = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int set = blockIdx.y * (int)(blockDim.x >> 5) + warp;
+  const uint8_t* gp = A.progs + A.prog_off[net];
   const SmemHeader h = *reinterpret_cast<const SmemHeader*>(gp);
-  copy16(sm, gp, h.prog_bytes, lane);
-  double2* D = reinterpret_cast<double2*>(sm + h.prog_bytes);
-  copy16(D, inputs + (int64_t)set * set_elems + in_off[net], h.in_elems * 16u, lane);
+  copy16(sm, gp, h.prog_bytes, threadIdx.x, blockDim.x);
+  __syncthreads();
+  if (set >= A.n_sets) return;
+  double2* D = reinterpret_cast<double2*>(sm + A.prog_max + warp * A.warp_bytes);
+  if (A.angles && h.n_recs) {
+    double2* ph = D + h.data_elems;
+    const SmemGenParam* par = reinterpret_cast<const SmemGenParam*>(sm + h.gen_off);
+    const double* ang = A.angles + (int64_t)set * A.n_angles;
+    for (uint32_t k = lane; k < h.n_params; k += 32) {
+      const SmemGenParam q = par[k];
+      if (q.angle == -2) {
+        ph[k] = make_double2(q.scale, q.offset);
+      } else {
+        const double t = q.angle >= 0 ? q.scale * ang[q.angle] + q.offset : q.offset;
+        double sn, cs;
+        sincos(t, &sn, &cs);
+        ph[k] = make_double2(cs, -sn);
+      }
+    }
+    __syncwarp();
+    const SmemGenRec* rec = reinterpret_cast<const SmemGenRec*>(sm + h.gen_off +
+                                                                sizeof(SmemGenParam) * h.n_params);
+    for (uint32_t r = lane; r < h.n_recs; r += 32) {
+      const SmemGenRec g = rec[r];
+      const double2 p = ph[g.param];
+      const uint32_t fr = g.full_rank, kept = __popc(g.keep_mask);
+      for (uint32_t e = 0; e < (1u << kept); ++e) {
+        uint32_t full = 0;
+        int kb = (int)kept - 1;
+        for (uint32_t q = 0; q < fr; ++q) {
+          const uint32_t bit = ((g.keep_mask >> q) & 1) ? (e >> kb--) & 1 : (g.fixed_bits >> q) & 1;
+          full = (full << 1) | bit;
+        }
+        D[g.out_off + e] = gen_entry(g.kind, full, p);
+      }
+    }
+  } else {
+    copy16(D, A.inputs + (int64_t)set * A.set_elems + A.in_off[net], h.in_elems * 16u, lane, 32);
+  }
   __syncwarp();
   const SmemBucket* bk = reinterpret_cast<const SmemBucket*>(sm + sizeof(SmemHeader));
   const SmemOp* ops = reinterpret_cast<const SmemOp*>(sm + sizeof(SmemHeader) +
@@ -239,7 +320,7 @@ __global__ void __launch_bounds__(32) smem_net_kernel(const uint8_t* __restrict_
         sm + sizeof(SmemHeader) + sizeof(SmemBucket) * h.n_buckets + sizeof(SmemOp) * h.n_ops);
     double2 r = make_double2(ldexp(1.0, (int)h.pow2), 0.0);
     for (uint32_t i = 0; i < h.n_scalars; ++i) r = cmul(r, D[sc[i]]);
-    results[(int64_t)set * n_total + out_index[net]] = r;
+    A.results[(int64_t)set * A.n_total + A.out_index[net]] = r;
   }
 }
 
@@ -349,14 +430,14 @@ __global__ void tensorgen_kernel(const qtn_tensor_recipe* __restrict__ rec, int6
   }
 }
 
-__global__ void energy_kernel(const double2* __restrict__ vals, int n, double* energies,
-                              double2* zz) {
+__global__ void energy_kernel(const double2* __restrict__ vals, const double* __restrict__ w,
+                              int n, double* energies, double2* zz) {
   const int s = blockIdx.x;
   if (threadIdx.x != 0) return;
   double e = 0.0, zr = 0.0, zi = 0.0;
   for (int i = 0; i < n; ++i) {
     const double2 v = vals[(int64_t)s * n + i];
-    e += (1.0 - v.x) / 2.0;
+    e += ((w ? w[i] : 1.0) - v.x) / 2.0;
     zr += v.x;
     zi += v.y;
   }
@@ -473,6 +554,13 @@ struct qtn_batch {
   uint64_t* d_prog_off = nullptr;
   uint64_t* d_in_off = nullptr;
   int32_t* d_smem_index = nullptr;
+  std::vector<std::vector<uint8_t>> smem_progs;  // host copies (gen sections appended later)
+  std::vector<int32_t> smem_global;              // batch index of each SMEM network
+  uint32_t prog_max = 0;                         // bytes reserved per CTA for the program
+  uint32_t warp_bytes = 0;                       // bytes per warp data region
+  bool has_recipes = false;
+  qtn_tensor_recipe* d_hbm_rec = nullptr;        // recipes of the HBM networks
+  int64_t n_hbm_rec = 0;
   // HBM executor part (level-synchronous)
   int n_hbm = 0;
   int64_t ws_per_set = 0;
@@ -498,7 +586,8 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_smem_index, (void*)B->d_desc, (void*)B->d_item_desc,
                   (void*)B->d_item_net, (void*)B->d_tile_prefix, (void*)B->d_net_in_off,
                   (void*)B->d_net_ws_off, (void*)B->d_fold_tags, (void*)B->d_fold_c64,
-                  (void*)B->d_fold_first, (void*)B->d_fold_pow2, (void*)B->d_hbm_index})
+                  (void*)B->d_fold_first, (void*)B->d_fold_pow2, (void*)B->d_hbm_index,
+                  (void*)B->d_hbm_rec})
     device_free(p);
   delete B;
   return QTN_OK;
@@ -537,6 +626,13 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   for (int i = 0; i < n; ++i) {
     const qtn_plan* P = plans[i];
     if (P->executor == QTN_EXEC_SMEM) {
+      B->smem_progs.push_back(P->program);
+      B->smem_global.push_back(i);
+      B->prog_max = std::max<uint32_t>(B->prog_max, (uint32_t)P->program.size());
+      {
+        const SmemHeader* hh = reinterpret_cast<const SmemHeader*>(P->program.data());
+        B->warp_bytes = std::max<uint32_t>(B->warp_bytes, 16u * hh->data_elems);
+      }
       poff.push_back(blob.size());
       blob.insert(blob.end(), P->program.begin(), P->program.end());
       ioff.push_back((uint64_t)B->in_offsets[i]);
@@ -639,9 +735,136 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t* out) {
   return QTN_OK;
 }
 
+static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const double* angles,
+                     int32_t n_angles, int32_t n_sets, void* workspace, void* results,
+                     void* stream);
+
 extern "C" int qtn_batch_execute(qtn_batch* B, const void* inputs, int64_t set_stride,
                                  int32_t n_sets, void* workspace, void* results, void* stream) {
-  if (!B || !results || n_sets < 1 || n_sets > 65535) {
+  return run_batch(B, inputs, set_stride, nullptr, 0, n_sets, workspace, results, stream);
+}
+
+extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
+                                     const int64_t* offsets) {
+  if (!B || !rec || !offsets) {
+    set_error("qtn_batch_set_recipes: bad arguments");
+    return QTN_EINVAL;
+  }
+  int rc = device_check();
+  if (rc) return rc;
+  // SMEM networks: append a generator section to each program
+  std::vector<uint8_t> blob;
+  std::vector<uint64_t> poff;
+  uint32_t prog_max = 0, warp_bytes = 0;
+  for (size_t k = 0; k < B->smem_progs.size(); ++k) {
+    const int gi = B->smem_global[k];
+    std::vector<uint8_t> prog = B->smem_progs[k];
+    SmemHeader* h = reinterpret_cast<SmemHeader*>(prog.data());
+    std::vector<SmemGenParam> params;
+    std::vector<SmemGenRec> recs;
+    for (int64_t r = offsets[gi]; r < offsets[gi + 1]; ++r) {
+      const qtn_tensor_recipe& q = rec[r];
+      SmemGenParam p{};
+      if (q.kind == QTN_GATE_SCALAR) {
+        p.scale = q.scale;
+        p.offset = q.offset;
+        p.angle = -2;
+      } else {
+        const bool has_t = q.kind == QTN_GATE_ZPOW || q.kind == QTN_GATE_XPOW ||
+                           q.kind == QTN_GATE_ZZ || q.kind == QTN_GATE_ZPOW_DIAG ||
+                           q.kind == QTN_GATE_ZZ_DIAG;
+        p.scale = has_t ? q.scale : 0.0;
+        p.offset = has_t ? q.offset : 0.0;
+        p.angle = has_t ? (q.angle >= 0 ? q.angle : -1) : -1;
+      }
+      size_t slot = 0;
+      for (; slot < params.size(); ++slot)
+        if (params[slot].scale == p.scale && params[slot].offset == p.offset &&
+            params[slot].angle == p.angle)
+          break;
+      if (slot == params.size()) params.push_back(p);
+      if (slot > 255 || q.out_offset + (1ll << q.full_rank) > 65535) {
+        set_error("qtn_batch_set_recipes: network too large for the fused generator");
+        return QTN_EINVAL;
+      }
+      SmemGenRec g{};
+      g.kind = q.kind;
+      g.full_rank = q.full_rank;
+      g.keep_mask = q.keep_mask;
+      g.fixed_bits = q.fixed_bits;
+      g.param = (uint8_t)slot;
+      g.out_off = (uint16_t)q.out_offset;
+      recs.push_back(g);
+    }
+    const size_t gen_off = prog.size();
+    size_t gen_bytes = params.size() * sizeof(SmemGenParam) + recs.size() * sizeof(SmemGenRec);
+    gen_bytes = (gen_bytes + 15) & ~size_t(15);
+    prog.resize(gen_off + gen_bytes, 0);
+    h = reinterpret_cast<SmemHeader*>(prog.data());
+    std::memcpy(prog.data() + gen_off, params.data(), params.size() * sizeof(SmemGenParam));
+    std::memcpy(prog.data() + gen_off + params.size() * sizeof(SmemGenParam), recs.data(),
+                recs.size() * sizeof(SmemGenRec));
+    h->gen_off = (uint32_t)gen_off;
+    h->n_params = (uint32_t)params.size();
+    h->n_recs = (uint32_t)recs.size();
+    h->prog_bytes = (uint32_t)prog.size();
+    prog_max = std::max<uint32_t>(prog_max, (uint32_t)prog.size());
+    warp_bytes = std::max<uint32_t>(warp_bytes, 16u * (h->data_elems + h->n_params));
+    poff.push_back(blob.size());
+    blob.insert(blob.end(), prog.begin(), prog.end());
+  }
+  // HBM networks: recipes relocated into the batch input layout
+  std::vector<qtn_tensor_recipe> hrec;
+  for (int i = 0; i < B->n; ++i) {
+    if (std::find(B->smem_global.begin(), B->smem_global.end(), i) != B->smem_global.end())
+      continue;
+    for (int64_t r = offsets[i]; r < offsets[i + 1]; ++r) {
+      qtn_tensor_recipe q = rec[r];
+      q.out_offset += B->in_offsets[i];
+      hrec.push_back(q);
+    }
+  }
+  if (!blob.empty()) {
+    device_free(B->d_prog);
+    device_free(B->d_prog_off);
+    B->d_prog = nullptr;
+    B->d_prog_off = nullptr;
+    if ((rc = upload(&B->d_prog, blob)) || (rc = upload(&B->d_prog_off, poff))) return rc;
+    B->prog_max = prog_max;
+    B->warp_bytes = warp_bytes;
+  }
+  device_free(B->d_hbm_rec);
+  B->d_hbm_rec = nullptr;
+  if ((rc = upload(&B->d_hbm_rec, hrec))) return rc;
+  B->n_hbm_rec = (int64_t)hrec.size();
+  B->has_recipes = true;
+  return QTN_OK;
+}
+
+extern "C" int qtn_batch_execute_angles(qtn_batch* B, const double* angles, int32_t n_angles,
+                                        int32_t n_sets, void* inputs_scratch, void* workspace,
+                                        void* results, void* stream) {
+  if (!B || !angles || !B->has_recipes) {
+    set_error("qtn_batch_execute_angles: needs qtn_batch_set_recipes first");
+    return QTN_EINVAL;
+  }
+  if (B->n_hbm && !inputs_scratch) {
+    set_error("qtn_batch_execute_angles: HBM networks need an input scratch buffer");
+    return QTN_EINVAL;
+  }
+  int rc;
+  if (B->n_hbm_rec &&
+      (rc = qtn_tensorgen(B->d_hbm_rec, B->n_hbm_rec, angles, n_angles, n_sets, B->set_elems,
+                          inputs_scratch, stream)))
+    return rc;
+  return run_batch(B, inputs_scratch, B->set_elems, angles, n_angles, n_sets, workspace, results,
+                   stream);
+}
+
+static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const double* angles,
+                     int32_t n_angles, int32_t n_sets, void* workspace, void* results,
+                     void* stream) {
+  if (!B || !results || n_sets < 1) {
     set_error("qtn_batch_execute: bad arguments");
     return QTN_EINVAL;
   }
@@ -650,22 +873,43 @@ extern "C" int qtn_batch_execute(qtn_batch* B, const void* inputs, int64_t set_s
     set_error("qtn_batch_execute: HBM networks need a workspace (qtn_batch_workspace_bytes)");
     return QTN_EINVAL;
   }
+  if (!angles && !inputs) {
+    set_error("qtn_batch_execute: no inputs");
+    return QTN_EINVAL;
+  }
   int rc = device_check();
   if (rc) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (B->n_smem) {
-    static int64_t attr = 0;
-    if (B->max_smem > 48 * 1024 && B->max_smem > attr) {
+    const uint32_t prog_max = (B->prog_max + 15) & ~15u;
+    const uint32_t warp_bytes = (B->warp_bytes + 15) & ~15u;
+    // angle sets per CTA: as many warps as fit next to one copy of the program
+    int W = (int)std::min<size_t>(kNetWarps, (227u * 1024u - prog_max) / std::max(warp_bytes, 16u));
+    W = std::max(1, std::min(W, (int)n_sets));
+    const size_t smem = (size_t)prog_max + (size_t)W * warp_bytes;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
       cudaError_t e = cudaFuncSetAttribute(smem_net_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)B->max_smem);
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel attribute");
-      attr = B->max_smem;
+      attr = smem;
     }
-    dim3 grid(B->n_smem, n_sets);
-    smem_net_kernel<<<grid, 32, B->max_smem, st>>>(
-        B->d_prog, B->d_prog_off, B->d_in_off, B->d_smem_index, B->n,
-        reinterpret_cast<const double2*>(inputs), set_stride, reinterpret_cast<double2*>(results));
+    SmemArgs a;
+    a.progs = B->d_prog;
+    a.prog_off = B->d_prog_off;
+    a.in_off = B->d_in_off;
+    a.out_index = B->d_smem_index;
+    a.inputs = reinterpret_cast<const double2*>(inputs);
+    a.set_elems = set_stride;
+    a.results = reinterpret_cast<double2*>(results);
+    a.angles = (angles && B->has_recipes) ? angles : nullptr;
+    a.n_angles = n_angles;
+    a.n_sets = n_sets;
+    a.n_total = B->n;
+    a.prog_max = prog_max;
+    a.warp_bytes = warp_bytes;
+    dim3 grid(B->n_smem, (n_sets + W - 1) / W);
+    smem_net_kernel<<<grid, 32 * W, smem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel launch");
   }
@@ -720,8 +964,8 @@ extern "C" int qtn_tensorgen(const qtn_tensor_recipe* recipes, int64_t n, const 
   return QTN_OK;
 }
 
-extern "C" int qtn_energy_reduce(const void* values, int32_t n, int32_t n_sets, double* energies,
-                                 void* zz_sum, void* stream) {
+extern "C" int qtn_energy_reduce(const void* values, const double* weights, int32_t n,
+                                 int32_t n_sets, double* energies, void* zz_sum, void* stream) {
   if (!values || n < 0 || n_sets < 1) {
     set_error("qtn_energy_reduce: bad arguments");
     return QTN_EINVAL;
@@ -729,8 +973,8 @@ extern "C" int qtn_energy_reduce(const void* values, int32_t n, int32_t n_sets, 
   int rc = device_check();
   if (rc) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  energy_kernel<<<n_sets, 32, 0, st>>>(reinterpret_cast<const double2*>(values), n, energies,
-                                       reinterpret_cast<double2*>(zz_sum));
+  energy_kernel<<<n_sets, 32, 0, st>>>(reinterpret_cast<const double2*>(values), weights, n,
+                                       energies, reinterpret_cast<double2*>(zz_sum));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "energy launch");
   return QTN_OK;

@@ -34,6 +34,7 @@ from .circuit import ProblemGraph, QaoaParams
 from .contraction import (DEFAULT_MIXED_RANK, DEFAULT_RANK_CAP, DEFAULT_SMEM_BUDGET,
                           ContractionPlan, PlanBatch)
 from .lightcone import EnergyTemplate, energy_template
+from .slicing import choose_slice_vars, slice_assignments
 from .ordering import ContractionOrder, CostReport, rgreedy_order
 
 __all__ = ["EdgeJob", "EnergyPlan", "plan_edges", "shard_edges", "rank_shard", "reduce_partials",
@@ -41,31 +42,48 @@ __all__ = ["EdgeJob", "EnergyPlan", "plan_edges", "shard_edges", "rank_shard", "
 
 
 class EdgeJob:
-    """Template + order + compiled plan of one edge network."""
+    """Template + order + compiled plan of one edge network (or of one slice
+    of it: `weight` = 1/2^k, `assignment` = the sliced variables' bits)."""
 
     def __init__(self, index: int, template: EnergyTemplate, order: ContractionOrder,
-                 report: CostReport, plan: ContractionPlan):
+                 report: CostReport, plan: ContractionPlan, weight: float = 1.0,
+                 assignment: dict | None = None):
         self.index = index
         self.template = template
         self.order = order
         self.report = report
         self.plan = plan
+        self.weight = weight
+        self.assignment = assignment or {}
+
+    @property
+    def cost(self) -> float:
+        return self.report.flops_sum
 
 
 def plan_edges(graph: ProblemGraph, p: int, mode: str, edge_ids, rank_cap=DEFAULT_RANK_CAP,
                dtype="complex64", mixed_rank=DEFAULT_MIXED_RANK, smem_budget=DEFAULT_SMEM_BUDGET,
-               n_repeats=10, temp=0.02, seed=0, compile_plans=True):
-    """Host planning for a set of edges: template, rgreedy order, plan."""
+               n_repeats=10, temp=0.02, seed=0, compile_plans=True, slice_k: int = 0):
+    """Host planning for a set of edges: template, reference rgreedy order,
+    compiled plan.  slice_k > 0 splits every edge network into 2^slice_k
+    slices (slicing.py) that share one plan and differ only in their data."""
     jobs = []
     for e in edge_ids:
         tpl = energy_template(graph, graph.edges[e], p, mode)
         order, report = rgreedy_order(tpl.line_graph(), n_repeats=n_repeats, temp=temp, seed=seed)
+        assigns = [{}]
+        if slice_k > 0:
+            svars, _, order, report = choose_slice_vars(tpl.line_graph(), order, slice_k)
+            assigns = slice_assignments(svars)
+        tpls = [tpl.resliced(a) if a else tpl for a in assigns]
         plan = None
         if compile_plans:
-            plan = ContractionPlan(tpl.structure, tpl.variable_count, tpl.fixed, order.sequence,
+            t0 = tpls[0]
+            plan = ContractionPlan(t0.structure, t0.variable_count, t0.fixed, order.sequence,
                                    rank_cap=rank_cap, dtype=dtype, mixed_rank=mixed_rank,
                                    smem_budget=smem_budget)
-        jobs.append(EdgeJob(e, tpl, order, report, plan))
+        for a, t in zip(assigns, tpls):
+            jobs.append(EdgeJob(e, t, order, report, plan, 1.0 / len(assigns), a))
     return jobs
 
 
@@ -88,21 +106,23 @@ class EnergyPlan:
     def __init__(self, graph: ProblemGraph, p: int, mode: str = "zz+diagonal",
                  dtype="complex64", edge_ids=None, rank_cap=DEFAULT_RANK_CAP,
                  mixed_rank=DEFAULT_MIXED_RANK, smem_budget=DEFAULT_SMEM_BUDGET,
-                 n_repeats=10, temp=0.02, seed=0, jobs=None):
+                 n_repeats=10, temp=0.02, seed=0, jobs=None, slice_k: int = 0):
         self.graph = graph
         self.p = p
         self.mode = mode
-        self.edge_ids = list(range(graph.edge_count)) if edge_ids is None else list(edge_ids)
         t0 = time.perf_counter()
         if jobs is None:
-            jobs = plan_edges(graph, p, mode, self.edge_ids, rank_cap, dtype, mixed_rank,
-                              smem_budget, n_repeats, temp, seed)
-        self.jobs = jobs
+            ids = list(range(graph.edge_count)) if edge_ids is None else list(edge_ids)
+            jobs = plan_edges(graph, p, mode, ids, rank_cap, dtype, mixed_rank,
+                              smem_budget, n_repeats, temp, seed, slice_k=slice_k)
+        self.jobs = list(jobs)
+        self.edge_ids = sorted({j.index for j in self.jobs})
         self.plan_seconds = time.perf_counter() - t0
         self.smem_jobs = [j for j in jobs if j.plan.executor == N.EXEC_SMEM]
         self.hbm_jobs = [j for j in jobs if j.plan.executor == N.EXEC_HBM]
         self._device = None
         self._bufs = {}
+        self.fused = True  # generate gate tensors inside the executors
 
     # ---------------------------------------------------------- statistics
     @property
@@ -132,21 +152,31 @@ class EnergyPlan:
         # one device program for every edge network; input set layout from it
         self._batch = PlanBatch([j.plan for j in self.jobs])
         self.set_elems = self._batch.set_elems
-        recs = []
-        for j, off in zip(self.jobs, self._batch.input_offsets):
-            r = j.template.recipes.copy()
-            r["out_offset"] = j.plan.input_offsets + off
-            recs.append(r)
-        allrec = np.concatenate(recs) if recs else np.zeros(0, dtype=N.RECIPE_DTYPE)
+        recs = [j.template.recipes.copy() for j in self.jobs]
+        for r, j in zip(recs, self.jobs):
+            r["out_offset"] = j.plan.input_offsets
+        # fused path: SMEM networks build their tensors inside the executor
+        self._batch.set_recipes(recs)
+        # unfused path (tensorgen into an input buffer, then the executors)
+        allrec = np.concatenate([r.copy() for r in recs]) if recs else np.zeros(
+            0, dtype=N.RECIPE_DTYPE)
+        pos = 0
+        for r, off in zip(recs, self._batch.input_offsets):
+            allrec["out_offset"][pos: pos + len(r)] += off
+            pos += len(r)
         self._n_recipes = len(allrec)
         self._recipes = torch.from_numpy(allrec.view(np.uint8).copy()).to(dev)
+        w = np.asarray([j.weight for j in self.jobs], dtype=np.float64)
+        self._weights = torch.from_numpy(w).to(dev)
 
     def _buffers(self, n_sets):
         if n_sets not in self._bufs:
             t = self._torch
             dev = self._device
+            need_inputs = (not self.fused) or self._batch.has_hbm
             self._bufs[n_sets] = dict(
-                inputs=t.zeros(n_sets * self.set_elems, dtype=t.complex128, device=dev),
+                inputs=t.zeros(n_sets * self.set_elems if need_inputs else 2, dtype=t.complex128,
+                               device=dev),
                 ws=t.empty(max(self._batch.workspace_bytes(n_sets), 16), dtype=t.uint8,
                            device=dev),
                 res=t.zeros((n_sets, len(self.jobs)), dtype=t.complex128, device=dev),
@@ -156,9 +186,9 @@ class EnergyPlan:
 
     @property
     def launches_per_eval(self) -> int:
-        """Kernel launches of one evaluation: tensorgen + executors + energy."""
+        """Kernel launches of one evaluation (executors + energy reduction)."""
         self._prepare()
-        return 2 + self._batch.launches
+        return self._batch.launches + 1 + (0 if self.fused else 1)
 
     def launch(self, angles_dev, stream=None):
         """Enqueue one evaluation for every angle set in `angles_dev`
@@ -170,14 +200,20 @@ class EnergyPlan:
         b = self._buffers(n_sets)
         st = stream if stream is not None else t.cuda.current_stream(self._device)
         sp = st.cuda_stream
-        N.check(N.lib.qtn_tensorgen(self._recipes.data_ptr(), self._n_recipes,
-                                    angles_dev.data_ptr(), 2 * self.p, n_sets, self.set_elems,
-                                    b["inputs"].data_ptr(), sp), "tensorgen")
-        self._batch.execute(b["inputs"].data_ptr(), n_sets, b["ws"].data_ptr(),
-                            b["res"].data_ptr(), sp, set_stride=self.set_elems)
-        N.check(N.lib.qtn_energy_reduce(b["res"].data_ptr(), len(self.jobs), n_sets,
-                                        b["energy"].data_ptr(), None, sp), "energy")
-        self.launches = 2 + self._batch.launches
+        if self.fused:
+            self._batch.execute_angles(angles_dev.data_ptr(), 2 * self.p, n_sets,
+                                       b["inputs"].data_ptr(), b["ws"].data_ptr(),
+                                       b["res"].data_ptr(), sp)
+        else:
+            N.check(N.lib.qtn_tensorgen(self._recipes.data_ptr(), self._n_recipes,
+                                        angles_dev.data_ptr(), 2 * self.p, n_sets, self.set_elems,
+                                        b["inputs"].data_ptr(), sp), "tensorgen")
+            self._batch.execute(b["inputs"].data_ptr(), n_sets, b["ws"].data_ptr(),
+                                b["res"].data_ptr(), sp, set_stride=self.set_elems)
+        N.check(N.lib.qtn_energy_reduce(b["res"].data_ptr(), self._weights.data_ptr(),
+                                        len(self.jobs), n_sets, b["energy"].data_ptr(), None, sp),
+                "energy")
+        self.launches = self.launches_per_eval
         return b
 
     def energies(self, angle_sets) -> np.ndarray:
@@ -201,16 +237,21 @@ class EnergyPlan:
         a = t.from_numpy(np.atleast_2d(params.as_vector())).to(self._device)
         b = self.launch(a)
         r = b["res"][0].cpu().numpy()
-        return {j.index: complex(r[k]) for k, j in enumerate(self.jobs)}
+        out = {}
+        for k, j in enumerate(self.jobs):  # slices of one edge add up
+            out[j.index] = out.get(j.index, 0j) + complex(r[k])
+        return out
 
 
 def rank_shard(graph: ProblemGraph, p: int, mode: str, rank: int, world: int,
-               n_repeats=10, temp=0.02, seed=0):
-    """This rank's edges: LPT over the reference cost model.  Every rank
-    computes the same (deterministic) orders, so no exchange is needed."""
-    allj = plan_edges(graph, p, mode, range(graph.edge_count), compile_plans=False,
-                      n_repeats=n_repeats, temp=temp, seed=seed)
-    return shard_edges([j.report.flops_sum for j in allj], world)[rank]
+               n_repeats=10, temp=0.02, seed=0, slice_k: int = 0, **plan_kw):
+    """This rank's jobs (edges, or edge slices): LPT over the reference cost
+    model.  Every rank computes the same deterministic orders, so the
+    partition needs no exchange."""
+    allj = plan_edges(graph, p, mode, range(graph.edge_count), n_repeats=n_repeats, temp=temp,
+                      seed=seed, slice_k=slice_k, **plan_kw)
+    keep = shard_edges([j.cost for j in allj], world)[rank]
+    return [allj[k] for k in keep]
 
 
 def reduce_partials(partial: np.ndarray, group=None, device=None) -> np.ndarray:
@@ -238,12 +279,11 @@ def energy_expectation(graph: ProblemGraph, params: QaoaParams, mode: str = "zz+
     dist = torch.distributed
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     if plan is None:
-        edge_ids = None
+        jobs = None
         if world > 1:
-            edge_ids = rank_shard(graph, params.p, mode, dist.get_rank(group), world,
-                                  **{k: v for k, v in kw.items()
-                                     if k in ("n_repeats", "temp", "seed")})
-        plan = EnergyPlan(graph, params.p, mode, dtype, edge_ids=edge_ids, **kw)
+            jobs = rank_shard(graph, params.p, mode, dist.get_rank(group), world, dtype=dtype,
+                              **kw)
+        plan = EnergyPlan(graph, params.p, mode, dtype, jobs=jobs, **kw)
     e = plan.energies(params)
     dev = torch.device("cuda", torch.cuda.current_device()) if world > 1 else None
     return float(reduce_partials(e, group, dev)[0])

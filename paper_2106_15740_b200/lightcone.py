@@ -153,7 +153,12 @@ _KIND_DIAG = {GateKind.ZPOW: N.GATE_ZPOW_DIAG, GateKind.ZZ: N.GATE_ZZ_DIAG}
 
 @dataclass
 class EnergyTemplate:
-    """Angle-independent description of one edge's energy network."""
+    """Angle-independent description of one edge's energy network.
+
+    `tensors` keeps the unsliced description (full variables, gate kind,
+    angle slot, scale, offset); `structure` / `recipes` are its slicing by
+    `fixed` (network.py:153-165).  `resliced` adds more fixed variables —
+    the 2^k slices of §8(e) — without re-walking the circuit."""
 
     edge: tuple
     m: int
@@ -162,9 +167,43 @@ class EnergyTemplate:
     structure: list            # sliced variable tuples, network order
     recipes: np.ndarray        # RECIPE_DTYPE, out_offset relative to the network
     unfixed: tuple
+    tensors: list = None       # (full vars, kind, angle, scale, offset)
 
     def line_graph(self) -> LineGraph:
         return LineGraph.from_hyperedges(self.unfixed, [s for s in self.structure if len(s) >= 1])
+
+    def resliced(self, assignment: dict) -> "EnergyTemplate":
+        """The same network with extra variables fixed to 0/1."""
+        fixed = dict(self.fixed)
+        for v, bit in assignment.items():
+            if v in fixed:
+                raise ValueError(f"variable {v} is already fixed")
+            if bit not in (0, 1):
+                raise ValueError("slice bits must be 0 or 1")
+            fixed[int(v)] = int(bit)
+        return _slice(self.edge, self.m, self.variable_count, fixed, self.tensors)
+
+
+def _slice(edge, m, nvar, fixed, tens) -> EnergyTemplate:
+    rec = np.zeros(len(tens), dtype=N.RECIPE_DTYPE)
+    structure = []
+    off = 0
+    for k, (vs, kind, ang, sc, of) in enumerate(tens):
+        keep = 0
+        fbits = 0
+        kept = []
+        for pos, v in enumerate(vs):
+            if v in fixed:
+                fbits |= fixed[v] << pos
+            else:
+                keep |= 1 << pos
+                kept.append(v)
+        structure.append(tuple(kept))
+        rec[k] = (off, sc, of, ang, kind, len(vs), keep, fbits)
+        off += 1 << len(kept)
+    unfixed = tuple(v for v in range(nvar) if v not in fixed)
+    return EnergyTemplate((int(edge[0]), int(edge[1])), m, nvar, fixed, structure, rec, unfixed,
+                          tens)
 
 
 def energy_template(graph: ProblemGraph, edge, p: int, mode) -> EnergyTemplate:
@@ -194,21 +233,4 @@ def energy_template(graph: ProblemGraph, edge, p: int, mode) -> EnergyTemplate:
             nvar += 2
     fixed = {wire[q]: 0 for q in range(m)}
     tens.append(((), N.GATE_SCALAR, -1, 1.0, 0.0))  # phase exactly 1
-    rec = np.zeros(len(tens), dtype=N.RECIPE_DTYPE)
-    structure = []
-    off = 0
-    for k, (vs, kind, ang, sc, of) in enumerate(tens):
-        keep = 0
-        fbits = 0
-        kept = []
-        for pos, v in enumerate(vs):
-            if v in fixed:
-                fbits |= fixed[v] << pos
-            else:
-                keep |= 1 << pos
-                kept.append(v)
-        structure.append(tuple(kept))
-        rec[k] = (off, sc, of, ang, kind, len(vs), keep, fbits)
-        off += 1 << len(kept)
-    unfixed = tuple(v for v in range(nvar) if v not in fixed)
-    return EnergyTemplate((int(edge[0]), int(edge[1])), m, nvar, fixed, structure, rec, unfixed)
+    return _slice(edge, m, nvar, fixed, tens)

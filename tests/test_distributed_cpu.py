@@ -35,7 +35,8 @@ def _worker(rank, world, port, golden_path, out_q):
     G = json.load(open(golden_path))
     graph = Q.random_regular_graph(G["n"], 3, 0)
     edges = [tuple(e) for e in graph.edges]
-    shard = Q.energy.rank_shard(graph, G["p"], "zz+diagonal", rank, world)
+    shard = [j.index for j in Q.energy.rank_shard(graph, G["p"], "zz+diagonal", rank, world,
+                                                  compile_plans=False)]
     # two angle sets: the config's and a second one
     sets = [(G["gammas"], G["betas"]), ([0.3, 1.1], [0.9, 0.2])]
     partial = np.zeros(len(sets))

@@ -195,3 +195,53 @@ def test_rank_cap_raised_before_execution():
         Q.ContractionPlan(tpl.structure, tpl.variable_count, tpl.fixed, order.sequence,
                           rank_cap=rep.width - 1)
     assert ei.value.cap == rep.width - 1
+
+
+@pytest.mark.parametrize("edge_index,k", [(16, 3), (1058, 3)])
+def test_config4_sliced_c64(golden, edge_index, k):
+    """2^k slices of the config-4 network, one batch, summed on device."""
+    G = golden("config4.json")
+    rec = [r for r in G["modes"]["zz+diagonal"] if r["edge_index"] == edge_index][0]
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    plan = Q.EnergyPlan(graph, G["p"], "zz+diagonal", dtype="complex64", edge_ids=[edge_index],
+                        slice_k=k)
+    assert len(plan.jobs) == 2 ** k
+    assert max(j.report.width for j in plan.jobs) < rec["width"]
+    zz = plan.zz_values(params)[edge_index]
+    w = complex(*rec["value"])
+    assert abs(zz - w) / abs(w) < 1e-5
+    e = plan.energies(params)[0]
+    assert abs(e - (1 - w.real) / 2) < 1e-5
+
+
+def test_config2_sliced_energy_c128(golden):
+    G = golden("config2.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    plan = Q.EnergyPlan(graph, 2, "zz+diagonal", dtype="complex128", slice_k=1)
+    want = sum((1 - r["value"][0]) / 2 for r in G["modes"]["zz+diagonal"])
+    assert abs(plan.energies(params)[0] - want) < 1e-10
+
+
+def test_fused_and_unfused_generation_agree(golden):
+    """In-executor tensor generation (fused) == tensorgen + executor."""
+    G = golden("config2.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    rng = np.random.default_rng(3)
+    sets = rng.uniform(0, math.pi, (7, 4))
+    plan = Q.EnergyPlan(graph, 2, "zz+diagonal", edge_ids=list(range(0, 150, 5)))
+    fused = plan.energies(sets)
+    plan.fused = False
+    plan._bufs.clear()
+    unfused = plan.energies(sets)
+    assert np.allclose(fused, unfused, rtol=0, atol=1e-12)
+    # default mode (FULL networks: H/CNOT/XPOW... all gate kinds), mixed executors
+    G3 = golden("config3.json")
+    g3 = Q.random_regular_graph(244, 3, 0)
+    p3 = Q.EnergyPlan(g3, 3, "default", dtype="complex128", edge_ids=[0, 23])
+    f3 = p3.energies(rng.uniform(0, math.pi, (3, 6)))
+    p3.fused = False
+    p3._bufs.clear()
+    u3 = p3.energies(rng.uniform(0, math.pi, (3, 6)))
+    assert f3.shape == u3.shape

@@ -247,3 +247,54 @@ def test_shard_edges_lpt():
     assert max(loads) - min(loads) <= 1.0
     assert Q.shard_edges(costs, 2) == sh  # deterministic
     assert Q.shard_edges(costs, 8)[7] == []
+
+
+# ------------------------------------------------------------------ slicing
+def test_slices_sum_to_unsliced_value(golden):
+    """2^k slices (extra fixed variables, reduced reference order) add up to
+    the unsliced contraction (oracle contraction of each slice)."""
+    import qtn_oracle as O
+    from paper_2106_15740_b200.slicing import choose_slice_vars, slice_assignments
+
+    G = golden("config2.json")
+    graph = Q.random_regular_graph(100, 3, 0)
+    edges = [tuple(e) for e in G["edges"]]
+    for r in G["modes"]["zz+diagonal"][:3]:
+        tpl = Q.energy_template(graph, graph.edges[r["edge_index"]], 2, "zz+diagonal")
+        order, rep = Q.rgreedy_order(tpl.line_graph())
+        for k in (1, 3):
+            svars, lg2, o2, rep2 = choose_slice_vars(tpl.line_graph(), order, k)
+            assert len(svars) == k and rep2.width <= rep.width
+            tens, nv, fixed = O.edge_network(100, edges, edges[r["edge_index"]], G["gammas"],
+                                             G["betas"], "zz+diagonal")
+            total = 0j
+            for a in slice_assignments(svars):
+                t2 = tpl.resliced(a)
+                assert sorted(o2.sequence) == list(t2.unfixed)
+                val, ranks = O.contract(tens, nv, {**fixed, **a}, list(o2.sequence))
+                assert max(ranks) == rep2.width
+                total += val
+            assert abs(total - complex(*r["value"])) < 1e-12
+
+
+def test_slice_choice_config4_widths():
+    """Edge #1058 (width 26): k=3 -> 23, k=6 -> 20."""
+    from paper_2106_15740_b200.slicing import choose_slice_vars
+
+    graph = Q.random_regular_graph(1000, 3, 0)
+    tpl = Q.energy_template(graph, graph.edges[1058], 5, "zz+diagonal")
+    order, rep = Q.rgreedy_order(tpl.line_graph())
+    assert rep.width == 26
+    assert choose_slice_vars(tpl.line_graph(), order, 3)[3].width == 23
+    _, lg6, o6, rep6 = choose_slice_vars(tpl.line_graph(), order, 6)
+    assert rep6.width == 20
+    assert Q.contraction_width(lg6, o6) == rep6
+
+
+def test_sliced_jobs_share_one_plan():
+    graph = Q.random_regular_graph(100, 3, 0)
+    jobs = Q.plan_edges(graph, 2, "zz+diagonal", [5], slice_k=2)
+    assert len(jobs) == 4 and len({id(j.plan) for j in jobs}) == 1
+    assert sum(j.weight for j in jobs) == 1.0
+    assert all(j.template.structure == jobs[0].template.structure for j in jobs)
+    assert len({tuple(j.template.recipes["fixed_bits"]) for j in jobs}) == 4
