@@ -83,7 +83,8 @@ struct SmemHeader {
   uint32_t gen_off;            // byte offset of the generator section (0: none)
   uint32_t n_params;           // generator: distinct gate parameters
   uint32_t n_recs;             // generator: one record per input tensor
-  uint32_t pad[2];
+  uint32_t tab_off;            // byte offset of the u16 gather tables
+  uint32_t pad;
 };
 // Generator section (appended by qtn_batch_set_recipes): the warp builds its
 // own input tensors in shared memory from the angles of its set — the
@@ -110,16 +111,21 @@ struct SmemBucket {
   uint16_t first_op;
   uint16_t pad;
 };
-constexpr int kSmemOpRuns = 14;
+// Operand of a bucket: element e of the output reads
+//   D[off + tab[lo + (e & 31)] + (R > 5 ? tab[hi + (e >> 5)] : 0) (+ vstep for v=1)]
+// where tab is the program's u16 gather table (the bit gather of the output
+// index, precomputed at plan time; gathers are OR-linear, so the 5 low and
+// the R-5 high output bits are tabulated separately).
+constexpr int kSmemMaxR = 10;
 struct SmemOp {
   uint16_t off;
-  uint8_t vshift;
-  uint8_t n_runs;
-  uint16_t runs[kSmemOpRuns];  // src | dst<<5 | len<<10
+  uint16_t vstep;
+  uint16_t lo;                 // u16 index of the low-bits table (32 entries or 2^R)
+  uint16_t hi;                 // u16 index of the high-bits table (2^(R-5) entries)
 };
 static_assert(sizeof(SmemHeader) == 48, "header");
 static_assert(sizeof(SmemBucket) == 8, "bucket");
-static_assert(sizeof(SmemOp) == 32, "op");
+static_assert(sizeof(SmemOp) == 8, "op");
 
 // ------------------------------------------------------------- host plan
 struct TensorRec {

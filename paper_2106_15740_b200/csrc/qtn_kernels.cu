@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -176,16 +177,6 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 // ------------------------------------------------------- SMEM executor
 
-__device__ __forceinline__ uint32_t sgather(uint32_t e, const SmemOp& o) {
-  uint32_t idx = 0;
-  for (uint32_t r = 0; r < o.n_runs; ++r) {
-    const uint32_t w = o.runs[r];
-    const uint32_t s = w & 31, d = (w >> 5) & 31, l = (w >> 10) & 31;
-    idx |= ((e >> s) & ((1u << l) - 1)) << d;
-  }
-  return idx;
-}
-
 __device__ __forceinline__ void copy16(void* dst, const void* src, uint32_t bytes, uint32_t t,
                                        uint32_t nt) {
   const uint4* s = reinterpret_cast<const uint4*>(src);
@@ -240,33 +231,41 @@ struct SmemArgs {
   int32_t n_sets;
   int32_t n_total;
   uint32_t prog_max;           // bytes reserved for the program (CTA-shared)
-  uint32_t warp_bytes;         // bytes of one warp's data region
+  uint32_t set_bytes;          // bytes of one angle set's data region
+  int32_t sets_per_warp;
 };
 
-constexpr int kNetWarps = 4;   // angle sets per CTA (one warp each)
+constexpr int kNetWarps = 4;   // warps per CTA (upper bound)
 
-// One CTA = one network x kNetWarps angle sets.  The bucket program is
-// staged once per CTA; each warp owns a data region (inputs + intermediates)
-// and either generates its inputs from its angle vector or copies them.
+// One CTA = one network; each warp evaluates `sets_per_warp` angle sets at
+// once: a bucket of 2^R outputs is S*2^R (set, element) items spread over
+// the 32 lanes, so the many tiny buckets of these networks (R <= 4 for 97%
+// of config-2 buckets) still fill the warp.  The bucket program, gather
+// tables and generator records are staged once per CTA; every operand index
+// is one table lookup (two for R > 5).
 __global__ void __launch_bounds__(32 * kNetWarps) smem_net_kernel(const __grid_constant__ SmemArgs A) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int net = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int set = blockIdx.y * (int)(blockDim.x >> 5) + warp;
+  const int S = A.sets_per_warp;
+  const int set0 = (blockIdx.y * (int)(blockDim.x >> 5) + warp) * S;
   const uint8_t* gp = A.progs + A.prog_off[net];
   const SmemHeader h = *reinterpret_cast<const SmemHeader*>(gp);
   copy16(sm, gp, h.prog_bytes, threadIdx.x, blockDim.x);
   __syncthreads();
-  if (set >= A.n_sets) return;
-  double2* D = reinterpret_cast<double2*>(sm + A.prog_max + warp * A.warp_bytes);
+  if (set0 >= A.n_sets) return;
+  const int ns = min(S, A.n_sets - set0);
+  const uint32_t stride = A.set_bytes / 16;  // complex128 elements per set region
+  double2* D0 = reinterpret_cast<double2*>(sm + A.prog_max + (size_t)warp * S * A.set_bytes);
   if (A.angles && h.n_recs) {
-    double2* ph = D + h.data_elems;
     const SmemGenParam* par = reinterpret_cast<const SmemGenParam*>(sm + h.gen_off);
-    const double* ang = A.angles + (int64_t)set * A.n_angles;
-    for (uint32_t k = lane; k < h.n_params; k += 32) {
+    for (uint32_t it = lane; it < (uint32_t)ns * h.n_params; it += 32) {
+      const uint32_t s = it / h.n_params, k = it - s * h.n_params;
       const SmemGenParam q = par[k];
+      double2* ph = D0 + s * stride + h.data_elems;
       if (q.angle == -2) {
         ph[k] = make_double2(q.scale, q.offset);
       } else {
+        const double* ang = A.angles + (int64_t)(set0 + s) * A.n_angles;
         const double t = q.angle >= 0 ? q.scale * ang[q.angle] + q.offset : q.offset;
         double sn, cs;
         sincos(t, &sn, &cs);
@@ -276,9 +275,11 @@ __global__ void __launch_bounds__(32 * kNetWarps) smem_net_kernel(const __grid_c
     __syncwarp();
     const SmemGenRec* rec = reinterpret_cast<const SmemGenRec*>(sm + h.gen_off +
                                                                 sizeof(SmemGenParam) * h.n_params);
-    for (uint32_t r = lane; r < h.n_recs; r += 32) {
+    for (uint32_t it = lane; it < (uint32_t)ns * h.n_recs; it += 32) {
+      const uint32_t s = it / h.n_recs, r = it - s * h.n_recs;
+      double2* D = D0 + s * stride;
       const SmemGenRec g = rec[r];
-      const double2 p = ph[g.param];
+      const double2 p = D[h.data_elems + g.param];
       const uint32_t fr = g.full_rank, kept = __popc(g.keep_mask);
       for (uint32_t e = 0; e < (1u << kept); ++e) {
         uint32_t full = 0;
@@ -291,36 +292,45 @@ __global__ void __launch_bounds__(32 * kNetWarps) smem_net_kernel(const __grid_c
       }
     }
   } else {
-    copy16(D, A.inputs + (int64_t)set * A.set_elems + A.in_off[net], h.in_elems * 16u, lane, 32);
+    for (int s = 0; s < ns; ++s)
+      copy16(D0 + s * stride, A.inputs + (int64_t)(set0 + s) * A.set_elems + A.in_off[net],
+             h.in_elems * 16u, lane, 32);
   }
   __syncwarp();
   const SmemBucket* bk = reinterpret_cast<const SmemBucket*>(sm + sizeof(SmemHeader));
   const SmemOp* ops = reinterpret_cast<const SmemOp*>(sm + sizeof(SmemHeader) +
                                                       sizeof(SmemBucket) * h.n_buckets);
+  const uint16_t* tab = reinterpret_cast<const uint16_t*>(sm + h.tab_off);
   for (uint32_t bi = 0; bi < h.n_buckets; ++bi) {
     const SmemBucket b = bk[bi];
     const SmemOp* bo = ops + b.first_op;
-    const uint32_t n = 1u << b.R;
-    for (uint32_t e = lane; e < n; e += 32) {
-      const SmemOp& o0 = bo[0];
-      uint32_t idx = o0.off + sgather(e, o0);
-      double2 a0 = D[idx], a1 = D[idx + (1u << o0.vshift)];
+    const uint32_t R = b.R;
+    const uint32_t n = (uint32_t)ns << R;
+    const uint32_t emask = (1u << R) - 1u;
+    for (uint32_t it = lane; it < n; it += 32) {
+      const uint32_t s = it >> R, e = it & emask;
+      const double2* D = D0 + s * stride;
+      const uint32_t hi_e = e >> 5, lo_e = e & 31;
+      SmemOp o = bo[0];
+      uint32_t idx = o.off + tab[o.lo + lo_e] + (R > 5 ? tab[o.hi + hi_e] : 0u);
+      double2 a0 = D[idx], a1 = D[idx + o.vstep];
       for (uint32_t k = 1; k < b.n_ops; ++k) {
-        const SmemOp& o = bo[k];
-        idx = o.off + sgather(e, o);
+        o = bo[k];
+        idx = o.off + tab[o.lo + lo_e] + (R > 5 ? tab[o.hi + hi_e] : 0u);
         a0 = cmul(a0, D[idx]);
-        a1 = cmul(a1, D[idx + (1u << o.vshift)]);
+        a1 = cmul(a1, D[idx + o.vstep]);
       }
-      D[b.out_off + e] = cadd(a0, a1);
+      D0[s * stride + b.out_off + e] = cadd(a0, a1);
     }
     __syncwarp();
   }
-  if (lane == 0) {
+  if (lane < ns) {
+    const double2* D = D0 + lane * stride;
     const uint16_t* sc = reinterpret_cast<const uint16_t*>(
         sm + sizeof(SmemHeader) + sizeof(SmemBucket) * h.n_buckets + sizeof(SmemOp) * h.n_ops);
     double2 r = make_double2(ldexp(1.0, (int)h.pow2), 0.0);
     for (uint32_t i = 0; i < h.n_scalars; ++i) r = cmul(r, D[sc[i]]);
-    A.results[(int64_t)set * A.n_total + A.out_index[net]] = r;
+    A.results[(int64_t)(set0 + lane) * A.n_total + A.out_index[net]] = r;
   }
 }
 
@@ -883,10 +893,19 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
   if (B->n_smem) {
     const uint32_t prog_max = (B->prog_max + 15) & ~15u;
     const uint32_t warp_bytes = (B->warp_bytes + 15) & ~15u;
-    // angle sets per CTA: as many warps as fit next to one copy of the program
-    int W = (int)std::min<size_t>(kNetWarps, (227u * 1024u - prog_max) / std::max(warp_bytes, 16u));
-    W = std::max(1, std::min(W, (int)n_sets));
-    const size_t smem = (size_t)prog_max + (size_t)W * warp_bytes;
+    // S angle sets per warp, W warps per CTA (as many as fit next to one
+    // copy of the program)
+    static int env_s = -1;
+    if (env_s < 0) {
+      const char* v = getenv("QTN_SETS_PER_WARP");
+      env_s = v ? std::max(1, atoi(v)) : 2;
+    }
+    const int S = std::max(1, std::min(env_s, (int)n_sets));
+    const size_t per_warp = (size_t)S * warp_bytes;
+    int W = (int)std::min<size_t>(kNetWarps, (227u * 1024u - prog_max) / std::max<size_t>(per_warp, 16));
+    const int warps_needed = (n_sets + S - 1) / S;
+    W = std::max(1, std::min(W, warps_needed));
+    const size_t smem = (size_t)prog_max + (size_t)W * per_warp;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
       cudaError_t e = cudaFuncSetAttribute(smem_net_kernel,
@@ -907,8 +926,9 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     a.n_sets = n_sets;
     a.n_total = B->n;
     a.prog_max = prog_max;
-    a.warp_bytes = warp_bytes;
-    dim3 grid(B->n_smem, (n_sets + W - 1) / W);
+    a.set_bytes = warp_bytes;
+    a.sets_per_warp = S;
+    dim3 grid(B->n_smem, (warps_needed + W - 1) / W);
     smem_net_kernel<<<grid, 32 * W, smem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel launch");

@@ -500,18 +500,76 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       data_elems = std::max<int64_t>(data_elems, t.sm_off + ((int64_t)1 << t.rank()));
     }
     size_t n_ops = 0;
-    for (auto& b : P->buckets) n_ops += b.ops.size();
+    int maxR = 0;
+    for (auto& b : P->buckets) {
+      n_ops += b.ops.size();
+      maxR = std::max(maxR, (int)b.rank);
+    }
+    if (data_elems > 65535 || n_ops > 65535 || maxR > kSmemMaxR) smem_ok = false;
+    // gather tables (deduplicated) and op records
+    std::vector<uint16_t> tab;
+    std::map<std::vector<uint16_t>, uint16_t> seen;
+    auto intern = [&](const std::vector<uint16_t>& t) -> int64_t {
+      auto it = seen.find(t);
+      if (it != seen.end()) return it->second;
+      const int64_t at = (int64_t)tab.size();
+      if (at + (int64_t)t.size() > 65535) return -1;
+      tab.insert(tab.end(), t.begin(), t.end());
+      seen.emplace(t, (uint16_t)at);
+      return at;
+    };
+    std::vector<SmemBucket> sbk(nb);
+    std::vector<SmemOp> sop;
+    std::vector<std::pair<int, int>> sd;
+    std::vector<uint32_t> runs;
+    for (int bi = 0; bi < nb && smem_ok; ++bi) {
+      const auto& b = P->buckets[bi];
+      const auto& out = P->tensors[b.out];
+      sbk[bi].out_off = (uint16_t)out.sm_off;
+      sbk[bi].R = (uint8_t)b.rank;
+      sbk[bi].n_ops = (uint8_t)b.ops.size();
+      sbk[bi].first_op = (uint16_t)sop.size();
+      // primary first: its entries seed the accumulator
+      std::vector<int32_t> ord = b.ops;
+      std::swap(ord[0], ord[b.primary]);
+      const int R = b.rank;
+      for (int32_t id : ord) {
+        int vs;
+        operand_map(P->tensors[id].vars, out.vars, b.v, sd, vs);
+        make_runs(sd, runs);
+        auto g = [&](uint32_t e) {
+          uint32_t idx = 0;
+          for (uint32_t w : runs) {
+            const uint32_t s0 = w & 0xff, d0 = (w >> 8) & 0xff, l0 = (w >> 16) & 0xff;
+            idx |= ((e >> s0) & ((1u << l0) - 1)) << d0;
+          }
+          return (uint16_t)idx;
+        };
+        std::vector<uint16_t> lo, hi;
+        for (uint32_t e = 0; e < (1u << std::min(R, 5)); ++e) lo.push_back(g(e));
+        for (uint32_t j = 0; R > 5 && j < (1u << (R - 5)); ++j) hi.push_back(g(j << 5));
+        const int64_t l = intern(lo), h = R > 5 ? intern(hi) : 0;
+        if (l < 0 || h < 0 || (1 << vs) > 65535) {
+          smem_ok = false;
+          break;
+        }
+        SmemOp o;
+        o.off = (uint16_t)P->tensors[id].sm_off;
+        o.vstep = (uint16_t)(1u << vs);
+        o.lo = (uint16_t)l;
+        o.hi = (uint16_t)h;
+        sop.push_back(o);
+      }
+    }
     int64_t prog = sizeof(SmemHeader) + sizeof(SmemBucket) * nb + sizeof(SmemOp) * n_ops +
                    2 * (int64_t)P->scalars.size();
     prog = (prog + 15) / 16 * 16;
+    const int64_t tab_off = prog;
+    prog += ((int64_t)tab.size() * 2 + 15) / 16 * 16;
     const int64_t smem = prog + 16 * data_elems;
-    if (data_elems > 65535 || n_ops > 65535 || smem > smem_budget) smem_ok = false;
-    // every operand must fit the packed run encoding
-    std::vector<std::pair<int, int>> sd;
-    std::vector<uint32_t> runs;
-    std::vector<uint8_t> blob;
+    if (smem > smem_budget) smem_ok = false;
     if (smem_ok) {
-      blob.assign(prog, 0);
+      std::vector<uint8_t> blob(prog, 0);
       SmemHeader* h = reinterpret_cast<SmemHeader*>(blob.data());
       h->n_buckets = nb;
       h->n_ops = (uint32_t)n_ops;
@@ -520,47 +578,17 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       h->in_elems = (uint32_t)P->input_elems;
       h->data_elems = (uint32_t)data_elems;
       h->prog_bytes = (uint32_t)prog;
-      SmemBucket* sb = reinterpret_cast<SmemBucket*>(blob.data() + sizeof(SmemHeader));
-      SmemOp* so = reinterpret_cast<SmemOp*>(blob.data() + sizeof(SmemHeader) +
-                                            sizeof(SmemBucket) * nb);
-      uint32_t op_i = 0;
-      for (int bi = 0; bi < nb && smem_ok; ++bi) {
-        const auto& b = P->buckets[bi];
-        const auto& out = P->tensors[b.out];
-        sb[bi].out_off = (uint16_t)out.sm_off;
-        sb[bi].R = (uint8_t)b.rank;
-        sb[bi].n_ops = (uint8_t)b.ops.size();
-        sb[bi].first_op = (uint16_t)op_i;
-        // primary first: its product seeds the accumulator
-        std::vector<int32_t> ord = b.ops;
-        std::swap(ord[0], ord[b.primary]);
-        for (int32_t id : ord) {
-          int vs;
-          operand_map(P->tensors[id].vars, out.vars, b.v, sd, vs);
-          make_runs(sd, runs);
-          if ((int)runs.size() > kSmemOpRuns || b.rank > 31) {
-            smem_ok = false;
-            break;
-          }
-          SmemOp& o = so[op_i++];
-          o.off = (uint16_t)P->tensors[id].sm_off;
-          o.vshift = (uint8_t)vs;
-          o.n_runs = (uint8_t)runs.size();
-          for (size_t r = 0; r < runs.size(); ++r) {
-            uint32_t s = runs[r] & 0xff, d = (runs[r] >> 8) & 0xff, l = (runs[r] >> 16) & 0xff;
-            o.runs[r] = (uint16_t)(s | (d << 5) | (l << 10));
-          }
-        }
-      }
+      h->tab_off = (uint32_t)tab_off;
+      std::memcpy(blob.data() + sizeof(SmemHeader), sbk.data(), sizeof(SmemBucket) * nb);
+      std::memcpy(blob.data() + sizeof(SmemHeader) + sizeof(SmemBucket) * nb, sop.data(),
+                  sizeof(SmemOp) * n_ops);
       uint16_t* sc = reinterpret_cast<uint16_t*>(blob.data() + sizeof(SmemHeader) +
-                                                 sizeof(SmemBucket) * nb +
-                                                 sizeof(SmemOp) * n_ops);
+                                                 sizeof(SmemBucket) * nb + sizeof(SmemOp) * n_ops);
       for (size_t i = 0; i < P->scalars.size(); ++i)
         sc[i] = (uint16_t)P->tensors[P->scalars[i]].sm_off;
-      if (smem_ok) {
-        P->program = std::move(blob);
-        P->smem_bytes = smem;
-      }
+      std::memcpy(blob.data() + tab_off, tab.data(), tab.size() * 2);
+      P->program = std::move(blob);
+      P->smem_bytes = smem;
     }
   }
   if (smem_ok) {
