@@ -82,9 +82,11 @@ struct SmemHeader {
   uint32_t prog_bytes;         // whole blob, multiple of 16
   uint32_t gen_off;            // byte offset of the generator section (0: none)
   uint32_t n_params;           // generator: distinct gate parameters
-  uint32_t n_recs;             // generator: one record per input tensor
+  uint32_t n_recs;             // generator: one record per input tensor ENTRY
   uint32_t tab_off;            // byte offset of the u16 gather tables
-  uint32_t pad;
+  uint32_t in_off;             // byte offset of the SmemIn records
+  uint32_t n_init;             // leading SmemIn records materialised before bucket 0
+  uint32_t pad[3];
 };
 // Generator section (appended by qtn_batch_set_recipes): the warp builds its
 // own input tensors in shared memory from the angles of its set — the
@@ -96,11 +98,12 @@ struct SmemGenParam {          // phase e^{-i t}, t = scale*angles[angle] + offs
   int32_t angle;               // -1: constant t = offset; -2: literal value (scale + i*offset)
   int32_t pad;
 };
-struct SmemGenRec {
-  uint8_t kind, full_rank, keep_mask, fixed_bits;
-  uint8_t param;
-  uint8_t pad;
-  uint16_t out_off;            // element offset in the warp's data region
+struct SmemGenRec {            // one tensor ENTRY (entries of all inputs, flattened)
+  uint16_t sm_off;             // element offset in the warp's data region
+  uint8_t kind;                // QTN_GATE_*
+  uint8_t full;                // index into the unsliced gate tensor
+  uint8_t param;               // parameter slot
+  uint8_t pad[3];
 };
 static_assert(sizeof(SmemGenParam) == 24, "gen param");
 static_assert(sizeof(SmemGenRec) == 8, "gen rec");
@@ -109,8 +112,22 @@ struct SmemBucket {
   uint8_t R;
   uint8_t n_ops;
   uint16_t first_op;
-  uint16_t pad;
+  uint16_t first_in;           // input tensors materialised just before this bucket
+  uint8_t n_in;
+  uint8_t pad[7];
 };
+// An input tensor is generated (or copied) into shared memory right before
+// the bucket that consumes it (every input is consumed exactly once), so it
+// occupies smem only for that bucket: the data region holds the live
+// intermediates plus one bucket's inputs, not the whole network.
+struct SmemIn {
+  uint16_t input;              // input tensor index (generator record / packed input)
+  uint16_t sm_off;             // destination element offset in the data region
+  uint16_t in_off;             // element offset in the packed input (copy path)
+  uint8_t rank;
+  uint8_t pad;
+};
+static_assert(sizeof(SmemIn) == 8, "in");
 // Operand of a bucket: element e of the output reads
 //   D[off + tab[lo + (e & 31)] + (R > 5 ? tab[hi + (e >> 5)] : 0) (+ vstep for v=1)]
 // where tab is the program's u16 gather table (the bit gather of the output
@@ -123,8 +140,8 @@ struct SmemOp {
   uint16_t lo;                 // u16 index of the low-bits table (32 entries or 2^R)
   uint16_t hi;                 // u16 index of the high-bits table (2^(R-5) entries)
 };
-static_assert(sizeof(SmemHeader) == 48, "header");
-static_assert(sizeof(SmemBucket) == 8, "bucket");
+static_assert(sizeof(SmemHeader) == 64, "header");
+static_assert(sizeof(SmemBucket) == 16, "bucket");
 static_assert(sizeof(SmemOp) == 8, "op");
 
 // ------------------------------------------------------------- host plan

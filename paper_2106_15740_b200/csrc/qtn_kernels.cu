@@ -272,31 +272,33 @@ __global__ void __launch_bounds__(32 * kNetWarps) smem_net_kernel(const __grid_c
         ph[k] = make_double2(cs, -sn);
       }
     }
-    __syncwarp();
-    const SmemGenRec* rec = reinterpret_cast<const SmemGenRec*>(sm + h.gen_off +
-                                                                sizeof(SmemGenParam) * h.n_params);
-    for (uint32_t it = lane; it < (uint32_t)ns * h.n_recs; it += 32) {
-      const uint32_t s = it / h.n_recs, r = it - s * h.n_recs;
-      double2* D = D0 + s * stride;
-      const SmemGenRec g = rec[r];
-      const double2 p = D[h.data_elems + g.param];
-      const uint32_t fr = g.full_rank, kept = __popc(g.keep_mask);
-      for (uint32_t e = 0; e < (1u << kept); ++e) {
-        uint32_t full = 0;
-        int kb = (int)kept - 1;
-        for (uint32_t q = 0; q < fr; ++q) {
-          const uint32_t bit = ((g.keep_mask >> q) & 1) ? (e >> kb--) & 1 : (g.fixed_bits >> q) & 1;
-          full = (full << 1) | bit;
-        }
-        D[g.out_off + e] = gen_entry(g.kind, full, p);
-      }
-    }
-  } else {
-    for (int s = 0; s < ns; ++s)
-      copy16(D0 + s * stride, A.inputs + (int64_t)(set0 + s) * A.set_elems + A.in_off[net],
-             h.in_elems * 16u, lane, 32);
   }
   __syncwarp();
+  const bool gen = A.angles && h.n_recs;
+  const SmemGenRec* grec = reinterpret_cast<const SmemGenRec*>(sm + h.gen_off +
+                                                               sizeof(SmemGenParam) * h.n_params);
+  const SmemIn* sin = reinterpret_cast<const SmemIn*>(sm + h.in_off);
+  if (gen) {
+    // every input entry of every set of the warp: one item each
+    for (uint32_t it = lane; it < (uint32_t)ns * h.n_recs; it += 32) {
+      const uint32_t s = it / h.n_recs;
+      const SmemGenRec g = grec[it - s * h.n_recs];
+      double2* D = D0 + s * stride;
+      D[g.sm_off] = gen_entry(g.kind, g.full, D[h.data_elems + g.param]);
+    }
+  }
+  // copy path: input tensors [first, first+cnt) from the packed input buffer
+  auto materialise = [&](uint32_t first, uint32_t cnt) {
+    if (gen) return;
+    for (uint32_t it = lane; it < (uint32_t)ns * cnt; it += 32) {
+      const uint32_t s = it / cnt;
+      const SmemIn r = sin[first + (it - s * cnt)];
+      double2* D = D0 + s * stride;
+      const double2* src = A.inputs + (int64_t)(set0 + s) * A.set_elems + A.in_off[net] + r.in_off;
+      for (uint32_t e = 0; e < (1u << r.rank); ++e) D[r.sm_off + e] = src[e];
+    }
+  };
+  materialise(0, h.n_init);
   const SmemBucket* bk = reinterpret_cast<const SmemBucket*>(sm + sizeof(SmemHeader));
   const SmemOp* ops = reinterpret_cast<const SmemOp*>(sm + sizeof(SmemHeader) +
                                                       sizeof(SmemBucket) * h.n_buckets);
@@ -307,6 +309,10 @@ __global__ void __launch_bounds__(32 * kNetWarps) smem_net_kernel(const __grid_c
     const uint32_t R = b.R;
     const uint32_t n = (uint32_t)ns << R;
     const uint32_t emask = (1u << R) - 1u;
+    if (b.n_in) {
+      materialise(b.first_in, b.n_in);
+      __syncwarp();
+    }
     for (uint32_t it = lane; it < n; it += 32) {
       const uint32_t s = it >> R, e = it & emask;
       const double2* D = D0 + s * stride;
@@ -772,6 +778,17 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
     SmemHeader* h = reinterpret_cast<SmemHeader*>(prog.data());
     std::vector<SmemGenParam> params;
     std::vector<SmemGenRec> recs;
+    // where each input tensor lives in the data region (from the program)
+    std::vector<int32_t> in_sm(offsets[gi + 1] - offsets[gi], -1);
+    {
+      const SmemIn* sin = reinterpret_cast<const SmemIn*>(prog.data() + h->in_off);
+      uint32_t n_in = 0;
+      const SmemBucket* bk = reinterpret_cast<const SmemBucket*>(prog.data() + sizeof(SmemHeader));
+      n_in = h->n_init;
+      for (uint32_t b = 0; b < h->n_buckets; ++b) n_in = std::max<uint32_t>(n_in, bk[b].first_in + bk[b].n_in);
+      for (uint32_t i = 0; i < n_in; ++i)
+        if (sin[i].input < in_sm.size()) in_sm[sin[i].input] = sin[i].sm_off;
+    }
     for (int64_t r = offsets[gi]; r < offsets[gi + 1]; ++r) {
       const qtn_tensor_recipe& q = rec[r];
       SmemGenParam p{};
@@ -793,18 +810,28 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
             params[slot].angle == p.angle)
           break;
       if (slot == params.size()) params.push_back(p);
-      if (slot > 255 || q.out_offset + (1ll << q.full_rank) > 65535) {
-        set_error("qtn_batch_set_recipes: network too large for the fused generator");
+      const int32_t base = in_sm[r - offsets[gi]];
+      if (slot > 255 || base < 0) {
+        set_error("qtn_batch_set_recipes: recipes do not match the plan's inputs");
         return QTN_EINVAL;
       }
-      SmemGenRec g{};
-      g.kind = q.kind;
-      g.full_rank = q.full_rank;
-      g.keep_mask = q.keep_mask;
-      g.fixed_bits = q.fixed_bits;
-      g.param = (uint8_t)slot;
-      g.out_off = (uint16_t)q.out_offset;
-      recs.push_back(g);
+      // one record per kept entry: slicing (network.py:153-165) resolved here
+      const int fr = q.full_rank;
+      const int kept = __builtin_popcount(q.keep_mask);
+      for (uint32_t e = 0; e < (1u << kept); ++e) {
+        uint32_t full = 0;
+        int kb = kept - 1;
+        for (int pos = 0; pos < fr; ++pos) {
+          const uint32_t bit = ((q.keep_mask >> pos) & 1) ? (e >> kb--) & 1 : (q.fixed_bits >> pos) & 1;
+          full = (full << 1) | bit;
+        }
+        SmemGenRec g{};
+        g.sm_off = (uint16_t)(base + e);
+        g.kind = q.kind;
+        g.full = (uint8_t)full;
+        g.param = (uint8_t)slot;
+        recs.push_back(g);
+      }
     }
     const size_t gen_off = prog.size();
     size_t gen_bytes = params.size() * sizeof(SmemGenParam) + recs.size() * sizeof(SmemGenRec);
@@ -898,9 +925,13 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     static int env_s = -1;
     if (env_s < 0) {
       const char* v = getenv("QTN_SETS_PER_WARP");
-      env_s = v ? std::max(1, atoi(v)) : 2;
+      env_s = v ? std::max(1, atoi(v)) : 0;
     }
-    const int S = std::max(1, std::min(env_s, (int)n_sets));
+    // measured: 2 sets per warp when a set's region is small (config 2,
+    // ~5 KB), 1 when it is large (config 3, ~20 KB) — occupancy wins there
+    int S = env_s > 0 ? env_s : (warp_bytes <= 12 * 1024 ? 2 : 1);
+    S = std::max(1, std::min(S, (int)n_sets));
+    while (S > 1 && (size_t)prog_max + (size_t)S * warp_bytes > 227u * 1024u) --S;
     const size_t per_warp = (size_t)S * warp_bytes;
     int W = (int)std::min<size_t>(kNetWarps, (227u * 1024u - prog_max) / std::max<size_t>(per_warp, 16));
     const int warps_needed = (n_sets + S - 1) / S;

@@ -487,17 +487,25 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
   bool smem_ok = smem_budget > 0 && nb < 65535;
   int64_t data_elems = 0;
   std::vector<Block> sblocks;
+  // Inputs are materialised in one lane-parallel pass before bucket 0 (the
+  // measured-faster choice for these networks: generating each bucket's
+  // inputs just before it halves the smem footprint but serialises the warp
+  // on tiny steps).  Their smem is reusable by intermediates once consumed.
+  // The program format also supports per-bucket materialisation
+  // (SmemBucket.first_in / n_in).
+  std::vector<std::vector<int32_t>> bucket_inputs(nb);
+  std::vector<int32_t> init_inputs;
   if (smem_ok) {
     for (int k = 0; k < P->n_inputs; ++k) {
       auto& t = P->tensors[k];
-      sblocks.push_back({t.in_off, 1ll << t.rank(), -1, t.last_use});
-      t.sm_off = t.in_off;
-    }
-    data_elems = P->input_elems;
-    for (size_t id = P->n_inputs; id < P->tensors.size(); ++id) {
-      auto& t = P->tensors[id];
-      t.sm_off = place(sblocks, 1ll << t.rank(), t.born, t.last_use, 1);
+      init_inputs.push_back(k);
+      t.sm_off = place(sblocks, 1ll << t.rank(), -1, t.rank() == 0 ? nb : t.last_use, 1);
       data_elems = std::max<int64_t>(data_elems, t.sm_off + ((int64_t)1 << t.rank()));
+    }
+    for (int bi = 0; bi < nb; ++bi) {
+      auto& o = P->tensors[P->buckets[bi].out];
+      o.sm_off = place(sblocks, 1ll << o.rank(), bi, o.last_use, 1);
+      data_elems = std::max<int64_t>(data_elems, o.sm_off + ((int64_t)1 << o.rank()));
     }
     size_t n_ops = 0;
     int maxR = 0;
@@ -522,6 +530,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     std::vector<SmemOp> sop;
     std::vector<std::pair<int, int>> sd;
     std::vector<uint32_t> runs;
+    size_t n_in_before = 0;
     for (int bi = 0; bi < nb && smem_ok; ++bi) {
       const auto& b = P->buckets[bi];
       const auto& out = P->tensors[b.out];
@@ -529,6 +538,10 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       sbk[bi].R = (uint8_t)b.rank;
       sbk[bi].n_ops = (uint8_t)b.ops.size();
       sbk[bi].first_op = (uint16_t)sop.size();
+      sbk[bi].first_in = (uint16_t)(init_inputs.size() + n_in_before);
+      sbk[bi].n_in = (uint8_t)bucket_inputs[bi].size();
+      n_in_before += bucket_inputs[bi].size();
+      if (bucket_inputs[bi].size() > 255) smem_ok = false;
       // primary first: its entries seed the accumulator
       std::vector<int32_t> ord = b.ops;
       std::swap(ord[0], ord[b.primary]);
@@ -561,9 +574,26 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         sop.push_back(o);
       }
     }
+    // input materialisation records: rank-0 inputs first, then per bucket
+    std::vector<SmemIn> sin;
+    auto add_in = [&](int32_t k) {
+      const auto& t = P->tensors[k];
+      SmemIn r{};
+      r.input = (uint16_t)k;
+      r.sm_off = (uint16_t)t.sm_off;
+      r.in_off = (uint16_t)t.in_off;
+      r.rank = (uint8_t)t.rank();
+      sin.push_back(r);
+    };
+    for (int32_t k : init_inputs) add_in(k);
+    for (int bi = 0; bi < nb; ++bi)
+      for (int32_t k : bucket_inputs[bi]) add_in(k);
+    if (P->n_inputs > 65535 || P->input_elems > 65535) smem_ok = false;
     int64_t prog = sizeof(SmemHeader) + sizeof(SmemBucket) * nb + sizeof(SmemOp) * n_ops +
                    2 * (int64_t)P->scalars.size();
     prog = (prog + 15) / 16 * 16;
+    const int64_t sin_off = prog;
+    prog += ((int64_t)sin.size() * (int64_t)sizeof(SmemIn) + 15) / 16 * 16;
     const int64_t tab_off = prog;
     prog += ((int64_t)tab.size() * 2 + 15) / 16 * 16;
     const int64_t smem = prog + 16 * data_elems;
@@ -579,6 +609,9 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       h->data_elems = (uint32_t)data_elems;
       h->prog_bytes = (uint32_t)prog;
       h->tab_off = (uint32_t)tab_off;
+      h->in_off = (uint32_t)sin_off;
+      h->n_init = (uint32_t)init_inputs.size();
+      std::memcpy(blob.data() + sin_off, sin.data(), sin.size() * sizeof(SmemIn));
       std::memcpy(blob.data() + sizeof(SmemHeader), sbk.data(), sizeof(SmemBucket) * nb);
       std::memcpy(blob.data() + sizeof(SmemHeader) + sizeof(SmemBucket) * nb, sop.data(),
                   sizeof(SmemOp) * n_ops);
