@@ -1,5 +1,9 @@
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
-tail -4 gpurun_out/pytest_gpu.log
-for S in 1 2 4 8; do QTN_SETS_PER_WARP=$S timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-config5 > gpurun_out/b_S$S.json 2>&1; echo S=$S rc=$?; done
-for S in 1 2 4; do QTN_SETS_PER_WARP=$S timeout 300 python bench.py --workload config3 --angle-sets 256 --steps 5 --warmup 3 --no-cpu-baseline --no-config5 > gpurun_out/b_c3_S$S.json 2>&1; echo c3 rc=$?; done
+tail -2 gpurun_out/pytest_gpu.log
+for V in default s3; do
+  if [ $V = s3 ]; then export QTN_LIB=$PWD/build_alt/libqtn_b200_s3.so; fi
+  timeout 300 python bench.py --workload config5 --steps 5 --c5-ws 28,30,32 --c5-ms 4,16 > gpurun_out/c5_$V.json 2>&1; echo c5 rc=$?
+  timeout 300 python bench.py --steps 5 --warmup 3 --workload config4 --angle-sets 1 --no-config5 --no-cpu-baseline > gpurun_out/b_c4_$V.json 2>&1; echo c4 rc=$?
+  timeout 300 python bench.py --steps 3 --warmup 3 --workload config3-default --angle-sets 1 --no-config5 --no-cpu-baseline > gpurun_out/b_c3d_$V.json 2>&1; echo c3d rc=$?
+done

@@ -13,7 +13,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqtn_b200.so")
+LIB_PATH = os.environ.get("QTN_LIB") or os.path.join(_HERE, "libqtn_b200.so")
 
 QTN_OK, QTN_EINVAL, QTN_ERANKCAP, QTN_ENOMEM, QTN_ECUDA, QTN_ENODEV = range(6)
 DTYPE_C128, DTYPE_C64 = 0, 1

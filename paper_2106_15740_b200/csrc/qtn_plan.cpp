@@ -314,6 +314,35 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
     g[i].n_runs = (uint8_t)(src.n_lo + src.n_hi);
     std::copy(src.lo, src.lo + src.n_lo, g[i].runs);
     std::copy(src.hi, src.hi + src.n_hi, g[i].runs + src.n_lo);
+    // Staging: if the operand depends on only k <= 9 of the tile's output
+    // bits, a tile touches 2^(k+1) of its entries; the consumers gather that
+    // slice into shared memory once per tile instead of every element
+    // re-reading it from L2 (the "two wide operands -> wider output" buckets).
+    g[i].stage_k = 0xff;
+    std::vector<std::pair<int, int>> pairs;  // (output bit, operand bit)
+    for (int r = 0; r < g[i].n_runs; ++r) {
+      const uint32_t w = g[i].runs[r];
+      for (uint32_t q = 0; q < ((w >> 16) & 0xff); ++q)
+        pairs.push_back({(int)(w & 0xff) + (int)q, (int)((w >> 8) & 0xff) + (int)q});
+    }
+    std::sort(pairs.begin(), pairs.end());
+    std::vector<std::pair<int, int>> s_sd, g_sd;
+    for (auto& pr : pairs)
+      if (pr.first < tb) {
+        s_sd.push_back({pr.first, (int)s_sd.size()});
+        g_sd.push_back({(int)g_sd.size(), pr.second});
+      }
+    const int k = (int)s_sd.size();
+    if (i == 0 && k <= kStageMaxK && k <= tb - 2) {
+      std::vector<uint32_t> sr, grr;
+      make_runs(s_sd, sr);
+      make_runs(g_sd, grr);
+      g[i].stage_k = (uint8_t)k;
+      g[i].n_srun = (uint8_t)sr.size();
+      g[i].n_grun = (uint8_t)grr.size();
+      std::copy(sr.begin(), sr.end(), g[i].srun);
+      std::copy(grr.begin(), grr.end(), g[i].grun);
+    }
   }
   STRec* t = reinterpret_cast<STRec*>(blob.data() + base + sizeof(SHdr) + ng * sizeof(SGRec));
   for (uint32_t j = 0; j < a.nt; ++j) {

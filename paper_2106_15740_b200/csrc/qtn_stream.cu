@@ -45,10 +45,12 @@ constexpr int kDescSlot = (kSDescMax + 127) / 128 * 128;
 struct __align__(128) Smem {
   uint8_t chunk[kStages][kChunkBytes];
   uint8_t desc[kStages][kDescSlot];
-  double2 tab[kTabEntries];
-  float2 tab32[kTabEntries];  // the same tables rounded to complex64 (F32 path)
+  double2 tab[kTabEntries];   // lookup tables (complex64 in the F32 fast path)
+  double2 gslice[kStages][2 << kStageMaxK];  // staged tile slice of gathered operand 0
+                                             // (raw complex64 or complex128 entries)
   uint64_t gjj[kSMaxG][kJ];   // thread-independent gather parts (per descriptor)
   uint32_t tjj[kSMaxT][kJ];
+  uint32_t tjs[kJ];           // ... of the staged slice index
   uint64_t full[kStages];
   uint64_t empty[kStages];
 };
@@ -86,6 +88,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void cp_async(void* dst, const void* src, uint32_t bytes) {
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
 }
 // consumer-warps-only barrier (the producer warp never joins)
 __device__ __forceinline__ void consumers_sync() {
@@ -207,6 +217,8 @@ struct ThreadState {
   uint32_t gvs[kSMaxG], gc64[kSMaxG];
   char* out;
   uint32_t ng, nt, tile_elems, tb, pmask, pk, split, pstep;
+  uint32_t ts;                        // staged slice index, lane part
+  uint32_t stage_k;                   // 0xff: operand 0 not staged
 };
 
 // Generic tile: any dtypes, any operand counts, partial tiles.
@@ -256,10 +268,12 @@ __device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
 // Full tile, operand counts known at compile time.  F32: complex64 primary
 // and output, float32 arithmetic with complex64 lookup tables (the tables
 // themselves are products formed in float64); otherwise complex128 / float64.
-template <bool F32, int NT, int NG>
-__device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* chunk, const Smem& S,
+template <bool F32, int NT, int NG, bool STAGED = false>
+__device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* chunk, Smem& S,
                                           const SGRec* gr, const STRec* tr, uint64_t obase,
-                                          uint32_t tid) {
+                                          uint32_t tid, const double2* gsl) {
+  // STAGED: the producer warp already gathered the 2^(k+1) entries of
+  // operand 0 this tile touches into gsl (raw storage type)
   uint64_t gb[NG > 0 ? NG : 1];
   uint32_t tbs[NT > 0 ? NT : 1];
 #pragma unroll
@@ -279,15 +293,29 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
         const float4 tv = *reinterpret_cast<const float4*>(
-            S.tab32 + T.toff[q] + ((tbs[q] | S.tjj[q][j]) << 1));
+            reinterpret_cast<const float2*>(S.tab) + T.toff[q] + ((tbs[q] | S.tjj[q][j]) << 1));
         a0 = cmulf(a0, make_float2(tv.x, tv.y));
         a1 = cmulf(a1, make_float2(tv.z, tv.w));
       }
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
-        const uint64_t idx = gb[g] | S.gjj[g][j];
-        const double2 x = ldg_c(T.gptr[g], idx, T.gc64[g]);
-        const double2 y = ldg_c(T.gptr[g], idx + (1ull << T.gvs[g]), T.gc64[g]);
+        double2 x, y;
+        if (STAGED && g == 0) {
+          const uint32_t si = (T.ts | S.tjs[j]) << 1;
+          if (T.gc64[0]) {
+            const float2 xf = reinterpret_cast<const float2*>(gsl)[si];
+            const float2 yf = reinterpret_cast<const float2*>(gsl)[si + 1];
+            x = make_double2(xf.x, xf.y);
+            y = make_double2(yf.x, yf.y);
+          } else {
+            x = gsl[si];
+            y = gsl[si + 1];
+          }
+        } else {
+          const uint64_t idx = gb[g] | S.gjj[g][j];
+          x = ldg_c(T.gptr[g], idx, T.gc64[g]);
+          y = ldg_c(T.gptr[g], idx + (1ull << T.gvs[g]), T.gc64[g]);
+        }
         a0 = cmulf(a0, make_float2((float)x.x, (float)x.y));
         a1 = cmulf(a1, make_float2((float)y.x, (float)y.y));
       }
@@ -303,9 +331,25 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
       }
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
-        const uint64_t idx = gb[g] | S.gjj[g][j];
-        a0 = cmul(a0, ldg_c(T.gptr[g], idx, T.gc64[g]));
-        a1 = cmul(a1, ldg_c(T.gptr[g], idx + (1ull << T.gvs[g]), T.gc64[g]));
+        if (STAGED && g == 0) {
+          const uint32_t si = (T.ts | S.tjs[j]) << 1;
+          double2 x, y;
+          if (T.gc64[0]) {
+            const float2 xf = reinterpret_cast<const float2*>(gsl)[si];
+            const float2 yf = reinterpret_cast<const float2*>(gsl)[si + 1];
+            x = make_double2(xf.x, xf.y);
+            y = make_double2(yf.x, yf.y);
+          } else {
+            x = gsl[si];
+            y = gsl[si + 1];
+          }
+          a0 = cmul(a0, x);
+          a1 = cmul(a1, y);
+        } else {
+          const uint64_t idx = gb[g] | S.gjj[g][j];
+          a0 = cmul(a0, ldg_c(T.gptr[g], idx, T.gc64[g]));
+          a1 = cmul(a1, ldg_c(T.gptr[g], idx + (1ull << T.gvs[g]), T.gc64[g]));
+        }
       }
       reinterpret_cast<double2*>(T.out)[obase + e] = make_double2(a0.x + a1.x, a0.y + a1.y);
     }
@@ -326,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (t0 >= t1) return;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&S.full[s], 1);
+      mbar_init(&S.full[s], 1 + 32);
       mbar_init(&S.empty[s], kWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -335,17 +379,41 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (tid >= kCompute) {
     // ---------------- producer warp
-    if (tid == kCompute) {
-      uint32_t hint = 0;
-      uint64_t i = 0;
-      for (uint64_t t = t0; t < t1; ++t, ++i) {
-        const int s = (int)(i % kStages);
-        if (i >= (uint64_t)kStages) mbar_wait(&S.empty[s], (uint32_t)(((i / kStages) - 1) & 1));
-        const Loc l = locate(L, t, hint);
-        hint = l.item;
-        issue_tile(L, D, S, l, s);
+    // lane 0 issues the bulk copies; all 32 lanes gather the staged slice
+    // of gathered operand 0 with cp.async and arrive on full[s] when their
+    // copies land (full[s] expects 1 + 32 arrivals per phase)
+    const uint32_t lane = tid & 31;
+    uint32_t hint = 0;
+    uint64_t i = 0;
+    for (uint64_t t = t0; t < t1; ++t, ++i) {
+      const int s = (int)(i % kStages);
+      if (i >= (uint64_t)kStages) mbar_wait(&S.empty[s], (uint32_t)(((i / kStages) - 1) & 1));
+      const Loc l = locate(L, t, hint);
+      hint = l.item;
+      if (lane == 0) issue_tile(L, D, S, l, s);
+      const uint8_t* dsc = L.item_desc ? L.descs + L.item_desc[l.item] : D.bytes;
+      const SHdr* h = reinterpret_cast<const SHdr*>(dsc);
+      const SGRec* G = reinterpret_cast<const SGRec*>(dsc + sizeof(SHdr));
+      if (h->ng >= 1 && G->stage_k != 0xff) {
+        const Bases b = bases_of(L, l);
+        const char* gp = resolve(G->ptr, b);
+        const uint32_t esz = G->c64 ? 8u : 16u;
+        const uint64_t gbh = gather(l.tile << h->tb, G->runs, G->n_runs);
+        const uint32_t n = 2u << G->stage_k;
+        char* dst = reinterpret_cast<char*>(S.gslice[s]);
+        for (uint32_t j = lane; j < n; j += 32) {
+          const uint64_t gi = gbh | gather(j >> 1, G->grun, G->n_grun) |
+                              ((uint64_t)(j & 1) << G->vshift);
+          cp_async(dst + j * esz, gp + gi * esz, esz);
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                         smem_u32(&S.full[s]))
+                     : "memory");
+      } else {
+        mbar_arrive(&S.full[s]);
       }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     return;
   }
 
@@ -368,6 +436,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Bases b = bases_of(L, l);
       const SORec* orr = reinterpret_cast<const SORec*>(dsc + sizeof(SHdr) + h->ng * sizeof(SGRec) +
                                                         h->nt * sizeof(STRec));
+      const bool full_tile = (1u << h->tb) == (uint32_t)(kJ * kCompute);
+      const bool tab_f32 = full_tile && h->nt <= 2 && h->ng <= 1 && h->p_c64 && h->out_c64;
       for (uint32_t q = 0; q < h->nt; ++q) {
         const STRec& TR = tr[q];
         const uint32_t n = 2u << TR.nbits;
@@ -379,8 +449,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t idx = gather(bits, O.runs, O.n_runs) | ((uint64_t)v << O.vshift);
             acc = cmul(acc, ldg_c(resolve(O.ptr, b), idx, O.c64));
           }
-          S.tab[TR.smem_off + e] = acc;
-          S.tab32[TR.smem_off + e] = make_float2((float)acc.x, (float)acc.y);
+          if (tab_f32)
+            reinterpret_cast<float2*>(S.tab)[TR.smem_off + e] = make_float2((float)acc.x, (float)acc.y);
+          else
+            S.tab[TR.smem_off + e] = acc;
         }
       }
       T.ng = h->ng;
@@ -410,8 +482,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           T.gt[g] = gather(lane_e, gr[g].runs, gr[g].n_runs);
         }
       }
+      T.stage_k = (T.ng >= 1) ? gr[0].stage_k : 0xffu;
+      if (T.stage_k != 0xffu) T.ts = (uint32_t)gather(lane_e, gr[0].srun, gr[0].n_srun);
       if (tid < kJ) {
         const uint64_t ej = ((uint64_t)tid * kCompute) & (T.tile_elems - 1);
+        if (T.stage_k != 0xffu) S.tjs[tid] = (uint32_t)gather(ej, gr[0].srun, gr[0].n_srun);
         for (uint32_t q = 0; q < T.nt; ++q) S.tjj[q][tid] = (uint32_t)gather(ej, tr[q].runs, tr[q].n_runs);
         for (uint32_t g = 0; g < T.ng; ++g) S.gjj[g][tid] = gather(ej, gr[g].runs, gr[g].n_runs);
       }
@@ -420,8 +495,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       pc64 = h->p_c64;
       oc64 = h->out_c64;
       variant = 0;
-      if (T.tile_elems == (uint32_t)(kJ * kCompute) && T.nt <= 2 && T.ng <= 1 && pc64 == oc64)
+      if (T.tile_elems == (uint32_t)(kJ * kCompute) && T.nt <= 2 && T.ng <= 1 && pc64 == oc64) {
         variant = 1 + (pc64 ? 6u : 0u) + T.nt * 2 + T.ng;
+        if (T.ng == 1 && T.stage_k != 0xffu) variant = 13 + (pc64 ? 3u : 0u) + T.nt;
+      }
       cur_item = l.item;
       cur_set = l.set;
       consumers_sync();  // tables visible
@@ -429,18 +506,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t obase = l.tile << T.tb;
     const uint8_t* chunk = S.chunk[s];
     switch (variant) {
-      case 1: tile_fast<false, 0, 0>(T, chunk, S, gr, tr, obase, tid); break;
-      case 2: tile_fast<false, 0, 1>(T, chunk, S, gr, tr, obase, tid); break;
-      case 3: tile_fast<false, 1, 0>(T, chunk, S, gr, tr, obase, tid); break;
-      case 4: tile_fast<false, 1, 1>(T, chunk, S, gr, tr, obase, tid); break;
-      case 5: tile_fast<false, 2, 0>(T, chunk, S, gr, tr, obase, tid); break;
-      case 6: tile_fast<false, 2, 1>(T, chunk, S, gr, tr, obase, tid); break;
-      case 7: tile_fast<true, 0, 0>(T, chunk, S, gr, tr, obase, tid); break;
-      case 8: tile_fast<true, 0, 1>(T, chunk, S, gr, tr, obase, tid); break;
-      case 9: tile_fast<true, 1, 0>(T, chunk, S, gr, tr, obase, tid); break;
-      case 10: tile_fast<true, 1, 1>(T, chunk, S, gr, tr, obase, tid); break;
-      case 11: tile_fast<true, 2, 0>(T, chunk, S, gr, tr, obase, tid); break;
-      case 12: tile_fast<true, 2, 1>(T, chunk, S, gr, tr, obase, tid); break;
+      case 1: tile_fast<false, 0, 0>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 2: tile_fast<false, 0, 1>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 3: tile_fast<false, 1, 0>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 4: tile_fast<false, 1, 1>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 5: tile_fast<false, 2, 0>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 6: tile_fast<false, 2, 1>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 7: tile_fast<true, 0, 0>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 8: tile_fast<true, 0, 1>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 9: tile_fast<true, 1, 0>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 10: tile_fast<true, 1, 1>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 11: tile_fast<true, 2, 0>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 12: tile_fast<true, 2, 1>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 13: tile_fast<false, 0, 1, true>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 14: tile_fast<false, 1, 1, true>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 15: tile_fast<false, 2, 1, true>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 16: tile_fast<true, 0, 1, true>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 17: tile_fast<true, 1, 1, true>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
+      case 18: tile_fast<true, 2, 1, true>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;
       default: tile_generic(T, chunk, S, gr, tr, obase, tid, pc64, oc64); break;
     }
     __syncwarp();

@@ -39,10 +39,17 @@ struct SHdr {
   uint64_t n_tiles;
   uint8_t pad1[24];
 };
+constexpr int kStageMaxK = 7;    // stage a gathered operand's tile slice if it
+                                 // depends on <= 9 tile-local output bits
 struct SGRec {
   uint64_t ptr;          // tagged
-  uint8_t vshift, c64, n_runs, pad;
+  uint8_t vshift, c64, n_runs;
+  uint8_t stage_k;       // 0xff: not staged; else #tile-local bits the operand depends on
   uint32_t runs[kSGRuns];  // output bits -> operand bits (src | dst<<8 | len<<16)
+  uint8_t n_srun, n_grun, pad2[2];
+  uint32_t srun[kStageMaxK];  // tile-local output bits -> slice index bits
+  uint32_t grun[kStageMaxK];  // slice index bits -> operand bits
+  uint32_t pad3[1];
 };
 struct STRec {
   uint8_t nbits, n_runs, first_op, n_ops;
@@ -57,7 +64,7 @@ struct SORec {
   uint32_t runs[kSTRuns];  // table index bits -> operand bits
 };
 static_assert(sizeof(SHdr) == 64, "SHdr");
-static_assert(sizeof(SGRec) == 144, "SGRec");
+static_assert(sizeof(SGRec) % 16 == 0, "SGRec");
 static_assert(sizeof(STRec) == 48, "STRec");
 static_assert(sizeof(SORec) == 48, "SORec");
 constexpr int kSDescMax = sizeof(SHdr) + kSMaxG * sizeof(SGRec) + kSMaxT * sizeof(STRec) +
