@@ -709,7 +709,8 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   ffirst.push_back((uint32_t)ftags.size());
   if ((rc = upload(&B->d_prog, blob)) || (rc = upload(&B->d_prog_off, poff)) ||
       (rc = upload(&B->d_in_off, ioff)) || (rc = upload(&B->d_smem_index, sidx)) ||
-      (rc = upload(&B->d_desc, desc)) || (rc = upload(&B->d_item_desc, item_desc)) ||
+      (rc = (desc.resize(desc.size() + 1024, 0), upload(&B->d_desc, desc))) ||
+      (rc = upload(&B->d_item_desc, item_desc)) ||
       (rc = upload(&B->d_item_net, item_net)) || (rc = upload(&B->d_tile_prefix, prefix)) ||
       (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
       (rc = upload(&B->d_fold_tags, ftags)) || (rc = upload(&B->d_fold_c64, fc64)) ||

@@ -290,7 +290,7 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
   SHdr* h = reinterpret_cast<SHdr*>(blob.data() + base);
   const int R = (int)s.out_vars.size();
   const bool pc64 = s.opc64[s.primary] != 0;
-  const int tb = std::min(R, pc64 ? 11 : 10);
+  const int tb = std::min(R, pc64 ? kTileBitsC64 : kTileBitsC128);
   h->out = s.out_tag;
   h->p = s.optag[s.primary];
   h->R = (uint8_t)R;
@@ -301,10 +301,67 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
   h->ng = (uint8_t)ng;
   h->nt = (uint8_t)a.nt;
   h->ntop = (uint8_t)a.ntop;
+  // tile-local bits: ta low bits of the primary + tn of the new (high) bits,
+  // so an expanding bucket (output wider than the primary) reuses each
+  // primary slice from shared memory instead of re-reading it 2^(new) times
+  const int rp1 = (int)s.opvars[s.primary].size() - 1;
+  const int dnew = R - rp1;
+  // e-bit of an output bit for a given split (ta, tn); -1: not tile-local
+  auto e_bit = [&](int ob, int ta_, int tn_) -> int {
+    if (ob < ta_) return ob;
+    if (ob >= rp1 && ob < rp1 + tn_) return ta_ + (ob - rp1);
+    return -1;
+  };
+  // choose tn (new-bit part of the tile) by a per-tile byte model: primary
+  // slice + gathered operands (staged slice if it depends on <= kStageMaxK
+  // tile-local bits, else one 32-byte sector per element and v)
+  int ta = std::min(rp1, tb), tn = tb - ta;
+  {
+    double best = 1e300;
+    const int esz = pc64 ? 8 : 16;
+    for (int tn_c = std::max(0, tb - rp1); tn_c <= std::min(dnew, tb); ++tn_c) {
+      const int ta_c = tb - tn_c;
+      if (ta_c > rp1 || ta_c < 0) continue;
+      double cost = (double)(2 << ta_c) * esz;
+      for (int i = 1; i < (int)a.ng; ++i) {
+        int k = 0;
+        const GOpArg& src = a.g[i];
+        for (uint32_t r = 0; r < src.n_lo + src.n_hi; ++r) {
+          const uint32_t w = r < src.n_lo ? src.lo[r] : src.hi[r - src.n_lo];
+          for (uint32_t q = 0; q < ((w >> 16) & 0xff); ++q)
+            if (e_bit((int)(w & 0xff) + (int)q, ta_c, tn_c) >= 0) ++k;
+        }
+        cost += (i == 1 && k <= kStageMaxK) ? (double)(2 << k) * 32.0 : (double)(2 << tb) * 32.0;
+      }
+      if (cost < best - 1e-9) {
+        best = cost;
+        ta = ta_c;
+        tn = tn_c;
+      }
+    }
+  }
   h->tb = (uint8_t)tb;
+  h->ta = (uint8_t)ta;
+  h->tn = (uint8_t)tn;
+  auto e_of = [&](int ob) -> int { return e_bit(ob, ta, tn); };
+  auto pairs_of = [](const uint32_t* runs, int n) {
+    std::vector<std::pair<int, int>> pr;
+    for (int r = 0; r < n; ++r)
+      for (uint32_t q = 0; q < ((runs[r] >> 16) & 0xff); ++q)
+        pr.push_back({(int)(runs[r] & 0xff) + (int)q, (int)((runs[r] >> 8) & 0xff) + (int)q});
+    return pr;
+  };
+  auto eruns_of = [&](const uint32_t* runs, int n, std::vector<uint32_t>& out) {
+    std::vector<std::pair<int, int>> ep;
+    for (auto& pr : pairs_of(runs, n)) {
+      const int e = e_of(pr.first);
+      if (e >= 0) ep.push_back({e, pr.second});
+    }
+    make_runs(ep, out);
+  };
   h->table_entries = (uint16_t)a.table_entries;
   h->desc_bytes = (uint16_t)bytes;
-  h->n_tiles = 1ull << (R - tb);
+  h->n_tiles = 1ull << (R - ta - tn);
   SGRec* g = reinterpret_cast<SGRec*>(blob.data() + base + sizeof(SHdr));
   for (int i = 0; i < ng; ++i) {
     const GOpArg& src = a.g[i + 1];
@@ -314,24 +371,32 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
     g[i].n_runs = (uint8_t)(src.n_lo + src.n_hi);
     std::copy(src.lo, src.lo + src.n_lo, g[i].runs);
     std::copy(src.hi, src.hi + src.n_hi, g[i].runs + src.n_lo);
-    // Staging: if the operand depends on only k <= 9 of the tile's output
-    // bits, a tile touches 2^(k+1) of its entries; the consumers gather that
-    // slice into shared memory once per tile instead of every element
-    // re-reading it from L2 (the "two wide operands -> wider output" buckets).
-    g[i].stage_k = 0xff;
-    std::vector<std::pair<int, int>> pairs;  // (output bit, operand bit)
-    for (int r = 0; r < g[i].n_runs; ++r) {
-      const uint32_t w = g[i].runs[r];
-      for (uint32_t q = 0; q < ((w >> 16) & 0xff); ++q)
-        pairs.push_back({(int)(w & 0xff) + (int)q, (int)((w >> 8) & 0xff) + (int)q});
+    std::vector<uint32_t> er;
+    eruns_of(g[i].runs, g[i].n_runs, er);
+    if ((int)er.size() > kERuns) {
+      set_error("gathered operand needs too many tile-local runs");
+      return QTN_EINVAL;
     }
-    std::sort(pairs.begin(), pairs.end());
+    g[i].n_erun = (uint8_t)er.size();
+    std::copy(er.begin(), er.end(), g[i].erun);
+    // Staging: if the operand depends on only k <= 7 tile-local bits, a tile
+    // touches 2^(k+1) of its entries; the producer warp gathers that slice
+    // into the stage with cp.async instead of every element re-reading it
+    // from L2 (the "two wide operands -> wider output" buckets).
+    g[i].stage_k = 0xff;
     std::vector<std::pair<int, int>> s_sd, g_sd;
-    for (auto& pr : pairs)
-      if (pr.first < tb) {
+    {
+      std::vector<std::pair<int, int>> ep;
+      for (auto& pr : pairs_of(g[i].runs, g[i].n_runs)) {
+        const int e = e_of(pr.first);
+        if (e >= 0) ep.push_back({e, pr.second});
+      }
+      std::sort(ep.begin(), ep.end());
+      for (auto& pr : ep) {
         s_sd.push_back({pr.first, (int)s_sd.size()});
         g_sd.push_back({(int)g_sd.size(), pr.second});
       }
+    }
     const int k = (int)s_sd.size();
     if (i == 0 && k <= kStageMaxK && k <= tb - 2) {
       std::vector<uint32_t> sr, grr;
@@ -354,6 +419,10 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
     t[j].smem_off = (uint16_t)src.smem_off;
     std::copy(src.lo, src.lo + src.n_lo, t[j].runs);
     std::copy(src.hi, src.hi + src.n_hi, t[j].runs + src.n_lo);
+    std::vector<uint32_t> er;
+    eruns_of(t[j].runs, t[j].n_runs, er);
+    t[j].n_erun = (uint8_t)er.size();
+    std::copy(er.begin(), er.end(), t[j].erun);
   }
   SORec* o = reinterpret_cast<SORec*>(blob.data() + base + sizeof(SHdr) + ng * sizeof(SGRec) +
                                       a.nt * sizeof(STRec));

@@ -36,9 +36,9 @@ constexpr int kCompute = 256;               // 8 consumer warps (9 warps/block
                                             // leave 168 registers per thread)
 constexpr int kWarps = kCompute / 32;
 constexpr int kThreads = kCompute + 32;     // + 1 producer warp
-constexpr int kStages = 4;
-constexpr int kChunkBytes = 32768;          // primary slice per stage
-constexpr int kJ = 8;                        // elements per consumer thread per tile
+constexpr int kStages = kStreamStages;
+constexpr int kChunkBytes = kStreamChunk;     // primary slice per stage
+constexpr int kJ = (1 << kTileBitsC64) / kCompute;  // elements per consumer thread per tile
 constexpr int kTabEntries = kSMaxT * 512;    // complex128 entries
 constexpr int kDescSlot = (kSDescMax + 127) / 128 * 128;
 
@@ -51,6 +51,7 @@ struct __align__(128) Smem {
   uint64_t gjj[kSMaxG][kJ];   // thread-independent gather parts (per descriptor)
   uint32_t tjj[kSMaxT][kJ];
   uint32_t tjs[kJ];           // ... of the staged slice index
+  __align__(16) uint8_t pdesc[sizeof(SHdr) + sizeof(SGRec)];  // producer's descriptor cache
   uint64_t full[kStages];
   uint64_t empty[kStages];
 };
@@ -139,7 +140,26 @@ struct Loc {
   uint64_t tile;
 };
 
-__device__ __forceinline__ Loc locate(const StreamLaunch& L, uint64_t t, uint32_t hint) {
+// Output base of a tile: the tile index enumerates the output bits that are
+// not tile-local (primary bits [ta, rP-1), then new bits [rP-1+tn, R)).
+__device__ __forceinline__ uint64_t tile_base(const SHdr& h, uint64_t t) {
+  const uint32_t r1 = h.p_rank - 1u, a = h.ta;
+  const uint64_t low = t & ((1ull << (r1 - a)) - 1);
+  return (low << a) | ((t >> (r1 - a)) << (r1 + h.tn));
+}
+// Tile-local element e -> output offset within the tile.
+__device__ __forceinline__ uint64_t tile_off(uint32_t e, uint32_t a, uint32_t r1) {
+  return (uint64_t)(e & ((1u << a) - 1u)) | ((uint64_t)(e >> a) << r1);
+}
+
+// Cached item range of the last lookup (tiles of one block are contiguous,
+// so consecutive tiles almost always hit the same item).
+struct LocCache {
+  uint32_t item = 0;
+  uint64_t lo = 1, hi = 0;  // empty
+};
+
+__device__ __forceinline__ Loc locate(const StreamLaunch& L, uint64_t t, LocCache& c) {
   Loc r;
   if (!L.item_desc) {
     r.item = 0;
@@ -149,19 +169,24 @@ __device__ __forceinline__ Loc locate(const StreamLaunch& L, uint64_t t, uint32_
   }
   r.set = (uint32_t)(t / L.total_tiles);
   const uint64_t tt = t - (uint64_t)r.set * L.total_tiles;
-  uint32_t it = hint < L.n_items ? hint : 0;
-  if (L.tile_prefix[it] > tt) it = 0;
-  if (L.tile_prefix[it + 1] <= tt) {
-    uint32_t lo = it, hi = L.n_items;
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (L.tile_prefix[mid] <= tt) lo = mid;
-      else hi = mid;
+  if (!(tt >= c.lo && tt < c.hi)) {
+    uint32_t it = c.item < L.n_items ? c.item : 0;
+    if (L.tile_prefix[it] > tt) it = 0;
+    if (L.tile_prefix[it + 1] <= tt) {
+      uint32_t lo = it, hi = L.n_items;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (L.tile_prefix[mid] <= tt) lo = mid;
+        else hi = mid;
+      }
+      it = lo;
     }
-    it = lo;
+    c.item = it;
+    c.lo = L.tile_prefix[it];
+    c.hi = L.tile_prefix[it + 1];
   }
-  r.item = it;
-  r.tile = tt - L.tile_prefix[it];
+  r.item = c.item;
+  r.tile = tt - c.lo;
   return r;
 }
 
@@ -176,14 +201,13 @@ __device__ __forceinline__ Bases bases_of(const StreamLaunch& L, const Loc& l) {
 
 // Producer: the primary slice of one tile (+ the descriptor in work-list
 // mode) into stage `s`, completing on full[s].
-__device__ void issue_tile(const StreamLaunch& L, const InlineDesc& D, Smem& S, const Loc& l, int s) {
-  const uint8_t* dsc = L.item_desc ? L.descs + L.item_desc[l.item] : D.bytes;
-  const SHdr h = *reinterpret_cast<const SHdr*>(dsc);
+__device__ void issue_tile(const StreamLaunch& L, const uint8_t* dsc, const SHdr& h, Smem& S,
+                           const Loc& l, int s) {
   const Bases b = bases_of(L, l);
   const uint32_t esz = h.p_c64 ? 8u : 16u;
   const uint32_t tb = h.tb;
-  const uint32_t ptb = min(tb, (uint32_t)h.p_rank - 1u);
-  const uint64_t op = (l.tile << tb) & ((1ull << (h.p_rank - 1)) - 1);
+  const uint32_t ptb = h.ta;
+  const uint64_t op = tile_base(h, l.tile) & ((1ull << (h.p_rank - 1)) - 1);
   const uint64_t pidx = (op & ((1ull << h.p_k) - 1)) | ((op >> h.p_k) << (h.p_k + 1));
   const char* P = resolve(h.p, b);
   const bool split = ptb >= 1 && h.p_k >= ptb;
@@ -218,6 +242,7 @@ struct ThreadState {
   char* out;
   uint32_t ng, nt, tile_elems, tb, pmask, pk, split, pstep;
   uint32_t ts;                        // staged slice index, lane part
+  uint32_t ta, r1;                    // tile-local primary bits, primary rank - 1
   uint32_t stage_k;                   // 0xff: operand 0 not staged
 };
 
@@ -255,9 +280,9 @@ __device__ __noinline__ void tile_generic(const ThreadState& T, const uint8_t* c
     }
     const double2 r = make_double2(a0.x + a1.x, a0.y + a1.y);
     if (oc64)
-      reinterpret_cast<float2*>(T.out)[obase + e] = make_float2((float)r.x, (float)r.y);
+      reinterpret_cast<float2*>(T.out)[obase + tile_off(e, T.ta, T.r1)] = make_float2((float)r.x, (float)r.y);
     else
-      reinterpret_cast<double2*>(T.out)[obase + e] = r;
+      reinterpret_cast<double2*>(T.out)[obase + tile_off(e, T.ta, T.r1)] = r;
   }
 }
 
@@ -299,27 +324,33 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
       }
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
-        double2 x, y;
+        float2 x, y;
         if (STAGED && g == 0) {
           const uint32_t si = (T.ts | S.tjs[j]) << 1;
           if (T.gc64[0]) {
-            const float2 xf = reinterpret_cast<const float2*>(gsl)[si];
-            const float2 yf = reinterpret_cast<const float2*>(gsl)[si + 1];
-            x = make_double2(xf.x, xf.y);
-            y = make_double2(yf.x, yf.y);
+            x = reinterpret_cast<const float2*>(gsl)[si];
+            y = reinterpret_cast<const float2*>(gsl)[si + 1];
           } else {
-            x = gsl[si];
-            y = gsl[si + 1];
+            x = make_float2((float)gsl[si].x, (float)gsl[si].y);
+            y = make_float2((float)gsl[si + 1].x, (float)gsl[si + 1].y);
           }
         } else {
           const uint64_t idx = gb[g] | S.gjj[g][j];
-          x = ldg_c(T.gptr[g], idx, T.gc64[g]);
-          y = ldg_c(T.gptr[g], idx + (1ull << T.gvs[g]), T.gc64[g]);
+          if (T.gc64[g]) {
+            x = __ldg(reinterpret_cast<const float2*>(T.gptr[g]) + idx);
+            y = __ldg(reinterpret_cast<const float2*>(T.gptr[g]) + idx + (1ull << T.gvs[g]));
+          } else {
+            const double2 xd = ldg_c(T.gptr[g], idx, 0);
+            const double2 yd = ldg_c(T.gptr[g], idx + (1ull << T.gvs[g]), 0);
+            x = make_float2((float)xd.x, (float)xd.y);
+            y = make_float2((float)yd.x, (float)yd.y);
+          }
         }
-        a0 = cmulf(a0, make_float2((float)x.x, (float)x.y));
-        a1 = cmulf(a1, make_float2((float)y.x, (float)y.y));
+        a0 = cmulf(a0, x);
+        a1 = cmulf(a1, y);
       }
-      reinterpret_cast<float2*>(T.out)[obase + e] = make_float2(a0.x + a1.x, a0.y + a1.y);
+      reinterpret_cast<float2*>(T.out)[obase + tile_off(e, T.ta, T.r1)] =
+          make_float2(a0.x + a1.x, a0.y + a1.y);
     } else {
       double2 a0 = reinterpret_cast<const double2*>(chunk)[i0];
       double2 a1 = reinterpret_cast<const double2*>(chunk)[i1];
@@ -351,7 +382,8 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
           a1 = cmul(a1, ldg_c(T.gptr[g], idx + (1ull << T.gvs[g]), T.gc64[g]));
         }
       }
-      reinterpret_cast<double2*>(T.out)[obase + e] = make_double2(a0.x + a1.x, a0.y + a1.y);
+      reinterpret_cast<double2*>(T.out)[obase + tile_off(e, T.ta, T.r1)] =
+          make_double2(a0.x + a1.x, a0.y + a1.y);
     }
   }
 }
@@ -383,22 +415,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     // of gathered operand 0 with cp.async and arrive on full[s] when their
     // copies land (full[s] expects 1 + 32 arrivals per phase)
     const uint32_t lane = tid & 31;
-    uint32_t hint = 0;
+    LocCache lc;
+    uint32_t pitem = 0xffffffffu;
+    const uint8_t* dsc = D.bytes;
     uint64_t i = 0;
     for (uint64_t t = t0; t < t1; ++t, ++i) {
       const int s = (int)(i % kStages);
       if (i >= (uint64_t)kStages) mbar_wait(&S.empty[s], (uint32_t)(((i / kStages) - 1) & 1));
-      const Loc l = locate(L, t, hint);
-      hint = l.item;
-      if (lane == 0) issue_tile(L, D, S, l, s);
-      const uint8_t* dsc = L.item_desc ? L.descs + L.item_desc[l.item] : D.bytes;
-      const SHdr* h = reinterpret_cast<const SHdr*>(dsc);
-      const SGRec* G = reinterpret_cast<const SGRec*>(dsc + sizeof(SHdr));
+      const Loc l = locate(L, t, lc);
+      if (l.item != pitem) {
+        // cache the header + first gather record of the new descriptor
+        if (L.item_desc) {
+          dsc = L.descs + L.item_desc[l.item];
+          const uint4* src = reinterpret_cast<const uint4*>(dsc);
+          uint4* dst = reinterpret_cast<uint4*>(S.pdesc);
+          for (uint32_t w = lane; w < sizeof(S.pdesc) / 16; w += 32) dst[w] = __ldg(src + w);
+        } else {
+          for (uint32_t w = lane; w < sizeof(S.pdesc) / 16; w += 32)
+            reinterpret_cast<uint4*>(S.pdesc)[w] = reinterpret_cast<const uint4*>(D.bytes)[w];
+        }
+        __syncwarp();
+        pitem = l.item;
+      }
+      const SHdr* h = reinterpret_cast<const SHdr*>(S.pdesc);
+      const SGRec* G = reinterpret_cast<const SGRec*>(S.pdesc + sizeof(SHdr));
+      if (lane == 0) issue_tile(L, dsc, *h, S, l, s);
       if (h->ng >= 1 && G->stage_k != 0xff) {
         const Bases b = bases_of(L, l);
         const char* gp = resolve(G->ptr, b);
         const uint32_t esz = G->c64 ? 8u : 16u;
-        const uint64_t gbh = gather(l.tile << h->tb, G->runs, G->n_runs);
+        const uint64_t gbh = gather(tile_base(*h, l.tile), G->runs, G->n_runs);
         const uint32_t n = 2u << G->stage_k;
         char* dst = reinterpret_cast<char*>(S.gslice[s]);
         for (uint32_t j = lane; j < n; j += 32) {
@@ -419,13 +465,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ---------------- consumer warps
   ThreadState T;
-  uint32_t cur_item = 0xffffffffu, cur_set = 0xffffffffu, hint = 0;
+  uint32_t cur_item = 0xffffffffu, cur_set = 0xffffffffu;
+  LocCache lc;
   uint32_t variant = 0, pc64 = 0, oc64 = 0;
   uint64_t i = 0;
   for (uint64_t t = t0; t < t1; ++t, ++i) {
     const int s = (int)(i % kStages);
-    const Loc l = locate(L, t, hint);
-    hint = l.item;
+    const Loc l = locate(L, t, lc);
     mbar_wait(&S.full[s], (uint32_t)((i / kStages) & 1));
     const uint8_t* dsc = L.item_desc ? S.desc[s] : D.bytes;
     const SHdr* h = reinterpret_cast<const SHdr*>(dsc);
@@ -460,7 +506,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       T.tb = h->tb;
       T.tile_elems = 1u << h->tb;
       T.out = const_cast<char*>(resolve(h->out, b));
-      const uint32_t ptb = min((uint32_t)h->tb, (uint32_t)h->p_rank - 1u);
+      const uint32_t ptb = h->ta;
+      T.ta = h->ta;
+      T.r1 = h->p_rank - 1u;
       T.pk = h->p_k;
       T.split = (ptb >= 1 && T.pk >= ptb) ? 1u : 0u;
       T.pmask = (1u << ptb) - 1u;
@@ -470,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int q = 0; q < kSMaxT; ++q) {
         if (q < (int)T.nt) {
           T.toff[q] = tr[q].smem_off;
-          T.tt[q] = (uint32_t)gather(lane_e, tr[q].runs, tr[q].n_runs);
+          T.tt[q] = (uint32_t)gather(lane_e, tr[q].erun, tr[q].n_erun);
         }
       }
 #pragma unroll
@@ -479,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           T.gptr[g] = resolve(gr[g].ptr, b);
           T.gvs[g] = gr[g].vshift;
           T.gc64[g] = gr[g].c64;
-          T.gt[g] = gather(lane_e, gr[g].runs, gr[g].n_runs);
+          T.gt[g] = gather(lane_e, gr[g].erun, gr[g].n_erun);
         }
       }
       T.stage_k = (T.ng >= 1) ? gr[0].stage_k : 0xffu;
@@ -487,8 +535,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tid < kJ) {
         const uint64_t ej = ((uint64_t)tid * kCompute) & (T.tile_elems - 1);
         if (T.stage_k != 0xffu) S.tjs[tid] = (uint32_t)gather(ej, gr[0].srun, gr[0].n_srun);
-        for (uint32_t q = 0; q < T.nt; ++q) S.tjj[q][tid] = (uint32_t)gather(ej, tr[q].runs, tr[q].n_runs);
-        for (uint32_t g = 0; g < T.ng; ++g) S.gjj[g][tid] = gather(ej, gr[g].runs, gr[g].n_runs);
+        for (uint32_t q = 0; q < T.nt; ++q) S.tjj[q][tid] = (uint32_t)gather(ej, tr[q].erun, tr[q].n_erun);
+        for (uint32_t g = 0; g < T.ng; ++g) S.gjj[g][tid] = gather(ej, gr[g].erun, gr[g].n_erun);
       }
       // fast path: full tiles, <= 2 tables, <= 1 gathered operand, matching
       // dtypes; variant = 1 + F32*6 + NT*2 + NG, 0 = generic
@@ -503,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       cur_set = l.set;
       consumers_sync();  // tables visible
     }
-    const uint64_t obase = l.tile << T.tb;
+    const uint64_t obase = tile_base(*h, l.tile);
     const uint8_t* chunk = S.chunk[s];
     switch (variant) {
       case 1: tile_fast<false, 0, 0>(T, chunk, S, gr, tr, obase, tid, S.gslice[s]); break;

@@ -15,6 +15,18 @@ inline uint64_t tag_abs(const void* p) { return (uint64_t)(uintptr_t)p; }
 inline uint64_t tag_in(uint64_t byte_off) { return (1ull << kSelShift) | byte_off; }
 inline uint64_t tag_ws(uint64_t byte_off) { return (2ull << kSelShift) | byte_off; }
 
+// pipeline geometry (overridable at build time for A/B experiments)
+#ifndef QTN_STREAM_STAGES
+#define QTN_STREAM_STAGES 4
+#endif
+#ifndef QTN_TILE_BITS_C64
+#define QTN_TILE_BITS_C64 11
+#endif
+constexpr int kStreamStages = QTN_STREAM_STAGES;
+constexpr int kTileBitsC64 = QTN_TILE_BITS_C64;      // tile = 2^11 complex64 outputs
+constexpr int kTileBitsC128 = QTN_TILE_BITS_C64 - 1;
+constexpr int kStreamChunk = 16 << kTileBitsC64;     // primary slice bytes per stage
+
 constexpr int kSMaxG = 3;        // gathered operands besides the primary
 constexpr int kSMaxT = 4;        // lookup tables
 constexpr int kSMaxTOps = 16;    // small operands folded into tables
@@ -32,30 +44,39 @@ struct SHdr {
   uint8_t p_k;           // bit of v inside the primary
   uint8_t p_rank;
   uint8_t ng, nt, ntop;
-  uint8_t tb;            // tile bits
-  uint8_t pad0[3];
+  uint8_t tb;            // tile bits = ta + tn
+  uint8_t ta;            // tile-local bits taken from the primary's low bits
+  uint8_t tn;            // tile-local bits taken from the new (high) bits
+  uint8_t pad0;
   uint16_t table_entries;
   uint16_t desc_bytes;
   uint64_t n_tiles;
   uint8_t pad1[24];
 };
+// Tile-local element e (tb bits) maps to output bits: e[0,ta) -> o[0,ta),
+// e[ta,tb) -> o[rP-1, rP-1+tn) (rP = primary rank).  Every gather is split
+// into a per-tile part over o (`runs`, applied to the tile base) and a
+// tile-local part over e (`erun`).
 constexpr int kStageMaxK = 7;    // stage a gathered operand's tile slice if it
-                                 // depends on <= 9 tile-local output bits
+                                 // depends on <= 7 tile-local bits
+constexpr int kERuns = 12;
 struct SGRec {
   uint64_t ptr;          // tagged
   uint8_t vshift, c64, n_runs;
   uint8_t stage_k;       // 0xff: not staged; else #tile-local bits the operand depends on
   uint32_t runs[kSGRuns];  // output bits -> operand bits (src | dst<<8 | len<<16)
-  uint8_t n_srun, n_grun, pad2[2];
-  uint32_t srun[kStageMaxK];  // tile-local output bits -> slice index bits
+  uint8_t n_srun, n_grun, n_erun, pad2;
+  uint32_t srun[kStageMaxK];  // tile-local e bits -> slice index bits
   uint32_t grun[kStageMaxK];  // slice index bits -> operand bits
-  uint32_t pad3[1];
+  uint32_t erun[kERuns];      // tile-local e bits -> operand bits
+  uint32_t pad3[5];
 };
 struct STRec {
   uint8_t nbits, n_runs, first_op, n_ops;
   uint16_t smem_off;
-  uint16_t pad;
+  uint8_t n_erun, pad;
   uint32_t runs[kSTRuns];  // output bits -> table index bits
+  uint32_t erun[kSTRuns];  // tile-local e bits -> table index bits
   uint32_t pad2[2];
 };
 struct SORec {
@@ -65,7 +86,7 @@ struct SORec {
 };
 static_assert(sizeof(SHdr) == 64, "SHdr");
 static_assert(sizeof(SGRec) % 16 == 0, "SGRec");
-static_assert(sizeof(STRec) == 48, "STRec");
+static_assert(sizeof(STRec) % 16 == 0, "STRec");
 static_assert(sizeof(SORec) == 48, "SORec");
 constexpr int kSDescMax = sizeof(SHdr) + kSMaxG * sizeof(SGRec) + kSMaxT * sizeof(STRec) +
                           kSMaxTOps * sizeof(SORec);
