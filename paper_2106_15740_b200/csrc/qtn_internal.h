@@ -86,7 +86,8 @@ struct SmemHeader {
   uint32_t tab_off;            // byte offset of the u16 gather tables
   uint32_t in_off;             // byte offset of the SmemIn records
   uint32_t n_init;             // leading SmemIn records materialised before bucket 0
-  uint32_t pad[3];
+  uint32_t n_init_gen;         // leading generator entries materialised before bucket 0
+  uint32_t pad[2];
 };
 // Generator section (appended by qtn_batch_set_recipes): the warp builds its
 // own input tensors in shared memory from the angles of its set — the
@@ -114,7 +115,10 @@ struct SmemBucket {
   uint16_t first_op;
   uint16_t first_in;           // input tensors materialised just before this bucket
   uint8_t n_in;
-  uint8_t pad[7];
+  uint8_t pad0;
+  uint16_t first_gen;          // ... as generator entries (set by qtn_batch_set_recipes)
+  uint16_t n_gen;
+  uint8_t pad[2];
 };
 // An input tensor is generated (or copied) into shared memory right before
 // the bucket that consumes it (every input is consumed exactly once), so it

@@ -232,111 +232,105 @@ struct SmemArgs {
   int32_t n_total;
   uint32_t prog_max;           // bytes reserved for the program (CTA-shared)
   uint32_t set_bytes;          // bytes of one angle set's data region
-  int32_t sets_per_warp;
+  int32_t lanes_per_set;       // L: lanes per set (power of two); 32/L sets per warp
 };
 
 constexpr int kNetWarps = 4;   // warps per CTA (upper bound)
 
-// One CTA = one network; each warp evaluates `sets_per_warp` angle sets at
-// once: a bucket of 2^R outputs is S*2^R (set, element) items spread over
-// the 32 lanes, so the many tiny buckets of these networks (R <= 4 for 97%
-// of config-2 buckets) still fill the warp.  The bucket program, gather
-// tables and generator records are staged once per CTA; every operand index
-// is one table lookup (two for R > 5).
+// One CTA = one network.  A warp evaluates G = 32/L angle sets; each set is
+// handled by L lanes (L = A.lanes_per_set, a power of two).  With L = 1
+// every lane runs the whole bucket program for its own set, sequentially,
+// with no cross-lane dependency at all; larger L splits each bucket's
+// outputs over L lanes (for networks whose per-set data is too large to
+// keep 32 sets resident).  Set s's element x lives at D[G*x + s]: lanes of
+// different sets hit different banks.  The program, gather tables and
+// generator entries are staged once per CTA and read as warp-uniform
+// broadcasts; every operand index is one table lookup (two for R > 5);
+// input tensors are generated from the set's angles right before their
+// bucket.
 __global__ void __launch_bounds__(32 * kNetWarps) smem_net_kernel(const __grid_constant__ SmemArgs A) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int net = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = A.sets_per_warp;
-  const int set0 = (blockIdx.y * (int)(blockDim.x >> 5) + warp) * S;
+  const int L = A.lanes_per_set, G = 32 / L;
+  const int sub = lane & (L - 1), gs = lane / L;  // lane within the set, set within the warp
+  const int wset0 = (blockIdx.y * (int)(blockDim.x >> 5) + warp) * G;
+  const int set = wset0 + gs;
   const uint8_t* gp = A.progs + A.prog_off[net];
   const SmemHeader h = *reinterpret_cast<const SmemHeader*>(gp);
   copy16(sm, gp, h.prog_bytes, threadIdx.x, blockDim.x);
   __syncthreads();
-  if (set0 >= A.n_sets) return;
-  const int ns = min(S, A.n_sets - set0);
-  const uint32_t stride = A.set_bytes / 16;  // complex128 elements per set region
-  double2* D0 = reinterpret_cast<double2*>(sm + A.prog_max + (size_t)warp * S * A.set_bytes);
-  if (A.angles && h.n_recs) {
-    const SmemGenParam* par = reinterpret_cast<const SmemGenParam*>(sm + h.gen_off);
-    for (uint32_t it = lane; it < (uint32_t)ns * h.n_params; it += 32) {
-      const uint32_t s = it / h.n_params, k = it - s * h.n_params;
-      const SmemGenParam q = par[k];
-      double2* ph = D0 + s * stride + h.data_elems;
-      if (q.angle == -2) {
-        ph[k] = make_double2(q.scale, q.offset);
-      } else {
-        const double* ang = A.angles + (int64_t)(set0 + s) * A.n_angles;
-        const double t = q.angle >= 0 ? q.scale * ang[q.angle] + q.offset : q.offset;
-        double sn, cs;
-        sincos(t, &sn, &cs);
-        ph[k] = make_double2(cs, -sn);
-      }
-    }
-  }
-  __syncwarp();
+  if (wset0 >= A.n_sets) return;
+  const bool live = set < A.n_sets;
+  double2* D = reinterpret_cast<double2*>(sm + A.prog_max + (size_t)warp * G * A.set_bytes) + gs;
   const bool gen = A.angles && h.n_recs;
   const SmemGenRec* grec = reinterpret_cast<const SmemGenRec*>(sm + h.gen_off +
                                                                sizeof(SmemGenParam) * h.n_params);
   const SmemIn* sin = reinterpret_cast<const SmemIn*>(sm + h.in_off);
+  const double2* src_in = A.inputs + (int64_t)(live ? set : 0) * A.set_elems + A.in_off[net];
   if (gen) {
-    // every input entry of every set of the warp: one item each
-    for (uint32_t it = lane; it < (uint32_t)ns * h.n_recs; it += 32) {
-      const uint32_t s = it / h.n_recs;
-      const SmemGenRec g = grec[it - s * h.n_recs];
-      double2* D = D0 + s * stride;
-      D[g.sm_off] = gen_entry(g.kind, g.full, D[h.data_elems + g.param]);
+    const SmemGenParam* par = reinterpret_cast<const SmemGenParam*>(sm + h.gen_off);
+    const double* ang = A.angles + (int64_t)(live ? set : 0) * A.n_angles;
+    for (uint32_t k = sub; k < h.n_params; k += L) {
+      const SmemGenParam q = par[k];
+      double2 ph;
+      if (q.angle == -2) {
+        ph = make_double2(q.scale, q.offset);
+      } else {
+        const double t = q.angle >= 0 ? q.scale * ang[q.angle] + q.offset : q.offset;
+        double sn, cs;
+        sincos(t, &sn, &cs);
+        ph = make_double2(cs, -sn);
+      }
+      D[G * (h.data_elems + k)] = ph;
     }
+    if (L > 1) __syncwarp();
   }
-  // copy path: input tensors [first, first+cnt) from the packed input buffer
-  auto materialise = [&](uint32_t first, uint32_t cnt) {
-    if (gen) return;
-    for (uint32_t it = lane; it < (uint32_t)ns * cnt; it += 32) {
-      const uint32_t s = it / cnt;
-      const SmemIn r = sin[first + (it - s * cnt)];
-      double2* D = D0 + s * stride;
-      const double2* src = A.inputs + (int64_t)(set0 + s) * A.set_elems + A.in_off[net] + r.in_off;
-      for (uint32_t e = 0; e < (1u << r.rank); ++e) D[r.sm_off + e] = src[e];
+  auto materialise = [&](uint32_t gfirst, uint32_t gcnt, uint32_t first, uint32_t cnt) {
+    if (gen) {
+      for (uint32_t i = gfirst + sub; i < gfirst + gcnt; i += L) {
+        const SmemGenRec g = grec[i];
+        D[G * g.sm_off] = gen_entry(g.kind, g.full, D[G * (h.data_elems + g.param)]);
+      }
+    } else {
+      for (uint32_t i = first; i < first + cnt; ++i) {
+        const SmemIn r = sin[i];
+        for (uint32_t e = sub; e < (1u << r.rank); e += L) D[G * (r.sm_off + e)] = src_in[r.in_off + e];
+      }
     }
+    if (L > 1) __syncwarp();
   };
-  materialise(0, h.n_init);
+  materialise(0, h.n_init_gen, 0, h.n_init);
   const SmemBucket* bk = reinterpret_cast<const SmemBucket*>(sm + sizeof(SmemHeader));
   const SmemOp* ops = reinterpret_cast<const SmemOp*>(sm + sizeof(SmemHeader) +
                                                       sizeof(SmemBucket) * h.n_buckets);
   const uint16_t* tab = reinterpret_cast<const uint16_t*>(sm + h.tab_off);
   for (uint32_t bi = 0; bi < h.n_buckets; ++bi) {
     const SmemBucket b = bk[bi];
+    materialise(b.first_gen, b.n_gen, b.first_in, b.n_in);
     const SmemOp* bo = ops + b.first_op;
     const uint32_t R = b.R;
-    const uint32_t n = (uint32_t)ns << R;
-    const uint32_t emask = (1u << R) - 1u;
-    if (b.n_in) {
-      materialise(b.first_in, b.n_in);
-      __syncwarp();
-    }
-    for (uint32_t it = lane; it < n; it += 32) {
-      const uint32_t s = it >> R, e = it & emask;
-      const double2* D = D0 + s * stride;
+    const uint32_t n = 1u << R;
+    for (uint32_t e = sub; e < n; e += L) {
       const uint32_t hi_e = e >> 5, lo_e = e & 31;
       SmemOp o = bo[0];
       uint32_t idx = o.off + tab[o.lo + lo_e] + (R > 5 ? tab[o.hi + hi_e] : 0u);
-      double2 a0 = D[idx], a1 = D[idx + o.vstep];
+      double2 a0 = D[G * idx], a1 = D[G * (idx + o.vstep)];
       for (uint32_t k = 1; k < b.n_ops; ++k) {
         o = bo[k];
         idx = o.off + tab[o.lo + lo_e] + (R > 5 ? tab[o.hi + hi_e] : 0u);
-        a0 = cmul(a0, D[idx]);
-        a1 = cmul(a1, D[idx + o.vstep]);
+        a0 = cmul(a0, D[G * idx]);
+        a1 = cmul(a1, D[G * (idx + o.vstep)]);
       }
-      D0[s * stride + b.out_off + e] = cadd(a0, a1);
+      D[G * (b.out_off + e)] = cadd(a0, a1);
     }
-    __syncwarp();
+    if (L > 1) __syncwarp();
   }
-  if (lane < ns) {
-    const double2* D = D0 + lane * stride;
+  if (live && sub == 0) {
     const uint16_t* sc = reinterpret_cast<const uint16_t*>(
         sm + sizeof(SmemHeader) + sizeof(SmemBucket) * h.n_buckets + sizeof(SmemOp) * h.n_ops);
     double2 r = make_double2(ldexp(1.0, (int)h.pow2), 0.0);
-    for (uint32_t i = 0; i < h.n_scalars; ++i) r = cmul(r, D[sc[i]]);
-    A.results[(int64_t)(set0 + lane) * A.n_total + A.out_index[net]] = r;
+    for (uint32_t i = 0; i < h.n_scalars; ++i) r = cmul(r, D[G * sc[i]]);
+    A.results[(int64_t)set * A.n_total + A.out_index[net]] = r;
   }
 }
 
@@ -779,18 +773,23 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
     SmemHeader* h = reinterpret_cast<SmemHeader*>(prog.data());
     std::vector<SmemGenParam> params;
     std::vector<SmemGenRec> recs;
-    // where each input tensor lives in the data region (from the program)
-    std::vector<int32_t> in_sm(offsets[gi + 1] - offsets[gi], -1);
-    {
-      const SmemIn* sin = reinterpret_cast<const SmemIn*>(prog.data() + h->in_off);
-      uint32_t n_in = 0;
-      const SmemBucket* bk = reinterpret_cast<const SmemBucket*>(prog.data() + sizeof(SmemHeader));
-      n_in = h->n_init;
-      for (uint32_t b = 0; b < h->n_buckets; ++b) n_in = std::max<uint32_t>(n_in, bk[b].first_in + bk[b].n_in);
-      for (uint32_t i = 0; i < n_in; ++i)
-        if (sin[i].input < in_sm.size()) in_sm[sin[i].input] = sin[i].sm_off;
-    }
-    for (int64_t r = offsets[gi]; r < offsets[gi + 1]; ++r) {
+    // generator entries are emitted in materialisation order (the SmemIn
+    // records: rank-0 inputs, then bucket by bucket), so every bucket's
+    // inputs are one contiguous entry range
+    const SmemIn* sin = reinterpret_cast<const SmemIn*>(prog.data() + h->in_off);
+    SmemBucket* bk = reinterpret_cast<SmemBucket*>(prog.data() + sizeof(SmemHeader));
+    uint32_t n_sin = h->n_init;
+    for (uint32_t b = 0; b < h->n_buckets; ++b)
+      n_sin = std::max<uint32_t>(n_sin, bk[b].first_in + bk[b].n_in);
+    std::vector<uint32_t> entry_at(n_sin + 1, 0);
+    for (uint32_t si = 0; si < n_sin; ++si) {
+      entry_at[si] = (uint32_t)recs.size();
+      const int64_t r = offsets[gi] + sin[si].input;
+      if (r >= offsets[gi + 1]) {
+        set_error("qtn_batch_set_recipes: recipes do not match the plan's inputs");
+        return QTN_EINVAL;
+      }
+      const int32_t base = sin[si].sm_off;
       const qtn_tensor_recipe& q = rec[r];
       SmemGenParam p{};
       if (q.kind == QTN_GATE_SCALAR) {
@@ -811,9 +810,8 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
             params[slot].angle == p.angle)
           break;
       if (slot == params.size()) params.push_back(p);
-      const int32_t base = in_sm[r - offsets[gi]];
-      if (slot > 255 || base < 0) {
-        set_error("qtn_batch_set_recipes: recipes do not match the plan's inputs");
+      if (slot > 255) {
+        set_error("qtn_batch_set_recipes: too many distinct gate parameters");
         return QTN_EINVAL;
       }
       // one record per kept entry: slicing (network.py:153-165) resolved here
@@ -833,6 +831,16 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
         g.param = (uint8_t)slot;
         recs.push_back(g);
       }
+    }
+    entry_at[n_sin] = (uint32_t)recs.size();
+    if (recs.size() > 65535) {
+      set_error("qtn_batch_set_recipes: network too large for the fused generator");
+      return QTN_EINVAL;
+    }
+    h->n_init_gen = entry_at[h->n_init];
+    for (uint32_t b = 0; b < h->n_buckets; ++b) {
+      bk[b].first_gen = (uint16_t)entry_at[bk[b].first_in];
+      bk[b].n_gen = (uint16_t)(entry_at[bk[b].first_in + bk[b].n_in] - entry_at[bk[b].first_in]);
     }
     const size_t gen_off = prog.size();
     size_t gen_bytes = params.size() * sizeof(SmemGenParam) + recs.size() * sizeof(SmemGenRec);
@@ -921,21 +929,26 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
   if (B->n_smem) {
     const uint32_t prog_max = (B->prog_max + 15) & ~15u;
     const uint32_t warp_bytes = (B->warp_bytes + 15) & ~15u;
-    // S angle sets per warp, W warps per CTA (as many as fit next to one
-    // copy of the program)
-    static int env_s = -1;
-    if (env_s < 0) {
-      const char* v = getenv("QTN_SETS_PER_WARP");
-      env_s = v ? std::max(1, atoi(v)) : 0;
+    // lanes per set L (measured on B200, config 2 / config 3): 16 lanes per
+    // set (2 sets per warp) for small per-set regions, 32 for large ones;
+    // one lane per set (32 sets per warp, fully independent lanes) is
+    // latency-bound at ~4 warps/SM and 4x slower
+    static int env_l = -1;
+    if (env_l < 0) {
+      const char* v = getenv("QTN_LANES_PER_SET");
+      env_l = v ? std::max(1, atoi(v)) : 0;
     }
-    // measured: 2 sets per warp when a set's region is small (config 2,
-    // ~5 KB), 1 when it is large (config 3, ~20 KB) — occupancy wins there
-    int S = env_s > 0 ? env_s : (warp_bytes <= 12 * 1024 ? 2 : 1);
-    S = std::max(1, std::min(S, (int)n_sets));
-    while (S > 1 && (size_t)prog_max + (size_t)S * warp_bytes > 227u * 1024u) --S;
+    const size_t cap = 227u * 1024u;
+    int L = env_l > 0 ? env_l : (warp_bytes <= 12 * 1024 ? 16 : 32);
+    while (L < 32 && (size_t)prog_max + (size_t)(32 / L) * warp_bytes > cap) L *= 2;
+    if ((size_t)prog_max + warp_bytes > cap) {
+      set_error("smem executor: a network's shared-memory footprint exceeds 227 KiB");
+      return QTN_EINVAL;
+    }
+    const int S = 32 / L;
     const size_t per_warp = (size_t)S * warp_bytes;
-    int W = (int)std::min<size_t>(kNetWarps, (227u * 1024u - prog_max) / std::max<size_t>(per_warp, 16));
     const int warps_needed = (n_sets + S - 1) / S;
+    int W = (int)std::min<size_t>(kNetWarps, (cap - prog_max) / std::max<size_t>(per_warp, 16));
     W = std::max(1, std::min(W, warps_needed));
     const size_t smem = (size_t)prog_max + (size_t)W * per_warp;
     static size_t attr = 0;
@@ -959,7 +972,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     a.n_total = B->n;
     a.prog_max = prog_max;
     a.set_bytes = warp_bytes;
-    a.sets_per_warp = S;
+    a.lanes_per_set = L;
     dim3 grid(B->n_smem, (warps_needed + W - 1) / W);
     smem_net_kernel<<<grid, 32 * W, smem, st>>>(a);
     cudaError_t e = cudaGetLastError();

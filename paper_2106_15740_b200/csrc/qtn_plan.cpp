@@ -15,6 +15,7 @@
 // largest operand streams contiguously.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -585,22 +586,37 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
   bool smem_ok = smem_budget > 0 && nb < 65535;
   int64_t data_elems = 0;
   std::vector<Block> sblocks;
-  // Inputs are materialised in one lane-parallel pass before bucket 0 (the
-  // measured-faster choice for these networks: generating each bucket's
-  // inputs just before it halves the smem footprint but serialises the warp
-  // on tiny steps).  Their smem is reusable by intermediates once consumed.
-  // The program format also supports per-bucket materialisation
-  // (SmemBucket.first_in / n_in).
+  // Input tensors are materialised (generated from the angles, or copied) in
+  // one parallel pass before bucket 0 and their smem is reused by
+  // intermediates once consumed.  QTN_SMEM_LAZY=1 instead materialises each
+  // input right before the bucket that consumes it (every input is consumed
+  // exactly once), which shrinks a set's region to the live intermediates +
+  // one bucket's inputs; measured on B200 it is ~3% faster on config 2 and
+  // ~25% slower on config 3, so it is not the default.
   std::vector<std::vector<int32_t>> bucket_inputs(nb);
   std::vector<int32_t> init_inputs;
+  static int lazy = -1;
+  if (lazy < 0) {
+    const char* e = getenv("QTN_SMEM_LAZY");
+    lazy = e ? atoi(e) : 0;
+  }
   if (smem_ok) {
     for (int k = 0; k < P->n_inputs; ++k) {
       auto& t = P->tensors[k];
-      init_inputs.push_back(k);
-      t.sm_off = place(sblocks, 1ll << t.rank(), -1, t.rank() == 0 ? nb : t.last_use, 1);
-      data_elems = std::max<int64_t>(data_elems, t.sm_off + ((int64_t)1 << t.rank()));
+      if (t.rank() == 0 || !lazy) {
+        init_inputs.push_back(k);
+        t.sm_off = place(sblocks, 1ll << t.rank(), -1, t.rank() == 0 ? nb : t.last_use, 1);
+        data_elems = std::max<int64_t>(data_elems, t.sm_off + ((int64_t)1 << t.rank()));
+      } else {
+        bucket_inputs[t.last_use].push_back(k);
+      }
     }
     for (int bi = 0; bi < nb; ++bi) {
+      for (int32_t k : bucket_inputs[bi]) {
+        auto& t = P->tensors[k];
+        t.sm_off = place(sblocks, 1ll << t.rank(), bi, bi, 1);
+        data_elems = std::max<int64_t>(data_elems, t.sm_off + ((int64_t)1 << t.rank()));
+      }
       auto& o = P->tensors[P->buckets[bi].out];
       o.sm_off = place(sblocks, 1ll << o.rank(), bi, o.last_use, 1);
       data_elems = std::max<int64_t>(data_elems, o.sm_off + ((int64_t)1 << o.rank()));
