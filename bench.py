@@ -331,13 +331,23 @@ def run_gpu(args):
     import paper_2106_15740_b200 as Q
 
     world, rank, local = dist_env()
+    # QTN_DIST_BACKEND=gloo + QTN_SHARE_GPU=1: exercise the multi-rank path
+    # with several ranks on one GPU (no rank waits on another's kernels; the
+    # only exchange is the host-side gloo all-reduce).  Default: NCCL, one
+    # GPU per rank.
+    backend = os.environ.get("QTN_DIST_BACKEND", "nccl")
+    if os.environ.get("QTN_SHARE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     wl = WORKLOADS[args.workload]
     graph = Q.random_regular_graph(wl["n"], 3, 0)
     edge_ids = wl["edges"] if wl["edges"] is not None else list(range(graph.edge_count))

@@ -245,3 +245,63 @@ def test_fused_and_unfused_generation_agree(golden):
     p3._bufs.clear()
     u3 = p3.energies(rng.uniform(0, math.pi, (3, 6)))
     assert f3.shape == u3.shape
+
+
+# ---------------------------------------------------------------- amplitudes
+def test_reference_amplitude_path_k4(golden):
+    """The reference's own workload: build_network amplitudes (pipeline.py:70-81)
+    of K4 at default_angles, all four modes (SPEC.md examples)."""
+    kat = golden("kat.json")["k4_p1_default_angles"]
+    graph = Q.random_regular_graph(4, 3, 0)
+    for mode in Q.MODE_ORDER:
+        net = Q.build_network(graph, 1, mode)
+        order, rep = Q.rgreedy_order(Q.line_graph(net))
+        assert rep.width == kat[mode]["width"]
+        for dt, tol in (("complex128", 1e-13), ("complex64", 1e-6)):
+            v = Q.contract(net, order, dtype=dt)
+            assert abs(v - complex(*kat[mode]["value"])) < tol
+
+
+def test_random_circuits_vs_statevector():
+    """Random small circuits over the whole gate set, both network modes,
+    greedy and rgreedy orders, SMEM and forced-HBM executors, against the
+    oracle statevector amplitude."""
+    rng = np.random.default_rng(5)
+    kinds = ["H", "ZPOW", "XPOW", "CNOT", "ZZ"]
+    for trial in range(12):
+        n = int(rng.integers(2, 7))
+        gates, ogates = [], []
+        for _ in range(int(rng.integers(5, 25))):
+            k = kinds[int(rng.integers(0, 5))]
+            if k in ("CNOT", "ZZ"):
+                a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+                qs = (a, b)
+            else:
+                qs = (int(rng.integers(0, n)),)
+            t = float(rng.uniform(-3, 3)) if k in ("ZPOW", "XPOW", "ZZ") else None
+            gates.append(Q.Gate(Q.GateKind[k], qs, t))
+            ogates.append((k, qs, t))
+        circ = Q.Circuit(n, tuple(gates), complex(np.exp(1j * rng.uniform(0, 6))))
+        bits = "".join(str(int(x)) for x in rng.integers(0, 2, n))
+        psi = O.statevector(n, ogates, circ.phase)
+        want = complex(psi[tuple(int(c) for c in bits)])
+        for mode in (Q.NetworkMode.FULL, Q.NetworkMode.DIAGONAL):
+            net = Q.circuit_to_network(circ, mode, bits)
+            lg = Q.line_graph(net)
+            for order in (Q.greedy_order(lg), Q.rgreedy_order(lg, 4, 0.5, trial)[0]):
+                for budget in (Q.contraction.DEFAULT_SMEM_BUDGET, 0):
+                    v = Q.contract(net, order, smem_budget=budget)
+                    assert abs(v - want) < 1e-12, (trial, mode, budget)
+
+
+def test_degenerate_networks():
+    """Empty buckets (factor 2), scalar-only networks, a single variable."""
+    t0 = Q.Tensor(0, (0,), np.array([1.0, 2.0 + 1j]))
+    net = Q.TensorNetwork((t0, Q.Tensor(1, (), np.array(3.0))), 3, {2: 0})
+    v = Q.contract(net, Q.ContractionOrder((1, 0)))
+    assert abs(v - 2 * 3 * (3.0 + 1j)) < 1e-12
+    only = Q.TensorNetwork((Q.Tensor(0, (), np.array(2.0 - 1j)),), 1, {0: 1})
+    assert abs(Q.contract(only, Q.ContractionOrder(())) - (2.0 - 1j)) < 1e-15
+    for budget in (Q.contraction.DEFAULT_SMEM_BUDGET, 0):
+        assert abs(Q.contract(net, Q.ContractionOrder((0, 1)), smem_budget=budget)
+                   - 6 * (3.0 + 1j)) < 1e-12
