@@ -448,7 +448,12 @@ def run_gpu(args):
     peak, peak_kind = hbm_peak()
     kt = sum(kern_times) / len(kern_times)
     alg = plan.alg_bytes * A
-    kname = "stream_kernel" if plan.hbm_jobs else "smem_net_kernel"
+    if plan.hbm_jobs:
+        kname = "stream_kernel"
+    elif plan._batch.uses_setmajor(A):
+        kname = "sm_level_kernel"
+    else:
+        kname = "smem_net_kernel"
     achieved = alg / kt / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": profile_traffic(kname), "kernel": kname,

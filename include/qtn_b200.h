@@ -143,8 +143,11 @@ int qtn_batch_input_elems(const qtn_batch* batch, int64_t* out_elems);
 int qtn_batch_input_offsets(const qtn_batch* batch, int64_t* out_offsets);
 /* device workspace needed by qtn_batch_execute for n_sets input sets */
 int qtn_batch_workspace_bytes(const qtn_batch* batch, int32_t n_sets, int64_t* out_bytes);
-/* number of kernel launches one qtn_batch_execute issues */
-int qtn_batch_launches(const qtn_batch* batch, int32_t* out_launches);
+/* number of kernel launches one evaluation of n_sets input sets issues */
+int qtn_batch_launches(const qtn_batch* batch, int32_t n_sets, int32_t* out_launches);
+/* 1 if an evaluation of n_sets input sets runs the small networks on the
+ * set-major executor (after qtn_batch_set_recipes), else 0 */
+int qtn_batch_uses_setmajor(const qtn_batch* batch, int32_t n_sets, int32_t* out_flag);
 /* results[s*n + i] = value of network i under input set s (complex128).
  * Input set s starts at inputs + s*set_stride elements (0: the batch's own
  * qtn_batch_input_elems). */
@@ -188,7 +191,10 @@ int qtn_tensorgen(const qtn_tensor_recipe* recipes_dev, int64_t n_recipes,
  * recipes[offsets[i] .. offsets[i+1]), out_offset relative to the network's
  * packed input).  Afterwards qtn_batch_execute_angles builds every input on
  * device: SMEM-executor networks generate their tensors inside the executor
- * kernel (no input buffer at all), HBM networks through qtn_tensorgen. */
+ * kernel (no input buffer at all), HBM networks through qtn_tensorgen.  With
+ * many input sets (>= 64, env QTN_SETMAJOR_MIN_SETS) the small networks run
+ * on the set-major streaming executor instead (angle sets as the fastest
+ * tensor dimension in HBM, gate tensors generated on the fly). */
 int qtn_batch_set_recipes(qtn_batch* batch, const qtn_tensor_recipe* recipes,
                           const int64_t* offsets);
 /* One evaluation for n_sets angle vectors (angles_dev: n_sets x n_angles

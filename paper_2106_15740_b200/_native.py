@@ -89,7 +89,8 @@ _SIGNATURES = {
     "qtn_batch_input_elems": [_p, _i64p],
     "qtn_batch_input_offsets": [_p, _i64p],
     "qtn_batch_workspace_bytes": [_p, C.c_int32, _i64p],
-    "qtn_batch_launches": [_p, _i32p],
+    "qtn_batch_launches": [_p, C.c_int32, _i32p],
+    "qtn_batch_uses_setmajor": [_p, C.c_int32, _i32p],
     "qtn_batch_execute": [_p, _p, C.c_int64, C.c_int32, _p, _p, _p],
     "qtn_batch_destroy": [_p],
     "qtn_batch_set_recipes": [_p, _p, _i64p],

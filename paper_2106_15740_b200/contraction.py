@@ -166,6 +166,7 @@ class PlanBatch:
     def __init__(self, plans):
         _torch_cuda()
         self.plans = list(plans)
+        self._recipes_set = False
         arr = (C.c_void_p * len(self.plans))(*[p.handle for p in self.plans])
         h = C.c_void_p()
         N.check(N.lib.qtn_batch_create(arr, len(self.plans), C.byref(h)), "batch create")
@@ -176,9 +177,18 @@ class PlanBatch:
         offs = np.zeros(len(self.plans), dtype=np.int64)
         N.check(N.lib.qtn_batch_input_offsets(h, N.i64(offs)))
         self.input_offsets = offs
+        self.launches = self.launches_for(1)
+
+    def launches_for(self, n_sets: int) -> int:
         nl = C.c_int32()
-        N.check(N.lib.qtn_batch_launches(h, C.byref(nl)))
-        self.launches = int(nl.value)
+        N.check(N.lib.qtn_batch_launches(self._h, int(n_sets), C.byref(nl)))
+        return int(nl.value) + (1 if (self.has_hbm and self._recipes_set) else 0)
+
+    def uses_setmajor(self, n_sets: int) -> bool:
+        """Whether n_sets input sets run the small networks set-major."""
+        f = C.c_int32()
+        N.check(N.lib.qtn_batch_uses_setmajor(self._h, int(n_sets), C.byref(f)))
+        return bool(f.value)
 
     def workspace_bytes(self, n_sets: int) -> int:
         w = C.c_int64()
@@ -210,10 +220,7 @@ class PlanBatch:
         offs[1:] = np.cumsum([len(r) for r in recipes_per_plan])
         N.check(N.lib.qtn_batch_set_recipes(self._h, allrec.ctypes.data, N.i64(offs)),
                 "set recipes")
-        nl = C.c_int32()
-        N.check(N.lib.qtn_batch_launches(self._h, C.byref(nl)))
-        # + tensorgen for HBM networks
-        self.launches = int(nl.value) + (1 if self.has_hbm else 0)
+        self._recipes_set = True  # execute_angles adds a tensorgen launch for HBM networks
 
     def execute_angles(self, angles_ptr, n_angles, n_sets, scratch_ptr, workspace_ptr,
                        results_ptr, stream):

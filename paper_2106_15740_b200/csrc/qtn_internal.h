@@ -194,6 +194,26 @@ struct qtn_plan {
   std::vector<int32_t> hbm_level;
   std::vector<uint64_t> hbm_tiles;
   int32_t n_levels = 0;
+  // Set-major form of an SMEM-eligible network (qtn_setmajor.cu): angle
+  // sets are the fastest-varying dimension of every tensor in HBM, one
+  // region per intermediate (no reuse: buckets of a level run concurrently),
+  // input tensors generated on the fly.
+  struct SMOpRec {
+    int32_t input;                       // input tensor index, or -1
+    uint32_t off;                        // data-region element offset (intermediates)
+    std::vector<uint16_t> idx;           // per output element e: v=0, v=1 operand element
+  };
+  struct SMBucketRec {
+    int32_t level;
+    uint32_t out_off;
+    int32_t R;
+    std::vector<SMOpRec> ops;            // primary first
+  };
+  std::vector<SMBucketRec> sm_buckets;
+  uint32_t sm_elems = 0;                 // data-region elements (intermediates)
+  std::vector<uint32_t> sm_scalar_off;   // rank-0 intermediates folded at the end
+  std::vector<int32_t> sm_scalar_in;     // rank-0 inputs folded at the end
+  int32_t sm_levels = 0;
   qtn_batch* self_batch = nullptr;       // device copy for single-plan runs
   ~qtn_plan();
 };

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "qtn_internal.h"
+#include "qtn_setmajor.h"
 #include "qtn_stream.h"
 
 using namespace qtn;
@@ -569,6 +570,8 @@ struct qtn_batch {
   uint32_t prog_max = 0;                         // bytes reserved per CTA for the program
   uint32_t warp_bytes = 0;                       // bytes per warp data region
   bool has_recipes = false;
+  qtn::SetMajor* sm = nullptr;                   // set-major form of the SMEM networks
+  std::vector<const qtn_plan*> smem_plans;
   qtn_tensor_recipe* d_hbm_rec = nullptr;        // recipes of the HBM networks
   int64_t n_hbm_rec = 0;
   // HBM executor part (level-synchronous)
@@ -599,6 +602,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_fold_first, (void*)B->d_fold_pow2, (void*)B->d_hbm_index,
                   (void*)B->d_hbm_rec})
     device_free(p);
+  qtn::setmajor_destroy(B->sm);
   delete B;
   return QTN_OK;
 }
@@ -637,6 +641,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     const qtn_plan* P = plans[i];
     if (P->executor == QTN_EXEC_SMEM) {
       B->smem_progs.push_back(P->program);
+      B->smem_plans.push_back(P);
       B->smem_global.push_back(i);
       B->prog_max = std::max<uint32_t>(B->prog_max, (uint32_t)P->program.size());
       {
@@ -729,20 +734,35 @@ extern "C" int qtn_batch_input_offsets(const qtn_batch* B, int64_t* out) {
   return QTN_OK;
 }
 
+static bool use_setmajor(const qtn_batch* B, int32_t n_sets) {
+  const char* v = getenv("QTN_SETMAJOR_MIN_SETS");  // read per call: tests switch it
+  const int min_sets = v ? atoi(v) : 64;
+  return B->sm && min_sets > 0 && n_sets >= min_sets;
+}
+
 extern "C" int qtn_batch_workspace_bytes(const qtn_batch* B, int32_t n_sets, int64_t* out) {
   if (!B || !out || n_sets < 1) return QTN_EINVAL;
-  *out = B->ws_per_set * n_sets;
+  *out = B->ws_per_set * n_sets + (B->sm ? qtn::setmajor_workspace(B->sm, n_sets) : 0);
   return QTN_OK;
 }
 
-extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t* out) {
+static bool use_setmajor(const qtn_batch* B, int32_t n_sets);
+
+extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* out) {
   if (!B || !out) return QTN_EINVAL;
   int c = B->n_smem ? 1 : 0;
+  if (B->n_smem && use_setmajor(B, n_sets)) c = qtn::setmajor_launches(B->sm);
   if (B->n_hbm) {
     for (uint64_t t : B->level_tiles) c += t ? 1 : 0;
     c += 1;
   }
   *out = c;
+  return QTN_OK;
+}
+
+extern "C" int qtn_batch_uses_setmajor(const qtn_batch* B, int32_t n_sets, int32_t* out) {
+  if (!B || !out) return QTN_EINVAL;
+  *out = (B->n_smem && use_setmajor(B, n_sets)) ? 1 : 0;
   return QTN_OK;
 }
 
@@ -884,6 +904,11 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
   if ((rc = upload(&B->d_hbm_rec, hrec))) return rc;
   B->n_hbm_rec = (int64_t)hrec.size();
   B->has_recipes = true;
+  qtn::setmajor_destroy(B->sm);
+  B->sm = nullptr;
+  if (!B->smem_plans.empty() &&
+      (rc = qtn::setmajor_build(&B->sm, B->smem_plans, B->smem_global, rec, offsets, B->n)))
+    return rc;
   return QTN_OK;
 }
 
@@ -903,6 +928,18 @@ extern "C" int qtn_batch_execute_angles(qtn_batch* B, const double* angles, int3
       (rc = qtn_tensorgen(B->d_hbm_rec, B->n_hbm_rec, angles, n_angles, n_sets, B->set_elems,
                           inputs_scratch, stream)))
     return rc;
+  if (use_setmajor(B, n_sets)) {
+    // small networks: set-major streaming executor; HBM networks as usual
+    char* smws = reinterpret_cast<char*>(workspace) + B->ws_per_set * n_sets;
+    if ((rc = qtn::setmajor_run(B->sm, angles, n_angles, n_sets, smws, results, stream))) return rc;
+    if (!B->n_hbm) return QTN_OK;
+    const int n_smem = B->n_smem;
+    B->n_smem = 0;  // skip the SMEM executor for this call
+    rc = run_batch(B, inputs_scratch, B->set_elems, angles, n_angles, n_sets, workspace, results,
+                   stream);
+    B->n_smem = n_smem;
+    return rc;
+  }
   return run_batch(B, inputs_scratch, B->set_elems, angles, n_angles, n_sets, workspace, results,
                    stream);
 }

@@ -741,6 +741,51 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
   if (smem_ok) {
     P->executor = QTN_EXEC_SMEM;
     for (auto& t : P->tensors) t.c64 = false;
+    // ---- set-major form (levels, one region per intermediate)
+    std::vector<int32_t> tlev(P->tensors.size(), 0);
+    std::vector<uint32_t> toff(P->tensors.size(), 0);
+    uint32_t next = 0;
+    for (int bi = 0; bi < nb; ++bi) {
+      const auto& b = P->buckets[bi];
+      const auto& out = P->tensors[b.out];
+      qtn_plan::SMBucketRec rb;
+      int32_t lv = 0;
+      for (int32_t id : b.ops) lv = std::max(lv, tlev[id]);
+      rb.level = lv;
+      tlev[b.out] = lv + 1;
+      P->sm_levels = std::max(P->sm_levels, lv + 1);
+      toff[b.out] = next;
+      rb.out_off = next;
+      next += 1u << b.rank;
+      rb.R = b.rank;
+      std::vector<int32_t> ord = b.ops;
+      std::swap(ord[0], ord[b.primary]);
+      std::vector<std::pair<int, int>> sd;
+      std::vector<uint32_t> runs;
+      for (int32_t id : ord) {
+        const auto& t = P->tensors[id];
+        int vs;
+        operand_map(t.vars, out.vars, b.v, sd, vs);
+        make_runs(sd, runs);
+        qtn_plan::SMOpRec o;
+        o.input = t.input ? id : -1;
+        o.off = t.input ? 0u : toff[id];
+        for (uint32_t e = 0; e < (1u << b.rank); ++e) {
+          uint32_t j = 0;
+          for (uint32_t w : runs)
+            j |= ((e >> (w & 0xff)) & ((1u << ((w >> 16) & 0xff)) - 1)) << ((w >> 8) & 0xff);
+          o.idx.push_back((uint16_t)j);
+          o.idx.push_back((uint16_t)(j + (1u << vs)));
+        }
+        rb.ops.push_back(std::move(o));
+      }
+      P->sm_buckets.push_back(std::move(rb));
+    }
+    P->sm_elems = next;
+    for (int32_t id : P->scalars) {
+      if (P->tensors[id].input) P->sm_scalar_in.push_back(id);
+      else P->sm_scalar_off.push_back(toff[id]);
+    }
   } else {
     P->executor = QTN_EXEC_HBM;
     // levels of the elimination tree: a bucket runs after the buckets that

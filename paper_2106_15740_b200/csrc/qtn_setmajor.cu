@@ -1,0 +1,726 @@
+// Set-major executor (sm_100a): many small networks x many angle sets.
+//
+// The QAOA loop evaluates the same networks at many angle vectors.  Here the
+// angle-set index is made the fastest-varying dimension of every tensor:
+// element x of network n for set s lives at ws[(base_n + x) * A + s].  A
+// bucket  out[e][s] = sum_v prod_t T_t[idx_t(e, v)][s]
+// (contraction.py:42-54, 90-96) then reads and writes 32 consecutive sets
+// per warp — fully coalesced 512-byte rows — and every (bucket, element) is
+// one CTA streaming the A sets.  All buckets of one level of the elimination
+// trees of every network run in one launch (level-synchronous; each
+// intermediate has its own region, so concurrent buckets never alias).
+// Input tensors are never stored: an operand that is a gate tensor is
+// generated on the fly from its gate kind, the entry's index in the unsliced
+// gate (slicing resolved at build time, network.py:153-165) and the set's
+// phase e^{-i t} for the gate's angle (circuit.py:186-205), read from a
+// [param][set] phase table computed once per evaluation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "qtn_setmajor.h"
+
+namespace qtn {
+
+struct SMOpDev {
+  uint32_t tab;     // u16 table index: 2 entries per output element (v = 0, 1)
+  uint32_t off;     // data-region offset (intermediates)
+  uint8_t gen;      // 1: generated gate tensor
+  uint8_t kind;     // QTN_GATE_* (gen)
+  uint16_t param;   // phase-table row (gen)
+  uint32_t pad;
+};
+struct SMBucketDev {
+  uint32_t net;
+  uint32_t out_off;
+  uint32_t first_op;
+  uint8_t R, n_ops;
+  uint16_t pad;
+};
+static_assert(sizeof(SMOpDev) == 16 && sizeof(SMBucketDev) == 16, "sm layouts");
+
+struct SMParam {
+  double scale, offset;
+  int32_t angle;  // -1 constant, -2 literal (scale + i offset)
+  int32_t pad;
+};
+
+// Fused form: one warp evaluates one network for a tile of S = 2^sh sets,
+// every intermediate in shared memory ([element][set], liveness-packed).
+struct SMFNet {
+  uint32_t first_bk, n_bk;
+  uint32_t first_par, n_par;   // net-local phase slots
+  uint32_t first_sc, n_sc;     // rank-0 intermediates (data offsets)
+  uint32_t first_sg, n_sg;     // rank-0 gate inputs (kind | idx << 8 | slot << 16)
+  double2 cst;
+  uint32_t sh;                 // log2 sets per warp
+  int32_t gidx;
+  uint32_t n_elems;            // peak live data elements
+  uint32_t pad;
+};
+struct SMFBucket {
+  uint32_t out_off, first_op;
+  uint16_t R, n_ops;
+  uint32_t pad;
+};
+static_assert(sizeof(SMFNet) == 64 && sizeof(SMFBucket) == 16, "smf layouts");
+
+struct SetMajor {
+  int32_t n_nets = 0, n_total = 0, n_levels = 0;
+  uint64_t total_elems = 0;
+  std::vector<uint32_t> level_first;   // bucket index of each level start (+ end)
+  std::vector<uint32_t> level_blocks;  // CTAs per level
+  SMBucketDev* d_bk = nullptr;
+  uint32_t* d_prefix = nullptr;        // per bucket: CTA prefix within its level (+1 per level)
+  std::vector<uint32_t> prefix_first;  // index into d_prefix of each level
+  SMOpDev* d_ops = nullptr;
+  uint32_t* d_tabs = nullptr;          // data ops: i0 | i1 << 16 per output element
+  double* d_gco = nullptr;             // gen ops: (a, u, w) x (v = 0, 1) per output element
+  uint64_t* d_base = nullptr;
+  SMParam* d_params = nullptr;
+  int32_t n_params = 0;
+  double2* d_const = nullptr;          // per net: 2^n_empty * rank-0 inputs
+  uint32_t* d_scal_first = nullptr;
+  uint32_t* d_scal_off = nullptr;
+  uint32_t* d_sgen_first = nullptr;    // per net: rank-0 gate inputs (all vars sliced)
+  uint32_t* d_sgen = nullptr;          // kind | full index << 8 | param << 16
+  int32_t* d_gidx = nullptr;
+  // fused form
+  bool fused_ok = false;
+  int64_t f_smem = 0;                  // dynamic shared memory per warp-CTA
+  std::vector<uint32_t> f_sh;          // per fused net (unit order)
+  SMFNet* d_fnets = nullptr;
+  SMFBucket* d_fbk = nullptr;
+  SMOpDev* d_fops = nullptr;
+  uint32_t* d_ftabs = nullptr;
+  SMParam* d_fpar = nullptr;
+  uint32_t* d_fsc = nullptr;
+  uint32_t* d_fsg = nullptr;
+  std::map<int32_t, std::pair<uint32_t*, uint32_t>> f_prefix;  // n_sets -> (unit prefix, units)
+};
+
+static bool fused_on(const SetMajor* S) {
+  const char* v = getenv("QTN_SETMAJOR_FUSED");
+  return S->fused_ok && v && v[0] == '1';  // opt-in: slower than the level form on config 2/3
+}
+
+namespace {
+
+// Gate entry as an affine form of the phase ph = e^{-i t}:
+// entry = (a + u * ph.x, w * ph.y)  (host mirror of gate_entry below).
+struct GateCoef {
+  double a, u, w;
+};
+GateCoef gate_coef(uint32_t kind, uint32_t i) {
+  const double s = 0.70710678118654757;
+  const uint32_t row = i >> 2, col = i & 3;
+  switch (kind) {
+    case QTN_GATE_INIT: return {i == 0 ? 1.0 : 0.0, 0.0, 0.0};
+    case QTN_GATE_H: return {i == 3 ? -s : s, 0.0, 0.0};
+    case QTN_GATE_ZPOW: return i == 0 ? GateCoef{1.0, 0.0, 0.0} : (i == 3 ? GateCoef{0.0, 1.0, 1.0} : GateCoef{0.0, 0.0, 0.0});
+    case QTN_GATE_ZPOW_DIAG: return i == 0 ? GateCoef{1.0, 0.0, 0.0} : GateCoef{0.0, 1.0, 1.0};
+    case QTN_GATE_XPOW: return (i == 0 || i == 3) ? GateCoef{0.5, 0.5, 0.5} : GateCoef{0.5, -0.5, -0.5};
+    case QTN_GATE_CNOT: return {col == (row < 2 ? row : (row ^ 1)) ? 1.0 : 0.0, 0.0, 0.0};
+    case QTN_GATE_ZZ:
+      if (row != col) return {0.0, 0.0, 0.0};
+      return (row == 0 || row == 3) ? GateCoef{0.0, 1.0, -1.0} : GateCoef{0.0, 1.0, 1.0};
+    case QTN_GATE_ZZ_DIAG: return (i == 0 || i == 3) ? GateCoef{0.0, 1.0, -1.0} : GateCoef{0.0, 1.0, 1.0};
+    case QTN_GATE_SCALAR: return {0.0, 1.0, 1.0};
+  }
+  return {0.0, 0.0, 0.0};
+}
+
+template <typename T>
+int upload_vec(T** dst, const std::vector<T>& v) {
+  int rc = device_alloc((void**)dst, std::max<size_t>(v.size(), 1) * sizeof(T));
+  if (rc) return rc;
+  if (!v.empty()) rc = h2d(*dst, v.data(), v.size() * sizeof(T));
+  return rc;
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+// Gate entry from the phase ph = e^{-i t} (same conventions as the SMEM
+// executor's generator).
+__device__ __forceinline__ double2 gate_entry(uint32_t kind, uint32_t i, double2 ph) {
+  const double s = 0.70710678118654757;
+  switch (kind) {
+    case QTN_GATE_INIT: return make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+    case QTN_GATE_H: return make_double2(i == 3 ? -s : s, 0.0);
+    case QTN_GATE_ZPOW: return i == 0 ? make_double2(1.0, 0.0) : (i == 3 ? ph : make_double2(0.0, 0.0));
+    case QTN_GATE_ZPOW_DIAG: return i == 0 ? make_double2(1.0, 0.0) : ph;
+    case QTN_GATE_XPOW: {
+      const bool d = (i == 0 || i == 3);
+      return d ? make_double2(0.5 * (1.0 + ph.x), 0.5 * ph.y)
+               : make_double2(0.5 * (1.0 - ph.x), -0.5 * ph.y);
+    }
+    case QTN_GATE_CNOT: {
+      const uint32_t row = i >> 2, col = i & 3;
+      return make_double2(col == (row < 2 ? row : (row ^ 1)) ? 1.0 : 0.0, 0.0);
+    }
+    case QTN_GATE_ZZ: {
+      const uint32_t row = i >> 2, col = i & 3;
+      if (row != col) return make_double2(0.0, 0.0);
+      return (row == 0 || row == 3) ? make_double2(ph.x, -ph.y) : ph;
+    }
+    case QTN_GATE_ZZ_DIAG: return (i == 0 || i == 3) ? make_double2(ph.x, -ph.y) : ph;
+    case QTN_GATE_SCALAR: return ph;
+  }
+  return make_double2(0.0, 0.0);
+}
+
+__device__ __forceinline__ double2 phase_of(const SMParam& q, const double* __restrict__ row) {
+  if (q.angle == -2) return make_double2(q.scale, q.offset);
+  const double t = q.angle >= 0 ? q.scale * row[q.angle] + q.offset : q.offset;
+  double sn, cs;
+  sincos(t, &sn, &cs);
+  return make_double2(cs, -sn);
+}
+
+// Fused set-major executor: one 32-thread CTA = one (network, tile of S sets).
+// Lane = (group g, set s); the G = 32/S groups split each bucket's output
+// elements, the S lanes of a group read/write S consecutive sets of one
+// element (S*16 contiguous bytes of shared memory).
+__global__ void __launch_bounds__(32) smf_kernel(
+    const SMFNet* __restrict__ nets, const uint32_t* __restrict__ prefix, int n_nets,
+    const SMFBucket* __restrict__ bks, const SMOpDev* __restrict__ ops,
+    const uint32_t* __restrict__ tabs, const SMParam* __restrict__ par,
+    const uint32_t* __restrict__ sc, const uint32_t* __restrict__ sg,
+    const double* __restrict__ angles, int n_angles, int A, int n_total,
+    double2* __restrict__ results) {
+  extern __shared__ double2 smf[];
+  const uint32_t u = blockIdx.x;
+  uint32_t lo = 0, hi = n_nets;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (prefix[mid] <= u) lo = mid;
+    else hi = mid;
+  }
+  const SMFNet& net = nets[lo];
+  const uint32_t sh = net.sh, S = 1u << sh, G = 32u >> sh;
+  const uint32_t lane = threadIdx.x, s = lane & (S - 1), g = lane >> sh;
+  const int set = (int)((u - prefix[lo]) * S + s);
+  const bool valid = set < A;
+  const double* row = angles + (int64_t)(valid ? set : A - 1) * n_angles;
+  double2* ph = smf;
+  double2* data = smf + net.n_par * S;
+  for (uint32_t p = g; p < net.n_par; p += G) ph[p * S + s] = phase_of(par[net.first_par + p], row);
+  __syncwarp();
+  for (uint32_t b = 0; b < net.n_bk; ++b) {
+    const SMFBucket bk = bks[net.first_bk + b];
+    const uint32_t ne = 1u << bk.R;
+    for (uint32_t e = g; e < ne; e += G) {
+      double2 a0, a1;
+      for (uint32_t k = 0; k < bk.n_ops; ++k) {
+        const SMOpDev o = ops[bk.first_op + k];
+        const uint32_t t = __ldg(tabs + o.tab + e);
+        const uint32_t i0 = t & 0xffffu, i1 = t >> 16;
+        double2 x, y;
+        if (o.gen) {
+          const double2 pp = ph[o.param * S + s];
+          x = gate_entry(o.kind, i0, pp);
+          y = gate_entry(o.kind, i1, pp);
+        } else {
+          x = data[(o.off + i0) * S + s];
+          y = data[(o.off + i1) * S + s];
+        }
+        if (k == 0) {
+          a0 = x;
+          a1 = y;
+        } else {
+          a0 = cmul(a0, x);
+          a1 = cmul(a1, y);
+        }
+      }
+      data[(bk.out_off + e) * S + s] = make_double2(a0.x + a1.x, a0.y + a1.y);
+    }
+    __syncwarp();
+  }
+  if (g == 0 && valid) {
+    double2 r = net.cst;
+    for (uint32_t k = 0; k < net.n_sc; ++k) r = cmul(r, data[sc[net.first_sc + k] * S + s]);
+    for (uint32_t k = 0; k < net.n_sg; ++k) {
+      const uint32_t q = sg[net.first_sg + k];
+      r = cmul(r, gate_entry(q & 0xff, (q >> 8) & 0xff, ph[(q >> 16) * S + s]));
+    }
+    results[(int64_t)set * n_total + net.gidx] = r;
+  }
+}
+
+__global__ void sm_phase_kernel(const SMParam* __restrict__ par, int n_params,
+                                const double* __restrict__ angles, int n_angles, int A,
+                                double2* __restrict__ ph) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  if (s >= A || k >= n_params) return;
+  const SMParam q = par[k];
+  double2 r;
+  if (q.angle == -2) {
+    r = make_double2(q.scale, q.offset);
+  } else {
+    const double t = q.angle >= 0 ? q.scale * angles[(int64_t)s * n_angles + q.angle] + q.offset
+                                  : q.offset;
+    double sn, cs;
+    sincos(t, &sn, &cs);
+    r = make_double2(cs, -sn);
+  }
+  ph[(int64_t)k * A + s] = r;
+}
+
+// One CTA per (bucket, output element) of the level; each thread carries J
+// sets (stride 128) through the operand loop, so the per-operand uniform work
+// (record, index pair, gate coefficients) is paid once per J sets.
+template <int J>
+__global__ void __launch_bounds__(128) sm_level_kernel(
+    const SMBucketDev* __restrict__ bk, const uint32_t* __restrict__ prefix, uint32_t nb,
+    const SMOpDev* __restrict__ ops, const uint32_t* __restrict__ tabs,
+    const double* __restrict__ gco, const uint64_t* __restrict__ base,
+    const double2* __restrict__ ph, double2* ws, int A) {
+  const uint32_t blk = blockIdx.x;
+  uint32_t lo = 0, hi = nb;  // last prefix <= blk
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (prefix[mid] <= blk) lo = mid;
+    else hi = mid;
+  }
+  const SMBucketDev b = bk[lo];
+  const uint32_t e = blk - prefix[lo];
+  const uint64_t nb0 = base[b.net];
+  const SMOpDev* bo = ops + b.first_op;
+  for (int s0 = threadIdx.x; s0 < A; s0 += 128 * J) {
+    double2 a0[J], a1[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) a0[j] = a1[j] = make_double2(1.0, 0.0);
+    for (uint32_t k = 0; k < b.n_ops; ++k) {
+      const SMOpDev o = bo[k];
+      if (o.gen) {
+        const double* c = gco + (size_t)(o.tab + e) * 6;
+        const double ca0 = c[0], cu0 = c[1], cw0 = c[2], ca1 = c[3], cu1 = c[4], cw1 = c[5];
+        const double2* pp = ph + (int64_t)o.param * A + s0;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          if (s0 + j * 128 < A) {
+            const double2 p = pp[j * 128];
+            a0[j] = cmul(a0[j], make_double2(fma(cu0, p.x, ca0), cw0 * p.y));
+            a1[j] = cmul(a1[j], make_double2(fma(cu1, p.x, ca1), cw1 * p.y));
+          }
+        }
+      } else {
+        const uint32_t t = tabs[o.tab + e];
+        const double2* px = ws + (nb0 + o.off + (t & 0xffffu)) * A + s0;
+        const double2* py = ws + (nb0 + o.off + (t >> 16)) * A + s0;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          if (s0 + j * 128 < A) {
+            a0[j] = cmul(a0[j], px[j * 128]);
+            a1[j] = cmul(a1[j], py[j * 128]);
+          }
+        }
+      }
+    }
+    double2* out = ws + (nb0 + b.out_off + e) * A + s0;
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (s0 + j * 128 < A) out[j * 128] = make_double2(a0[j].x + a1[j].x, a0[j].y + a1[j].y);
+  }
+}
+
+__global__ void sm_fold_kernel(const double2* __restrict__ cst, const uint32_t* __restrict__ first,
+                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ gfirst,
+                               const uint32_t* __restrict__ gen, const uint64_t* __restrict__ base,
+                               const int32_t* __restrict__ gidx, int n_nets, int n_total,
+                               const double2* __restrict__ ph, const double2* ws, int A,
+                               double2* __restrict__ results) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = blockIdx.y;
+  if (s >= A || n >= n_nets) return;
+  double2 r = cst[n];
+  for (uint32_t k = first[n]; k < first[n + 1]; ++k) r = cmul(r, ws[(base[n] + off[k]) * A + s]);
+  for (uint32_t k = gfirst[n]; k < gfirst[n + 1]; ++k) {
+    const uint32_t g = gen[k];
+    r = cmul(r, gate_entry(g & 0xff, (g >> 8) & 0xff, ph[(int64_t)(g >> 16) * A + s]));
+  }
+  results[(int64_t)s * n_total + gidx[n]] = r;
+}
+
+}  // namespace
+
+int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
+                   const std::vector<int32_t>& gidx, const qtn_tensor_recipe* rec,
+                   const int64_t* offsets, int32_t n_total) {
+  SetMajor* S = new SetMajor();
+  S->n_nets = (int32_t)plans.size();
+  S->n_total = n_total;
+  std::map<std::tuple<double, double, int32_t>, int32_t> pidx;
+  std::vector<SMParam> params;
+  auto param_of = [&](const qtn_tensor_recipe& q) -> int32_t {
+    SMParam p{};
+    if (q.kind == QTN_GATE_SCALAR) {
+      p.scale = q.scale;
+      p.offset = q.offset;
+      p.angle = -2;
+    } else {
+      const bool has_t = q.kind == QTN_GATE_ZPOW || q.kind == QTN_GATE_XPOW || q.kind == QTN_GATE_ZZ ||
+                         q.kind == QTN_GATE_ZPOW_DIAG || q.kind == QTN_GATE_ZZ_DIAG;
+      p.scale = has_t ? q.scale : 0.0;
+      p.offset = has_t ? q.offset : 0.0;
+      p.angle = has_t ? (q.angle >= 0 ? q.angle : -1) : -1;
+    }
+    auto key = std::make_tuple(p.scale, p.offset, p.angle);
+    auto it = pidx.find(key);
+    if (it != pidx.end()) return it->second;
+    const int32_t k = (int32_t)params.size();
+    params.push_back(p);
+    pidx.emplace(key, k);
+    return k;
+  };
+  // full (unsliced) index of kept entry j of recipe q
+  auto full_of = [](const qtn_tensor_recipe& q, uint32_t j) {
+    const int kept = __builtin_popcount(q.keep_mask);
+    uint32_t full = 0;
+    int kb = kept - 1;
+    for (int pos = 0; pos < q.full_rank; ++pos) {
+      const uint32_t bit = ((q.keep_mask >> pos) & 1) ? (j >> kb--) & 1 : (q.fixed_bits >> pos) & 1;
+      full = (full << 1) | bit;
+    }
+    return full;
+  };
+  int32_t max_lev = 0;
+  for (auto* P : plans) max_lev = std::max(max_lev, P->sm_levels);
+  S->n_levels = max_lev;
+  std::vector<uint64_t> base;
+  std::vector<double2> cst;
+  std::vector<uint32_t> scal_first, scal_off, sgen_first, sgen;
+  uint64_t elems = 0;
+  for (size_t k = 0; k < plans.size(); ++k) {
+    const qtn_plan* P = plans[k];
+    base.push_back(elems);
+    elems += P->sm_elems;
+    double re = std::ldexp(1.0, P->n_empty), im = 0.0;
+    sgen_first.push_back((uint32_t)sgen.size());
+    for (int32_t id : P->sm_scalar_in) {
+      const qtn_tensor_recipe& q = rec[offsets[gidx[k]] + id];
+      if (q.kind != QTN_GATE_SCALAR) {
+        // a gate whose variables are all sliced: one angle-dependent entry
+        sgen.push_back((uint32_t)q.kind | (full_of(q, 0) << 8) | ((uint32_t)param_of(q) << 16));
+        continue;
+      }
+      const double nr = re * q.scale - im * q.offset, ni = re * q.offset + im * q.scale;
+      re = nr;
+      im = ni;
+    }
+    cst.push_back(make_double2(re, im));
+    scal_first.push_back((uint32_t)scal_off.size());
+    for (uint32_t o : P->sm_scalar_off) scal_off.push_back(o);
+  }
+  scal_first.push_back((uint32_t)scal_off.size());
+  sgen_first.push_back((uint32_t)sgen.size());
+  S->total_elems = elems;
+  // level-major buckets over all networks
+  std::vector<SMBucketDev> bks;
+  std::vector<uint32_t> prefix;
+  std::vector<SMOpDev> ops;
+  std::vector<uint32_t> tabs;
+  std::vector<double> gco;
+  for (int32_t lev = 0; lev < max_lev; ++lev) {
+    S->level_first.push_back((uint32_t)bks.size());
+    S->prefix_first.push_back((uint32_t)prefix.size());
+    uint32_t acc = 0;
+    for (size_t k = 0; k < plans.size(); ++k) {
+      const qtn_plan* P = plans[k];
+      for (const auto& rb : P->sm_buckets) {
+        if (rb.level != lev) continue;
+        SMBucketDev d{};
+        d.net = (uint32_t)k;
+        d.out_off = rb.out_off;
+        d.first_op = (uint32_t)ops.size();
+        d.R = (uint8_t)rb.R;
+        d.n_ops = (uint8_t)rb.ops.size();
+        for (const auto& o : rb.ops) {
+          SMOpDev od{};
+          if (o.input >= 0) {
+            const qtn_tensor_recipe& q = rec[offsets[gidx[k]] + o.input];
+            od.tab = (uint32_t)(gco.size() / 6);
+            od.gen = 1;
+            od.kind = q.kind;
+            od.param = (uint16_t)param_of(q);
+            for (uint16_t j : o.idx) {
+              const GateCoef c = gate_coef(q.kind, full_of(q, j));
+              gco.push_back(c.a);
+              gco.push_back(c.u);
+              gco.push_back(c.w);
+            }
+          } else {
+            od.tab = (uint32_t)tabs.size();
+            od.off = o.off;
+            for (size_t e = 0; e < o.idx.size(); e += 2)
+              tabs.push_back((uint32_t)o.idx[e] | ((uint32_t)o.idx[e + 1] << 16));
+          }
+          ops.push_back(od);
+        }
+        bks.push_back(d);
+        prefix.push_back(acc);
+        acc += 1u << rb.R;
+      }
+    }
+    prefix.push_back(acc);
+    S->level_blocks.push_back(acc);
+  }
+  S->level_first.push_back((uint32_t)bks.size());
+
+  // ---- fused form: per network, liveness-packed offsets and local phase slots
+  std::vector<SMFNet> fnets;
+  std::vector<SMFBucket> fbk;
+  std::vector<SMOpDev> fops;
+  std::vector<uint32_t> ftabs, fsc, fsg;
+  std::vector<SMParam> fpar;
+  std::vector<uint64_t> fcost;
+  const char* bv = getenv("QTN_SMF_BUDGET");
+  const int64_t budget = bv ? atoll(bv) : 32768;
+  const int64_t kMaxSmem = 227 * 1024;
+  int64_t need_max = 0;
+  bool fused_ok = true;
+  for (size_t k = 0; k < plans.size() && fused_ok; ++k) {
+    const qtn_plan* P = plans[k];
+    SMFNet fn{};
+    fn.first_bk = (uint32_t)fbk.size();
+    fn.first_par = (uint32_t)fpar.size();
+    std::map<int32_t, uint32_t> slot;  // global param -> local slot
+    auto slot_of = [&](const qtn_tensor_recipe& q) -> uint32_t {
+      const int32_t gp = param_of(q);
+      auto it = slot.find(gp);
+      if (it != slot.end()) return it->second;
+      const uint32_t sl = (uint32_t)slot.size();
+      slot.emplace(gp, sl);
+      fpar.push_back(params[gp]);
+      return sl;
+    };
+    // first-fit allocator over data elements; an output is allocated before
+    // its operands are released, so a bucket never overwrites what it reads
+    std::vector<uint8_t> used;
+    std::vector<uint32_t> remap(P->sm_elems + 1, 0), rsize(P->sm_elems + 1, 0);
+    uint32_t peak = 0;
+    auto alloc = [&](uint32_t n) {
+      uint32_t a = 0;
+      for (;;) {
+        uint32_t r = 0;
+        while (r < n && a + r < used.size() && !used[a + r]) ++r;
+        if (r == n || a + r >= used.size()) break;
+        a += r + 1;
+      }
+      if (a + n > used.size()) used.resize(a + n, 0);
+      for (uint32_t i = 0; i < n; ++i) used[a + i] = 1;
+      peak = std::max(peak, a + n);
+      return a;
+    };
+    uint64_t cost = 0;
+    for (const auto& rb : P->sm_buckets) {
+      SMFBucket d{};
+      const uint32_t n = 1u << rb.R;
+      d.out_off = alloc(n);
+      remap[rb.out_off] = d.out_off;
+      rsize[rb.out_off] = n;
+      d.first_op = (uint32_t)fops.size();
+      d.R = (uint16_t)rb.R;
+      d.n_ops = (uint16_t)rb.ops.size();
+      cost += (uint64_t)n * rb.ops.size();
+      for (const auto& o : rb.ops) {
+        SMOpDev od{};
+        od.tab = (uint32_t)ftabs.size();
+        if (o.input >= 0) {
+          const qtn_tensor_recipe& q = rec[offsets[gidx[k]] + o.input];
+          od.gen = 1;
+          od.kind = q.kind;
+          od.param = (uint16_t)slot_of(q);
+          for (size_t e = 0; e < o.idx.size(); e += 2)
+            ftabs.push_back(full_of(q, o.idx[e]) | (full_of(q, o.idx[e + 1]) << 16));
+        } else {
+          od.off = remap[o.off];
+          for (size_t e = 0; e < o.idx.size(); e += 2)
+            ftabs.push_back((uint32_t)o.idx[e] | ((uint32_t)o.idx[e + 1] << 16));
+        }
+        fops.push_back(od);
+      }
+      for (const auto& o : rb.ops)
+        if (o.input < 0)
+          for (uint32_t i = 0; i < rsize[o.off]; ++i) used[remap[o.off] + i] = 0;
+      fbk.push_back(d);
+    }
+    fn.n_bk = (uint32_t)(fbk.size() - fn.first_bk);
+    fn.first_sc = (uint32_t)fsc.size();
+    for (uint32_t o : P->sm_scalar_off) fsc.push_back(remap[o]);
+    fn.n_sc = (uint32_t)(fsc.size() - fn.first_sc);
+    fn.first_sg = (uint32_t)fsg.size();
+    double re = std::ldexp(1.0, P->n_empty), im = 0.0;
+    for (int32_t id : P->sm_scalar_in) {
+      const qtn_tensor_recipe& q = rec[offsets[gidx[k]] + id];
+      if (q.kind != QTN_GATE_SCALAR) {
+        fsg.push_back((uint32_t)q.kind | (full_of(q, 0) << 8) | (slot_of(q) << 16));
+        continue;
+      }
+      const double nr = re * q.scale - im * q.offset, ni = re * q.offset + im * q.scale;
+      re = nr;
+      im = ni;
+    }
+    fn.n_sg = (uint32_t)(fsg.size() - fn.first_sg);
+    fn.cst = make_double2(re, im);
+    fn.n_par = (uint32_t)slot.size();
+    fn.n_elems = peak;
+    fn.gidx = gidx[k];
+    const int64_t per_set = (int64_t)(peak + fn.n_par) * 16;
+    uint32_t sh = 5;
+    while (sh > 0 && per_set * (1 << sh) > budget) --sh;
+    fn.sh = sh;
+    need_max = std::max(need_max, per_set << sh);
+    if (need_max > kMaxSmem || fn.n_par > 65535) fused_ok = false;
+    fnets.push_back(fn);
+    fcost.push_back(cost);
+  }
+  if (fused_ok && !fnets.empty()) {
+    // heaviest units first (work per unit ~ cost * S / min(32, ...)): sort by
+    // per-set cost, stable
+    std::vector<size_t> perm(fnets.size());
+    for (size_t i = 0; i < perm.size(); ++i) perm[i] = i;
+    std::stable_sort(perm.begin(), perm.end(), [&](size_t a, size_t b) {
+      return (fcost[a] << fnets[a].sh) > (fcost[b] << fnets[b].sh);
+    });
+    std::vector<SMFNet> sorted;
+    for (size_t i : perm) sorted.push_back(fnets[i]);
+    fnets.swap(sorted);
+    for (const auto& fn : fnets) S->f_sh.push_back(fn.sh);
+    S->f_smem = need_max;
+    int rc;
+    if ((rc = upload_vec(&S->d_fnets, fnets)) || (rc = upload_vec(&S->d_fbk, fbk)) ||
+        (rc = upload_vec(&S->d_fops, fops)) || (rc = upload_vec(&S->d_ftabs, ftabs)) ||
+        (rc = upload_vec(&S->d_fpar, fpar)) || (rc = upload_vec(&S->d_fsc, fsc)) ||
+        (rc = upload_vec(&S->d_fsg, fsg))) {
+      setmajor_destroy(S);
+      return rc;
+    }
+    S->fused_ok = true;
+  }
+
+  if (params.size() > 65535) {
+    delete S;
+    set_error("set-major executor: too many gate parameters");
+    return QTN_EINVAL;
+  }
+  S->n_params = (int32_t)params.size();
+  int rc;
+  if ((rc = upload_vec(&S->d_bk, bks)) || (rc = upload_vec(&S->d_prefix, prefix)) ||
+      (rc = upload_vec(&S->d_ops, ops)) || (rc = upload_vec(&S->d_tabs, tabs)) ||
+      (rc = upload_vec(&S->d_gco, gco)) ||
+      (rc = upload_vec(&S->d_base, base)) || (rc = upload_vec(&S->d_params, params)) ||
+      (rc = upload_vec(&S->d_const, cst)) || (rc = upload_vec(&S->d_scal_first, scal_first)) ||
+      (rc = upload_vec(&S->d_scal_off, scal_off)) || (rc = upload_vec(&S->d_sgen_first, sgen_first)) ||
+      (rc = upload_vec(&S->d_sgen, sgen)) ||
+      (rc = upload_vec(&S->d_gidx, std::vector<int32_t>(gidx.begin(), gidx.end())))) {
+    setmajor_destroy(S);
+    return rc;
+  }
+  *out = S;
+  return QTN_OK;
+}
+
+int64_t setmajor_workspace(const SetMajor* S, int32_t n_sets) {
+  if (fused_on(S)) return 256;
+  return (int64_t)(S->total_elems + (uint64_t)S->n_params) * n_sets * 16 + 256;
+}
+
+int setmajor_launches(const SetMajor* S) {
+  if (fused_on(S)) return 1;
+  int c = 2;  // phases + fold
+  for (uint32_t b : S->level_blocks) c += b ? 1 : 0;
+  return c;
+}
+
+int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_sets,
+                 void* workspace, void* results, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (fused_on(S)) {
+    auto it = S->f_prefix.find(n_sets);
+    if (it == S->f_prefix.end()) {
+      std::vector<uint32_t> pre;
+      uint32_t acc = 0;
+      for (uint32_t sh : S->f_sh) {
+        pre.push_back(acc);
+        acc += (uint32_t)((n_sets + (1 << sh) - 1) >> sh);
+      }
+      uint32_t* d = nullptr;
+      int rc = upload_vec(&d, pre);
+      if (rc) return rc;
+      it = S->f_prefix.emplace(n_sets, std::make_pair(d, acc)).first;
+    }
+    static int64_t attr_set = -1;
+    if (attr_set < S->f_smem) {
+      cudaFuncSetAttribute(smf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->f_smem);
+      attr_set = S->f_smem;
+    }
+    smf_kernel<<<it->second.second, 32, S->f_smem, st>>>(
+        S->d_fnets, it->second.first, S->n_nets, S->d_fbk, S->d_fops, S->d_ftabs, S->d_fpar,
+        S->d_fsc, S->d_fsg, angles, n_angles, n_sets, S->n_total,
+        reinterpret_cast<double2*>(results));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_error(std::string("set-major fused executor launch: ") + cudaGetErrorString(e));
+      return QTN_ECUDA;
+    }
+    return QTN_OK;
+  }
+  double2* ws = reinterpret_cast<double2*>(workspace);
+  double2* ph = ws + S->total_elems * (uint64_t)n_sets;
+  {
+    dim3 g((n_sets + 127) / 128, std::max(S->n_params, 1));
+    sm_phase_kernel<<<g, 128, 0, st>>>(S->d_params, S->n_params, angles, n_angles, n_sets, ph);
+  }
+  for (int32_t lev = 0; lev < S->n_levels; ++lev) {
+    const uint32_t blocks = S->level_blocks[lev];
+    if (!blocks) continue;
+    const uint32_t b0 = S->level_first[lev], nb = S->level_first[lev + 1] - b0;
+    const SMBucketDev* bk = S->d_bk + b0;
+    const uint32_t* pre = S->d_prefix + S->prefix_first[lev];
+    if (n_sets > 256)
+      sm_level_kernel<4><<<blocks, 128, 0, st>>>(bk, pre, nb, S->d_ops, S->d_tabs, S->d_gco,
+                                                 S->d_base, ph, ws, n_sets);
+    else if (n_sets > 128)
+      sm_level_kernel<2><<<blocks, 128, 0, st>>>(bk, pre, nb, S->d_ops, S->d_tabs, S->d_gco,
+                                                 S->d_base, ph, ws, n_sets);
+    else
+      sm_level_kernel<1><<<blocks, 128, 0, st>>>(bk, pre, nb, S->d_ops, S->d_tabs, S->d_gco,
+                                                 S->d_base, ph, ws, n_sets);
+  }
+  {
+    dim3 g((n_sets + 127) / 128, S->n_nets);
+    sm_fold_kernel<<<g, 128, 0, st>>>(S->d_const, S->d_scal_first, S->d_scal_off, S->d_sgen_first,
+                                      S->d_sgen, S->d_base, S->d_gidx, S->n_nets, S->n_total, ph,
+                                      ws, n_sets,
+                                      reinterpret_cast<double2*>(results));
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("set-major executor launch: ") + cudaGetErrorString(e));
+    return QTN_ECUDA;
+  }
+  return QTN_OK;
+}
+
+void setmajor_destroy(SetMajor* S) {
+  if (!S) return;
+  for (void* p : {(void*)S->d_bk, (void*)S->d_prefix, (void*)S->d_ops, (void*)S->d_tabs, (void*)S->d_gco,
+                  (void*)S->d_base, (void*)S->d_params, (void*)S->d_const, (void*)S->d_scal_first,
+                  (void*)S->d_scal_off, (void*)S->d_sgen_first, (void*)S->d_sgen, (void*)S->d_gidx,
+                  (void*)S->d_fnets, (void*)S->d_fbk, (void*)S->d_fops, (void*)S->d_ftabs,
+                  (void*)S->d_fpar, (void*)S->d_fsc, (void*)S->d_fsg})
+    device_free(p);
+  for (auto& kv : S->f_prefix) device_free(kv.second.first);
+  delete S;
+}
+
+}  // namespace qtn

@@ -184,11 +184,10 @@ class EnergyPlan:
             )
         return self._bufs[n_sets]
 
-    @property
-    def launches_per_eval(self) -> int:
+    def launches_per_eval(self, n_sets: int = 1) -> int:
         """Kernel launches of one evaluation (executors + energy reduction)."""
         self._prepare()
-        return self._batch.launches + 1 + (0 if self.fused else 1)
+        return self._batch.launches_for(n_sets) + 1 + (0 if self.fused else 1)
 
     def launch(self, angles_dev, stream=None):
         """Enqueue one evaluation for every angle set in `angles_dev`
@@ -213,7 +212,7 @@ class EnergyPlan:
         N.check(N.lib.qtn_energy_reduce(b["res"].data_ptr(), self._weights.data_ptr(),
                                         len(self.jobs), n_sets, b["energy"].data_ptr(), None, sp),
                 "energy")
-        self.launches = self.launches_per_eval
+        self.launches = self.launches_per_eval(n_sets)
         return b
 
     def energies(self, angle_sets) -> np.ndarray:

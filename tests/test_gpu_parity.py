@@ -2,6 +2,7 @@
 the golden vectors produced by the real reference (tests/golden)."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -240,11 +241,65 @@ def test_fused_and_unfused_generation_agree(golden):
     G3 = golden("config3.json")
     g3 = Q.random_regular_graph(244, 3, 0)
     p3 = Q.EnergyPlan(g3, 3, "default", dtype="complex128", edge_ids=[0, 23])
-    f3 = p3.energies(rng.uniform(0, math.pi, (3, 6)))
+    s3 = rng.uniform(0, math.pi, (3, 6))
+    f3 = p3.energies(s3)
     p3.fused = False
     p3._bufs.clear()
-    u3 = p3.energies(rng.uniform(0, math.pi, (3, 6)))
-    assert f3.shape == u3.shape
+    u3 = p3.energies(s3)
+    assert np.allclose(f3, u3, rtol=0, atol=1e-11)
+
+
+@pytest.fixture
+def setmajor_min_sets(monkeypatch):
+    """Switch the set-major executor threshold (read per call by the library)."""
+    def set_(n):
+        monkeypatch.setenv("QTN_SETMAJOR_MIN_SETS", str(n))
+    return set_
+
+
+@pytest.mark.parametrize("mode,slice_k", [("zz+diagonal", 0), ("zz+diagonal", 1), ("default", 0)])
+def test_setmajor_matches_warp_executor(golden, setmajor_min_sets, mode, slice_k):
+    """Set-major streaming executor (many angle sets) == warp-resident SMEM
+    executor, every gate kind, sliced networks with rank-0 gate inputs."""
+    rng = np.random.default_rng(11)
+    if mode == "default":
+        graph, p, ids = Q.random_regular_graph(244, 3, 0), 3, None
+        # default-mode config-3 networks that fit the warp executor
+        sets = rng.uniform(0, math.pi, (70, 6))
+        plan = Q.EnergyPlan(graph, p, mode, dtype="complex128", edge_ids=list(range(0, 366, 7)))
+    else:
+        graph, p = Q.random_regular_graph(100, 3, 0), 2
+        sets = rng.uniform(0, math.pi, (70, 4))
+        plan = Q.EnergyPlan(graph, p, mode, dtype="complex128", slice_k=slice_k)
+    setmajor_min_sets(0)
+    warp = plan.energies(sets)
+    for fused in ("1", "0"):  # warp-per-tile fused form, level-synchronous form
+        os.environ["QTN_SETMAJOR_FUSED"] = fused
+        try:
+            plan._bufs.clear()
+            setmajor_min_sets(1)
+            sm = plan.energies(sets)
+            assert plan.launches == plan.launches_per_eval(len(sets))
+        finally:
+            del os.environ["QTN_SETMAJOR_FUSED"]
+        assert np.allclose(sm, warp, rtol=1e-12, atol=1e-11), (fused, np.abs(sm - warp).max())
+
+
+def test_setmajor_vs_oracle(golden, setmajor_min_sets):
+    """Set-major executor against the oracle at each angle set, including a
+    set count that is not a multiple of 32."""
+    setmajor_min_sets(1)
+    G = golden("config2.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    edges = [tuple(e) for e in G["edges"]]
+    plan = Q.EnergyPlan(graph, 2, "zz+diagonal", edge_ids=list(range(0, 150, 15)))
+    rng = np.random.default_rng(17)
+    sets = rng.uniform(0, math.pi, (37, 4))
+    got = plan.energies(sets)
+    for s in (0, 1, 31, 32, 36):
+        g, b = list(sets[s, :2]), list(sets[s, 2:])
+        zz = [O.edge_zz(100, edges, edges[e], g, b, "zz+diagonal") for e in plan.edge_ids]
+        assert abs(got[s] - O.energy_from_zz(zz)) < 1e-10
 
 
 # ---------------------------------------------------------------- amplitudes
