@@ -751,7 +751,7 @@ static bool use_setmajor(const qtn_batch* B, int32_t n_sets);
 extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* out) {
   if (!B || !out) return QTN_EINVAL;
   int c = B->n_smem ? 1 : 0;
-  if (B->n_smem && use_setmajor(B, n_sets)) c = qtn::setmajor_launches(B->sm);
+  if (B->n_smem && use_setmajor(B, n_sets)) c = qtn::setmajor_launches(B->sm, n_sets);
   if (B->n_hbm) {
     for (uint64_t t : B->level_tiles) c += t ? 1 : 0;
     c += 1;

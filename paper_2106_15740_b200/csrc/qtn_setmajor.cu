@@ -73,14 +73,9 @@ static_assert(sizeof(SMFNet) == 64 && sizeof(SMFBucket) == 16, "smf layouts");
 struct SetMajor {
   int32_t n_nets = 0, n_total = 0, n_levels = 0;
   uint64_t total_elems = 0;
-  std::vector<uint32_t> level_first;   // bucket index of each level start (+ end)
   std::vector<uint32_t> level_blocks;  // CTAs per level
-  SMBucketDev* d_bk = nullptr;
-  uint32_t* d_prefix = nullptr;        // per bucket: CTA prefix within its level (+1 per level)
-  std::vector<uint32_t> prefix_first;  // index into d_prefix of each level
-  SMOpDev* d_ops = nullptr;
-  uint32_t* d_tabs = nullptr;          // data ops: i0 | i1 << 16 per output element
-  double* d_gco = nullptr;             // gen ops: (a, u, w) x (v = 0, 1) per output element
+  std::vector<uint32_t> level_rec;     // first CTA record of each level
+  uint32_t* d_recs = nullptr;          // kRecWords per CTA (see sm_level_kernel)
   uint64_t* d_base = nullptr;
   SMParam* d_params = nullptr;
   int32_t n_params = 0;
@@ -111,6 +106,8 @@ static bool fused_on(const SetMajor* S) {
 
 namespace {
 
+constexpr int kMaxOps = 8;  // operands per bucket in the set-major form
+
 // Gate entry as an affine form of the phase ph = e^{-i t}:
 // entry = (a + u * ph.x, w * ph.y)  (host mirror of gate_entry below).
 struct GateCoef {
@@ -133,6 +130,18 @@ GateCoef gate_coef(uint32_t kind, uint32_t i) {
     case QTN_GATE_SCALAR: return {0.0, 1.0, 1.0};
   }
   return {0.0, 0.0, 0.0};
+}
+
+// the distinct affine forms gate_coef produces (kGateCoef on device)
+constexpr int kNumCoef = 8;
+const double kCoefHost[kNumCoef][3] = {
+    {0.0, 0.0, 0.0}, {1.0, 0.0, 0.0}, {0.70710678118654757, 0.0, 0.0},
+    {-0.70710678118654757, 0.0, 0.0}, {0.0, 1.0, 1.0}, {0.0, 1.0, -1.0},
+    {0.5, 0.5, 0.5}, {0.5, -0.5, -0.5}};
+int coef_code(const GateCoef& c) {
+  for (int i = 0; i < kNumCoef; ++i)
+    if (kCoefHost[i][0] == c.a && kCoefHost[i][1] == c.u && kCoefHost[i][2] == c.w) return i;
+  return -1;
 }
 
 template <typename T>
@@ -274,61 +283,108 @@ __global__ void sm_phase_kernel(const SMParam* __restrict__ par, int n_params,
   ph[(int64_t)k * A + s] = r;
 }
 
-// One CTA per (bucket, output element) of the level; each thread carries J
-// sets (stride 128) through the operand loop, so the per-operand uniform work
-// (record, index pair, gate coefficients) is paid once per J sets.
+// ---- level kernel
+// One CTA per (bucket, output element e) of a level; 256 threads stream the
+// sets, J per thread per pass.  Everything the CTA needs is one fixed-size
+// record (a single dependent load): word 0 = absolute output element, word 1 =
+// operand count, then per operand two words —
+//   intermediate: absolute elements of entries idx(e, v=0) and idx(e, v=1);
+//   gate        : 0x80000000 | phase row, and the affine-coefficient codes of
+//                 its two entries (code0 | code1 << 8, see kGateCoef).
+// The operand loop stays rolled (~31-48 registers, full occupancy): the L2
+// round trip of each operand is hidden by resident warps, not by unrolling.
+constexpr int kRecWords = 2 + 2 * kMaxOps;
+
+__constant__ double kGateCoef[kNumCoef][3];
+
+struct OpSetup {
+  const double2* px;  // intermediate: row of entry v=0; gate: phase row
+  const double2* py;  // intermediate: row of entry v=1
+  double c[6];        // gate: (a, u, w) for v = 0, 1
+  int gen;
+  int pad;
+};
+
+// per-iteration shared-memory reads (asm volatile: not hoisted out of the set
+// loop, which would pin every operand's setup in registers)
+__device__ __forceinline__ uint64_t lds_u64(const void* p) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(const void* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
+
 template <int J>
-__global__ void __launch_bounds__(128) sm_level_kernel(
-    const SMBucketDev* __restrict__ bk, const uint32_t* __restrict__ prefix, uint32_t nb,
-    const SMOpDev* __restrict__ ops, const uint32_t* __restrict__ tabs,
-    const double* __restrict__ gco, const uint64_t* __restrict__ base,
-    const double2* __restrict__ ph, double2* ws, int A) {
-  const uint32_t blk = blockIdx.x;
-  uint32_t lo = 0, hi = nb;  // last prefix <= blk
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (prefix[mid] <= blk) lo = mid;
-    else hi = mid;
+__global__ void __launch_bounds__(256) sm_level_kernel(const uint32_t* __restrict__ recs,
+                                                       const double2* __restrict__ ph,
+                                                       double2* ws, int A) {
+  __shared__ OpSetup su[kMaxOps];
+  const uint32_t* r = recs + (size_t)blockIdx.x * kRecWords;
+  const uint2 hd = *reinterpret_cast<const uint2*>(r);
+  const int n = (int)hd.y;
+  if (threadIdx.x < n) {
+    const uint2 w = reinterpret_cast<const uint2*>(r + 2)[threadIdx.x];
+    OpSetup& u = su[threadIdx.x];
+    if (w.x & 0x80000000u) {
+      u.gen = 1;
+      u.px = u.py = ph + (size_t)(w.x & 0x7fffffffu) * A;
+      const uint32_t c0 = w.y & 0xff, c1 = w.y >> 8;
+      for (int i = 0; i < 3; ++i) {
+        u.c[i] = kGateCoef[c0][i];
+        u.c[3 + i] = kGateCoef[c1][i];
+      }
+    } else {
+      u.gen = 0;
+      u.px = ws + (size_t)w.x * A;
+      u.py = ws + (size_t)w.y * A;
+    }
   }
-  const SMBucketDev b = bk[lo];
-  const uint32_t e = blk - prefix[lo];
-  const uint64_t nb0 = base[b.net];
-  const SMOpDev* bo = ops + b.first_op;
-  for (int s0 = threadIdx.x; s0 < A; s0 += 128 * J) {
+  __syncthreads();
+  double2* out = ws + (size_t)hd.x * A;
+#pragma unroll 1
+  for (int s0 = threadIdx.x; s0 < A; s0 += 256 * J) {
     double2 a0[J], a1[J];
-#pragma unroll
-    for (int j = 0; j < J; ++j) a0[j] = a1[j] = make_double2(1.0, 0.0);
-    for (uint32_t k = 0; k < b.n_ops; ++k) {
-      const SMOpDev o = bo[k];
-      if (o.gen) {
-        const double* c = gco + (size_t)(o.tab + e) * 6;
-        const double ca0 = c[0], cu0 = c[1], cw0 = c[2], ca1 = c[3], cu1 = c[4], cw1 = c[5];
-        const double2* pp = ph + (int64_t)o.param * A + s0;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+      const double2* px = reinterpret_cast<const double2*>(lds_u64(&su[k].px));
+      double2 x[J], y[J];
+      if (su[k].gen) {
+        const double* c = su[k].c;
+        const double c0 = lds_f64(c), c1 = lds_f64(c + 1), c2 = lds_f64(c + 2);
+        const double c3 = lds_f64(c + 3), c4 = lds_f64(c + 4), c5 = lds_f64(c + 5);
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-          if (s0 + j * 128 < A) {
-            const double2 p = pp[j * 128];
-            a0[j] = cmul(a0[j], make_double2(fma(cu0, p.x, ca0), cw0 * p.y));
-            a1[j] = cmul(a1[j], make_double2(fma(cu1, p.x, ca1), cw1 * p.y));
-          }
+          const double2 p = s0 + 256 * j < A ? px[s0 + 256 * j] : make_double2(0.0, 0.0);
+          x[j] = make_double2(fma(c1, p.x, c0), c2 * p.y);
+          y[j] = make_double2(fma(c4, p.x, c3), c5 * p.y);
         }
       } else {
-        const uint32_t t = tabs[o.tab + e];
-        const double2* px = ws + (nb0 + o.off + (t & 0xffffu)) * A + s0;
-        const double2* py = ws + (nb0 + o.off + (t >> 16)) * A + s0;
+        const double2* py = reinterpret_cast<const double2*>(lds_u64(&su[k].py));
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-          if (s0 + j * 128 < A) {
-            a0[j] = cmul(a0[j], px[j * 128]);
-            a1[j] = cmul(a1[j], py[j * 128]);
-          }
+          const bool ok = s0 + 256 * j < A;
+          x[j] = ok ? px[s0 + 256 * j] : make_double2(0.0, 0.0);
+          y[j] = ok ? py[s0 + 256 * j] : make_double2(0.0, 0.0);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (k == 0) {
+          a0[j] = x[j];
+          a1[j] = y[j];
+        } else {
+          a0[j] = cmul(a0[j], x[j]);
+          a1[j] = cmul(a1[j], y[j]);
         }
       }
     }
-    double2* out = ws + (nb0 + b.out_off + e) * A + s0;
 #pragma unroll
     for (int j = 0; j < J; ++j)
-      if (s0 + j * 128 < A) out[j * 128] = make_double2(a0[j].x + a1[j].x, a0[j].y + a1[j].y);
+      if (s0 + 256 * j < A) out[s0 + 256 * j] = make_double2(a0[j].x + a1[j].x, a0[j].y + a1[j].y);
   }
 }
 
@@ -423,57 +479,61 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
   scal_first.push_back((uint32_t)scal_off.size());
   sgen_first.push_back((uint32_t)sgen.size());
   S->total_elems = elems;
-  // level-major buckets over all networks
-  std::vector<SMBucketDev> bks;
-  std::vector<uint32_t> prefix;
-  std::vector<SMOpDev> ops;
-  std::vector<uint32_t> tabs;
-  std::vector<double> gco;
+  if (elems >= 0x80000000ull) {
+    delete S;
+    set_error("set-major executor: too many elements");
+    return QTN_EINVAL;
+  }
+  // level-major CTA records over all networks, heaviest buckets of a level first
+  std::vector<uint32_t> recs;
+  uint32_t n_cta = 0;
   for (int32_t lev = 0; lev < max_lev; ++lev) {
-    S->level_first.push_back((uint32_t)bks.size());
-    S->prefix_first.push_back((uint32_t)prefix.size());
+    S->level_rec.push_back(n_cta);
+    std::vector<std::tuple<uint64_t, size_t, const qtn_plan::SMBucketRec*>> lvb;
+    for (size_t k = 0; k < plans.size(); ++k)
+      for (const auto& rb : plans[k]->sm_buckets)
+        if (rb.level == lev) lvb.emplace_back(~((uint64_t)rb.ops.size() << rb.R), k, &rb);
+    std::stable_sort(lvb.begin(), lvb.end(),
+                     [](const auto& a, const auto& b) { return std::get<0>(a) < std::get<0>(b); });
     uint32_t acc = 0;
-    for (size_t k = 0; k < plans.size(); ++k) {
-      const qtn_plan* P = plans[k];
-      for (const auto& rb : P->sm_buckets) {
-        if (rb.level != lev) continue;
-        SMBucketDev d{};
-        d.net = (uint32_t)k;
-        d.out_off = rb.out_off;
-        d.first_op = (uint32_t)ops.size();
-        d.R = (uint8_t)rb.R;
-        d.n_ops = (uint8_t)rb.ops.size();
-        for (const auto& o : rb.ops) {
-          SMOpDev od{};
+    for (const auto& it : lvb) {
+      const size_t k = std::get<1>(it);
+      const auto& rb = *std::get<2>(it);
+      if (rb.ops.size() > (size_t)kMaxOps) {
+        delete S;
+        set_error("set-major executor: bucket with more than 8 operands");
+        return QTN_EINVAL;
+      }
+      for (uint32_t e = 0; e < (1u << rb.R); ++e) {
+        const size_t r0 = recs.size();
+        recs.resize(r0 + kRecWords, 0);
+        recs[r0] = (uint32_t)(base[k] + rb.out_off + e);
+        recs[r0 + 1] = (uint32_t)rb.ops.size();
+        for (size_t t = 0; t < rb.ops.size(); ++t) {
+          const auto& o = rb.ops[t];
+          const uint32_t i0 = o.idx[2 * e], i1 = o.idx[2 * e + 1];
           if (o.input >= 0) {
             const qtn_tensor_recipe& q = rec[offsets[gidx[k]] + o.input];
-            od.tab = (uint32_t)(gco.size() / 6);
-            od.gen = 1;
-            od.kind = q.kind;
-            od.param = (uint16_t)param_of(q);
-            for (uint16_t j : o.idx) {
-              const GateCoef c = gate_coef(q.kind, full_of(q, j));
-              gco.push_back(c.a);
-              gco.push_back(c.u);
-              gco.push_back(c.w);
+            const int c0 = coef_code(gate_coef(q.kind, full_of(q, i0)));
+            const int c1 = coef_code(gate_coef(q.kind, full_of(q, i1)));
+            if (c0 < 0 || c1 < 0) {
+              delete S;
+              set_error("set-major executor: unsupported gate coefficient");
+              return QTN_EINVAL;
             }
+            recs[r0 + 2 + 2 * t] = 0x80000000u | (uint32_t)param_of(q);
+            recs[r0 + 3 + 2 * t] = (uint32_t)c0 | ((uint32_t)c1 << 8);
           } else {
-            od.tab = (uint32_t)tabs.size();
-            od.off = o.off;
-            for (size_t e = 0; e < o.idx.size(); e += 2)
-              tabs.push_back((uint32_t)o.idx[e] | ((uint32_t)o.idx[e + 1] << 16));
+            recs[r0 + 2 + 2 * t] = (uint32_t)(base[k] + o.off + i0);
+            recs[r0 + 3 + 2 * t] = (uint32_t)(base[k] + o.off + i1);
           }
-          ops.push_back(od);
         }
-        bks.push_back(d);
-        prefix.push_back(acc);
-        acc += 1u << rb.R;
+        ++acc;
       }
     }
-    prefix.push_back(acc);
     S->level_blocks.push_back(acc);
+    n_cta += acc;
   }
-  S->level_first.push_back((uint32_t)bks.size());
 
   // ---- fused form: per network, liveness-packed offsets and local phase slots
   std::vector<SMFNet> fnets;
@@ -614,10 +674,16 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
   }
   S->n_params = (int32_t)params.size();
   int rc;
-  if ((rc = upload_vec(&S->d_bk, bks)) || (rc = upload_vec(&S->d_prefix, prefix)) ||
-      (rc = upload_vec(&S->d_ops, ops)) || (rc = upload_vec(&S->d_tabs, tabs)) ||
-      (rc = upload_vec(&S->d_gco, gco)) ||
-      (rc = upload_vec(&S->d_base, base)) || (rc = upload_vec(&S->d_params, params)) ||
+  static bool coef_up = false;
+  if (!coef_up) {
+    if (cudaMemcpyToSymbol(kGateCoef, kCoefHost, sizeof(kCoefHost)) != cudaSuccess) {
+      setmajor_destroy(S);
+      set_error("set-major executor: coefficient upload failed");
+      return QTN_ECUDA;
+    }
+    coef_up = true;
+  }
+  if ((rc = upload_vec(&S->d_recs, recs)) || (rc = upload_vec(&S->d_base, base)) || (rc = upload_vec(&S->d_params, params)) ||
       (rc = upload_vec(&S->d_const, cst)) || (rc = upload_vec(&S->d_scal_first, scal_first)) ||
       (rc = upload_vec(&S->d_scal_off, scal_off)) || (rc = upload_vec(&S->d_sgen_first, sgen_first)) ||
       (rc = upload_vec(&S->d_sgen, sgen)) ||
@@ -634,7 +700,7 @@ int64_t setmajor_workspace(const SetMajor* S, int32_t n_sets) {
   return (int64_t)(S->total_elems + (uint64_t)S->n_params) * n_sets * 16 + 256;
 }
 
-int setmajor_launches(const SetMajor* S) {
+int setmajor_launches(const SetMajor* S, int32_t n_sets) {
   if (fused_on(S)) return 1;
   int c = 2;  // phases + fold
   for (uint32_t b : S->level_blocks) c += b ? 1 : 0;
@@ -683,18 +749,11 @@ int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_
   for (int32_t lev = 0; lev < S->n_levels; ++lev) {
     const uint32_t blocks = S->level_blocks[lev];
     if (!blocks) continue;
-    const uint32_t b0 = S->level_first[lev], nb = S->level_first[lev + 1] - b0;
-    const SMBucketDev* bk = S->d_bk + b0;
-    const uint32_t* pre = S->d_prefix + S->prefix_first[lev];
-    if (n_sets > 256)
-      sm_level_kernel<4><<<blocks, 128, 0, st>>>(bk, pre, nb, S->d_ops, S->d_tabs, S->d_gco,
-                                                 S->d_base, ph, ws, n_sets);
-    else if (n_sets > 128)
-      sm_level_kernel<2><<<blocks, 128, 0, st>>>(bk, pre, nb, S->d_ops, S->d_tabs, S->d_gco,
-                                                 S->d_base, ph, ws, n_sets);
+    const uint32_t* r = S->d_recs + (size_t)S->level_rec[lev] * kRecWords;
+    if (n_sets >= 1024)
+      sm_level_kernel<2><<<blocks, 256, 0, st>>>(r, ph, ws, n_sets);
     else
-      sm_level_kernel<1><<<blocks, 128, 0, st>>>(bk, pre, nb, S->d_ops, S->d_tabs, S->d_gco,
-                                                 S->d_base, ph, ws, n_sets);
+      sm_level_kernel<1><<<blocks, 256, 0, st>>>(r, ph, ws, n_sets);
   }
   {
     dim3 g((n_sets + 127) / 128, S->n_nets);
@@ -713,8 +772,7 @@ int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_
 
 void setmajor_destroy(SetMajor* S) {
   if (!S) return;
-  for (void* p : {(void*)S->d_bk, (void*)S->d_prefix, (void*)S->d_ops, (void*)S->d_tabs, (void*)S->d_gco,
-                  (void*)S->d_base, (void*)S->d_params, (void*)S->d_const, (void*)S->d_scal_first,
+  for (void* p : {(void*)S->d_recs, (void*)S->d_base, (void*)S->d_params, (void*)S->d_const, (void*)S->d_scal_first,
                   (void*)S->d_scal_off, (void*)S->d_sgen_first, (void*)S->d_sgen, (void*)S->d_gidx,
                   (void*)S->d_fnets, (void*)S->d_fbk, (void*)S->d_fops, (void*)S->d_ftabs,
                   (void*)S->d_fpar, (void*)S->d_fsc, (void*)S->d_fsg})

@@ -17,7 +17,7 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
                    const std::vector<int32_t>& gidx, const qtn_tensor_recipe* rec,
                    const int64_t* offsets, int32_t n_total);
 int64_t setmajor_workspace(const SetMajor* S, int32_t n_sets);
-int setmajor_launches(const SetMajor* S);
+int setmajor_launches(const SetMajor* S, int32_t n_sets);
 // results[s*n_total + gidx[k]] for every set s
 int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_sets,
                  void* workspace, void* results, void* stream);
