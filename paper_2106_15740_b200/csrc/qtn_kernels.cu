@@ -441,19 +441,39 @@ __global__ void tensorgen_kernel(const qtn_tensor_recipe* __restrict__ rec, int6
   }
 }
 
-__global__ void energy_kernel(const double2* __restrict__ vals, const double* __restrict__ w,
-                              int n, double* energies, double2* zz) {
+// One 128-thread CTA per input set: strided partial sums, then a fixed-order
+// shuffle + shared-memory tree (deterministic for a given n).
+__global__ void __launch_bounds__(128) energy_kernel(const double2* __restrict__ vals,
+                                                     const double* __restrict__ w, int n,
+                                                     double* energies, double2* zz) {
   const int s = blockIdx.x;
-  if (threadIdx.x != 0) return;
   double e = 0.0, zr = 0.0, zi = 0.0;
-  for (int i = 0; i < n; ++i) {
+  for (int i = threadIdx.x; i < n; i += 128) {
     const double2 v = vals[(int64_t)s * n + i];
     e += ((w ? w[i] : 1.0) - v.x) / 2.0;
     zr += v.x;
     zi += v.y;
   }
-  if (energies) energies[s] = e;
-  if (zz) zz[s] = make_double2(zr, zi);
+  for (int o = 16; o > 0; o >>= 1) {
+    e += __shfl_xor_sync(0xffffffffu, e, o);
+    zr += __shfl_xor_sync(0xffffffffu, zr, o);
+    zi += __shfl_xor_sync(0xffffffffu, zi, o);
+  }
+  __shared__ double red[3][4];
+  const int wp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][wp] = e;
+    red[1][wp] = zr;
+    red[2][wp] = zi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    e = (red[0][0] + red[0][1]) + (red[0][2] + red[0][3]);
+    zr = (red[1][0] + red[1][1]) + (red[1][2] + red[1][3]);
+    zi = (red[2][0] + red[2][1]) + (red[2][2] + red[2][3]);
+    if (energies) energies[s] = e;
+    if (zz) zz[s] = make_double2(zr, zi);
+  }
 }
 
 }  // namespace
@@ -1075,7 +1095,7 @@ extern "C" int qtn_energy_reduce(const void* values, const double* weights, int3
   int rc = device_check();
   if (rc) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  energy_kernel<<<n_sets, 32, 0, st>>>(reinterpret_cast<const double2*>(values), weights, n,
+  energy_kernel<<<n_sets, 128, 0, st>>>(reinterpret_cast<const double2*>(values), weights, n,
                                        energies, reinterpret_cast<double2*>(zz_sum));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "energy launch");

@@ -76,6 +76,12 @@ struct SetMajor {
   std::vector<uint32_t> level_blocks;  // CTAs per level
   std::vector<uint32_t> level_rec;     // first CTA record of each level
   uint32_t* d_recs = nullptr;          // kRecWords per CTA (see sm_level_kernel)
+  // bucket-tile form (sm_bucket_kernel)
+  std::vector<uint32_t> level_bk;      // buckets per level
+  std::vector<uint32_t> level_bk_first;
+  uint32_t* d_brec = nullptr;          // variable-size bucket records
+  uint32_t* d_brec_off = nullptr;      // word offset of each bucket's record (level-major)
+  uint32_t* d_btab = nullptr;          // per (operand, element) index pair / coefficient codes
   uint64_t* d_base = nullptr;
   SMParam* d_params = nullptr;
   int32_t n_params = 0;
@@ -318,10 +324,109 @@ __device__ __forceinline__ double lds_f64(const void* p) {
   return v;
 }
 
-template <int J>
+// grid.y > 1 (levels with few CTAs): CTA y covers sets [y*256*J, (y+1)*256*J).
+struct OpRow {
+  uint64_t ox, oy;  // row starts (double2 units): intermediates in ws, gates in ph
+  double c[6];      // gate: (a, u, w) for v = 0, 1
+  int gen;
+  int pad;
+};
+
+__device__ __forceinline__ int lds_s32(const void* p) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
+
+// Values of operand k at sets s0 + 256 j (0 beyond A).  Rows read here were
+// written by earlier launches only, hence the non-coherent path (__ldg).
+template <int J, bool FULL>
+__device__ __forceinline__ void load_operand(const OpRow* su, int k, int s0, int A,
+                                             const double2* __restrict__ ph,
+                                             const double2* ws, double2 (&x)[J],
+                                             double2 (&y)[J]) {
+  const uint64_t ox = lds_u64(&su[k].ox);
+  if (lds_s32(&su[k].gen)) {
+    const double* c = su[k].c;
+    const double c0 = lds_f64(c), c1 = lds_f64(c + 1), c2 = lds_f64(c + 2);
+    const double c3 = lds_f64(c + 3), c4 = lds_f64(c + 4), c5 = lds_f64(c + 5);
+    const double2* pp = ph + ox;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int s = s0 + 256 * j;
+      const double2 p = (J == 1 || FULL || s < A) ? __ldg(pp + s) : make_double2(0.0, 0.0);
+      x[j] = make_double2(fma(c1, p.x, c0), c2 * p.y);
+      y[j] = make_double2(fma(c4, p.x, c3), c5 * p.y);
+    }
+  } else {
+    const double2* px = ws + ox;
+    const double2* py = ws + lds_u64(&su[k].oy);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int s = s0 + 256 * j;
+      const bool ok = J == 1 || FULL || s < A;
+      x[j] = ok ? __ldg(px + s) : make_double2(0.0, 0.0);
+      y[j] = ok ? __ldg(py + s) : make_double2(0.0, 0.0);
+    }
+  }
+}
+
+// FULL: A is a multiple of 256 * J * gridDim.y (no per-set bounds checks)
+template <int J, bool FULL>
 __global__ void __launch_bounds__(256) sm_level_kernel(const uint32_t* __restrict__ recs,
                                                        const double2* __restrict__ ph,
                                                        double2* ws, int A) {
+  __shared__ OpRow su[kMaxOps];
+  const uint32_t* r = recs + (size_t)blockIdx.x * kRecWords;
+  const uint2 hd = *reinterpret_cast<const uint2*>(r);
+  const int n = (int)hd.y;
+  if (threadIdx.x < n) {
+    const uint2 w = reinterpret_cast<const uint2*>(r + 2)[threadIdx.x];
+    OpRow& u = su[threadIdx.x];
+    if (w.x & 0x80000000u) {
+      u.gen = 1;
+      u.ox = u.oy = (uint64_t)(w.x & 0x7fffffffu) * A;
+      const uint32_t c0 = w.y & 0xff, c1 = w.y >> 8;
+      for (int i = 0; i < 3; ++i) {
+        u.c[i] = kGateCoef[c0][i];
+        u.c[3 + i] = kGateCoef[c1][i];
+      }
+    } else {
+      u.gen = 0;
+      u.ox = (uint64_t)w.x * A;
+      u.oy = (uint64_t)w.y * A;
+    }
+  }
+  __syncthreads();
+  double2* out = ws + (size_t)hd.x * A;
+  const int s_step = 256 * J * gridDim.y;
+#pragma unroll 1
+  for (int s0 = blockIdx.y * 256 * J + threadIdx.x; s0 < A; s0 += s_step) {
+    double2 a0[J], a1[J];
+    load_operand<J, FULL>(su, 0, s0, A, ph, ws, a0, a1);
+#pragma unroll 1
+    for (int k = 1; k < n; ++k) {
+      double2 x[J], y[J];
+      load_operand<J, FULL>(su, k, s0, A, ph, ws, x, y);
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        a0[j] = cmul(a0[j], x[j]);
+        a1[j] = cmul(a1[j], y[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (FULL || s0 + 256 * j < A) out[s0 + 256 * j] = make_double2(a0[j].x + a1[j].x, a0[j].y + a1[j].y);
+  }
+}
+
+// Software-pipelined variant: the (set pass, operand) steps of a thread form
+// one flattened sequence and the loads of step t+1 are issued before step t
+// is multiplied in, so a warp pays roughly one L2/DRAM round trip per CTA
+// instead of one per operand.  grid.y > 1 splits the sets over CTAs.
+__global__ void __launch_bounds__(256) sm_level_pipe_kernel(const uint32_t* __restrict__ recs,
+                                                            const double2* __restrict__ ph,
+                                                            double2* ws, int A) {
   __shared__ OpSetup su[kMaxOps];
   const uint32_t* r = recs + (size_t)blockIdx.x * kRecWords;
   const uint2 hd = *reinterpret_cast<const uint2*>(r);
@@ -345,46 +450,133 @@ __global__ void __launch_bounds__(256) sm_level_kernel(const uint32_t* __restric
   }
   __syncthreads();
   double2* out = ws + (size_t)hd.x * A;
+  const int s_first = blockIdx.y * 256 + threadIdx.x, s_step = 256 * gridDim.y;
+  if (s_first >= A) return;
+  const int passes = (A - 1 - s_first) / s_step + 1;
+  const int steps = passes * n;
+  // step t: set s_first + (t / n) * s_step, operand t % n
+  int k = 0, s = s_first;
+  double2 r0 = reinterpret_cast<const double2*>(lds_u64(&su[0].px))[s];
+  double2 r1 = su[0].gen ? r0 : reinterpret_cast<const double2*>(lds_u64(&su[0].py))[s];
+  double2 a0 = make_double2(1.0, 0.0), a1 = a0;
 #pragma unroll 1
-  for (int s0 = threadIdx.x; s0 < A; s0 += 256 * J) {
-    double2 a0[J], a1[J];
-#pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-      const double2* px = reinterpret_cast<const double2*>(lds_u64(&su[k].px));
-      double2 x[J], y[J];
-      if (su[k].gen) {
-        const double* c = su[k].c;
-        const double c0 = lds_f64(c), c1 = lds_f64(c + 1), c2 = lds_f64(c + 2);
-        const double c3 = lds_f64(c + 3), c4 = lds_f64(c + 4), c5 = lds_f64(c + 5);
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const double2 p = s0 + 256 * j < A ? px[s0 + 256 * j] : make_double2(0.0, 0.0);
-          x[j] = make_double2(fma(c1, p.x, c0), c2 * p.y);
-          y[j] = make_double2(fma(c4, p.x, c3), c5 * p.y);
-        }
-      } else {
-        const double2* py = reinterpret_cast<const double2*>(lds_u64(&su[k].py));
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const bool ok = s0 + 256 * j < A;
-          x[j] = ok ? px[s0 + 256 * j] : make_double2(0.0, 0.0);
-          y[j] = ok ? py[s0 + 256 * j] : make_double2(0.0, 0.0);
-        }
+  for (int t = 0; t < steps; ++t) {
+    // prefetch step t + 1
+    int kn = k + 1, sn = s;
+    if (kn == n) {
+      kn = 0;
+      sn += s_step;
+    }
+    double2 q0 = r0, q1 = r1;
+    if (t + 1 < steps) {
+      q0 = reinterpret_cast<const double2*>(lds_u64(&su[kn].px))[sn];
+      if (!su[kn].gen) q1 = reinterpret_cast<const double2*>(lds_u64(&su[kn].py))[sn];
+    }
+    double2 x = r0, y = r1;
+    if (su[k].gen) {
+      const double* c = su[k].c;
+      y = make_double2(fma(lds_f64(c + 4), r0.x, lds_f64(c + 3)), lds_f64(c + 5) * r0.y);
+      x = make_double2(fma(lds_f64(c + 1), r0.x, lds_f64(c + 0)), lds_f64(c + 2) * r0.y);
+    }
+    if (k == 0) {
+      a0 = x;
+      a1 = y;
+    } else {
+      a0 = cmul(a0, x);
+      a1 = cmul(a1, y);
+    }
+    if (k == n - 1) out[s] = make_double2(a0.x + a1.x, a0.y + a1.y);
+    k = kn;
+    s = sn;
+    r0 = q0;
+    r1 = q1;
+  }
+}
+
+// ---- bucket-tile kernel
+// One CTA per (bucket, tile of kTile = 64 sets); 256 threads = 4 element
+// groups x 64 sets.  Operands whose rows are reused across the bucket's
+// output elements (every intermediate of rank < R + 1, every gate's phase
+// row) are staged once into shared memory for the tile; full-rank operands
+// (each row read once) stream from L2/HBM.  This removes the L2 re-reads of
+// the per-element form (one CTA per output element re-fetching shared rows).
+// Record (u32 words, 16-byte aligned): [0] first output element (absolute),
+// [1] R | n_ops << 8, [2..3] pad, then per operand a uint4:
+//   x = mode << 30 | v   mode 0 stream: v = absolute base element
+//                        mode 1 staged: v = first shared-memory row
+//                        mode 2 gate  : v = shared-memory row of its phase
+//   y = staged: absolute base element; gate: phase-table row
+//   z = staged: rows
+//   w = word offset of its per-element table in btab
+//       (intermediates: i0 | i1 << 16; gates: code0 | code1 << 8)
+constexpr int kTile = 64;
+constexpr int64_t kStageBudget = 32 * 1024;
+
+__global__ void __launch_bounds__(256) sm_bucket_kernel(const uint32_t* __restrict__ brec,
+                                                        const uint32_t* __restrict__ boff,
+                                                        const uint32_t* __restrict__ btab,
+                                                        const double2* __restrict__ ph,
+                                                        double2* ws, int A) {
+  extern __shared__ double2 stg[];
+  __shared__ uint4 od[kMaxOps];
+  const uint32_t* r = brec + boff[blockIdx.x];
+  const uint2 hd = *reinterpret_cast<const uint2*>(r);
+  const uint32_t R = hd.y & 0xff;
+  const int n = (int)((hd.y >> 8) & 0xff);
+  if (threadIdx.x < n) od[threadIdx.x] = reinterpret_cast<const uint4*>(r + 4)[threadIdx.x];
+  __syncthreads();
+  const int s0 = blockIdx.y * kTile;
+  for (int k = 0; k < n; ++k) {
+    const uint4 o = od[k];
+    const uint32_t mode = o.x >> 30, dst = o.x & 0x3fffffffu;
+    if (mode == 1) {
+      for (uint32_t i = threadIdx.x; i < o.z * kTile; i += 256) {
+        const uint32_t row = i / kTile, c = i % kTile;
+        const int s = s0 + (int)c;
+        stg[(dst + row) * kTile + c] = s < A ? ws[(size_t)(o.y + row) * A + s] : make_double2(0.0, 0.0);
       }
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        if (k == 0) {
-          a0[j] = x[j];
-          a1[j] = y[j];
-        } else {
-          a0[j] = cmul(a0[j], x[j]);
-          a1[j] = cmul(a1[j], y[j]);
-        }
+    } else if (mode == 2) {
+      if (threadIdx.x < kTile) {
+        const int s = s0 + (int)threadIdx.x;
+        stg[dst * kTile + threadIdx.x] = s < A ? ph[(size_t)o.y * A + s] : make_double2(0.0, 0.0);
       }
     }
-#pragma unroll
-    for (int j = 0; j < J; ++j)
-      if (s0 + 256 * j < A) out[s0 + 256 * j] = make_double2(a0[j].x + a1[j].x, a0[j].y + a1[j].y);
+  }
+  __syncthreads();
+  const uint32_t c = threadIdx.x % kTile, g = threadIdx.x / kTile;
+  const int s = s0 + (int)c;
+  const bool valid = s < A;
+  const uint32_t ne = 1u << R;
+#pragma unroll 1
+  for (uint32_t e = g; e < ne; e += 256 / kTile) {
+    double2 a0 = make_double2(1.0, 0.0), a1 = a0;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+      const uint4 o = od[k];
+      const uint32_t t = __ldg(btab + o.w + e);
+      const uint32_t mode = o.x >> 30, v = o.x & 0x3fffffffu;
+      double2 x, y;
+      if (mode == 0) {
+        x = valid ? ws[(size_t)(v + (t & 0xffffu)) * A + s] : make_double2(0.0, 0.0);
+        y = valid ? ws[(size_t)(v + (t >> 16)) * A + s] : make_double2(0.0, 0.0);
+      } else if (mode == 1) {
+        x = stg[(v + (t & 0xffffu)) * kTile + c];
+        y = stg[(v + (t >> 16)) * kTile + c];
+      } else {
+        const double2 p = stg[v * kTile + c];
+        const uint32_t c0 = t & 0xff, c1 = (t >> 8) & 0xff;
+        x = make_double2(fma(kGateCoef[c0][1], p.x, kGateCoef[c0][0]), kGateCoef[c0][2] * p.y);
+        y = make_double2(fma(kGateCoef[c1][1], p.x, kGateCoef[c1][0]), kGateCoef[c1][2] * p.y);
+      }
+      if (k == 0) {
+        a0 = x;
+        a1 = y;
+      } else {
+        a0 = cmul(a0, x);
+        a1 = cmul(a1, y);
+      }
+    }
+    if (valid) ws[(size_t)(hd.x + e) * A + s] = make_double2(a0.x + a1.x, a0.y + a1.y);
   }
 }
 
@@ -535,6 +727,83 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
     n_cta += acc;
   }
 
+  // bucket-tile records (sm_bucket_kernel), same level-major heaviest-first order
+  std::vector<uint32_t> brec, boff, btab;
+  for (int32_t lev = 0; lev < max_lev; ++lev) {
+    S->level_bk_first.push_back((uint32_t)boff.size());
+    std::vector<std::tuple<uint64_t, size_t, const qtn_plan::SMBucketRec*>> lvb;
+    for (size_t k = 0; k < plans.size(); ++k)
+      for (const auto& rb : plans[k]->sm_buckets)
+        if (rb.level == lev) lvb.emplace_back(~((uint64_t)rb.ops.size() << rb.R), k, &rb);
+    std::stable_sort(lvb.begin(), lvb.end(),
+                     [](const auto& a, const auto& b) { return std::get<0>(a) < std::get<0>(b); });
+    for (const auto& it : lvb) {
+      const size_t k = std::get<1>(it);
+      const auto& rb = *std::get<2>(it);
+      const uint32_t ne = 1u << rb.R;
+      const size_t r0 = brec.size();
+      boff.push_back((uint32_t)r0);
+      brec.resize(r0 + 4 + 4 * rb.ops.size(), 0);
+      brec[r0] = (uint32_t)(base[k] + rb.out_off);
+      brec[r0 + 1] = rb.R | ((uint32_t)rb.ops.size() << 8);
+      // staging choice: gates always (one phase row), intermediates by reuse
+      std::vector<std::pair<uint32_t, size_t>> cand;  // (rows, op)
+      std::vector<uint32_t> rows_of(rb.ops.size(), 0);
+      for (size_t t = 0; t < rb.ops.size(); ++t) {
+        const auto& o = rb.ops[t];
+        uint32_t mx = 0;
+        for (uint16_t v : o.idx) mx = std::max<uint32_t>(mx, v);
+        rows_of[t] = mx + 1;
+        if (o.input < 0 && rows_of[t] < 2 * ne) cand.emplace_back(rows_of[t], t);
+      }
+      std::sort(cand.begin(), cand.end());
+      uint32_t nrows = 0;
+      for (const auto& o : rb.ops)
+        if (o.input >= 0) ++nrows;
+      std::vector<int> staged(rb.ops.size(), 0);
+      for (const auto& cd : cand)
+        if ((int64_t)(nrows + cd.first) * kTile * 16 <= kStageBudget) {
+          staged[cd.second] = 1;
+          nrows += cd.first;
+        }
+      uint32_t row = 0;
+      for (size_t t = 0; t < rb.ops.size(); ++t) {
+        const auto& o = rb.ops[t];
+        uint32_t* q4 = &brec[r0 + 4 + 4 * t];
+        q4[3] = (uint32_t)btab.size();
+        if (o.input >= 0) {
+          const qtn_tensor_recipe& q = rec[offsets[gidx[k]] + o.input];
+          q4[0] = (2u << 30) | row;
+          q4[1] = (uint32_t)param_of(q);
+          q4[2] = 1;
+          row += 1;
+          for (uint32_t e = 0; e < ne; ++e) {
+            const int c0 = coef_code(gate_coef(q.kind, full_of(q, o.idx[2 * e])));
+            const int c1 = coef_code(gate_coef(q.kind, full_of(q, o.idx[2 * e + 1])));
+            if (c0 < 0 || c1 < 0) {
+              delete S;
+              set_error("set-major executor: unsupported gate coefficient");
+              return QTN_EINVAL;
+            }
+            btab.push_back((uint32_t)c0 | ((uint32_t)c1 << 8));
+          }
+        } else {
+          if (staged[t]) {
+            q4[0] = (1u << 30) | row;
+            q4[1] = (uint32_t)(base[k] + o.off);
+            q4[2] = rows_of[t];
+            row += rows_of[t];
+          } else {
+            q4[0] = (uint32_t)(base[k] + o.off);
+          }
+          for (uint32_t e = 0; e < ne; ++e)
+            btab.push_back((uint32_t)o.idx[2 * e] | ((uint32_t)o.idx[2 * e + 1] << 16));
+        }
+      }
+    }
+    S->level_bk.push_back((uint32_t)(boff.size() - S->level_bk_first.back()));
+  }
+
   // ---- fused form: per network, liveness-packed offsets and local phase slots
   std::vector<SMFNet> fnets;
   std::vector<SMFBucket> fbk;
@@ -683,7 +952,8 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
     }
     coef_up = true;
   }
-  if ((rc = upload_vec(&S->d_recs, recs)) || (rc = upload_vec(&S->d_base, base)) || (rc = upload_vec(&S->d_params, params)) ||
+  if ((rc = upload_vec(&S->d_recs, recs)) || (rc = upload_vec(&S->d_brec, brec)) ||
+      (rc = upload_vec(&S->d_brec_off, boff)) || (rc = upload_vec(&S->d_btab, btab)) || (rc = upload_vec(&S->d_base, base)) || (rc = upload_vec(&S->d_params, params)) ||
       (rc = upload_vec(&S->d_const, cst)) || (rc = upload_vec(&S->d_scal_first, scal_first)) ||
       (rc = upload_vec(&S->d_scal_off, scal_off)) || (rc = upload_vec(&S->d_sgen_first, sgen_first)) ||
       (rc = upload_vec(&S->d_sgen, sgen)) ||
@@ -750,10 +1020,25 @@ int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_
     const uint32_t blocks = S->level_blocks[lev];
     if (!blocks) continue;
     const uint32_t* r = S->d_recs + (size_t)S->level_rec[lev] * kRecWords;
-    if (n_sets >= 1024)
-      sm_level_kernel<2><<<blocks, 256, 0, st>>>(r, ph, ws, n_sets);
+    // few CTAs (tail levels): split the sets over grid.y so the level is not
+    // bound by one CTA's chain of operand round trips
+    const uint32_t split = blocks < 4u * 148u ? (uint32_t)((n_sets + 255) / 256) : 1u;
+    const char* bv = getenv("QTN_SM_BUCKET");
+    const char* pv = getenv("QTN_SM_PIPE");
+    if (bv && bv[0] == '1') {
+      const uint32_t nbk = S->level_bk[lev];
+      sm_bucket_kernel<<<dim3(nbk, (n_sets + kTile - 1) / kTile), 256, kStageBudget, st>>>(
+          S->d_brec, S->d_brec_off + S->level_bk_first[lev], S->d_btab, ph, ws, n_sets);
+    } else if (pv && pv[0] == '1')
+      sm_level_pipe_kernel<<<dim3(blocks, split), 256, 0, st>>>(r, ph, ws, n_sets);
+    else if (split > 1)
+      sm_level_kernel<1, false><<<dim3(blocks, split), 256, 0, st>>>(r, ph, ws, n_sets);
+    else if (n_sets >= 1024 && n_sets % 512 == 0)
+      sm_level_kernel<2, true><<<blocks, 256, 0, st>>>(r, ph, ws, n_sets);
+    else if (n_sets >= 1024)
+      sm_level_kernel<2, false><<<blocks, 256, 0, st>>>(r, ph, ws, n_sets);
     else
-      sm_level_kernel<1><<<blocks, 256, 0, st>>>(r, ph, ws, n_sets);
+      sm_level_kernel<1, false><<<blocks, 256, 0, st>>>(r, ph, ws, n_sets);
   }
   {
     dim3 g((n_sets + 127) / 128, S->n_nets);
@@ -772,7 +1057,7 @@ int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_
 
 void setmajor_destroy(SetMajor* S) {
   if (!S) return;
-  for (void* p : {(void*)S->d_recs, (void*)S->d_base, (void*)S->d_params, (void*)S->d_const, (void*)S->d_scal_first,
+  for (void* p : {(void*)S->d_recs, (void*)S->d_brec, (void*)S->d_brec_off, (void*)S->d_btab, (void*)S->d_base, (void*)S->d_params, (void*)S->d_const, (void*)S->d_scal_first,
                   (void*)S->d_scal_off, (void*)S->d_sgen_first, (void*)S->d_sgen, (void*)S->d_gidx,
                   (void*)S->d_fnets, (void*)S->d_fbk, (void*)S->d_fops, (void*)S->d_ftabs,
                   (void*)S->d_fpar, (void*)S->d_fsc, (void*)S->d_fsg})
