@@ -2,7 +2,6 @@
 the golden vectors produced by the real reference (tests/golden)."""
 
 import math
-import os
 
 import numpy as np
 import pytest
@@ -273,16 +272,11 @@ def test_setmajor_matches_warp_executor(golden, setmajor_min_sets, mode, slice_k
         plan = Q.EnergyPlan(graph, p, mode, dtype="complex128", slice_k=slice_k)
     setmajor_min_sets(0)
     warp = plan.energies(sets)
-    for fused in ("1", "0"):  # warp-per-tile fused form, level-synchronous form
-        os.environ["QTN_SETMAJOR_FUSED"] = fused
-        try:
-            plan._bufs.clear()
-            setmajor_min_sets(1)
-            sm = plan.energies(sets)
-            assert plan.launches == plan.launches_per_eval(len(sets))
-        finally:
-            del os.environ["QTN_SETMAJOR_FUSED"]
-        assert np.allclose(sm, warp, rtol=1e-12, atol=1e-11), (fused, np.abs(sm - warp).max())
+    plan._bufs.clear()
+    setmajor_min_sets(1)
+    sm = plan.energies(sets)
+    assert plan.launches == plan.launches_per_eval(len(sets))
+    assert np.allclose(sm, warp, rtol=1e-12, atol=1e-11), np.abs(sm - warp).max()
 
 
 def test_setmajor_vs_oracle(golden, setmajor_min_sets):
