@@ -71,12 +71,26 @@ def main():
     out = sys.argv[1]
     kernels = {}
     for rep in sys.argv[2:]:
+        per = {}
         for d in raw(rep):
             short = d["kernel"].split("(")[0].split("::")[-1].split("<")[0]
             rd, wr = d.get("dram__bytes_read.sum"), d.get("dram__bytes_write.sum")
             d["dram_bytes_per_launch"] = (rd or 0) + (wr or 0)
             d["report"] = rep
-            kernels[short] = d
+            per.setdefault(short, []).append(d)
+        for short, ds in per.items():
+            if len(ds) == 1:
+                kernels[short] = ds[0]
+                continue
+            # several launches of one kernel in one report (e.g. the level
+            # launches of one set-major evaluation): metrics of the longest
+            # launch, times and DRAM bytes summed over the captured launches
+            big = dict(max(ds, key=lambda d: d.get("gpu__time_duration.sum", 0)))
+            big["launches_summed"] = len(ds)
+            big["time_sum_s"] = sum(d.get("gpu__time_duration.sum", 0) for d in ds)
+            big["dram_bytes_per_launch"] = sum(d["dram_bytes_per_launch"] for d in ds)
+            big["dram_bytes_note"] = "summed over the captured launches (one evaluation)"
+            kernels[short] = big
     json.dump({"kernels": kernels}, open(out, "w"), indent=1)
 
 

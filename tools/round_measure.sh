@@ -14,8 +14,10 @@ timeout 300 python bench.py --workload config4 --angle-sets 1 --slices 3 --steps
 timeout 600 python bench.py --workload config5 --steps 5 > gpurun_out/r/config5_sweep.json 2>&1; echo "c5 rc=$?"
 # ncu: launch list of the default bench step, then full captures of the two hot kernels
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config5 > gpurun_out/r/plain_c2.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/r/launches_config2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config5 > gpurun_out/r/ncu1.log 2>&1; echo "ncu1 rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:smem_net -s 3 -c 1 -o gpurun_out/r/prof_smem python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config5 > gpurun_out/r/ncu2.log 2>&1; echo "ncu2 rc=$?"
+ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv --log-file gpurun_out/r/launches_config2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config5 > gpurun_out/r/ncu1.log 2>&1; echo "ncu1 rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:sm_level_kernel -c 15 -o gpurun_out/r/prof_setmajor python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config5 > gpurun_out/r/ncu2.log 2>&1; echo "ncu2 rc=$?"
+python bench.py --steps 3 --warmup 3 --angle-sets 16 --no-cpu-baseline --no-config5 > gpurun_out/r/plain_c2_16.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:smem_net -s 3 -c 1 -o gpurun_out/r/prof_smem python bench.py --steps 3 --warmup 3 --angle-sets 16 --no-cpu-baseline --no-config5 > gpurun_out/r/ncu2b.log 2>&1; echo "ncu2b rc=$?"
 python bench.py --workload config5 --steps 2 --c5-ws 30 --c5-ms 16 > gpurun_out/r/plain_c5.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 2 -c 1 -o gpurun_out/r/prof_stream_c5 python bench.py --workload config5 --steps 2 --c5-ws 30 --c5-ms 16 > gpurun_out/r/ncu3.log 2>&1; echo "ncu3 rc=$?"
 python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-baseline --no-config5 > gpurun_out/r/plain_c4.log 2>&1 && \
