@@ -129,8 +129,9 @@ WORKLOADS = {
 
 
 def profile_traffic(kernel_key):
-    """dram bytes per launch of the dominant kernel from a committed
-    `ncu --set full` summary (profiles/ncu_full_*.json), or None."""
+    """DRAM bytes of the dominant kernel for one evaluation of this workload
+    (key "kernel@workload") from a committed ncu summary
+    (profiles/ncu_full_*.json), or None when that pair was not captured."""
     prof = os.path.join(ROOT, "profiles")
     if not os.path.isdir(prof):
         return None
@@ -456,9 +457,13 @@ def run_gpu(args):
         kname = "smem_net_kernel"
     achieved = alg / kt / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": profile_traffic(kname), "kernel": kname,
+            "frac": achieved / peak, "traffic": profile_traffic(f"{kname}@{args.workload}"),
+            "kernel": kname,
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-            "alg_bytes_per_launch": alg, "avg_launch_s": kt}
+            "alg_bytes_per_launch": alg, "avg_launch_s": kt,
+            "scope": "one evaluation of all angle sets: every executor launch of the step "
+                     "(set-major: gate rows + level launches + fold; HBM: level launches + "
+                     "fold), timed with CUDA events on the launching stream"}
 
     out = None
     if rank == 0:
