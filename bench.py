@@ -149,6 +149,20 @@ def profile_traffic(kernel_key):
 
 
 # ------------------------------------------------------------ CPU baseline
+def host_cpu():
+    """nproc and CPU model of the box (record them)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
 def _cpu_worker_init(n, edges, p, mode, orders):
     global _W
     _W = (n, edges, p, mode, orders)
@@ -259,7 +273,8 @@ def run_reference(args):
                    "mode": wl["mode"]},
         "cpu_baseline": {"value": value, "unit": "contractions/s", "cores": cores, "kind": "port",
                          "sample": f"1 angle set x {per_step} edge networks per step "
-                                   "(oracle network build + bucket elimination, complex128)"},
+                                   "(oracle network build + bucket elimination, complex128)",
+                         "host": host_cpu()},
         "e2e": {"value": value, "unit": "contractions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -364,12 +379,19 @@ def run_gpu(args):
     plan_s = time.perf_counter() - t0
     A = args.angle_sets
     sets = angle_sets(wl["p"], A)
-    ang = torch.from_numpy(sets).to(dev)
+    # the QAOA loop re-draws angles every step: a ring of
+    # R angle batches, set 0 of batch 0 = the config's seeded angles
+    R = 4
+    ring_host = [sets] + [np.random.default_rng(2000 + k).uniform(0.0, math.pi, sets.shape)
+                          for k in range(1, R)]
+    ring_dev = [torch.from_numpy(h).to(dev) for h in ring_host]
+    it_box = [0]
     st = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
-        b = plan.launch(ang, st)
+        b = plan.launch(ring_dev[it_box[0] % R], st)
+        it_box[0] += 1
         if world > 1:
             dist.all_reduce(b["energy"])
         return b
@@ -379,7 +401,8 @@ def run_gpu(args):
     # launching stream
     def kernel_only():
         b = plan._buffers(A)
-        plan._batch.execute_angles(ang.data_ptr(), 2 * wl["p"], A, b["inputs"].data_ptr(),
+        a = ring_dev[it_box[0] % R]
+        plan._batch.execute_angles(a.data_ptr(), 2 * wl["p"], A, b["inputs"].data_ptr(),
                                    b["ws"].data_ptr(), b["res"].data_ptr(), st.cuda_stream)
 
     clk = ClockSampler(local).__enter__()  # sampled through warm-up, timed and e2e loops
@@ -425,13 +448,14 @@ def run_gpu(args):
         if dist is not None:
             dist.barrier()
         t1 = time.perf_counter()
+        hs = ring_host[it % R]
         if world > 1:
-            en = plan.energies(sets)
+            en = plan.energies(hs)
             buf = torch.from_numpy(en).to(dev)
             dist.all_reduce(buf)
             en = buf.cpu().numpy()
         else:
-            en = plan.energies(sets)
+            en = plan.energies(hs)
         dt = time.perf_counter() - t1
         if it >= args.warmup:
             e2e_times.append(dt)
@@ -443,7 +467,12 @@ def run_gpu(args):
     e2e_value = n_contr / e2e_total
     clk.__exit__(None, None, None)
 
-    # sanity: set-0 energy is the config's energy
+    # sanity: set-0 energy at the seeded angles is the config's energy
+    en = plan.energies(sets)
+    if world > 1:
+        buf = torch.from_numpy(en).to(dev)
+        dist.all_reduce(buf)
+        en = buf.cpu().numpy()
     energy0 = float(en[0])
 
     peak, peak_kind = hbm_peak()
@@ -470,7 +499,7 @@ def run_gpu(args):
         cpu = None
         if not args.no_cpu_baseline:
             v, n, dt = cpu_baseline(wl, graph, sets[:1], seconds=args.cpu_seconds, cores=1)
-            cpu = {"value": v, "unit": "contractions/s", "cores": 1, "kind": "port",
+            cpu = {"value": v, "unit": "contractions/s", "cores": 1, "kind": "port", "host": host_cpu(),
                    "sample": f"{n} edge networks (angle set 0) in {dt:.1f}s: oracle network build "
                              "+ bucket elimination, complex128, orders cached"}
         b5 = None
@@ -500,7 +529,8 @@ def run_gpu(args):
                        "contractions_per_step": len(edge_ids) * A,
                        "l2": "flushed between timed steps (256 MiB write)",
                        "parallelism": f"edges LPT-sharded over {world} GPU(s)",
-                       "energy_set0": energy0, "plan_seconds": plan_s},
+                       "energy_set0": energy0, "plan_seconds": plan_s,
+                       "angles": f"re-drawn every step (ring of {R} batches of {A} sets)"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "contractions/s",

@@ -25,6 +25,8 @@ from __future__ import annotations
 
 import ctypes as C
 import heapq
+import os
+from concurrent.futures import ThreadPoolExecutor
 import time
 
 import numpy as np
@@ -63,12 +65,18 @@ class EdgeJob:
 
 def plan_edges(graph: ProblemGraph, p: int, mode: str, edge_ids, rank_cap=DEFAULT_RANK_CAP,
                dtype="complex64", mixed_rank=DEFAULT_MIXED_RANK, smem_budget=DEFAULT_SMEM_BUDGET,
-               n_repeats=10, temp=0.02, seed=0, compile_plans=True, slice_k: int = 0):
+               n_repeats=10, temp=0.02, seed=0, compile_plans=True, slice_k: int = 0,
+               workers: int | None = None):
     """Host planning for a set of edges: template, reference rgreedy order,
     compiled plan.  slice_k > 0 splits every edge network into 2^slice_k
-    slices (slicing.py) that share one plan and differ only in their data."""
-    jobs = []
-    for e in edge_ids:
+    slices (slicing.py) that share one plan and differ only in their data.
+
+    Edges are planned on a thread pool: the ordering
+    passes and the plan compiler are native calls that release the GIL, and
+    every edge is independent, so the result is identical to a serial loop
+    (jobs in `edge_ids` order).  workers=1 plans serially."""
+    def plan_one(e):
+        out = []
         tpl = energy_template(graph, graph.edges[e], p, mode)
         order, report = rgreedy_order(tpl.line_graph(), n_repeats=n_repeats, temp=temp, seed=seed)
         assigns = [{}]
@@ -83,8 +91,18 @@ def plan_edges(graph: ProblemGraph, p: int, mode: str, edge_ids, rank_cap=DEFAUL
                                    rank_cap=rank_cap, dtype=dtype, mixed_rank=mixed_rank,
                                    smem_budget=smem_budget)
         for a, t in zip(assigns, tpls):
-            jobs.append(EdgeJob(e, t, order, report, plan, 1.0 / len(assigns), a))
-    return jobs
+            out.append(EdgeJob(e, t, order, report, plan, 1.0 / len(assigns), a))
+        return out
+
+    edge_ids = list(edge_ids)
+    if workers is None:
+        workers = min(32, os.cpu_count() or 1)
+    if workers <= 1 or len(edge_ids) <= 1:
+        per_edge = [plan_one(e) for e in edge_ids]
+    else:
+        with ThreadPoolExecutor(max_workers=min(workers, len(edge_ids))) as ex:
+            per_edge = list(ex.map(plan_one, edge_ids))
+    return [j for js in per_edge for j in js]
 
 
 def shard_edges(costs, world_size: int):

@@ -298,3 +298,19 @@ def test_sliced_jobs_share_one_plan():
     assert sum(j.weight for j in jobs) == 1.0
     assert all(j.template.structure == jobs[0].template.structure for j in jobs)
     assert len({tuple(j.template.recipes["fixed_bits"]) for j in jobs}) == 4
+
+
+def test_threaded_planning_matches_serial():
+    """plan_edges on a thread pool (native ordering + plan compiler release
+    the GIL) gives the same jobs, orders and plans as the serial loop."""
+    g = Q.random_regular_graph(100, 3, 0)
+    ids = list(range(0, 150, 7))
+    a = Q.plan_edges(g, 2, "zz+diagonal", ids, workers=1)
+    b = Q.plan_edges(g, 2, "zz+diagonal", ids, workers=4)
+    assert [j.index for j in a] == [j.index for j in b] == ids
+    for x, y in zip(a, b):
+        assert x.order.sequence == y.order.sequence
+        assert x.report == y.report
+        assert x.plan.step_ranks == y.plan.step_ranks
+        assert x.plan.program_bytes == y.plan.program_bytes
+        assert x.plan.alg_bytes == y.plan.alg_bytes
