@@ -199,6 +199,11 @@ class EnergyPlan:
                            device=dev),
                 res=t.zeros((n_sets, len(self.jobs)), dtype=t.complex128, device=dev),
                 energy=t.zeros(n_sets, dtype=t.float64, device=dev),
+                # host <-> device staging of the public energies() call
+                angles=t.empty((n_sets, 2 * self.p), dtype=t.float64, device=dev),
+                angles_host=t.empty((n_sets, 2 * self.p), dtype=t.float64).pin_memory(),
+                energy_host=t.empty(n_sets, dtype=t.float64).pin_memory(),
+                launches=self.launches_per_eval(n_sets),
             )
         return self._bufs[n_sets]
 
@@ -230,7 +235,7 @@ class EnergyPlan:
         N.check(N.lib.qtn_energy_reduce(b["res"].data_ptr(), self._weights.data_ptr(),
                                         len(self.jobs), n_sets, b["energy"].data_ptr(), None, sp),
                 "energy")
-        self.launches = self.launches_per_eval(n_sets)
+        self.launches = b["launches"]
         return b
 
     def energies(self, angle_sets) -> np.ndarray:
@@ -243,9 +248,14 @@ class EnergyPlan:
         a = np.atleast_2d(np.asarray(angle_sets, dtype=np.float64))
         if a.shape[1] != 2 * self.p:
             raise ValueError(f"expected {2 * self.p} angles per set, got {a.shape[1]}")
-        dev_a = t.from_numpy(a).pin_memory().to(self._device, non_blocking=True)
-        b = self.launch(dev_a)
-        return b["energy"].cpu().numpy().copy()
+        b = self._buffers(a.shape[0])
+        st = t.cuda.current_stream(self._device)
+        b["angles_host"].numpy()[...] = a
+        b["angles"].copy_(b["angles_host"], non_blocking=True)
+        self.launch(b["angles"], st)
+        b["energy_host"].copy_(b["energy"], non_blocking=True)
+        st.synchronize()
+        return b["energy_host"].numpy().copy()
 
     def zz_values(self, params: QaoaParams) -> dict:
         """Per-edge <Z_iZ_j> (complex) for one angle set, keyed by edge index."""
