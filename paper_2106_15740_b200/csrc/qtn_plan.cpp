@@ -15,6 +15,7 @@
 // largest operand streams contiguously.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -410,6 +411,10 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
       std::copy(grr.begin(), grr.end(), g[i].grun);
     }
   }
+  if (getenv("QTN_DEBUG_DESC") && R >= 18)
+    fprintf(stderr, "desc R=%d prank=%d pc64=%d oc64=%d tb=%d ta=%d tn=%d pk=%d ng=%d nt=%d stage_k=%d\n", R,
+            (int)h->p_rank, (int)pc64, (int)h->out_c64, tb, ta, tn, (int)a.p_k, ng, (int)a.nt,
+            ng ? (int)g[0].stage_k : -1);
   STRec* t = reinterpret_cast<STRec*>(blob.data() + base + sizeof(SHdr) + ng * sizeof(SGRec));
   for (uint32_t j = 0; j < a.nt; ++j) {
     const TableArg& src = a.t[j];

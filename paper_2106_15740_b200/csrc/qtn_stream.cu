@@ -157,6 +157,8 @@ __device__ __forceinline__ uint64_t tile_off(uint32_t e, uint32_t a, uint32_t r1
 struct LocCache {
   uint32_t item = 0;
   uint64_t lo = 1, hi = 0;  // empty
+  uint32_t set = 0;
+  uint64_t set_lo = 1, set_hi = 0;  // tile range of the cached set (no 64-bit divide per tile)
 };
 
 __device__ __forceinline__ Loc locate(const StreamLaunch& L, uint64_t t, LocCache& c) {
@@ -167,8 +169,13 @@ __device__ __forceinline__ Loc locate(const StreamLaunch& L, uint64_t t, LocCach
     r.tile = t;
     return r;
   }
-  r.set = (uint32_t)(t / L.total_tiles);
-  const uint64_t tt = t - (uint64_t)r.set * L.total_tiles;
+  if (!(t >= c.set_lo && t < c.set_hi)) {
+    c.set = (uint32_t)(t / L.total_tiles);
+    c.set_lo = (uint64_t)c.set * L.total_tiles;
+    c.set_hi = c.set_lo + L.total_tiles;
+  }
+  r.set = c.set;
+  const uint64_t tt = t - c.set_lo;
   if (!(tt >= c.lo && tt < c.hi)) {
     uint32_t it = c.item < L.n_items ? c.item : 0;
     if (L.tile_prefix[it] > tt) it = 0;
@@ -244,12 +251,18 @@ struct ThreadState {
   uint32_t ts;                        // staged slice index, lane part
   uint32_t ta, r1;                    // tile-local primary bits, primary rank - 1
   uint32_t stage_k;                   // 0xff: operand 0 not staged
+  uint32_t pi0[kJ];                   // per element j: primary index (v = 0) in the chunk
+  uint64_t ooff[kJ];                  // per element j: output offset within the tile
 };
 
-// Generic tile: any dtypes, any operand counts, partial tiles.
-__device__ __noinline__ void tile_generic(const ThreadState& T, const uint8_t* chunk, const Smem& S,
-                                          const SGRec* gr, const STRec* tr, uint64_t obase,
-                                          uint32_t tid, uint32_t pc64, uint32_t oc64) {
+// Generic tile: any dtypes, any operand counts, partial tiles.  Inlined
+// with constant-index (guarded, unrolled) operand loops so ThreadState stays
+// in registers.
+__device__ __forceinline__ void tile_generic(const ThreadState& T, const uint8_t* chunk,
+                                             const Smem& S, const SGRec* gr, const STRec* tr,
+                                             uint64_t obase, uint32_t tid, uint32_t pc64,
+                                             uint32_t oc64) {
+#pragma unroll 1
   for (uint32_t e = tid; e < T.tile_elems; e += kCompute) {
     const uint32_t j = e / kCompute;
     const uint32_t pe = e & T.pmask;
@@ -265,18 +278,23 @@ __device__ __noinline__ void tile_generic(const ThreadState& T, const uint8_t* c
       a0 = reinterpret_cast<const double2*>(chunk)[i0];
       a1 = reinterpret_cast<const double2*>(chunk)[i1];
     }
-    for (uint32_t q = 0; q < T.nt; ++q) {
-      const uint32_t ti = (uint32_t)gather(obase, tr[q].runs, tr[q].n_runs) | T.tt[q] | S.tjj[q][j];
-      const double2* tp = S.tab + tr[q].smem_off + (ti << 1);
-      a0 = cmul(a0, tp[0]);
-      a1 = cmul(a1, tp[1]);
+#pragma unroll
+    for (int q = 0; q < kSMaxT; ++q) {
+      if (q < (int)T.nt) {
+        const uint32_t ti = (uint32_t)gather(obase, tr[q].runs, tr[q].n_runs) | T.tt[q] | S.tjj[q][j];
+        const double2* tp = S.tab + tr[q].smem_off + (ti << 1);
+        a0 = cmul(a0, tp[0]);
+        a1 = cmul(a1, tp[1]);
+      }
     }
-    for (uint32_t g = 0; g < T.ng; ++g) {
-      const uint64_t idx = gather(obase, gr[g].runs, gr[g].n_runs) | T.gt[g] | S.gjj[g][j];
-      const char* gp = g == 0 ? T.gptr[0] : (g == 1 ? T.gptr[1] : T.gptr[2]);
-      const uint32_t gc = gr[g].c64, vs = gr[g].vshift;
-      a0 = cmul(a0, ldg_c(gp, idx, gc));
-      a1 = cmul(a1, ldg_c(gp, idx + (1ull << vs), gc));
+#pragma unroll
+    for (int g = 0; g < kSMaxG; ++g) {
+      if (g < (int)T.ng) {
+        const uint64_t idx = gather(obase, gr[g].runs, gr[g].n_runs) | T.gt[g] | S.gjj[g][j];
+        const uint32_t gc = gr[g].c64, vs = gr[g].vshift;
+        a0 = cmul(a0, ldg_c(T.gptr[g], idx, gc));
+        a1 = cmul(a1, ldg_c(T.gptr[g], idx + (1ull << vs), gc));
+      }
     }
     const double2 r = make_double2(a0.x + a1.x, a0.y + a1.y);
     if (oc64)
@@ -308,9 +326,7 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
     tbs[q] = (uint32_t)gather(obase, tr[q].runs, tr[q].n_runs) | T.tt[q];
 #pragma unroll
   for (int j = 0; j < kJ; ++j) {
-    const uint32_t e = tid + (uint32_t)j * kCompute;
-    const uint32_t pe = e & T.pmask;
-    const uint32_t i0 = T.split ? pe : ((pe & ((1u << T.pk) - 1u)) | ((pe >> T.pk) << (T.pk + 1)));
+    const uint32_t i0 = T.pi0[j];
     const uint32_t i1 = i0 + T.pstep;
     if constexpr (F32) {
       float2 a0 = reinterpret_cast<const float2*>(chunk)[i0];
@@ -349,8 +365,7 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
         a0 = cmulf(a0, x);
         a1 = cmulf(a1, y);
       }
-      reinterpret_cast<float2*>(T.out)[obase + tile_off(e, T.ta, T.r1)] =
-          make_float2(a0.x + a1.x, a0.y + a1.y);
+      reinterpret_cast<float2*>(T.out)[obase + T.ooff[j]] = make_float2(a0.x + a1.x, a0.y + a1.y);
     } else {
       double2 a0 = reinterpret_cast<const double2*>(chunk)[i0];
       double2 a1 = reinterpret_cast<const double2*>(chunk)[i1];
@@ -382,8 +397,7 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
           a1 = cmul(a1, ldg_c(T.gptr[g], idx + (1ull << T.gvs[g]), T.gc64[g]));
         }
       }
-      reinterpret_cast<double2*>(T.out)[obase + tile_off(e, T.ta, T.r1)] =
-          make_double2(a0.x + a1.x, a0.y + a1.y);
+      reinterpret_cast<double2*>(T.out)[obase + T.ooff[j]] = make_double2(a0.x + a1.x, a0.y + a1.y);
     }
   }
 }
@@ -546,6 +560,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (T.tile_elems == (uint32_t)(kJ * kCompute) && T.nt <= 2 && T.ng <= 1 && pc64 == oc64) {
         variant = 1 + (pc64 ? 6u : 0u) + T.nt * 2 + T.ng;
         if (T.ng == 1 && T.stage_k != 0xffu) variant = 13 + (pc64 ? 3u : 0u) + T.nt;
+      }
+      // per-element primary index and output offset of the fast paths
+      if (variant != 0) {
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+          const uint32_t e = tid + (uint32_t)j * kCompute;
+          const uint32_t pe = e & T.pmask;
+          T.pi0[j] = T.split ? pe : ((pe & ((1u << T.pk) - 1u)) | ((pe >> T.pk) << (T.pk + 1)));
+          T.ooff[j] = tile_off(e, T.ta, T.r1);
+        }
       }
       cur_item = l.item;
       cur_set = l.set;
