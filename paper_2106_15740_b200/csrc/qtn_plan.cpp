@@ -321,7 +321,11 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
   {
     double best = 1e300;
     const int esz = pc64 ? 8 : 16;
-    for (int tn_c = std::max(0, tb - rp1); tn_c <= std::min(dnew, tb); ++tn_c) {
+    const char* tmv = getenv("QTN_TN_MAX");  // experiment knob: cap the new-bit tile part
+    const int tn_max = tmv ? atoi(tmv) : 64;
+    const char* swv = getenv("QTN_STAGE_W");
+    const double stage_w = swv ? atof(swv) : 256.0;  // measured: cp.async-gathered entries cost ~8x bulk bytes
+    for (int tn_c = std::max(0, tb - rp1); tn_c <= std::min(std::min(dnew, tb), std::max(tn_max, tb - rp1)); ++tn_c) {
       const int ta_c = tb - tn_c;
       if (ta_c > rp1 || ta_c < 0) continue;
       double cost = (double)(2 << ta_c) * esz;
@@ -333,7 +337,7 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
           for (uint32_t q = 0; q < ((w >> 16) & 0xff); ++q)
             if (e_bit((int)(w & 0xff) + (int)q, ta_c, tn_c) >= 0) ++k;
         }
-        cost += (i == 1 && k <= kStageMaxK) ? (double)(2 << k) * 32.0 : (double)(2 << tb) * 32.0;
+        cost += (i == 1 && k <= kStageMaxK) ? (double)(2 << k) * stage_w : (double)(2 << tb) * 32.0;
       }
       if (cost < best - 1e-9) {
         best = cost;
