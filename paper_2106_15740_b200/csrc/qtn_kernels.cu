@@ -606,6 +606,10 @@ struct qtn_batch {
   std::vector<uint32_t> level_item0;    // first item of each level (+ end)
   std::vector<uint64_t> level_prefix0;  // first prefix entry of each level
   std::vector<uint64_t> level_tiles;    // tiles of one set per level
+  // small buckets (R <= kSmallR) of each level: warp-per-bucket kernel
+  uint64_t* d_sitem_desc = nullptr;
+  uint32_t* d_sitem_net = nullptr;
+  std::vector<uint32_t> level_sitem0;   // first small item of each level (+ end)
   uint64_t* d_fold_tags = nullptr;
   uint8_t* d_fold_c64 = nullptr;
   uint32_t* d_fold_first = nullptr;
@@ -620,7 +624,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_item_net, (void*)B->d_tile_prefix, (void*)B->d_net_in_off,
                   (void*)B->d_net_ws_off, (void*)B->d_fold_tags, (void*)B->d_fold_c64,
                   (void*)B->d_fold_first, (void*)B->d_fold_pow2, (void*)B->d_hbm_index,
-                  (void*)B->d_hbm_rec})
+                  (void*)B->d_hbm_rec, (void*)B->d_sitem_desc, (void*)B->d_sitem_net})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
   delete B;
@@ -684,8 +688,10 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   B->n_smem = (int)sidx.size();
   B->n_hbm = (int)hidx.size();
   // level-major item lists over all HBM networks
-  std::vector<uint64_t> item_desc, prefix;
-  std::vector<uint32_t> item_net;
+  std::vector<uint64_t> item_desc, prefix, sitem_desc;
+  std::vector<uint32_t> item_net, sitem_net;
+  const char* sv = getenv("QTN_SMALL_R");  // buckets up to this output rank: small kernel
+  const int small_r = sv ? atoi(sv) : qtn::kSmallR;
   std::vector<uint64_t> desc_base(B->n_hbm);
   for (int h = 0; h < B->n_hbm; ++h) {
     const qtn_plan* P = plans[hidx[h]];
@@ -695,12 +701,31 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   for (int32_t lev = 0; lev < max_lev; ++lev) {
     B->level_item0.push_back((uint32_t)item_desc.size());
     B->level_prefix0.push_back(prefix.size());
+    B->level_sitem0.push_back((uint32_t)sitem_desc.size());
     uint64_t acc = 0;
     prefix.push_back(0);
+    // small buckets go to the warp/CTA-per-bucket kernel, unless the level
+    // launches the streaming kernel anyway and they are few (one launch less)
+    int n_small = 0, n_large = 0;
     for (int h = 0; h < B->n_hbm; ++h) {
       const qtn_plan* P = plans[hidx[h]];
       for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
         if (P->hbm_level[bi] != lev) continue;
+        const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
+        ((int)sh->R <= small_r ? n_small : n_large) += 1;
+      }
+    }
+    const bool split_small = n_small > 0 && (n_large == 0 || n_small >= 148);
+    for (int h = 0; h < B->n_hbm; ++h) {
+      const qtn_plan* P = plans[hidx[h]];
+      for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
+        if (P->hbm_level[bi] != lev) continue;
+        const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
+        if (split_small && (int)sh->R <= small_r) {
+          sitem_desc.push_back(desc_base[h] + P->hbm_desc_off[bi]);
+          sitem_net.push_back((uint32_t)h);
+          continue;
+        }
         item_desc.push_back(desc_base[h] + P->hbm_desc_off[bi]);
         item_net.push_back((uint32_t)h);
         acc += P->hbm_tiles[bi];
@@ -710,6 +735,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     B->level_tiles.push_back(acc);
   }
   B->level_item0.push_back((uint32_t)item_desc.size());
+  B->level_sitem0.push_back((uint32_t)sitem_desc.size());
   // scalar folds
   std::vector<uint64_t> ftags;
   std::vector<uint8_t> fc64;
@@ -731,6 +757,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = (desc.resize(desc.size() + 1024, 0), upload(&B->d_desc, desc))) ||
       (rc = upload(&B->d_item_desc, item_desc)) ||
       (rc = upload(&B->d_item_net, item_net)) || (rc = upload(&B->d_tile_prefix, prefix)) ||
+      (rc = upload(&B->d_sitem_desc, sitem_desc)) || (rc = upload(&B->d_sitem_net, sitem_net)) ||
       (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
       (rc = upload(&B->d_fold_tags, ftags)) || (rc = upload(&B->d_fold_c64, fc64)) ||
       (rc = upload(&B->d_fold_first, ffirst)) || (rc = upload(&B->d_fold_pow2, fpow2)) ||
@@ -773,7 +800,8 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
   int c = B->n_smem ? 1 : 0;
   if (B->n_smem && use_setmajor(B, n_sets)) c = qtn::setmajor_launches(B->sm, n_sets);
   if (B->n_hbm) {
-    for (uint64_t t : B->level_tiles) c += t ? 1 : 0;
+    for (size_t lev = 0; lev < B->level_tiles.size(); ++lev)
+      c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0);
     c += 1;
   }
   *out = c;
@@ -1037,22 +1065,30 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
   }
   if (B->n_hbm) {
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
-      if (!B->level_tiles[lev]) continue;
       StreamLaunch L;
       std::memset(&L, 0, sizeof(L));
       L.descs = B->d_desc;
-      L.item_desc = B->d_item_desc + B->level_item0[lev];
-      L.item_net = B->d_item_net + B->level_item0[lev];
-      L.tile_prefix = B->d_tile_prefix + B->level_prefix0[lev];
-      L.n_items = B->level_item0[lev + 1] - B->level_item0[lev];
       L.n_sets = (uint32_t)n_sets;
-      L.total_tiles = B->level_tiles[lev];
       L.in_base = reinterpret_cast<const char*>(inputs);
       L.in_set_stride = 16 * set_stride;
       L.net_in_off = B->d_net_in_off;
       L.ws_base = reinterpret_cast<char*>(workspace);
       L.ws_set_stride = B->ws_per_set;
       L.net_ws_off = B->d_net_ws_off;
+      const uint32_t ns = B->level_sitem0[lev + 1] - B->level_sitem0[lev];
+      if (ns) {
+        StreamLaunch Ls = L;
+        Ls.item_desc = B->d_sitem_desc + B->level_sitem0[lev];
+        Ls.item_net = B->d_sitem_net + B->level_sitem0[lev];
+        Ls.n_items = ns;
+        if ((rc = qtn::launch_small(Ls, stream))) return rc;
+      }
+      if (!B->level_tiles[lev]) continue;
+      L.item_desc = B->d_item_desc + B->level_item0[lev];
+      L.item_net = B->d_item_net + B->level_item0[lev];
+      L.tile_prefix = B->d_tile_prefix + B->level_prefix0[lev];
+      L.n_items = B->level_item0[lev + 1] - B->level_item0[lev];
+      L.total_tiles = B->level_tiles[lev];
       if ((rc = launch_stream(L, stream))) return rc;
     }
     dim3 grid((B->n_hbm + 127) / 128, n_sets);

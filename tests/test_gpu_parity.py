@@ -354,3 +354,23 @@ def test_degenerate_networks():
     for budget in (Q.contraction.DEFAULT_SMEM_BUDGET, 0):
         assert abs(Q.contract(net, Q.ContractionOrder((0, 1)), smem_budget=budget)
                    - 6 * (3.0 + 1j)) < 1e-12
+
+
+def test_hbm_small_bucket_kernel_matches_stream_kernel(golden, monkeypatch):
+    """HBM networks: buckets of output rank <= 9 on the warp/CTA-per-bucket
+    kernel give the same values as the tile pipeline (QTN_SMALL_R=-1), and
+    both match the reference values."""
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    recs = G["modes"]["default"][:8]
+    ids = [r["edge_index"] for r in recs]
+    vals = {}
+    for small_r in ("-1", "9", "12"):
+        monkeypatch.setenv("QTN_SMALL_R", small_r)
+        plan = Q.EnergyPlan(graph, G["p"], "default", dtype="complex128", edge_ids=ids)
+        vals[small_r] = plan.zz_values(params)
+    for r in recs:
+        w = complex(*r["value"])
+        for small_r, zz in vals.items():
+            assert abs(zz[r["edge_index"]] - w) <= 1e-11 * abs(w) + 1e-12, (small_r, r["edge_index"])
