@@ -415,7 +415,7 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
       std::copy(grr.begin(), grr.end(), g[i].grun);
     }
   }
-  if (getenv("QTN_DEBUG_DESC") && R >= 18)
+  if (getenv("QTN_DEBUG_DESC") && R >= atoi(getenv("QTN_DEBUG_DESC")))
     fprintf(stderr, "desc R=%d prank=%d pc64=%d oc64=%d tb=%d ta=%d tn=%d pk=%d ng=%d nt=%d stage_k=%d\n", R,
             (int)h->p_rank, (int)pc64, (int)h->out_c64, tb, ta, tn, (int)a.p_k, ng, (int)a.nt,
             ng ? (int)g[0].stage_k : -1);

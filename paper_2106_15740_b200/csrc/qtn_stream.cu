@@ -503,11 +503,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t n = 2u << TR.nbits;
         for (uint32_t e = tid; e < n; e += kCompute) {
           const uint32_t bits = e >> 1, v = e & 1;
+          // operand loads issued 4 at a time (independent L2 round trips)
           double2 acc = make_double2(1.0, 0.0);
-          for (uint32_t k = 0; k < TR.n_ops; ++k) {
-            const SORec& O = orr[TR.first_op + k];
-            const uint64_t idx = gather(bits, O.runs, O.n_runs) | ((uint64_t)v << O.vshift);
-            acc = cmul(acc, ldg_c(resolve(O.ptr, b), idx, O.c64));
+          for (uint32_t k0 = 0; k0 < TR.n_ops; k0 += 4) {
+            double2 x[4];
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+              x[u] = make_double2(1.0, 0.0);
+              if (k0 + u < TR.n_ops) {
+                const SORec& O = orr[TR.first_op + k0 + u];
+                const uint64_t idx = gather(bits, O.runs, O.n_runs) | ((uint64_t)v << O.vshift);
+                x[u] = ldg_c(resolve(O.ptr, b), idx, O.c64);
+              }
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) acc = cmul(acc, x[u]);
           }
           if (tab_f32)
             reinterpret_cast<float2*>(S.tab)[TR.smem_off + e] = make_float2((float)acc.x, (float)acc.y);

@@ -17,10 +17,10 @@ inline uint64_t tag_ws(uint64_t byte_off) { return (2ull << kSelShift) | byte_of
 
 // pipeline geometry (overridable at build time for A/B experiments)
 #ifndef QTN_STREAM_STAGES
-#define QTN_STREAM_STAGES 4
+#define QTN_STREAM_STAGES 2
 #endif
 #ifndef QTN_TILE_BITS_C64
-#define QTN_TILE_BITS_C64 11
+#define QTN_TILE_BITS_C64 12
 #endif
 constexpr int kStreamStages = QTN_STREAM_STAGES;
 constexpr int kTileBitsC64 = QTN_TILE_BITS_C64;      // tile = 2^11 complex64 outputs
