@@ -610,6 +610,7 @@ struct qtn_batch {
   uint64_t* d_sitem_desc = nullptr;
   uint32_t* d_sitem_net = nullptr;
   std::vector<uint32_t> level_sitem0;   // first small item of each level (+ end)
+  std::vector<uint32_t> level_smax_r;   // widest small item of each level
   uint64_t* d_fold_tags = nullptr;
   uint8_t* d_fold_c64 = nullptr;
   uint32_t* d_fold_first = nullptr;
@@ -706,24 +707,33 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     prefix.push_back(0);
     // small buckets go to the warp/CTA-per-bucket kernel, unless the level
     // launches the streaming kernel anyway and they are few (one launch less)
+    // a tiny level (few output elements in all) goes entirely to the small
+    // kernel: the tile pipeline's fixed cost dominates there
     int n_small = 0, n_large = 0;
+    uint64_t lev_elems = 0;
     for (int h = 0; h < B->n_hbm; ++h) {
       const qtn_plan* P = plans[hidx[h]];
       for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
         if (P->hbm_level[bi] != lev) continue;
         const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
         ((int)sh->R <= small_r ? n_small : n_large) += 1;
+        lev_elems += 1ull << sh->R;
       }
     }
-    const bool split_small = n_small > 0 && (n_large == 0 || n_small >= 148);
+    const char* tv = getenv("QTN_TINY_LEVEL");
+    const uint64_t tiny = tv ? strtoull(tv, nullptr, 10) : (1ull << 17);
+    const bool all_small = lev_elems <= tiny;
+    const bool split_small = all_small || (n_small > 0 && (n_large == 0 || n_small >= 148));
+    uint32_t smax_r = 0;
     for (int h = 0; h < B->n_hbm; ++h) {
       const qtn_plan* P = plans[hidx[h]];
       for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
         if (P->hbm_level[bi] != lev) continue;
         const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
-        if (split_small && (int)sh->R <= small_r) {
+        if (split_small && (all_small || (int)sh->R <= small_r)) {
           sitem_desc.push_back(desc_base[h] + P->hbm_desc_off[bi]);
           sitem_net.push_back((uint32_t)h);
+          smax_r = std::max<uint32_t>(smax_r, sh->R);
           continue;
         }
         item_desc.push_back(desc_base[h] + P->hbm_desc_off[bi]);
@@ -733,6 +743,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       }
     }
     B->level_tiles.push_back(acc);
+    B->level_smax_r.push_back(smax_r);
   }
   B->level_item0.push_back((uint32_t)item_desc.size());
   B->level_sitem0.push_back((uint32_t)sitem_desc.size());
@@ -1081,7 +1092,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         Ls.item_desc = B->d_sitem_desc + B->level_sitem0[lev];
         Ls.item_net = B->d_sitem_net + B->level_sitem0[lev];
         Ls.n_items = ns;
-        if ((rc = qtn::launch_small(Ls, stream))) return rc;
+        if ((rc = qtn::launch_small(Ls, B->level_smax_r[lev], stream))) return rc;
       }
       if (!B->level_tiles[lev]) continue;
       L.item_desc = B->d_item_desc + B->level_item0[lev];

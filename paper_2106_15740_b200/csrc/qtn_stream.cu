@@ -651,6 +651,9 @@ int launch(const StreamLaunch& L, const InlineDesc& D, uint64_t total, void* str
 // out[o] = sum_v P[o | v] * prod_tables prod_ops Op[..] * prod_gathered G[..]
 // with the same index maps as the tile kernel applied to the full output
 // index o (every run list covers all output bits).
+// CTA mode (tpi = 256): blockIdx.y selects a chunk of kSmallChunk elements,
+// so a few wide buckets (tail levels of one network) still spread over SMs.
+constexpr uint32_t kSmallChunk = 1024;
 __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ StreamLaunch L,
                                                     uint32_t tpi_log2) {
   const uint32_t tpi = 1u << tpi_log2;
@@ -659,7 +662,7 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
   const uint32_t lane = threadIdx.x & (tpi - 1);
   Loc l;
   l.item = item;
-  l.set = blockIdx.y;
+  l.set = blockIdx.z;
   l.tile = 0;
   const Bases b = bases_of(L, l);
   const uint8_t* dsc = L.descs + L.item_desc[item];
@@ -671,8 +674,11 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
   const char* P = resolve(h.p, b);
   char* out = const_cast<char*>(resolve(h.out, b));
   const uint32_t r1 = h.p_rank - 1u, pk = h.p_k;
-  const uint64_t n_out = 1ull << h.R;
-  for (uint64_t o = lane; o < n_out; o += tpi) {
+  const uint64_t n_all = 1ull << h.R;
+  const uint64_t o0 = tpi == 256 ? (uint64_t)blockIdx.y * kSmallChunk : 0;
+  if (o0 >= n_all) return;
+  const uint64_t n_out = tpi == 256 ? min(n_all, o0 + kSmallChunk) : n_all;
+  for (uint64_t o = o0 + lane; o < n_out; o += tpi) {
     const uint64_t op = o & ((1ull << r1) - 1);
     const uint64_t p0 = (op & ((1ull << pk) - 1)) | ((op >> pk) << (pk + 1));
     double2 a0 = ldg_c(P, p0, h.p_c64), a1 = ldg_c(P, p0 | (1ull << pk), h.p_c64);
@@ -700,12 +706,15 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
   }
 }
 
-int launch_small(const StreamLaunch& L, void* stream) {
+int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream) {
   if (L.n_items == 0 || L.n_sets == 0) return QTN_OK;
-  // many items: a warp each; few items (tails of one network): a CTA each
+  // many items: a warp each; few items (tails of one network): CTAs of
+  // kSmallChunk elements each
   const uint32_t tpi_log2 = (uint64_t)L.n_items * L.n_sets >= 4u * 148u * 8u ? 5u : 8u;
   const uint32_t per_block = 256u >> tpi_log2;
-  dim3 grid((L.n_items + per_block - 1) / per_block, L.n_sets);
+  const uint32_t chunks =
+      tpi_log2 == 8u ? (uint32_t)(((1ull << max_r) + kSmallChunk - 1) / kSmallChunk) : 1u;
+  dim3 grid((L.n_items + per_block - 1) / per_block, chunks, L.n_sets);
   small_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(L, tpi_log2);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -126,12 +126,12 @@ struct StreamLaunch {
 
 int launch_stream(const StreamLaunch& L, void* stream);
 
-// Small buckets (output rank <= kSmallR): one warp per (item, set), lanes over
-// output elements, every operand gathered through L1/L2 from the same
+// Small buckets (output rank <= kSmallR, or every bucket of a tiny level):
+// a warp or a CTA per (item, chunk, set), threads over output elements, every operand gathered through L1/L2 from the same
 // descriptors — no tile pipeline, no shared-memory tables.  Uses L.descs,
 // L.item_desc, L.item_net, L.n_items, L.n_sets and the base/offset fields.
 constexpr int kSmallR = 9;
-int launch_small(const StreamLaunch& L, void* stream);
+int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream);
 // single descriptor with absolute pointers, descriptor passed by value
 int launch_stream_single(const std::vector<uint8_t>& desc, void* stream);
 
