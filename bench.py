@@ -59,6 +59,33 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        # in-process NVML samples taken while a timed step is executing: the
+        # timed region of a fast workload is shorter than nvidia-smi's period
+        self.nv = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+        except Exception:
+            self.nv = None
+
+    def sample_now(self):
+        """One NVML sample (clocks + event reasons) appended to rows."""
+        if self.nv is None:
+            return
+        nv, h = self.nv
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = fn(h)
+            flag = lambda b: "Active" if bits & b else "Not Active"
+            # hw_slowdown 0x8, hw_thermal 0x40, sw_thermal 0x20, sw_power_cap 0x4
+            self.rows.append([str(sm), str(mx), flag(0x8), flag(0x40), flag(0x20), flag(0x4)])
+        except Exception:
+            pass
 
     def __enter__(self):
         try:
@@ -422,6 +449,7 @@ def run_gpu(args):
             e0.record(st)
             step()
             e1.record(st)
+            clk.sample_now()  # while the step executes
             e1.synchronize()
             step_times.append(e0.elapsed_time(e1) / 1e3)
             launches += plan.launches
