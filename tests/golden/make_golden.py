@@ -208,8 +208,56 @@ def synthetic_buckets():
     return out
 
 
+def amplitude_path():
+    """Front end of the amplitude path: the reference's
+    text formats, ZZ fusion, `cost`/`amplitude` CLI output and run_benchmark
+    rows, on small instances."""
+    import contextlib
+    import io
+    import tempfile
+
+    from qtnsim.bench import BenchSpec, run_benchmark
+    from qtnsim.cli import main as cli_main
+
+    out = {"circuits": [], "cli": [], "bench": []}
+    gate = lambda g: [g.kind.value, list(g.qubits), g.param]
+    for n, p in ((4, 1), (6, 2), (8, 1)):
+        graph = Q.random_regular_graph(n, 3, 0)
+        params = Q.default_angles(p)
+        raw = Q.build_qaoa_maxcut_circuit(graph, params, fused=False)
+        fused = Q.fuse_zz(raw)
+        with tempfile.TemporaryDirectory() as d:
+            gp, cp = os.path.join(d, "g.txt"), os.path.join(d, "c.txt")
+            Q.write_graph(graph, gp)
+            Q.write_circuit(raw, cp)
+            graph_text, circ_text = open(gp).read(), open(cp).read()
+            rec = {"n": n, "p": p, "graph_text": graph_text, "circuit_text": circ_text,
+                   "raw_gates": [gate(g) for g in raw.gates],
+                   "fused_gates": [gate(g) for g in fused.gates],
+                   "fused_phase": [fused.phase.real, fused.phase.imag]}
+            out["circuits"].append(rec)
+            for mode in Q.MODE_ORDER:
+                for cmd in ("cost", "amplitude"):
+                    buf = io.StringIO()
+                    with contextlib.redirect_stdout(buf):
+                        rc = cli_main([cmd, "--circuit", cp, "--mode", mode])
+                    lines = [l for l in buf.getvalue().splitlines() if not l.startswith("order_seconds")]
+                    out["cli"].append({"n": n, "p": p, "mode": mode, "cmd": cmd, "rc": rc,
+                                       "stdout": lines})
+    spec = BenchSpec(ns=(4, 6), ps=(1, 2), seeds=(0, 1), contract=True)
+    for r in run_benchmark(spec):
+        out["bench"].append({"graph_seed": r.graph_seed, "n": r.n, "p": r.p, "mode": r.mode,
+                             "width": r.width, "memory_bytes": r.memory_bytes,
+                             "contracted": r.contracted, "amp": [r.amp_re, r.amp_im]})
+    return out
+
+
 def main():
-    which = set(sys.argv[1:]) or {"kat", "c1", "c2", "c3", "c4", "synth"}
+    which = set(sys.argv[1:]) or {"kat", "c1", "c2", "c3", "c4", "synth", "amp"}
+    if "amp" in which:
+        with open(os.path.join(HERE, "amplitude_path.json"), "w") as f:
+            json.dump(amplitude_path(), f)
+        print("amplitude path done", flush=True)
     if "kat" in which:
         with open(os.path.join(HERE, "kat.json"), "w") as f:
             json.dump(kats(), f)
