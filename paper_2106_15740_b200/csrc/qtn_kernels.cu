@@ -792,9 +792,14 @@ extern "C" int qtn_batch_input_offsets(const qtn_batch* B, int64_t* out) {
   return QTN_OK;
 }
 
+// Set-major pays ~7 us per level launch but streams at HBM speed; the
+// warp-resident executor has one launch but its throughput falls with the
+// per-set footprint (occupancy).  Measured crossovers (B200): config 2
+// (<= 8 KiB per set) between 64 and 128 sets, config 3 (up to 78 KiB per
+// set) below 64.  QTN_SETMAJOR_MIN_SETS overrides (read per call).
 static bool use_setmajor(const qtn_batch* B, int32_t n_sets) {
-  const char* v = getenv("QTN_SETMAJOR_MIN_SETS");  // read per call: tests switch it
-  const int min_sets = v ? atoi(v) : 64;
+  const char* v = getenv("QTN_SETMAJOR_MIN_SETS");
+  const int min_sets = v ? atoi(v) : (B->warp_bytes <= 8192u ? 128 : 32);
   return B->sm && min_sets > 0 && n_sets >= min_sets;
 }
 
