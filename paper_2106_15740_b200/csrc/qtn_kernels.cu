@@ -20,6 +20,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <vector>
 
 #include "qtn_internal.h"
@@ -574,6 +576,19 @@ static int upload(T** dst, const std::vector<T>& v) {
   return rc;
 }
 
+// The launch sequence of one evaluation (tensorgen, level launches, folds)
+// is captured once per (buffers, set count) into a CUDA graph and replayed:
+// one launch instead of up to ~80 (QTN_GRAPHS=0 disables).
+struct GraphKey {
+  const void *angles, *inputs, *ws, *results;
+  int32_t n_angles, n_sets;
+  bool sm;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(angles, inputs, ws, results, n_angles, n_sets, sm) <
+           std::tie(o.angles, o.inputs, o.ws, o.results, o.n_angles, o.n_sets, o.sm);
+  }
+};
+
 struct qtn_batch {
   int n = 0;
   int64_t set_elems = 0;
@@ -611,6 +626,9 @@ struct qtn_batch {
   uint32_t* d_sitem_net = nullptr;
   std::vector<uint32_t> level_sitem0;   // first small item of each level (+ end)
   std::vector<uint32_t> level_smax_r;   // widest small item of each level
+  // captured evaluations (qtn_batch_execute_angles)
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  cudaStream_t cap_stream = nullptr;
   uint64_t* d_fold_tags = nullptr;
   uint8_t* d_fold_c64 = nullptr;
   uint32_t* d_fold_first = nullptr;
@@ -620,6 +638,8 @@ struct qtn_batch {
 
 extern "C" int qtn_batch_destroy(qtn_batch* B) {
   if (!B) return QTN_OK;
+  for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
+  if (B->cap_stream) cudaStreamDestroy(B->cap_stream);
   for (void* p : {(void*)B->d_prog, (void*)B->d_prog_off, (void*)B->d_in_off,
                   (void*)B->d_smem_index, (void*)B->d_desc, (void*)B->d_item_desc,
                   (void*)B->d_item_net, (void*)B->d_tile_prefix, (void*)B->d_net_in_off,
@@ -976,9 +996,55 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
   return QTN_OK;
 }
 
+static int execute_angles_direct(qtn_batch* B, const double* angles, int32_t n_angles,
+                                 int32_t n_sets, void* inputs_scratch, void* workspace,
+                                 void* results, void* stream);
+
 extern "C" int qtn_batch_execute_angles(qtn_batch* B, const double* angles, int32_t n_angles,
                                         int32_t n_sets, void* inputs_scratch, void* workspace,
                                         void* results, void* stream) {
+  const char* gv = getenv("QTN_GRAPHS");
+  int32_t n_launch = 0;
+  if (B) qtn_batch_launches(B, n_sets, &n_launch);
+  if (!B || (gv && gv[0] == '0') || n_launch <= 2)  // a single executor launch: nothing to save
+    return execute_angles_direct(B, angles, n_angles, n_sets, inputs_scratch, workspace, results,
+                                 stream);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const GraphKey key{angles, inputs_scratch, workspace, results, n_angles, n_sets,
+                     use_setmajor(B, n_sets)};
+  auto it = B->graphs.find(key);
+  if (it == B->graphs.end()) {
+    if (B->graphs.size() >= 16) {  // bounded cache
+      for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
+      B->graphs.clear();
+    }
+    if (!B->cap_stream && cudaStreamCreateWithFlags(&B->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "capture stream");
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(B->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(e, "graph capture begin");
+    int rc = execute_angles_direct(B, angles, n_angles, n_sets, inputs_scratch, workspace, results,
+                                   B->cap_stream);
+    e = cudaStreamEndCapture(B->cap_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "graph capture end");
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
+    it = B->graphs.emplace(key, ex).first;
+  }
+  cudaError_t e = cudaGraphLaunch(it->second, st);
+  if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+  return QTN_OK;
+}
+
+static int execute_angles_direct(qtn_batch* B, const double* angles, int32_t n_angles,
+                                 int32_t n_sets, void* inputs_scratch, void* workspace,
+                                 void* results, void* stream) {
   if (!B || !angles || !B->has_recipes) {
     set_error("qtn_batch_execute_angles: needs qtn_batch_set_recipes first");
     return QTN_EINVAL;
