@@ -211,6 +211,16 @@ int qtn_batch_execute_angles(qtn_batch* batch, const double* angles_dev, int32_t
 int qtn_energy_reduce(const void* values_dev, const double* weights_dev, int32_t n,
                       int32_t n_sets, double* energies_dev, void* zz_sum_dev, void* stream);
 
+/* Host-to-host energy evaluation, the QAOA optimiser's call: copy n_sets
+ * angle vectors from host memory (any host pointer; staged through pinned
+ * memory owned by the batch) to angles_dev, run qtn_batch_execute_angles and
+ * qtn_energy_reduce on `stream`, copy the energies back to energies_host and
+ * wait for the stream.  Device buffers as for those two calls. */
+int qtn_batch_energies_host(qtn_batch* batch, const double* angles_host, int32_t n_angles,
+                            int32_t n_sets, double* angles_dev, void* inputs_scratch,
+                            void* workspace, void* results, const double* weights_dev,
+                            double* energies_dev, double* energies_host, void* stream);
+
 /* --------------------------------------------------- single-bucket entry */
 
 /* One bucket: out[o] = sum_{v in {0,1}} prod_t T_t[idx_t(o, v)] over

@@ -184,6 +184,10 @@ class PlanBatch:
         N.check(N.lib.qtn_batch_launches(self._h, int(n_sets), C.byref(nl)))
         return int(nl.value) + (1 if (self.has_hbm and self._recipes_set) else 0)
 
+    @property
+    def handle(self):
+        return self._h
+
     def uses_setmajor(self, n_sets: int) -> bool:
         """Whether n_sets input sets run the small networks set-major."""
         f = C.c_int32()

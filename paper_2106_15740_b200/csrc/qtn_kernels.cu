@@ -629,6 +629,9 @@ struct qtn_batch {
   // captured evaluations (qtn_batch_execute_angles)
   std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaStream_t cap_stream = nullptr;
+  // pinned staging of qtn_batch_energies_host
+  double* pin = nullptr;
+  size_t pin_doubles = 0;
   uint64_t* d_fold_tags = nullptr;
   uint8_t* d_fold_c64 = nullptr;
   uint32_t* d_fold_first = nullptr;
@@ -640,6 +643,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
   if (!B) return QTN_OK;
   for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
   if (B->cap_stream) cudaStreamDestroy(B->cap_stream);
+  if (B->pin) cudaFreeHost(B->pin);
   for (void* p : {(void*)B->d_prog, (void*)B->d_prog_off, (void*)B->d_in_off,
                   (void*)B->d_smem_index, (void*)B->d_desc, (void*)B->d_item_desc,
                   (void*)B->d_item_net, (void*)B->d_tile_prefix, (void*)B->d_net_in_off,
@@ -1217,5 +1221,42 @@ extern "C" int qtn_energy_reduce(const void* values, const double* weights, int3
                                        energies, reinterpret_cast<double2*>(zz_sum));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "energy launch");
+  return QTN_OK;
+}
+
+extern "C" int qtn_batch_energies_host(qtn_batch* B, const double* angles_host, int32_t n_angles,
+                                       int32_t n_sets, double* angles_dev, void* inputs_scratch,
+                                       void* workspace, void* results, const double* weights_dev,
+                                       double* energies_dev, double* energies_host, void* stream) {
+  if (!B || !angles_host || !angles_dev || !energies_dev || !energies_host || n_sets < 1 ||
+      n_angles < 1) {
+    set_error("qtn_batch_energies_host: bad arguments");
+    return QTN_EINVAL;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t na = (size_t)n_sets * n_angles, need = na + (size_t)n_sets;
+  if (B->pin_doubles < need) {
+    if (B->pin) cudaFreeHost(B->pin);
+    B->pin = nullptr;
+    B->pin_doubles = 0;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&B->pin), need * sizeof(double),
+                                  cudaHostAllocDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "pinned staging");
+    B->pin_doubles = need;
+  }
+  std::memcpy(B->pin, angles_host, na * sizeof(double));
+  cudaError_t e = cudaMemcpyAsync(angles_dev, B->pin, na * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "angles H2D");
+  int rc = qtn_batch_execute_angles(B, angles_dev, n_angles, n_sets, inputs_scratch, workspace,
+                                    results, stream);
+  if (rc) return rc;
+  if ((rc = qtn_energy_reduce(results, weights_dev, B->n, n_sets, energies_dev, nullptr, stream)))
+    return rc;
+  double* eh = B->pin + na;
+  e = cudaMemcpyAsync(eh, energies_dev, (size_t)n_sets * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(e, "energies D2H");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "energies sync");
+  std::memcpy(energies_host, eh, (size_t)n_sets * sizeof(double));
   return QTN_OK;
 }

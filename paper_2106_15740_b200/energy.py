@@ -250,6 +250,18 @@ class EnergyPlan:
             raise ValueError(f"expected {2 * self.p} angles per set, got {a.shape[1]}")
         b = self._buffers(a.shape[0])
         st = t.cuda.current_stream(self._device)
+        if self.fused:
+            # one native call: H2D of the angles, the captured evaluation,
+            # the energy reduction, D2H and the stream wait
+            a = np.ascontiguousarray(a)
+            out = np.empty(a.shape[0], dtype=np.float64)
+            N.check(N.lib.qtn_batch_energies_host(
+                self._batch.handle, a.ctypes.data, 2 * self.p, a.shape[0], b["angles"].data_ptr(),
+                b["inputs"].data_ptr(), b["ws"].data_ptr(), b["res"].data_ptr(),
+                self._weights.data_ptr(), b["energy"].data_ptr(), out.ctypes.data,
+                st.cuda_stream), "energies")
+            self.launches = b["launches"]
+            return out
         b["angles_host"].numpy()[...] = a
         b["angles"].copy_(b["angles_host"], non_blocking=True)
         self.launch(b["angles"], st)
