@@ -32,7 +32,10 @@
 namespace qtn {
 namespace {
 
-constexpr int kCompute = 256;               // 8 consumer warps (9 warps/block
+#ifndef QTN_STREAM_COMPUTE
+#define QTN_STREAM_COMPUTE 256
+#endif
+constexpr int kCompute = QTN_STREAM_COMPUTE;  // 8 consumer warps (9 warps/block
                                             // leave 168 registers per thread)
 constexpr int kWarps = kCompute / 32;
 constexpr int kThreads = kCompute + 32;     // + 1 producer warp
