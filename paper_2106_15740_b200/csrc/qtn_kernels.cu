@@ -1175,7 +1175,12 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       L.tile_prefix = B->d_tile_prefix + B->level_prefix0[lev];
       L.n_items = B->level_item0[lev + 1] - B->level_item0[lev];
       L.total_tiles = B->level_tiles[lev];
-      if ((rc = launch_stream(L, stream))) return rc;
+      // many items of few tiles each (per-item setup dominates): the
+      // 16-consumer-warp build hides more latency (measured: config 3 default)
+      const char* wv = getenv("QTN_WIDE_TPI");
+      const uint64_t wide_tpi = wv ? strtoull(wv, nullptr, 10) : 32;
+      const bool wide = L.total_tiles < wide_tpi * L.n_items;
+      if ((rc = launch_stream(L, stream, wide))) return rc;
     }
     dim3 grid((B->n_hbm + 127) / 128, n_sets);
     hbm_fold_kernel<<<grid, 128, 0, st>>>(

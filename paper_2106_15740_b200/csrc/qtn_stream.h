@@ -124,7 +124,16 @@ struct StreamLaunch {
   const int64_t* net_ws_off;    // device, bytes
 };
 
-int launch_stream(const StreamLaunch& L, void* stream);
+// wide: the 512-consumer build of the kernel (levels of many small items)
+int launch_stream(const StreamLaunch& L, void* stream, bool wide = false);
+namespace s256 {
+int launch_list(const StreamLaunch& L, void* stream);
+int launch_one(const std::vector<uint8_t>& desc, void* stream);
+}  // namespace s256
+namespace s512 {
+int launch_list(const StreamLaunch& L, void* stream);
+int launch_one(const std::vector<uint8_t>& desc, void* stream);
+}  // namespace s512
 
 // Small buckets (output rank <= kSmallR, or every bucket of a tiny level):
 // a warp or a CTA per (item, chunk, set), threads over output elements, every operand gathered through L1/L2 from the same
