@@ -25,6 +25,7 @@ namespace QTN_STREAM_NS {
 constexpr int kCompute = QTN_STREAM_COMPUTE;  // 8 consumer warps (9 warps/block
                                             // leave 168 registers per thread)
 constexpr int kWarps = kCompute / 32;
+constexpr bool kPrecomp = kCompute <= 256;
 constexpr int kThreads = kCompute + 32;     // + 1 producer warp
 constexpr int kStages = kStreamStages;
 constexpr int kChunkBytes = kStreamChunk;     // primary slice per stage
@@ -241,8 +242,11 @@ struct ThreadState {
   uint32_t ts;                        // staged slice index, lane part
   uint32_t ta, r1;                    // tile-local primary bits, primary rank - 1
   uint32_t stage_k;                   // 0xff: operand 0 not staged
-  uint32_t pi0[kJ];                   // per element j: primary index (v = 0) in the chunk
-  uint64_t ooff[kJ];                  // per element j: output offset within the tile
+  // per element j: primary index (v = 0) in the chunk and output offset in
+  // the tile, precomputed per descriptor (256-consumer build; the
+  // 512-consumer build recomputes them to stay within 96 registers)
+  uint32_t pi0[kPrecomp ? kJ : 1];
+  uint64_t ooff[kPrecomp ? kJ : 1];
 };
 
 // Generic tile: any dtypes, any operand counts, partial tiles.  Inlined
@@ -316,7 +320,17 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
     tbs[q] = (uint32_t)gather(obase, tr[q].runs, tr[q].n_runs) | T.tt[q];
 #pragma unroll
   for (int j = 0; j < kJ; ++j) {
-    const uint32_t i0 = T.pi0[j];
+    uint32_t i0;
+    uint64_t oo;
+    if constexpr (kPrecomp) {
+      i0 = T.pi0[j];
+      oo = T.ooff[j];
+    } else {
+      const uint32_t e = tid + (uint32_t)j * kCompute;
+      const uint32_t pe = e & T.pmask;
+      i0 = T.split ? pe : ((pe & ((1u << T.pk) - 1u)) | ((pe >> T.pk) << (T.pk + 1)));
+      oo = tile_off(e, T.ta, T.r1);
+    }
     const uint32_t i1 = i0 + T.pstep;
     if constexpr (F32) {
       float2 a0 = reinterpret_cast<const float2*>(chunk)[i0];
@@ -355,7 +369,7 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
         a0 = cmulf(a0, x);
         a1 = cmulf(a1, y);
       }
-      reinterpret_cast<float2*>(T.out)[obase + T.ooff[j]] = make_float2(a0.x + a1.x, a0.y + a1.y);
+      reinterpret_cast<float2*>(T.out)[obase + oo] = make_float2(a0.x + a1.x, a0.y + a1.y);
     } else {
       double2 a0 = reinterpret_cast<const double2*>(chunk)[i0];
       double2 a1 = reinterpret_cast<const double2*>(chunk)[i1];
@@ -387,7 +401,7 @@ __device__ __forceinline__ void tile_fast(const ThreadState& T, const uint8_t* c
           a1 = cmul(a1, ldg_c(T.gptr[g], idx + (1ull << T.gvs[g]), T.gc64[g]));
         }
       }
-      reinterpret_cast<double2*>(T.out)[obase + T.ooff[j]] = make_double2(a0.x + a1.x, a0.y + a1.y);
+      reinterpret_cast<double2*>(T.out)[obase + oo] = make_double2(a0.x + a1.x, a0.y + a1.y);
     }
   }
 }
@@ -562,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (T.ng == 1 && T.stage_k != 0xffu) variant = 13 + (pc64 ? 3u : 0u) + T.nt;
       }
       // per-element primary index and output offset of the fast paths
-      if (variant != 0) {
+      if (kPrecomp && variant != 0) {
 #pragma unroll
         for (int j = 0; j < kJ; ++j) {
           const uint32_t e = tid + (uint32_t)j * kCompute;
