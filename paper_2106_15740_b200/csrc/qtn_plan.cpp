@@ -324,7 +324,7 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
     const char* tmv = getenv("QTN_TN_MAX");  // experiment knob: cap the new-bit tile part
     const int tn_max = tmv ? atoi(tmv) : 64;
     const char* swv = getenv("QTN_STAGE_W");
-    const double stage_w = swv ? atof(swv) : 256.0;  // measured: cp.async-gathered entries cost ~8x bulk bytes
+    const double stage_w = swv ? atof(swv) : 1024.0;  // measured: a cp.async-gathered entry costs far more than a bulk byte
     for (int tn_c = std::max(0, tb - rp1); tn_c <= std::min(std::min(dnew, tb), std::max(tn_max, tb - rp1)); ++tn_c) {
       const int ta_c = tb - tn_c;
       if (ta_c > rp1 || ta_c < 0) continue;
