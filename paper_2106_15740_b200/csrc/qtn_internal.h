@@ -161,6 +161,16 @@ struct TensorRec {
   int rank() const { return (int)vars.size(); }
 };
 
+// A chain of single-operand buckets fused into one multi-variable sum
+// (HBM executor): out[o] = sum over the k eliminated bits of src.
+constexpr int kMaxRed = 12;
+struct RedRec {
+  int32_t level = 0;
+  uint64_t src = 0, out = 0;   // tagged pointers (qtn_stream.h)
+  uint8_t src_c64 = 0, out_c64 = 0, R = 0, k = 0;
+  uint8_t pos[kMaxRed] = {};   // eliminated bit positions in src's index, ascending
+};
+
 struct BucketRec {
   int32_t v;
   std::vector<int32_t> ops;    // tensor ids, ascending (reference order)
@@ -191,7 +201,8 @@ struct qtn_plan {
   // elimination tree (level-synchronous execution) and its tile count.
   std::vector<uint8_t> hbm_desc;
   std::vector<uint64_t> hbm_desc_off;
-  std::vector<int32_t> hbm_level;
+  std::vector<int32_t> hbm_level;        // -1: absorbed into a fused reduction
+  std::vector<qtn::RedRec> hbm_red;      // fused single-operand chains
   std::vector<uint64_t> hbm_tiles;
   int32_t n_levels = 0;
   // Set-major form of an SMEM-eligible network (qtn_setmajor.cu): angle

@@ -626,6 +626,10 @@ struct qtn_batch {
   uint32_t* d_sitem_net = nullptr;
   std::vector<uint32_t> level_sitem0;   // first small item of each level (+ end)
   std::vector<uint32_t> level_smax_r;   // widest small item of each level
+  // fused single-operand chains per level (reduce_kernel)
+  qtn::RedDev* d_red = nullptr;
+  uint32_t* d_red_prefix = nullptr;
+  std::vector<uint32_t> level_red0, level_rprefix0, level_rchunks;
   // captured evaluations (qtn_batch_execute_angles)
   std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaStream_t cap_stream = nullptr;
@@ -649,7 +653,8 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_item_net, (void*)B->d_tile_prefix, (void*)B->d_net_in_off,
                   (void*)B->d_net_ws_off, (void*)B->d_fold_tags, (void*)B->d_fold_c64,
                   (void*)B->d_fold_first, (void*)B->d_fold_pow2, (void*)B->d_hbm_index,
-                  (void*)B->d_hbm_rec, (void*)B->d_sitem_desc, (void*)B->d_sitem_net})
+                  (void*)B->d_hbm_rec, (void*)B->d_sitem_desc, (void*)B->d_sitem_net,
+                  (void*)B->d_red, (void*)B->d_red_prefix})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
   delete B;
@@ -738,7 +743,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     for (int h = 0; h < B->n_hbm; ++h) {
       const qtn_plan* P = plans[hidx[h]];
       for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
-        if (P->hbm_level[bi] != lev) continue;
+        if (P->hbm_level[bi] != lev || !P->hbm_tiles[bi]) continue;  // 0 tiles: fused chain
         const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
         ((int)sh->R <= small_r ? n_small : n_large) += 1;
         lev_elems += 1ull << sh->R;
@@ -752,7 +757,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     for (int h = 0; h < B->n_hbm; ++h) {
       const qtn_plan* P = plans[hidx[h]];
       for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
-        if (P->hbm_level[bi] != lev) continue;
+        if (P->hbm_level[bi] != lev || !P->hbm_tiles[bi]) continue;  // 0 tiles: fused chain
         const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
         if (split_small && (all_small || (int)sh->R <= small_r)) {
           sitem_desc.push_back(desc_base[h] + P->hbm_desc_off[bi]);
@@ -771,6 +776,35 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   }
   B->level_item0.push_back((uint32_t)item_desc.size());
   B->level_sitem0.push_back((uint32_t)sitem_desc.size());
+  // fused reductions, level-major over all HBM networks
+  std::vector<qtn::RedDev> reds;
+  std::vector<uint32_t> rprefix;
+  for (int32_t lev = 0; lev < max_lev; ++lev) {
+    B->level_red0.push_back((uint32_t)reds.size());
+    B->level_rprefix0.push_back((uint32_t)rprefix.size());
+    uint32_t acc = 0;
+    for (int h = 0; h < B->n_hbm; ++h) {
+      for (const auto& r : plans[hidx[h]]->hbm_red) {
+        if (r.level != lev) continue;
+        qtn::RedDev d{};
+        d.src = r.src;
+        d.out = r.out;
+        d.net = (uint32_t)h;
+        d.src_c64 = r.src_c64;
+        d.out_c64 = r.out_c64;
+        d.R = r.R;
+        d.k = r.k;
+        for (int q = 0; q < r.k; ++q) d.pos[q] = r.pos[q];
+        reds.push_back(d);
+        rprefix.push_back(acc);
+        const uint64_t ch = qtn::red_chunk(r.k);
+        acc += (uint32_t)(((1ull << r.R) + ch - 1) / ch);
+      }
+    }
+    rprefix.push_back(acc);
+    B->level_rchunks.push_back(acc);
+  }
+  B->level_red0.push_back((uint32_t)reds.size());
   // scalar folds
   std::vector<uint64_t> ftags;
   std::vector<uint8_t> fc64;
@@ -793,6 +827,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_item_desc, item_desc)) ||
       (rc = upload(&B->d_item_net, item_net)) || (rc = upload(&B->d_tile_prefix, prefix)) ||
       (rc = upload(&B->d_sitem_desc, sitem_desc)) || (rc = upload(&B->d_sitem_net, sitem_net)) ||
+      (rc = upload(&B->d_red, reds)) || (rc = upload(&B->d_red_prefix, rprefix)) ||
       (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
       (rc = upload(&B->d_fold_tags, ftags)) || (rc = upload(&B->d_fold_c64, fc64)) ||
       (rc = upload(&B->d_fold_first, ffirst)) || (rc = upload(&B->d_fold_pow2, fpow2)) ||
@@ -841,7 +876,8 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
   if (B->n_smem && use_setmajor(B, n_sets)) c = qtn::setmajor_launches(B->sm, n_sets);
   if (B->n_hbm) {
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev)
-      c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0);
+      c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
+           (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0);
     c += 1;
   }
   *out = c;
@@ -1161,6 +1197,11 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       L.ws_base = reinterpret_cast<char*>(workspace);
       L.ws_set_stride = B->ws_per_set;
       L.net_ws_off = B->d_net_ws_off;
+      const uint32_t nr = B->level_red0[lev + 1] - B->level_red0[lev];
+      if (nr && (rc = qtn::launch_reduce(L, B->d_red + B->level_red0[lev],
+                                         B->d_red_prefix + B->level_rprefix0[lev], nr,
+                                         B->level_rchunks[lev], stream)))
+        return rc;
       const uint32_t ns = B->level_sitem0[lev + 1] - B->level_sitem0[lev];
       if (ns) {
         StreamLaunch Ls = L;

@@ -110,6 +110,132 @@ int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream) {
   return QTN_OK;
 }
 
+// ---- fused single-operand chains (multi-variable partial traces)
+// out[o] = sum over the 2^k source entries spread(o) | offs[m].  A CTA of 8
+// warps covers 32 * (8 / G) consecutive outputs: lanes = outputs (32
+// consecutive outputs read 32 consecutive source entries for a given m:
+// coalesced), G = min(8, 2^k) warps split the m range, each lane keeping 4
+// loads in flight; the G partial sums meet in shared memory.  Every source
+// entry is read once and no intermediate of the chain is stored.
+__global__ void __launch_bounds__(256) reduce_kernel(const __grid_constant__ StreamLaunch L,
+                                                     const RedDev* __restrict__ items,
+                                                     const uint32_t* __restrict__ prefix,
+                                                     uint32_t n_items) {
+  __shared__ uint64_t offs[256];
+  __shared__ double2 part[8][32];
+  const uint32_t cb = blockIdx.x;
+  uint32_t lo = 0, hi = n_items;  // last item with prefix <= cb
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (prefix[mid] <= cb) lo = mid;
+    else hi = mid;
+  }
+  const RedDev r = items[lo];
+  const uint32_t k = r.k, nm = 1u << k;
+  const uint32_t G = nm < 8u ? nm : 8u;          // warps per output block
+  const uint32_t blocks = 8u / G;                // output blocks of 32 per CTA
+  for (uint32_t m = threadIdx.x; m < nm; m += 256) {
+    uint64_t o = 0;
+    for (uint32_t q = 0; q < k; ++q) o |= (uint64_t)((m >> q) & 1u) << r.pos[q];
+    offs[m] = o;
+  }
+  __syncthreads();
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t blk = warp / G, g = warp % G;
+  const uint64_t n_out = 1ull << r.R;
+  const uint32_t set = blockIdx.y;
+  Bases b;
+  b.in = L.in_base + (int64_t)set * L.in_set_stride + L.net_in_off[r.net];
+  b.ws = L.ws_base + (int64_t)set * L.ws_set_stride + L.net_ws_off[r.net];
+  const char* src = resolve(r.src, b);
+  char* out = const_cast<char*>(resolve(r.out, b));
+  // kRedIters sub-chunks of 32 * blocks outputs per CTA
+  for (uint32_t it = 0; it < kRedIters; ++it) {
+    const uint64_t o = (((uint64_t)(cb - prefix[lo]) * kRedIters + it) * blocks + blk) * 32u + lane;
+    const bool valid = o < n_out;
+    uint64_t idx = valid ? o : 0;
+    for (uint32_t q = 0; q < k; ++q) {
+      const uint32_t p = r.pos[q];
+      idx = (idx & ((1ull << p) - 1)) | ((idx >> p) << (p + 1));
+    }
+    double2 a[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
+                    make_double2(0.0, 0.0)};
+    if (valid) {
+      uint32_t m = g;
+      if (r.src_c64) {
+        const float2* s2 = reinterpret_cast<const float2*>(src);
+        for (; m + 3 * G < nm; m += 4 * G) {
+          float2 x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = __ldg(s2 + (idx | offs[m + u * G]));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            a[u].x += x[u].x;
+            a[u].y += x[u].y;
+          }
+        }
+        for (; m < nm; m += G) {
+          const float2 x = __ldg(s2 + (idx | offs[m]));
+          a[0].x += x.x;
+          a[0].y += x.y;
+        }
+      } else {
+        const double2* s2 = reinterpret_cast<const double2*>(src);
+        for (; m + 3 * G < nm; m += 4 * G) {
+          double2 x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = __ldg(s2 + (idx | offs[m + u * G]));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            a[u].x += x[u].x;
+            a[u].y += x[u].y;
+          }
+        }
+        for (; m < nm; m += G) {
+          const double2 x = __ldg(s2 + (idx | offs[m]));
+          a[0].x += x.x;
+          a[0].y += x.y;
+        }
+      }
+    }
+    if (G > 1) {
+      part[warp][lane] = make_double2((a[0].x + a[1].x) + (a[2].x + a[3].x),
+                                      (a[0].y + a[1].y) + (a[2].y + a[3].y));
+      __syncthreads();
+    }
+    if (g == 0 && valid) {
+      double2 t;
+      if (G > 1) {
+        t = part[warp][lane];
+        for (uint32_t q = 1; q < G; ++q) {
+          t.x += part[warp + q][lane].x;
+          t.y += part[warp + q][lane].y;
+        }
+      } else {
+        t = make_double2((a[0].x + a[1].x) + (a[2].x + a[3].x), (a[0].y + a[1].y) + (a[2].y + a[3].y));
+      }
+      if (r.out_c64)
+        reinterpret_cast<float2*>(out)[o] = make_float2((float)t.x, (float)t.y);
+      else
+        reinterpret_cast<double2*>(out)[o] = t;
+    }
+    if (G > 1) __syncthreads();  // part reused by the next sub-chunk
+  }
+}
+
+int launch_reduce(const StreamLaunch& L, const RedDev* items, const uint32_t* prefix,
+                  uint32_t n_items, uint32_t total_chunks, void* stream) {
+  if (!n_items || !total_chunks || !L.n_sets) return QTN_OK;
+  dim3 grid(total_chunks, L.n_sets);
+  reduce_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(L, items, prefix, n_items);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("reduce_kernel launch: ") + cudaGetErrorString(e));
+    return QTN_ECUDA;
+  }
+  return QTN_OK;
+}
+
 int launch_stream(const StreamLaunch& L, void* stream, bool wide) {
   return wide ? s512::launch_list(L, stream) : s256::launch_list(L, stream);
 }

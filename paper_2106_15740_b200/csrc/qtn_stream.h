@@ -140,6 +140,23 @@ int launch_one(const std::vector<uint8_t>& desc, void* stream);
 // descriptors — no tile pipeline, no shared-memory tables.  Uses L.descs,
 // L.item_desc, L.item_net, L.n_items, L.n_sets and the base/offset fields.
 constexpr int kSmallR = 9;
+
+// Fused single-operand chains: out[o] = sum over k eliminated source bits.
+struct RedDev {
+  uint64_t src, out;            // tagged pointers
+  uint32_t net;                 // network index (bases)
+  uint8_t src_c64, out_c64, R, k;
+  uint8_t pos[8];               // eliminated bit positions, ascending
+};
+static_assert(sizeof(RedDev) == 32, "RedDev");
+// outputs per CTA: kRedIters sub-chunks of 32 * 8 / min(8, 2^k)
+constexpr uint32_t kRedIters = 16;
+inline uint32_t red_chunk(uint32_t k) {
+  return kRedIters * 32u * (8u / ((1u << k) < 8u ? (1u << k) : 8u));
+}
+// items: device array; prefix: device, n_items + 1 CTA prefix (chunks of red_chunk(k))
+int launch_reduce(const StreamLaunch& L, const RedDev* items, const uint32_t* prefix,
+                  uint32_t n_items, uint32_t total_chunks, void* stream);
 int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream);
 // single descriptor with absolute pointers, descriptor passed by value
 int launch_stream_single(const std::vector<uint8_t>& desc, void* stream);

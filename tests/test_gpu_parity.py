@@ -399,3 +399,28 @@ def test_setmajor_large_batch_and_graph_replay(golden, setmajor_min_sets):
     assert np.allclose(g2, w2, rtol=1e-12, atol=1e-11)
     assert np.array_equal(g1, g1b)
     assert not np.allclose(g1, g2)
+
+
+@pytest.mark.parametrize("min_pos", ["0", "3"])
+def test_fused_reduction_chains_opt_in(golden, monkeypatch, min_pos):
+    """QTN_FUSE_REDUCE=1: chains of single-operand buckets run as one
+    multi-variable sum (reduce_kernel) — same values as the reference."""
+    monkeypatch.setenv("QTN_FUSE_REDUCE", "1")
+    monkeypatch.setenv("QTN_FUSE_MIN_POS", min_pos)
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    recs = G["modes"]["default"][:6]
+    plan = Q.EnergyPlan(graph, G["p"], "default", dtype="complex128",
+                        edge_ids=[r["edge_index"] for r in recs])
+    assert any(j.plan.executor == 1 for j in plan.jobs)
+    zz = plan.zz_values(params)
+    for r in recs:
+        w = complex(*r["value"])
+        assert abs(zz[r["edge_index"]] - w) <= 1e-11 * abs(w) + 1e-12
+    G4 = golden("config4.json")
+    rec = [r for r in G4["modes"]["zz+diagonal"] if r["edge_index"] == 16][0]
+    g4 = Q.random_regular_graph(G4["n"], 3, 0)
+    p4 = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype="complex64", edge_ids=[16])
+    z4 = p4.zz_values(Q.QaoaParams(G4["gammas"], G4["betas"]))[16]
+    assert abs(z4 - complex(*rec["value"])) / abs(complex(*rec["value"])) < 1e-5
