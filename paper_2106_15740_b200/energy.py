@@ -23,7 +23,6 @@ single all-reduce of the per-set partial energies (float64) finishes the job.
 
 from __future__ import annotations
 
-import ctypes as C
 import heapq
 import os
 from concurrent.futures import ThreadPoolExecutor

@@ -24,7 +24,7 @@ from __future__ import annotations
 import itertools
 
 from .network import LineGraph
-from .ordering import ContractionOrder, CostReport, contraction_width
+from .ordering import ContractionOrder, contraction_width
 
 __all__ = ["choose_slice_vars", "slice_assignments", "remove_vertices"]
 

@@ -4,7 +4,6 @@ the CLI and the run_benchmark sweep, against outputs of the real reference
 
 import contextlib
 import io
-import os
 
 import pytest
 
