@@ -1031,8 +1031,12 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
   qtn::setmajor_destroy(B->sm);
   B->sm = nullptr;
   if (!B->smem_plans.empty() &&
-      (rc = qtn::setmajor_build(&B->sm, B->smem_plans, B->smem_global, rec, offsets, B->n)))
-    return rc;
+      (rc = qtn::setmajor_build(&B->sm, B->smem_plans, B->smem_global, rec, offsets, B->n))) {
+    // a structural limit of the set-major form (more than 8 operands in a
+    // bucket, ...): the small networks keep the warp-resident executor
+    B->sm = nullptr;
+    if (rc != QTN_EINVAL) return rc;
+  }
   return QTN_OK;
 }
 
