@@ -424,3 +424,21 @@ def test_fused_reduction_chains_opt_in(golden, monkeypatch, min_pos):
     p4 = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype="complex64", edge_ids=[16])
     z4 = p4.zz_values(Q.QaoaParams(G4["gammas"], G4["betas"]))[16]
     assert abs(z4 - complex(*rec["value"])) / abs(complex(*rec["value"])) < 1e-5
+
+
+def test_setmajor_limit_falls_back_to_warp_executor():
+    """Complete graph K8 at p=1: buckets with 9 operands exceed the set-major
+    form (<= 8); a 200-set evaluation then runs on the warp-resident executor
+    and still matches the oracle."""
+    import itertools
+
+    graph = Q.ProblemGraph(8, tuple(itertools.combinations(range(8), 2)))
+    plan = Q.EnergyPlan(graph, 1, "zz+diagonal", dtype="complex128")
+    rng = np.random.default_rng(5)
+    sets = rng.uniform(0, math.pi, (200, 2))
+    got = plan.energies(sets)
+    assert not plan._batch.uses_setmajor(200)
+    edges = [tuple(e) for e in graph.edges]
+    for s in (0, 199):
+        zz = [O.edge_zz(8, edges, e, [sets[s, 0]], [sets[s, 1]], "zz+diagonal") for e in edges]
+        assert abs(got[s] - O.energy_from_zz(zz)) < 1e-10
