@@ -21,7 +21,9 @@ CUDA device these functions raise.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
+import threading
 
 import numpy as np
 
@@ -199,8 +201,8 @@ class PlanBatch:
         N.check(N.lib.qtn_batch_workspace_bytes(self._h, int(n_sets), C.byref(w)))
         return int(w.value)
 
-    def pack(self, datas_list) -> np.ndarray:
-        host = np.zeros(max(self.set_elems, 1), dtype=np.complex128)
+    def pack(self, datas_list, out: np.ndarray | None = None) -> np.ndarray:
+        host = out if out is not None else np.zeros(max(self.set_elems, 1), dtype=np.complex128)
         for p, off, datas in zip(self.plans, self.input_offsets, datas_list):
             p.pack(datas, host[off: off + p.input_elems])
         return host
@@ -254,14 +256,66 @@ def _run_plans(plans, datas_list):
     return [complex(x) for x in out]
 
 
+class _CachedRun:
+    """A compiled plan with its device program and buffers, reused by every
+    contract() call on the same (sliced structure, order, options): the QAOA
+    loop re-contracts the same networks with new tensor data."""
+
+    def __init__(self, plan):
+        torch = _torch_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.plan = plan
+        self.batch = PlanBatch([plan])
+        self.host = torch.zeros(max(self.batch.set_elems, 1), dtype=torch.complex128).pin_memory()
+        self.inp = torch.empty_like(self.host, device=dev)
+        self.ws = torch.empty(max(self.batch.workspace_bytes(1), 16), dtype=torch.uint8, device=dev)
+        self.res = torch.empty(1, dtype=torch.complex128, device=dev)
+        self.res_host = torch.empty(1, dtype=torch.complex128).pin_memory()
+        self.dev = dev
+
+    def run(self, datas) -> complex:
+        torch = _torch_cuda()
+        stream = torch.cuda.current_stream(self.dev)
+        h = self.host.numpy()
+        self.batch.pack([datas], out=h)
+        self.inp.copy_(self.host, non_blocking=True)
+        self.batch.execute(self.inp.data_ptr(), 1, self.ws.data_ptr(), self.res.data_ptr(),
+                           stream.cuda_stream)
+        self.res_host.copy_(self.res, non_blocking=True)
+        stream.synchronize()
+        return complex(self.res_host.numpy()[0])
+
+
+_RUNS: "collections.OrderedDict" = collections.OrderedDict()
+_RUNS_LOCK = threading.Lock()
+_RUNS_MAX = 64
+
+
 def _contract_with_ranks(network: TensorNetwork, order: ContractionOrder, rank_cap: int,
                          dtype="complex128", **kw):
     unfixed = network.unfixed_variables()
     if sorted(order.sequence) != list(unfixed):
         raise ValueError("order is not a permutation of the network's unfixed variables")
-    plan, sl = ContractionPlan.from_network(network, order, rank_cap=rank_cap, dtype=dtype, **kw)
-    (value,) = _run_plans([plan], [[t.data for t in sl]])
-    return value, list(plan.step_ranks)
+    sl = sliced_tensors(network)
+    import torch
+
+    key = (tuple(t.variables for t in sl), network.variable_count, frozenset(network.fixed),
+           tuple(order.sequence), int(rank_cap), _dtype_code(dtype), tuple(sorted(kw.items())),
+           torch.cuda.current_device() if torch.cuda.is_available() else -1)
+    with _RUNS_LOCK:
+        run = _RUNS.get(key)
+        if run is not None:
+            _RUNS.move_to_end(key)
+    if run is None:
+        # RankCapExceeded / ValueError surface here, before any device work
+        plan = ContractionPlan([t.variables for t in sl], network.variable_count, network.fixed,
+                               order.sequence, rank_cap=rank_cap, dtype=dtype, **kw)
+        run = _CachedRun(plan)  # raises without a CUDA device (no CPU fallback)
+        with _RUNS_LOCK:
+            _RUNS[key] = run
+            while len(_RUNS) > _RUNS_MAX:
+                _RUNS.popitem(last=False)
+    return run.run([t.data for t in sl]), list(run.plan.step_ranks)
 
 
 def contract(network: TensorNetwork, order: ContractionOrder, rank_cap: int = DEFAULT_RANK_CAP,

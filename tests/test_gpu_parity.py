@@ -442,3 +442,22 @@ def test_setmajor_limit_falls_back_to_warp_executor():
     for s in (0, 199):
         zz = [O.edge_zz(8, edges, e, [sets[s, 0]], [sets[s, 1]], "zz+diagonal") for e in edges]
         assert abs(got[s] - O.energy_from_zz(zz)) < 1e-10
+
+
+def test_contract_plan_cache_reuses_structure_with_new_data(golden):
+    """contract() caches the compiled plan and device program per (sliced
+    structure, order); a second network with the same structure but other
+    tensor data (new angles) must give its own value."""
+    graph = Q.random_regular_graph(20, 3, 0)
+    edges = [tuple(e) for e in graph.edges]
+    rng = np.random.default_rng(31)
+    order = None
+    for _ in range(3):
+        g, b = list(rng.uniform(0, math.pi, 1)), list(rng.uniform(0, math.pi, 1))
+        net = Q.build_energy_network(graph, graph.edges[3], Q.QaoaParams(g, b), "default")
+        if order is None:
+            order, _ = Q.rgreedy_order(Q.line_graph(net))
+        got = Q.contract(net, order)
+        tensors, nv, fixed = O.edge_network(20, edges, edges[3], g, b, "default")
+        want, _ = O.contract(tensors, nv, fixed, list(order.sequence))
+        assert abs(got - want) < 1e-12
