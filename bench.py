@@ -39,6 +39,16 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 
+def dtype_label(plan, n_sets):
+    """Arithmetic/storage type of the measured path."""
+    eb = plan._batch.setmajor_elem_bytes(n_sets)
+    if plan.hbm_jobs:
+        return "c128 inputs, c64 storage + f32 math for rank>=12"
+    if eb == 8:
+        return "c64 (set-major rows complex64, f32 products; gate entries formed in f64)"
+    return "c128"
+
+
 def hbm_peak():
     try:
         with open(PEAKS_PATH) as f:
@@ -505,7 +515,7 @@ def run_gpu(args):
 
     peak, peak_kind = hbm_peak()
     kt = sum(kern_times) / len(kern_times)
-    alg = plan.alg_bytes * A
+    alg = plan.alg_bytes_eval(A)
     if plan.hbm_jobs:
         kname = "stream_kernel"
     elif plan._batch.uses_setmajor(A):
@@ -548,7 +558,7 @@ def run_gpu(args):
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "c128" if not plan.hbm_jobs else "c128 (c64 storage for rank>=12)",
+            "dtype": dtype_label(plan, A),
             "data": "synthetic (seeded random 3-regular graph, seeded angles)",
             "config": {"workload": args.workload, "n": wl["n"], "p": wl["p"], "mode": wl["mode"],
                        "edges": len(edge_ids), "angle_sets_per_step": A,

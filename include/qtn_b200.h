@@ -148,6 +148,10 @@ int qtn_batch_launches(const qtn_batch* batch, int32_t n_sets, int32_t* out_laun
 /* 1 if an evaluation of n_sets input sets runs the small networks on the
  * set-major executor (after qtn_batch_set_recipes), else 0 */
 int qtn_batch_uses_setmajor(const qtn_batch* batch, int32_t n_sets, int32_t* out_flag);
+/* bytes per stored set-major element for an evaluation of n_sets sets: 8
+ * (complex64 rows: every plan of the batch asked for QTN_DTYPE_C64; products
+ * in float32), 16 (complex128 rows, float64), 0 (set-major not used) */
+int qtn_batch_setmajor_elem_bytes(const qtn_batch* batch, int32_t n_sets, int32_t* out_bytes);
 /* results[s*n + i] = value of network i under input set s (complex128).
  * Input set s starts at inputs + s*set_stride elements (0: the batch's own
  * qtn_batch_input_elems). */

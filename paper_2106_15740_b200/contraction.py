@@ -196,6 +196,12 @@ class PlanBatch:
         N.check(N.lib.qtn_batch_uses_setmajor(self._h, int(n_sets), C.byref(f)))
         return bool(f.value)
 
+    def setmajor_elem_bytes(self, n_sets: int) -> int:
+        """Bytes per set-major element at n_sets sets: 8 (complex64 rows), 16, or 0."""
+        f = C.c_int32()
+        N.check(N.lib.qtn_batch_setmajor_elem_bytes(self._h, int(n_sets), C.byref(f)))
+        return int(f.value)
+
     def workspace_bytes(self, n_sets: int) -> int:
         w = C.c_int64()
         N.check(N.lib.qtn_batch_workspace_bytes(self._h, int(n_sets), C.byref(w)))

@@ -190,6 +190,7 @@ struct qtn_plan {
   int32_t n_empty = 0;
   int32_t width = 0;
   int32_t executor = QTN_EXEC_HBM;
+  int32_t dtype = QTN_DTYPE_C128;        // requested storage policy
   int64_t input_elems = 0;
   int64_t workspace_bytes = 0;
   int64_t smem_bytes = 0;

@@ -890,6 +890,12 @@ extern "C" int qtn_batch_uses_setmajor(const qtn_batch* B, int32_t n_sets, int32
   return QTN_OK;
 }
 
+extern "C" int qtn_batch_setmajor_elem_bytes(const qtn_batch* B, int32_t n_sets, int32_t* out) {
+  if (!B || !out) return QTN_EINVAL;
+  *out = (B->n_smem && use_setmajor(B, n_sets)) ? qtn::setmajor_elem_bytes(B->sm) : 0;
+  return QTN_OK;
+}
+
 static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const double* angles,
                      int32_t n_angles, int32_t n_sets, void* workspace, void* results,
                      void* stream);

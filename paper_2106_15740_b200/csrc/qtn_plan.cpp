@@ -486,6 +486,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     set_error("out of host memory");
     return QTN_ENOMEM;
   }
+  P->dtype = dtype;
   // ---- inputs (sliced tensors, network order)
   std::vector<std::vector<int32_t>> by_var(nvar);
   int64_t in_off = 0;

@@ -20,6 +20,8 @@
 // variables (network.py:153-165) is resolved when the records are built.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -50,6 +52,7 @@ struct SetMajor {
   int32_t n_nets = 0, n_total = 0, n_levels = 0;
   uint64_t total_elems = 0;            // intermediate rows
   int32_t n_gate_rows = 0;             // gate rows, after the intermediates
+  bool c64 = false;                    // complex64 rows (float32 products)
   std::vector<uint32_t> level_blocks;  // CTAs per level
   std::vector<uint32_t> level_rec;     // first CTA record of each level
   uint32_t* d_recs = nullptr;          // kRecWords per CTA (see sm_level_kernel)
@@ -117,27 +120,37 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 
 // gate rows: grow[r][s] = form code_r of the phase of param_r at set s
+// (formed in float64; complex64 rows round the entry).  Sets A..stride-1 of
+// a padded complex64 row are written as zero.
+template <typename RowT>
 __global__ void sm_gate_rows_kernel(const SMGateRow* __restrict__ rows, int n_rows,
                                     const SMParam* __restrict__ par,
                                     const double* __restrict__ angles, int n_angles, int A,
-                                    double2* __restrict__ grow) {
+                                    int stride, RowT* __restrict__ grow) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
-  if (s >= A || r >= n_rows) return;
-  const SMGateRow g = rows[r];
-  const SMParam q = par[g.param];
-  double2 ph;
-  if (q.angle == -2) {
-    ph = make_double2(q.scale, q.offset);
-  } else {
-    const double t = q.angle >= 0 ? q.scale * angles[(int64_t)s * n_angles + q.angle] + q.offset
-                                  : q.offset;
-    double sn, cs;
-    sincos(t, &sn, &cs);
-    ph = make_double2(cs, -sn);
+  if (s >= stride || r >= n_rows) return;
+  double2 v = make_double2(0.0, 0.0);
+  if (s < A) {
+    const SMGateRow g = rows[r];
+    const SMParam q = par[g.param];
+    double2 ph;
+    if (q.angle == -2) {
+      ph = make_double2(q.scale, q.offset);
+    } else {
+      const double t = q.angle >= 0 ? q.scale * angles[(int64_t)s * n_angles + q.angle] + q.offset
+                                    : q.offset;
+      double sn, cs;
+      sincos(t, &sn, &cs);
+      ph = make_double2(cs, -sn);
+    }
+    v = make_double2(fma(kGateCoef[g.code][1], ph.x, kGateCoef[g.code][0]),
+                     kGateCoef[g.code][2] * ph.y);
   }
-  grow[(int64_t)r * A + s] =
-      make_double2(fma(kGateCoef[g.code][1], ph.x, kGateCoef[g.code][0]), kGateCoef[g.code][2] * ph.y);
+  if constexpr (sizeof(RowT) == 8)
+    grow[(int64_t)r * stride + s] = make_float2((float)v.x, (float)v.y);
+  else
+    grow[(int64_t)r * stride + s] = v;
 }
 
 // ---- level kernel
@@ -212,16 +225,87 @@ __global__ void __launch_bounds__(256) sm_level_kernel(const uint32_t* __restric
   }
 }
 
+__device__ __forceinline__ float4 ldg_nc_f4(uint64_t gaddr) {
+  float4 v;
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(gaddr));
+  return v;
+}
+// two complex64 products at once: (a.xy * b.xy, a.zw * b.zw)
+__device__ __forceinline__ float4 cmul2(float4 a, float4 b) {
+  return make_float4(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x),
+                     fmaf(a.z, b.z, -a.w * b.w), fmaf(a.z, b.w, a.w * b.z));
+}
+
+// Complex64 rows (the configs' complex64 storage; products in float32): the
+// same records, each thread streams J float4 = 2 consecutive sets per pass,
+// half the bytes of the complex128 form.  Rows are padded to an even
+// stride; a pass covers 512*J sets.  FULL: stride is a multiple of
+// 512 * J * gridDim.y.
+template <int J, bool FULL>
+__global__ void __launch_bounds__(256) sm_level_kernel_c64(const uint32_t* __restrict__ recs,
+                                                           float2* ws, int stride) {
+  __shared__ uint64_t rowp[kMaxOps][2];
+  const uint32_t* r = recs + (size_t)blockIdx.x * kRecWords;
+  const uint2 hd = *reinterpret_cast<const uint2*>(r);
+  const int n = (int)hd.y;
+  if (threadIdx.x < n) {
+    const uint2 w = reinterpret_cast<const uint2*>(r + 2)[threadIdx.x];
+    rowp[threadIdx.x][0] = reinterpret_cast<uint64_t>(ws + (size_t)w.x * stride);
+    rowp[threadIdx.x][1] = reinterpret_cast<uint64_t>(ws + (size_t)w.y * stride);
+  }
+  __syncthreads();
+  float4* out = reinterpret_cast<float4*>(ws + (size_t)hd.x * stride);
+  const int s_step = 512 * J * gridDim.y;
+#pragma unroll 1
+  for (int s0 = blockIdx.y * 512 * J + 2 * threadIdx.x; s0 < stride; s0 += s_step) {
+    const uint64_t so = (uint64_t)s0 * sizeof(float2);
+    float4 a0[J], a1[J];
+    {
+      const uint64_t p0 = lds_u64(&rowp[0][0]) + so, p1 = lds_u64(&rowp[0][1]) + so;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const bool ok = J == 1 || FULL || s0 + 512 * j < stride;
+        a0[j] = ok ? ldg_nc_f4(p0 + 4096 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        a1[j] = ok ? ldg_nc_f4(p1 + 4096 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll 1
+    for (int k = 1; k < n; ++k) {
+      const uint64_t p0 = lds_u64(&rowp[k][0]) + so, p1 = lds_u64(&rowp[k][1]) + so;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const bool ok = J == 1 || FULL || s0 + 512 * j < stride;
+        const float4 x = ok ? ldg_nc_f4(p0 + 4096 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 y = ok ? ldg_nc_f4(p1 + 4096 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        a0[j] = cmul2(a0[j], x);
+        a1[j] = cmul2(a1[j], y);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (FULL || s0 + 512 * j < stride)
+        out[(s0 >> 1) + 256 * j] = make_float4(a0[j].x + a1[j].x, a0[j].y + a1[j].y,
+                                               a0[j].z + a1[j].z, a0[j].w + a1[j].w);
+  }
+}
+
 // per (network, set): 2^n_empty * literals * product of its rank-0 rows
+// (float64 products)
+template <typename RowT>
 __global__ void sm_fold_kernel(const double2* __restrict__ cst, const uint32_t* __restrict__ first,
                                const uint32_t* __restrict__ rows, const int32_t* __restrict__ gidx,
-                               int n_nets, int n_total, const double2* ws, int A,
+                               int n_nets, int n_total, const RowT* ws, int A, int stride,
                                double2* __restrict__ results) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = blockIdx.y;
   if (s >= A || n >= n_nets) return;
   double2 r = cst[n];
-  for (uint32_t k = first[n]; k < first[n + 1]; ++k) r = cmul(r, ws[(size_t)rows[k] * A + s]);
+  for (uint32_t k = first[n]; k < first[n + 1]; ++k) {
+    const RowT x = ws[(size_t)rows[k] * stride + s];
+    r = cmul(r, make_double2((double)x.x, (double)x.y));
+  }
   results[(int64_t)s * n_total + gidx[n]] = r;
 }
 
@@ -233,6 +317,15 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
   SetMajor* S = new SetMajor();
   S->n_nets = (int32_t)plans.size();
   S->n_total = n_total;
+  // complex64 rows when every network asked for complex64 storage
+  // (QTN_SETMAJOR_C64=0 keeps complex128 rows for A/B measurements)
+  {
+    bool c64 = !plans.empty();
+    for (auto* P : plans) c64 = c64 && P->dtype == QTN_DTYPE_C64;
+    const char* ev = getenv("QTN_SETMAJOR_C64");
+    if (ev && ev[0] == '0') c64 = false;
+    S->c64 = c64;
+  }
   auto fail = [&](const char* msg) {
     delete S;
     set_error(std::string("set-major executor: ") + msg);
@@ -397,9 +490,18 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
   return QTN_OK;
 }
 
-int64_t setmajor_workspace(const SetMajor* S, int32_t n_sets) {
-  return (int64_t)(S->total_elems + (uint64_t)S->n_gate_rows) * n_sets * 16 + 256;
+// row stride in sets: complex64 rows are padded to an even length (float4 pairs)
+static int32_t row_stride(const SetMajor* S, int32_t n_sets) {
+  return S->c64 ? (n_sets + 1) & ~1 : n_sets;
 }
+
+int64_t setmajor_workspace(const SetMajor* S, int32_t n_sets) {
+  return (int64_t)(S->total_elems + (uint64_t)S->n_gate_rows) * row_stride(S, n_sets) *
+             (S->c64 ? 8 : 16) +
+         256;
+}
+
+int setmajor_elem_bytes(const SetMajor* S) { return S->c64 ? 8 : 16; }
 
 int setmajor_launches(const SetMajor* S, int32_t n_sets) {
   (void)n_sets;
@@ -411,33 +513,54 @@ int setmajor_launches(const SetMajor* S, int32_t n_sets) {
 int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_sets,
                  void* workspace, void* results, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  double2* ws = reinterpret_cast<double2*>(workspace);
-  {
-    dim3 g((n_sets + 127) / 128, std::max(S->n_gate_rows, 1));
-    sm_gate_rows_kernel<<<g, 128, 0, st>>>(S->d_grows, S->n_gate_rows, S->d_params, angles,
-                                           n_angles, n_sets, ws + S->total_elems * (uint64_t)n_sets);
-  }
-  for (int32_t lev = 0; lev < S->n_levels; ++lev) {
-    const uint32_t blocks = S->level_blocks[lev];
-    if (!blocks) continue;
-    const uint32_t* r = S->d_recs + (size_t)S->level_rec[lev] * kRecWords;
-    // few CTAs (tail levels): split the sets over grid.y so the level is not
-    // bound by one CTA's chain of operand round trips
-    const uint32_t split = blocks < 4u * 148u ? (uint32_t)((n_sets + 255) / 256) : 1u;
-    if (split > 1)
-      sm_level_kernel<1, false><<<dim3(blocks, split), 256, 0, st>>>(r, ws, n_sets);
-    else if (n_sets >= 1024 && n_sets % 512 == 0)
-      sm_level_kernel<2, true><<<blocks, 256, 0, st>>>(r, ws, n_sets);
-    else if (n_sets >= 1024)
-      sm_level_kernel<2, false><<<blocks, 256, 0, st>>>(r, ws, n_sets);
-    else
-      sm_level_kernel<1, false><<<blocks, 256, 0, st>>>(r, ws, n_sets);
-  }
-  {
-    dim3 g((n_sets + 127) / 128, S->n_nets);
-    sm_fold_kernel<<<g, 128, 0, st>>>(S->d_const, S->d_scal_first, S->d_scal, S->d_gidx,
-                                      S->n_nets, S->n_total, ws, n_sets,
-                                      reinterpret_cast<double2*>(results));
+  const int stride = row_stride(S, n_sets);
+  const uint64_t grow_off = S->total_elems * (uint64_t)stride;
+  const dim3 gg((stride + 127) / 128, std::max(S->n_gate_rows, 1));
+  const dim3 gf((n_sets + 127) / 128, S->n_nets);
+  double2* res = reinterpret_cast<double2*>(results);
+  if (S->c64) {
+    float2* ws = reinterpret_cast<float2*>(workspace);
+    sm_gate_rows_kernel<float2><<<gg, 128, 0, st>>>(S->d_grows, S->n_gate_rows, S->d_params, angles,
+                                                    n_angles, n_sets, stride, ws + grow_off);
+    for (int32_t lev = 0; lev < S->n_levels; ++lev) {
+      const uint32_t blocks = S->level_blocks[lev];
+      if (!blocks) continue;
+      const uint32_t* r = S->d_recs + (size_t)S->level_rec[lev] * kRecWords;
+      const uint32_t split = blocks < 4u * 148u ? (uint32_t)((stride + 511) / 512) : 1u;
+      if (split > 1)
+        sm_level_kernel_c64<1, false><<<dim3(blocks, split), 256, 0, st>>>(r, ws, stride);
+      else if (stride >= 1024 && stride % 1024 == 0)
+        sm_level_kernel_c64<2, true><<<blocks, 256, 0, st>>>(r, ws, stride);
+      else if (stride >= 1024)
+        sm_level_kernel_c64<2, false><<<blocks, 256, 0, st>>>(r, ws, stride);
+      else
+        sm_level_kernel_c64<1, false><<<blocks, 256, 0, st>>>(r, ws, stride);
+    }
+    sm_fold_kernel<float2><<<gf, 128, 0, st>>>(S->d_const, S->d_scal_first, S->d_scal, S->d_gidx,
+                                               S->n_nets, S->n_total, ws, n_sets, stride, res);
+  } else {
+    double2* ws = reinterpret_cast<double2*>(workspace);
+    sm_gate_rows_kernel<double2><<<gg, 128, 0, st>>>(S->d_grows, S->n_gate_rows, S->d_params,
+                                                     angles, n_angles, n_sets, stride,
+                                                     ws + grow_off);
+    for (int32_t lev = 0; lev < S->n_levels; ++lev) {
+      const uint32_t blocks = S->level_blocks[lev];
+      if (!blocks) continue;
+      const uint32_t* r = S->d_recs + (size_t)S->level_rec[lev] * kRecWords;
+      // few CTAs (tail levels): split the sets over grid.y so the level is not
+      // bound by one CTA's chain of operand round trips
+      const uint32_t split = blocks < 4u * 148u ? (uint32_t)((n_sets + 255) / 256) : 1u;
+      if (split > 1)
+        sm_level_kernel<1, false><<<dim3(blocks, split), 256, 0, st>>>(r, ws, n_sets);
+      else if (n_sets >= 1024 && n_sets % 512 == 0)
+        sm_level_kernel<2, true><<<blocks, 256, 0, st>>>(r, ws, n_sets);
+      else if (n_sets >= 1024)
+        sm_level_kernel<2, false><<<blocks, 256, 0, st>>>(r, ws, n_sets);
+      else
+        sm_level_kernel<1, false><<<blocks, 256, 0, st>>>(r, ws, n_sets);
+    }
+    sm_fold_kernel<double2><<<gf, 128, 0, st>>>(S->d_const, S->d_scal_first, S->d_scal, S->d_gidx,
+                                                S->n_nets, S->n_total, ws, n_sets, stride, res);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

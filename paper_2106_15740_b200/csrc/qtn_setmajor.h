@@ -18,6 +18,8 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
                    const int64_t* offsets, int32_t n_total);
 int64_t setmajor_workspace(const SetMajor* S, int32_t n_sets);
 int setmajor_launches(const SetMajor* S, int32_t n_sets);
+// bytes per stored element: 8 (complex64 rows) or 16 (complex128 rows)
+int setmajor_elem_bytes(const SetMajor* S);
 // results[s*n_total + gidx[k]] for every set s
 int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_sets,
                  void* workspace, void* results, void* stream);

@@ -151,6 +151,16 @@ class EnergyPlan:
         """Algorithmic bytes of one evaluation (one angle set)."""
         return float(sum(j.plan.alg_bytes for j in self.jobs))
 
+    def alg_bytes_eval(self, n_sets: int) -> float:
+        """Algorithmic bytes of one evaluation of n_sets angle sets, each tensor
+        counted at the element size it is stored in: the
+        set-major executor's complex64 rows count 8 bytes per entry."""
+        self._prepare()
+        eb = self._batch.setmajor_elem_bytes(n_sets)
+        small = float(sum(j.plan.alg_bytes for j in self.smem_jobs))
+        big = float(sum(j.plan.alg_bytes for j in self.hbm_jobs))
+        return n_sets * (big + small * (eb / 16.0 if eb else 1.0))
+
     @property
     def flops_sum(self) -> float:
         return float(sum(j.report.flops_sum for j in self.jobs))

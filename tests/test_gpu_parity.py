@@ -286,7 +286,10 @@ def test_setmajor_vs_oracle(golden, setmajor_min_sets):
     G = golden("config2.json")
     graph = Q.random_regular_graph(G["n"], 3, 0)
     edges = [tuple(e) for e in G["edges"]]
-    plan = Q.EnergyPlan(graph, 2, "zz+diagonal", edge_ids=list(range(0, 150, 15)))
+    plan = Q.EnergyPlan(graph, 2, "zz+diagonal", dtype="complex128",
+                        edge_ids=list(range(0, 150, 15)))
+    plan._prepare()
+    assert plan._batch.setmajor_elem_bytes(37) == 16
     rng = np.random.default_rng(17)
     sets = rng.uniform(0, math.pi, (37, 4))
     got = plan.energies(sets)
@@ -461,3 +464,72 @@ def test_contract_plan_cache_reuses_structure_with_new_data(golden):
         tensors, nv, fixed = O.edge_network(20, edges, edges[3], g, b, "default")
         want, _ = O.contract(tensors, nv, fixed, list(order.sequence))
         assert abs(got - want) < 1e-12
+
+
+# ------------------------------------------------ complex64 set-major rows
+def _setmajor_values(plan, sets):
+    """(energies, per-job values) of one set-major evaluation of `sets`."""
+    import torch
+
+    b = plan.launch(torch.from_numpy(np.ascontiguousarray(sets)).cuda())
+    torch.cuda.synchronize()
+    return b["energy"].cpu().numpy().copy(), b["res"].cpu().numpy().copy()
+
+
+@pytest.mark.parametrize("n_sets", [37, 1024, 1100])
+def test_setmajor_c64_config2_vs_oracle(golden, setmajor_min_sets, n_sets):
+    """complex64 set-major rows (config 2's dtype): every edge value within
+    1e-5 (abs, |<ZZ>| <= 1) and every energy within 1e-5 relative of the
+    complex128 executor; sampled sets against the oracle.  37 sets: odd count
+    (padded row stride); 1024: the full-pass kernel; 1100: partial passes."""
+    setmajor_min_sets(1)
+    G = golden("config2.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    edges = [tuple(e) for e in G["edges"]]
+    rng = np.random.default_rng(29)
+    sets = rng.uniform(0, math.pi, (n_sets, 4))
+    sets[0] = list(G["gammas"]) + list(G["betas"])
+    p64 = Q.EnergyPlan(graph, 2, "zz+diagonal", dtype="complex64")
+    p128 = Q.EnergyPlan(graph, 2, "zz+diagonal", dtype="complex128")
+    p64._prepare()
+    p128._prepare()
+    assert p64._batch.setmajor_elem_bytes(n_sets) == 8
+    assert p128._batch.setmajor_elem_bytes(n_sets) == 16
+    e64, r64 = _setmajor_values(p64, sets)
+    e128, r128 = _setmajor_values(p128, sets)
+    assert np.abs(r64 - r128).max() < 1e-5
+    assert np.all(np.abs(e64 - e128) <= 1e-5 * np.abs(e128))
+    # set 0 = the config's seeded angles: the golden energy of the reference
+    want = sum((1 - r["value"][0]) / 2 for r in G["modes"]["zz+diagonal"])
+    assert abs(e64[0] - want) / abs(want) < 1e-5
+    for s in (1, n_sets - 1):
+        g, b = list(sets[s, :2]), list(sets[s, 2:])
+        zz = [O.edge_zz(100, edges, edges[e], g, b, "zz+diagonal") for e in range(0, 150, 10)]
+        got = [r64[s, p64.jobs.index(next(j for j in p64.jobs if j.index == e))]
+               for e in range(0, 150, 10)]
+        assert np.abs(np.asarray(got) - np.asarray(zz)).max() < 1e-5
+    # the public host-to-host call (captured graph) gives the same energies
+    assert np.allclose(p64.energies(sets), e64, rtol=0, atol=1e-9)
+
+
+def test_setmajor_c64_config3_zzdiag(golden, setmajor_min_sets):
+    """Config 3 zz+diagonal (p=3, deeper networks) on complex64 set-major
+    rows: energy at the seeded angles within 1e-5 of the reference golden,
+    all 256 sets within 1e-5 relative of the complex128 rows."""
+    setmajor_min_sets(1)
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    rng = np.random.default_rng(31)
+    sets = rng.uniform(0, math.pi, (256, 6))
+    sets[0] = list(G["gammas"]) + list(G["betas"])
+    p64 = Q.EnergyPlan(graph, 3, "zz+diagonal", dtype="complex64")
+    p128 = Q.EnergyPlan(graph, 3, "zz+diagonal", dtype="complex128")
+    p64._prepare()
+    assert p64._batch.setmajor_elem_bytes(256) == 8
+    e64, r64 = _setmajor_values(p64, sets)
+    e128, r128 = _setmajor_values(p128, sets)
+    assert np.abs(r64 - r128).max() < 1e-5
+    assert np.all(np.abs(e64 - e128) <= 1e-5 * np.abs(e128))
+    want = sum((1 - r["value"][0]) / 2 for r in G["modes"]["zz+diagonal"])
+    assert abs(e64[0] - want) / abs(want) < 1e-5
+    assert abs(e128[0] - want) / abs(want) < 1e-10
