@@ -1,0 +1,194 @@
+// Expanding-bucket kernel (sm_100a): buckets whose output is wider than
+// their primary operand, e.g. two rank-17 operands -> a rank-25 output in
+// config 4 (contraction.py:42-54 `_product` + :94-96 `.sum`).  Such a bucket
+// is an outer product summed over the eliminated variable v:
+//   out[o] = sum_v A_v(o) * B_v(o)
+// with A_v the product of the operands that live on the primary's variables
+// and B_v the product of the others.  It moves few input bytes and many
+// output bytes, so it is bound by the output write stream when each output
+// costs a handful of instructions; the streaming tile kernel (which gathers
+// every non-primary operand per output element) spends ~60 there.
+//
+// Per tile (one CTA of 256 threads): 2^9 A positions x 2^h B positions.
+//   1. the B-side product over (x_b, x_c, v) into shared memory, x_c = the
+//      tile-local A bits a B-side operand depends on (host keeps it small);
+//   2. per thread A_v for its two adjacent outputs (primary: coalesced);
+//   3. for each x_b: two 16-byte shared loads, the v-sum, one 16-byte store
+//      (a warp writes 512 contiguous bytes).
+// Products of the staged/A factors are formed in float64; the inner loop is
+// float32 for complex64 outputs (the complex64 storage policy), float64 for
+// complex128 outputs.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "qtn_internal.h"
+#include "qtn_stream.h"
+
+namespace qtn {
+namespace {
+
+__device__ __forceinline__ double2 xcmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 xld(const char* p, uint64_t i, uint32_t c64) {
+  if (c64) {
+    const float2 f = __ldg(reinterpret_cast<const float2*>(p) + i);
+    return make_double2(f.x, f.y);
+  }
+  return __ldg(reinterpret_cast<const double2*>(p) + i);
+}
+__device__ __forceinline__ uint64_t xgather(uint64_t o, const uint32_t* runs, uint32_t n) {
+  uint64_t idx = 0;
+  for (uint32_t r = 0; r < n; ++r) {
+    const uint32_t w = runs[r];
+    const uint32_t s = w & 0xff, d = (w >> 8) & 0xff, l = (w >> 16) & 0xff;
+    idx |= ((o >> s) & ((1ull << l) - 1)) << d;
+  }
+  return idx;
+}
+__device__ __forceinline__ const char* xresolve(uint64_t tag, const char* in, char* ws) {
+  const uint64_t sel = tag >> kSelShift, off = tag & kOffMask;
+  if (sel == 1) return in + off;
+  if (sel == 2) return ws + off;
+  return reinterpret_cast<const char*>(off);
+}
+
+// product of ops[k0, k1) at output index o and v
+__device__ __forceinline__ double2 xprod(const XDesc& d, uint32_t k0, uint32_t k1, uint64_t o,
+                                         uint32_t v, const char* in, char* ws) {
+  double2 pr = make_double2(1.0, 0.0);
+  for (uint32_t k = k0; k < k1; ++k) {
+    const XOp& op = d.ops[k];
+    const uint64_t idx = xgather(o, op.runs, op.n_runs) | ((uint64_t)v << op.vshift);
+    pr = xcmul(pr, xld(xresolve(op.ptr, in, ws), idx, op.c64));
+  }
+  return pr;
+}
+
+__device__ __forceinline__ float4 f4mac(float2 a0, float2 a1, float4 b) {
+  // a0 * (b.x, b.y) + a1 * (b.z, b.w) for one output, packed as float2 in .xy
+  float2 r;
+  r.x = fmaf(a0.x, b.x, fmaf(-a0.y, b.y, fmaf(a1.x, b.z, -a1.y * b.w)));
+  r.y = fmaf(a0.x, b.y, fmaf(a0.y, b.x, fmaf(a1.x, b.w, a1.y * b.z)));
+  return make_float4(r.x, r.y, 0.f, 0.f);
+}
+
+template <bool F32>
+__device__ __forceinline__ void expand_tile(const XDesc& d, uint64_t tile, const char* in,
+                                            char* ws, unsigned char* smem) {
+  const uint32_t tid = threadIdx.x;
+  const uint32_t c = d.c, h = d.h;
+  const uint64_t obase = xgather(tile, d.trun, d.n_trun);
+  // 1. B-side stage: entry ((x_b << c) | x_c) * 2 + v
+  const uint32_t n_st = 2u << (h + c);
+  for (uint32_t i = tid; i < n_st; i += 256) {
+    const uint32_t v = i & 1u, xc = (i >> 1) & ((1u << c) - 1u), xb = i >> (c + 1);
+    const uint64_t o = obase | xgather(xb, d.brun, d.n_brun) | xgather(xc, d.crun, d.n_crun);
+    const double2 pr = xprod(d, d.nA, d.nA + d.nB, o, v, in, ws);
+    if (F32)
+      reinterpret_cast<float2*>(smem)[i] = make_float2((float)pr.x, (float)pr.y);
+    else
+      reinterpret_cast<double2*>(smem)[i] = pr;
+  }
+  // 2. A-side factors of this thread's two adjacent outputs
+  const uint32_t e0 = 2u * tid;
+  const uint64_t oa = obase | xgather(e0, d.arun, d.n_arun);  // bit 0 of e is output bit 0
+  const uint32_t cx0 = (uint32_t)xgather(e0, d.acrun, d.n_acrun) << 1;
+  const uint32_t cx1 = (uint32_t)xgather(e0 + 1u, d.acrun, d.n_acrun) << 1;
+  const double2 a00 = xprod(d, 0, d.nA, oa, 0, in, ws), a01 = xprod(d, 0, d.nA, oa, 1, in, ws);
+  const double2 a10 = xprod(d, 0, d.nA, oa | 1u, 0, in, ws),
+                a11 = xprod(d, 0, d.nA, oa | 1u, 1, in, ws);
+  __syncthreads();
+  char* outp = const_cast<char*>(xresolve(d.out, in, ws));
+  // x_b -> output offset by a masked increment (pdep of a counter)
+  uint64_t bmask = 0;
+  for (uint32_t r = 0; r < d.n_brun; ++r) {
+    const uint32_t w = d.brun[r];
+    bmask |= ((1ull << ((w >> 16) & 0xff)) - 1) << ((w >> 8) & 0xff);
+  }
+  const uint32_t nb = 1u << h;
+  if (F32) {
+    const float2 A00 = make_float2((float)a00.x, (float)a00.y), A01 = make_float2((float)a01.x, (float)a01.y);
+    const float2 A10 = make_float2((float)a10.x, (float)a10.y), A11 = make_float2((float)a11.x, (float)a11.y);
+    const float4* st = reinterpret_cast<const float4*>(smem);
+    float4* out = reinterpret_cast<float4*>(reinterpret_cast<float2*>(outp) + oa);
+    uint64_t ob = 0;
+#pragma unroll 4
+    for (uint32_t xb = 0; xb < nb; ++xb) {
+      const uint32_t sb = xb << (c + 1);
+      const float4 b0 = st[(sb | cx0) >> 1], b1 = st[(sb | cx1) >> 1];
+      const float4 r0 = f4mac(A00, A01, b0), r1 = f4mac(A10, A11, b1);
+      __stcs(reinterpret_cast<float4*>(reinterpret_cast<float2*>(out) + ob),
+             make_float4(r0.x, r0.y, r1.x, r1.y));
+      ob = ((ob | ~bmask) + 1) & bmask;
+    }
+  } else {
+    const double2* st = reinterpret_cast<const double2*>(smem);
+    double2* out = reinterpret_cast<double2*>(outp) + oa;
+    uint64_t ob = 0;
+#pragma unroll 2
+    for (uint32_t xb = 0; xb < nb; ++xb) {
+      const uint32_t sb = xb << (c + 1);
+      const double2 b00 = st[sb | cx0], b01 = st[sb | cx0 | 1u];
+      const double2 b10 = st[sb | cx1], b11 = st[sb | cx1 | 1u];
+      const double2 p0 = xcmul(a00, b00), q0 = xcmul(a01, b01);
+      const double2 p1 = xcmul(a10, b10), q1 = xcmul(a11, b11);
+      __stcs(out + ob, make_double2(p0.x + q0.x, p0.y + q0.y));
+      __stcs(out + ob + 1, make_double2(p1.x + q1.x, p1.y + q1.y));
+      ob = ((ob | ~bmask) + 1) & bmask;
+    }
+  }
+}
+
+// grid: x = tiles of one set over all items of the launch, y = set
+__global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ XLaunch L) {
+  extern __shared__ __align__(16) unsigned char xsmem[];
+  const uint64_t t = blockIdx.x;
+  uint32_t lo = 0, hi = L.n_items;  // last item whose first tile <= t
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (L.tile_prefix[mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  const XDesc& d = L.descs[L.item_desc[lo]];
+  const uint32_t net = L.item_net[lo];
+  const uint32_t set = blockIdx.y;
+  const char* in = L.in_base + (int64_t)set * L.in_set_stride + L.net_in_off[net];
+  char* ws = L.ws_base + (int64_t)set * L.ws_set_stride + L.net_ws_off[net];
+  const uint64_t tile = t - L.tile_prefix[lo];
+  if (d.out_c64)
+    expand_tile<true>(d, tile, in, ws, xsmem);
+  else
+    expand_tile<false>(d, tile, in, ws, xsmem);
+}
+
+}  // namespace
+
+int launch_expand(const XLaunch& L, void* stream) {
+  if (!L.n_items || !L.n_sets || !L.total_tiles) return QTN_OK;
+  if (L.n_sets > 65535 || L.total_tiles > 0x7fffffffull) {
+    set_error("expand_kernel: grid too large");
+    return QTN_EINVAL;
+  }
+  static uint32_t attr = 0;
+  if (L.stage_bytes > 48u * 1024u && L.stage_bytes > attr) {
+    cudaError_t e = cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)L.stage_bytes);
+    if (e != cudaSuccess) {
+      set_error(std::string("expand_kernel attribute: ") + cudaGetErrorString(e));
+      return QTN_ECUDA;
+    }
+    attr = L.stage_bytes;
+  }
+  dim3 grid((uint32_t)L.total_tiles, L.n_sets);
+  expand_kernel<<<grid, 256, L.stage_bytes, reinterpret_cast<cudaStream_t>(stream)>>>(L);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("expand_kernel launch: ") + cudaGetErrorString(e));
+    return QTN_ECUDA;
+  }
+  return QTN_OK;
+}
+
+}  // namespace qtn

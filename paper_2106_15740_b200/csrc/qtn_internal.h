@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/qtn_b200.h"
+#include "qtn_stream.h"
 
 namespace qtn {
 
@@ -205,6 +206,8 @@ struct qtn_plan {
   std::vector<int32_t> hbm_level;        // -1: absorbed into a fused reduction
   std::vector<qtn::RedRec> hbm_red;      // fused single-operand chains
   std::vector<uint64_t> hbm_tiles;
+  std::vector<int32_t> hbm_xidx;         // expanding-bucket descriptor per bucket, or -1
+  std::vector<qtn::XDesc> hbm_xdesc;
   int32_t n_levels = 0;
   // Set-major form of an SMEM-eligible network (qtn_setmajor.cu): angle
   // sets are the fastest-varying dimension of every tensor in HBM, one

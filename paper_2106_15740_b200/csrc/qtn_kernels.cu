@@ -626,6 +626,14 @@ struct qtn_batch {
   uint32_t* d_sitem_net = nullptr;
   std::vector<uint32_t> level_sitem0;   // first small item of each level (+ end)
   std::vector<uint32_t> level_smax_r;   // widest small item of each level
+  // expanding buckets of each level (expand_kernel)
+  qtn::XDesc* d_xdesc = nullptr;
+  uint32_t* d_xitem_desc = nullptr;
+  uint32_t* d_xitem_net = nullptr;
+  uint64_t* d_xprefix = nullptr;
+  std::vector<uint32_t> level_xitem0;   // first expand item of each level (+ end)
+  std::vector<uint64_t> level_xprefix0, level_xtiles;
+  std::vector<uint32_t> level_xstage;   // stage bytes (max over the level's items)
   // fused single-operand chains per level (reduce_kernel)
   qtn::RedDev* d_red = nullptr;
   uint32_t* d_red_prefix = nullptr;
@@ -654,7 +662,8 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_net_ws_off, (void*)B->d_fold_tags, (void*)B->d_fold_c64,
                   (void*)B->d_fold_first, (void*)B->d_fold_pow2, (void*)B->d_hbm_index,
                   (void*)B->d_hbm_rec, (void*)B->d_sitem_desc, (void*)B->d_sitem_net,
-                  (void*)B->d_red, (void*)B->d_red_prefix})
+                  (void*)B->d_red, (void*)B->d_red_prefix, (void*)B->d_xdesc,
+                  (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
   delete B;
@@ -723,17 +732,31 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   const char* sv = getenv("QTN_SMALL_R");  // buckets up to this output rank: small kernel
   const int small_r = sv ? atoi(sv) : qtn::kSmallR;
   std::vector<uint64_t> desc_base(B->n_hbm);
+  std::vector<uint32_t> xdesc_base(B->n_hbm);
+  std::vector<qtn::XDesc> xdescs;
   for (int h = 0; h < B->n_hbm; ++h) {
     const qtn_plan* P = plans[hidx[h]];
     desc_base[h] = desc.size();
     desc.insert(desc.end(), P->hbm_desc.begin(), P->hbm_desc.end());
+    xdesc_base[h] = (uint32_t)xdescs.size();
+    xdescs.insert(xdescs.end(), P->hbm_xdesc.begin(), P->hbm_xdesc.end());
   }
+  // expanding buckets take the outer-product kernel (QTN_EXPAND=0: the
+  // streaming kernel, for A/B measurements)
+  const char* xv = getenv("QTN_EXPAND");
+  const bool use_expand = !(xv && xv[0] == '0');
+  std::vector<uint32_t> xitem_desc, xitem_net;
+  std::vector<uint64_t> xprefix;
   for (int32_t lev = 0; lev < max_lev; ++lev) {
     B->level_item0.push_back((uint32_t)item_desc.size());
     B->level_prefix0.push_back(prefix.size());
     B->level_sitem0.push_back((uint32_t)sitem_desc.size());
-    uint64_t acc = 0;
+    B->level_xitem0.push_back((uint32_t)xitem_desc.size());
+    B->level_xprefix0.push_back(xprefix.size());
+    uint64_t acc = 0, xacc = 0;
+    uint32_t xstage = 0;
     prefix.push_back(0);
+    xprefix.push_back(0);
     // small buckets go to the warp/CTA-per-bucket kernel, unless the level
     // launches the streaming kernel anyway and they are few (one launch less)
     // a tiny level (few output elements in all) goes entirely to the small
@@ -765,6 +788,15 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
           smax_r = std::max<uint32_t>(smax_r, sh->R);
           continue;
         }
+        if (use_expand && P->hbm_xidx[bi] >= 0) {
+          const qtn::XDesc& xd = P->hbm_xdesc[P->hbm_xidx[bi]];
+          xitem_desc.push_back(xdesc_base[h] + (uint32_t)P->hbm_xidx[bi]);
+          xitem_net.push_back((uint32_t)h);
+          xacc += xd.n_tiles;
+          xprefix.push_back(xacc);
+          xstage = std::max<uint32_t>(xstage, (2u << (xd.h + xd.c)) * (xd.out_c64 ? 8u : 16u));
+          continue;
+        }
         item_desc.push_back(desc_base[h] + P->hbm_desc_off[bi]);
         item_net.push_back((uint32_t)h);
         acc += P->hbm_tiles[bi];
@@ -773,9 +805,12 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     }
     B->level_tiles.push_back(acc);
     B->level_smax_r.push_back(smax_r);
+    B->level_xtiles.push_back(xacc);
+    B->level_xstage.push_back(xstage);
   }
   B->level_item0.push_back((uint32_t)item_desc.size());
   B->level_sitem0.push_back((uint32_t)sitem_desc.size());
+  B->level_xitem0.push_back((uint32_t)xitem_desc.size());
   // fused reductions, level-major over all HBM networks
   std::vector<qtn::RedDev> reds;
   std::vector<uint32_t> rprefix;
@@ -828,6 +863,8 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_item_net, item_net)) || (rc = upload(&B->d_tile_prefix, prefix)) ||
       (rc = upload(&B->d_sitem_desc, sitem_desc)) || (rc = upload(&B->d_sitem_net, sitem_net)) ||
       (rc = upload(&B->d_red, reds)) || (rc = upload(&B->d_red_prefix, rprefix)) ||
+      (rc = upload(&B->d_xdesc, xdescs)) || (rc = upload(&B->d_xitem_desc, xitem_desc)) ||
+      (rc = upload(&B->d_xitem_net, xitem_net)) || (rc = upload(&B->d_xprefix, xprefix)) ||
       (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
       (rc = upload(&B->d_fold_tags, ftags)) || (rc = upload(&B->d_fold_c64, fc64)) ||
       (rc = upload(&B->d_fold_first, ffirst)) || (rc = upload(&B->d_fold_pow2, fpow2)) ||
@@ -877,7 +914,7 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
   if (B->n_hbm) {
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev)
       c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
-           (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0);
+           (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0);
     c += 1;
   }
   *out = c;
@@ -1219,6 +1256,25 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         Ls.item_net = B->d_sitem_net + B->level_sitem0[lev];
         Ls.n_items = ns;
         if ((rc = qtn::launch_small(Ls, B->level_smax_r[lev], stream))) return rc;
+      }
+      if (B->level_xtiles[lev]) {
+        qtn::XLaunch X;
+        std::memset(&X, 0, sizeof(X));
+        X.descs = B->d_xdesc;
+        X.item_desc = B->d_xitem_desc + B->level_xitem0[lev];
+        X.item_net = B->d_xitem_net + B->level_xitem0[lev];
+        X.tile_prefix = B->d_xprefix + B->level_xprefix0[lev];
+        X.n_items = B->level_xitem0[lev + 1] - B->level_xitem0[lev];
+        X.n_sets = (uint32_t)n_sets;
+        X.total_tiles = B->level_xtiles[lev];
+        X.stage_bytes = B->level_xstage[lev];
+        X.in_base = L.in_base;
+        X.in_set_stride = L.in_set_stride;
+        X.net_in_off = L.net_in_off;
+        X.ws_base = L.ws_base;
+        X.ws_set_stride = L.ws_set_stride;
+        X.net_ws_off = L.net_ws_off;
+        if ((rc = qtn::launch_expand(X, stream))) return rc;
       }
       if (!B->level_tiles[lev]) continue;
       L.item_desc = B->d_item_desc + B->level_item0[lev];

@@ -447,6 +447,129 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
   return QTN_OK;
 }
 
+// Expanding-bucket descriptor (qtn_stream.h XDesc, kernel in qtn_expand.cu).
+// Geometry: A bits = output bits 0-5 plus 3 more bits the B-side operands do
+// not depend on where possible (so the stage stays small), B bits = the
+// lowest h bits no A-side operand depends on, h as large as the stage
+// (<= kXStageMax entries) and a healthy tile count allow.
+bool encode_expand_desc(const BucketSpec& s, XDesc& d) {
+  const char* ev = getenv("QTN_EXPAND_MIN_R");
+  const int min_r = ev ? atoi(ev) : 14;
+  const int R = (int)s.out_vars.size();
+  if (R < min_r || R > 40) return false;
+  std::memset(&d, 0, sizeof(d));
+  auto obit = [&](int32_t u) -> int {
+    for (int i = 0; i < R; ++i)
+      if (s.out_vars[i] == u) return R - 1 - i;
+    return -1;
+  };
+  const int n = (int)s.opvars.size();
+  std::vector<uint64_t> dep(n, 0);  // output bits each operand depends on
+  for (int t = 0; t < n; ++t)
+    for (int32_t u : s.opvars[t])
+      if (u != s.v) {
+        const int b = obit(u);
+        if (b < 0) return false;
+        dep[t] |= 1ull << b;
+      }
+  const uint64_t pdep = dep[s.primary];
+  std::vector<int> A, Bs;
+  for (int t = 0; t < n; ++t) ((dep[t] & ~pdep) == 0 ? A : Bs).push_back(t);
+  if (Bs.empty() || (int)A.size() > kXMaxOps || (int)Bs.size() > kXMaxOps) return false;
+  uint64_t adep = 0, bdep = 0;
+  for (int t : A) adep |= dep[t];
+  for (int t : Bs) bdep |= dep[t];
+  // A bits: 0..5 (coalesced 512-byte warp stores) + 3 more, never a bit the
+  // A side does not depend on (those are the candidates for B bits)
+  std::vector<int> ta;
+  for (int b = 0; b < 6; ++b) {
+    if (!((adep >> b) & 1)) return false;
+    ta.push_back(b);
+  }
+  for (int pass = 0; pass < 2 && (int)ta.size() < kXABits; ++pass)
+    for (int b = 6; b < R && (int)ta.size() < kXABits; ++b) {
+      if (!((adep >> b) & 1) || std::find(ta.begin(), ta.end(), b) != ta.end()) continue;
+      if (pass == 0 && ((bdep >> b) & 1)) continue;  // first: bits B does not see
+      ta.push_back(b);
+    }
+  if ((int)ta.size() < kXABits) return false;
+  std::sort(ta.begin(), ta.end());
+  std::vector<int> tc;  // tile-local A bits the B side depends on
+  for (int b : ta)
+    if ((bdep >> b) & 1) tc.push_back(b);
+  const int c = (int)tc.size();
+  std::vector<int> nbits;  // B-bit candidates: no A-side dependence
+  for (int b = 0; b < R; ++b)
+    if (!((adep >> b) & 1)) nbits.push_back(b);
+  int h = std::min<int>((int)nbits.size(), 8);
+  while (h > 0 && (2 << (h + c)) > kXStageMax) --h;
+  // keep >= ~2 tiles per SM when the bucket allows it
+  while (h > 2 && R - kXABits - h < 9) --h;
+  if (h < 2) return false;
+  std::vector<int> tb(nbits.begin(), nbits.begin() + h);
+  std::vector<int> rest;
+  for (int b = 0; b < R; ++b)
+    if (std::find(ta.begin(), ta.end(), b) == ta.end() && std::find(tb.begin(), tb.end(), b) == tb.end())
+      rest.push_back(b);
+  auto put = [&](const std::vector<std::pair<int, int>>& pr, uint32_t* dst, uint8_t& cnt) {
+    std::vector<uint32_t> runs;
+    make_runs(pr, runs);
+    if ((int)runs.size() > kXRuns) return false;
+    std::copy(runs.begin(), runs.end(), dst);
+    cnt = (uint8_t)runs.size();
+    return true;
+  };
+  std::vector<std::pair<int, int>> pr;
+  for (size_t i = 0; i < rest.size(); ++i) pr.push_back({(int)i, rest[i]});
+  if (!put(pr, d.trun, d.n_trun)) return false;
+  pr.clear();
+  for (size_t i = 0; i < ta.size(); ++i) pr.push_back({(int)i, ta[i]});
+  if (!put(pr, d.arun, d.n_arun)) return false;
+  pr.clear();
+  for (size_t i = 0; i < tb.size(); ++i) pr.push_back({(int)i, tb[i]});
+  if (!put(pr, d.brun, d.n_brun)) return false;
+  pr.clear();
+  for (size_t i = 0; i < tc.size(); ++i) pr.push_back({(int)i, tc[i]});
+  if (!put(pr, d.crun, d.n_crun)) return false;
+  pr.clear();
+  for (size_t i = 0; i < ta.size(); ++i) {
+    auto it = std::find(tc.begin(), tc.end(), ta[i]);
+    if (it != tc.end()) pr.push_back({(int)i, (int)(it - tc.begin())});
+  }
+  if (!put(pr, d.acrun, d.n_acrun)) return false;
+  auto op_of = [&](int t, XOp& o) {
+    const auto& vs = s.opvars[t];
+    const int rk = (int)vs.size();
+    std::vector<std::pair<int, int>> q;
+    o.vshift = 0xff;
+    for (int j = 0; j < rk; ++j) {
+      if (vs[j] == s.v) o.vshift = (uint8_t)(rk - 1 - j);
+      else q.push_back({obit(vs[j]), rk - 1 - j});
+    }
+    if (o.vshift == 0xff) return false;
+    o.ptr = s.optag[t];
+    o.c64 = s.opc64[t];
+    return put(q, o.runs, o.n_runs);
+  };
+  int k = 0;
+  for (int t : A)
+    if (!op_of(t, d.ops[k++])) return false;
+  for (int t : Bs)
+    if (!op_of(t, d.ops[k++])) return false;
+  d.out = s.out_tag;
+  d.R = (uint8_t)R;
+  d.out_c64 = s.out_c64 ? 1 : 0;
+  d.h = (uint8_t)h;
+  d.c = (uint8_t)c;
+  d.nA = (uint8_t)A.size();
+  d.nB = (uint8_t)Bs.size();
+  d.n_tiles = 1ull << (R - kXABits - h);
+  if (getenv("QTN_DEBUG_DESC") && R >= atoi(getenv("QTN_DEBUG_DESC")))
+    fprintf(stderr, "xdesc R=%d h=%d c=%d nA=%d nB=%d tiles=%llu\n", R, h, c, (int)A.size(),
+            (int)Bs.size(), (unsigned long long)d.n_tiles);
+  return true;
+}
+
 }  // namespace qtn
 
 using namespace qtn;
@@ -898,6 +1021,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       const auto& t = P->tensors[id];
       return t.input ? tag_in(16ull * (uint64_t)t.in_off) : tag_ws((uint64_t)t.ws_off);
     };
+    P->hbm_xidx.assign(nb, -1);
     for (int bi = 0; bi < nb; ++bi) {
       const auto& b = P->buckets[bi];
       P->hbm_desc_off.push_back(P->hbm_desc.size());
@@ -946,6 +1070,11 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       }
       const SHdr* h = reinterpret_cast<const SHdr*>(P->hbm_desc.data() + P->hbm_desc_off.back());
       P->hbm_tiles.push_back(h->n_tiles);
+      XDesc xd;
+      if (encode_expand_desc(spec, xd)) {
+        P->hbm_xidx[bi] = (int32_t)P->hbm_xdesc.size();
+        P->hbm_xdesc.push_back(xd);
+      }
     }
   }
   // algorithmic bytes: e * (operand entries + output entries) per bucket

@@ -158,6 +158,61 @@ inline uint32_t red_chunk(uint32_t k) {
 int launch_reduce(const StreamLaunch& L, const RedDev* items, const uint32_t* prefix,
                   uint32_t n_items, uint32_t total_chunks, void* stream);
 int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream);
+// ---- expanding buckets (output wider than its primary operand): the
+// outer-product form.  Output bits split into tile-local A bits (9: 256
+// threads x 2 adjacent outputs, bits 0-5 always among them so a warp writes
+// 512 contiguous bytes), tile-local B bits (h, among the bits no A-side
+// operand depends on) and per-tile base bits.  A-side operands (the primary
+// and every operand whose variables are the primary's) give, per thread,
+// A_v(e) for its 2 outputs; B-side operands (all others) are multiplied once
+// per tile into a shared-memory stage Bst[x_b][x_c][v] over the B bits and
+// the c tile-local A bits they depend on; then
+//   out[base | e | x_b] = A_0(e) Bst[x_b][c(e)][0] + A_1(e) Bst[x_b][c(e)][1]
+// is two 16-byte shared loads, ~10 FMAs and one 16-byte store per 2 outputs.
+constexpr int kXMaxOps = 6;      // per side
+constexpr int kXRuns = 24;
+constexpr int kXABits = 9;       // tile-local A bits (256 threads x 2)
+constexpr int kXStageMax = 4096; // staged B entries (x_b, x_c, v)
+struct XOp {
+  uint64_t ptr;                  // tagged
+  uint8_t vshift, c64, n_runs, pad;
+  uint32_t runs[kXRuns];         // output bits -> operand bits
+  uint32_t pad2;
+};
+struct XDesc {
+  uint64_t out;                  // tagged
+  uint64_t n_tiles;
+  uint8_t R, out_c64, h, c, nA, nB, n_trun, n_arun, n_brun, n_crun, n_acrun, pad[5];
+  uint32_t trun[kXRuns];         // tile index bits -> output bits
+  uint32_t arun[kXRuns];         // tile-local A element bits -> output bits
+  uint32_t brun[kXRuns];         // x_b bits -> output bits
+  uint32_t crun[kXRuns];         // x_c bits -> output bits
+  uint32_t acrun[kXRuns];        // tile-local A element bits -> x_c bits
+  XOp ops[2 * kXMaxOps];         // A-side ops [0, nA), B-side [nA, nA + nB)
+};
+static_assert(sizeof(XOp) % 16 == 0, "XOp");
+static_assert(sizeof(XDesc) % 16 == 0, "XDesc");
+// Host encoder: fills d and returns true when the bucket takes the
+// expanding-bucket kernel (output rank >= 14, >= 2 B bits, operand limits).
+bool encode_expand_desc(const BucketSpec& b, XDesc& d);
+struct XLaunch {
+  const XDesc* descs;            // device
+  const uint32_t* item_desc;     // device: descriptor index per item
+  const uint32_t* item_net;      // device: network index per item
+  const uint64_t* tile_prefix;   // device: n_items + 1
+  uint32_t n_items;
+  uint32_t n_sets;
+  uint64_t total_tiles;          // tiles of one set
+  uint32_t stage_bytes;          // dynamic shared memory (max over items)
+  const char* in_base;
+  int64_t in_set_stride;
+  const int64_t* net_in_off;
+  char* ws_base;
+  int64_t ws_set_stride;
+  const int64_t* net_ws_off;
+};
+int launch_expand(const XLaunch& L, void* stream);
+
 // single descriptor with absolute pointers, descriptor passed by value
 int launch_stream_single(const std::vector<uint8_t>& desc, void* stream);
 

@@ -533,3 +533,51 @@ def test_setmajor_c64_config3_zzdiag(golden, setmajor_min_sets):
     want = sum((1 - r["value"][0]) / 2 for r in G["modes"]["zz+diagonal"])
     assert abs(e64[0] - want) / abs(want) < 1e-5
     assert abs(e128[0] - want) / abs(want) < 1e-10
+
+
+# ------------------------------------------------- expanding-bucket kernel
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-11), ("complex64", 1e-5)])
+def test_expand_kernel_config4(golden, monkeypatch, dtype, tol):
+    """Config 4 edges #16 and #1058 (expanding buckets [2,17,17]->25,
+    [1,22,21]->26, ...) on the outer-product kernel equal the streaming
+    kernel (QTN_EXPAND=0) and the reference values; one angle set and a
+    batch of 3 (grid.y over sets)."""
+    G = golden("config4.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    ids = [16, 1058]
+    recs = {r["edge_index"]: complex(*r["value"]) for r in G["modes"]["zz+diagonal"]
+            if r["edge_index"] in ids}
+    rng = np.random.default_rng(41)
+    sets = rng.uniform(0, math.pi, (3, 2 * G["p"]))
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_EXPAND", flag)
+        plan = Q.EnergyPlan(graph, G["p"], "zz+diagonal", dtype=dtype, edge_ids=ids)
+        out[flag] = (plan.zz_values(params), plan.energies(sets))
+        assert plan.launches == plan.launches_per_eval(3)
+    for e in ids:
+        assert abs(out["1"][0][e] - recs[e]) <= tol * abs(recs[e])
+        assert abs(out["1"][0][e] - out["0"][0][e]) <= tol * abs(recs[e])
+    assert np.allclose(out["1"][1], out["0"][1], rtol=tol, atol=0)
+
+
+def test_expand_kernel_config3_default(golden, monkeypatch):
+    """Config 3 default-mode networks (H/CNOT, 2-operand buckets): the
+    outer-product kernel wherever it applies equals the streaming kernel and
+    the reference values (complex128)."""
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    recs = G["modes"]["default"][:12]
+    ids = [r["edge_index"] for r in recs]
+    vals = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_EXPAND", flag)
+        monkeypatch.setenv("QTN_EXPAND_MIN_R", "12")
+        plan = Q.EnergyPlan(graph, G["p"], "default", dtype="complex128", edge_ids=ids)
+        vals[flag] = plan.zz_values(params)
+    for r in recs:
+        w = complex(*r["value"])
+        assert abs(vals["1"][r["edge_index"]] - w) <= 1e-11 * abs(w) + 1e-13
+        assert abs(vals["1"][r["edge_index"]] - vals["0"][r["edge_index"]]) <= 1e-11 * abs(w) + 1e-13
