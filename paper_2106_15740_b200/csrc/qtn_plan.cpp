@@ -540,6 +540,7 @@ bool encode_expand_desc(const BucketSpec& s, XDesc& d) {
   auto op_of = [&](int t, XOp& o) {
     const auto& vs = s.opvars[t];
     const int rk = (int)vs.size();
+    if (rk > 32) return false;  // 32-bit operand offsets in the kernel
     std::vector<std::pair<int, int>> q;
     o.vshift = 0xff;
     for (int j = 0; j < rk; ++j) {
