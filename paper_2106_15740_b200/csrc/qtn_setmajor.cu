@@ -30,6 +30,7 @@
 #include <tuple>
 #include <vector>
 
+#include "qtn_pdl.cuh"
 #include "qtn_setmajor.h"
 
 namespace qtn {
@@ -129,6 +130,8 @@ __global__ void sm_gate_rows_kernel(const SMGateRow* __restrict__ rows, int n_ro
                                     int stride, RowT* __restrict__ grow) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
+  pdl_trigger();
+  pdl_wait();
   if (s >= stride || r >= n_rows) return;
   double2 v = make_double2(0.0, 0.0);
   if (s < A) {
@@ -190,7 +193,9 @@ __global__ void __launch_bounds__(256) sm_level_kernel(const uint32_t* __restric
     rowp[threadIdx.x][0] = reinterpret_cast<uint64_t>(ws + (size_t)w.x * A);
     rowp[threadIdx.x][1] = reinterpret_cast<uint64_t>(ws + (size_t)w.y * A);
   }
+  pdl_trigger();
   __syncthreads();
+  pdl_wait();  // rows of earlier levels
   double2* out = ws + (size_t)hd.x * A;
   const int s_step = 256 * J * gridDim.y;
 #pragma unroll 1
@@ -255,7 +260,9 @@ __global__ void __launch_bounds__(256) sm_level_kernel_c64(const uint32_t* __res
     rowp[threadIdx.x][0] = reinterpret_cast<uint64_t>(ws + (size_t)w.x * stride);
     rowp[threadIdx.x][1] = reinterpret_cast<uint64_t>(ws + (size_t)w.y * stride);
   }
+  pdl_trigger();
   __syncthreads();
+  pdl_wait();  // rows of earlier levels
   float4* out = reinterpret_cast<float4*>(ws + (size_t)hd.x * stride);
   const int s_step = 512 * J * gridDim.y;
 #pragma unroll 1
@@ -300,6 +307,8 @@ __global__ void sm_fold_kernel(const double2* __restrict__ cst, const uint32_t* 
                                double2* __restrict__ results) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = blockIdx.y;
+  pdl_trigger();
+  pdl_wait();
   if (s >= A || n >= n_nets) return;
   double2 r = cst[n];
   for (uint32_t k = first[n]; k < first[n + 1]; ++k) {
@@ -520,29 +529,32 @@ int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_
   double2* res = reinterpret_cast<double2*>(results);
   if (S->c64) {
     float2* ws = reinterpret_cast<float2*>(workspace);
-    sm_gate_rows_kernel<float2><<<gg, 128, 0, st>>>(S->d_grows, S->n_gate_rows, S->d_params, angles,
-                                                    n_angles, n_sets, stride, ws + grow_off);
+    launch_pdl(sm_gate_rows_kernel<float2>, gg, dim3(128), 0, st, (const SMGateRow*)S->d_grows,
+               S->n_gate_rows, (const SMParam*)S->d_params, angles, (int)n_angles, (int)n_sets,
+               stride, ws + grow_off);
     for (int32_t lev = 0; lev < S->n_levels; ++lev) {
       const uint32_t blocks = S->level_blocks[lev];
       if (!blocks) continue;
       const uint32_t* r = S->d_recs + (size_t)S->level_rec[lev] * kRecWords;
       const uint32_t split = blocks < 4u * 148u ? (uint32_t)((stride + 511) / 512) : 1u;
       if (split > 1)
-        sm_level_kernel_c64<1, false><<<dim3(blocks, split), 256, 0, st>>>(r, ws, stride);
+        launch_pdl(sm_level_kernel_c64<1, false>, dim3(blocks, split), dim3(256), 0, st, r, ws, stride);
       else if (stride >= 1024 && stride % 1024 == 0)
-        sm_level_kernel_c64<2, true><<<blocks, 256, 0, st>>>(r, ws, stride);
+        launch_pdl(sm_level_kernel_c64<2, true>, blocks, dim3(256), 0, st, r, ws, stride);
       else if (stride >= 1024)
-        sm_level_kernel_c64<2, false><<<blocks, 256, 0, st>>>(r, ws, stride);
+        launch_pdl(sm_level_kernel_c64<2, false>, blocks, dim3(256), 0, st, r, ws, stride);
       else
-        sm_level_kernel_c64<1, false><<<blocks, 256, 0, st>>>(r, ws, stride);
+        launch_pdl(sm_level_kernel_c64<1, false>, blocks, dim3(256), 0, st, r, ws, stride);
     }
-    sm_fold_kernel<float2><<<gf, 128, 0, st>>>(S->d_const, S->d_scal_first, S->d_scal, S->d_gidx,
-                                               S->n_nets, S->n_total, ws, n_sets, stride, res);
+    launch_pdl(sm_fold_kernel<float2>, gf, dim3(128), 0, st, (const double2*)S->d_const,
+               (const uint32_t*)S->d_scal_first, (const uint32_t*)S->d_scal,
+               (const int32_t*)S->d_gidx, S->n_nets, S->n_total, (const float2*)ws, (int)n_sets,
+               stride, res);
   } else {
     double2* ws = reinterpret_cast<double2*>(workspace);
-    sm_gate_rows_kernel<double2><<<gg, 128, 0, st>>>(S->d_grows, S->n_gate_rows, S->d_params,
-                                                     angles, n_angles, n_sets, stride,
-                                                     ws + grow_off);
+    launch_pdl(sm_gate_rows_kernel<double2>, gg, dim3(128), 0, st, (const SMGateRow*)S->d_grows,
+               S->n_gate_rows, (const SMParam*)S->d_params, angles, (int)n_angles, (int)n_sets,
+               stride, ws + grow_off);
     for (int32_t lev = 0; lev < S->n_levels; ++lev) {
       const uint32_t blocks = S->level_blocks[lev];
       if (!blocks) continue;
@@ -551,16 +563,18 @@ int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_
       // bound by one CTA's chain of operand round trips
       const uint32_t split = blocks < 4u * 148u ? (uint32_t)((n_sets + 255) / 256) : 1u;
       if (split > 1)
-        sm_level_kernel<1, false><<<dim3(blocks, split), 256, 0, st>>>(r, ws, n_sets);
+        launch_pdl(sm_level_kernel<1, false>, dim3(blocks, split), dim3(256), 0, st, r, ws, (int)n_sets);
       else if (n_sets >= 1024 && n_sets % 512 == 0)
-        sm_level_kernel<2, true><<<blocks, 256, 0, st>>>(r, ws, n_sets);
+        launch_pdl(sm_level_kernel<2, true>, blocks, dim3(256), 0, st, r, ws, (int)n_sets);
       else if (n_sets >= 1024)
-        sm_level_kernel<2, false><<<blocks, 256, 0, st>>>(r, ws, n_sets);
+        launch_pdl(sm_level_kernel<2, false>, blocks, dim3(256), 0, st, r, ws, (int)n_sets);
       else
-        sm_level_kernel<1, false><<<blocks, 256, 0, st>>>(r, ws, n_sets);
+        launch_pdl(sm_level_kernel<1, false>, blocks, dim3(256), 0, st, r, ws, (int)n_sets);
     }
-    sm_fold_kernel<double2><<<gf, 128, 0, st>>>(S->d_const, S->d_scal_first, S->d_scal, S->d_gidx,
-                                                S->n_nets, S->n_total, ws, n_sets, stride, res);
+    launch_pdl(sm_fold_kernel<double2>, gf, dim3(128), 0, st, (const double2*)S->d_const,
+               (const uint32_t*)S->d_scal_first, (const uint32_t*)S->d_scal,
+               (const int32_t*)S->d_gidx, S->n_nets, S->n_total, (const double2*)ws, (int)n_sets,
+               stride, res);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
