@@ -26,6 +26,7 @@
 
 #include "qtn_internal.h"
 #include "qtn_stream.h"
+#include "qtn_pdl.cuh"
 
 namespace qtn {
 namespace {
@@ -160,6 +161,8 @@ __device__ __forceinline__ void expand_tile(const XDesc& d, XItemSmem& X, const 
 __global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ XLaunch L) {
   extern __shared__ __align__(16) unsigned char xsmem[];
   __shared__ XItemSmem X;
+  pdl_trigger();
+  pdl_wait();
   const uint64_t per = (L.total_tiles + gridDim.x - 1) / gridDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * per;
   const uint64_t t1 = min(L.total_tiles, t0 + per);
@@ -253,8 +256,9 @@ int launch_expand(const XLaunch& L, void* stream) {
   }
   const uint64_t ctas = std::min<uint64_t>(L.total_tiles, (uint64_t)n_sm * 4u);
   dim3 grid((uint32_t)ctas, L.n_sets);
-  expand_kernel<<<grid, 256, L.stage_bytes, reinterpret_cast<cudaStream_t>(stream)>>>(L);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl<true>(expand_kernel, grid, dim3(256), L.stage_bytes,
+                             reinterpret_cast<cudaStream_t>(stream), L);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("expand_kernel launch: ") + cudaGetErrorString(e));
     return QTN_ECUDA;

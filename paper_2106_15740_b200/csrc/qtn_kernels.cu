@@ -27,6 +27,7 @@
 #include "qtn_internal.h"
 #include "qtn_setmajor.h"
 #include "qtn_stream.h"
+#include "qtn_pdl.cuh"
 
 using namespace qtn;
 
@@ -346,6 +347,8 @@ __global__ void hbm_fold_kernel(const uint64_t* __restrict__ tags, const uint8_t
                                 const int64_t* __restrict__ net_in_off, const char* ws_base,
                                 int64_t ws_set_stride, const int64_t* __restrict__ net_ws_off,
                                 double2* __restrict__ results) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_hbm) return;
   const int set = blockIdx.y;
@@ -420,6 +423,8 @@ __device__ double2 gate_entry(int kind, double t, uint32_t i, double sre, double
 __global__ void tensorgen_kernel(const qtn_tensor_recipe* __restrict__ rec, int64_t n,
                                  const double* __restrict__ angles, int n_angles,
                                  int64_t set_elems, double2* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int set = blockIdx.y;
@@ -1290,12 +1295,15 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       if ((rc = launch_stream(L, stream, wide))) return rc;
     }
     dim3 grid((B->n_hbm + 127) / 128, n_sets);
-    hbm_fold_kernel<<<grid, 128, 0, st>>>(
-        B->d_fold_tags, B->d_fold_c64, B->d_fold_first, B->d_fold_pow2, B->d_hbm_index, B->n_hbm,
-        B->n, reinterpret_cast<const char*>(inputs), 16 * set_stride, B->d_net_in_off,
-        reinterpret_cast<const char*>(workspace), B->ws_per_set, B->d_net_ws_off,
+    cudaError_t e = launch_pdl<true>(
+        hbm_fold_kernel, grid, dim3(128), 0, st, (const uint64_t*)B->d_fold_tags,
+        (const uint8_t*)B->d_fold_c64, (const uint32_t*)B->d_fold_first,
+        (const int32_t*)B->d_fold_pow2, (const int32_t*)B->d_hbm_index, B->n_hbm, B->n,
+        reinterpret_cast<const char*>(inputs), (int64_t)(16 * set_stride),
+        (const int64_t*)B->d_net_in_off, reinterpret_cast<const char*>(workspace),
+        (int64_t)B->ws_per_set, (const int64_t*)B->d_net_ws_off,
         reinterpret_cast<double2*>(results));
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "hbm_fold_kernel launch");
   }
   return QTN_OK;
@@ -1313,9 +1321,9 @@ extern "C" int qtn_tensorgen(const qtn_tensor_recipe* recipes, int64_t n, const 
   if (n == 0) return QTN_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   dim3 grid((unsigned)((n + 127) / 128), n_sets);
-  tensorgen_kernel<<<grid, 128, 0, st>>>(recipes, n, angles, n_angles, set_elems,
-                                         reinterpret_cast<double2*>(out));
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl<true>(tensorgen_kernel, grid, dim3(128), 0, st, recipes, n, angles,
+                             (int)n_angles, set_elems, reinterpret_cast<double2*>(out));
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "tensorgen launch");
   return QTN_OK;
 }

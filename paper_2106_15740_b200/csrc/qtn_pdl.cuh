@@ -16,16 +16,23 @@
 
 namespace qtn {
 
-inline bool pdl_enabled() {
-  static int on = -1;
+// Set-major level kernels: on by default (QTN_PDL=0 disables; measured
+// config 2 +2.7 %).  HBM executor kernels: off by default (QTN_PDL_HBM=1
+// enables; measured config 4 -2 %, config 3 default -7 % with the trigger at
+// kernel start: early-resident dependents compete with the persistent tile
+// kernel).
+inline bool pdl_enabled(bool hbm) {
+  static int on = -1, on_hbm = -1;
   if (on < 0) {
     const char* v = getenv("QTN_PDL");
     on = (v && v[0] == '0') ? 0 : 1;
+    const char* h = getenv("QTN_PDL_HBM");
+    on_hbm = (h && h[0] == '1') ? 1 : 0;
   }
-  return on == 1;
+  return hbm ? on_hbm == 1 : on == 1;
 }
 
-template <typename... KArgs, typename... Args>
+template <bool HBM = false, typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg{};
@@ -37,7 +44,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl_enabled(HBM) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

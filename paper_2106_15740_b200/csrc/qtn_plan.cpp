@@ -454,7 +454,7 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
 // (<= kXStageMax entries) and a healthy tile count allow.
 bool encode_expand_desc(const BucketSpec& s, XDesc& d) {
   const char* ev = getenv("QTN_EXPAND_MIN_R");
-  const int min_r = ev ? atoi(ev) : 14;
+  const int min_r = ev ? atoi(ev) : 14;  // measured: 14 beats 18 on configs 3 default and 4
   const int R = (int)s.out_vars.size();
   if (R < min_r || R > 40) return false;
   std::memset(&d, 0, sizeof(d));

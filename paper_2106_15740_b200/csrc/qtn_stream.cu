@@ -22,6 +22,7 @@
 // flattened, each block takes a contiguous range of tiles.
 #define QTN_STREAM_NS s256
 #include "qtn_stream_tile.cuh"
+#include "qtn_pdl.cuh"
 
 namespace qtn {
 using s256::Bases;
@@ -42,6 +43,8 @@ using s256::resolve;
 constexpr uint32_t kSmallChunk = 1024;
 __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ StreamLaunch L,
                                                     uint32_t tpi_log2) {
+  pdl_trigger();
+  pdl_wait();
   const uint32_t tpi = 1u << tpi_log2;
   const uint32_t item = blockIdx.x * (256u >> tpi_log2) + (threadIdx.x >> tpi_log2);
   if (item >= L.n_items) return;
@@ -101,8 +104,9 @@ int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream) {
   const uint32_t chunks =
       tpi_log2 == 8u ? (uint32_t)(((1ull << max_r) + kSmallChunk - 1) / kSmallChunk) : 1u;
   dim3 grid((L.n_items + per_block - 1) / per_block, chunks, L.n_sets);
-  small_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(L, tpi_log2);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl<true>(small_kernel, grid, dim3(256), 0,
+                             reinterpret_cast<cudaStream_t>(stream), L, tpi_log2);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("small_kernel launch: ") + cudaGetErrorString(e));
     return QTN_ECUDA;
@@ -121,6 +125,8 @@ __global__ void __launch_bounds__(256) reduce_kernel(const __grid_constant__ Str
                                                      const RedDev* __restrict__ items,
                                                      const uint32_t* __restrict__ prefix,
                                                      uint32_t n_items) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ uint64_t offs[256];
   __shared__ double2 part[8][32];
   const uint32_t cb = blockIdx.x;
@@ -227,8 +233,9 @@ int launch_reduce(const StreamLaunch& L, const RedDev* items, const uint32_t* pr
                   uint32_t n_items, uint32_t total_chunks, void* stream) {
   if (!n_items || !total_chunks || !L.n_sets) return QTN_OK;
   dim3 grid(total_chunks, L.n_sets);
-  reduce_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(L, items, prefix, n_items);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl<true>(reduce_kernel, grid, dim3(256), 0,
+                             reinterpret_cast<cudaStream_t>(stream), L, items, prefix, n_items);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("reduce_kernel launch: ") + cudaGetErrorString(e));
     return QTN_ECUDA;

@@ -10,6 +10,7 @@
 
 #include "qtn_internal.h"
 #include "qtn_stream.h"
+#include "qtn_pdl.cuh"
 
 #ifndef QTN_STREAM_NS
 #error "define QTN_STREAM_NS before including qtn_stream_tile.cuh"
@@ -411,6 +412,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(128) uint8_t smraw[];
   Smem& S = *reinterpret_cast<Smem*>(smraw);
   const uint32_t tid = threadIdx.x;
+  pdl_trigger();
+  pdl_wait();  // operands written by the previous level
   uint64_t total;
   if (L.item_desc) total = L.total_tiles * L.n_sets;
   else total = reinterpret_cast<const SHdr*>(D.bytes)->n_tiles;
@@ -639,8 +642,9 @@ int prep() {
 
 int launch(const StreamLaunch& L, const InlineDesc& D, uint64_t total, void* stream) {
   const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)g_sms);
-  stream_kernel<<<grid, kThreads, sizeof(Smem), reinterpret_cast<cudaStream_t>(stream)>>>(L, D);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl<true>(stream_kernel, dim3(grid), dim3(kThreads), sizeof(Smem),
+                             reinterpret_cast<cudaStream_t>(stream), L, D);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("stream_kernel launch: ") + cudaGetErrorString(e));
     return QTN_ECUDA;
