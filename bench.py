@@ -519,7 +519,7 @@ def run_gpu(args):
     if plan.hbm_jobs:
         kname = "stream_kernel"
     elif plan._batch.uses_setmajor(A):
-        kname = "sm_level_kernel"
+        kname = "sm_level_kernel_c64" if plan._batch.setmajor_elem_bytes(A) == 8 else "sm_level_kernel"
     else:
         kname = "smem_net_kernel"
     achieved = alg / kt / 1e9

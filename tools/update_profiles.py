@@ -74,12 +74,17 @@ def main():
     smem = summary(os.path.join(R, "prof_smem.ncu-rep"))
     c5 = summary(os.path.join(R, "prof_stream_c5.ncu-rep"))
     s4 = agg["stream_kernel"]
+    x4 = agg.get("expand_kernel")
     out = {"note": "dram_bytes_per_launch: DRAM bytes (read+write) of the kernel for one "
                    "evaluation of the workload; for multi-launch executors (set-major levels, "
                    "streaming levels) summed over the launches of one evaluation",
            "kernels": {
-               "sm_level_kernel@config2": dict(sm, workload="config2: 150 edges x 1024 angle "
-                                                          "sets, one evaluation = 15 level launches"),
+               "sm_level_kernel_c64@config2": dict(sm, workload="config2: 150 edges x 1024 angle "
+                                                              "sets, complex64 rows, one evaluation "
+                                                              "= 15 level launches"),
+               "expand_kernel@config4": dict(summary(os.path.join(R, "prof_expand_c4.ncu-rep")),
+                                             workload="config4 edge #1058: the [1,22,21]->26 "
+                                                      "expanding bucket, one launch"),
                "smem_net_kernel@config2-16sets": dict(smem, workload="config2, 16 angle sets "
                                                                      "(warp-resident executor)"),
                "stream_kernel@config5": dict(c5, workload="config5 w=30 m=16, one launch"),
@@ -90,6 +95,12 @@ def main():
                                          "time_sum_s": s4["time_s"],
                                          "dram_bytes_per_launch": s4["dram_bytes"],
                                          "source": f"launches_{TAG}_config4.json"}}}
+    if x4:
+        out["kernels"]["expand_kernel@config4-all"] = {
+            "kernel": "expand_kernel", "workload": "config4 edge #1058, one contraction: its "
+                                                   "expand_kernel launches",
+            "launches_summed": x4["launches"], "time_sum_s": x4["time_s"],
+            "dram_bytes_per_launch": x4["dram_bytes"], "source": f"launches_{TAG}_config4.json"}
     json.dump(out, open(os.path.join(P, f"ncu_full_{TAG}.json"), "w"), indent=1)
     for name in sorted(os.listdir(P)):
         if name.startswith("bench_"):
