@@ -161,6 +161,7 @@ __device__ __forceinline__ void expand_tile(const XDesc& d, XItemSmem& X, const 
 __global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ XLaunch L) {
   extern __shared__ __align__(16) unsigned char xsmem[];
   __shared__ XItemSmem X;
+  __shared__ __align__(16) XDesc SD;
   pdl_trigger();
   pdl_wait();
   const uint64_t per = (L.total_tiles + gridDim.x - 1) / gridDim.x;
@@ -182,11 +183,17 @@ __global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ XLa
       }
       first = L.tile_prefix[lo];
       item_end = L.tile_prefix[lo + 1];
-      d = &L.descs[L.item_desc[lo]];
+      const XDesc* gd = &L.descs[L.item_desc[lo]];
       const uint32_t net = L.item_net[lo];
       in = L.in_base + (int64_t)set * L.in_set_stride + L.net_in_off[net];
       ws = L.ws_base + (int64_t)set * L.ws_set_stride + L.net_ws_off[net];
-      __syncthreads();  // the previous item's tables are no longer read
+      __syncthreads();  // the previous item's tables and descriptor are no longer read
+      // the descriptor into shared memory (one 16-byte load per thread): every
+      // run list below is read from there instead of through L1/L2
+      for (uint32_t i = tid; i < sizeof(XDesc) / 16; i += 256)
+        reinterpret_cast<uint4*>(&SD)[i] = __ldg(reinterpret_cast<const uint4*>(gd) + i);
+      __syncthreads();
+      d = &SD;
       const uint32_t nA = d->nA, nAB = d->nA + d->nB;
       if (tid < nAB) {
         X.ptr[tid] = xresolve(d->ops[tid].ptr, in, ws);

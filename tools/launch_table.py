@@ -12,7 +12,7 @@ for r in rows:
     d[r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * UNIT.get(r["Metric Unit"], 1)
 ks = sorted(ids)
 st = [k for k in ks if "tensorgen" in ids[k]["k"] or "gate_rows" in ids[k]["k"]][0]
-en = [k for k in ks if "energy" in ids[k]["k"] and k > st][0]
+en = ([k for k in ks if "energy" in ids[k]["k"] and k > st] or [ks[-1]])[0]
 tot = {}
 for k in ks:
     if k < st or k > en:
