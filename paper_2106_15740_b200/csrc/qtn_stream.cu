@@ -54,7 +54,18 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
   l.set = blockIdx.z;
   l.tile = 0;
   const Bases b = bases_of(L, l);
-  const uint8_t* dsc = L.descs + L.item_desc[item];
+  // the item's descriptor into shared memory (its run lists are read per
+  // element; from L1/L2 they were a chain of dependent loads)
+  __shared__ uint4 sdesc[8][(kSDescMax + 15) / 16];
+  const uint8_t* gdsc = L.descs + L.item_desc[item];
+  uint4* slot = sdesc[tpi == 256 ? 0 : (threadIdx.x >> 5)];
+  {
+    const uint32_t n16 = (reinterpret_cast<const SHdr*>(gdsc)->desc_bytes + 15u) / 16u;
+    for (uint32_t i = lane; i < n16; i += tpi) slot[i] = __ldg(reinterpret_cast<const uint4*>(gdsc) + i);
+    if (tpi == 256) __syncthreads();
+    else __syncwarp();
+  }
+  const uint8_t* dsc = reinterpret_cast<const uint8_t*>(slot);
   const SHdr& h = *reinterpret_cast<const SHdr*>(dsc);
   const SGRec* gr = reinterpret_cast<const SGRec*>(dsc + sizeof(SHdr));
   const STRec* tr = reinterpret_cast<const STRec*>(dsc + sizeof(SHdr) + h.ng * sizeof(SGRec));
