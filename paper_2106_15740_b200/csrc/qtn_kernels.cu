@@ -631,6 +631,9 @@ struct qtn_batch {
   uint32_t* d_sitem_net = nullptr;
   std::vector<uint32_t> level_sitem0;   // first small item of each level (+ end)
   std::vector<uint32_t> level_smax_r;   // widest small item of each level
+  std::vector<uint8_t> level_tiny;      // small_kernel-only level with <= QTN_CHAIN_ELEMS outputs
+  std::vector<uint32_t> chain_len;      // per level: length of the tiny-level chain starting here (0: none)
+  uint32_t* d_level_sitem0 = nullptr;
   // expanding buckets of each level (expand_kernel)
   qtn::XDesc* d_xdesc = nullptr;
   uint32_t* d_xitem_desc = nullptr;
@@ -668,7 +671,8 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_fold_first, (void*)B->d_fold_pow2, (void*)B->d_hbm_index,
                   (void*)B->d_hbm_rec, (void*)B->d_sitem_desc, (void*)B->d_sitem_net,
                   (void*)B->d_red, (void*)B->d_red_prefix, (void*)B->d_xdesc,
-                  (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix})
+                  (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix,
+                  (void*)B->d_level_sitem0})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
   delete B;
@@ -810,6 +814,15 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     }
     B->level_tiles.push_back(acc);
     B->level_smax_r.push_back(smax_r);
+    {
+      // chain_kernel candidates: few enough outputs for one CTA cluster
+      // (a warp per bucket: every bucket of the level at most 2^QTN_CHAIN_R outputs)
+      const char* ce = getenv("QTN_CHAIN_ELEMS");
+      const uint64_t chain_elems = ce ? strtoull(ce, nullptr, 10) : 16384;
+      const char* cr = getenv("QTN_CHAIN_R");
+      const uint32_t chain_r = cr ? (uint32_t)atoi(cr) : 9;
+      B->level_tiny.push_back(all_small && lev_elems <= chain_elems && smax_r <= chain_r ? 1 : 0);
+    }
     B->level_xtiles.push_back(xacc);
     B->level_xstage.push_back(xstage);
   }
@@ -845,6 +858,26 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     B->level_rchunks.push_back(acc);
   }
   B->level_red0.push_back((uint32_t)reds.size());
+  // runs of consecutive tiny levels (small items only) become one
+  // cluster launch each (chain_kernel) with QTN_CHAIN=1.  Off by default:
+  // measured equal to one small_kernel launch per level inside the captured
+  // graph (config 4: 788 vs 788 /s; config 3 default 69.6 k vs 69.5 k)
+  {
+    const char* cv = getenv("QTN_CHAIN");
+    const bool chain_on = cv && cv[0] == '1';
+    const size_t nl = B->level_tiles.size();
+    B->chain_len.assign(nl, 0);
+    auto tiny_only = [&](size_t l) {
+      return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] &&
+             B->level_red0[l + 1] == B->level_red0[l] && B->level_sitem0[l + 1] > B->level_sitem0[l];
+    };
+    for (size_t l = 0; chain_on && l < nl;) {
+      size_t e = l;
+      while (e < nl && tiny_only(e)) ++e;
+      if (e - l >= 2) B->chain_len[l] = (uint32_t)(e - l);
+      l = e > l ? e : l + 1;
+    }
+  }
   // scalar folds
   std::vector<uint64_t> ftags;
   std::vector<uint8_t> fc64;
@@ -870,6 +903,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_red, reds)) || (rc = upload(&B->d_red_prefix, rprefix)) ||
       (rc = upload(&B->d_xdesc, xdescs)) || (rc = upload(&B->d_xitem_desc, xitem_desc)) ||
       (rc = upload(&B->d_xitem_net, xitem_net)) || (rc = upload(&B->d_xprefix, xprefix)) ||
+      (rc = upload(&B->d_level_sitem0, B->level_sitem0)) ||
       (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
       (rc = upload(&B->d_fold_tags, ftags)) || (rc = upload(&B->d_fold_c64, fc64)) ||
       (rc = upload(&B->d_fold_first, ffirst)) || (rc = upload(&B->d_fold_pow2, fpow2)) ||
@@ -917,9 +951,15 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
   int c = B->n_smem ? 1 : 0;
   if (B->n_smem && use_setmajor(B, n_sets)) c = qtn::setmajor_launches(B->sm, n_sets);
   if (B->n_hbm) {
-    for (size_t lev = 0; lev < B->level_tiles.size(); ++lev)
+    for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
+      if (B->chain_len[lev]) {
+        c += 1;
+        lev += B->chain_len[lev] - 1;
+        continue;
+      }
       c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0);
+    }
     c += 1;
   }
   *out = c;
@@ -1249,6 +1289,16 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       L.ws_base = reinterpret_cast<char*>(workspace);
       L.ws_set_stride = B->ws_per_set;
       L.net_ws_off = B->d_net_ws_off;
+      if (B->chain_len[lev]) {
+        StreamLaunch Lc = L;
+        Lc.item_desc = B->d_sitem_desc;
+        Lc.item_net = B->d_sitem_net;
+        Lc.n_items = B->level_sitem0.back();
+        if ((rc = qtn::launch_chain(Lc, B->d_level_sitem0 + lev, B->chain_len[lev], stream)))
+          return rc;
+        lev += B->chain_len[lev] - 1;
+        continue;
+      }
       const uint32_t nr = B->level_red0[lev + 1] - B->level_red0[lev];
       if (nr && (rc = qtn::launch_reduce(L, B->d_red + B->level_red0[lev],
                                          B->d_red_prefix + B->level_rprefix0[lev], nr,

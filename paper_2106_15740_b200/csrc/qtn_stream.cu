@@ -40,6 +40,58 @@ using s256::resolve;
 // index o (every run list covers all output bits).
 // CTA mode (tpi = 256): blockIdx.y selects a chunk of kSmallChunk elements,
 // so a few wide buckets (tail levels of one network) still spread over SMs.
+// Elements o = o_begin, o_begin + o_step, ... < o_end of one bucket, every
+// operand gathered: out[o] = sum_v P[o | v] * prod_tables prod_ops Op[..] *
+// prod_gathered G[..].  CG: operand loads through L2 only (coherent with
+// writes of other CTAs ordered by a cluster barrier, chain_kernel).
+template <bool CG>
+__device__ __forceinline__ double2 ld_op(const void* p, uint64_t i, uint32_t c64) {
+  if (!CG) return ldg_c(p, i, c64);
+  if (c64) {
+    const float2 f = __ldcg(reinterpret_cast<const float2*>(p) + i);
+    return make_double2(f.x, f.y);
+  }
+  return __ldcg(reinterpret_cast<const double2*>(p) + i);
+}
+template <bool CG>
+__device__ __forceinline__ void small_eval(const uint8_t* dsc, const Bases& b, uint64_t o_begin,
+                                           uint64_t o_end, uint64_t o_step) {
+  const SHdr& h = *reinterpret_cast<const SHdr*>(dsc);
+  const SGRec* gr = reinterpret_cast<const SGRec*>(dsc + sizeof(SHdr));
+  const STRec* tr = reinterpret_cast<const STRec*>(dsc + sizeof(SHdr) + h.ng * sizeof(SGRec));
+  const SORec* orr =
+      reinterpret_cast<const SORec*>(dsc + sizeof(SHdr) + h.ng * sizeof(SGRec) + h.nt * sizeof(STRec));
+  const char* P = resolve(h.p, b);
+  char* out = const_cast<char*>(resolve(h.out, b));
+  const uint32_t r1 = h.p_rank - 1u, pk = h.p_k;
+  for (uint64_t o = o_begin; o < o_end; o += o_step) {
+    const uint64_t op = o & ((1ull << r1) - 1);
+    const uint64_t p0 = (op & ((1ull << pk) - 1)) | ((op >> pk) << (pk + 1));
+    double2 a0 = ld_op<CG>(P, p0, h.p_c64), a1 = ld_op<CG>(P, p0 | (1ull << pk), h.p_c64);
+    for (uint32_t q = 0; q < h.nt; ++q) {
+      const uint64_t bits = gather(o, tr[q].runs, tr[q].n_runs);
+      for (uint32_t k = 0; k < tr[q].n_ops; ++k) {
+        const SORec& O = orr[tr[q].first_op + k];
+        const char* op_p = resolve(O.ptr, b);
+        const uint64_t idx = gather(bits, O.runs, O.n_runs);
+        a0 = cmul(a0, ld_op<CG>(op_p, idx, O.c64));
+        a1 = cmul(a1, ld_op<CG>(op_p, idx | (1ull << O.vshift), O.c64));
+      }
+    }
+    for (uint32_t g = 0; g < h.ng; ++g) {
+      const char* gp = resolve(gr[g].ptr, b);
+      const uint64_t idx = gather(o, gr[g].runs, gr[g].n_runs);
+      a0 = cmul(a0, ld_op<CG>(gp, idx, gr[g].c64));
+      a1 = cmul(a1, ld_op<CG>(gp, idx | (1ull << gr[g].vshift), gr[g].c64));
+    }
+    const double2 r = make_double2(a0.x + a1.x, a0.y + a1.y);
+    if (h.out_c64)
+      reinterpret_cast<float2*>(out)[o] = make_float2((float)r.x, (float)r.y);
+    else
+      reinterpret_cast<double2*>(out)[o] = r;
+  }
+}
+
 constexpr uint32_t kSmallChunk = 1024;
 __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ StreamLaunch L,
                                                     uint32_t tpi_log2) {
@@ -66,44 +118,11 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
     else __syncwarp();
   }
   const uint8_t* dsc = reinterpret_cast<const uint8_t*>(slot);
-  const SHdr& h = *reinterpret_cast<const SHdr*>(dsc);
-  const SGRec* gr = reinterpret_cast<const SGRec*>(dsc + sizeof(SHdr));
-  const STRec* tr = reinterpret_cast<const STRec*>(dsc + sizeof(SHdr) + h.ng * sizeof(SGRec));
-  const SORec* orr =
-      reinterpret_cast<const SORec*>(dsc + sizeof(SHdr) + h.ng * sizeof(SGRec) + h.nt * sizeof(STRec));
-  const char* P = resolve(h.p, b);
-  char* out = const_cast<char*>(resolve(h.out, b));
-  const uint32_t r1 = h.p_rank - 1u, pk = h.p_k;
-  const uint64_t n_all = 1ull << h.R;
+  const uint64_t n_all = 1ull << reinterpret_cast<const SHdr*>(dsc)->R;
   const uint64_t o0 = tpi == 256 ? (uint64_t)blockIdx.y * kSmallChunk : 0;
   if (o0 >= n_all) return;
   const uint64_t n_out = tpi == 256 ? min(n_all, o0 + kSmallChunk) : n_all;
-  for (uint64_t o = o0 + lane; o < n_out; o += tpi) {
-    const uint64_t op = o & ((1ull << r1) - 1);
-    const uint64_t p0 = (op & ((1ull << pk) - 1)) | ((op >> pk) << (pk + 1));
-    double2 a0 = ldg_c(P, p0, h.p_c64), a1 = ldg_c(P, p0 | (1ull << pk), h.p_c64);
-    for (uint32_t q = 0; q < h.nt; ++q) {
-      const uint64_t bits = gather(o, tr[q].runs, tr[q].n_runs);
-      for (uint32_t k = 0; k < tr[q].n_ops; ++k) {
-        const SORec& O = orr[tr[q].first_op + k];
-        const char* op_p = resolve(O.ptr, b);
-        const uint64_t idx = gather(bits, O.runs, O.n_runs);
-        a0 = cmul(a0, ldg_c(op_p, idx, O.c64));
-        a1 = cmul(a1, ldg_c(op_p, idx | (1ull << O.vshift), O.c64));
-      }
-    }
-    for (uint32_t g = 0; g < h.ng; ++g) {
-      const char* gp = resolve(gr[g].ptr, b);
-      const uint64_t idx = gather(o, gr[g].runs, gr[g].n_runs);
-      a0 = cmul(a0, ldg_c(gp, idx, gr[g].c64));
-      a1 = cmul(a1, ldg_c(gp, idx | (1ull << gr[g].vshift), gr[g].c64));
-    }
-    const double2 r = make_double2(a0.x + a1.x, a0.y + a1.y);
-    if (h.out_c64)
-      reinterpret_cast<float2*>(out)[o] = make_float2((float)r.x, (float)r.y);
-    else
-      reinterpret_cast<double2*>(out)[o] = r;
-  }
+  small_eval<false>(dsc, b, o0 + lane, n_out, tpi);
 }
 
 int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream) {
@@ -120,6 +139,72 @@ int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream) {
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("small_kernel launch: ") + cudaGetErrorString(e));
+    return QTN_ECUDA;
+  }
+  return QTN_OK;
+}
+
+// ---- chains of tiny levels (head and tail of the elimination trees):
+// one cluster of kChainCTAs CTAs per angle set runs every level of the chain
+// in order, the level's buckets spread over the cluster's threads, a
+// cluster barrier (release/acquire) between levels instead of a kernel
+// launch per level.  Operands are read through L2 (ld.global.cg).
+constexpr uint32_t kChainCTAs = 8;
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__global__ void __launch_bounds__(256) chain_kernel(const __grid_constant__ StreamLaunch L,
+                                                    const uint32_t* __restrict__ level_item0,
+                                                    uint32_t n_levels) {
+  pdl_trigger();
+  pdl_wait();
+  // a warp per bucket (buckets of a level round-robin over the cluster's
+  // warps), its descriptor staged in the warp's shared-memory slot
+  __shared__ uint4 sdesc[8][(kSDescMax + 15) / 16];
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t gwarp = rank * 8u + warp, n_warps = 8u * kChainCTAs;
+  uint4* slot = sdesc[warp];
+  Loc l;
+  l.set = blockIdx.y;
+  l.tile = 0;
+  for (uint32_t lv = 0; lv < n_levels; ++lv) {
+    for (uint32_t it = level_item0[lv] + gwarp; it < level_item0[lv + 1]; it += n_warps) {
+      l.item = it;
+      const Bases b = bases_of(L, l);
+      const uint8_t* gdsc = L.descs + L.item_desc[it];
+      const uint32_t n16 = (reinterpret_cast<const SHdr*>(gdsc)->desc_bytes + 15u) / 16u;
+      __syncwarp();  // the warp's previous descriptor is no longer read
+      for (uint32_t i = lane; i < n16; i += 32) slot[i] = __ldg(reinterpret_cast<const uint4*>(gdsc) + i);
+      __syncwarp();
+      const uint8_t* dsc = reinterpret_cast<const uint8_t*>(slot);
+      small_eval<true>(dsc, b, lane, 1ull << reinterpret_cast<const SHdr*>(dsc)->R, 32);
+    }
+    cluster_sync_all();
+  }
+}
+
+int launch_chain(const StreamLaunch& L, const uint32_t* level_item0_dev, uint32_t n_levels,
+                 void* stream) {
+  if (!n_levels || !L.n_sets) return QTN_OK;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kChainCTAs, L.n_sets);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kChainCTAs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, chain_kernel, L, level_item0_dev, n_levels);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("chain_kernel launch: ") + cudaGetErrorString(e));
     return QTN_ECUDA;
   }
   return QTN_OK;

@@ -158,6 +158,12 @@ inline uint32_t red_chunk(uint32_t k) {
 int launch_reduce(const StreamLaunch& L, const RedDev* items, const uint32_t* prefix,
                   uint32_t n_items, uint32_t total_chunks, void* stream);
 int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream);
+// A run of consecutive tiny levels in one launch (a CTA cluster per set,
+// cluster barriers between levels).  L.item_desc/item_net: the small-item
+// lists; level_item0_dev[0..n_levels]: item range of each level (absolute
+// indices into those lists).
+int launch_chain(const StreamLaunch& L, const uint32_t* level_item0_dev, uint32_t n_levels,
+                 void* stream);
 // ---- expanding buckets (output wider than its primary operand): the
 // outer-product form.  Output bits split into tile-local A bits (9: 256
 // threads x 2 adjacent outputs, bits 0-5 always among them so a warp writes

@@ -581,3 +581,26 @@ def test_expand_kernel_config3_default(golden, monkeypatch):
         w = complex(*r["value"])
         assert abs(vals["1"][r["edge_index"]] - w) <= 1e-11 * abs(w) + 1e-13
         assert abs(vals["1"][r["edge_index"]] - vals["0"][r["edge_index"]]) <= 1e-11 * abs(w) + 1e-13
+
+
+def test_chain_kernel_opt_in(golden, monkeypatch):
+    """Tiny-level chains in one cluster launch (QTN_CHAIN=1, cluster barriers
+    between levels) equal the per-level small_kernel launches (config 4 edge
+    #16 and config 3 default networks, complex128), with fewer launches."""
+    G4 = golden("config4.json")
+    g4 = Q.random_regular_graph(G4["n"], 3, 0)
+    p4 = Q.QaoaParams(G4["gammas"], G4["betas"])
+    G3 = golden("config3.json")
+    g3 = Q.random_regular_graph(G3["n"], 3, 0)
+    p3 = Q.QaoaParams(G3["gammas"], G3["betas"])
+    ids3 = [r["edge_index"] for r in G3["modes"]["default"][:10]]
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_CHAIN", flag)
+        a = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype="complex128", edge_ids=[16])
+        b = Q.EnergyPlan(g3, G3["p"], "default", dtype="complex128", edge_ids=ids3)
+        out[flag] = (a.zz_values(p4)[16], b.zz_values(p3), a.launches_per_eval(1))
+    assert abs(out["1"][0] - out["0"][0]) <= 1e-12 * abs(out["0"][0])
+    for e in ids3:
+        assert abs(out["1"][1][e] - out["0"][1][e]) <= 1e-12 * abs(out["0"][1][e]) + 1e-14
+    assert out["1"][2] < out["0"][2]
