@@ -544,7 +544,10 @@ int setmajor_run(SetMajor* S, const double* angles, int32_t n_angles, int32_t n_
       else if (stride >= 1024)
         launch_pdl(sm_level_kernel_c64<2, false>, blocks, dim3(256), 0, st, r, ws, stride);
       else
-        launch_pdl(sm_level_kernel_c64<1, false>, blocks, dim3(256), 0, st, r, ws, stride);
+        // fewer than 512 sets: one pass needs only stride/2 threads
+        launch_pdl(sm_level_kernel_c64<1, false>, blocks,
+                   dim3(std::min(256, std::max(32, ((stride / 2) + 31) / 32 * 32))), 0, st, r, ws,
+                   stride);
     }
     launch_pdl(sm_fold_kernel<float2>, gf, dim3(128), 0, st, (const double2*)S->d_const,
                (const uint32_t*)S->d_scal_first, (const uint32_t*)S->d_scal,
