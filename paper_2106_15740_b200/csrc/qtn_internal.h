@@ -208,6 +208,8 @@ struct qtn_plan {
   std::vector<uint64_t> hbm_tiles;
   std::vector<int32_t> hbm_xidx;         // expanding-bucket descriptor per bucket, or -1
   std::vector<qtn::XDesc> hbm_xdesc;
+  std::vector<int32_t> hbm_r1idx;        // single-operand (trace) record per bucket, or -1
+  std::vector<qtn::R1Dev> hbm_r1;        // net = 0 here; set per batch
   int32_t n_levels = 0;
   // Set-major form of an SMEM-eligible network (qtn_setmajor.cu): angle
   // sets are the fastest-varying dimension of every tensor in HBM, one

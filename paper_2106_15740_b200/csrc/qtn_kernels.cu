@@ -634,6 +634,11 @@ struct qtn_batch {
   std::vector<uint8_t> level_tiny;      // small_kernel-only level with <= QTN_CHAIN_ELEMS outputs
   std::vector<uint32_t> chain_len;      // per level: length of the tiny-level chain starting here (0: none)
   uint32_t* d_level_sitem0 = nullptr;
+  // single-operand buckets of each level (trace_kernel)
+  qtn::R1Dev* d_r1 = nullptr;
+  uint64_t* d_r1prefix = nullptr;
+  std::vector<uint32_t> level_r1item0;  // first trace item of each level (+ end)
+  std::vector<uint64_t> level_r1prefix0, level_r1chunks;
   // expanding buckets of each level (expand_kernel)
   qtn::XDesc* d_xdesc = nullptr;
   uint32_t* d_xitem_desc = nullptr;
@@ -672,7 +677,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_hbm_rec, (void*)B->d_sitem_desc, (void*)B->d_sitem_net,
                   (void*)B->d_red, (void*)B->d_red_prefix, (void*)B->d_xdesc,
                   (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix,
-                  (void*)B->d_level_sitem0})
+                  (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
   delete B;
@@ -756,16 +761,27 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   const bool use_expand = !(xv && xv[0] == '0');
   std::vector<uint32_t> xitem_desc, xitem_net;
   std::vector<uint64_t> xprefix;
+  // single-operand buckets of output rank >= QTN_TRACE_MIN_R take
+  // trace_kernel (QTN_TRACE=0: the streaming kernel)
+  const char* tv0 = getenv("QTN_TRACE");
+  const bool use_trace = !(tv0 && tv0[0] == '0');
+  const char* tmr = getenv("QTN_TRACE_MIN_R");
+  const int trace_min_r = tmr ? atoi(tmr) : 10;
+  std::vector<qtn::R1Dev> r1items;
+  std::vector<uint64_t> r1prefix;
   for (int32_t lev = 0; lev < max_lev; ++lev) {
     B->level_item0.push_back((uint32_t)item_desc.size());
     B->level_prefix0.push_back(prefix.size());
     B->level_sitem0.push_back((uint32_t)sitem_desc.size());
     B->level_xitem0.push_back((uint32_t)xitem_desc.size());
     B->level_xprefix0.push_back(xprefix.size());
-    uint64_t acc = 0, xacc = 0;
+    B->level_r1item0.push_back((uint32_t)r1items.size());
+    B->level_r1prefix0.push_back(r1prefix.size());
+    uint64_t acc = 0, xacc = 0, r1acc = 0;
     uint32_t xstage = 0;
     prefix.push_back(0);
     xprefix.push_back(0);
+    r1prefix.push_back(0);
     // small buckets go to the warp/CTA-per-bucket kernel, unless the level
     // launches the streaming kernel anyway and they are few (one launch less)
     // a tiny level (few output elements in all) goes entirely to the small
@@ -797,6 +813,14 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
           smax_r = std::max<uint32_t>(smax_r, sh->R);
           continue;
         }
+        if (use_trace && P->hbm_r1idx[bi] >= 0 && (int)sh->R >= trace_min_r) {
+          qtn::R1Dev r = P->hbm_r1[P->hbm_r1idx[bi]];
+          r.net = (uint32_t)h;
+          r1items.push_back(r);
+          r1acc += ((1ull << r.R) + qtn::kTraceChunk - 1) / qtn::kTraceChunk;
+          r1prefix.push_back(r1acc);
+          continue;
+        }
         if (use_expand && P->hbm_xidx[bi] >= 0) {
           const qtn::XDesc& xd = P->hbm_xdesc[P->hbm_xidx[bi]];
           xitem_desc.push_back(xdesc_base[h] + (uint32_t)P->hbm_xidx[bi]);
@@ -825,7 +849,9 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     }
     B->level_xtiles.push_back(xacc);
     B->level_xstage.push_back(xstage);
+    B->level_r1chunks.push_back(r1acc);
   }
+  B->level_r1item0.push_back((uint32_t)r1items.size());
   B->level_item0.push_back((uint32_t)item_desc.size());
   B->level_sitem0.push_back((uint32_t)sitem_desc.size());
   B->level_xitem0.push_back((uint32_t)xitem_desc.size());
@@ -868,7 +894,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     const size_t nl = B->level_tiles.size();
     B->chain_len.assign(nl, 0);
     auto tiny_only = [&](size_t l) {
-      return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] &&
+      return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] && !B->level_r1chunks[l] &&
              B->level_red0[l + 1] == B->level_red0[l] && B->level_sitem0[l + 1] > B->level_sitem0[l];
     };
     for (size_t l = 0; chain_on && l < nl;) {
@@ -904,6 +930,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_xdesc, xdescs)) || (rc = upload(&B->d_xitem_desc, xitem_desc)) ||
       (rc = upload(&B->d_xitem_net, xitem_net)) || (rc = upload(&B->d_xprefix, xprefix)) ||
       (rc = upload(&B->d_level_sitem0, B->level_sitem0)) ||
+      (rc = upload(&B->d_r1, r1items)) || (rc = upload(&B->d_r1prefix, r1prefix)) ||
       (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
       (rc = upload(&B->d_fold_tags, ftags)) || (rc = upload(&B->d_fold_c64, fc64)) ||
       (rc = upload(&B->d_fold_first, ffirst)) || (rc = upload(&B->d_fold_pow2, fpow2)) ||
@@ -958,7 +985,8 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
         continue;
       }
       c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
-           (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0);
+           (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
+           (B->level_r1chunks[lev] ? 1 : 0);
     }
     c += 1;
   }
@@ -1312,6 +1340,12 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         Ls.n_items = ns;
         if ((rc = qtn::launch_small(Ls, B->level_smax_r[lev], stream))) return rc;
       }
+      if (B->level_r1chunks[lev] &&
+          (rc = qtn::launch_trace(L, B->d_r1 + B->level_r1item0[lev],
+                                  B->d_r1prefix + B->level_r1prefix0[lev],
+                                  B->level_r1item0[lev + 1] - B->level_r1item0[lev],
+                                  B->level_r1chunks[lev], stream)))
+        return rc;
       if (B->level_xtiles[lev]) {
         qtn::XLaunch X;
         std::memset(&X, 0, sizeof(X));

@@ -1023,6 +1023,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       return t.input ? tag_in(16ull * (uint64_t)t.in_off) : tag_ws((uint64_t)t.ws_off);
     };
     P->hbm_xidx.assign(nb, -1);
+    P->hbm_r1idx.assign(nb, -1);
     for (int bi = 0; bi < nb; ++bi) {
       const auto& b = P->buckets[bi];
       P->hbm_desc_off.push_back(P->hbm_desc.size());
@@ -1071,6 +1072,27 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       }
       const SHdr* h = reinterpret_cast<const SHdr*>(P->hbm_desc.data() + P->hbm_desc_off.back());
       P->hbm_tiles.push_back(h->n_tiles);
+      if (b.ops.size() == 1) {
+        // a partial trace: output = the operand's variables minus v, same order
+        std::vector<int32_t> rest;
+        for (int32_t u : spec.opvars[0])
+          if (u != b.v) rest.push_back(u);
+        const int rk = (int)spec.opvars[0].size();
+        int pk = -1;
+        for (int j = 0; j < rk; ++j)
+          if (spec.opvars[0][j] == b.v) pk = rk - 1 - j;
+        if (rest == spec.out_vars && pk >= 0) {
+          R1Dev r{};
+          r.src = spec.optag[0];
+          r.out = spec.out_tag;
+          r.R = (uint8_t)spec.out_vars.size();
+          r.pk = (uint8_t)pk;
+          r.src_c64 = spec.opc64[0];
+          r.out_c64 = spec.out_c64 ? 1 : 0;
+          P->hbm_r1idx[bi] = (int32_t)P->hbm_r1.size();
+          P->hbm_r1.push_back(r);
+        }
+      }
       XDesc xd;
       if (encode_expand_desc(spec, xd)) {
         P->hbm_xidx[bi] = (int32_t)P->hbm_xdesc.size();

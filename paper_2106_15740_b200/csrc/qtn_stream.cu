@@ -210,6 +210,80 @@ int launch_chain(const StreamLaunch& L, const uint32_t* level_item0_dev, uint32_
   return QTN_OK;
 }
 
+// ---- single-operand buckets (partial traces), see qtn_stream.h
+__global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ StreamLaunch L,
+                                                    const R1Dev* __restrict__ items,
+                                                    const uint64_t* __restrict__ prefix,
+                                                    uint32_t n_items) {
+  pdl_trigger();
+  pdl_wait();
+  const uint64_t cb = blockIdx.x;
+  uint32_t lo = 0, hi = n_items;  // last item whose first chunk <= cb
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (prefix[mid] <= cb) lo = mid;
+    else hi = mid;
+  }
+  const R1Dev r = items[lo];
+  const uint32_t set = blockIdx.y;
+  Bases b;
+  b.in = L.in_base + (int64_t)set * L.in_set_stride + L.net_in_off[r.net];
+  b.ws = L.ws_base + (int64_t)set * L.ws_set_stride + L.net_ws_off[r.net];
+  const char* src = resolve(r.src, b);
+  char* out = const_cast<char*>(resolve(r.out, b));
+  const uint64_t n = 1ull << r.R;
+  const uint64_t o0 = (cb - prefix[lo]) * kTraceChunk;
+  const uint64_t o1 = min(n, o0 + kTraceChunk);
+  const uint32_t pk = r.pk;
+  const uint64_t vstep = 1ull << pk;
+  if (r.src_c64 && r.out_c64 && r.R >= 1) {
+    // two adjacent outputs per thread and step, 16-byte loads and stores
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* out4 = reinterpret_cast<float4*>(out);
+#pragma unroll 8
+    for (uint64_t p = o0 + 2u * threadIdx.x; p < o1; p += 512) {
+      float4 x, y;
+      if (pk >= 1) {
+        const uint64_t i0 = (p & (vstep - 1)) | ((p >> pk) << (pk + 1));  // even
+        x = __ldg(s4 + (i0 >> 1));
+        y = __ldg(s4 + ((i0 + vstep) >> 1));
+        out4[p >> 1] = make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+      } else {
+        x = __ldg(s4 + p);       // entries 2p, 2p+1
+        y = __ldg(s4 + p + 1);   // entries 2p+2, 2p+3
+        out4[p >> 1] = make_float4(x.x + x.z, x.y + x.w, y.x + y.z, y.y + y.w);
+      }
+    }
+    return;
+  }
+  for (uint64_t o = o0 + threadIdx.x; o < o1; o += 256) {
+    const uint64_t i0 = (o & (vstep - 1)) | ((o >> pk) << (pk + 1));
+    const double2 x = ldg_c(src, i0, r.src_c64), y = ldg_c(src, i0 + vstep, r.src_c64);
+    const double2 z = make_double2(x.x + y.x, x.y + y.y);
+    if (r.out_c64)
+      reinterpret_cast<float2*>(out)[o] = make_float2((float)z.x, (float)z.y);
+    else
+      reinterpret_cast<double2*>(out)[o] = z;
+  }
+}
+
+int launch_trace(const StreamLaunch& L, const R1Dev* items, const uint64_t* prefix,
+                 uint32_t n_items, uint64_t total_chunks, void* stream) {
+  if (!n_items || !total_chunks || !L.n_sets) return QTN_OK;
+  if (total_chunks > 0x7fffffffull || L.n_sets > 65535) {
+    set_error("trace_kernel: grid too large");
+    return QTN_EINVAL;
+  }
+  cudaError_t e = launch_pdl<true>(trace_kernel, dim3((uint32_t)total_chunks, L.n_sets), dim3(256), 0,
+                                   reinterpret_cast<cudaStream_t>(stream), L, items, prefix, n_items);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("trace_kernel launch: ") + cudaGetErrorString(e));
+    return QTN_ECUDA;
+  }
+  return QTN_OK;
+}
+
 // ---- fused single-operand chains (multi-variable partial traces)
 // out[o] = sum over the 2^k source entries spread(o) | offs[m].  A CTA of 8
 // warps covers 32 * (8 / G) consecutive outputs: lanes = outputs (32

@@ -219,6 +219,21 @@ struct XLaunch {
 };
 int launch_expand(const XLaunch& L, void* stream);
 
+// ---- single-operand buckets (partial traces, contraction.py:94-96 on a
+// bucket of one tensor): out[o] = P[o with 0 at bit pk] + P[o with 1 at pk],
+// the output layout being the primary's minus v.  A pure stream of 3 entries
+// per output, run by trace_kernel: 4096 outputs per CTA, 16-byte loads and
+// stores, many items per launch (prefix over 4096-output chunks).
+struct R1Dev {
+  uint64_t src, out;             // tagged pointers
+  uint32_t net;                  // network index (bases)
+  uint8_t R, pk, src_c64, out_c64;
+};
+static_assert(sizeof(R1Dev) == 24, "R1Dev");
+constexpr uint32_t kTraceChunk = 4096;
+int launch_trace(const StreamLaunch& L, const R1Dev* items, const uint64_t* prefix,
+                 uint32_t n_items, uint64_t total_chunks, void* stream);
+
 // single descriptor with absolute pointers, descriptor passed by value
 int launch_stream_single(const std::vector<uint8_t>& desc, void* stream);
 

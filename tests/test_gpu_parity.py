@@ -604,3 +604,34 @@ def test_chain_kernel_opt_in(golden, monkeypatch):
     for e in ids3:
         assert abs(out["1"][1][e] - out["0"][1][e]) <= 1e-12 * abs(out["0"][1][e]) + 1e-14
     assert out["1"][2] < out["0"][2]
+
+
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-12), ("complex64", 1e-6)])
+def test_trace_kernel_matches_stream_kernel(golden, monkeypatch, dtype, tol):
+    """Single-operand buckets (partial traces, 59 % of config 3 default's
+    bytes) on trace_kernel equal the streaming kernel (QTN_TRACE=0) and the
+    reference values; config 3 default networks and config 4 edge #16."""
+    G3 = golden("config3.json")
+    g3 = Q.random_regular_graph(G3["n"], 3, 0)
+    p3 = Q.QaoaParams(G3["gammas"], G3["betas"])
+    recs = G3["modes"]["default"][:10]
+    ids3 = [r["edge_index"] for r in recs]
+    G4 = golden("config4.json")
+    g4 = Q.random_regular_graph(G4["n"], 3, 0)
+    p4 = Q.QaoaParams(G4["gammas"], G4["betas"])
+    w4 = complex(*[r for r in G4["modes"]["zz+diagonal"] if r["edge_index"] == 16][0]["value"])
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_TRACE", flag)
+        a = Q.EnergyPlan(g3, G3["p"], "default", dtype=dtype, edge_ids=ids3)
+        b = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype=dtype, edge_ids=[16])
+        out[flag] = (a.zz_values(p3), b.zz_values(p4)[16])
+        assert a.launches == a.launches_per_eval(1)
+    ref_tol = 1e-11 if dtype == "complex128" else 1e-5
+    for r in recs:
+        w = complex(*r["value"])
+        e = r["edge_index"]
+        assert abs(out["1"][0][e] - w) <= ref_tol * abs(w) + 1e-13
+        assert abs(out["1"][0][e] - out["0"][0][e]) <= tol * abs(w) + 1e-13
+    assert abs(out["1"][1] - w4) <= ref_tol * abs(w4)
+    assert abs(out["1"][1] - out["0"][1]) <= tol * abs(w4)
