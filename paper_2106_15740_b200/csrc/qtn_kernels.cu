@@ -801,6 +801,29 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     const uint64_t tiny = tv ? strtoull(tv, nullptr, 10) : (1ull << 17);
     const bool all_small = lev_elems <= tiny;
     const bool split_small = all_small || (n_small > 0 && (n_large == 0 || n_small >= 148));
+    // trace_kernel for this level's single-operand buckets when it saves a
+    // pass: no other streamed bucket in the level (no extra launch), or
+    // enough trace bytes to pay for the extra launch (QTN_TRACE_MIN_MB)
+    bool trace_level = false;
+    {
+      const char* tmb = getenv("QTN_TRACE_MIN_MB");
+      const double min_bytes = (tmb ? atof(tmb) : 32.0) * 1e6;
+      double tbytes = 0.0;
+      bool other = false;
+      for (int h = 0; h < B->n_hbm; ++h) {
+        const qtn_plan* P = plans[hidx[h]];
+        for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
+          if (P->hbm_level[bi] != lev || !P->hbm_tiles[bi]) continue;
+          const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
+          if (split_small && (all_small || (int)sh->R <= small_r)) continue;
+          if (P->hbm_r1idx[bi] >= 0 && (int)sh->R >= trace_min_r)
+            tbytes += std::ldexp(P->hbm_r1[P->hbm_r1idx[bi]].out_c64 ? 24.0 : 48.0, sh->R);
+          else if (!(use_expand && P->hbm_xidx[bi] >= 0))
+            other = true;
+        }
+      }
+      trace_level = !other || tbytes >= min_bytes;
+    }
     uint32_t smax_r = 0;
     for (int h = 0; h < B->n_hbm; ++h) {
       const qtn_plan* P = plans[hidx[h]];
@@ -813,7 +836,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
           smax_r = std::max<uint32_t>(smax_r, sh->R);
           continue;
         }
-        if (use_trace && P->hbm_r1idx[bi] >= 0 && (int)sh->R >= trace_min_r) {
+        if (use_trace && P->hbm_r1idx[bi] >= 0 && (int)sh->R >= trace_min_r && trace_level) {
           qtn::R1Dev r = P->hbm_r1[P->hbm_r1idx[bi]];
           r.net = (uint32_t)h;
           r1items.push_back(r);

@@ -1072,23 +1072,35 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       }
       const SHdr* h = reinterpret_cast<const SHdr*>(P->hbm_desc.data() + P->hbm_desc_off.back());
       P->hbm_tiles.push_back(h->n_tiles);
-      if (b.ops.size() == 1) {
-        // a partial trace: output = the operand's variables minus v, same order
+      {
+        // a (weighted) partial trace: the primary plus only v-only operands;
+        // output = the primary's variables minus v, same order
+        const int pi = b.primary;
+        bool ok = true;
+        int nw = 0;
+        for (int i = 0; i < (int)spec.opvars.size() && ok; ++i)
+          if (i != pi) ok = spec.opvars[i].size() == 1 && nw++ < kR1MaxW;
         std::vector<int32_t> rest;
-        for (int32_t u : spec.opvars[0])
+        for (int32_t u : spec.opvars[pi])
           if (u != b.v) rest.push_back(u);
-        const int rk = (int)spec.opvars[0].size();
+        const int rk = (int)spec.opvars[pi].size();
         int pk = -1;
         for (int j = 0; j < rk; ++j)
-          if (spec.opvars[0][j] == b.v) pk = rk - 1 - j;
-        if (rest == spec.out_vars && pk >= 0) {
+          if (spec.opvars[pi][j] == b.v) pk = rk - 1 - j;
+        if (ok && rest == spec.out_vars && pk >= 0) {
           R1Dev r{};
-          r.src = spec.optag[0];
+          r.src = spec.optag[pi];
           r.out = spec.out_tag;
           r.R = (uint8_t)spec.out_vars.size();
           r.pk = (uint8_t)pk;
-          r.src_c64 = spec.opc64[0];
+          r.src_c64 = spec.opc64[pi];
           r.out_c64 = spec.out_c64 ? 1 : 0;
+          for (int i = 0; i < (int)spec.opvars.size(); ++i)
+            if (i != pi) {
+              r.w[r.nw] = spec.optag[i];
+              r.w_c64[r.nw] = spec.opc64[i];
+              ++r.nw;
+            }
           P->hbm_r1idx[bi] = (int32_t)P->hbm_r1.size();
           P->hbm_r1.push_back(r);
         }

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ Stre
     if (prefix[mid] <= cb) lo = mid;
     else hi = mid;
   }
-  const R1Dev r = items[lo];
+  const R1Dev& r = items[lo];
   const uint32_t set = blockIdx.y;
   Bases b;
   b.in = L.in_base + (int64_t)set * L.in_set_stride + L.net_in_off[r.net];
@@ -236,6 +236,41 @@ __global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ Stre
   const uint64_t o1 = min(n, o0 + kTraceChunk);
   const uint32_t pk = r.pk;
   const uint64_t vstep = 1ull << pk;
+  // per-v weights: product of the v-only operands (float64)
+  double2 w0 = make_double2(1.0, 0.0), w1 = w0;
+  for (uint32_t k = 0; k < r.nw; ++k) {
+    const char* wp = resolve(r.w[k], b);
+    w0 = cmul(w0, ldg_c(wp, 0, r.w_c64[k]));
+    w1 = cmul(w1, ldg_c(wp, 1, r.w_c64[k]));
+  }
+  if (r.src_c64 && r.out_c64 && r.R >= 1 && r.nw) {
+    const float2 W0 = make_float2((float)w0.x, (float)w0.y), W1 = make_float2((float)w1.x, (float)w1.y);
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* out4 = reinterpret_cast<float4*>(out);
+    // out = W0 * a + W1 * b for one complex64 pair
+    auto wsum = [&](float ax, float ay, float bx, float by, float& rx, float& ry) {
+      rx = fmaf(W0.x, ax, fmaf(-W0.y, ay, fmaf(W1.x, bx, -W1.y * by)));
+      ry = fmaf(W0.x, ay, fmaf(W0.y, ax, fmaf(W1.x, by, W1.y * bx)));
+    };
+#pragma unroll 8
+    for (uint64_t p = o0 + 2u * threadIdx.x; p < o1; p += 512) {
+      float4 x, y, z;
+      if (pk >= 1) {
+        const uint64_t i0 = (p & (vstep - 1)) | ((p >> pk) << (pk + 1));
+        x = __ldg(s4 + (i0 >> 1));
+        y = __ldg(s4 + ((i0 + vstep) >> 1));
+        wsum(x.x, x.y, y.x, y.y, z.x, z.y);
+        wsum(x.z, x.w, y.z, y.w, z.z, z.w);
+      } else {
+        x = __ldg(s4 + p);
+        y = __ldg(s4 + p + 1);
+        wsum(x.x, x.y, x.z, x.w, z.x, z.y);
+        wsum(y.x, y.y, y.z, y.w, z.z, z.w);
+      }
+      out4[p >> 1] = z;
+    }
+    return;
+  }
   if (r.src_c64 && r.out_c64 && r.R >= 1) {
     // two adjacent outputs per thread and step, 16-byte loads and stores
     const float4* s4 = reinterpret_cast<const float4*>(src);
@@ -258,7 +293,7 @@ __global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ Stre
   }
   for (uint64_t o = o0 + threadIdx.x; o < o1; o += 256) {
     const uint64_t i0 = (o & (vstep - 1)) | ((o >> pk) << (pk + 1));
-    const double2 x = ldg_c(src, i0, r.src_c64), y = ldg_c(src, i0 + vstep, r.src_c64);
+    const double2 x = cmul(w0, ldg_c(src, i0, r.src_c64)), y = cmul(w1, ldg_c(src, i0 + vstep, r.src_c64));
     const double2 z = make_double2(x.x + y.x, x.y + y.y);
     if (r.out_c64)
       reinterpret_cast<float2*>(out)[o] = make_float2((float)z.x, (float)z.y);

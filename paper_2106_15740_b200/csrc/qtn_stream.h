@@ -224,12 +224,18 @@ int launch_expand(const XLaunch& L, void* stream);
 // the output layout being the primary's minus v.  A pure stream of 3 entries
 // per output, run by trace_kernel: 4096 outputs per CTA, 16-byte loads and
 // stores, many items per launch (prefix over 4096-output chunks).
+// Operands of the bucket that hold only v (rank-1 diagonal factors) are
+// folded in as per-v weights: out[o] = w_0 P[o|0] + w_1 P[o|1].
+constexpr int kR1MaxW = 3;
 struct R1Dev {
   uint64_t src, out;             // tagged pointers
+  uint64_t w[kR1MaxW];           // tagged pointers of rank-1 (v-only) operands
   uint32_t net;                  // network index (bases)
   uint8_t R, pk, src_c64, out_c64;
+  uint8_t nw, w_c64[kR1MaxW];
+  uint8_t pad[4];
 };
-static_assert(sizeof(R1Dev) == 24, "R1Dev");
+static_assert(sizeof(R1Dev) == 56, "R1Dev");
 constexpr uint32_t kTraceChunk = 4096;
 int launch_trace(const StreamLaunch& L, const R1Dev* items, const uint64_t* prefix,
                  uint32_t n_items, uint64_t total_chunks, void* stream);
