@@ -927,12 +927,12 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     // intermediates of the chain are never written.
     // chain_head[bi]: head bucket of bi's chain (bi itself for a head), -1
     // for buckets that are not single-operand.
-    // Opt-in (QTN_FUSE_REDUCE=1): measured slower than running the chain's
-    // buckets on the tile kernel (config 3 default 42.6 k vs 56.6 k/s,
-    // config 4 466 vs 585 /s) — the tile pipeline streams each pass near
-    // HBM speed while the reduce kernel is latency bound.
+    // On by default for chains of 2-4 buckets into outputs of rank >= 18
+    // (QTN_FUSE_REDUCE=0 disables): reduce_kernel streams 16-byte loads
+    // (config 4 782 -> 831 /s, config 3 default 79.4 k -> 80.7 k/s); longer
+    // chains into small outputs leave it too few outputs for its 2^k sums.
     const char* fv = getenv("QTN_FUSE_REDUCE");
-    const bool fuse = fv && fv[0] == '1';
+    const bool fuse = !(fv && fv[0] == '0');
     std::vector<int32_t> chain_head(nb, -1), chain_tail(nb, -1), chain_len(nb, 0);
     constexpr int kRedMax = 8;  // the reduce kernel keeps 2^k source offsets in shared memory
     if (fuse) {
@@ -953,7 +953,11 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     // otherwise its buckets run on the tile kernel as usual
     if (fuse) {
       const char* mpv = getenv("QTN_FUSE_MIN_POS");
-      const int min_pos = mpv ? atoi(mpv) : 3;
+      const int min_pos = mpv ? atoi(mpv) : 0;
+      const char* mrv = getenv("QTN_FUSE_MIN_R");
+      const int fuse_min_r = mrv ? atoi(mrv) : 18;
+      const char* mkv = getenv("QTN_FUSE_MAX_K");
+      const int fuse_max_k = mkv ? atoi(mkv) : 4;
       for (int bi = 0; bi < nb; ++bi) {
         if (chain_head[bi] != bi) continue;
         const auto& src = P->tensors[P->buckets[bi].ops[0]];
@@ -964,7 +968,12 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
           lowest = std::min(lowest, (int)(src.vars.end() - it) - 1);
           if (c == chain_tail[bi]) break;
         }
-        if (lowest < min_pos) {
+        // a chain of one bucket gains nothing from fusion (trace_kernel runs
+        // it); long chains into small outputs leave reduce_kernel with too
+        // few outputs for its 2^k-entry sums (measured: config 3 default)
+        const int out_rank = P->tensors[P->buckets[chain_tail[bi]].out].rank();
+        if (lowest < min_pos || chain_len[bi] < 2 || out_rank < fuse_min_r ||
+            chain_len[bi] > fuse_max_k) {
           for (int32_t c = bi;; c = P->tensors[P->buckets[c].out].last_use) {
             chain_head[c] = -1;
             if (c == chain_tail[bi]) break;

@@ -333,7 +333,6 @@ __global__ void __launch_bounds__(256) reduce_kernel(const __grid_constant__ Str
   pdl_trigger();
   pdl_wait();
   __shared__ uint64_t offs[256];
-  __shared__ double2 part[8][32];
   const uint32_t cb = blockIdx.x;
   uint32_t lo = 0, hi = n_items;  // last item with prefix <= cb
   while (hi - lo > 1) {
@@ -341,18 +340,14 @@ __global__ void __launch_bounds__(256) reduce_kernel(const __grid_constant__ Str
     if (prefix[mid] <= cb) lo = mid;
     else hi = mid;
   }
-  const RedDev r = items[lo];
+  const RedDev& r = items[lo];
   const uint32_t k = r.k, nm = 1u << k;
-  const uint32_t G = nm < 8u ? nm : 8u;          // warps per output block
-  const uint32_t blocks = 8u / G;                // output blocks of 32 per CTA
   for (uint32_t m = threadIdx.x; m < nm; m += 256) {
     uint64_t o = 0;
     for (uint32_t q = 0; q < k; ++q) o |= (uint64_t)((m >> q) & 1u) << r.pos[q];
     offs[m] = o;
   }
   __syncthreads();
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t blk = warp / G, g = warp % G;
   const uint64_t n_out = 1ull << r.R;
   const uint32_t set = blockIdx.y;
   Bases b;
@@ -360,77 +355,65 @@ __global__ void __launch_bounds__(256) reduce_kernel(const __grid_constant__ Str
   b.ws = L.ws_base + (int64_t)set * L.ws_set_stride + L.net_ws_off[r.net];
   const char* src = resolve(r.src, b);
   char* out = const_cast<char*>(resolve(r.out, b));
-  // kRedIters sub-chunks of 32 * blocks outputs per CTA
-  for (uint32_t it = 0; it < kRedIters; ++it) {
-    const uint64_t o = (((uint64_t)(cb - prefix[lo]) * kRedIters + it) * blocks + blk) * 32u + lane;
-    const bool valid = o < n_out;
-    uint64_t idx = valid ? o : 0;
+  const uint32_t chunk = red_chunk(k);
+  const uint64_t o0 = (uint64_t)(cb - prefix[lo]) * chunk, o1 = min(n_out, o0 + chunk);
+  auto spread = [&](uint64_t o) {
     for (uint32_t q = 0; q < k; ++q) {
       const uint32_t p = r.pos[q];
-      idx = (idx & ((1ull << p) - 1)) | ((idx >> p) << (p + 1));
+      o = (o & ((1ull << p) - 1)) | ((o >> p) << (p + 1));
     }
-    double2 a[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                    make_double2(0.0, 0.0)};
-    if (valid) {
-      uint32_t m = g;
-      if (r.src_c64) {
-        const float2* s2 = reinterpret_cast<const float2*>(src);
-        for (; m + 3 * G < nm; m += 4 * G) {
-          float2 x[4];
+    return o;
+  };
+  if (r.src_c64 && r.out_c64 && r.R >= 1) {
+    // two adjacent outputs per thread and step; bit 0 kept: one 16-byte load
+    // per m covers both outputs; bit 0 summed: one 16-byte load covers the
+    // (m, m+1) pair of one output
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* out4 = reinterpret_cast<float4*>(out);
+    const bool b0 = r.pos[0] == 0;
+    const uint64_t d1 = spread(1);
+    for (uint64_t p = o0 + 2u * threadIdx.x; p < o1; p += 512) {
+      const uint64_t i0 = spread(p);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!b0) {
+        uint32_t m = 0;
+        for (; m + 4 <= nm; m += 4) {
+          float4 x[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) x[u] = __ldg(s2 + (idx | offs[m + u * G]));
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            a[u].x += x[u].x;
-            a[u].y += x[u].y;
-          }
-        }
-        for (; m < nm; m += G) {
-          const float2 x = __ldg(s2 + (idx | offs[m]));
-          a[0].x += x.x;
-          a[0].y += x.y;
-        }
-      } else {
-        const double2* s2 = reinterpret_cast<const double2*>(src);
-        for (; m + 3 * G < nm; m += 4 * G) {
-          double2 x[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) x[u] = __ldg(s2 + (idx | offs[m + u * G]));
+          for (int u = 0; u < 4; ++u) x[u] = __ldg(s4 + ((i0 | offs[m + u]) >> 1));
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            a[u].x += x[u].x;
-            a[u].y += x[u].y;
+            acc.x += x[u].x; acc.y += x[u].y; acc.z += x[u].z; acc.w += x[u].w;
           }
         }
-        for (; m < nm; m += G) {
-          const double2 x = __ldg(s2 + (idx | offs[m]));
-          a[0].x += x.x;
-          a[0].y += x.y;
-        }
-      }
-    }
-    if (G > 1) {
-      part[warp][lane] = make_double2((a[0].x + a[1].x) + (a[2].x + a[3].x),
-                                      (a[0].y + a[1].y) + (a[2].y + a[3].y));
-      __syncthreads();
-    }
-    if (g == 0 && valid) {
-      double2 t;
-      if (G > 1) {
-        t = part[warp][lane];
-        for (uint32_t q = 1; q < G; ++q) {
-          t.x += part[warp + q][lane].x;
-          t.y += part[warp + q][lane].y;
+        for (; m < nm; ++m) {
+          const float4 x = __ldg(s4 + ((i0 | offs[m]) >> 1));
+          acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
         }
       } else {
-        t = make_double2((a[0].x + a[1].x) + (a[2].x + a[3].x), (a[0].y + a[1].y) + (a[2].y + a[3].y));
+        for (uint32_t m = 0; m < nm; m += 2) {
+          const float4 x = __ldg(s4 + ((i0 | offs[m]) >> 1));
+          const float4 y = __ldg(s4 + (((i0 + d1) | offs[m]) >> 1));
+          acc.x += x.x + x.z; acc.y += x.y + x.w;
+          acc.z += y.x + y.z; acc.w += y.y + y.w;
+        }
       }
-      if (r.out_c64)
-        reinterpret_cast<float2*>(out)[o] = make_float2((float)t.x, (float)t.y);
-      else
-        reinterpret_cast<double2*>(out)[o] = t;
+      out4[p >> 1] = acc;
     }
-    if (G > 1) __syncthreads();  // part reused by the next sub-chunk
+    return;
+  }
+  for (uint64_t o = o0 + threadIdx.x; o < o1; o += 256) {
+    const uint64_t i0 = spread(o);
+    double2 acc = make_double2(0.0, 0.0);
+    for (uint32_t m = 0; m < nm; ++m) {
+      const double2 x = ldg_c(src, i0 | offs[m], r.src_c64);
+      acc.x += x.x;
+      acc.y += x.y;
+    }
+    if (r.out_c64)
+      reinterpret_cast<float2*>(out)[o] = make_float2((float)acc.x, (float)acc.y);
+    else
+      reinterpret_cast<double2*>(out)[o] = acc;
   }
 }
 

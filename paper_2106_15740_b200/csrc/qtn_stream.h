@@ -149,11 +149,14 @@ struct RedDev {
   uint8_t pos[8];               // eliminated bit positions, ascending
 };
 static_assert(sizeof(RedDev) == 32, "RedDev");
-// outputs per CTA: kRedIters sub-chunks of 32 * 8 / min(8, 2^k)
-constexpr uint32_t kRedIters = 16;
-inline uint32_t red_chunk(uint32_t k) {
-  return kRedIters * 32u * (8u / ((1u << k) < 8u ? (1u << k) : 8u));
-}
+// outputs per CTA: 512 (256 threads x 2 adjacent outputs) x max(1, 8 / 2^k)
+// steps, so a CTA reads ~4096 x 2 source entries whatever k is
+#ifdef __CUDACC__
+#define QTN_HD __host__ __device__
+#else
+#define QTN_HD
+#endif
+QTN_HD inline uint32_t red_chunk(uint32_t k) { return 512u * (k >= 3 ? 1u : (8u >> k)); }
 // items: device array; prefix: device, n_items + 1 CTA prefix (chunks of red_chunk(k))
 int launch_reduce(const StreamLaunch& L, const RedDev* items, const uint32_t* prefix,
                   uint32_t n_items, uint32_t total_chunks, void* stream);

@@ -404,29 +404,39 @@ def test_setmajor_large_batch_and_graph_replay(golden, setmajor_min_sets):
     assert not np.allclose(g1, g2)
 
 
-@pytest.mark.parametrize("min_pos", ["0", "3"])
-def test_fused_reduction_chains_opt_in(golden, monkeypatch, min_pos):
-    """QTN_FUSE_REDUCE=1: chains of single-operand buckets run as one
-    multi-variable sum (reduce_kernel) — same values as the reference."""
-    monkeypatch.setenv("QTN_FUSE_REDUCE", "1")
-    monkeypatch.setenv("QTN_FUSE_MIN_POS", min_pos)
+@pytest.mark.parametrize("min_r,max_k", [("0", "8"), ("18", "4")])
+def test_fused_reduction_chains(golden, monkeypatch, min_r, max_k):
+    """Chains of single-operand buckets as one multi-variable sum
+    (reduce_kernel, default on for chains into rank >= 18): same values as
+    the unfused buckets (QTN_FUSE_REDUCE=0) and the reference; loosened
+    filters (min_r 0, max_k 8) fuse every chain, including those summing
+    bit 0 of their source."""
+    monkeypatch.setenv("QTN_FUSE_MIN_R", min_r)
+    monkeypatch.setenv("QTN_FUSE_MAX_K", max_k)
     G = golden("config3.json")
     graph = Q.random_regular_graph(G["n"], 3, 0)
     params = Q.QaoaParams(G["gammas"], G["betas"])
-    recs = G["modes"]["default"][:6]
-    plan = Q.EnergyPlan(graph, G["p"], "default", dtype="complex128",
-                        edge_ids=[r["edge_index"] for r in recs])
-    assert any(j.plan.executor == 1 for j in plan.jobs)
-    zz = plan.zz_values(params)
-    for r in recs:
-        w = complex(*r["value"])
-        assert abs(zz[r["edge_index"]] - w) <= 1e-11 * abs(w) + 1e-12
+    recs = G["modes"]["default"][:8]
     G4 = golden("config4.json")
-    rec = [r for r in G4["modes"]["zz+diagonal"] if r["edge_index"] == 16][0]
+    rec4 = complex(*[r for r in G4["modes"]["zz+diagonal"] if r["edge_index"] == 16][0]["value"])
     g4 = Q.random_regular_graph(G4["n"], 3, 0)
-    p4 = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype="complex64", edge_ids=[16])
-    z4 = p4.zz_values(Q.QaoaParams(G4["gammas"], G4["betas"]))[16]
-    assert abs(z4 - complex(*rec["value"])) / abs(complex(*rec["value"])) < 1e-5
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_FUSE_REDUCE", flag)
+        for dt in ("complex128", "complex64"):
+            plan = Q.EnergyPlan(graph, G["p"], "default", dtype=dt,
+                                edge_ids=[r["edge_index"] for r in recs])
+            p4 = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype=dt, edge_ids=[16])
+            out[flag, dt] = (plan.zz_values(params),
+                             p4.zz_values(Q.QaoaParams(G4["gammas"], G4["betas"]))[16])
+            assert plan.launches == plan.launches_per_eval(1)
+    for dt, tol in (("complex128", 1e-11), ("complex64", 1e-5)):
+        for r in recs:
+            w = complex(*r["value"])
+            e = r["edge_index"]
+            assert abs(out["1", dt][0][e] - w) <= tol * abs(w) + 1e-12
+            assert abs(out["1", dt][0][e] - out["0", dt][0][e]) <= tol * abs(w) + 1e-12
+        assert abs(out["1", dt][1] - rec4) <= tol * abs(rec4)
 
 
 def test_setmajor_limit_falls_back_to_warp_executor():
