@@ -853,6 +853,10 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
           xstage = std::max<uint32_t>(xstage, (2u << (xd.h + xd.c)) * (xd.out_c64 ? 8u : 16u));
           continue;
         }
+        if (getenv("QTN_DEBUG_ROUTE"))
+          fprintf(stderr, "stream-item lev=%d R=%d prank=%d pc64=%d ng=%d nt=%d ntop=%d ta=%d tn=%d nops=%zu\n",
+                  lev, (int)sh->R, (int)sh->p_rank, (int)sh->p_c64, (int)sh->ng, (int)sh->nt,
+                  (int)sh->ntop, (int)sh->ta, (int)sh->tn, P->buckets[bi].ops.size());
         item_desc.push_back(desc_base[h] + P->hbm_desc_off[bi]);
         item_net.push_back((uint32_t)h);
         acc += P->hbm_tiles[bi];
