@@ -9,7 +9,8 @@ a batch of A angle sets (set 0 is the config's seeded angles, the rest are
 seeded U[0, pi) draws — the parameter batch a QAOA optimiser evaluates),
 i.e. 150*A edge contractions: on-device tensor generation, the batched
 shared-memory executor, and the energy reduction.  With --gpus N the edges
-are LPT-sharded over N ranks (strong scaling) and the per-set partial
+are LPT-sharded over N ranks and the batch holds 1024*N angle sets (weak
+scaling: fixed work per GPU; --scaling strong keeps 1024) and the per-set partial
 energies are all-reduced over NCCL once per step.
 
 Other workloads for development (`--workload`): config3 / config3-default
@@ -414,7 +415,11 @@ def run_gpu(args):
         jobs = [jobs[k] for k in keep]
     plan = Q.EnergyPlan(graph, wl["p"], wl["mode"], dtype=dtype, jobs=jobs)
     plan_s = time.perf_counter() - t0
-    A = args.angle_sets
+    # weak scaling (default): the angle-set batch grows with the job
+    # (--angle-sets per GPU), every rank evaluates its LPT edge shard for the
+    # whole batch, so per-GPU work is fixed; strong: the batch stays at
+    # --angle-sets and the edges are split
+    A = args.angle_sets * (world if args.scaling == "weak" else 1)
     sets = angle_sets(wl["p"], A)
     # the QAOA loop re-draws angles every step: a ring of
     # R angle batches, set 0 of batch 0 = the config's seeded angles
@@ -556,7 +561,7 @@ def run_gpu(args):
             "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True,
-            "scaling": "strong",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": dtype_label(plan, A),
             "data": "synthetic (seeded random 3-regular graph, seeded angles)",
@@ -566,7 +571,10 @@ def run_gpu(args):
                        "width_max": max(j.report.width for j in plan.jobs),
                        "contractions_per_step": len(edge_ids) * A,
                        "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"edges LPT-sharded over {world} GPU(s)",
+                       "parallelism": f"edges LPT-sharded over {world} GPU(s), "
+                                      f"{args.angle_sets} angle sets per GPU per step"
+                                      if args.scaling == "weak" else
+                                      f"edges LPT-sharded over {world} GPU(s)",
                        "energy_set0": energy0, "plan_seconds": plan_s,
                        "angles": f"re-drawn every step (ring of {R} batches of {A} sets)"},
             "roofline": roof,
@@ -592,7 +600,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS) + ["config5"])
-    ap.add_argument("--angle-sets", type=int, default=1024)
+    ap.add_argument("--angle-sets", type=int, default=1024,
+                    help="angle sets per step per GPU (weak) or in all (strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="multi-GPU: weak = batch of angle sets x N, edges sharded; "
+                         "strong = fixed batch, edges sharded")
     ap.add_argument("--dtype", default=None)
     ap.add_argument("--slices", type=int, default=0,
                     help="split every edge network into 2^k slices (config 4)")
