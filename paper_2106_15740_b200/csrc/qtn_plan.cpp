@@ -1086,9 +1086,12 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         // output = the primary's variables minus v, same order
         const int pi = b.primary;
         bool ok = true;
-        int nw = 0;
+        int nw = 0, ns = 0;
         for (int i = 0; i < (int)spec.opvars.size() && ok; ++i)
-          if (i != pi) ok = spec.opvars[i].size() == 1 && nw++ < kR1MaxW;
+          if (i != pi) {
+            if (spec.opvars[i].size() == 1) ok = nw++ < kR1MaxW;
+            else ok = ns++ < kR1MaxS && spec.out_c64 && spec.opc64[pi];
+          }
         std::vector<int32_t> rest;
         for (int32_t u : spec.opvars[pi])
           if (u != b.v) rest.push_back(u);
@@ -1104,14 +1107,62 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
           r.pk = (uint8_t)pk;
           r.src_c64 = spec.opc64[pi];
           r.out_c64 = spec.out_c64 ? 1 : 0;
-          for (int i = 0; i < (int)spec.opvars.size(); ++i)
-            if (i != pi) {
+          const int R = (int)spec.out_vars.size();
+          for (int i = 0; i < (int)spec.opvars.size() && ok; ++i) {
+            if (i == pi) continue;
+            const auto& vs = spec.opvars[i];
+            if (vs.size() == 1) {
               r.w[r.nw] = spec.optag[i];
               r.w_c64[r.nw] = spec.opc64[i];
               ++r.nw;
+              continue;
             }
-          P->hbm_r1idx[bi] = (int32_t)P->hbm_r1.size();
-          P->hbm_r1.push_back(r);
+            // staged operand: output bits < 12 it depends on, compacted
+            R1Stage& g = r.st[r.ns++];
+            g.ptr = spec.optag[i];
+            g.c64 = spec.opc64[i];
+            const int rk = (int)vs.size();
+            std::vector<std::pair<int, int>> hi, lo;  // (output bit, operand bit)
+            for (int j = 0; j < rk; ++j) {
+              if (vs[j] == b.v) {
+                g.vshift = (uint8_t)(rk - 1 - j);
+                continue;
+              }
+              int ob = -1;
+              for (int q = 0; q < R; ++q)
+                if (spec.out_vars[q] == vs[j]) ob = R - 1 - q;
+              if (ob < 0) ok = false;
+              (ob < 12 ? lo : hi).push_back({ob, rk - 1 - j});
+            }
+            std::sort(lo.begin(), lo.end());
+            if ((int)lo.size() > kR1StageBits) {
+              ok = false;
+              break;
+            }
+            g.kl = (uint8_t)lo.size();
+            std::vector<std::pair<int, int>> lr, er;
+            for (size_t q = 0; q < lo.size(); ++q) {
+              lr.push_back({(int)q, lo[q].second});
+              er.push_back({lo[q].first, (int)q});
+            }
+            std::vector<uint32_t> runs;
+            make_runs(hi, runs);
+            if (runs.size() > 24) ok = false;
+            else {
+              std::copy(runs.begin(), runs.end(), g.hrun);
+              g.n_hrun = (uint8_t)runs.size();
+            }
+            make_runs(lr, runs);
+            std::copy(runs.begin(), runs.end(), g.lrun);
+            g.n_lrun = (uint8_t)runs.size();
+            make_runs(er, runs);
+            std::copy(runs.begin(), runs.end(), g.erun);
+            g.n_erun = (uint8_t)runs.size();
+          }
+          if (ok) {
+            P->hbm_r1idx[bi] = (int32_t)P->hbm_r1.size();
+            P->hbm_r1.push_back(r);
+          }
         }
       }
       XDesc xd;

@@ -243,6 +243,67 @@ __global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ Stre
     w0 = cmul(w0, ldg_c(wp, 0, r.w_c64[k]));
     w1 = cmul(w1, ldg_c(wp, 1, r.w_c64[k]));
   }
+  if (r.ns) {
+    // complex64 primary/output with 1-2 staged operands (plan-checked)
+    __shared__ float4 stg[kR1MaxS][1 << kR1StageBits];  // [op][l] = (v0, v1)
+    __shared__ uint32_t lj[kR1MaxS][8];                 // l bits of e = 512 j
+    const uint32_t ns = r.ns;
+    for (uint32_t g = 0; g < ns; ++g) {
+      const R1Stage& S = r.st[g];
+      const char* gp = resolve(S.ptr, b);
+      const uint64_t base = gather(o0, S.hrun, S.n_hrun);
+      const uint32_t ne = 1u << S.kl;
+      for (uint32_t l = threadIdx.x; l < ne; l += 256) {
+        const uint64_t idx = base | gather(l, S.lrun, S.n_lrun);
+        const double2 a = ldg_c(gp, idx, S.c64), c = ldg_c(gp, idx | (1ull << S.vshift), S.c64);
+        stg[g][l] = make_float4((float)a.x, (float)a.y, (float)c.x, (float)c.y);
+      }
+      if (threadIdx.x < 8) lj[g][threadIdx.x] = (uint32_t)gather(512ull * threadIdx.x, S.erun, S.n_erun);
+    }
+    __syncthreads();
+    uint32_t lt[kR1MaxS], lb[kR1MaxS];
+#pragma unroll
+    for (uint32_t g = 0; g < kR1MaxS; ++g) {
+      lt[g] = g < ns ? (uint32_t)gather(2u * threadIdx.x, r.st[g].erun, r.st[g].n_erun) : 0u;
+      lb[g] = g < ns ? (uint32_t)gather(1u, r.st[g].erun, r.st[g].n_erun) : 0u;
+    }
+    const float2 W0 = make_float2((float)w0.x, (float)w0.y), W1 = make_float2((float)w1.x, (float)w1.y);
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* out4 = reinterpret_cast<float4*>(out);
+    auto cm = [](float2 a, float2 c) {
+      return make_float2(fmaf(a.x, c.x, -a.y * c.y), fmaf(a.x, c.y, a.y * c.x));
+    };
+#pragma unroll 2
+    for (uint32_t j = 0; j < 8; ++j) {
+      const uint64_t p = o0 + 2u * threadIdx.x + 512u * j;
+      if (p >= o1) break;
+      float2 a00, a01, a10, a11;  // [output p / p+1][v]
+      if (pk >= 1) {
+        const uint64_t i0 = (p & (vstep - 1)) | ((p >> pk) << (pk + 1));
+        const float4 x = __ldg(s4 + (i0 >> 1)), y = __ldg(s4 + ((i0 + vstep) >> 1));
+        a00 = make_float2(x.x, x.y); a10 = make_float2(x.z, x.w);
+        a01 = make_float2(y.x, y.y); a11 = make_float2(y.z, y.w);
+      } else {
+        const float4 x = __ldg(s4 + p), y = __ldg(s4 + p + 1);
+        a00 = make_float2(x.x, x.y); a01 = make_float2(x.z, x.w);
+        a10 = make_float2(y.x, y.y); a11 = make_float2(y.z, y.w);
+      }
+#pragma unroll
+      for (uint32_t g = 0; g < kR1MaxS; ++g) {
+        if (g < ns) {
+          const uint32_t l0 = lt[g] | lj[g][j], l1 = l0 | lb[g];
+          const float4 q0 = stg[g][l0], q1 = stg[g][l1];
+          a00 = cm(a00, make_float2(q0.x, q0.y));
+          a01 = cm(a01, make_float2(q0.z, q0.w));
+          a10 = cm(a10, make_float2(q1.x, q1.y));
+          a11 = cm(a11, make_float2(q1.z, q1.w));
+        }
+      }
+      const float2 r0 = cm(W0, a00), r0b = cm(W1, a01), r1 = cm(W0, a10), r1b = cm(W1, a11);
+      out4[p >> 1] = make_float4(r0.x + r0b.x, r0.y + r0b.y, r1.x + r1b.x, r1.y + r1b.y);
+    }
+    return;
+  }
   if (r.src_c64 && r.out_c64 && r.R >= 1 && r.nw) {
     const float2 W0 = make_float2((float)w0.x, (float)w0.y), W1 = make_float2((float)w1.x, (float)w1.y);
     const float4* s4 = reinterpret_cast<const float4*>(src);

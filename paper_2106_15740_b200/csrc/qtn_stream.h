@@ -229,16 +229,31 @@ int launch_expand(const XLaunch& L, void* stream);
 // stores, many items per launch (prefix over 4096-output chunks).
 // Operands of the bucket that hold only v (rank-1 diagonal factors) are
 // folded in as per-v weights: out[o] = w_0 P[o|0] + w_1 P[o|1].
+// Complex64 buckets may also carry up to kR1MaxS "staged" operands: any
+// operand depending on <= 7 of the output's 12 low bits (the 4096 outputs of
+// a CTA touch 2^(kl+1) of its entries): they are gathered into shared memory
+// per CTA and read from there per output (config 4's [2,16,26]->25).
 constexpr int kR1MaxW = 3;
+constexpr int kR1MaxS = 2;
+constexpr int kR1StageBits = 7;
+struct R1Stage {
+  uint64_t ptr;                  // tagged
+  uint8_t vshift, c64, kl, n_hrun, n_lrun, n_erun, pad[2];
+  uint32_t hrun[24];             // output bits >= 12 -> operand bits (per-CTA base)
+  uint32_t lrun[kR1StageBits];   // compact local index bits -> operand bits
+  uint32_t erun[kR1StageBits];   // output bits < 12 -> compact local index bits
+  uint32_t pad2[2];
+};
+static_assert(sizeof(R1Stage) % 8 == 0, "R1Stage");
 struct R1Dev {
   uint64_t src, out;             // tagged pointers
   uint64_t w[kR1MaxW];           // tagged pointers of rank-1 (v-only) operands
   uint32_t net;                  // network index (bases)
   uint8_t R, pk, src_c64, out_c64;
   uint8_t nw, w_c64[kR1MaxW];
-  uint8_t pad[4];
+  uint8_t ns, pad[3];
+  R1Stage st[kR1MaxS];
 };
-static_assert(sizeof(R1Dev) == 56, "R1Dev");
 constexpr uint32_t kTraceChunk = 4096;
 int launch_trace(const StreamLaunch& L, const R1Dev* items, const uint64_t* prefix,
                  uint32_t n_items, uint64_t total_chunks, void* stream);
