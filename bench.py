@@ -522,7 +522,9 @@ def run_gpu(args):
     kt = sum(kern_times) / len(kern_times)
     alg = plan.alg_bytes_eval(A)
     if plan.hbm_jobs:
-        kname = "stream_kernel"
+        # level launches of the HBM executor: stream / expand / trace /
+        # reduce / small kernels (profiles: summed over one evaluation)
+        kname = "hbm_executor"
     elif plan._batch.uses_setmajor(A):
         kname = "sm_level_kernel_c64" if plan._batch.setmajor_elem_bytes(A) == 8 else "sm_level_kernel"
     else:

@@ -25,3 +25,4 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 # the largest expanding bucket of config 4 ([1,22,21]->26, 8th expand launch)
 ncu --set full --clock-control none --import-source on -k regex:expand_kernel -s 7 -c 1 -o gpurun_out/r/prof_expand_c4 python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-baseline --no-config5 > gpurun_out/r/ncu5.log 2>&1; echo "ncu5 rc=$?"
 python tools/micro/write_bw.py > gpurun_out/r/write_bw.txt 2>&1; echo "wbw rc=$?"
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 320 --csv --log-file gpurun_out/r/launches_config3d.csv python bench.py --steps 1 --warmup 3 --workload config3-default --angle-sets 1 --no-cpu-baseline --no-config5 > gpurun_out/r/ncu6.log 2>&1; echo "ncu6 rc=$?"

@@ -95,6 +95,26 @@ def main():
                                          "time_sum_s": s4["time_s"],
                                          "dram_bytes_per_launch": s4["dram_bytes"],
                                          "source": f"launches_{TAG}_config4.json"}}}
+    out["kernels"]["hbm_executor@config4"] = {
+        "kernel": "hbm_executor", "workload": "config4 edge #1058, one contraction: every "
+                                              "launch of the evaluation",
+        "launches_summed": sum(v["launches"] for v in agg.values()),
+        "time_sum_s": sum(v["time_s"] for v in agg.values()),
+        "dram_bytes_per_launch": sum(v["dram_bytes"] for v in agg.values()),
+        "by_kernel": agg, "source": f"launches_{TAG}_config4.json"}
+    c3d = os.path.join(R, "launches_config3d.csv")
+    if os.path.exists(c3d):
+        agg3, launches3 = launch_eval(c3d)
+        json.dump({"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+                             "dram__bytes_write.sum (serialised), one config-3-default evaluation",
+                   "kernels": agg3, "launches": launches3},
+                  open(os.path.join(P, f"launches_{TAG}_config3d.json"), "w"), indent=1)
+        out["kernels"]["hbm_executor@config3-default"] = {
+            "kernel": "hbm_executor", "workload": "config3 default, 366 edges, one evaluation",
+            "launches_summed": sum(v["launches"] for v in agg3.values()),
+            "time_sum_s": sum(v["time_s"] for v in agg3.values()),
+            "dram_bytes_per_launch": sum(v["dram_bytes"] for v in agg3.values()),
+            "by_kernel": agg3, "source": f"launches_{TAG}_config3d.json"}
     if x4:
         out["kernels"]["expand_kernel@config4-all"] = {
             "kernel": "expand_kernel", "workload": "config4 edge #1058, one contraction: its "
