@@ -89,6 +89,16 @@ __device__ __forceinline__ void expand_tile(const XDesc& d, XItemSmem& X, const 
   __syncthreads();
   // 1. B-side stage: entry ((x_b << c) | x_c) * 2 + v
   const uint32_t n_st = 2u << (h + c);
+  if (F32 && d.nB == 1 && X.c64[nA]) {
+    // one complex64 B operand (all of configs 3-4): the stage is a
+    // gather-copy; 4 independent loads per thread in flight
+    const float2* src = reinterpret_cast<const float2*>(X.ptr[nA]) + X.base[nA];
+    const uint32_t vs = X.vs[nA], cm = (1u << c) - 1u;
+    float2* dst = reinterpret_cast<float2*>(smem);
+#pragma unroll 4
+    for (uint32_t i = tid; i < n_st; i += 256)
+      dst[i] = __ldg(src + X.tb[0][i >> (c + 1)] + X.tc[0][(i >> 1) & cm] + ((i & 1u) << vs));
+  } else
   for (uint32_t i = tid; i < n_st; i += 256) {
     const uint32_t v = i & 1u, xc = (i >> 1) & ((1u << c) - 1u), xb = i >> (c + 1);
     double2 pr = make_double2(1.0, 0.0);
