@@ -816,9 +816,10 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
           if (P->hbm_level[bi] != lev || !P->hbm_tiles[bi]) continue;
           const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
           if (split_small && (all_small || (int)sh->R <= small_r)) continue;
-          if (P->hbm_r1idx[bi] >= 0 && (int)sh->R >= trace_min_r)
+          if (use_expand && P->hbm_xidx[bi] >= 0) continue;  // expand_kernel
+          if (use_trace && P->hbm_r1idx[bi] >= 0 && (int)sh->R >= trace_min_r)
             tbytes += std::ldexp(P->hbm_r1[P->hbm_r1idx[bi]].out_c64 ? 24.0 : 48.0, sh->R);
-          else if (!(use_expand && P->hbm_xidx[bi] >= 0))
+          else
             other = true;
         }
       }
@@ -836,14 +837,6 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
           smax_r = std::max<uint32_t>(smax_r, sh->R);
           continue;
         }
-        if (use_trace && P->hbm_r1idx[bi] >= 0 && (int)sh->R >= trace_min_r && trace_level) {
-          qtn::R1Dev r = P->hbm_r1[P->hbm_r1idx[bi]];
-          r.net = (uint32_t)h;
-          r1items.push_back(r);
-          r1acc += ((1ull << r.R) + qtn::kTraceChunk - 1) / qtn::kTraceChunk;
-          r1prefix.push_back(r1acc);
-          continue;
-        }
         if (use_expand && P->hbm_xidx[bi] >= 0) {
           const qtn::XDesc& xd = P->hbm_xdesc[P->hbm_xidx[bi]];
           xitem_desc.push_back(xdesc_base[h] + (uint32_t)P->hbm_xidx[bi]);
@@ -851,6 +844,14 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
           xacc += xd.n_tiles;
           xprefix.push_back(xacc);
           xstage = std::max<uint32_t>(xstage, (2u << (xd.h + xd.c)) * (xd.out_c64 ? 8u : 16u));
+          continue;
+        }
+        if (use_trace && P->hbm_r1idx[bi] >= 0 && (int)sh->R >= trace_min_r && trace_level) {
+          qtn::R1Dev r = P->hbm_r1[P->hbm_r1idx[bi]];
+          r.net = (uint32_t)h;
+          r1items.push_back(r);
+          r1acc += ((1ull << r.R) + qtn::kTraceChunk - 1) / qtn::kTraceChunk;
+          r1prefix.push_back(r1acc);
           continue;
         }
         if (getenv("QTN_DEBUG_ROUTE"))

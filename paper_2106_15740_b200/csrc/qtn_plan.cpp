@@ -1090,7 +1090,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         for (int i = 0; i < (int)spec.opvars.size() && ok; ++i)
           if (i != pi) {
             if (spec.opvars[i].size() == 1) ok = nw++ < kR1MaxW;
-            else ok = ns++ < kR1MaxS && spec.out_c64 && spec.opc64[pi];
+            else ok = ns++ < kR1MaxS;
           }
         std::vector<int32_t> rest;
         for (int32_t u : spec.opvars[pi])
@@ -1099,7 +1099,16 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         int pk = -1;
         for (int j = 0; j < rk; ++j)
           if (spec.opvars[pi][j] == b.v) pk = rk - 1 - j;
-        if (ok && rest == spec.out_vars && pk >= 0) {
+        // the output must be the primary's variables minus v on its low
+        // bits, in order; variables of staged operands may sit above
+        const size_t nr = rest.size();
+        const bool low_ok = spec.out_vars.size() >= nr &&
+                            std::equal(rest.begin(), rest.end(), spec.out_vars.end() - nr);
+        const bool expanding = spec.out_vars.size() > nr;
+        // expanding or complex128: only through the staged path, which needs
+        // a staged operand and a primary bit under the output pair
+        if (ok && (expanding || !spec.out_c64 || !spec.opc64[pi]) && (ns == 0 || nr < 1)) ok = false;
+        if (ok && low_ok && pk >= 0) {
           R1Dev r{};
           r.src = spec.optag[pi];
           r.out = spec.out_tag;
@@ -1107,6 +1116,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
           r.pk = (uint8_t)pk;
           r.src_c64 = spec.opc64[pi];
           r.out_c64 = spec.out_c64 ? 1 : 0;
+          r.pr = (uint8_t)nr;
           const int R = (int)spec.out_vars.size();
           for (int i = 0; i < (int)spec.opvars.size() && ok; ++i) {
             if (i == pi) continue;

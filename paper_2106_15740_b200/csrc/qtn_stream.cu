@@ -22,6 +22,8 @@
 // flattened, each block takes a contiguous range of tiles.
 #define QTN_STREAM_NS s256
 #include "qtn_stream_tile.cuh"
+
+#include <type_traits>
 #include "qtn_pdl.cuh"
 
 namespace qtn {
@@ -211,6 +213,90 @@ int launch_chain(const StreamLaunch& L, const uint32_t* level_item0_dev, uint32_
 }
 
 // ---- single-operand buckets (partial traces), see qtn_stream.h
+// Staged-operand path of trace_kernel: 1-2 operands depending on <= 7 of
+// the output's 12 low bits are gathered into shared memory per CTA as
+// (v0, v1) pairs; the primary is read at the output's low pr bits (so the
+// output may be wider: its new bits come from the staged operands).  PC64 /
+// OC64: primary / output element types; float32 math for complex64 outputs,
+// float64 for complex128 outputs.
+constexpr uint32_t kTraceSmem = kR1MaxS * (2u << kR1StageBits) * 16u + kR1MaxS * 8u * 4u;
+template <bool PC64, bool OC64>
+__device__ __forceinline__ void trace_staged(const R1Dev& r, const Bases& b, const char* src,
+                                             char* out, uint64_t o0, uint64_t o1, double2 w0,
+                                             double2 w1, unsigned char* sm) {
+  using C = typename std::conditional<OC64, float2, double2>::type;
+  // [op][2l + v] staged entries, then the l bits of e = 512 j
+  C (*stg)[2 << kR1StageBits] = reinterpret_cast<C (*)[2 << kR1StageBits]>(sm);
+  uint32_t (*lj)[8] = reinterpret_cast<uint32_t (*)[8]>(sm + kR1MaxS * (2u << kR1StageBits) * 16u);
+  const uint32_t ns = r.ns, pk = r.pk;
+  const uint64_t vstep = 1ull << pk, pmask = (1ull << r.pr) - 1;
+  for (uint32_t g = 0; g < ns; ++g) {
+    const R1Stage& S = r.st[g];
+    const char* gp = resolve(S.ptr, b);
+    const uint64_t base = gather(o0, S.hrun, S.n_hrun);
+    const uint32_t ne = 2u << S.kl;
+    for (uint32_t i = threadIdx.x; i < ne; i += 256) {
+      const uint64_t idx = base | gather(i >> 1, S.lrun, S.n_lrun) | ((uint64_t)(i & 1u) << S.vshift);
+      const double2 a = ldg_c(gp, idx, S.c64);
+      stg[g][i] = C{(decltype(C::x))a.x, (decltype(C::x))a.y};
+    }
+    if (threadIdx.x < 8) lj[g][threadIdx.x] = (uint32_t)gather(512ull * threadIdx.x, S.erun, S.n_erun);
+  }
+  __syncthreads();
+  uint32_t lt[kR1MaxS], lb[kR1MaxS];
+#pragma unroll
+  for (uint32_t g = 0; g < kR1MaxS; ++g) {
+    lt[g] = g < ns ? (uint32_t)gather(2u * threadIdx.x, r.st[g].erun, r.st[g].n_erun) : 0u;
+    lb[g] = g < ns ? (uint32_t)gather(1u, r.st[g].erun, r.st[g].n_erun) : 0u;
+  }
+  auto cm = [](C a, C c) {
+    if constexpr (OC64) return C{fmaf(a.x, c.x, -a.y * c.y), fmaf(a.x, c.y, a.y * c.x)};
+    else return C{fma(a.x, c.x, -a.y * c.y), fma(a.x, c.y, a.y * c.x)};
+  };
+  const C W0{(decltype(C::x))w0.x, (decltype(C::x))w0.y}, W1{(decltype(C::x))w1.x, (decltype(C::x))w1.y};
+  auto ld = [&](uint64_t i) -> C {  // primary entry i
+    if (PC64) {
+      const float2 f = __ldg(reinterpret_cast<const float2*>(src) + i);
+      return C{f.x, f.y};
+    }
+    const double2 d = __ldg(reinterpret_cast<const double2*>(src) + i);
+    return C{(decltype(C::x))d.x, (decltype(C::x))d.y};
+  };
+#pragma unroll 2
+  for (uint32_t j = 0; j < 8; ++j) {
+    const uint64_t p = o0 + 2u * threadIdx.x + 512u * j;
+    if (p >= o1) break;
+    const uint64_t po = p & pmask;  // even: bit 0 is a primary bit (pr >= 1)
+    C a00, a01, a10, a11;  // [output p / p+1][v]
+    if (pk >= 1) {
+      const uint64_t i0 = (po & (vstep - 1)) | ((po >> pk) << (pk + 1));
+      if (PC64) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(src) + (i0 >> 1));
+        const float4 y = __ldg(reinterpret_cast<const float4*>(src) + ((i0 + vstep) >> 1));
+        a00 = C{x.x, x.y}; a10 = C{x.z, x.w}; a01 = C{y.x, y.y}; a11 = C{y.z, y.w};
+      } else {
+        a00 = ld(i0); a10 = ld(i0 + 1); a01 = ld(i0 + vstep); a11 = ld(i0 + vstep + 1);
+      }
+    } else {
+      a00 = ld(2 * po); a01 = ld(2 * po + 1); a10 = ld(2 * po + 2); a11 = ld(2 * po + 3);
+    }
+#pragma unroll
+    for (uint32_t g = 0; g < kR1MaxS; ++g) {
+      if (g < ns) {
+        const uint32_t l0 = lt[g] | lj[g][j], l1 = l0 | lb[g];
+        a00 = cm(a00, stg[g][2 * l0]);
+        a01 = cm(a01, stg[g][2 * l0 + 1]);
+        a10 = cm(a10, stg[g][2 * l1]);
+        a11 = cm(a11, stg[g][2 * l1 + 1]);
+      }
+    }
+    const C r0 = cm(W0, a00), r0b = cm(W1, a01), r1 = cm(W0, a10), r1b = cm(W1, a11);
+    C* oc = reinterpret_cast<C*>(out) + p;
+    oc[0] = C{r0.x + r0b.x, r0.y + r0b.y};
+    oc[1] = C{r1.x + r1b.x, r1.y + r1b.y};
+  }
+}
+
 __global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ StreamLaunch L,
                                                     const R1Dev* __restrict__ items,
                                                     const uint64_t* __restrict__ prefix,
@@ -244,64 +330,15 @@ __global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ Stre
     w1 = cmul(w1, ldg_c(wp, 1, r.w_c64[k]));
   }
   if (r.ns) {
-    // complex64 primary/output with 1-2 staged operands (plan-checked)
-    __shared__ float4 stg[kR1MaxS][1 << kR1StageBits];  // [op][l] = (v0, v1)
-    __shared__ uint32_t lj[kR1MaxS][8];                 // l bits of e = 512 j
-    const uint32_t ns = r.ns;
-    for (uint32_t g = 0; g < ns; ++g) {
-      const R1Stage& S = r.st[g];
-      const char* gp = resolve(S.ptr, b);
-      const uint64_t base = gather(o0, S.hrun, S.n_hrun);
-      const uint32_t ne = 1u << S.kl;
-      for (uint32_t l = threadIdx.x; l < ne; l += 256) {
-        const uint64_t idx = base | gather(l, S.lrun, S.n_lrun);
-        const double2 a = ldg_c(gp, idx, S.c64), c = ldg_c(gp, idx | (1ull << S.vshift), S.c64);
-        stg[g][l] = make_float4((float)a.x, (float)a.y, (float)c.x, (float)c.y);
-      }
-      if (threadIdx.x < 8) lj[g][threadIdx.x] = (uint32_t)gather(512ull * threadIdx.x, S.erun, S.n_erun);
-    }
-    __syncthreads();
-    uint32_t lt[kR1MaxS], lb[kR1MaxS];
-#pragma unroll
-    for (uint32_t g = 0; g < kR1MaxS; ++g) {
-      lt[g] = g < ns ? (uint32_t)gather(2u * threadIdx.x, r.st[g].erun, r.st[g].n_erun) : 0u;
-      lb[g] = g < ns ? (uint32_t)gather(1u, r.st[g].erun, r.st[g].n_erun) : 0u;
-    }
-    const float2 W0 = make_float2((float)w0.x, (float)w0.y), W1 = make_float2((float)w1.x, (float)w1.y);
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    float4* out4 = reinterpret_cast<float4*>(out);
-    auto cm = [](float2 a, float2 c) {
-      return make_float2(fmaf(a.x, c.x, -a.y * c.y), fmaf(a.x, c.y, a.y * c.x));
-    };
-#pragma unroll 2
-    for (uint32_t j = 0; j < 8; ++j) {
-      const uint64_t p = o0 + 2u * threadIdx.x + 512u * j;
-      if (p >= o1) break;
-      float2 a00, a01, a10, a11;  // [output p / p+1][v]
-      if (pk >= 1) {
-        const uint64_t i0 = (p & (vstep - 1)) | ((p >> pk) << (pk + 1));
-        const float4 x = __ldg(s4 + (i0 >> 1)), y = __ldg(s4 + ((i0 + vstep) >> 1));
-        a00 = make_float2(x.x, x.y); a10 = make_float2(x.z, x.w);
-        a01 = make_float2(y.x, y.y); a11 = make_float2(y.z, y.w);
-      } else {
-        const float4 x = __ldg(s4 + p), y = __ldg(s4 + p + 1);
-        a00 = make_float2(x.x, x.y); a01 = make_float2(x.z, x.w);
-        a10 = make_float2(y.x, y.y); a11 = make_float2(y.z, y.w);
-      }
-#pragma unroll
-      for (uint32_t g = 0; g < kR1MaxS; ++g) {
-        if (g < ns) {
-          const uint32_t l0 = lt[g] | lj[g][j], l1 = l0 | lb[g];
-          const float4 q0 = stg[g][l0], q1 = stg[g][l1];
-          a00 = cm(a00, make_float2(q0.x, q0.y));
-          a01 = cm(a01, make_float2(q0.z, q0.w));
-          a10 = cm(a10, make_float2(q1.x, q1.y));
-          a11 = cm(a11, make_float2(q1.z, q1.w));
-        }
-      }
-      const float2 r0 = cm(W0, a00), r0b = cm(W1, a01), r1 = cm(W0, a10), r1b = cm(W1, a11);
-      out4[p >> 1] = make_float4(r0.x + r0b.x, r0.y + r0b.y, r1.x + r1b.x, r1.y + r1b.y);
-    }
+    __shared__ __align__(16) unsigned char tsm[kTraceSmem];
+    if (r.src_c64 && r.out_c64)
+      trace_staged<true, true>(r, b, src, out, o0, o1, w0, w1, tsm);
+    else if (r.out_c64)
+      trace_staged<false, true>(r, b, src, out, o0, o1, w0, w1, tsm);
+    else if (r.src_c64)
+      trace_staged<true, false>(r, b, src, out, o0, o1, w0, w1, tsm);
+    else
+      trace_staged<false, false>(r, b, src, out, o0, o1, w0, w1, tsm);
     return;
   }
   if (r.src_c64 && r.out_c64 && r.R >= 1 && r.nw) {

@@ -251,7 +251,9 @@ struct R1Dev {
   uint32_t net;                  // network index (bases)
   uint8_t R, pk, src_c64, out_c64;
   uint8_t nw, w_c64[kR1MaxW];
-  uint8_t ns, pad[3];
+  uint8_t ns;
+  uint8_t pr;                    // the primary's non-v bits = the output's low bits (new bits above)
+  uint8_t pad[2];
   R1Stage st[kR1MaxS];
 };
 constexpr uint32_t kTraceChunk = 4096;
