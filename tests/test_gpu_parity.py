@@ -645,3 +645,28 @@ def test_trace_kernel_matches_stream_kernel(golden, monkeypatch, dtype, tol):
         assert abs(out["1"][0][e] - out["0"][0][e]) <= tol * abs(w) + 1e-13
     assert abs(out["1"][1] - w4) <= ref_tol * abs(w4)
     assert abs(out["1"][1] - out["0"][1]) <= tol * abs(w4)
+
+
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-12), ("complex64", 1e-6)])
+def test_trace_kernel_every_eligible_bucket(golden, monkeypatch, dtype, tol):
+    """QTN_TRACE_MIN_MB=0 sends every eligible bucket to trace_kernel,
+    including complex128 primaries/outputs and outputs wider than the
+    primary (new bits from staged operands): same values as the streaming
+    kernel and the reference (config 3 default networks)."""
+    monkeypatch.setenv("QTN_TRACE_MIN_MB", "0")
+    G3 = golden("config3.json")
+    g3 = Q.random_regular_graph(G3["n"], 3, 0)
+    p3 = Q.QaoaParams(G3["gammas"], G3["betas"])
+    recs = G3["modes"]["default"][10:18]
+    ids3 = [r["edge_index"] for r in recs]
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_TRACE", flag)
+        a = Q.EnergyPlan(g3, G3["p"], "default", dtype=dtype, edge_ids=ids3)
+        out[flag] = a.zz_values(p3)
+    ref_tol = 1e-11 if dtype == "complex128" else 1e-5
+    for r in recs:
+        w = complex(*r["value"])
+        e = r["edge_index"]
+        assert abs(out["1"][e] - w) <= ref_tol * abs(w) + 1e-13
+        assert abs(out["1"][e] - out["0"][e]) <= tol * abs(w) + 1e-13
