@@ -487,6 +487,7 @@ def run_gpu(args):
     # end to end through the public API: host angles -> energies on host
     e2e_times = []
     for it in range(args.warmup + args.steps):
+        flush.zero_()  # L2 flushed between e2e steps too (not timed)
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
