@@ -13,7 +13,7 @@ are LPT-sharded over N ranks and the batch holds 1024*N angle sets (weak
 scaling: fixed work per GPU; --scaling strong keeps 1024) and the per-set partial
 energies are all-reduced over NCCL once per step.
 
-Other workloads for development (`--workload`): config3 / config3-default
+Other workloads (`--workload`): config1 (N=20, p=1, complex128), config3 / config3-default
 (N=244, p=3), config4 (N=1000, p=5, edge #1058), config5 (synthetic bucket
 sweep).  `--impl reference` times the CPU oracle (the restated reference
 bucket elimination, oracle/qtn_oracle.py) on all host cores instead.
@@ -159,6 +159,7 @@ def angle_sets(p, n_sets, seed=0):
 
 
 WORKLOADS = {
+    "config1": dict(n=20, p=1, mode="zz+diagonal", edges=None, dtype="complex128"),
     "config2": dict(n=100, p=2, mode="zz+diagonal", edges=None, dtype="complex64"),
     "config3": dict(n=244, p=3, mode="zz+diagonal", edges=None, dtype="complex64"),
     "config3-default": dict(n=244, p=3, mode="default", edges=None, dtype="complex64"),

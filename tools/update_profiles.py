@@ -54,7 +54,7 @@ def launch_eval(path):
 
 
 def main():
-    for src, dst in [("bench_default", "config2"), ("bench_reference", "reference_config2"),
+    for src, dst in [("bench_config1", "config1"), ("bench_default", "config2"), ("bench_reference", "reference_config2"),
                      ("bench_config3", "config3"), ("bench_config3d", "config3d"),
                      ("bench_config4", "config4"), ("bench_config4_k3", "config4_k3")]:
         line = last_json(os.path.join(R, src + ".json"))
