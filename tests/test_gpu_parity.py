@@ -604,6 +604,8 @@ def test_chain_kernel_opt_in(golden, monkeypatch):
     g3 = Q.random_regular_graph(G3["n"], 3, 0)
     p3 = Q.QaoaParams(G3["gammas"], G3["betas"])
     ids3 = [r["edge_index"] for r in G3["modes"]["default"][:10]]
+    monkeypatch.setenv("QTN_TINY_LEVEL", str(1 << 17))  # tiny levels exist
+    monkeypatch.setenv("QTN_SMALL_R", "9")
     out = {}
     for flag in ("0", "1"):
         monkeypatch.setenv("QTN_CHAIN", flag)
