@@ -740,6 +740,14 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   }
   B->n_smem = (int)sidx.size();
   B->n_hbm = (int)hidx.size();
+  // QTN_HBM_ALIGN=1: shallower networks run at the end of the level range
+  // (whole networks move, so their arena lifetimes stay valid)
+  std::vector<int32_t> hshift(B->n_hbm, 0);
+  {
+    const char* av = getenv("QTN_HBM_ALIGN");
+    if (av && av[0] == '1')
+      for (int h = 0; h < B->n_hbm; ++h) hshift[h] = max_lev - plans[hidx[h]]->n_levels;
+  }
   // level-major item lists over all HBM networks
   std::vector<uint64_t> item_desc, prefix, sitem_desc;
   std::vector<uint32_t> item_net, sitem_net;
@@ -791,7 +799,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     for (int h = 0; h < B->n_hbm; ++h) {
       const qtn_plan* P = plans[hidx[h]];
       for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
-        if (P->hbm_level[bi] != lev || !P->hbm_tiles[bi]) continue;  // 0 tiles: fused chain
+        if (P->hbm_level[bi] + hshift[h] != lev || !P->hbm_tiles[bi]) continue;  // 0 tiles: fused chain
         const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
         ((int)sh->R <= small_r ? n_small : n_large) += 1;
         lev_elems += 1ull << sh->R;
@@ -813,7 +821,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       for (int h = 0; h < B->n_hbm; ++h) {
         const qtn_plan* P = plans[hidx[h]];
         for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
-          if (P->hbm_level[bi] != lev || !P->hbm_tiles[bi]) continue;
+          if (P->hbm_level[bi] + hshift[h] != lev || !P->hbm_tiles[bi]) continue;
           const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
           if (split_small && (all_small || (int)sh->R <= small_r)) continue;
           if (use_expand && P->hbm_xidx[bi] >= 0) continue;  // expand_kernel
@@ -829,7 +837,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     for (int h = 0; h < B->n_hbm; ++h) {
       const qtn_plan* P = plans[hidx[h]];
       for (size_t bi = 0; bi < P->hbm_level.size(); ++bi) {
-        if (P->hbm_level[bi] != lev || !P->hbm_tiles[bi]) continue;  // 0 tiles: fused chain
+        if (P->hbm_level[bi] + hshift[h] != lev || !P->hbm_tiles[bi]) continue;  // 0 tiles: fused chain
         const qtn::SHdr* sh = reinterpret_cast<const qtn::SHdr*>(P->hbm_desc.data() + P->hbm_desc_off[bi]);
         if (split_small && (all_small || (int)sh->R <= small_r)) {
           sitem_desc.push_back(desc_base[h] + P->hbm_desc_off[bi]);
@@ -892,7 +900,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     uint32_t acc = 0;
     for (int h = 0; h < B->n_hbm; ++h) {
       for (const auto& r : plans[hidx[h]]->hbm_red) {
-        if (r.level != lev) continue;
+        if (r.level + hshift[h] != lev) continue;
         qtn::RedDev d{};
         d.src = r.src;
         d.out = r.out;
