@@ -20,6 +20,7 @@
 // variables (network.py:153-165) is resolved when the records are built.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <algorithm>
@@ -401,15 +402,15 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
   // config 3 99.7 M -> 102.7 M (measured; 2: 701 M).
   std::vector<int32_t> shift(plans.size(), 0);
   std::vector<std::vector<int32_t>> alap;
+  const char* align_v = getenv("QTN_SM_ALIGN");
+  const int align = align_v ? atoi(align_v) : 3;
   {
-    const char* av = getenv("QTN_SM_ALIGN");
-    const int align = av ? atoi(av) : 3;
     for (size_t k = 0; k < plans.size(); ++k) {
       const int32_t slack = max_lev - plans[k]->sm_levels;
       shift[k] = align == 2 ? slack : (align == 1 ? slack / 2 : 0);
     }
     // 3: every bucket as late as its consumer allows (per-bucket ALAP)
-    if (align == 3) {
+    if (align >= 3) {
       alap.resize(plans.size());
       for (size_t k = 0; k < plans.size(); ++k) {
         const qtn_plan* P = plans[k];
@@ -422,6 +423,56 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
         }
       }
     }
+  }
+  // 4: list scheduling towards even level widths: level by level, every
+  // ready bucket whose ALAP deadline is this level, then ready buckets by
+  // increasing deadline until the level holds total / levels CTAs
+  if (align == 4 && !alap.empty()) {
+    std::vector<std::vector<int32_t>> lev(plans.size());
+    std::vector<std::vector<int32_t>> npend(plans.size());  // unscheduled producers
+    double total = 0.0;
+    for (size_t k = 0; k < plans.size(); ++k) {
+      const qtn_plan* P = plans[k];
+      const int nb = (int)P->sm_buckets.size();
+      lev[k].assign(nb, -1);
+      npend[k].assign(nb, 0);
+      for (int bi = 0; bi < nb; ++bi) {
+        total += std::ldexp(1.0, P->sm_buckets[bi].R);
+        const int32_t c = P->tensors[P->buckets[bi].out].last_use;
+        if (c >= 0 && c < nb) ++npend[k][c];
+      }
+    }
+    const double target = total / std::max(1, max_lev);
+    std::vector<std::tuple<int32_t, size_t, int32_t>> ready;  // (deadline, net, bucket)
+    for (size_t k = 0; k < plans.size(); ++k)
+      for (int bi = 0; bi < (int)lev[k].size(); ++bi)
+        if (npend[k][bi] == 0) ready.emplace_back(alap[k][bi], k, bi);
+    for (int32_t l = 0; l < max_lev; ++l) {
+      std::sort(ready.begin(), ready.end());
+      double width = 0.0;
+      std::vector<std::tuple<int32_t, size_t, int32_t>> later, placed;
+      for (const auto& it : ready) {
+        const size_t k = std::get<1>(it);
+        const int32_t bi = std::get<2>(it);
+        const double w = std::ldexp(1.0, plans[k]->sm_buckets[bi].R);
+        if (std::get<0>(it) <= l || width + w <= target) {
+          lev[k][bi] = l;
+          width += w;
+          placed.push_back(it);
+        } else {
+          later.push_back(it);
+        }
+      }
+      ready.swap(later);
+      for (const auto& it : placed) {  // consumers become ready for level l + 1
+        const size_t k = std::get<1>(it);
+        const int32_t bi = std::get<2>(it);
+        const int32_t c = plans[k]->tensors[plans[k]->buckets[bi].out].last_use;
+        if (c >= 0 && c < (int32_t)lev[k].size() && --npend[k][c] == 0)
+          ready.emplace_back(alap[k][c], k, c);
+      }
+    }
+    alap.swap(lev);
   }
   auto level_of = [&](size_t k, ptrdiff_t bi) -> int32_t {
     if (!alap.empty() && alap[k].size() == plans[k]->sm_buckets.size()) return alap[k][bi];
@@ -501,6 +552,11 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
     }
     S->level_blocks.push_back(acc);
     n_cta += acc;
+  }
+  if (getenv("QTN_DEBUG_ROUTE")) {
+    fprintf(stderr, "set-major levels (CTAs):");
+    for (uint32_t b : S->level_blocks) fprintf(stderr, " %u", b);
+    fprintf(stderr, "\n");
   }
   if (elems + grows.size() >= kGateTag) return fail("too many rows");
   // gate row g lives at row total_elems + g
