@@ -271,7 +271,16 @@ int launch_expand(const XLaunch& L, void* stream) {
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (n_sm <= 0) n_sm = 148;
   }
-  const uint64_t ctas = std::min<uint64_t>(L.total_tiles, (uint64_t)n_sm * 4u);
+  // as many resident CTAs per SM as registers and this launch's stage allow
+  // (QTN_EXPAND_CTAS: a fixed count per SM, for experiments)
+  int per_sm = 0;
+  const char* xc = getenv("QTN_EXPAND_CTAS");
+  if (xc) per_sm = atoi(xc);
+  if (per_sm <= 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expand_kernel, 256, L.stage_bytes) != cudaSuccess)
+    per_sm = 4;
+  per_sm = std::max(1, per_sm);
+  const uint64_t ctas = std::min<uint64_t>(L.total_tiles, (uint64_t)n_sm * (uint64_t)per_sm);
   dim3 grid((uint32_t)ctas, L.n_sets);
   cudaError_t e = launch_pdl<true>(expand_kernel, grid, dim3(256), L.stage_bytes,
                              reinterpret_cast<cudaStream_t>(stream), L);

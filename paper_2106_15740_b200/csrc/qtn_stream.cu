@@ -297,7 +297,7 @@ __device__ __forceinline__ void trace_staged(const R1Dev& r, const Bases& b, con
   }
 }
 
-__global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ StreamLaunch L,
+__global__ void __launch_bounds__(256, 8) trace_kernel(const __grid_constant__ StreamLaunch L,
                                                     const R1Dev* __restrict__ items,
                                                     const uint64_t* __restrict__ prefix,
                                                     uint32_t n_items) {
