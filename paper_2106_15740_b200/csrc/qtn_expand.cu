@@ -168,7 +168,7 @@ __device__ __forceinline__ void expand_tile(const XDesc& d, XItemSmem& X, const 
 // Persistent: CTA b of grid.x takes a contiguous range of the launch's tiles
 // (all items, one set = blockIdx.y), rebuilding the per-item tables only
 // when the item changes.
-__global__ void __launch_bounds__(256) expand_kernel(const __grid_constant__ XLaunch L) {
+__global__ void __launch_bounds__(256, 5) expand_kernel(const __grid_constant__ XLaunch L) {
   extern __shared__ __align__(16) unsigned char xsmem[];
   __shared__ XItemSmem X;
   __shared__ __align__(16) XDesc SD;
