@@ -7,7 +7,7 @@ timeout 900 python -m pytest tests -q -m gpu > gpurun_out/r/pytest_gpu.log 2>&1;
 timeout 300 python __graft_entry__.py > gpurun_out/r/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 600 python bench.py > gpurun_out/r/bench_default.json 2> gpurun_out/r/bench_default.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/r/bench_reference.json 2>&1; echo "ref rc=$?"
-timeout 300 python bench.py --workload config1 --angle-sets 1024 --steps 10 --warmup 3 --no-config5 --cpu-seconds 5 > gpurun_out/r/bench_config1.json 2>&1; echo "c1 rc=$?"
+timeout 300 python bench.py --workload config1 --angle-sets 1024 --steps 50 --warmup 10 --no-config5 --cpu-seconds 5 > gpurun_out/r/bench_config1.json 2>&1; echo "c1 rc=$?"
 timeout 300 python bench.py --workload config3 --angle-sets 256 --steps 5 --warmup 3 --no-config5 --cpu-seconds 5 > gpurun_out/r/bench_config3.json 2>&1; echo "c3 rc=$?"
 timeout 300 python bench.py --workload config3-default --angle-sets 1 --steps 5 --warmup 3 --no-config5 --cpu-seconds 10 > gpurun_out/r/bench_config3d.json 2>&1; echo "c3d rc=$?"
 timeout 300 python bench.py --workload config4 --angle-sets 1 --steps 10 --warmup 3 --no-config5 --cpu-seconds 20 > gpurun_out/r/bench_config4.json 2>&1; echo "c4 rc=$?"
