@@ -774,7 +774,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   const char* tv0 = getenv("QTN_TRACE");
   const bool use_trace = !(tv0 && tv0[0] == '0');
   const char* tmr = getenv("QTN_TRACE_MIN_R");
-  const int trace_min_r = tmr ? atoi(tmr) : 10;
+  const int trace_min_r = tmr ? atoi(tmr) : 8;
   std::vector<qtn::R1Dev> r1items;
   std::vector<uint64_t> r1prefix;
   for (int32_t lev = 0; lev < max_lev; ++lev) {
