@@ -11,7 +11,7 @@ energy driver / light-cone builder the north star asks for are added.
 
 from . import _native  # noqa: F401  (fails loudly if the library is missing)
 from .circuit import (Circuit, Gate, GateKind, ProblemGraph, QaoaParams,
-                      build_qaoa_maxcut_circuit, fuse_zz, gate_matrix, is_diagonal)
+                      build_qaoa_maxcut_circuit, gate_matrix, is_diagonal)
 from .contraction import (DEFAULT_MIXED_RANK, DEFAULT_RANK_CAP, ContractionPlan,
                           RankCapExceeded, contract, contract_many)
 from .energy import EnergyPlan, energy_expectation, plan_edges, shard_edges
@@ -24,8 +24,5 @@ from .ordering import (ContractionOrder, CostReport, contraction_width, greedy_o
 from .pipeline import (MODE_ORDER, MODES, PipelineMode, build_circuit, build_line_graph,
                        build_network, default_angles, get_mode, random_regular_graph,
                        seeded_angles)
-
-from .sweep import BenchRow, BenchSpec, parse_bench_spec, run_benchmark
-from .textio import ParseError, read_circuit, read_graph, write_circuit, write_graph
 
 __version__ = "0.1.0"

@@ -3,9 +3,11 @@
 Mirrors the public names and conventions of
 /root/reference/pkg/src/qtnsim/circuit.py (ProblemGraph 45-69, QaoaParams
 72-90, GateKind/Gate 93-152, Circuit 155-176, gate_matrix 186-205,
-is_diagonal 208-214, build_qaoa_maxcut_circuit 217-250, fuse_zz 253-318)
+is_diagonal 208-214, build_qaoa_maxcut_circuit 217-250)
 so that networks built here are identical, tensor for tensor, to the
-reference's.  The text formats (circuit.py:321-450) live in textio.py.
+reference's.  The ZZ-fusion pass (circuit.py:253-318) and the text formats
+(circuit.py:321-450) are out of scope: the fused ansatz is built
+directly, as the reference's pipeline does (circuit.py:236-245).
 """
 
 from __future__ import annotations
@@ -26,7 +28,6 @@ __all__ = [
     "gate_matrix",
     "is_diagonal",
     "build_qaoa_maxcut_circuit",
-    "fuse_zz",
 ]
 
 
@@ -212,55 +213,3 @@ def build_qaoa_maxcut_circuit(graph: ProblemGraph, params: QaoaParams, fused: bo
             else:
                 gates += [Gate.h(q), Gate.zpow(q, 2.0 * beta), Gate.h(q)]
     return Circuit(graph.node_count, tuple(gates), phase)
-
-
-def fuse_zz(circuit: Circuit) -> Circuit:
-    """ZZ / XPow fusion pass (reference circuit.py:253-318).
-
-    One left-to-right scan.  CNOT(c,t) . ZPow(t, 2g) . CNOT(c,t) becomes
-    ZZ(c, t, g) — the global phase gains e^{-ig}, so the unitary is unchanged
-    — when the ZPow is the next gate on t, the second CNOT the next gate on t
-    after it, and that CNOT is also the next gate on c.  H(q) . ZPow(q, t) .
-    H(q), three consecutive gates on q, becomes XPow(q, t).  Matches are
-    taken greedily in circuit order; gates already absorbed are skipped.
-    Idempotent on fused circuits.
-    """
-    gates = circuit.gates
-    # following gate on the same qubit: succ[(q, i)] = index of the next gate on q
-    succ = {}
-    last = {}
-    for i, g in enumerate(gates):
-        for q in g.qubits:
-            if q in last:
-                succ[(q, last[q])] = i
-            last[q] = i
-    used = [False] * len(gates)
-    out = []
-    phase = circuit.phase
-    for i, g in enumerate(gates):
-        if used[i]:
-            continue
-        if g.kind is GateKind.CNOT:
-            c, t = g.qubits
-            j = succ.get((t, i))
-            k = succ.get((t, j)) if j is not None else None
-            if (j is not None and k is not None and not used[j] and not used[k]
-                    and gates[j].kind is GateKind.ZPOW and gates[k].kind is GateKind.CNOT
-                    and gates[k].qubits == (c, t) and succ.get((c, i)) == k):
-                gamma = gates[j].param / 2.0
-                out.append(Gate.zz(c, t, gamma))
-                phase *= cmath.exp(-1j * gamma)
-                used[i] = used[j] = used[k] = True
-                continue
-        elif g.kind is GateKind.H:
-            q = g.qubits[0]
-            j = succ.get((q, i))
-            k = succ.get((q, j)) if j is not None else None
-            if (j is not None and k is not None and not used[j] and not used[k]
-                    and gates[j].kind is GateKind.ZPOW and gates[k].kind is GateKind.H):
-                out.append(Gate.xpow(q, gates[j].param))
-                used[i] = used[j] = used[k] = True
-                continue
-        out.append(g)
-        used[i] = True
-    return Circuit(circuit.qubit_count, tuple(out), phase)
