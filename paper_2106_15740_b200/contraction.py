@@ -278,8 +278,17 @@ class _CachedRun:
         self.res = torch.empty(1, dtype=torch.complex128, device=dev)
         self.res_host = torch.empty(1, dtype=torch.complex128).pin_memory()
         self.dev = dev
+        self.device_bytes = int(self.ws.numel()) + 16 * int(self.inp.numel())
+        # the staging buffers, workspace and the batch's graph cache are
+        # shared by every caller of this structure: one contraction at a time
+        # (distinct structures still run concurrently)
+        self.lock = threading.Lock()
 
     def run(self, datas) -> complex:
+        with self.lock:
+            return self._run(datas)
+
+    def _run(self, datas) -> complex:
         torch = _torch_cuda()
         stream = torch.cuda.current_stream(self.dev)
         h = self.host.numpy()
@@ -295,6 +304,9 @@ class _CachedRun:
 _RUNS: "collections.OrderedDict" = collections.OrderedDict()
 _RUNS_LOCK = threading.Lock()
 _RUNS_MAX = 64
+# device bytes (workspace + inputs) the cache may keep alive: networks of
+# width 23-26 hold GBs of workspace each
+_RUNS_MAX_BYTES = 8 << 30
 
 
 def _contract_with_ranks(network: TensorNetwork, order: ContractionOrder, rank_cap: int,
@@ -319,8 +331,10 @@ def _contract_with_ranks(network: TensorNetwork, order: ContractionOrder, rank_c
         run = _CachedRun(plan)  # raises without a CUDA device (no CPU fallback)
         with _RUNS_LOCK:
             _RUNS[key] = run
-            while len(_RUNS) > _RUNS_MAX:
-                _RUNS.popitem(last=False)
+            total = sum(r.device_bytes for r in _RUNS.values())
+            while len(_RUNS) > 1 and (len(_RUNS) > _RUNS_MAX or total > _RUNS_MAX_BYTES):
+                _, old = _RUNS.popitem(last=False)
+                total -= old.device_bytes
     return run.run([t.data for t in sl]), list(run.plan.step_ranks)
 
 

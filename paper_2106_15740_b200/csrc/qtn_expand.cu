@@ -253,15 +253,15 @@ int launch_expand(const XLaunch& L, void* stream) {
   }
   // dynamic stage (<= kXStageMax complex128 entries) + the static per-item
   // tables exceed the default 48 KiB: opt in once for the largest stage
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (needs_setup(attr)) {
     cudaError_t e = cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kXStageMax * 16);
     if (e != cudaSuccess) {
       set_error(std::string("expand_kernel attribute: ") + cudaGetErrorString(e));
       return QTN_ECUDA;
     }
-    attr = true;
+    mark_setup(attr);
   }
   // persistent CTAs (several resident per SM), contiguous tile ranges
   static int n_sm = 0;

@@ -2,6 +2,7 @@
 // sm_100a kernels (qtn_kernels.cu).  Not part of the C ABI.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -9,7 +10,24 @@
 #include "../../include/qtn_b200.h"
 #include "qtn_stream.h"
 
+#include <cuda_runtime_api.h>
+
 namespace qtn {
+
+// Function attributes (dynamic shared-memory opt-in) are per device: a
+// one-time setup flag is a bit per device ordinal, not a process-wide bool,
+// so a process that later launches on another GPU sets them there too.
+inline uint64_t current_device_bit() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return 1ull << (dev & 63);
+}
+inline bool needs_setup(const std::atomic<uint64_t>& seen) {
+  return !(seen.load(std::memory_order_acquire) & current_device_bit());
+}
+inline void mark_setup(std::atomic<uint64_t>& seen) {
+  seen.fetch_or(current_device_bit(), std::memory_order_release);
+}
 
 // ---------------------------------------------------------------- bit runs
 // An operand's flat index is a bit-gather of the output index o:

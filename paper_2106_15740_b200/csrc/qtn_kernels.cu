@@ -512,11 +512,11 @@ int launch_bucket(const BucketArgs& a, void* stream) {
   const uint64_t n_tiles = a.n_out >> tile_bits;
   const size_t smem = (size_t)a.table_entries * sizeof(double2);
   const bool fast = a.primary && a.ng >= 1 && a.g[0].c64 && a.out_c64 && a.R >= 1;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};
+  if (needs_setup(attr_set)) {
     cudaFuncSetAttribute(bucket_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(bucket_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr_set = true;
+    mark_setup(attr_set);
   }
   const uint64_t max_blocks = (uint64_t)g_num_sms * 8;
   const unsigned blocks = (unsigned)std::min<uint64_t>(n_tiles, max_blocks);
@@ -1155,6 +1155,10 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
     poff.push_back(blob.size());
     blob.insert(blob.end(), prog.begin(), prog.end());
   }
+  // captured graphs hold kernel parameters that point at the buffers freed
+  // below: drop them before replacing the device program
+  for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
+  B->graphs.clear();
   // HBM networks: recipes relocated into the batch input layout
   std::vector<qtn_tensor_recipe> hrec;
   for (int i = 0; i < B->n; ++i) {
@@ -1314,12 +1318,14 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     int W = (int)std::min<size_t>(kNetWarps, (cap - prog_max) / std::max<size_t>(per_warp, 16));
     W = std::max(1, std::min(W, warps_needed));
     const size_t smem = (size_t)prog_max + (size_t)W * per_warp;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    static std::atomic<size_t> attr[64];  // per device ordinal
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (smem > 48 * 1024 && smem > attr[dev & 63].load()) {
       cudaError_t e = cudaFuncSetAttribute(smem_net_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel attribute");
-      attr = smem;
+      attr[dev & 63].store(smem);
     }
     SmemArgs a;
     a.progs = B->d_prog;

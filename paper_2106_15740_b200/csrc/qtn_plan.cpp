@@ -327,7 +327,9 @@ int encode_stream_desc(const BucketSpec& s, std::vector<uint8_t>& blob) {
     const double stage_w = swv ? atof(swv) : 1024.0;  // measured: a cp.async-gathered entry costs far more than a bulk byte
     for (int tn_c = std::max(0, tb - rp1); tn_c <= std::min(std::min(dnew, tb), std::max(tn_max, tb - rp1)); ++tn_c) {
       const int ta_c = tb - tn_c;
-      if (ta_c > rp1 || ta_c < 0) continue;
+      // ta = 0 with v off bit 0 of the primary would need the two-chunk
+      // (split) slice, which the tile kernel only takes for ta >= 1
+      if (ta_c > rp1 || ta_c < 0 || (ta_c == 0 && a.p_k >= 1)) continue;
       double cost = (double)(2 << ta_c) * esz;
       for (int i = 1; i < (int)a.ng; ++i) {
         int k = 0;

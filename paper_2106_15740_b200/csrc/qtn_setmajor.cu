@@ -101,7 +101,12 @@ const double kCoefHost[kNumCoef][3] = {
     {0.0, 0.0, 0.0}, {1.0, 0.0, 0.0}, {0.70710678118654757, 0.0, 0.0},
     {-0.70710678118654757, 0.0, 0.0}, {0.0, 1.0, 1.0}, {0.0, 1.0, -1.0},
     {0.5, 0.5, 0.5}, {0.5, -0.5, -0.5}};
-__constant__ double kGateCoef[kNumCoef][3];
+// statically initialised: __constant__ memory is per device, and a static
+// initializer is loaded with the module on every device the process uses
+__constant__ double kGateCoef[kNumCoef][3] = {
+    {0.0, 0.0, 0.0}, {1.0, 0.0, 0.0}, {0.70710678118654757, 0.0, 0.0},
+    {-0.70710678118654757, 0.0, 0.0}, {0.0, 1.0, 1.0}, {0.0, 1.0, -1.0},
+    {0.5, 0.5, 0.5}, {0.5, -0.5, -0.5}};
 
 int coef_code(const GateCoef& c) {
   for (int i = 0; i < kNumCoef; ++i)
@@ -570,15 +575,6 @@ int setmajor_build(SetMajor** out, const std::vector<const qtn_plan*>& plans,
     }
   for (uint32_t& w : scal) resolve(w);
   S->n_gate_rows = (int32_t)grows.size();
-  static bool coef_up = false;
-  if (!coef_up) {
-    if (cudaMemcpyToSymbol(kGateCoef, kCoefHost, sizeof(kCoefHost)) != cudaSuccess) {
-      delete S;
-      set_error("set-major executor: coefficient upload failed");
-      return QTN_ECUDA;
-    }
-    coef_up = true;
-  }
   int rc;
   if ((rc = upload_vec(&S->d_recs, recs)) || (rc = upload_vec(&S->d_params, params)) ||
       (rc = upload_vec(&S->d_grows, grows)) || (rc = upload_vec(&S->d_const, cst)) ||

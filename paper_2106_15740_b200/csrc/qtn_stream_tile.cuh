@@ -623,8 +623,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 int g_sms = 0;
 
 int prep() {
-  static bool done = false;
-  if (!done) {
+  static std::atomic<uint64_t> done{0};
+  if (needs_setup(done)) {
     cudaError_t e = cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(Smem));
     if (e != cudaSuccess) {
@@ -635,7 +635,7 @@ int prep() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_sms <= 0) g_sms = 148;
-    done = true;
+    mark_setup(done);
   }
   return QTN_OK;
 }

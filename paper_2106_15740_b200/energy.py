@@ -38,8 +38,8 @@ from .lightcone import EnergyTemplate, energy_template
 from .slicing import choose_slice_vars, slice_assignments
 from .ordering import ContractionOrder, CostReport, rgreedy_order
 
-__all__ = ["EdgeJob", "EnergyPlan", "plan_edges", "shard_edges", "rank_shard", "reduce_partials",
-           "energy_expectation"]
+__all__ = ["EdgeJob", "EnergyPlan", "plan_edges", "compile_jobs", "shard_edges", "rank_shard",
+           "reduce_partials", "energy_expectation"]
 
 
 class EdgeJob:
@@ -83,14 +83,11 @@ def plan_edges(graph: ProblemGraph, p: int, mode: str, edge_ids, rank_cap=DEFAUL
             svars, _, order, report = choose_slice_vars(tpl.line_graph(), order, slice_k)
             assigns = slice_assignments(svars)
         tpls = [tpl.resliced(a) if a else tpl for a in assigns]
-        plan = None
-        if compile_plans:
-            t0 = tpls[0]
-            plan = ContractionPlan(t0.structure, t0.variable_count, t0.fixed, order.sequence,
-                                   rank_cap=rank_cap, dtype=dtype, mixed_rank=mixed_rank,
-                                   smem_budget=smem_budget)
         for a, t in zip(assigns, tpls):
-            out.append(EdgeJob(e, t, order, report, plan, 1.0 / len(assigns), a))
+            out.append(EdgeJob(e, t, order, report, None, 1.0 / len(assigns), a))
+        if compile_plans:
+            compile_jobs(out, rank_cap=rank_cap, dtype=dtype, mixed_rank=mixed_rank,
+                         smem_budget=smem_budget, workers=1)
         return out
 
     edge_ids = list(edge_ids)
@@ -102,6 +99,38 @@ def plan_edges(graph: ProblemGraph, p: int, mode: str, edge_ids, rank_cap=DEFAUL
         with ThreadPoolExecutor(max_workers=min(workers, len(edge_ids))) as ex:
             per_edge = list(ex.map(plan_one, edge_ids))
     return [j for js in per_edge for j in js]
+
+
+def compile_jobs(jobs, rank_cap=DEFAULT_RANK_CAP, dtype="complex64",
+                 mixed_rank=DEFAULT_MIXED_RANK, smem_budget=DEFAULT_SMEM_BUDGET,
+                 workers: int | None = None):
+    """Compile the bucket program of every job that has none yet; the slices
+    of one edge share one plan (they differ only in their data).  Lets a rank
+    order every edge (the LPT partition needs all costs) but compile only the
+    shard it keeps."""
+    groups = {}
+    for j in jobs:
+        if j.plan is None:
+            groups.setdefault((j.index, tuple(j.order.sequence)), []).append(j)
+
+    def one(js):
+        t0 = js[0].template
+        plan = ContractionPlan(t0.structure, t0.variable_count, t0.fixed, js[0].order.sequence,
+                               rank_cap=rank_cap, dtype=dtype, mixed_rank=mixed_rank,
+                               smem_budget=smem_budget)
+        for j in js:
+            j.plan = plan
+
+    todo = list(groups.values())
+    if workers is None:
+        workers = min(32, os.cpu_count() or 1)
+    if workers <= 1 or len(todo) <= 1:
+        for js in todo:
+            one(js)
+    else:
+        with ThreadPoolExecutor(max_workers=min(workers, len(todo))) as ex:
+            list(ex.map(one, todo))
+    return jobs
 
 
 def shard_edges(costs, world_size: int):
@@ -135,6 +164,9 @@ class EnergyPlan:
         self.jobs = list(jobs)
         self.edge_ids = sorted({j.index for j in self.jobs})
         self.plan_seconds = time.perf_counter() - t0
+        if any(j.plan is None for j in self.jobs):
+            compile_jobs(self.jobs, rank_cap=rank_cap, dtype=dtype, mixed_rank=mixed_rank,
+                         smem_budget=smem_budget)
         self.smem_jobs = [j for j in jobs if j.plan.executor == N.EXEC_SMEM]
         self.hbm_jobs = [j for j in jobs if j.plan.executor == N.EXEC_HBM]
         self._device = None
@@ -156,6 +188,8 @@ class EnergyPlan:
         counted at the element size it is stored in: the
         set-major executor's complex64 rows count 8 bytes per entry."""
         self._prepare()
+        if self._batch is None:
+            return 0.0
         eb = self._batch.setmajor_elem_bytes(n_sets)
         small = float(sum(j.plan.alg_bytes for j in self.smem_jobs))
         big = float(sum(j.plan.alg_bytes for j in self.hbm_jobs))
@@ -171,10 +205,18 @@ class EnergyPlan:
             return
         import torch
 
+        self._torch = torch
+        if not self.jobs:
+            # an empty shard (more ranks than jobs): no device program; the
+            # rank contributes zero partial energies to the all-reduce
+            self._batch = None
+            self.set_elems = 0
+            self._device = (torch.device("cuda", torch.cuda.current_device())
+                            if torch.cuda.is_available() else torch.device("cpu"))
+            return
         if not torch.cuda.is_available():
             raise RuntimeError("a CUDA device is required: the B200 backend has no CPU fallback")
         dev = torch.device("cuda", torch.cuda.current_device())
-        self._torch = torch
         self._device = dev
         # one device program for every edge network; input set layout from it
         self._batch = PlanBatch([j.plan for j in self.jobs])
@@ -200,13 +242,13 @@ class EnergyPlan:
         if n_sets not in self._bufs:
             t = self._torch
             dev = self._device
-            need_inputs = (not self.fused) or self._batch.has_hbm
+            need_inputs = self._batch is not None and ((not self.fused) or self._batch.has_hbm)
+            ws_bytes = self._batch.workspace_bytes(n_sets) if self._batch is not None else 0
             self._bufs[n_sets] = dict(
                 inputs=t.zeros(n_sets * self.set_elems if need_inputs else 2, dtype=t.complex128,
                                device=dev),
-                ws=t.empty(max(self._batch.workspace_bytes(n_sets), 16), dtype=t.uint8,
-                           device=dev),
-                res=t.zeros((n_sets, len(self.jobs)), dtype=t.complex128, device=dev),
+                ws=t.empty(max(ws_bytes, 16), dtype=t.uint8, device=dev),
+                res=t.zeros((n_sets, max(len(self.jobs), 1)), dtype=t.complex128, device=dev),
                 energy=t.zeros(n_sets, dtype=t.float64, device=dev),
                 # host <-> device staging of the public energies() call
                 angles=t.empty((n_sets, 2 * self.p), dtype=t.float64, device=dev),
@@ -219,6 +261,8 @@ class EnergyPlan:
     def launches_per_eval(self, n_sets: int = 1) -> int:
         """Kernel launches of one evaluation (executors + energy reduction)."""
         self._prepare()
+        if self._batch is None:
+            return 0
         return self._batch.launches_for(n_sets) + 1 + (0 if self.fused else 1)
 
     def launch(self, angles_dev, stream=None):
@@ -231,6 +275,11 @@ class EnergyPlan:
         b = self._buffers(n_sets)
         st = stream if stream is not None else t.cuda.current_stream(self._device)
         sp = st.cuda_stream
+        if self._batch is None:
+            with t.cuda.stream(st):
+                b["energy"].zero_()
+            self.launches = 0
+            return b
         if self.fused:
             self._batch.execute_angles(angles_dev.data_ptr(), 2 * self.p, n_sets,
                                        b["inputs"].data_ptr(), b["ws"].data_ptr(),
@@ -257,6 +306,9 @@ class EnergyPlan:
         a = np.atleast_2d(np.asarray(angle_sets, dtype=np.float64))
         if a.shape[1] != 2 * self.p:
             raise ValueError(f"expected {2 * self.p} angles per set, got {a.shape[1]}")
+        if self._batch is None:
+            self.launches = 0
+            return np.zeros(a.shape[0], dtype=np.float64)
         b = self._buffers(a.shape[0])
         st = t.cuda.current_stream(self._device)
         if self.fused:
@@ -292,14 +344,21 @@ class EnergyPlan:
 
 
 def rank_shard(graph: ProblemGraph, p: int, mode: str, rank: int, world: int,
-               n_repeats=10, temp=0.02, seed=0, slice_k: int = 0, **plan_kw):
+               n_repeats=10, temp=0.02, seed=0, slice_k: int = 0, edge_ids=None,
+               compile_plans=True, **plan_kw):
     """This rank's jobs (edges, or edge slices): LPT over the reference cost
-    model.  Every rank computes the same deterministic orders, so the
-    partition needs no exchange."""
-    allj = plan_edges(graph, p, mode, range(graph.edge_count), n_repeats=n_repeats, temp=temp,
-                      seed=seed, slice_k=slice_k, **plan_kw)
+    model.  Every rank computes the same deterministic orders (the partition
+    needs every job's cost, and no exchange), then compiles plans only for
+    the jobs it keeps.  May be empty when there are fewer jobs than ranks."""
+    ids = range(graph.edge_count) if edge_ids is None else edge_ids
+    allj = plan_edges(graph, p, mode, ids, n_repeats=n_repeats, temp=temp, seed=seed,
+                      slice_k=slice_k, compile_plans=False,
+                      **{k: v for k, v in plan_kw.items() if k == "workers"})
     keep = shard_edges([j.cost for j in allj], world)[rank]
-    return [allj[k] for k in keep]
+    mine = [allj[k] for k in keep]
+    if compile_plans:
+        compile_jobs(mine, **plan_kw)
+    return mine
 
 
 def reduce_partials(partial: np.ndarray, group=None, device=None) -> np.ndarray:
