@@ -14,7 +14,8 @@ from .circuit import (Circuit, Gate, GateKind, ProblemGraph, QaoaParams,
                       build_qaoa_maxcut_circuit, gate_matrix, is_diagonal)
 from .contraction import (DEFAULT_MIXED_RANK, DEFAULT_RANK_CAP, ContractionPlan,
                           RankCapExceeded, contract, contract_many)
-from .energy import EnergyPlan, energy_expectation, plan_edges, shard_edges
+from .energy import (EnergyPlan, compile_jobs, energy_expectation, plan_edges, rank_shard,
+                     shard_edges)
 from .lightcone import (EnergyTemplate, build_edge_lightcone_circuit, build_energy_network,
                         edge_lightcone_gates, energy_template)
 from .network import (LineGraph, NetworkMode, Tensor, TensorNetwork, circuit_to_network,

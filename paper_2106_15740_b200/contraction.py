@@ -82,6 +82,7 @@ class ContractionPlan:
                  dtype="complex128", mixed_rank=DEFAULT_MIXED_RANK,
                  smem_budget=DEFAULT_SMEM_BUDGET):
         self._h = None
+        self.dtype = "complex64" if _dtype_code(dtype) == N.DTYPE_C64 else "complex128"
         ranks = np.asarray([len(s) for s in structure] or [0], dtype=np.int32)
         offs = np.zeros(len(structure) + 1, dtype=np.int32)
         offs[1:] = np.cumsum([len(s) for s in structure])

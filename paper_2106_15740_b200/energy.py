@@ -296,6 +296,40 @@ class EnergyPlan:
         self.launches = b["launches"]
         return b
 
+    def execute_only(self, angles_dev, stream=None):
+        """The contraction executors alone for every angle set in
+        `angles_dev` (no energy reduction): the launches the bench's roofline
+        times."""
+        self._prepare()
+        if self._batch is None:
+            return
+        t = self._torch
+        n_sets = int(angles_dev.shape[0])
+        b = self._buffers(n_sets)
+        st = stream if stream is not None else t.cuda.current_stream(self._device)
+        self._batch.execute_angles(angles_dev.data_ptr(), 2 * self.p, n_sets,
+                                   b["inputs"].data_ptr(), b["ws"].data_ptr(),
+                                   b["res"].data_ptr(), st.cuda_stream)
+
+    def describe(self, n_sets: int) -> dict:
+        """Executor and arithmetic of one evaluation of n_sets angle sets."""
+        self._prepare()
+        if self._batch is None:
+            return {"kernel": "none (empty shard)", "dtype": "none"}
+        if self.hbm_jobs:
+            kernel = "hbm_executor"
+            dtype = ("c128 inputs, c64 storage + f32 math for rank>=12"
+                     if any(j.plan.dtype == "complex64" for j in self.hbm_jobs) else "c128")
+        elif self._batch.uses_setmajor(n_sets):
+            c64 = self._batch.setmajor_elem_bytes(n_sets) == 8
+            kernel = "sm_level_kernel_c64" if c64 else "sm_level_kernel"
+            dtype = ("c64 (set-major rows complex64, f32 products; gate entries formed in f64)"
+                     if c64 else "c128")
+        else:
+            kernel = "smem_net_kernel"
+            dtype = "c128"
+        return {"kernel": kernel, "dtype": dtype}
+
     def energies(self, angle_sets) -> np.ndarray:
         """Energy per angle set; angle_sets: QaoaParams, a [2p] vector or an
         [n_sets, 2p] array of [gammas..., betas...]."""
