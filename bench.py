@@ -383,9 +383,12 @@ class CudaRig:
         e0.record(self.stream)
         return e0
 
-    def stop(self, e0):
+    def end(self):
         e1 = self.torch.cuda.Event(enable_timing=True)
         e1.record(self.stream)
+        return e1
+
+    def elapsed(self, e0, e1):
         e1.synchronize()
         return e0.elapsed_time(e1) / 1e3
 
@@ -445,15 +448,16 @@ def measure(rig, plan, p, A, steps, warmup, dist=None, clk=None, n_units=None, r
         rig.sync()
         e0 = rig.start()
         step()
+        e1 = rig.end()
         if clk is not None:
-            clk.sample_now()  # while the step executes
-        step_t.append(rig.stop(e0))
+            clk.sample_now()  # while the step executes (outside the events)
+        step_t.append(rig.elapsed(e0, e1))
         launches += plan.launches
         rig.flush()
         rig.sync()
         k0 = rig.start()
         plan.execute_only(ring_dev[it[0] % ring], rig.stream)
-        kern_t.append(rig.stop(k0))
+        kern_t.append(rig.elapsed(k0, rig.end()))
     total = sum(step_t)
     # end to end through the public API: host angles -> energies on host,
     # H2D of the angles and D2H of the energies inside the timed region

@@ -466,3 +466,27 @@ def synthetic_bucket(w, m_small, seed, dtype=np.complex64):
             r = int(rng.integers(1, w + 1))
             ops.append(((0, r), draw((2, 2))))
     return ops
+
+
+def bucket_sampled(outs, out_vars, operands_vars, fetch, v=0):
+    """Selected outputs of one bucket, float64: for each flat output index o
+    in `outs`, sum over the eliminated variable v of the product of every
+    operand's entry at idx_t(o, v) — contraction.py:82-96 (the `_product`
+    chain then `.sum`) evaluated only where asked, for buckets too large to
+    materialise on the host (config 5 at w > 28).  Index maps follow the
+    reference's C order (first variable = most significant bit,
+    network.py:36-61).  fetch(t, flat_indices) returns operand t's entries."""
+    outs = np.asarray(outs, dtype=np.int64)
+    r = len(out_vars)
+    val = {int(x): (outs >> (r - 1 - k)) & 1 for k, x in enumerate(out_vars)}
+    acc = np.zeros(len(outs), dtype=np.complex128)
+    for bit in (0, 1):
+        val[v] = np.full(len(outs), bit, dtype=np.int64)
+        prod = np.ones(len(outs), dtype=np.complex128)
+        for t, vs in enumerate(operands_vars):
+            idx = np.zeros(len(outs), dtype=np.int64)
+            for pos, x in enumerate(vs):
+                idx |= val[int(x)] << (len(vs) - 1 - pos)
+            prod *= np.asarray(fetch(t, idx), dtype=np.complex128)
+        acc += prod
+    return acc

@@ -278,7 +278,7 @@ def main():
             json.dump(blk, f)
     if "c3" in which:
         blk = config_block(244, 3, ["zz+diagonal"])
-        blk2 = config_block(244, 3, ["default"], edge_subset=list(range(0, 366, 23)))
+        blk2 = config_block(244, 3, ["default"])  # all 366 edges: the energy is asserted
         blk["modes"].update(blk2["modes"])
         with open(os.path.join(HERE, "config3.json"), "w") as f:
             json.dump(blk, f)

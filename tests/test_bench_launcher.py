@@ -38,8 +38,11 @@ class CpuRig:
     def start(self):
         return time.perf_counter()
 
-    def stop(self, t0):
-        return time.perf_counter() - t0
+    def end(self):
+        return time.perf_counter()
+
+    def elapsed(self, t0, t1):
+        return t1 - t0
 
     def clocks(self):
         import bench
