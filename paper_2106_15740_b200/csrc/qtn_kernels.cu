@@ -654,6 +654,11 @@ struct qtn_batch {
   // captured evaluations (qtn_batch_execute_angles)
   std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaStream_t cap_stream = nullptr;
+  // concurrent launches of one HBM level (independent buckets): side
+  // streams forked from / joined into the caller's stream with events
+  cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
   // pinned staging of qtn_batch_energies_host
   double* pin = nullptr;
   size_t pin_doubles = 0;
@@ -668,6 +673,11 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
   if (!B) return QTN_OK;
   for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
   if (B->cap_stream) cudaStreamDestroy(B->cap_stream);
+  for (int k = 0; k < 4; ++k) {
+    if (B->side[k]) cudaStreamDestroy(B->side[k]);
+    if (B->ev_join[k]) cudaEventDestroy(B->ev_join[k]);
+  }
+  if (B->ev_fork) cudaEventDestroy(B->ev_fork);
   if (B->pin) cudaFreeHost(B->pin);
   for (void* p : {(void*)B->d_prog, (void*)B->d_prog_off, (void*)B->d_in_off,
                   (void*)B->d_smem_index, (void*)B->d_desc, (void*)B->d_item_desc,
@@ -1348,7 +1358,37 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     if (e != cudaSuccess) return cuda_fail(e, "smem_net_kernel launch");
   }
   if (B->n_hbm) {
+    // The launches of one level are independent (their buckets sit at the
+    // same depth of the elimination trees, the arena never aliases buckets
+    // of one level): run them concurrently on forked streams (QTN_LEVEL_STREAMS=0:
+    // one stream, for A/B measurements).  A level's launches are joined
+    // back before the next level starts.
+    const char* lsv = getenv("QTN_LEVEL_STREAMS");
+    const bool level_streams = !(lsv && lsv[0] == '0');
+    if (level_streams && !B->ev_fork) {
+      cudaError_t e = cudaEventCreateWithFlags(&B->ev_fork, cudaEventDisableTiming);
+      for (int k = 0; k < 4 && e == cudaSuccess; ++k) {
+        e = cudaStreamCreateWithFlags(&B->side[k], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&B->ev_join[k], cudaEventDisableTiming);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "level streams");
+    }
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
+      // launches of this level, in issue order: reduce, small, trace, expand, stream
+      const int n_launch = (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) +
+                           (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
+                           (B->level_r1chunks[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
+                           (B->level_tiles[lev] ? 1 : 0);
+      const bool fork = level_streams && n_launch >= 2 && !B->chain_len[lev];
+      int slot = 0;  // launch k of the level goes to stream k (0: the caller's)
+      auto next_stream = [&]() -> void* {
+        if (!fork) return stream;
+        const int k = slot++;
+        if (k == 0) return stream;
+        cudaStreamWaitEvent(B->side[k - 1], B->ev_fork, 0);
+        return reinterpret_cast<void*>(B->side[k - 1]);
+      };
+      if (fork) cudaEventRecord(B->ev_fork, st);
       StreamLaunch L;
       std::memset(&L, 0, sizeof(L));
       L.descs = B->d_desc;
@@ -1372,7 +1412,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       const uint32_t nr = B->level_red0[lev + 1] - B->level_red0[lev];
       if (nr && (rc = qtn::launch_reduce(L, B->d_red + B->level_red0[lev],
                                          B->d_red_prefix + B->level_rprefix0[lev], nr,
-                                         B->level_rchunks[lev], stream)))
+                                         B->level_rchunks[lev], next_stream())))
         return rc;
       const uint32_t ns = B->level_sitem0[lev + 1] - B->level_sitem0[lev];
       if (ns) {
@@ -1380,13 +1420,13 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         Ls.item_desc = B->d_sitem_desc + B->level_sitem0[lev];
         Ls.item_net = B->d_sitem_net + B->level_sitem0[lev];
         Ls.n_items = ns;
-        if ((rc = qtn::launch_small(Ls, B->level_smax_r[lev], stream))) return rc;
+        if ((rc = qtn::launch_small(Ls, B->level_smax_r[lev], next_stream()))) return rc;
       }
       if (B->level_r1chunks[lev] &&
           (rc = qtn::launch_trace(L, B->d_r1 + B->level_r1item0[lev],
                                   B->d_r1prefix + B->level_r1prefix0[lev],
                                   B->level_r1item0[lev + 1] - B->level_r1item0[lev],
-                                  B->level_r1chunks[lev], stream)))
+                                  B->level_r1chunks[lev], next_stream())))
         return rc;
       if (B->level_xtiles[lev]) {
         qtn::XLaunch X;
@@ -1405,9 +1445,9 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         X.ws_base = L.ws_base;
         X.ws_set_stride = L.ws_set_stride;
         X.net_ws_off = L.net_ws_off;
-        if ((rc = qtn::launch_expand(X, stream))) return rc;
+        if ((rc = qtn::launch_expand(X, next_stream()))) return rc;
       }
-      if (!B->level_tiles[lev]) continue;
+      if (B->level_tiles[lev]) {
       L.item_desc = B->d_item_desc + B->level_item0[lev];
       L.item_net = B->d_item_net + B->level_item0[lev];
       L.tile_prefix = B->d_tile_prefix + B->level_prefix0[lev];
@@ -1418,7 +1458,13 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       const char* wv = getenv("QTN_WIDE_TPI");
       const uint64_t wide_tpi = wv ? strtoull(wv, nullptr, 10) : 32;
       const bool wide = L.total_tiles < wide_tpi * L.n_items;
-      if ((rc = launch_stream(L, stream, wide))) return rc;
+      if ((rc = launch_stream(L, next_stream(), wide))) return rc;
+      }
+      // join: the next level (or the fold) waits for every branch
+      for (int k = 1; k < slot; ++k) {
+        cudaEventRecord(B->ev_join[k - 1], B->side[k - 1]);
+        cudaStreamWaitEvent(st, B->ev_join[k - 1], 0);
+      }
     }
     dim3 grid((B->n_hbm + 127) / 128, n_sets);
     cudaError_t e = launch_pdl<true>(
