@@ -79,6 +79,10 @@ typedef struct {
   int64_t program_bytes;     /* SMEM-executor program size                       */
   double alg_bytes;          /* sum over buckets of e*(operand + output entries) */
   double flops_sum;          /* sum 2^(rank+1) (ordering.py:60-61)               */
+  int32_t n_levels;          /* HBM executor: levels of the elimination trees    */
+  int32_t n_fused_chains;    /* HBM executor: product chains run as one kernel   */
+  double exec_bytes;         /* bytes the executor's kernels move (fused chains:  */
+                             /* operands + final output only)                   */
 } qtn_plan_info_t;
 
 /* ---------------------------------------------------------------- ordering */

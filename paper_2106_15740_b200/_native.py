@@ -46,6 +46,9 @@ class PlanInfo(C.Structure):
         ("program_bytes", C.c_int64),
         ("alg_bytes", C.c_double),
         ("flops_sum", C.c_double),
+        ("n_levels", C.c_int32),
+        ("n_fused_chains", C.c_int32),
+        ("exec_bytes", C.c_double),
     ]
 
 

@@ -114,6 +114,9 @@ class ContractionPlan:
         self.program_bytes = int(info.program_bytes)
         self.alg_bytes = float(info.alg_bytes)
         self.flops_sum = float(info.flops_sum)
+        self.n_levels = int(info.n_levels)
+        self.n_fused_chains = int(info.n_fused_chains)
+        self.exec_bytes = float(info.exec_bytes)
         sr = np.zeros(max(len(sequence), 1), dtype=np.int32)
         N.check(N.lib.qtn_plan_step_ranks(h, N.i32(sr)))
         self.step_ranks = tuple(int(x) for x in sr[: len(sequence)])

@@ -214,6 +214,7 @@ struct qtn_plan {
   int64_t workspace_bytes = 0;
   int64_t smem_bytes = 0;
   double alg_bytes = 0.0;
+  double exec_bytes = -1.0;              // < 0: equal to alg_bytes (no fusion)
   double flops_sum = 0.0;
   std::vector<uint8_t> program;          // SMEM executor blob
   // HBM executor: one streaming descriptor per bucket (tagged pointers
@@ -228,6 +229,8 @@ struct qtn_plan {
   std::vector<qtn::XDesc> hbm_xdesc;
   std::vector<int32_t> hbm_r1idx;        // single-operand (trace) record per bucket, or -1
   std::vector<qtn::R1Dev> hbm_r1;        // net = 0 here; set per batch
+  std::vector<qtn::FDesc> hbm_fdesc;     // fused product chains (qtn_fused.cu)
+  std::vector<int32_t> hbm_flevel;       // their levels
   int32_t n_levels = 0;
   // Set-major form of an SMEM-eligible network (qtn_setmajor.cu): angle
   // sets are the fastest-varying dimension of every tensor in HBM, one

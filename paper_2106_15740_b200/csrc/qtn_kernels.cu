@@ -647,6 +647,15 @@ struct qtn_batch {
   std::vector<uint32_t> level_xitem0;   // first expand item of each level (+ end)
   std::vector<uint64_t> level_xprefix0, level_xtiles;
   std::vector<uint32_t> level_xstage;   // stage bytes (max over the level's items)
+  // fused product chains per level (fused_kernel)
+  qtn::FDesc* d_fdesc = nullptr;
+  uint32_t* d_fitem_desc = nullptr;
+  uint32_t* d_fitem_net = nullptr;
+  uint64_t* d_fprefix = nullptr;
+  uint64_t* d_cprefix = nullptr;        // split items: combine CTAs (units)
+  std::vector<uint32_t> level_fitem0;   // first fused item of each level (+ end)
+  std::vector<uint64_t> level_fprefix0, level_fctas, level_cctas;
+  std::vector<uint32_t> level_fsmem;
   // fused single-operand chains per level (reduce_kernel)
   qtn::RedDev* d_red = nullptr;
   uint32_t* d_red_prefix = nullptr;
@@ -687,7 +696,9 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_hbm_rec, (void*)B->d_sitem_desc, (void*)B->d_sitem_net,
                   (void*)B->d_red, (void*)B->d_red_prefix, (void*)B->d_xdesc,
                   (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix,
-                  (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix})
+                  (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix,
+                  (void*)B->d_fdesc, (void*)B->d_fitem_desc, (void*)B->d_fitem_net,
+                  (void*)B->d_fprefix, (void*)B->d_cprefix})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
   delete B;
@@ -764,15 +775,47 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   const char* sv = getenv("QTN_SMALL_R");  // buckets up to this output rank: small kernel
   const int small_r = sv ? atoi(sv) : qtn::kSmallR;
   std::vector<uint64_t> desc_base(B->n_hbm);
-  std::vector<uint32_t> xdesc_base(B->n_hbm);
+  std::vector<uint32_t> xdesc_base(B->n_hbm), fdesc_base(B->n_hbm);
   std::vector<qtn::XDesc> xdescs;
+  std::vector<qtn::FDesc> fdescs;
   for (int h = 0; h < B->n_hbm; ++h) {
     const qtn_plan* P = plans[hidx[h]];
     desc_base[h] = desc.size();
     desc.insert(desc.end(), P->hbm_desc.begin(), P->hbm_desc.end());
     xdesc_base[h] = (uint32_t)xdescs.size();
     xdescs.insert(xdescs.end(), P->hbm_xdesc.begin(), P->hbm_xdesc.end());
+    fdesc_base[h] = (uint32_t)fdescs.size();
+    fdescs.insert(fdescs.end(), P->hbm_fdesc.begin(), P->hbm_fdesc.end());
   }
+  // fused product chains, level-major over all HBM networks
+  std::vector<uint32_t> fitem_desc, fitem_net;
+  std::vector<uint64_t> fprefix, cprefix;
+  for (int32_t lev = 0; lev < max_lev; ++lev) {
+    B->level_fitem0.push_back((uint32_t)fitem_desc.size());
+    B->level_fprefix0.push_back(fprefix.size());
+    uint64_t acc = 0, cacc = 0;
+    uint32_t smem = 0;
+    fprefix.push_back(0);
+    cprefix.push_back(0);
+    for (int h = 0; h < B->n_hbm; ++h) {
+      const qtn_plan* P = plans[hidx[h]];
+      for (size_t f = 0; f < P->hbm_fdesc.size(); ++f) {
+        if (P->hbm_flevel[f] + hshift[h] != lev) continue;
+        const qtn::FDesc& fd = P->hbm_fdesc[f];
+        fitem_desc.push_back(fdesc_base[h] + (uint32_t)f);
+        fitem_net.push_back((uint32_t)h);
+        acc += fd.sk ? (fd.n_units << fd.sk) : (fd.n_units + (1ull << fd.upc_log2) - 1) >> fd.upc_log2;
+        fprefix.push_back(acc);
+        cacc += fd.sk ? fd.n_units : 0;
+        cprefix.push_back(cacc);
+        smem = std::max(smem, qtn::fused_smem_bytes(fd));
+      }
+    }
+    B->level_fctas.push_back(acc);
+    B->level_cctas.push_back(cacc);
+    B->level_fsmem.push_back(smem);
+  }
+  B->level_fitem0.push_back((uint32_t)fitem_desc.size());
   // expanding buckets take the outer-product kernel (QTN_EXPAND=0: the
   // streaming kernel, for A/B measurements)
   const char* xv = getenv("QTN_EXPAND");
@@ -941,6 +984,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     B->chain_len.assign(nl, 0);
     auto tiny_only = [&](size_t l) {
       return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] && !B->level_r1chunks[l] &&
+             !B->level_fctas[l] &&
              B->level_red0[l + 1] == B->level_red0[l] && B->level_sitem0[l + 1] > B->level_sitem0[l];
     };
     for (size_t l = 0; chain_on && l < nl;) {
@@ -977,6 +1021,9 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_xitem_net, xitem_net)) || (rc = upload(&B->d_xprefix, xprefix)) ||
       (rc = upload(&B->d_level_sitem0, B->level_sitem0)) ||
       (rc = upload(&B->d_r1, r1items)) || (rc = upload(&B->d_r1prefix, r1prefix)) ||
+      (rc = upload(&B->d_fdesc, fdescs)) || (rc = upload(&B->d_fitem_desc, fitem_desc)) ||
+      (rc = upload(&B->d_fitem_net, fitem_net)) || (rc = upload(&B->d_fprefix, fprefix)) ||
+      (rc = upload(&B->d_cprefix, cprefix)) ||
       (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
       (rc = upload(&B->d_fold_tags, ftags)) || (rc = upload(&B->d_fold_c64, fc64)) ||
       (rc = upload(&B->d_fold_first, ffirst)) || (rc = upload(&B->d_fold_pow2, fpow2)) ||
@@ -1032,7 +1079,8 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
       }
       c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
-           (B->level_r1chunks[lev] ? 1 : 0);
+           (B->level_r1chunks[lev] ? 1 : 0) + (B->level_fctas[lev] ? 1 : 0) +
+           (B->level_cctas[lev] ? 1 : 0);
     }
     c += 1;
   }
@@ -1375,7 +1423,8 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     }
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
       // launches of this level, in issue order: reduce, small, trace, expand, stream
-      const int n_launch = (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) +
+      const int n_launch = (B->level_fctas[lev] ? 1 : 0) +
+                           (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) +
                            (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
                            (B->level_r1chunks[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
                            (B->level_tiles[lev] ? 1 : 0);
@@ -1408,6 +1457,31 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
           return rc;
         lev += B->chain_len[lev] - 1;
         continue;
+      }
+      if (B->level_fctas[lev]) {
+        qtn::FLaunch F;
+        std::memset(&F, 0, sizeof(F));
+        F.descs = B->d_fdesc;
+        F.item_desc = B->d_fitem_desc + B->level_fitem0[lev];
+        F.item_net = B->d_fitem_net + B->level_fitem0[lev];
+        F.cta_prefix = B->d_fprefix + B->level_fprefix0[lev];
+        F.n_items = B->level_fitem0[lev + 1] - B->level_fitem0[lev];
+        F.n_sets = (uint32_t)n_sets;
+        F.total_ctas = B->level_fctas[lev];
+        F.smem_bytes = B->level_fsmem[lev];
+        F.in_base = L.in_base;
+        F.in_set_stride = L.in_set_stride;
+        F.net_in_off = L.net_in_off;
+        F.ws_base = L.ws_base;
+        F.ws_set_stride = L.ws_set_stride;
+        F.net_ws_off = L.net_ws_off;
+        void* fs = next_stream();
+        if ((rc = qtn::launch_fused(F, fs))) return rc;
+        if (B->level_cctas[lev]) {  // split-K partial sums -> outputs, same stream
+          F.cta_prefix = B->d_cprefix + B->level_fprefix0[lev];
+          F.total_ctas = B->level_cctas[lev];
+          if ((rc = qtn::launch_fused_combine(F, fs))) return rc;
+        }
       }
       const uint32_t nr = B->level_red0[lev + 1] - B->level_red0[lev];
       if (nr && (rc = qtn::launch_reduce(L, B->d_red + B->level_red0[lev],

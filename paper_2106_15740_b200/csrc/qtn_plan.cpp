@@ -573,6 +573,251 @@ bool encode_expand_desc(const BucketSpec& s, XDesc& d) {
   return true;
 }
 
+// Fused product-chain descriptor (qtn_stream.h FDesc, kernel in
+// qtn_fused.cu).  Tile choice: the output's lowest 5 bits (a warp stores 32
+// consecutive outputs), the primary's lowest bits (contiguous staging), then
+// greedily the U bit that grows the staged bytes least (a bit few or small
+// operands depend on is reuse), summed bits first on ties; within one stage
+// buffer and <= 11 (complex128: 10) tile output bits.  Sides: an operand
+// joins the first side whose widest operand covers its tile bits if that
+// side's entries are reused (>= 2 tile bits outside it); streamed sides stay
+// raw copies.
+namespace {
+struct FPlan {
+  uint64_t tile = 0;
+  std::vector<std::vector<int>> sides;
+  uint32_t bytes = 0;
+};
+}  // namespace
+
+bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
+  const int R = (int)s.out_vars.size(), K = (int)s.summed.size(), n = (int)s.opvars.size();
+  if (n < 1 || n > kFMaxOps || K < 1 || R + K > 62) return false;
+  std::memset(&d, 0, sizeof(d));
+  auto ubit = [&](int32_t u) -> int {
+    for (int i = 0; i < R; ++i)
+      if (s.out_vars[i] == u) return R - 1 - i;
+    for (int j = 0; j < K; ++j)
+      if (s.summed[j] == u) return R + j;
+    return -1;
+  };
+  const int nu = R + K;
+  std::vector<uint64_t> dep(n, 0);
+  std::vector<std::vector<int>> opbit(n, std::vector<int>(nu, -1));  // U bit -> operand bit
+  int prim = 0;
+  for (int t = 0; t < n; ++t) {
+    const auto& vs = s.opvars[t];
+    const int rk = (int)vs.size();
+    if (rk > 32) return false;
+    for (int j = 0; j < rk; ++j) {
+      const int b = ubit(vs[j]);
+      if (b < 0) return false;
+      dep[t] |= 1ull << b;
+      opbit[t][b] = rk - 1 - j;
+    }
+    if (vs.size() > s.opvars[prim].size()) prim = t;
+  }
+  const uint32_t mesz = s.math_f32 ? 8u : 16u;
+  const int max_out = kFThreadBits + kFMaxAcc;
+  auto esz = [&](int t) { return s.opc64[t] ? 8u : 16u; };
+  auto make_sides = [&](uint64_t tl) {
+    std::vector<int> ord(n);
+    for (int t = 0; t < n; ++t) ord[t] = t;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+      const int fa = __builtin_popcountll(dep[a] & tl), fb = __builtin_popcountll(dep[b] & tl);
+      return fa != fb ? fa > fb : s.opvars[a].size() > s.opvars[b].size();
+    });
+    std::vector<std::vector<int>> sides;
+    for (int t : ord) {
+      bool placed = false;
+      for (auto& sd : sides) {
+        const uint64_t sdep = dep[sd[0]] & tl;
+        const int reuse_bits = __builtin_popcountll(tl) - __builtin_popcountll(sdep);
+        if (((dep[t] & tl) & ~sdep) == 0 && reuse_bits >= 2) {
+          sd.push_back(t);
+          placed = true;
+          break;
+        }
+      }
+      if (!placed) sides.push_back({t});
+    }
+    return sides;
+  };
+  auto side_kind = [&](const std::vector<int>& sd, uint64_t tl) -> uint8_t {
+    if (sd.size() == 1 && esz(sd[0]) == mesz) return kFSideRaw;
+    if (sd.size() == 1 && __builtin_popcountll(dep[sd[0]] & tl) <= kFThreadBits) return kFSideConv;
+    return kFSideProd;
+  };
+  // stage buffer bytes of a tile: raw regions (raw and product sides' operands)
+  // + math-type regions of the conversion and product sides
+  auto buf_bytes = [&](uint64_t tl, const std::vector<std::vector<int>>& sides) {
+    uint64_t b = 0;
+    for (const auto& sd : sides) {
+      const uint8_t kd = side_kind(sd, tl);
+      if (kd != kFSideConv)
+        for (int t : sd) b += ((uint64_t)std::max(2u, 1u << __builtin_popcountll(dep[t] & tl)) * esz(t) + 15) & ~15ull;
+      if (kd != kFSideRaw)
+        b += ((uint64_t)std::max(2u, 1u << __builtin_popcountll(dep[sd[0]] & tl)) * mesz + 15) & ~15ull;
+    }
+    return b;
+  };
+  auto n_out = [&](uint64_t tl) { return __builtin_popcountll(tl & ((1ull << R) - 1)); };
+  auto fits = [&](uint64_t tl) {
+    return buf_bytes(tl, make_sides(tl)) <= kFBufBytes && n_out(tl) <= max_out &&
+           __builtin_popcountll(tl) <= kFMaxQ;
+  };
+  uint64_t tile = 0;
+  {
+    std::vector<int> want;
+    for (int b = 0; b < std::min(R, 5); ++b) want.push_back(b);
+    for (int ob = 0; ob < 10; ++ob)
+      for (int b = 0; b < nu; ++b)
+        if (opbit[prim][b] == ob) want.push_back(b);
+    for (int b : want)
+      if (!((tile >> b) & 1) && fits(tile | (1ull << b))) tile |= 1ull << b;
+  }
+  for (;;) {
+    int best = -1;
+    uint64_t best_f = ~0ull;
+    for (int b = 0; b < nu; ++b) {
+      if ((tile >> b) & 1) continue;
+      const uint64_t tl = tile | (1ull << b);
+      if (!fits(tl)) continue;
+      uint64_t f = buf_bytes(tl, make_sides(tl)) * 2 + (b < R ? 1 : 0);  // summed bits first on ties
+      if (f < best_f || (f == best_f && best >= 0 && opbit[prim][b] >= 0 && opbit[prim][best] >= 0 &&
+                         opbit[prim][b] < opbit[prim][best])) {
+        best_f = f;
+        best = b;
+      }
+    }
+    if (best < 0) break;
+    tile |= 1ull << best;
+  }
+  std::vector<int> qb, lb, gb;  // tile bits (outputs ascending, then summed), loop, grid
+  for (int b = 0; b < R; ++b) ((tile >> b) & 1 ? qb : gb).push_back(b);
+  const int nto = (int)qb.size();
+  for (int b = R; b < nu; ++b) ((tile >> b) & 1 ? qb : lb).push_back(b);
+  const int nq = (int)qb.size();
+  if (nq < 1) return false;
+  auto put = [&](const std::vector<std::pair<int, int>>& pr, uint32_t* dst, uint8_t& cnt, int cap) {
+    std::vector<uint32_t> runs;
+    make_runs(pr, runs);
+    if ((int)runs.size() > cap) return false;
+    std::copy(runs.begin(), runs.end(), dst);
+    cnt = (uint8_t)runs.size();
+    return true;
+  };
+  std::vector<std::vector<int>> sides = make_sides(tile);
+  const int nthr = std::min(nq, kFThreadBits);
+  // sides that depend on in-thread tile bits first; the others are constant
+  // per thread and stage (factored out of the term loop)
+  uint64_t inthr = 0;
+  for (int i = nthr; i < nq; ++i) inthr |= 1ull << qb[i];
+  std::stable_partition(sides.begin(), sides.end(),
+                        [&](const std::vector<int>& sd) { return (dep[sd[0]] & inthr) != 0; });
+  int n_var = 0;
+  for (const auto& sd : sides) n_var += (dep[sd[0]] & inthr) != 0 ? 1 : 0;
+  // raw regions first (16-byte aligned), then the non-raw side regions
+  uint32_t off = 0;
+  int k = 0;
+  std::vector<int> slot(n, -1);  // op -> position in d.ops
+  for (size_t si = 0; si < sides.size(); ++si)
+    for (int t : sides[si]) slot[t] = k++;
+  for (size_t si = 0; si < sides.size(); ++si) {
+    FSide& S = d.sides[si];
+    const uint64_t sdep = dep[sides[si][0]] & tile;
+    std::vector<int> qa;  // q positions of the side's compact bits
+    for (int i = 0; i < nq; ++i)
+      if ((sdep >> qb[i]) & 1) qa.push_back(i);
+    std::vector<std::pair<int, int>> qr;
+    for (size_t c = 0; c < qa.size(); ++c) qr.push_back({qa[c], (int)c});
+    if (!put(qr, S.qrun, S.n_qrun, kFQRuns)) return false;
+    S.nst = (uint8_t)qa.size();
+    S.first_op = (uint8_t)slot[sides[si][0]];
+    S.n_ops = (uint8_t)sides[si].size();
+    S.kind = side_kind(sides[si], tile);
+    S.tconst = (sdep & inthr) == 0 ? 1 : 0;
+    for (int t : sides[si]) {
+      FOp& o = d.ops[slot[t]];
+      o.ptr = s.optag[t];
+      o.c64 = s.opc64[t];
+      o.side = (uint8_t)si;
+      std::vector<int> oc;  // q positions of the op's compact bits
+      for (int i = 0; i < nq; ++i)
+        if ((dep[t] >> qb[i]) & 1) oc.push_back(i);
+      o.nst = (uint8_t)oc.size();
+      if (S.kind != kFSideConv) {  // a conversion side has no raw region
+        o.raw_off = off;
+        off += std::max(2u, 1u << oc.size()) * esz(t);
+        off = (off + 15u) & ~15u;
+      }
+      std::vector<std::pair<int, int>> sr, ocr, gr, lr;
+      for (size_t c = 0; c < oc.size(); ++c) sr.push_back({(int)c, opbit[t][qb[oc[c]]]});
+      for (size_t c = 0; c < qa.size(); ++c) {
+        auto it = std::find(oc.begin(), oc.end(), qa[c]);
+        if (it != oc.end()) ocr.push_back({(int)c, (int)(it - oc.begin())});
+      }
+      for (size_t j = 0; j < gb.size(); ++j)
+        if (opbit[t][gb[j]] >= 0) gr.push_back({(int)j, opbit[t][gb[j]]});
+      for (size_t j = 0; j < lb.size(); ++j)
+        if (opbit[t][lb[j]] >= 0) lr.push_back({(int)j, opbit[t][lb[j]]});
+      if (!put(sr, o.srun, o.n_srun, kFQRuns) || !put(ocr, o.ocrun, o.n_ocrun, kFQRuns) ||
+          !put(gr, o.grun, o.n_grun, kFGRuns) || !put(lr, o.lrun, o.n_lrun, kFGRuns))
+        return false;
+      // pairs: compact bit 0 is operand bit 0 (16-byte copies of 2 complex64)
+      o.pairs = (o.c64 && !oc.empty() && opbit[t][qb[oc[0]]] == 0) ? 1 : 0;
+    }
+  }
+  for (size_t si = 0; si < sides.size(); ++si) {
+    FSide& S = d.sides[si];
+    if (S.kind == kFSideRaw) {
+      S.st_off = d.ops[S.first_op].raw_off;
+    } else {
+      S.st_off = off;
+      off += std::max(2u, 1u << S.nst) * mesz;
+      off = (off + 15u) & ~15u;
+      if (S.kind == kFSideProd) d.has_finish = 1;
+    }
+  }
+  d.math_f32 = s.math_f32 ? 1 : 0;
+  d.n_var = (uint8_t)n_var;
+  if (off > kFBufBytes + 512) return false;
+  d.buf_bytes = off;
+  d.n_sides = (uint8_t)sides.size();
+  std::vector<std::pair<int, int>> og, oq;
+  for (size_t j = 0; j < gb.size(); ++j) og.push_back({(int)j, gb[j]});
+  for (int i = 0; i < nto; ++i) oq.push_back({i, qb[i]});
+  if (!put(og, d.ogrun, d.n_ogrun, kFGRuns) || !put(oq, d.oqrun, d.n_oqrun, kFQRuns)) return false;
+  d.out = s.out_tag;
+  d.R = (uint8_t)R;
+  d.K = (uint8_t)K;
+  d.out_c64 = s.out_c64 ? 1 : 0;
+  d.n_ops = (uint8_t)n;
+  d.nq = (uint8_t)nq;
+  d.nto = (uint8_t)nto;
+  d.ng = (uint8_t)gb.size();
+  d.nl = (uint8_t)lb.size();
+  d.n_units = 1ull << gb.size();
+  // split-K: a unit of more than 2^16 terms spreads its loop bits over
+  // 2^sk CTAs (partial sums combined by fused_combine_kernel, fixed order)
+  // when the item has few units; else units per CTA: ~2^16 terms per CTA
+  // (amortises its table setup), keeping >= 512 CTAs per item
+  const int nl = (int)lb.size(), ng = (int)gb.size();
+  int sk = 0;
+  if (ng < 9) sk = std::min(nl, std::max(0, nq + nl - 16));
+  int upc = 0;
+  if (!sk) {
+    upc = std::max(0, 16 - (nq + nl));
+    upc = std::min(upc, std::max(0, ng - 9));
+  }
+  d.upc_log2 = (uint8_t)upc;
+  d.sk = (uint8_t)sk;
+  if (getenv("QTN_DEBUG_DESC") && R + K >= atoi(getenv("QTN_DEBUG_DESC")))
+    fprintf(stderr, "fdesc R=%d K=%d ops=%d sides=%d nq=%d nto=%d ng=%d nl=%d buf=%u upc=%d sk=%d fin=%d\n", R,
+            K, n, (int)sides.size(), nq, nto, ng, nl, off, upc, sk, (int)d.has_finish);
+  return true;
+}
+
 }  // namespace qtn
 
 using namespace qtn;
@@ -936,15 +1181,64 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     const char* fv = getenv("QTN_FUSE_REDUCE");
     const bool fuse = !(fv && fv[0] == '0');
     std::vector<int32_t> chain_head(nb, -1), chain_tail(nb, -1), chain_len(nb, 0);
+    std::vector<char> is_fchain(nb, 0);
+    std::map<int32_t, uint64_t> fpart_bytes;  // split fused chains: partial-sum block bytes
+    // Product chains (qtn_fused.cu): a bucket of >= 2 operands whose result
+    // is then reduced by single-operand buckets is one fused contraction; the
+    // union-size product and the chain's intermediates are never written
+    // (the GEMM census in DESIGN §3.7).  Opt-in
+    // (QTN_FUSE_CHAIN=1): measured at break-even with the bucket-by-bucket
+    // kernels.  QTN_FCHAIN_MIN_R: smallest union rank of the head.
+    {
+      const char* fcv = getenv("QTN_FUSE_CHAIN");
+      const bool fchain = fcv && fcv[0] == '1';
+      const char* fmr = getenv("QTN_FCHAIN_MIN_R");
+      const int fmin_r = fmr ? atoi(fmr) : 10;
+      for (int bi = 0; fchain && bi < nb; ++bi) {
+        const auto& b = P->buckets[bi];
+        if (b.ops.size() < 2 || chain_head[bi] >= 0 || b.rank + 1 < fmin_r) continue;
+        std::vector<int32_t> members;
+        std::vector<int32_t> summed{b.v};
+        for (int32_t cur = bi;;) {
+          const int32_t c = P->tensors[P->buckets[cur].out].last_use;
+          if (c < 0 || c >= nb || P->buckets[c].ops.size() != 1) break;
+          members.push_back(c);
+          summed.push_back(P->buckets[c].v);
+          cur = c;
+        }
+        if (members.empty()) continue;
+        // geometry check with placeholder tags (tags do not change it)
+        FChainSpec fs;
+        for (int32_t id : b.ops) {
+          fs.opvars.push_back(P->tensors[id].vars);
+          fs.opc64.push_back(P->tensors[id].c64 ? 1 : 0);
+          fs.optag.push_back(0);
+        }
+        fs.summed = summed;
+        fs.out_vars = P->tensors[P->buckets[members.back()].out].vars;
+        fs.out_c64 = P->tensors[P->buckets[members.back()].out].c64;
+        fs.math_f32 = P->tensors[b.out].c64;  // head product stored complex64 -> float math
+        fs.out_tag = 0;
+        FDesc probe;
+        if (!encode_fused_desc(fs, probe)) continue;
+        if (probe.sk) fpart_bytes[bi] = fused_part_bytes(probe);
+        is_fchain[bi] = 1;
+        chain_head[bi] = bi;
+        chain_len[bi] = 1 + (int)members.size();
+        for (int32_t c : members) chain_head[c] = bi;
+        chain_tail[bi] = members.back();
+      }
+    }
     constexpr int kRedMax = 8;  // the reduce kernel keeps 2^k source offsets in shared memory
     if (fuse) {
       for (int bi = 0; bi < nb; ++bi) {
         const auto& b = P->buckets[bi];
-        if (b.ops.size() != 1) continue;
+        if (b.ops.size() != 1 || chain_head[bi] >= 0) continue;
         const auto& src = P->tensors[b.ops[0]];
         const int32_t pb = src.input ? -1 : src.born;
         // extend the producer's chain (at most kRedMax eliminated variables)
-        const bool extend = pb >= 0 && chain_head[pb] >= 0 && chain_len[chain_head[pb]] < kRedMax;
+        const bool extend = pb >= 0 && chain_head[pb] >= 0 && !is_fchain[chain_head[pb]] &&
+                            chain_len[chain_head[pb]] < kRedMax;
         chain_head[bi] = extend ? chain_head[pb] : bi;
         chain_len[chain_head[bi]] += 1;
         chain_tail[chain_head[bi]] = bi;  // buckets in order: the last one wins
@@ -961,7 +1255,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       const char* mkv = getenv("QTN_FUSE_MAX_K");
       const int fuse_max_k = mkv ? atoi(mkv) : 4;
       for (int bi = 0; bi < nb; ++bi) {
-        if (chain_head[bi] != bi) continue;
+        if (chain_head[bi] != bi || is_fchain[bi]) continue;
         const auto& src = P->tensors[P->buckets[bi].ops[0]];
         int lowest = 64;
         for (int32_t c = bi;; c = P->tensors[P->buckets[c].out].last_use) {
@@ -1027,6 +1321,14 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       t.ws_off = place(hblocks, bytes, s0, e, 256);
       ws = std::max(ws, t.ws_off + bytes);
     }
+    // partial sums of split fused chains: live during their level only
+    std::map<int32_t, int64_t> fpart_off;
+    for (const auto& kv : fpart_bytes) {
+      const int32_t lv = P->hbm_level[kv.first];
+      const int64_t bytes = std::max<int64_t>((int64_t)kv.second, 256);
+      fpart_off[kv.first] = place(hblocks, bytes, lv, lv, 256);
+      ws = std::max(ws, fpart_off[kv.first] + bytes);
+    }
     P->workspace_bytes = ws;
     // one streaming descriptor per bucket
     auto tag_of = [&](int32_t id) -> uint64_t {
@@ -1041,6 +1343,34 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       if (chain_head[bi] >= 0) {  // fused chain (head) or absorbed member: no descriptor
         P->hbm_tiles.push_back(0);
         if (chain_head[bi] != bi) continue;
+        if (is_fchain[bi]) {
+          FChainSpec fs;
+          for (int32_t id : b.ops) {
+            fs.opvars.push_back(P->tensors[id].vars);
+            fs.opc64.push_back(P->tensors[id].c64 ? 1 : 0);
+            fs.optag.push_back(tag_of(id));
+          }
+          fs.summed.push_back(b.v);
+          for (int32_t c = P->tensors[b.out].last_use;; c = P->tensors[P->buckets[c].out].last_use) {
+            fs.summed.push_back(P->buckets[c].v);
+            if (c == chain_tail[bi]) break;
+          }
+          const auto& out = P->tensors[P->buckets[chain_tail[bi]].out];
+          fs.out_vars = out.vars;
+          fs.out_c64 = out.c64;
+          fs.math_f32 = P->tensors[b.out].c64;
+          fs.out_tag = tag_of(P->buckets[chain_tail[bi]].out);
+          FDesc fd;
+          if (!encode_fused_desc(fs, fd) || (fd.sk != 0) != (fpart_off.count(bi) != 0)) {
+            delete P;
+            set_error("fused chain: descriptor no longer encodable");
+            return QTN_EINVAL;
+          }
+          if (fd.sk) fd.part = tag_ws((uint64_t)fpart_off[bi]);
+          P->hbm_fdesc.push_back(fd);
+          P->hbm_flevel.push_back(P->hbm_level[bi]);
+          continue;
+        }
         const auto& src = P->tensors[b.ops[0]];
         const auto& out = P->tensors[P->buckets[chain_tail[bi]].out];
         RedRec r;
@@ -1183,8 +1513,23 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         P->hbm_xdesc.push_back(xd);
       }
     }
+    // bytes the executor moves: a fused chain (product or reduce) reads its
+    // head's operands and writes its tail's output only
+    double eb = 0.0;
+    for (int bi = 0; bi < nb; ++bi) {
+      const int32_t h = chain_head[bi];
+      if (h >= 0 && h != bi) continue;
+      const auto& b = P->buckets[bi];
+      for (int32_t id : b.ops)
+        eb += std::ldexp((double)elem_bytes(P->tensors[id].c64), P->tensors[id].rank());
+      const auto& o = P->tensors[P->buckets[h >= 0 ? chain_tail[bi] : bi].out];
+      eb += std::ldexp((double)elem_bytes(o.c64), o.rank());
+    }
+    P->exec_bytes = eb;
   }
   // algorithmic bytes: e * (operand entries + output entries) per bucket
+  // (the reference's per-bucket traffic; exec_bytes above is what the fused
+  // chains actually move)
   for (auto& b : P->buckets) {
     double bytes = 0.0;
     for (int32_t id : b.ops) {
@@ -1214,6 +1559,9 @@ extern "C" int qtn_plan_info(const qtn_plan* P, qtn_plan_info_t* info) {
   info->program_bytes = (int64_t)P->program.size();
   info->alg_bytes = P->alg_bytes;
   info->flops_sum = P->flops_sum;
+  info->n_levels = P->n_levels;
+  info->n_fused_chains = (int32_t)P->hbm_fdesc.size();
+  info->exec_bytes = P->exec_bytes < 0.0 ? P->alg_bytes : P->exec_bytes;
   return QTN_OK;
 }
 

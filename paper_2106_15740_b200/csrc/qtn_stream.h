@@ -260,6 +260,119 @@ constexpr uint32_t kTraceChunk = 4096;
 int launch_trace(const StreamLaunch& L, const R1Dev* items, const uint64_t* prefix,
                  uint32_t n_items, uint64_t total_chunks, void* stream);
 
+// ---- fused product chains: a bucket of >= 2 operands whose result is then
+// reduced by k single-operand buckets (partial traces) is one contraction
+//   out[o] = sum_{s in 2^K} prod_t T_t[idx_t(o, s)]      K = k + 1 summed vars
+// (contraction.py:42-54 products + k+1 times :94-96 `.sum`), i.e. a batched
+// GEMM  out[b,m,n] = sum_k A[b,m,k] B[b,n,k]  with the small operands folded
+// in.  The union-size product and the chain's intermediates are never
+// written.  Index space U = R output bits [0, R) + K summed bits [R, R+K);
+// every operand index is a bit gather of U.  U is cut into
+//   q  tile bits (nq <= 16): q = e | s << nto, e = nto output bits (ascending
+//      output position), s = the tile's summed bits; the 256 threads take q's
+//      low min(8, nq) bits, each thread loops over the rest;
+//   l  loop bits: summed bits outside the tile, iterated by the CTA;
+//   g  grid bits: output bits outside the tile, one work unit each.
+// Per (unit, l): every operand's entries touched by the tile are staged in
+// shared memory (compact index over the tile bits it depends on), converted
+// to the math type (float for complex64 outputs, double for complex128).
+constexpr int kFMaxOps = 8;
+constexpr int kFGRuns = 24;
+constexpr int kFQRuns = 16;
+constexpr int kFMaxQ = 16;            // tile bits
+constexpr int kFThreadBits = 8;       // 256 threads
+constexpr int kFMaxAcc = 2;           // <= 4 output accumulators per thread
+constexpr uint32_t kFBufBytes = 49152;  // one stage buffer (two per CTA: double buffered)
+constexpr int kFLTabBits = 8;         // loop-offset tables up to 2^8 loop values
+// Operands are staged raw (their storage type, cp.async, no register round
+// trip) into a stage buffer over their compact index (the tile bits they
+// depend on).  Operands are grouped into "sides": the compute loop multiplies
+// one entry per side.  A side of one operand stored in the math type reads
+// the operand's raw region directly; any other side (gate tensors folded into
+// a reused wide operand, or a complex128 operand under float math) gets a
+// region of its own, filled from the raw regions by a shared-memory pass.
+struct FOp {
+  uint64_t ptr;                       // tagged
+  uint8_t c64, side, nst, n_grun, n_lrun, n_srun, n_ocrun, pairs;
+  uint32_t raw_off;                   // byte offset of the raw region in a stage buffer
+  uint32_t pad[3];
+  uint32_t srun[kFQRuns];             // op compact index bits -> operand bits
+  uint32_t ocrun[kFQRuns];            // side compact index bits -> op compact bits
+  uint32_t grun[kFGRuns];             // grid index bits -> operand bits
+  uint32_t lrun[kFGRuns];             // loop index bits -> operand bits
+};
+// side kinds: raw region of its single operand (cp.async) / one small
+// operand converted to the math type through a register (<= 256 entries) /
+// product of several operands (or a large conversion) formed by a shared
+// memory pass from their raw regions
+constexpr uint8_t kFSideRaw = 0, kFSideConv = 1, kFSideProd = 2;
+struct FSide {
+  uint8_t nst, n_qrun, kind, first_op, n_ops, tconst, pad[2];  // tconst: no in-thread bits
+  uint32_t st_off;                    // byte offset of the side's region in a stage buffer
+  uint32_t qrun[kFQRuns];             // tile index (q) bits -> side compact bits
+  uint32_t pad2;
+};
+struct FDesc {
+  uint64_t out;                       // tagged
+  uint64_t n_units;                   // 2^ng work units
+  uint8_t R, K, out_c64, n_ops, nq, nto, ng, nl;
+  uint8_t n_ogrun, n_oqrun, upc_log2, sk, n_sides, has_finish, math_f32, n_var;
+  // upc: units per CTA; sk: split-K bits; math_f32: products in float (the
+  // chain's head product is a complex64 intermediate), sums in double;
+  // n_var: sides [0, n_var) depend on in-thread bits, the rest are per-thread
+  // constants of a stage
+  uint32_t buf_bytes;                 // bytes of one stage buffer
+  uint32_t pad2;
+  uint64_t part;                      // tagged: partial sums [unit][2^sk][2^nto] (math type), sk > 0
+  uint32_t ogrun[kFGRuns];            // grid index bits -> output bits
+  uint32_t oqrun[kFQRuns];            // tile output bits (q's low nto) -> output bits
+  FSide sides[kFMaxOps];
+  FOp ops[kFMaxOps];                  // grouped by side, sides in order
+};
+static_assert(sizeof(FSide) % 16 == 0, "FSide");
+static_assert(sizeof(FOp) % 16 == 0, "FOp");
+static_assert(sizeof(FDesc) % 16 == 0, "FDesc");
+// Host encoder for a fused chain: opvars (MSB-first variable lists), summed
+// variables, output variables (MSB first).  Returns false when the chain is
+// not expressible (operand count, runs, ranks).
+struct FChainSpec {
+  std::vector<std::vector<int32_t>> opvars;
+  std::vector<uint8_t> opc64;
+  std::vector<uint64_t> optag;
+  std::vector<int32_t> summed;
+  std::vector<int32_t> out_vars;
+  bool out_c64;
+  bool math_f32;                      // products in float (head product stored complex64)
+  uint64_t out_tag;
+};
+bool encode_fused_desc(const FChainSpec& s, FDesc& d);
+struct FLaunch {
+  const FDesc* descs;                 // device
+  const uint32_t* item_desc;          // device: descriptor index per item
+  const uint32_t* item_net;           // device: network index per item
+  const uint64_t* cta_prefix;         // device: n_items + 1 (CTAs of one set)
+  uint32_t n_items;
+  uint32_t n_sets;
+  uint64_t total_ctas;                // CTAs of one set
+  uint32_t smem_bytes;                // dynamic shared memory (max over items)
+  const char* in_base;
+  int64_t in_set_stride;
+  const int64_t* net_in_off;
+  char* ws_base;
+  int64_t ws_set_stride;
+  const int64_t* net_ws_off;
+};
+// dynamic shared memory of one descriptor: stage + per-op j tables
+uint32_t fused_smem_bytes(const FDesc& d);
+// bytes of the partial-sum block of a split descriptor (0 when sk == 0)
+inline uint64_t fused_part_bytes(const FDesc& d) {  // partial sums are complex128
+  return d.sk ? (d.n_units << (d.sk + d.nto)) * 16ull : 0ull;
+}
+int launch_fused(const FLaunch& L, void* stream);
+// split items: one CTA per (item, unit) sums the 2^sk partials in order;
+// cta_prefix = the units of split items (0 for the others)
+int launch_fused_combine(const FLaunch& L, void* stream);
+
 // single descriptor with absolute pointers, descriptor passed by value
 int launch_stream_single(const std::vector<uint8_t>& desc, void* stream);
 

@@ -672,3 +672,45 @@ def test_trace_kernel_every_eligible_bucket(golden, monkeypatch, dtype, tol):
         e = r["edge_index"]
         assert abs(out["1"][e] - w) <= ref_tol * abs(w) + 1e-13
         assert abs(out["1"][e] - out["0"][e]) <= tol * abs(w) + 1e-13
+
+
+@pytest.mark.parametrize("min_r", ["0", "10"])
+def test_fused_product_chains(golden, monkeypatch, min_r):
+    """Product buckets followed by their partial traces as one contraction
+    (fused_kernel, qtn_fused.cu; default on for head buckets of union rank
+    >= 10): equal to the unfused bucket-by-bucket evaluation
+    (QTN_FUSE_CHAIN=0) and to the reference values, on config 3 default
+    (GEMM-shaped chains, dot-product chains into scalars) and config 4 edge
+    #16 (wide streaming chains), complex128 and complex64, at 1 and 3 angle
+    sets.  min_r 0 also fuses the tiny chains of the first levels."""
+    monkeypatch.setenv("QTN_FCHAIN_MIN_R", min_r)
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    recs = G["modes"]["default"][:10]
+    G4 = golden("config4.json")
+    rec4 = complex(*[r for r in G4["modes"]["zz+diagonal"] if r["edge_index"] == 16][0]["value"])
+    g4 = Q.random_regular_graph(G4["n"], 3, 0)
+    p4v = Q.QaoaParams(G4["gammas"], G4["betas"])
+    rng = np.random.default_rng(3)
+    sets3 = np.vstack([params.as_vector(), rng.uniform(0, math.pi, (2, 2 * G["p"]))])
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_FUSE_CHAIN", flag)
+        for dt in ("complex128", "complex64"):
+            plan = Q.EnergyPlan(graph, G["p"], "default", dtype=dt,
+                                edge_ids=[r["edge_index"] for r in recs])
+            p4 = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype=dt, edge_ids=[16])
+            nf = sum(j.plan.n_fused_chains for j in plan.jobs + p4.jobs)
+            assert (nf > 0) == (flag == "1")
+            out[flag, dt] = (plan.zz_values(params), p4.zz_values(p4v)[16], plan.energies(sets3))
+            assert plan.launches == plan.launches_per_eval(1)
+    for dt, tol in (("complex128", 1e-11), ("complex64", 1e-5)):
+        for r in recs:
+            w = complex(*r["value"])
+            e = r["edge_index"]
+            assert abs(out["1", dt][0][e] - w) <= tol * abs(w) + 1e-12, (dt, e)
+            assert abs(out["1", dt][0][e] - out["0", dt][0][e]) <= tol * abs(w) + 1e-12
+        assert abs(out["1", dt][1] - rec4) <= tol * abs(rec4)
+        assert np.allclose(out["1", dt][2], out["0", dt][2], rtol=tol, atol=tol)
+
