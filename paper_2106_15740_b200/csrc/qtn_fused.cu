@@ -107,49 +107,63 @@ static_assert(sizeof(OpIssue) == 16, "OpIssue");
 // Shared-memory layout of a CTA (dynamic part):
 //   buf[2]  two stage buffers of d.buf_bytes
 //   red     256 x 16 B: cross-thread reduction of summed thread bits
-//   issue   per operand OpIssue
-//   ktab    per operand: gather(k << 8) (pairs: k << 9) of its compact index;
-//           the per-thread part gather(tid) (pairs: 2 tid) is a register
-//   ltab    per operand 2^nl u32 loop-index offsets (nl <= kFLTabBits)
-//   jts     per side njs u32: byte offset of the summed in-thread bits
-//   jta     per side 4 u32: byte offset of the in-thread output bits
-//   oslot   4 u64: output offset of the in-thread output bits
+//   issue   per operand OpIssue (pointers resolved for the CTA's item/set)
+//   tab     the descriptor's lookup tables, built on the host
+//           (fused_build_tables) and copied in with the descriptor:
+//     os    4 u64: output offset of the in-thread output bits
+//     on    2 x 16 u64: output offset of the thread index (low / high nibble)
+//     per operand: kt  gather(k << 8) (pairs: k << 9) of its compact index
+//                  lt  2^nl loop-index offsets (nl <= kFLTabBits)
+//                  tn  2 x 16: element offset of the thread index (nibbles)
+//     per side:    js  njs byte offsets of the summed in-thread bits
+//                  ja  4 byte offsets of the in-thread output bits
+//                  cn  2 x 16: byte offset of the thread's entry (nibbles)
+// Gathers are OR-linear over disjoint bits, so a thread index's offset is
+// lo[tid & 15] + hi[tid >> 4].
 struct FLayout {
-  uint32_t bstride, red, issue, ktab, ltab, jts, jta, oslot, total;
-  uint32_t kofs[kFMaxOps], lofs[kFMaxOps];
+  uint32_t bstride, red, issue, tab, total;  // bytes
+  uint32_t os, on, words;                    // words within tab
+  uint32_t kt[kFMaxOps], lt[kFMaxOps], tn[kFMaxOps];
+  uint32_t js[kFMaxOps], ja[kFMaxOps], cn[kFMaxOps];
 };
 __host__ __device__ inline FLayout fused_layout(const FDesc& d) {
   FLayout L{};
   const uint32_t nthr = d.nq < kFThreadBits ? d.nq : kFThreadBits;
   const uint32_t jn = d.nq - nthr, na = d.nto > nthr ? d.nto - nthr : 0u;
+  const uint32_t njs = 1u << (jn - na);
+  const uint32_t nlt = d.nl <= kFLTabBits ? 1u << d.nl : 0u;
+  uint32_t w = 0;
+  L.os = w;
+  w += 2u * kAcc;
+  L.on = w;
+  w += 2u * 32u;
+  for (uint32_t t = 0; t < d.n_ops; ++t) {
+    const uint32_t nst = d.ops[t].nst, sh = d.ops[t].pairs ? 9u : 8u;
+    L.kt[t] = w;
+    w += nst > sh ? 1u << (nst - sh) : 1u;
+    L.lt[t] = w;
+    w += nlt;
+    L.tn[t] = w;
+    w += 32u;
+  }
+  for (uint32_t s = 0; s < d.n_sides; ++s) {
+    L.js[s] = w;
+    w += njs;
+    L.ja[s] = w;
+    w += kAcc;
+    L.cn[s] = w;
+    w += 32u;
+  }
+  L.words = (w + 3u) & ~3u;
   L.bstride = (d.buf_bytes + 15u) & ~15u;
   uint32_t off = 2u * L.bstride;
   L.red = off;
   off += 256u * 16u;
   L.issue = off;
   off += 16u * d.n_ops;
-  L.ktab = off;
-  for (uint32_t t = 0; t < d.n_ops; ++t) {
-    const uint32_t nst = d.ops[t].nst, sh = d.ops[t].pairs ? 9u : 8u;
-    L.kofs[t] = (off - L.ktab) / 4u;
-    off += 4u * (nst > sh ? 1u << (nst - sh) : 1u);
-  }
   off = (off + 15u) & ~15u;
-  L.ltab = off;
-  const uint32_t nlt = d.nl <= kFLTabBits ? 1u << d.nl : 0u;
-  for (uint32_t t = 0; t < d.n_ops; ++t) {
-    L.lofs[t] = (off - L.ltab) / 4u;
-    off += 4u * nlt;
-  }
-  off = (off + 15u) & ~15u;
-  L.jts = off;
-  off += 4u * d.n_sides * (1u << (jn - na));
-  off = (off + 15u) & ~15u;
-  L.jta = off;
-  off += 4u * d.n_sides * kAcc;
-  off = (off + 15u) & ~15u;
-  L.oslot = off;
-  off += 8u * kAcc;
+  L.tab = off;
+  off += 4u * L.words;
   L.total = (off + 15u) & ~15u;
   return L;
 }
@@ -158,18 +172,19 @@ __host__ __device__ inline FLayout fused_layout(const FDesc& d) {
 // partial sums: for each summed in-thread value js and output slot a < 2^NA,
 // the product of one staged entry per varying side (32-bit shared addresses:
 // thread base + js part + slot part).
+// (side tables: sj[s * sstr + js] = summed part, sj[s * sstr + njs + a] = slot part)
 template <typename C, int NS, int NA>
-__device__ __forceinline__ void stage_terms(const uint32_t* jts, const uint32_t* cb, const uint32_t* jtas,
+__device__ __forceinline__ void stage_terms(const uint32_t* sj, uint32_t sstr, const uint32_t* cb,
                                             uint32_t njs, C (&ps)[kAcc]) {
   uint32_t jta[NS][1 << NA];
 #pragma unroll
   for (int s = 0; s < NS; ++s)
 #pragma unroll
-    for (int a = 0; a < (1 << NA); ++a) jta[s][a] = jtas[s * kAcc + a];
+    for (int a = 0; a < (1 << NA); ++a) jta[s][a] = sj[s * sstr + njs + a];
   for (uint32_t js = 0; js < njs; ++js) {
     uint32_t off[NS];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) off[s] = cb[s] + jts[s * njs + js];
+    for (int s = 0; s < NS; ++s) off[s] = cb[s] + sj[s * sstr + js];
 #pragma unroll
     for (int a = 0; a < (1 << NA); ++a) {
       C p = lds_c(off[0] + jta[0][a], (C*)nullptr);
@@ -180,26 +195,25 @@ __device__ __forceinline__ void stage_terms(const uint32_t* jts, const uint32_t*
   }
 }
 template <typename C, int NS>
-__device__ __forceinline__ void stage_terms_na(uint32_t na, const uint32_t* jts, const uint32_t* cb,
-                                               const uint32_t* jtas, uint32_t njs, C (&ps)[kAcc]) {
+__device__ __forceinline__ void stage_terms_na(uint32_t na, const uint32_t* sj, uint32_t sstr,
+                                               const uint32_t* cb, uint32_t njs, C (&ps)[kAcc]) {
   switch (na) {
-    case 0: stage_terms<C, NS, 0>(jts, cb, jtas, njs, ps); break;
-    case 1: stage_terms<C, NS, 1>(jts, cb, jtas, njs, ps); break;
-    default: stage_terms<C, NS, 2>(jts, cb, jtas, njs, ps); break;
+    case 0: stage_terms<C, NS, 0>(sj, sstr, cb, njs, ps); break;
+    case 1: stage_terms<C, NS, 1>(sj, sstr, cb, njs, ps); break;
+    default: stage_terms<C, NS, 2>(sj, sstr, cb, njs, ps); break;
   }
 }
 // more than 4 varying sides: slot offsets from shared memory
 template <typename C>
-__device__ __forceinline__ void stage_terms_any(uint32_t nv, uint32_t na, const uint32_t* jts,
-                                                const uint32_t* cb, const uint32_t* jtas, uint32_t njs,
-                                                C (&ps)[kAcc]) {
+__device__ __forceinline__ void stage_terms_any(uint32_t nv, uint32_t na, const uint32_t* sj, uint32_t sstr,
+                                                const uint32_t* cb, uint32_t njs, C (&ps)[kAcc]) {
   for (uint32_t js = 0; js < njs; ++js) {
 #pragma unroll
     for (uint32_t a = 0; a < (uint32_t)kAcc; ++a) {
       if (a < (1u << na)) {
-        C p = lds_c(cb[0] + jts[js] + jtas[a], (C*)nullptr);
+        C p = lds_c(cb[0] + sj[js] + sj[njs + a], (C*)nullptr);
         for (uint32_t s = 1; s < nv; ++s)
-          p = cm(p, lds_c(cb[s] + jts[s * njs + js] + jtas[s * kAcc + a], (C*)nullptr));
+          p = cm(p, lds_c(cb[s] + sj[s * sstr + js] + sj[s * sstr + njs + a], (C*)nullptr));
         ps[a] = cadd(ps[a], p);
       }
     }
@@ -207,9 +221,9 @@ __device__ __forceinline__ void stage_terms_any(uint32_t nv, uint32_t na, const 
 }
 
 template <typename C>
-__device__ __forceinline__ void fused_body(const FDesc& d, const char* in, char* ws, uint64_t u0,
-                                           uint64_t u1, uint32_t l0, uint32_t l1, uint32_t split,
-                                           unsigned char* smem) {
+__device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs, const char* in, char* ws,
+                                           uint64_t u0, uint64_t u1, uint32_t l0, uint32_t l1,
+                                           uint32_t split, unsigned char* smem) {
   using E = typename Elem<C>::T;
   const FLayout Lo = fused_layout(d);
   const uint32_t tid = threadIdx.x, n = d.n_ops, ns = d.n_sides, nv = d.n_var;
@@ -221,83 +235,55 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const char* in, char*
   const bool active = tid < (1u << nthr);
   const uint32_t sbase = smem_u32(smem);
   const bool ltab_on = d.nl <= kFLTabBits;
-  // ---- per-CTA tables
+  // ---- per-CTA tables: the host-built tables with the descriptor (one
+  // 16-byte copy per thread), the copy records with resolved pointers
+  const uint32_t* tw = reinterpret_cast<const uint32_t*>(smem + Lo.tab);
   {
-    OpIssue* iss = reinterpret_cast<OpIssue*>(smem + Lo.issue);
-    uint32_t* ktab = reinterpret_cast<uint32_t*>(smem + Lo.ktab);
-    uint32_t* ltab = reinterpret_cast<uint32_t*>(smem + Lo.ltab);
-    uint32_t* jts = reinterpret_cast<uint32_t*>(smem + Lo.jts);
-    uint32_t* jtas = reinterpret_cast<uint32_t*>(smem + Lo.jta);
-    for (uint32_t t = 0; t < n; ++t) {
-      const FOp& o = d.ops[t];
-      const uint32_t sh = o.pairs ? 9u : 8u;
-      const uint32_t nk = o.nst > sh ? 1u << (o.nst - sh) : 1u;
-      for (uint32_t k = tid; k < nk; k += 256u)
-        ktab[Lo.kofs[t] + k] = (uint32_t)fgather_ol((uint64_t)k << sh, o.srun, o.n_srun);
-      if (ltab_on)
-        for (uint32_t l = tid; l < (1u << d.nl); l += 256u)
-          ltab[Lo.lofs[t] + l] = (uint32_t)fgather_ol(l, o.lrun, o.n_lrun);
-      if (tid == 0) {
-        const FSide& S = d.sides[o.side];
-        OpIssue r;
-        r.src = fresolve(o.ptr, in, ws);
-        r.c64 = o.c64;
-        if (S.kind == kFSideConv) {
-          r.mode = 3;
-          r.dst = S.st_off;
-          r.n = (uint16_t)(1u << o.nst);
-        } else {
-          r.mode = o.pairs ? 1 : (o.c64 ? 0 : 2);
-          r.dst = o.raw_off;
-          r.n = (uint16_t)(o.pairs ? (1u << o.nst) >> 1 : 1u << o.nst);
-        }
-        iss[t] = r;
+    const uint4* src = reinterpret_cast<const uint4*>(tabs + d.tab_off / 4u);
+    uint4* dst = reinterpret_cast<uint4*>(smem + Lo.tab);
+    for (uint32_t i = tid; i < Lo.words / 4u; i += 256u) dst[i] = __ldg(src + i);
+    if (tid < n) {
+      const FOp& o = d.ops[tid];
+      const FSide& S = d.sides[o.side];
+      OpIssue r;
+      r.src = fresolve(o.ptr, in, ws);
+      r.c64 = o.c64;
+      if (S.kind == kFSideConv) {
+        r.mode = 3;
+        r.dst = S.st_off;
+        r.n = (uint16_t)(1u << o.nst);
+      } else {
+        r.mode = o.pairs ? 1 : (o.c64 ? 0 : 2);
+        r.dst = o.raw_off;
+        r.n = (uint16_t)(o.pairs ? (1u << o.nst) >> 1 : 1u << o.nst);
       }
-    }
-    if (tid < (uint32_t)kAcc)
-      reinterpret_cast<uint64_t*>(smem + Lo.oslot)[tid] =
-          tid < (1u << na) ? fgather_ol((uint64_t)tid << nthr, d.oqrun, d.n_oqrun) : 0ull;
-    for (uint32_t si = 0; si < ns; ++si) {
-      for (uint32_t js = tid; js < njs; js += 256u)
-        jts[si * njs + js] = (uint32_t)sizeof(C) *
-            (uint32_t)fgather_ol((uint64_t)(js << na) << nthr, d.sides[si].qrun, d.sides[si].n_qrun);
-      if (tid < (uint32_t)kAcc)
-        jtas[si * kAcc + tid] = tid < (1u << na)
-            ? (uint32_t)sizeof(C) * (uint32_t)fgather_ol((uint64_t)tid << nthr, d.sides[si].qrun, d.sides[si].n_qrun)
-            : 0u;
+      reinterpret_cast<OpIssue*>(smem + Lo.issue)[tid] = r;
     }
   }
+  __syncthreads();
   // per-thread parts: operand element offsets (copies), side entry addresses (terms)
+  const uint32_t tlo = tid & 15u, thi = tid >> 4;
   uint32_t thr[kFMaxOps], cth[kFMaxOps];
   for (uint32_t t = 0; t < kFMaxOps; ++t) {
-    thr[t] = 0;
-    cth[t] = 0;
-    if (t < n) {
-      const FOp& o = d.ops[t];
-      const uint32_t x = o.pairs ? 2u * tid : tid;
-      const uint32_t nb = o.nst < 8u ? o.nst : 8u;
-      thr[t] = (uint32_t)fgather_ol(x & ((2u << nb) - 1u), o.srun, o.n_srun);
-    }
-    if (t < ns)  // shared byte address of the thread's entry of side t in buffer 0
-      cth[t] = sbase + d.sides[t].st_off +
-               (active ? (uint32_t)sizeof(C) * (uint32_t)fgather_ol(tid, d.sides[t].qrun, d.sides[t].n_qrun) : 0u);
+    thr[t] = t < n ? tw[Lo.tn[t] + tlo] + tw[Lo.tn[t] + 16u + thi] : 0u;
+    // shared byte address of the thread's entry of side t in buffer 0
+    cth[t] = t < ns ? sbase + d.sides[t].st_off + (active ? tw[Lo.cn[t] + tlo] + tw[Lo.cn[t] + 16u + thi] : 0u)
+                    : 0u;
   }
   char* outp = const_cast<char*>(fresolve(d.out, in, ws));
   double2* part = d.sk ? reinterpret_cast<double2*>(const_cast<char*>(fresolve(d.part, in, ws))) : nullptr;
-  const uint64_t othr = fgather_ol(tid, d.oqrun, d.n_oqrun);
+  const uint64_t* tw64 = reinterpret_cast<const uint64_t*>(tw);
+  const uint64_t othr = tw64[Lo.on / 2u + tlo] + tw64[Lo.on / 2u + 16u + thi];
   const OpIssue* iss = reinterpret_cast<const OpIssue*>(smem + Lo.issue);
-  const uint32_t* ktab = reinterpret_cast<const uint32_t*>(smem + Lo.ktab);
-  const uint32_t* ltab = reinterpret_cast<const uint32_t*>(smem + Lo.ltab);
-  const uint32_t* jts = reinterpret_cast<const uint32_t*>(smem + Lo.jts);
-  const uint32_t* jtas = reinterpret_cast<const uint32_t*>(smem + Lo.jta);
-  const uint64_t* oslot = reinterpret_cast<const uint64_t*>(smem + Lo.oslot);
+  const uint64_t* oslot = tw64 + Lo.os / 2u;
+  const uint32_t* sj = tw + Lo.js[0];
+  const uint32_t sstr = njs + (uint32_t)kAcc + 32u;  // side table stride (fused_layout)
   const uint32_t nlr = l1 - l0;  // a power of two
   const uint32_t lsh = 31u - __clz(nlr), lmask = nlr - 1u;
   const uint32_t nit = (uint32_t)(u1 - u0) * nlr;
   uint64_t gbu[kFMaxOps];
   uint64_t gunit = ~0ull;
-  C pend[kFMaxOps];  // conversion sides: this thread's element of the next stage
-  __syncthreads();   // tables visible
+  C pend[kFMaxOps];  // conversion sides: this thread's element of the next stage (few live)
   // issue the copies of iteration `it` into buffer `buf` (shared byte address);
   // conversion sides load into `pend` (stored after the current stage's terms)
   auto issue = [&](uint32_t it, uint32_t buf) {
@@ -311,8 +297,8 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const char* in, char*
     for (uint32_t t = 0; t < n; ++t) {
       const OpIssue r = iss[t];
       const uint64_t base =
-          gbu[t] + (ltab_on ? ltab[Lo.lofs[t] + l] : fgather(l, d.ops[t].lrun, d.ops[t].n_lrun));
-      const uint32_t* kt = ktab + Lo.kofs[t];
+          gbu[t] + (ltab_on ? tw[Lo.lt[t] + l] : fgather(l, d.ops[t].lrun, d.ops[t].n_lrun));
+      const uint32_t* kt = tw + Lo.kt[t];
       if (r.mode == 3) {
         if (tid < r.n) pend[t] = ld_conv<C>(r.src, base, r.c64);
         continue;
@@ -392,11 +378,11 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const char* in, char*
       for (int a = 0; a < kAcc; ++a) ps[a] = C{0, 0};
       switch (nv) {
         case 0: ps[0] = C{1, 0}; break;
-        case 1: stage_terms_na<C, 1>(na, jts, cb, jtas, njs, ps); break;
-        case 2: stage_terms_na<C, 2>(na, jts, cb, jtas, njs, ps); break;
-        case 3: stage_terms_na<C, 3>(na, jts, cb, jtas, njs, ps); break;
-        case 4: stage_terms_na<C, 4>(na, jts, cb, jtas, njs, ps); break;
-        default: stage_terms_any<C>(nv, na, jts, cb, jtas, njs, ps); break;
+        case 1: stage_terms_na<C, 1>(na, sj, sstr, cb, njs, ps); break;
+        case 2: stage_terms_na<C, 2>(na, sj, sstr, cb, njs, ps); break;
+        case 3: stage_terms_na<C, 3>(na, sj, sstr, cb, njs, ps); break;
+        case 4: stage_terms_na<C, 4>(na, sj, sstr, cb, njs, ps); break;
+        default: stage_terms_any<C>(nv, na, sj, sstr, cb, njs, ps); break;
       }
       // sides constant over the in-thread bits multiply the stage's sums once
       C tc = C{1, 0};
@@ -445,7 +431,10 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const char* in, char*
 
 constexpr uint32_t kFHdrBytes = offsetof(FDesc, ops);
 
-__global__ void __launch_bounds__(256, 2) fused_kernel(const __grid_constant__ FLaunch L) {
+// complex64 math (most of the work): 3 CTAs per SM (80 registers);
+// complex128 math: 2
+template <typename C>
+__global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) fused_kernel(const __grid_constant__ FLaunch L) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ __align__(16) FDesc SD;
   pdl_trigger();
@@ -480,10 +469,7 @@ __global__ void __launch_bounds__(256, 2) fused_kernel(const __grid_constant__ F
     u0 = c << SD.upc_log2;
     u1 = min((uint64_t)SD.n_units, (uint64_t)(u0 + (1ull << SD.upc_log2)));
   }
-  if (SD.math_f32)
-    fused_body<float2>(SD, in, ws, u0, u1, l0, l1, split, fsm);
-  else
-    fused_body<double2>(SD, in, ws, u0, u1, l0, l1, split, fsm);
+  fused_body<C>(SD, L.tabs, in, ws, u0, u1, l0, l1, split, fsm);
 }
 
 // Split-K combine: one CTA per (split item, unit); thread e sums its output's
@@ -523,6 +509,61 @@ __global__ void __launch_bounds__(256) fused_combine_kernel(const __grid_constan
 
 uint32_t fused_smem_bytes(const FDesc& d) { return fused_layout(d).total; }
 
+static uint64_t hgather(uint64_t x, const uint32_t* runs, uint32_t n) {
+  uint64_t idx = 0;
+  for (uint32_t r = 0; r < n; ++r) {
+    const uint32_t w = runs[r];
+    const uint32_t s = w & 0xff, d = (w >> 8) & 0xff, l = (w >> 16) & 0xff;
+    idx |= ((x >> s) & ((1ull << l) - 1)) << d;
+  }
+  return idx;
+}
+
+void fused_build_tables(FDesc& d, std::vector<uint32_t>& blob) {
+  const FLayout L = fused_layout(d);
+  std::vector<uint32_t> w(L.words, 0u);
+  const uint32_t nthr = d.nq < kFThreadBits ? d.nq : kFThreadBits;
+  const uint32_t jn = d.nq - nthr, na = d.nto > nthr ? d.nto - nthr : 0u;
+  const uint32_t njs = 1u << (jn - na);
+  const uint32_t esz = d.math_f32 ? 8u : 16u;
+  auto put64 = [&](uint32_t at, uint64_t v) {
+    w[at] = (uint32_t)v;
+    w[at + 1] = (uint32_t)(v >> 32);
+  };
+  for (uint32_t a = 0; a < (uint32_t)kAcc; ++a)
+    put64(L.os + 2 * a, a < (1u << na) ? hgather((uint64_t)a << nthr, d.oqrun, d.n_oqrun) : 0ull);
+  for (uint32_t i = 0; i < 16; ++i) {
+    put64(L.on + 2 * i, hgather(i, d.oqrun, d.n_oqrun));
+    put64(L.on + 32 + 2 * i, hgather((uint64_t)i << 4, d.oqrun, d.n_oqrun));
+  }
+  for (uint32_t t = 0; t < d.n_ops; ++t) {
+    const FOp& o = d.ops[t];
+    const uint32_t sh = o.pairs ? 9u : 8u;
+    const uint32_t nk = o.nst > sh ? 1u << (o.nst - sh) : 1u;
+    for (uint32_t k = 0; k < nk; ++k) w[L.kt[t] + k] = (uint32_t)hgather((uint64_t)k << sh, o.srun, o.n_srun);
+    if (d.nl <= kFLTabBits)
+      for (uint32_t l = 0; l < (1u << d.nl); ++l) w[L.lt[t] + l] = (uint32_t)hgather(l, o.lrun, o.n_lrun);
+    const uint32_t m = o.pairs ? 2u : 1u;  // copy index of thread tid: tid (pairs: 2 tid)
+    for (uint32_t i = 0; i < 16; ++i) {
+      w[L.tn[t] + i] = (uint32_t)hgather(m * i, o.srun, o.n_srun);
+      w[L.tn[t] + 16 + i] = (uint32_t)hgather((uint64_t)m * (i << 4), o.srun, o.n_srun);
+    }
+  }
+  for (uint32_t s = 0; s < d.n_sides; ++s) {
+    const FSide& S = d.sides[s];
+    for (uint32_t js = 0; js < njs; ++js)
+      w[L.js[s] + js] = esz * (uint32_t)hgather((uint64_t)(js << na) << nthr, S.qrun, S.n_qrun);
+    for (uint32_t a = 0; a < (uint32_t)kAcc; ++a)
+      w[L.ja[s] + a] = a < (1u << na) ? esz * (uint32_t)hgather((uint64_t)a << nthr, S.qrun, S.n_qrun) : 0u;
+    for (uint32_t i = 0; i < 16; ++i) {
+      w[L.cn[s] + i] = esz * (uint32_t)hgather(i, S.qrun, S.n_qrun);
+      w[L.cn[s] + 16 + i] = esz * (uint32_t)hgather((uint64_t)i << 4, S.qrun, S.n_qrun);
+    }
+  }
+  d.tab_words = L.words;
+  blob.insert(blob.end(), w.begin(), w.end());
+}
+
 int launch_fused(const FLaunch& L, void* stream) {
   if (!L.n_items || !L.n_sets || !L.total_ctas) return QTN_OK;
   if (L.n_sets > 65535 || L.total_ctas > 0x7fffffffull) {
@@ -531,8 +572,11 @@ int launch_fused(const FLaunch& L, void* stream) {
   }
   static std::atomic<uint64_t> attr{0};
   if (needs_setup(attr)) {
-    cudaError_t e = cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(2 * kFBufBytes + 16384));
+    cudaError_t e = cudaFuncSetAttribute(fused_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(2 * kFBufBytes + 32768));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fused_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(2 * kFBufBytes + 32768));
     if (e != cudaSuccess) {
       set_error(std::string("fused_kernel attribute: ") + cudaGetErrorString(e));
       return QTN_ECUDA;
@@ -540,8 +584,10 @@ int launch_fused(const FLaunch& L, void* stream) {
     mark_setup(attr);
   }
   dim3 grid((uint32_t)L.total_ctas, L.n_sets);
-  cudaError_t e = launch_pdl<true>(fused_kernel, grid, dim3(256), L.smem_bytes,
-                                   reinterpret_cast<cudaStream_t>(stream), L);
+  cudaError_t e = L.f64 ? launch_pdl<true>(fused_kernel<double2>, grid, dim3(256), L.smem_bytes,
+                                           reinterpret_cast<cudaStream_t>(stream), L)
+                        : launch_pdl<true>(fused_kernel<float2>, grid, dim3(256), L.smem_bytes,
+                                           reinterpret_cast<cudaStream_t>(stream), L);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("fused_kernel launch: ") + cudaGetErrorString(e));

@@ -649,13 +649,22 @@ struct qtn_batch {
   std::vector<uint32_t> level_xstage;   // stage bytes (max over the level's items)
   // fused product chains per level (fused_kernel)
   qtn::FDesc* d_fdesc = nullptr;
+  uint32_t* d_ftab = nullptr;
   uint32_t* d_fitem_desc = nullptr;
   uint32_t* d_fitem_net = nullptr;
   uint64_t* d_fprefix = nullptr;
   uint64_t* d_cprefix = nullptr;        // split items: combine CTAs (units)
-  std::vector<uint32_t> level_fitem0;   // first fused item of each level (+ end)
-  std::vector<uint64_t> level_fprefix0, level_fctas, level_cctas;
-  std::vector<uint32_t> level_fsmem;
+  // a level's fused items in groups of one math type (one launch each):
+  // items [item0, item0 + n_items), CTA prefix at fprefix[prefix0 ..]
+  struct FGroup {
+    uint32_t item0, n_items;
+    uint64_t prefix0, ctas, cctas;
+    uint32_t smem;
+    uint8_t f64;
+  };
+  std::vector<FGroup> fgroups;
+  std::vector<uint32_t> level_fgroup0;  // first group of each level (+ end)
+  std::vector<uint64_t> level_fctas;    // fused CTAs of one set per level (0: none)
   // fused single-operand chains per level (reduce_kernel)
   qtn::RedDev* d_red = nullptr;
   uint32_t* d_red_prefix = nullptr;
@@ -665,9 +674,10 @@ struct qtn_batch {
   cudaStream_t cap_stream = nullptr;
   // concurrent launches of one HBM level (independent buckets): side
   // streams forked from / joined into the caller's stream with events
-  cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+  static constexpr int kSide = 7;  // up to 8 concurrent launches per level
+  cudaStream_t side[kSide] = {};
   cudaEvent_t ev_fork = nullptr;
-  cudaEvent_t ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_join[kSide] = {};
   // pinned staging of qtn_batch_energies_host
   double* pin = nullptr;
   size_t pin_doubles = 0;
@@ -682,7 +692,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
   if (!B) return QTN_OK;
   for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
   if (B->cap_stream) cudaStreamDestroy(B->cap_stream);
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < qtn_batch::kSide; ++k) {
     if (B->side[k]) cudaStreamDestroy(B->side[k]);
     if (B->ev_join[k]) cudaEventDestroy(B->ev_join[k]);
   }
@@ -698,7 +708,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix,
                   (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix,
                   (void*)B->d_fdesc, (void*)B->d_fitem_desc, (void*)B->d_fitem_net,
-                  (void*)B->d_fprefix, (void*)B->d_cprefix})
+                  (void*)B->d_fprefix, (void*)B->d_cprefix, (void*)B->d_ftab})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
   delete B;
@@ -787,35 +797,50 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     fdesc_base[h] = (uint32_t)fdescs.size();
     fdescs.insert(fdescs.end(), P->hbm_fdesc.begin(), P->hbm_fdesc.end());
   }
+  // host-built lookup tables of every fused descriptor (16-byte aligned each)
+  std::vector<uint32_t> ftabs;
+  for (auto& fd : fdescs) {
+    fd.tab_off = 4ull * ftabs.size();
+    qtn::fused_build_tables(fd, ftabs);
+    while (ftabs.size() & 3u) ftabs.push_back(0u);
+  }
   // fused product chains, level-major over all HBM networks
   std::vector<uint32_t> fitem_desc, fitem_net;
   std::vector<uint64_t> fprefix, cprefix;
   for (int32_t lev = 0; lev < max_lev; ++lev) {
-    B->level_fitem0.push_back((uint32_t)fitem_desc.size());
-    B->level_fprefix0.push_back(fprefix.size());
-    uint64_t acc = 0, cacc = 0;
-    uint32_t smem = 0;
-    fprefix.push_back(0);
-    cprefix.push_back(0);
-    for (int h = 0; h < B->n_hbm; ++h) {
-      const qtn_plan* P = plans[hidx[h]];
-      for (size_t f = 0; f < P->hbm_fdesc.size(); ++f) {
-        if (P->hbm_flevel[f] + hshift[h] != lev) continue;
-        const qtn::FDesc& fd = P->hbm_fdesc[f];
-        fitem_desc.push_back(fdesc_base[h] + (uint32_t)f);
-        fitem_net.push_back((uint32_t)h);
-        acc += fd.sk ? (fd.n_units << fd.sk) : (fd.n_units + (1ull << fd.upc_log2) - 1) >> fd.upc_log2;
-        fprefix.push_back(acc);
-        cacc += fd.sk ? fd.n_units : 0;
-        cprefix.push_back(cacc);
-        smem = std::max(smem, qtn::fused_smem_bytes(fd));
+    B->level_fgroup0.push_back((uint32_t)B->fgroups.size());
+    uint64_t lev_ctas = 0;
+    for (int mt = 0; mt < 2; ++mt) {  // complex64 math, then complex128 math
+      qtn_batch::FGroup g{};
+      g.item0 = (uint32_t)fitem_desc.size();
+      g.prefix0 = fprefix.size();
+      g.f64 = (uint8_t)mt;
+      uint64_t acc = 0, cacc = 0;
+      fprefix.push_back(0);
+      cprefix.push_back(0);
+      for (int h = 0; h < B->n_hbm; ++h) {
+        const qtn_plan* P = plans[hidx[h]];
+        for (size_t f = 0; f < P->hbm_fdesc.size(); ++f) {
+          const qtn::FDesc& fd = P->hbm_fdesc[f];
+          if (P->hbm_flevel[f] + hshift[h] != lev || (fd.math_f32 ? 0 : 1) != mt) continue;
+          fitem_desc.push_back(fdesc_base[h] + (uint32_t)f);
+          fitem_net.push_back((uint32_t)h);
+          acc += fd.sk ? (fd.n_units << fd.sk) : (fd.n_units + (1ull << fd.upc_log2) - 1) >> fd.upc_log2;
+          fprefix.push_back(acc);
+          cacc += fd.sk ? fd.n_units : 0;
+          cprefix.push_back(cacc);
+          g.smem = std::max(g.smem, qtn::fused_smem_bytes(fd));
+        }
       }
+      g.n_items = (uint32_t)fitem_desc.size() - g.item0;
+      g.ctas = acc;
+      g.cctas = cacc;
+      if (g.n_items) B->fgroups.push_back(g);
+      lev_ctas += acc;
     }
-    B->level_fctas.push_back(acc);
-    B->level_cctas.push_back(cacc);
-    B->level_fsmem.push_back(smem);
+    B->level_fctas.push_back(lev_ctas);
   }
-  B->level_fitem0.push_back((uint32_t)fitem_desc.size());
+  B->level_fgroup0.push_back((uint32_t)B->fgroups.size());
   // expanding buckets take the outer-product kernel (QTN_EXPAND=0: the
   // streaming kernel, for A/B measurements)
   const char* xv = getenv("QTN_EXPAND");
@@ -1022,6 +1047,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_level_sitem0, B->level_sitem0)) ||
       (rc = upload(&B->d_r1, r1items)) || (rc = upload(&B->d_r1prefix, r1prefix)) ||
       (rc = upload(&B->d_fdesc, fdescs)) || (rc = upload(&B->d_fitem_desc, fitem_desc)) ||
+      (rc = upload(&B->d_ftab, ftabs)) ||
       (rc = upload(&B->d_fitem_net, fitem_net)) || (rc = upload(&B->d_fprefix, fprefix)) ||
       (rc = upload(&B->d_cprefix, cprefix)) ||
       (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
@@ -1079,8 +1105,9 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
       }
       c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
-           (B->level_r1chunks[lev] ? 1 : 0) + (B->level_fctas[lev] ? 1 : 0) +
-           (B->level_cctas[lev] ? 1 : 0);
+           (B->level_r1chunks[lev] ? 1 : 0);
+      for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi)
+        c += 1 + (B->fgroups[gi].cctas ? 1 : 0);
     }
     c += 1;
   }
@@ -1415,7 +1442,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     const bool level_streams = !(lsv && lsv[0] == '0');
     if (level_streams && !B->ev_fork) {
       cudaError_t e = cudaEventCreateWithFlags(&B->ev_fork, cudaEventDisableTiming);
-      for (int k = 0; k < 4 && e == cudaSuccess; ++k) {
+      for (int k = 0; k < qtn_batch::kSide && e == cudaSuccess; ++k) {
         e = cudaStreamCreateWithFlags(&B->side[k], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&B->ev_join[k], cudaEventDisableTiming);
       }
@@ -1423,7 +1450,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     }
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
       // launches of this level, in issue order: reduce, small, trace, expand, stream
-      const int n_launch = (B->level_fctas[lev] ? 1 : 0) +
+      const int n_launch = (int)(B->level_fgroup0[lev + 1] - B->level_fgroup0[lev]) +
                            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) +
                            (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
                            (B->level_r1chunks[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
@@ -1458,17 +1485,20 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         lev += B->chain_len[lev] - 1;
         continue;
       }
-      if (B->level_fctas[lev]) {
+      for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi) {
+        const qtn_batch::FGroup& g = B->fgroups[gi];
         qtn::FLaunch F;
         std::memset(&F, 0, sizeof(F));
         F.descs = B->d_fdesc;
-        F.item_desc = B->d_fitem_desc + B->level_fitem0[lev];
-        F.item_net = B->d_fitem_net + B->level_fitem0[lev];
-        F.cta_prefix = B->d_fprefix + B->level_fprefix0[lev];
-        F.n_items = B->level_fitem0[lev + 1] - B->level_fitem0[lev];
+        F.tabs = B->d_ftab;
+        F.item_desc = B->d_fitem_desc + g.item0;
+        F.item_net = B->d_fitem_net + g.item0;
+        F.cta_prefix = B->d_fprefix + g.prefix0;
+        F.n_items = g.n_items;
         F.n_sets = (uint32_t)n_sets;
-        F.total_ctas = B->level_fctas[lev];
-        F.smem_bytes = B->level_fsmem[lev];
+        F.total_ctas = g.ctas;
+        F.smem_bytes = g.smem;
+        F.f64 = g.f64;
         F.in_base = L.in_base;
         F.in_set_stride = L.in_set_stride;
         F.net_in_off = L.net_in_off;
@@ -1477,9 +1507,9 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         F.net_ws_off = L.net_ws_off;
         void* fs = next_stream();
         if ((rc = qtn::launch_fused(F, fs))) return rc;
-        if (B->level_cctas[lev]) {  // split-K partial sums -> outputs, same stream
-          F.cta_prefix = B->d_cprefix + B->level_fprefix0[lev];
-          F.total_ctas = B->level_cctas[lev];
+        if (g.cctas) {  // split-K partial sums -> outputs, same stream
+          F.cta_prefix = B->d_cprefix + g.prefix0;
+          F.total_ctas = g.cctas;
           if ((rc = qtn::launch_fused_combine(F, fs))) return rc;
         }
       }

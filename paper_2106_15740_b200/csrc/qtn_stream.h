@@ -322,8 +322,10 @@ struct FDesc {
   // n_var: sides [0, n_var) depend on in-thread bits, the rest are per-thread
   // constants of a stage
   uint32_t buf_bytes;                 // bytes of one stage buffer
-  uint32_t pad2;
-  uint64_t part;                      // tagged: partial sums [unit][2^sk][2^nto] (math type), sk > 0
+  uint32_t tab_words;                 // host-built tables (fused_build_tables), 32-bit words
+  uint64_t part;                      // tagged: partial sums [unit][2^sk][2^nto] (complex128), sk > 0
+  uint64_t tab_off;                   // byte offset of the tables in the batch's table blob
+  uint64_t pad3;
   uint32_t ogrun[kFGRuns];            // grid index bits -> output bits
   uint32_t oqrun[kFQRuns];            // tile output bits (q's low nto) -> output bits
   FSide sides[kFMaxOps];
@@ -348,6 +350,7 @@ struct FChainSpec {
 bool encode_fused_desc(const FChainSpec& s, FDesc& d);
 struct FLaunch {
   const FDesc* descs;                 // device
+  const uint32_t* tabs;               // device: table blob (FDesc::tab_off)
   const uint32_t* item_desc;          // device: descriptor index per item
   const uint32_t* item_net;           // device: network index per item
   const uint64_t* cta_prefix;         // device: n_items + 1 (CTAs of one set)
@@ -355,6 +358,7 @@ struct FLaunch {
   uint32_t n_sets;
   uint64_t total_ctas;                // CTAs of one set
   uint32_t smem_bytes;                // dynamic shared memory (max over items)
+  uint32_t f64;                       // items compute in double (complex128 math); one type per launch
   const char* in_base;
   int64_t in_set_stride;
   const int64_t* net_in_off;
@@ -362,8 +366,11 @@ struct FLaunch {
   int64_t ws_set_stride;
   const int64_t* net_ws_off;
 };
-// dynamic shared memory of one descriptor: stage + per-op j tables
+// dynamic shared memory of one descriptor: stage buffers + tables
 uint32_t fused_smem_bytes(const FDesc& d);
+// the descriptor's lookup tables (pure function of d): appended to `blob`;
+// d.tab_words is set, d.tab_off is left to the caller
+void fused_build_tables(FDesc& d, std::vector<uint32_t>& blob);
 // bytes of the partial-sum block of a split descriptor (0 when sk == 0)
 inline uint64_t fused_part_bytes(const FDesc& d) {  // partial sums are complex128
   return d.sk ? (d.n_units << (d.sk + d.nto)) * 16ull : 0ull;
