@@ -89,15 +89,19 @@ __device__ __forceinline__ void expand_tile(const XDesc& d, XItemSmem& X, const 
   __syncthreads();
   // 1. B-side stage: entry ((x_b << c) | x_c) * 2 + v
   const uint32_t n_st = 2u << (h + c);
-  if (F32 && d.nB == 1 && X.c64[nA]) {
+  const bool async_stage = F32 && d.nB == 1 && X.c64[nA];
+  if (async_stage) {
     // one complex64 B operand (all of configs 3-4): the stage is a
-    // gather-copy; 4 independent loads per thread in flight
+    // gather-copy, issued as cp.async (every copy of the thread in flight at
+    // once, no register round trip); the A-side loads below overlap it
     const float2* src = reinterpret_cast<const float2*>(X.ptr[nA]) + X.base[nA];
     const uint32_t vs = X.vs[nA], cm = (1u << c) - 1u;
-    float2* dst = reinterpret_cast<float2*>(smem);
-#pragma unroll 4
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     for (uint32_t i = tid; i < n_st; i += 256)
-      dst[i] = __ldg(src + X.tb[0][i >> (c + 1)] + X.tc[0][(i >> 1) & cm] + ((i & 1u) << vs));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * i),
+                   "l"(src + X.tb[0][i >> (c + 1)] + X.tc[0][(i >> 1) & cm] + ((i & 1u) << vs))
+                   : "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
   } else
   for (uint32_t i = tid; i < n_st; i += 256) {
     const uint32_t v = i & 1u, xc = (i >> 1) & ((1u << c) - 1u), xb = i >> (c + 1);
@@ -125,6 +129,7 @@ __device__ __forceinline__ void expand_tile(const XDesc& d, XItemSmem& X, const 
     }
   }
   const uint32_t cx0 = ea[kXMaxOps] << 1, cx1 = eb[kXMaxOps] << 1;
+  if (async_stage) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   // x_b -> output offset by a masked increment (pdep of a counter)
   uint64_t bmask = 0;

@@ -1448,6 +1448,13 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       }
       if (e != cudaSuccess) return cuda_fail(e, "level streams");
     }
+    static int pdl_tiny_env = -1;
+    if (pdl_tiny_env < 0) {
+      const char* pv = getenv("QTN_PDL_TINY");
+      pdl_tiny_env = (pv && pv[0] == '0') ? 0 : 1;
+    }
+    const bool pdl_tiny = pdl_tiny_env == 1;
+    bool prev_single_small = false;  // the previous level was one small_kernel launch
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
       // launches of this level, in issue order: reduce, small, trace, expand, stream
       const int n_launch = (int)(B->level_fgroup0[lev + 1] - B->level_fgroup0[lev]) +
@@ -1483,6 +1490,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         if ((rc = qtn::launch_chain(Lc, B->d_level_sitem0 + lev, B->chain_len[lev], stream)))
           return rc;
         lev += B->chain_len[lev] - 1;
+        prev_single_small = false;
         continue;
       }
       for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi) {
@@ -1524,7 +1532,10 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         Ls.item_desc = B->d_sitem_desc + B->level_sitem0[lev];
         Ls.item_net = B->d_sitem_net + B->level_sitem0[lev];
         Ls.n_items = ns;
-        if ((rc = qtn::launch_small(Ls, B->level_smax_r[lev], next_stream()))) return rc;
+        // a level made of this one small launch after a level that was too:
+        // PDL (QTN_PDL_TINY=0 disables)
+        const bool tiny_pdl = pdl_tiny && n_launch == 1 && prev_single_small;
+        if ((rc = qtn::launch_small(Ls, B->level_smax_r[lev], next_stream(), tiny_pdl))) return rc;
       }
       if (B->level_r1chunks[lev] &&
           (rc = qtn::launch_trace(L, B->d_r1 + B->level_r1item0[lev],
@@ -1569,6 +1580,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         cudaEventRecord(B->ev_join[k - 1], B->side[k - 1]);
         cudaStreamWaitEvent(st, B->ev_join[k - 1], 0);
       }
+      prev_single_small = n_launch == 1 && ns != 0;
     }
     dim3 grid((B->n_hbm + 127) / 128, n_sets);
     cudaError_t e = launch_pdl<true>(

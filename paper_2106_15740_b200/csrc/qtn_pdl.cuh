@@ -32,6 +32,24 @@ inline bool pdl_enabled(bool hbm) {
   return hbm ? on_hbm == 1 : on == 1;
 }
 
+// force: PDL for this launch regardless of the executor default (chains of
+// tiny HBM levels, whose kernels stage only static data before pdl_wait)
+template <bool HBM = false, typename... KArgs, typename... Args>
+cudaError_t launch_pdl_if(bool force, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (force || pdl_enabled(HBM)) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <bool HBM = false, typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t st, Args&&... args) {

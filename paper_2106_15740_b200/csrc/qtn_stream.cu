@@ -98,7 +98,6 @@ constexpr uint32_t kSmallChunk = 1024;
 __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ StreamLaunch L,
                                                     uint32_t tpi_log2) {
   pdl_trigger();
-  pdl_wait();
   const uint32_t tpi = 1u << tpi_log2;
   const uint32_t item = blockIdx.x * (256u >> tpi_log2) + (threadIdx.x >> tpi_log2);
   if (item >= L.n_items) return;
@@ -120,6 +119,9 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
     else __syncwarp();
   }
   const uint8_t* dsc = reinterpret_cast<const uint8_t*>(slot);
+  // the item lookup and descriptor staging above read static data only: with
+  // PDL they overlap the previous level's tail; tensors are read after this
+  pdl_wait();
   const uint64_t n_all = 1ull << reinterpret_cast<const SHdr*>(dsc)->R;
   const uint64_t o0 = tpi == 256 ? (uint64_t)blockIdx.y * kSmallChunk : 0;
   if (o0 >= n_all) return;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
   small_eval<false>(dsc, b, o0 + lane, n_out, tpi);
 }
 
-int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream) {
+int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream, bool pdl) {
   if (L.n_items == 0 || L.n_sets == 0) return QTN_OK;
   // many items: a warp each; few items (tails of one network): CTAs of
   // kSmallChunk elements each
@@ -136,8 +138,8 @@ int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream) {
   const uint32_t chunks =
       tpi_log2 == 8u ? (uint32_t)(((1ull << max_r) + kSmallChunk - 1) / kSmallChunk) : 1u;
   dim3 grid((L.n_items + per_block - 1) / per_block, chunks, L.n_sets);
-  cudaError_t e = launch_pdl<true>(small_kernel, grid, dim3(256), 0,
-                             reinterpret_cast<cudaStream_t>(stream), L, tpi_log2);
+  cudaError_t e = launch_pdl_if<true>(pdl, small_kernel, grid, dim3(256), 0,
+                                      reinterpret_cast<cudaStream_t>(stream), L, tpi_log2);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("small_kernel launch: ") + cudaGetErrorString(e));

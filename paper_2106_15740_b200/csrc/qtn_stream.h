@@ -160,7 +160,9 @@ QTN_HD inline uint32_t red_chunk(uint32_t k) { return 512u * (k >= 3 ? 1u : (8u 
 // items: device array; prefix: device, n_items + 1 CTA prefix (chunks of red_chunk(k))
 int launch_reduce(const StreamLaunch& L, const RedDev* items, const uint32_t* prefix,
                   uint32_t n_items, uint32_t total_chunks, void* stream);
-int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream);
+// pdl: programmatic dependent launch (the kernel stages its descriptors
+// before waiting on the previous launch; used between tiny levels)
+int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream, bool pdl = false);
 // A run of consecutive tiny levels in one launch (a CTA cluster per set,
 // cluster barriers between levels).  L.item_desc/item_net: the small-item
 // lists; level_item0_dev[0..n_levels]: item range of each level (absolute
