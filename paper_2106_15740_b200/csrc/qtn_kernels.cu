@@ -1454,7 +1454,13 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       pdl_tiny_env = (pv && pv[0] == '0') ? 0 : 1;
     }
     const bool pdl_tiny = pdl_tiny_env == 1;
+    static int pdl_single_env = -1;
+    if (pdl_single_env < 0) {
+      const char* pv = getenv("QTN_PDL_SINGLE");
+      pdl_single_env = (pv && pv[0] == '1') ? 1 : 0;
+    }
     bool prev_single_small = false;  // the previous level was one small_kernel launch
+    bool prev_single = false;        // the previous level was one launch
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
       // launches of this level, in issue order: reduce, small, trace, expand, stream
       const int n_launch = (int)(B->level_fgroup0[lev + 1] - B->level_fgroup0[lev]) +
@@ -1463,6 +1469,9 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
                            (B->level_r1chunks[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
                            (B->level_tiles[lev] ? 1 : 0);
       const bool fork = level_streams && n_launch >= 2 && !B->chain_len[lev];
+      // one launch after one launch: PDL for it (QTN_PDL_SINGLE=1; tiny
+      // small_kernel levels take it by default below)
+      qtn::g_pdl_next = pdl_single_env == 1 && n_launch == 1 && prev_single;
       int slot = 0;  // launch k of the level goes to stream k (0: the caller's)
       auto next_stream = [&]() -> void* {
         if (!fork) return stream;
@@ -1491,6 +1500,8 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
           return rc;
         lev += B->chain_len[lev] - 1;
         prev_single_small = false;
+        prev_single = false;
+        qtn::g_pdl_next = false;
         continue;
       }
       for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi) {
@@ -1581,6 +1592,8 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         cudaStreamWaitEvent(st, B->ev_join[k - 1], 0);
       }
       prev_single_small = n_launch == 1 && ns != 0;
+      prev_single = n_launch == 1;
+      qtn::g_pdl_next = false;
     }
     dim3 grid((B->n_hbm + 127) / 128, n_sets);
     cudaError_t e = launch_pdl<true>(

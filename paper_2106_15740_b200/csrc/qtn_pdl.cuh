@@ -50,6 +50,11 @@ cudaError_t launch_pdl_if(bool force, void (*kernel)(KArgs...), dim3 grid, dim3 
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Set by the HBM executor around the launch of a level that is one kernel
+// following a level that was one kernel too (same stream, no fork/join):
+// such a launch takes PDL even where the executor default is off.
+inline thread_local bool g_pdl_next = false;
+
 template <bool HBM = false, typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t st, Args&&... args) {
@@ -62,7 +67,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled(HBM) ? 1 : 0;
+  cfg.numAttrs = (pdl_enabled(HBM) || (HBM && g_pdl_next)) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -1194,6 +1194,12 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       const bool fchain = fcv && fcv[0] == '1';
       const char* fmr = getenv("QTN_FCHAIN_MIN_R");
       const int fmin_r = fmr ? atoi(fmr) : 10;
+      // output-rank window of the fused chains (experiments: dot products
+      // into scalars vs GEMM-shaped chains)
+      const char* fmo = getenv("QTN_FCHAIN_MAX_OUT");
+      const int fmax_out = fmo ? atoi(fmo) : 64;
+      const char* fno = getenv("QTN_FCHAIN_MIN_OUT");
+      const int fmin_out = fno ? atoi(fno) : 0;
       for (int bi = 0; fchain && bi < nb; ++bi) {
         const auto& b = P->buckets[bi];
         if (b.ops.size() < 2 || chain_head[bi] >= 0 || b.rank + 1 < fmin_r) continue;
@@ -1207,6 +1213,10 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
           cur = c;
         }
         if (members.empty()) continue;
+        {
+          const int orank = P->tensors[P->buckets[members.back()].out].rank();
+          if (orank > fmax_out || orank < fmin_out) continue;
+        }
         // geometry check with placeholder tags (tags do not change it)
         FChainSpec fs;
         for (int32_t id : b.ops) {
