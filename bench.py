@@ -506,6 +506,11 @@ def roofline(plan, A, kt, key):
          "scope": "one evaluation of all angle sets: every executor launch (set-major: gate "
                   "rows + level launches + fold; HBM: level launches + fold), CUDA events on "
                   "the launching stream"}
+    ex = plan.exec_bytes_eval(A) if hasattr(plan, "exec_bytes_eval") else alg
+    if ex != alg:
+        # fused chains skip the union-size products: the bytes the kernels move
+        r["exec_bytes_per_launch"] = ex
+        r["exec_frac"] = ex / kt / 1e9 / peak
     if traffic:
         # DRAM bytes of the committed ncu capture of the same evaluation over
         # the live executor time: the fraction of HBM actually moving

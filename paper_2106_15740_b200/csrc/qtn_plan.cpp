@@ -1186,20 +1186,21 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     // Product chains (qtn_fused.cu): a bucket of >= 2 operands whose result
     // is then reduced by single-operand buckets is one fused contraction; the
     // union-size product and the chain's intermediates are never written
-    // (the GEMM census in DESIGN §3.7).  Opt-in
-    // (QTN_FUSE_CHAIN=1): measured at break-even with the bucket-by-bucket
-    // kernels.  QTN_FCHAIN_MIN_R: smallest union rank of the head.
+    // (the GEMM census in DESIGN §3.7).  On for chains
+    // whose head has union rank >= 10 and whose output rank is 1..15
+    // (measured: config 3 default 3.69 -> 3.17 ms; dot products
+    // into scalars and wide streaming chains run faster unfused);
+    // QTN_FUSE_CHAIN=0 disables, QTN_FCHAIN_MIN_R / _MIN_OUT / _MAX_OUT move
+    // the window.
     {
       const char* fcv = getenv("QTN_FUSE_CHAIN");
-      const bool fchain = fcv && fcv[0] == '1';
+      const bool fchain = !(fcv && fcv[0] == '0');
       const char* fmr = getenv("QTN_FCHAIN_MIN_R");
       const int fmin_r = fmr ? atoi(fmr) : 10;
-      // output-rank window of the fused chains (experiments: dot products
-      // into scalars vs GEMM-shaped chains)
       const char* fmo = getenv("QTN_FCHAIN_MAX_OUT");
-      const int fmax_out = fmo ? atoi(fmo) : 64;
+      const int fmax_out = fmo ? atoi(fmo) : 15;
       const char* fno = getenv("QTN_FCHAIN_MIN_OUT");
-      const int fmin_out = fno ? atoi(fno) : 0;
+      const int fmin_out = fno ? atoi(fno) : 1;
       for (int bi = 0; fchain && bi < nb; ++bi) {
         const auto& b = P->buckets[bi];
         if (b.ops.size() < 2 || chain_head[bi] >= 0 || b.rank + 1 < fmin_r) continue;

@@ -195,6 +195,18 @@ class EnergyPlan:
         big = float(sum(j.plan.alg_bytes for j in self.hbm_jobs))
         return n_sets * (big + small * (eb / 16.0 if eb else 1.0))
 
+    def exec_bytes_eval(self, n_sets: int) -> float:
+        """Bytes the HBM executor's kernels actually move for one evaluation
+        (fused chains read their head operands and write their tail output
+        only; everything else as alg_bytes_eval)."""
+        self._prepare()
+        if self._batch is None:
+            return 0.0
+        eb = self._batch.setmajor_elem_bytes(n_sets)
+        small = float(sum(j.plan.alg_bytes for j in self.smem_jobs))
+        big = float(sum(j.plan.exec_bytes for j in self.hbm_jobs))
+        return n_sets * (big + small * (eb / 16.0 if eb else 1.0))
+
     @property
     def flops_sum(self) -> float:
         return float(sum(j.report.flops_sum for j in self.jobs))

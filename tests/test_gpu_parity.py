@@ -677,13 +677,15 @@ def test_trace_kernel_every_eligible_bucket(golden, monkeypatch, dtype, tol):
 @pytest.mark.parametrize("min_r", ["0", "10"])
 def test_fused_product_chains(golden, monkeypatch, min_r):
     """Product buckets followed by their partial traces as one contraction
-    (fused_kernel, qtn_fused.cu; default on for head buckets of union rank
-    >= 10): equal to the unfused bucket-by-bucket evaluation
+    (fused_kernel, qtn_fused.cu; every chain here, whatever the default
+    window): equal to the unfused bucket-by-bucket evaluation
     (QTN_FUSE_CHAIN=0) and to the reference values, on config 3 default
     (GEMM-shaped chains, dot-product chains into scalars) and config 4 edge
     #16 (wide streaming chains), complex128 and complex64, at 1 and 3 angle
     sets.  min_r 0 also fuses the tiny chains of the first levels."""
     monkeypatch.setenv("QTN_FCHAIN_MIN_R", min_r)
+    monkeypatch.setenv("QTN_FCHAIN_MIN_OUT", "0")   # every chain: dot products,
+    monkeypatch.setenv("QTN_FCHAIN_MAX_OUT", "64")  # wide streaming chains too
     G = golden("config3.json")
     graph = Q.random_regular_graph(G["n"], 3, 0)
     params = Q.QaoaParams(G["gammas"], G["betas"])

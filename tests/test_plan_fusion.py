@@ -6,23 +6,27 @@ import paper_2106_15740_b200 as Q
 
 
 def test_fused_chain_census_and_levels(golden):
-    """Config 4 edge #1058: with QTN_FUSE_CHAIN=1 the product chains fuse
-    (fewer levels, fewer bytes moved than the reference's per-bucket bytes);
-    without it
-    (the default) leaves them off; the width invariant holds either way."""
+    """Config 4 edge #1058: with every chain fused (QTN_FCHAIN_MAX_OUT=64)
+    the product chains fuse (fewer levels, fewer bytes moved than the
+    reference's per-bucket bytes); with QTN_FUSE_CHAIN=0
+    none do; the width invariant holds either way."""
     import os
 
     G4 = golden("config4.json")
     g4 = Q.random_regular_graph(G4["n"], 3, 0)
-    os.environ["QTN_FUSE_CHAIN"] = "1"
+    os.environ["QTN_FCHAIN_MAX_OUT"] = "64"  # every chain, wide streaming ones too
     try:
         j = Q.plan_edges(g4, G4["p"], "zz+diagonal", [1058], dtype="complex64")[0]
     finally:
-        del os.environ["QTN_FUSE_CHAIN"]
+        del os.environ["QTN_FCHAIN_MAX_OUT"]
     assert j.plan.n_fused_chains >= 5
     assert j.plan.exec_bytes < 0.8 * j.plan.alg_bytes
     assert max(j.plan.step_ranks) == j.report.width
-    k = Q.plan_edges(g4, G4["p"], "zz+diagonal", [1058], dtype="complex64")[0]  # default: off
+    os.environ["QTN_FUSE_CHAIN"] = "0"
+    try:
+        k = Q.plan_edges(g4, G4["p"], "zz+diagonal", [1058], dtype="complex64")[0]
+    finally:
+        del os.environ["QTN_FUSE_CHAIN"]
     assert k.plan.n_fused_chains == 0
     assert k.plan.n_levels > j.plan.n_levels
     assert k.plan.alg_bytes == j.plan.alg_bytes
@@ -30,17 +34,14 @@ def test_fused_chain_census_and_levels(golden):
 
 
 def test_fused_chains_config3_default_every_network(golden):
-    """All 366 config-3 default networks compile with fused chains; the
-    deepest elimination tree gets much shorter (70 levels unfused)."""
+    """Config 3 default networks compile with fused chains by default (the
+    output-rank window 1..15); the deepest elimination tree gets shorter
+    (70 levels unfused) and the executed bytes drop."""
     import os
 
     G = golden("config3.json")
     graph = Q.random_regular_graph(G["n"], 3, 0)
-    os.environ["QTN_FUSE_CHAIN"] = "1"
-    try:
-        jobs = Q.plan_edges(graph, G["p"], "default", range(0, 366, 3), dtype="complex64")
-    finally:
-        del os.environ["QTN_FUSE_CHAIN"]
+    jobs = Q.plan_edges(graph, G["p"], "default", range(0, 366, 3), dtype="complex64")  # default window
     assert sum(j.plan.n_fused_chains for j in jobs) > 100
-    assert max(j.plan.n_levels for j in jobs) <= 40
-    assert sum(j.plan.exec_bytes for j in jobs) < 0.7 * sum(j.plan.alg_bytes for j in jobs)
+    assert max(j.plan.n_levels for j in jobs) <= 55
+    assert sum(j.plan.exec_bytes for j in jobs) < 0.8 * sum(j.plan.alg_bytes for j in jobs)
