@@ -496,8 +496,16 @@ __global__ void __launch_bounds__(256) fused_combine_kernel(const __grid_constan
   for (uint32_t e = threadIdx.x; e < (1u << nto); e += 256u) {
     const uint64_t o = og | fgather(e, d.oqrun, d.n_oqrun);
     const double2* p = part + ((unit << (sk + nto)) | e);
-    double2 r = p[0];
-    for (uint32_t s = 1; s < (1u << sk); ++s) r = cadd(r, p[(uint64_t)s << nto]);
+    // 4 partial sums in flight (sk >= 1 when split); combined in split order
+    const uint32_t ns = 1u << sk;
+    double2 r = make_double2(0.0, 0.0);
+    uint32_t s = 0;
+    for (; s + 4u <= ns; s += 4u) {
+      const double2 a = __ldcg(p + ((uint64_t)s << nto)), b = __ldcg(p + ((uint64_t)(s + 1) << nto));
+      const double2 c = __ldcg(p + ((uint64_t)(s + 2) << nto)), e2 = __ldcg(p + ((uint64_t)(s + 3) << nto));
+      r = cadd(cadd(cadd(cadd(r, a), b), c), e2);
+    }
+    for (; s < ns; ++s) r = cadd(r, __ldcg(p + ((uint64_t)s << nto)));
     if (d.out_c64)
       reinterpret_cast<float2*>(outp)[o] = make_float2((float)r.x, (float)r.y);
     else
