@@ -671,6 +671,9 @@ struct qtn_batch {
   std::vector<uint32_t> level_red0, level_rprefix0, level_rchunks;
   // captured evaluations (qtn_batch_execute_angles)
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  // captured host-facing calls (qtn_batch_energies_host): angles H2D from the
+  // pinned staging, the evaluation, the energy reduction and the D2H
+  std::map<std::vector<uintptr_t>, cudaGraphExec_t> egraphs;
   cudaStream_t cap_stream = nullptr;
   // concurrent launches of one HBM level (independent buckets): side
   // streams forked from / joined into the caller's stream with events
@@ -691,6 +694,7 @@ struct qtn_batch {
 extern "C" int qtn_batch_destroy(qtn_batch* B) {
   if (!B) return QTN_OK;
   for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : B->egraphs) cudaGraphExecDestroy(kv.second);
   if (B->cap_stream) cudaStreamDestroy(B->cap_stream);
   for (int k = 0; k < qtn_batch::kSide; ++k) {
     if (B->side[k]) cudaStreamDestroy(B->side[k]);
@@ -1244,6 +1248,8 @@ extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
   // below: drop them before replacing the device program
   for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
   B->graphs.clear();
+  for (auto& kv : B->egraphs) cudaGraphExecDestroy(kv.second);
+  B->egraphs.clear();
   // HBM networks: recipes relocated into the batch input layout
   std::vector<qtn_tensor_recipe> hrec;
   for (int i = 0; i < B->n; ++i) {
@@ -1666,16 +1672,55 @@ extern "C" int qtn_batch_energies_host(qtn_batch* B, const double* angles_host, 
     B->pin_doubles = need;
   }
   std::memcpy(B->pin, angles_host, na * sizeof(double));
-  cudaError_t e = cudaMemcpyAsync(angles_dev, B->pin, na * sizeof(double), cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_fail(e, "angles H2D");
-  int rc = qtn_batch_execute_angles(B, angles_dev, n_angles, n_sets, inputs_scratch, workspace,
-                                    results, stream);
-  if (rc) return rc;
-  if ((rc = qtn_energy_reduce(results, weights_dev, B->n, n_sets, energies_dev, nullptr, stream)))
-    return rc;
   double* eh = B->pin + na;
-  e = cudaMemcpyAsync(eh, energies_dev, (size_t)n_sets * sizeof(double), cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return cuda_fail(e, "energies D2H");
+  // the whole call as one graph: H2D, evaluation, reduction, D2H (QTN_GRAPHS=0:
+  // stream-ordered calls)
+  auto body = [&](cudaStream_t s2) -> int {
+    cudaError_t e2 = cudaMemcpyAsync(angles_dev, B->pin, na * sizeof(double), cudaMemcpyHostToDevice, s2);
+    if (e2 != cudaSuccess) return cuda_fail(e2, "angles H2D");
+    int rc2 = execute_angles_direct(B, angles_dev, n_angles, n_sets, inputs_scratch, workspace, results, s2);
+    if (rc2) return rc2;
+    if ((rc2 = qtn_energy_reduce(results, weights_dev, B->n, n_sets, energies_dev, nullptr, s2))) return rc2;
+    e2 = cudaMemcpyAsync(eh, energies_dev, (size_t)n_sets * sizeof(double), cudaMemcpyDeviceToHost, s2);
+    if (e2 != cudaSuccess) return cuda_fail(e2, "energies D2H");
+    return QTN_OK;
+  };
+  const char* gv = getenv("QTN_GRAPHS");
+  cudaError_t e = cudaSuccess;
+  if (gv && gv[0] == '0') {
+    int rc = body(st);
+    if (rc) return rc;
+  } else {
+    const std::vector<uintptr_t> key{(uintptr_t)angles_dev, (uintptr_t)inputs_scratch, (uintptr_t)workspace,
+                                     (uintptr_t)results, (uintptr_t)weights_dev, (uintptr_t)energies_dev,
+                                     (uintptr_t)B->pin, (uintptr_t)n_angles, (uintptr_t)n_sets};
+    auto it = B->egraphs.find(key);
+    if (it == B->egraphs.end()) {
+      if (B->egraphs.size() >= 16) {
+        for (auto& kv : B->egraphs) cudaGraphExecDestroy(kv.second);
+        B->egraphs.clear();
+      }
+      if (!B->cap_stream && cudaStreamCreateWithFlags(&B->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return cuda_fail(cudaGetLastError(), "capture stream");
+      cudaGraph_t g = nullptr;
+      e = cudaStreamBeginCapture(B->cap_stream, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return cuda_fail(e, "graph capture begin");
+      const int rc = body(B->cap_stream);
+      e = cudaStreamEndCapture(B->cap_stream, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "graph capture end");
+      cudaGraphExec_t ex = nullptr;
+      e = cudaGraphInstantiate(&ex, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
+      it = B->egraphs.emplace(key, ex).first;
+    }
+    e = cudaGraphLaunch(it->second, st);
+    if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+  }
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "energies sync");
   std::memcpy(energies_host, eh, (size_t)n_sets * sizeof(double));
