@@ -173,34 +173,41 @@ __host__ __device__ inline FLayout fused_layout(const FDesc& d) {
 // the product of one staged entry per varying side (32-bit shared addresses:
 // thread base + js part + slot part).
 // (side tables: sj[s * sstr + js] = summed part, sj[s * sstr + njs + a] = slot part)
-template <typename C, int NS, int NA>
+// G0: side 0 is streamed from global memory (element offsets, base g0)
+template <typename C, int NS, int NA, bool G0>
 __device__ __forceinline__ void stage_terms(const uint32_t* sj, uint32_t sstr, const uint32_t* cb,
-                                            uint32_t njs, C (&ps)[kAcc]) {
+                                            uint32_t njs, C (&ps)[kAcc], const C* g0) {
   uint32_t jta[NS][1 << NA];
 #pragma unroll
   for (int s = 0; s < NS; ++s)
 #pragma unroll
     for (int a = 0; a < (1 << NA); ++a) jta[s][a] = sj[s * sstr + njs + a];
+#pragma unroll 2
   for (uint32_t js = 0; js < njs; ++js) {
     uint32_t off[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) off[s] = cb[s] + sj[s * sstr + js];
+    C v0[1 << NA];
+#pragma unroll
+    for (int a = 0; a < (1 << NA); ++a)  // the streamed loads of all slots first
+      v0[a] = G0 ? __ldg(g0 + off[0] + jta[0][a]) : lds_c(off[0] + jta[0][a], (C*)nullptr);
 #pragma unroll
     for (int a = 0; a < (1 << NA); ++a) {
-      C p = lds_c(off[0] + jta[0][a], (C*)nullptr);
+      C p = v0[a];
 #pragma unroll
       for (int s = 1; s < NS; ++s) p = cm(p, lds_c(off[s] + jta[s][a], (C*)nullptr));
       ps[a] = cadd(ps[a], p);
     }
   }
 }
-template <typename C, int NS>
+template <typename C, int NS, bool G0>
 __device__ __forceinline__ void stage_terms_na(uint32_t na, const uint32_t* sj, uint32_t sstr,
-                                               const uint32_t* cb, uint32_t njs, C (&ps)[kAcc]) {
+                                               const uint32_t* cb, uint32_t njs, C (&ps)[kAcc],
+                                               const C* g0) {
   switch (na) {
-    case 0: stage_terms<C, NS, 0>(sj, sstr, cb, njs, ps); break;
-    case 1: stage_terms<C, NS, 1>(sj, sstr, cb, njs, ps); break;
-    default: stage_terms<C, NS, 2>(sj, sstr, cb, njs, ps); break;
+    case 0: stage_terms<C, NS, 0, G0>(sj, sstr, cb, njs, ps, g0); break;
+    case 1: stage_terms<C, NS, 1, G0>(sj, sstr, cb, njs, ps, g0); break;
+    default: stage_terms<C, NS, 2, G0>(sj, sstr, cb, njs, ps, g0); break;
   }
 }
 // more than 4 varying sides: slot offsets from shared memory
@@ -248,7 +255,11 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
       OpIssue r;
       r.src = fresolve(o.ptr, in, ws);
       r.c64 = o.c64;
-      if (S.kind == kFSideConv) {
+      if (S.kind == kFSideStream) {
+        r.mode = 4;  // read by the terms from global memory: no copies
+        r.dst = 0;
+        r.n = 0;
+      } else if (S.kind == kFSideConv) {
         r.mode = 3;
         r.dst = S.st_off;
         r.n = (uint16_t)(1u << o.nst);
@@ -267,8 +278,9 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
   for (uint32_t t = 0; t < kFMaxOps; ++t) {
     thr[t] = t < n ? tw[Lo.tn[t] + tlo] + tw[Lo.tn[t] + 16u + thi] : 0u;
     // shared byte address of the thread's entry of side t in buffer 0
-    cth[t] = t < ns ? sbase + d.sides[t].st_off + (active ? tw[Lo.cn[t] + tlo] + tw[Lo.cn[t] + 16u + thi] : 0u)
-                    : 0u;
+    // (streamed side 0: the thread's element offset in the operand)
+    const uint32_t tpart = active && t < ns ? tw[Lo.cn[t] + tlo] + tw[Lo.cn[t] + 16u + thi] : 0u;
+    cth[t] = t < ns ? (d.sides[t].kind == kFSideStream ? tpart : sbase + d.sides[t].st_off + tpart) : 0u;
   }
   char* outp = const_cast<char*>(fresolve(d.out, in, ws));
   double2* part = d.sk ? reinterpret_cast<double2*>(const_cast<char*>(fresolve(d.part, in, ws))) : nullptr;
@@ -299,6 +311,7 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
       const uint64_t base =
           gbu[t] + (ltab_on ? tw[Lo.lt[t] + l] : fgather(l, d.ops[t].lrun, d.ops[t].n_lrun));
       const uint32_t* kt = tw + Lo.kt[t];
+      if (r.mode == 4) continue;  // streamed side: no copies
       if (r.mode == 3) {
         if (tid < r.n) pend[t] = ld_conv<C>(r.src, base, r.c64);
         continue;
@@ -350,6 +363,9 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
       }
     }
   };
+  // a streamed side 0 (kFSideStream) is read by the terms from global memory
+  const bool stream0 = ns > 0 && d.sides[0].kind == kFSideStream && nv >= 1 && nv <= 4;
+  uint64_t sunit = ~0ull, sgb = 0;
   issue(0, sbase);
   store_pend(0);
   double2 acc[kAcc];
@@ -376,13 +392,33 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
       C ps[kAcc];
 #pragma unroll
       for (int a = 0; a < kAcc; ++a) ps[a] = C{0, 0};
-      switch (nv) {
-        case 0: ps[0] = C{1, 0}; break;
-        case 1: stage_terms_na<C, 1>(na, sj, sstr, cb, njs, ps); break;
-        case 2: stage_terms_na<C, 2>(na, sj, sstr, cb, njs, ps); break;
-        case 3: stage_terms_na<C, 3>(na, sj, sstr, cb, njs, ps); break;
-        case 4: stage_terms_na<C, 4>(na, sj, sstr, cb, njs, ps); break;
-        default: stage_terms_any<C>(nv, na, sj, sstr, cb, njs, ps); break;
+      if (stream0) {
+        // side 0 from global memory at this iteration's operand base
+        cb[0] = cth[0];
+        const uint64_t unit = u0 + (it >> lsh);
+        const uint32_t l = l0 + (it & lmask);
+        const uint32_t t0 = d.sides[0].first_op;
+        if (unit != sunit) {
+          sgb = fgather_ol(unit, d.ops[t0].grun, d.ops[t0].n_grun);
+          sunit = unit;
+        }
+        const C* g0 = reinterpret_cast<const C*>(iss[t0].src) + sgb +
+                      (ltab_on ? tw[Lo.lt[t0] + l] : fgather(l, d.ops[t0].lrun, d.ops[t0].n_lrun));
+        switch (nv) {
+          case 1: stage_terms_na<C, 1, true>(na, sj, sstr, cb, njs, ps, g0); break;
+          case 2: stage_terms_na<C, 2, true>(na, sj, sstr, cb, njs, ps, g0); break;
+          case 3: stage_terms_na<C, 3, true>(na, sj, sstr, cb, njs, ps, g0); break;
+          default: stage_terms_na<C, 4, true>(na, sj, sstr, cb, njs, ps, g0); break;
+        }
+      } else {
+        switch (nv) {
+          case 0: ps[0] = C{1, 0}; break;
+          case 1: stage_terms_na<C, 1, false>(na, sj, sstr, cb, njs, ps, nullptr); break;
+          case 2: stage_terms_na<C, 2, false>(na, sj, sstr, cb, njs, ps, nullptr); break;
+          case 3: stage_terms_na<C, 3, false>(na, sj, sstr, cb, njs, ps, nullptr); break;
+          case 4: stage_terms_na<C, 4, false>(na, sj, sstr, cb, njs, ps, nullptr); break;
+          default: stage_terms_any<C>(nv, na, sj, sstr, cb, njs, ps); break;
+        }
       }
       // sides constant over the in-thread bits multiply the stage's sums once
       C tc = C{1, 0};
@@ -559,13 +595,18 @@ void fused_build_tables(FDesc& d, std::vector<uint32_t>& blob) {
   }
   for (uint32_t s = 0; s < d.n_sides; ++s) {
     const FSide& S = d.sides[s];
-    for (uint32_t js = 0; js < njs; ++js)
-      w[L.js[s] + js] = esz * (uint32_t)hgather((uint64_t)(js << na) << nthr, S.qrun, S.n_qrun);
-    for (uint32_t a = 0; a < (uint32_t)kAcc; ++a)
-      w[L.ja[s] + a] = a < (1u << na) ? esz * (uint32_t)hgather((uint64_t)a << nthr, S.qrun, S.n_qrun) : 0u;
+    // offset of tile index q: shared byte offset of the side's compact
+    // entry, or (streamed side) the element offset in the operand
+    const FOp& o0 = d.ops[S.first_op];
+    auto off = [&](uint64_t q) -> uint32_t {
+      const uint64_t c = hgather(q, S.qrun, S.n_qrun);
+      return S.kind == kFSideStream ? (uint32_t)hgather(c, o0.srun, o0.n_srun) : esz * (uint32_t)c;
+    };
+    for (uint32_t js = 0; js < njs; ++js) w[L.js[s] + js] = off((uint64_t)(js << na) << nthr);
+    for (uint32_t a = 0; a < (uint32_t)kAcc; ++a) w[L.ja[s] + a] = a < (1u << na) ? off((uint64_t)a << nthr) : 0u;
     for (uint32_t i = 0; i < 16; ++i) {
-      w[L.cn[s] + i] = esz * (uint32_t)hgather(i, S.qrun, S.n_qrun);
-      w[L.cn[s] + 16 + i] = esz * (uint32_t)hgather((uint64_t)i << 4, S.qrun, S.n_qrun);
+      w[L.cn[s] + i] = off(i);
+      w[L.cn[s] + 16 + i] = off((uint64_t)i << 4);
     }
   }
   d.tab_words = L.words;

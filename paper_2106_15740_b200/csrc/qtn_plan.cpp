@@ -643,7 +643,18 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
     }
     return sides;
   };
+  static int stream_env = -1;
+  if (stream_env < 0) {
+    // streamed sides are opt-in (QTN_FSTREAM=1): measured slower than the
+    // cp.async stage (config 3 default 3.18 -> 3.50 ms, config 4 with every
+    // chain fused 1.32 -> 1.60 ms)
+    const char* sv = getenv("QTN_FSTREAM");
+    stream_env = (sv && sv[0] == '1') ? 1 : 0;
+  }
   auto side_kind = [&](const std::vector<int>& sd, uint64_t tl) -> uint8_t {
+    if (stream_env && sd.size() == 1 && esz(sd[0]) == mesz && (dep[sd[0]] & tl) == tl &&
+        __builtin_popcountll(tl) > kFThreadBits)
+      return kFSideStream;
     if (sd.size() == 1 && esz(sd[0]) == mesz) return kFSideRaw;
     if (sd.size() == 1 && __builtin_popcountll(dep[sd[0]] & tl) <= kFThreadBits) return kFSideConv;
     return kFSideProd;
@@ -652,8 +663,16 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
   // + math-type regions of the conversion and product sides
   auto buf_bytes = [&](uint64_t tl, const std::vector<std::vector<int>>& sides) {
     uint64_t b = 0;
+    bool streamed = false;  // at most one streamed side (the kernel reads side 0 from global)
     for (const auto& sd : sides) {
-      const uint8_t kd = side_kind(sd, tl);
+      uint8_t kd = side_kind(sd, tl);
+      if (kd == kFSideStream) {
+        if (!streamed) {
+          streamed = true;
+          continue;
+        }
+        kd = kFSideRaw;
+      }
       if (kd != kFSideConv)
         for (int t : sd) b += ((uint64_t)std::max(2u, 1u << __builtin_popcountll(dep[t] & tl)) * esz(t) + 15) & ~15ull;
       if (kd != kFSideRaw)
@@ -717,6 +736,14 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
                         [&](const std::vector<int>& sd) { return (dep[sd[0]] & inthr) != 0; });
   int n_var = 0;
   for (const auto& sd : sides) n_var += (dep[sd[0]] & inthr) != 0 ? 1 : 0;
+  // the streamed side (if any) goes first: the kernel reads side 0 from global
+  {
+    int first_stream = -1;
+    for (size_t si = 0; si < sides.size() && first_stream < 0; ++si)
+      if (side_kind(sides[si], tile) == kFSideStream && (dep[sides[si][0]] & inthr) != 0)
+        first_stream = (int)si;
+    if (first_stream > 0) std::rotate(sides.begin(), sides.begin() + first_stream, sides.begin() + first_stream + 1);
+  }
   // raw regions first (16-byte aligned), then the non-raw side regions
   uint32_t off = 0;
   int k = 0;
@@ -736,6 +763,7 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
     S.first_op = (uint8_t)slot[sides[si][0]];
     S.n_ops = (uint8_t)sides[si].size();
     S.kind = side_kind(sides[si], tile);
+    if (S.kind == kFSideStream && si != 0) S.kind = kFSideRaw;  // only side 0 streams
     S.tconst = (sdep & inthr) == 0 ? 1 : 0;
     for (int t : sides[si]) {
       FOp& o = d.ops[slot[t]];
@@ -746,7 +774,7 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
       for (int i = 0; i < nq; ++i)
         if ((dep[t] >> qb[i]) & 1) oc.push_back(i);
       o.nst = (uint8_t)oc.size();
-      if (S.kind != kFSideConv) {  // a conversion side has no raw region
+      if (S.kind != kFSideConv && S.kind != kFSideStream) {  // no raw region: conversion, streamed
         o.raw_off = off;
         off += std::max(2u, 1u << oc.size()) * esz(t);
         off = (off + 15u) & ~15u;
@@ -770,7 +798,9 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
   }
   for (size_t si = 0; si < sides.size(); ++si) {
     FSide& S = d.sides[si];
-    if (S.kind == kFSideRaw) {
+    if (S.kind == kFSideStream) {
+      S.st_off = 0;
+    } else if (S.kind == kFSideRaw) {
       S.st_off = d.ops[S.first_op].raw_off;
     } else {
       S.st_off = off;
@@ -813,8 +843,8 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
   d.upc_log2 = (uint8_t)upc;
   d.sk = (uint8_t)sk;
   if (getenv("QTN_DEBUG_DESC") && R + K >= atoi(getenv("QTN_DEBUG_DESC")))
-    fprintf(stderr, "fdesc R=%d K=%d ops=%d sides=%d nq=%d nto=%d ng=%d nl=%d buf=%u upc=%d sk=%d fin=%d\n", R,
-            K, n, (int)sides.size(), nq, nto, ng, nl, off, upc, sk, (int)d.has_finish);
+    fprintf(stderr, "fdesc R=%d K=%d ops=%d sides=%d nq=%d nto=%d ng=%d nl=%d buf=%u upc=%d sk=%d fin=%d s0=%d\n", R,
+            K, n, (int)sides.size(), nq, nto, ng, nl, off, upc, sk, (int)d.has_finish, (int)d.sides[0].kind);
   return true;
 }
 

@@ -307,7 +307,10 @@ struct FOp {
 // operand converted to the math type through a register (<= 256 entries) /
 // product of several operands (or a large conversion) formed by a shared
 // memory pass from their raw regions
-constexpr uint8_t kFSideRaw = 0, kFSideConv = 1, kFSideProd = 2;
+// kFSideStream: a raw single-operand side that depends on every tile bit
+// (each entry feeds exactly one term): not staged, its terms read it from
+// global memory (coalesced), so the stage holds only reused operands
+constexpr uint8_t kFSideRaw = 0, kFSideConv = 1, kFSideProd = 2, kFSideStream = 3;
 struct FSide {
   uint8_t nst, n_qrun, kind, first_op, n_ops, tconst, pad[2];  // tconst: no in-thread bits
   uint32_t st_off;                    // byte offset of the side's region in a stage buffer
