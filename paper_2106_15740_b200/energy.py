@@ -256,6 +256,17 @@ class EnergyPlan:
             dev = self._device
             need_inputs = self._batch is not None and ((not self.fused) or self._batch.has_hbm)
             ws_bytes = self._batch.workspace_bytes(n_sets) if self._batch is not None else 0
+            # device-memory fit check: the evaluation's buffers
+            # against what the device has free, before any allocation
+            need = (16 * n_sets * self.set_elems if need_inputs else 0) + ws_bytes
+            if dev.type == "cuda" and need > 0:
+                free, total = t.cuda.mem_get_info(dev)
+                if need > free:
+                    raise MemoryError(
+                        f"an evaluation of {n_sets} angle set(s) needs {need / 2**30:.2f} GiB of "
+                        f"device memory (inputs + intermediate arena); {free / 2**30:.2f} GiB of "
+                        f"{total / 2**30:.2f} GiB are free: use fewer angle sets per call or slice "
+                        f"the networks (slice_k)")
             self._bufs[n_sets] = dict(
                 inputs=t.zeros(n_sets * self.set_elems if need_inputs else 2, dtype=t.complex128,
                                device=dev),

@@ -716,3 +716,46 @@ def test_fused_product_chains(golden, monkeypatch, min_r):
         assert abs(out["1", dt][1] - rec4) <= tol * abs(rec4)
         assert np.allclose(out["1", dt][2], out["0", dt][2], rtol=tol, atol=tol)
 
+
+
+def test_device_memory_fit_check():
+    """an evaluation whose buffers exceed the free device memory
+    raises MemoryError before allocating (config 4 edge #16 at 2^20 angle
+    sets needs ~100 TB of arena)."""
+    g4 = Q.random_regular_graph(1000, 3, 0)
+    plan = Q.EnergyPlan(g4, 5, "zz+diagonal", dtype="complex64", edge_ids=[16])
+    with pytest.raises(MemoryError):
+        plan.energies(np.zeros((1 << 20, 10)))
+    # and a normal call still works afterwards
+    z = plan.energies(np.zeros((1, 10)))
+    assert np.isfinite(z).all()
+
+
+def test_repeatable_bitwise_results():
+    """Every kernel path is deterministic (fixed reduction orders, no atomics
+    on data): repeated evaluations of HBM-executor networks (config 3 default
+    edges 0-7: small, stream, trace, expand, reduce and fused-chain kernels
+    with split-K; config 4 edge #16) and of the set-major executor give
+    bit-identical energies — a data race in a cp.async / mbarrier pipeline
+    would show up as run-to-run differences.  (compute-sanitizer is not
+    available on the build's GPU pool.)"""
+    import os
+
+    os.environ["QTN_GRAPHS"] = "0"
+    try:
+        g3 = Q.random_regular_graph(244, 3, 0)
+        p3 = Q.EnergyPlan(g3, 3, "default", dtype="complex64", edge_ids=list(range(8)))
+        g4 = Q.random_regular_graph(1000, 3, 0)
+        p4 = Q.EnergyPlan(g4, 5, "zz+diagonal", dtype="complex64", edge_ids=[16])
+        g2 = Q.random_regular_graph(100, 3, 0)
+        p2 = Q.EnergyPlan(g2, 2, "zz+diagonal", dtype="complex64")
+        rng = np.random.default_rng(11)
+        a3, a4, a2 = (rng.uniform(0, math.pi, (2, 6)), rng.uniform(0, math.pi, (1, 10)),
+                      rng.uniform(0, math.pi, (256, 4)))
+        ref = (p3.energies(a3), p4.energies(a4), p2.energies(a2))
+        for _ in range(4):
+            got = (p3.energies(a3), p4.energies(a4), p2.energies(a2))
+            for x, y in zip(got, ref):
+                assert np.array_equal(x, y)
+    finally:
+        del os.environ["QTN_GRAPHS"]
