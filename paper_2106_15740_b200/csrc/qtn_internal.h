@@ -229,6 +229,12 @@ struct qtn_plan {
   std::vector<qtn::XDesc> hbm_xdesc;
   std::vector<int32_t> hbm_r1idx;        // single-operand (trace) record per bucket, or -1
   std::vector<qtn::R1Dev> hbm_r1;        // net = 0 here; set per batch
+  struct SubRec {                        // tiny subtree (qtn_stream.h SubItem)
+    int32_t level;
+    uint32_t first, count, smem;         // member descriptors hbm_sub_desc[first .. +count)
+  };
+  std::vector<SubRec> hbm_sub;
+  std::vector<uint64_t> hbm_sub_desc;    // member descriptor byte offsets (hbm_desc), in order
   std::vector<qtn::FDesc> hbm_fdesc;     // fused product chains (qtn_fused.cu)
   std::vector<int32_t> hbm_flevel;       // their levels
   int32_t n_levels = 0;

@@ -665,6 +665,11 @@ struct qtn_batch {
   std::vector<FGroup> fgroups;
   std::vector<uint32_t> level_fgroup0;  // first group of each level (+ end)
   std::vector<uint64_t> level_fctas;    // fused CTAs of one set per level (0: none)
+  // tiny subtrees per level (subtree_kernel)
+  qtn::SubItem* d_sub_items = nullptr;
+  uint64_t* d_sub_desc = nullptr;
+  std::vector<uint32_t> level_sub0;     // first subtree item of each level (+ end)
+  std::vector<uint32_t> level_sub_smem;
   // fused single-operand chains per level (reduce_kernel)
   qtn::RedDev* d_red = nullptr;
   uint32_t* d_red_prefix = nullptr;
@@ -712,7 +717,8 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix,
                   (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix,
                   (void*)B->d_fdesc, (void*)B->d_fitem_desc, (void*)B->d_fitem_net,
-                  (void*)B->d_fprefix, (void*)B->d_cprefix, (void*)B->d_ftab})
+                  (void*)B->d_fprefix, (void*)B->d_cprefix, (void*)B->d_ftab,
+                  (void*)B->d_sub_items, (void*)B->d_sub_desc})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
   delete B;
@@ -808,6 +814,29 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     qtn::fused_build_tables(fd, ftabs);
     while (ftabs.size() & 3u) ftabs.push_back(0u);
   }
+  // tiny subtrees, level-major over all HBM networks
+  std::vector<qtn::SubItem> sub_items;
+  std::vector<uint64_t> sub_desc;
+  for (int32_t lev = 0; lev < max_lev; ++lev) {
+    B->level_sub0.push_back((uint32_t)sub_items.size());
+    uint32_t smem = 0;
+    for (int h = 0; h < B->n_hbm; ++h) {
+      const qtn_plan* P = plans[hidx[h]];
+      for (const auto& r : P->hbm_sub) {
+        if (r.level + hshift[h] != lev) continue;
+        qtn::SubItem it;
+        it.net = (uint32_t)h;
+        it.first = (uint32_t)sub_desc.size();
+        it.count = r.count;
+        it.smem = r.smem;
+        for (uint32_t k = 0; k < r.count; ++k) sub_desc.push_back(desc_base[h] + P->hbm_sub_desc[r.first + k]);
+        sub_items.push_back(it);
+        smem = std::max(smem, r.smem);
+      }
+    }
+    B->level_sub_smem.push_back(smem);
+  }
+  B->level_sub0.push_back((uint32_t)sub_items.size());
   // fused product chains, level-major over all HBM networks
   std::vector<uint32_t> fitem_desc, fitem_net;
   std::vector<uint64_t> fprefix, cprefix;
@@ -1013,7 +1042,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     B->chain_len.assign(nl, 0);
     auto tiny_only = [&](size_t l) {
       return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] && !B->level_r1chunks[l] &&
-             !B->level_fctas[l] &&
+             !B->level_fctas[l] && B->level_sub0[l + 1] == B->level_sub0[l] &&
              B->level_red0[l + 1] == B->level_red0[l] && B->level_sitem0[l + 1] > B->level_sitem0[l];
     };
     for (size_t l = 0; chain_on && l < nl;) {
@@ -1052,6 +1081,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_r1, r1items)) || (rc = upload(&B->d_r1prefix, r1prefix)) ||
       (rc = upload(&B->d_fdesc, fdescs)) || (rc = upload(&B->d_fitem_desc, fitem_desc)) ||
       (rc = upload(&B->d_ftab, ftabs)) ||
+      (rc = upload(&B->d_sub_items, sub_items)) || (rc = upload(&B->d_sub_desc, sub_desc)) ||
       (rc = upload(&B->d_fitem_net, fitem_net)) || (rc = upload(&B->d_fprefix, fprefix)) ||
       (rc = upload(&B->d_cprefix, cprefix)) ||
       (rc = upload(&B->d_net_in_off, net_in)) || (rc = upload(&B->d_net_ws_off, net_ws)) ||
@@ -1109,7 +1139,7 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
       }
       c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
-           (B->level_r1chunks[lev] ? 1 : 0);
+           (B->level_r1chunks[lev] ? 1 : 0) + (B->level_sub0[lev + 1] > B->level_sub0[lev] ? 1 : 0);
       for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi)
         c += 1 + (B->fgroups[gi].cctas ? 1 : 0);
     }
@@ -1469,7 +1499,8 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     bool prev_single = false;        // the previous level was one launch
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
       // launches of this level, in issue order: reduce, small, trace, expand, stream
-      const int n_launch = (int)(B->level_fgroup0[lev + 1] - B->level_fgroup0[lev]) +
+      const uint32_t nsub = B->level_sub0[lev + 1] - B->level_sub0[lev];
+      const int n_launch = (int)(B->level_fgroup0[lev + 1] - B->level_fgroup0[lev]) + (nsub ? 1 : 0) +
                            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) +
                            (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
                            (B->level_r1chunks[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
@@ -1510,6 +1541,9 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         qtn::g_pdl_next = false;
         continue;
       }
+      if (nsub && (rc = qtn::launch_subtree(L, B->d_sub_items + B->level_sub0[lev], nsub, B->d_sub_desc,
+                                            B->level_sub_smem[lev], next_stream())))
+        return rc;
       for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi) {
         const qtn_batch::FGroup& g = B->fgroups[gi];
         qtn::FLaunch F;

@@ -1318,13 +1318,92 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         }
       }
     }
-    // levels of the elimination tree: a bucket (or fused chain, at its head)
-    // runs after the producers of its intermediate operands
+    // Tiny subtrees (qtn_stream.h SubItem): connected sets of small buckets
+    // (output rank <= QTN_SUBTREE_R, default 9, outside fused chains) run
+    // as one CTA each with their internal intermediates in shared memory
+    // (QTN_SUBTREE=0 disables).  Members are in elimination order, the root
+    // (last member) writes its result to the workspace.  Opt-in
+    // (QTN_SUBTREE=1): measured slower — config 4's head forest becomes a
+    // few subtrees of ~100 members that one CTA walks serially (107 us vs
+    // ~100 us of level launches): config 4 0.968 -> 0.999 ms, config 3
+    // default 3.187 -> 3.26 ms.
+    std::vector<int32_t> sub_of(nb, -1);  // subtree index of a member bucket
+    std::vector<std::vector<int32_t>> subs;
+    std::vector<int64_t> sm_off(P->tensors.size(), -1);  // internal tensors: shared byte offset
+    std::vector<uint32_t> sub_smem;
+    {
+      const char* sv = getenv("QTN_SUBTREE");
+      const bool on = sv && sv[0] == '1';
+      const char* rv = getenv("QTN_SUBTREE_R");
+      const int sub_r = rv ? atoi(rv) : kSmallR;
+      std::vector<int32_t> grp(nb, -1);
+      std::vector<std::vector<int32_t>> groups;
+      for (int bi = 0; on && bi < nb; ++bi) {
+        const auto& b = P->buckets[bi];
+        if (chain_head[bi] >= 0 || b.rank > sub_r) continue;
+        std::vector<int32_t> mem;
+        for (int32_t id : b.ops) {
+          const auto& t = P->tensors[id];
+          if (t.input || t.born < 0 || grp[t.born] < 0) continue;
+          auto& g = groups[grp[t.born]];
+          mem.insert(mem.end(), g.begin(), g.end());
+          g.clear();
+        }
+        mem.push_back(bi);
+        std::sort(mem.begin(), mem.end());
+        const int32_t gid = (int32_t)groups.size();
+        for (int32_t m : mem) grp[m] = gid;
+        groups.push_back(std::move(mem));
+      }
+      for (auto& g : groups) {
+        if (g.size() < 2) continue;
+        // shared memory of the internal intermediates: first fit over member positions
+        std::vector<Block> blocks;
+        int64_t top = 0;
+        std::vector<std::pair<int32_t, int64_t>> offs;
+        for (size_t k = 0; k + 1 < g.size(); ++k) {
+          const int32_t id = P->buckets[g[k]].out;
+          const auto& t = P->tensors[id];
+          const int32_t cons = t.last_use;
+          const int32_t end = (int32_t)(std::find(g.begin(), g.end(), cons) - g.begin());
+          const int64_t bytes = std::max<int64_t>(16, elem_bytes(t.c64) << t.rank());
+          const int64_t o = place(blocks, bytes, (int32_t)k, end, 16);
+          offs.push_back({id, o});
+          top = std::max(top, o + bytes);
+        }
+        if (top > 48 * 1024) continue;  // too large for one CTA: run level by level
+        const int32_t si = (int32_t)subs.size();
+        for (int32_t m : g) sub_of[m] = si;
+        for (auto& pr : offs) sm_off[pr.first] = pr.second;
+        subs.push_back(g);
+        sub_smem.push_back((uint32_t)((top + 15) & ~15ll));
+      }
+    }
+    // levels of the elimination tree: a bucket (or fused chain, at its head;
+    // or tiny subtree, at its root) runs after the producers of its
+    // intermediate operands
     std::vector<int32_t> tlevel(P->tensors.size(), 0);
-    std::vector<char> virt(P->tensors.size(), 0);  // chain-internal: never stored
+    std::vector<char> virt(P->tensors.size(), 0);  // chain/subtree-internal: never stored
+    std::vector<int32_t> sub_level(subs.size(), 0);
     int32_t nlev = 0;
     P->hbm_level.assign(nb, 0);
     for (int bi = 0; bi < nb; ++bi) {
+      if (sub_of[bi] >= 0) {  // tiny subtree: runs at its root, after every external operand
+        P->hbm_level[bi] = -1;
+        const auto& g = subs[sub_of[bi]];
+        if (g.back() != bi) {
+          virt[P->buckets[bi].out] = 1;
+          continue;
+        }
+        int32_t lv = 0;
+        for (int32_t m : g)
+          for (int32_t id : P->buckets[m].ops)
+            if (sm_off[id] < 0) lv = std::max(lv, tlevel[id]);
+        sub_level[sub_of[bi]] = lv;
+        tlevel[P->buckets[bi].out] = lv + 1;
+        nlev = std::max(nlev, lv + 1);
+        continue;
+      }
       const int32_t h = chain_head[bi];
       if (h >= 0 && h != bi) {  // absorbed into its chain
         P->hbm_level[bi] = -1;
@@ -1340,11 +1419,14 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         virt[P->buckets[c].out] = 1;
     }
     P->n_levels = nlev;
-    // level at which each intermediate is produced / last read
-    auto born_level = [&](const TensorRec& t) {
-      const int32_t h = chain_head[t.born];
-      return P->hbm_level[h >= 0 ? h : t.born];
+    // level at which a bucket runs (its chain's head, its subtree's root)
+    auto exec_level = [&](int32_t bi) {
+      if (sub_of[bi] >= 0) return sub_level[sub_of[bi]];
+      const int32_t h = chain_head[bi];
+      return P->hbm_level[h >= 0 ? h : bi];
     };
+    // level at which each intermediate is produced / last read
+    auto born_level = [&](const TensorRec& t) { return exec_level(t.born); };
     // device arena: lifetimes in levels (concurrent buckets never alias)
     std::vector<Block> hblocks;
     int64_t ws = 0;
@@ -1355,10 +1437,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       bytes = std::max<int64_t>(bytes, 256);
       const int32_t s0 = born_level(t);
       int32_t e = nlev + 1;
-      if (t.last_use < nb) {
-        const int32_t h = chain_head[t.last_use];
-        e = P->hbm_level[h >= 0 ? h : t.last_use];
-      }
+      if (t.last_use < nb) e = exec_level(t.last_use);
       t.ws_off = place(hblocks, bytes, s0, e, 256);
       ws = std::max(ws, t.ws_off + bytes);
     }
@@ -1437,20 +1516,26 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         continue;
       }
       BucketSpec spec;
+      auto tag_x = [&](int32_t id) { return sm_off[id] >= 0 ? tag_sm((uint64_t)sm_off[id]) : tag_of(id); };
       for (int32_t id : b.ops) {
         spec.opvars.push_back(P->tensors[id].vars);
         spec.opc64.push_back(P->tensors[id].c64 ? 1 : 0);
-        spec.optag.push_back(tag_of(id));
+        spec.optag.push_back(tag_x(id));
       }
       spec.primary = b.primary;
       spec.v = b.v;
       spec.out_vars = P->tensors[b.out].vars;
       spec.out_c64 = P->tensors[b.out].c64;
-      spec.out_tag = tag_of(b.out);
+      spec.out_tag = tag_x(b.out);
       int rc = encode_stream_desc(spec, P->hbm_desc);
       if (rc) {
         delete P;
         return rc;
+      }
+      if (sub_of[bi] >= 0) {  // subtree member: evaluated by its subtree's CTA only
+        const SHdr* h = reinterpret_cast<const SHdr*>(P->hbm_desc.data() + P->hbm_desc_off.back());
+        P->hbm_tiles.push_back(h->n_tiles);
+        continue;
       }
       const SHdr* h = reinterpret_cast<const SHdr*>(P->hbm_desc.data() + P->hbm_desc_off.back());
       P->hbm_tiles.push_back(h->n_tiles);
@@ -1554,6 +1639,16 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         P->hbm_xdesc.push_back(xd);
       }
     }
+    // subtree records: member descriptors contiguous, in elimination order
+    for (size_t si = 0; si < subs.size(); ++si) {
+      qtn_plan::SubRec r;
+      r.level = sub_level[si];
+      r.first = (uint32_t)P->hbm_sub_desc.size();
+      r.count = (uint32_t)subs[si].size();
+      r.smem = sub_smem[si];
+      for (int32_t m : subs[si]) P->hbm_sub_desc.push_back(P->hbm_desc_off[m]);
+      P->hbm_sub.push_back(r);
+    }
     // bytes the executor moves: a fused chain (product or reduce) reads its
     // head's operands and writes its tail's output only
     double eb = 0.0;
@@ -1562,7 +1657,9 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       if (h >= 0 && h != bi) continue;
       const auto& b = P->buckets[bi];
       for (int32_t id : b.ops)
-        eb += std::ldexp((double)elem_bytes(P->tensors[id].c64), P->tensors[id].rank());
+        if (sm_off[id] < 0)  // subtree-internal operands never leave the SM
+          eb += std::ldexp((double)elem_bytes(P->tensors[id].c64), P->tensors[id].rank());
+      if (sm_off[b.out] >= 0) continue;
       const auto& o = P->tensors[P->buckets[h >= 0 ? chain_tail[bi] : bi].out];
       eb += std::ldexp((double)elem_bytes(o.c64), o.rank());
     }

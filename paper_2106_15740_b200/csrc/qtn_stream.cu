@@ -46,8 +46,17 @@ using s256::resolve;
 // operand gathered: out[o] = sum_v P[o | v] * prod_tables prod_ops Op[..] *
 // prod_gathered G[..].  CG: operand loads through L2 only (coherent with
 // writes of other CTAs ordered by a cluster barrier, chain_kernel).
-template <bool CG>
+// CG: 0 read-only path (__ldg), 1 L2 (__ldcg, coherent with writes of other
+// CTAs), 2 generic loads (operands in shared or global memory: subtrees)
+template <int CG>
 __device__ __forceinline__ double2 ld_op(const void* p, uint64_t i, uint32_t c64) {
+  if (CG == 2) {
+    if (c64) {
+      const float2 f = reinterpret_cast<const float2*>(p)[i];
+      return make_double2(f.x, f.y);
+    }
+    return reinterpret_cast<const double2*>(p)[i];
+  }
   if (!CG) return ldg_c(p, i, c64);
   if (c64) {
     const float2 f = __ldcg(reinterpret_cast<const float2*>(p) + i);
@@ -55,7 +64,7 @@ __device__ __forceinline__ double2 ld_op(const void* p, uint64_t i, uint32_t c64
   }
   return __ldcg(reinterpret_cast<const double2*>(p) + i);
 }
-template <bool CG>
+template <int CG>
 __device__ __forceinline__ void small_eval(const uint8_t* dsc, const Bases& b, uint64_t o_begin,
                                            uint64_t o_end, uint64_t o_step) {
   const SHdr& h = *reinterpret_cast<const SHdr*>(dsc);
@@ -126,7 +135,56 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
   const uint64_t o0 = tpi == 256 ? (uint64_t)blockIdx.y * kSmallChunk : 0;
   if (o0 >= n_all) return;
   const uint64_t n_out = tpi == 256 ? min(n_all, o0 + kSmallChunk) : n_all;
-  small_eval<false>(dsc, b, o0 + lane, n_out, tpi);
+  small_eval<0>(dsc, b, o0 + lane, n_out, tpi);
+}
+
+// ---- tiny subtrees (qtn_stream.h SubItem): one CTA per (subtree, set)
+// evaluates the member buckets in order, each with the small-bucket routine
+// (threads over output elements), intermediates in shared memory.
+__global__ void __launch_bounds__(256) subtree_kernel(const __grid_constant__ StreamLaunch L,
+                                                      const SubItem* __restrict__ items,
+                                                      const uint64_t* __restrict__ sub_desc) {
+  extern __shared__ __align__(16) unsigned char ssm[];
+  __shared__ uint4 sdesc[(kSDescMax + 15) / 16];
+  pdl_trigger();
+  const SubItem it = items[blockIdx.x];
+  Bases b;
+  b.in = L.in_base + (int64_t)blockIdx.y * L.in_set_stride + L.net_in_off[it.net];
+  b.ws = L.ws_base + (int64_t)blockIdx.y * L.ws_set_stride + L.net_ws_off[it.net];
+  b.sm = reinterpret_cast<char*>(ssm);
+  pdl_wait();
+  for (uint32_t k = 0; k < it.count; ++k) {
+    const uint8_t* gdsc = L.descs + sub_desc[it.first + k];
+    const uint32_t n16 = (reinterpret_cast<const SHdr*>(gdsc)->desc_bytes + 15u) / 16u;
+    __syncthreads();  // previous member done (its output visible, descriptor free)
+    for (uint32_t i = threadIdx.x; i < n16; i += 256u) sdesc[i] = __ldg(reinterpret_cast<const uint4*>(gdsc) + i);
+    __syncthreads();
+    const uint8_t* dsc = reinterpret_cast<const uint8_t*>(sdesc);
+    small_eval<2>(dsc, b, threadIdx.x, 1ull << reinterpret_cast<const SHdr*>(dsc)->R, 256);
+  }
+}
+
+int launch_subtree(const StreamLaunch& L, const SubItem* items, uint32_t n_items,
+                   const uint64_t* sub_desc, uint32_t smem_bytes, void* stream) {
+  if (!n_items || !L.n_sets) return QTN_OK;
+  static std::atomic<uint64_t> attr{0};
+  if (needs_setup(attr)) {
+    cudaError_t e = cudaFuncSetAttribute(subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         96 * 1024);
+    if (e != cudaSuccess) {
+      set_error(std::string("subtree_kernel attribute: ") + cudaGetErrorString(e));
+      return QTN_ECUDA;
+    }
+    mark_setup(attr);
+  }
+  cudaError_t e = launch_pdl<true>(subtree_kernel, dim3(n_items, L.n_sets), dim3(256), smem_bytes,
+                                   reinterpret_cast<cudaStream_t>(stream), L, items, sub_desc);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("subtree_kernel launch: ") + cudaGetErrorString(e));
+    return QTN_ECUDA;
+  }
+  return QTN_OK;
 }
 
 int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream, bool pdl) {
@@ -184,7 +242,7 @@ __global__ void __launch_bounds__(256) chain_kernel(const __grid_constant__ Stre
       for (uint32_t i = lane; i < n16; i += 32) slot[i] = __ldg(reinterpret_cast<const uint4*>(gdsc) + i);
       __syncwarp();
       const uint8_t* dsc = reinterpret_cast<const uint8_t*>(slot);
-      small_eval<true>(dsc, b, lane, 1ull << reinterpret_cast<const SHdr*>(dsc)->R, 32);
+      small_eval<1>(dsc, b, lane, 1ull << reinterpret_cast<const SHdr*>(dsc)->R, 32);
     }
     cluster_sync_all();
   }

@@ -14,6 +14,8 @@ constexpr uint64_t kOffMask = (1ull << kSelShift) - 1;
 inline uint64_t tag_abs(const void* p) { return (uint64_t)(uintptr_t)p; }
 inline uint64_t tag_in(uint64_t byte_off) { return (1ull << kSelShift) | byte_off; }
 inline uint64_t tag_ws(uint64_t byte_off) { return (2ull << kSelShift) | byte_off; }
+// 3: shared memory of a tiny-subtree CTA (intermediates that never leave the SM)
+inline uint64_t tag_sm(uint64_t byte_off) { return (3ull << kSelShift) | byte_off; }
 
 // pipeline geometry (overridable at build time for A/B experiments)
 #ifndef QTN_STREAM_STAGES
@@ -384,6 +386,21 @@ int launch_fused(const FLaunch& L, void* stream);
 // split items: one CTA per (item, unit) sums the 2^sk partials in order;
 // cta_prefix = the units of split items (0 for the others)
 int launch_fused_combine(const FLaunch& L, void* stream);
+
+// ---- tiny subtrees: a connected set of small buckets (output rank <= 9)
+// of one elimination tree, evaluated by ONE CTA in elimination order with
+// its internal intermediates in shared memory (operand tags with selector
+// 3); the subtree's external operands come from the inputs / workspace, its
+// root's result goes to the workspace.  One launch per level covers every
+// subtree of the level (a CTA per subtree and angle set): the levels of
+// tiny buckets and their launch-to-launch latency disappear.
+struct SubItem {
+  uint32_t net;                 // network index (bases)
+  uint32_t first, count;        // member descriptors sub_desc[first .. first+count)
+  uint32_t smem;                // shared-memory bytes of its intermediates
+};
+int launch_subtree(const StreamLaunch& L, const SubItem* items, uint32_t n_items,
+                   const uint64_t* sub_desc, uint32_t smem_bytes, void* stream);
 
 // single descriptor with absolute pointers, descriptor passed by value
 int launch_stream_single(const std::vector<uint8_t>& desc, void* stream);

@@ -118,12 +118,14 @@ __device__ __forceinline__ uint64_t gather(uint64_t o, const uint32_t* runs, uin
 struct Bases {
   const char* in;
   char* ws;
+  char* sm = nullptr;  // shared memory of a tiny-subtree CTA (tag selector 3)
 };
 
 __device__ __forceinline__ const char* resolve(uint64_t tag, const Bases& b) {
   const uint64_t sel = tag >> kSelShift, off = tag & kOffMask;
   if (sel == 1) return b.in + off;
   if (sel == 2) return b.ws + off;
+  if (sel == 3) return b.sm + off;
   return reinterpret_cast<const char*>(off);
 }
 
@@ -190,7 +192,7 @@ __device__ __forceinline__ Loc locate(const StreamLaunch& L, uint64_t t, LocCach
 }
 
 __device__ __forceinline__ Bases bases_of(const StreamLaunch& L, const Loc& l) {
-  Bases b{nullptr, nullptr};
+  Bases b{nullptr, nullptr, nullptr};
   if (!L.item_desc) return b;
   const uint32_t net = L.item_net[l.item];
   b.in = L.in_base + (int64_t)l.set * L.in_set_stride + L.net_in_off[net];

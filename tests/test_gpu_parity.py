@@ -597,6 +597,7 @@ def test_chain_kernel_opt_in(golden, monkeypatch):
     """Tiny-level chains in one cluster launch (QTN_CHAIN=1, cluster barriers
     between levels) equal the per-level small_kernel launches (config 4 edge
     #16 and config 3 default networks, complex128), with fewer launches."""
+    monkeypatch.setenv("QTN_SUBTREE", "0")  # tiny levels must exist for the chains
     G4 = golden("config4.json")
     g4 = Q.random_regular_graph(G4["n"], 3, 0)
     p4 = Q.QaoaParams(G4["gammas"], G4["betas"])
@@ -759,3 +760,37 @@ def test_repeatable_bitwise_results():
                 assert np.array_equal(x, y)
     finally:
         del os.environ["QTN_GRAPHS"]
+
+
+@pytest.mark.parametrize("sub_r", ["9", "12"])
+def test_tiny_subtrees(golden, monkeypatch, sub_r):
+    """Tiny subtrees (subtree_kernel: a connected set of small buckets
+    evaluated by one CTA with its intermediates in shared memory): equal to
+    the level-by-level buckets (QTN_SUBTREE=0) and to the reference on
+    config 3 default (10 edges) and config 4 edge #16, complex128 and
+    complex64; QTN_SUBTREE_R=12 also takes larger buckets."""
+    monkeypatch.setenv("QTN_SUBTREE_R", sub_r)
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    recs = G["modes"]["default"][:10]
+    G4 = golden("config4.json")
+    rec4 = complex(*[r for r in G4["modes"]["zz+diagonal"] if r["edge_index"] == 16][0]["value"])
+    g4 = Q.random_regular_graph(G4["n"], 3, 0)
+    p4v = Q.QaoaParams(G4["gammas"], G4["betas"])
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_SUBTREE", flag)
+        for dt in ("complex128", "complex64"):
+            plan = Q.EnergyPlan(graph, G["p"], "default", dtype=dt,
+                                edge_ids=[r["edge_index"] for r in recs])
+            p4 = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype=dt, edge_ids=[16])
+            out[flag, dt] = (plan.zz_values(params), p4.zz_values(p4v)[16])
+            assert plan.launches == plan.launches_per_eval(1)
+    for dt, tol in (("complex128", 1e-11), ("complex64", 1e-5)):
+        for r in recs:
+            w = complex(*r["value"])
+            e = r["edge_index"]
+            assert abs(out["1", dt][0][e] - w) <= tol * abs(w) + 1e-12, (dt, e)
+            assert abs(out["1", dt][0][e] - out["0", dt][0][e]) <= tol * abs(w) + 1e-12
+        assert abs(out["1", dt][1] - rec4) <= tol * abs(rec4)
