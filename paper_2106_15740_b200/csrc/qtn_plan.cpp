@@ -619,6 +619,11 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
   }
   const uint32_t mesz = s.math_f32 ? 8u : 16u;
   const int max_out = kFThreadBits + kFMaxAcc;
+  // tuning knobs (experiments): stage budget, terms per CTA, split threshold
+  static const uint64_t fbuf = getenv("QTN_FBUF") ? strtoull(getenv("QTN_FBUF"), nullptr, 10) : kFBufBytes;
+  static const int fupc = getenv("QTN_FUPC") ? atoi(getenv("QTN_FUPC")) : 16;
+  static const int fsplit = getenv("QTN_FSPLIT") ? atoi(getenv("QTN_FSPLIT")) : 16;
+  static const int fmaxq = getenv("QTN_FMAXQ") ? atoi(getenv("QTN_FMAXQ")) : kFMaxQ;
   auto esz = [&](int t) { return s.opc64[t] ? 8u : 16u; };
   auto make_sides = [&](uint64_t tl) {
     std::vector<int> ord(n);
@@ -682,8 +687,8 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
   };
   auto n_out = [&](uint64_t tl) { return __builtin_popcountll(tl & ((1ull << R) - 1)); };
   auto fits = [&](uint64_t tl) {
-    return buf_bytes(tl, make_sides(tl)) <= kFBufBytes && n_out(tl) <= max_out &&
-           __builtin_popcountll(tl) <= kFMaxQ;
+    return buf_bytes(tl, make_sides(tl)) <= std::min<uint64_t>(fbuf, kFBufBytes) && n_out(tl) <= max_out &&
+           __builtin_popcountll(tl) <= std::min(fmaxq, kFMaxQ);
   };
   uint64_t tile = 0;
   {
@@ -834,10 +839,10 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
   // (amortises its table setup), keeping >= 512 CTAs per item
   const int nl = (int)lb.size(), ng = (int)gb.size();
   int sk = 0;
-  if (ng < 9) sk = std::min(nl, std::max(0, nq + nl - 16));
+  if (ng < 9) sk = std::min(nl, std::max(0, nq + nl - fsplit));
   int upc = 0;
   if (!sk) {
-    upc = std::max(0, 16 - (nq + nl));
+    upc = std::max(0, fupc - (nq + nl));
     upc = std::min(upc, std::max(0, ng - 9));
   }
   d.upc_log2 = (uint8_t)upc;

@@ -286,7 +286,7 @@ constexpr int kFQRuns = 16;
 constexpr int kFMaxQ = 16;            // tile bits
 constexpr int kFThreadBits = 8;       // 256 threads
 constexpr int kFMaxAcc = 2;           // <= 4 output accumulators per thread
-constexpr uint32_t kFBufBytes = 49152;  // one stage buffer (two per CTA: double buffered)
+constexpr uint32_t kFBufBytes = 24576;  // one stage buffer (two per CTA: double buffered; measured best of 16-48 KiB)
 constexpr int kFLTabBits = 8;         // loop-offset tables up to 2^8 loop values
 // Operands are staged raw (their storage type, cp.async, no register round
 // trip) into a stage buffer over their compact index (the tile bits they
