@@ -1222,8 +1222,8 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     // is then reduced by single-operand buckets is one fused contraction; the
     // union-size product and the chain's intermediates are never written
     // (the GEMM census in DESIGN §3.7).  On for chains
-    // whose head has union rank >= 10 and whose output rank is 1..15
-    // (measured: config 3 default 3.69 -> 3.17 ms; dot products
+    // whose head has union rank >= 10 and whose output rank is 1..17
+    // (measured: config 3 default 3.69 -> 2.84 ms; dot products
     // into scalars and wide streaming chains run faster unfused);
     // QTN_FUSE_CHAIN=0 disables, QTN_FCHAIN_MIN_R / _MIN_OUT / _MAX_OUT move
     // the window.
@@ -1233,7 +1233,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       const char* fmr = getenv("QTN_FCHAIN_MIN_R");
       const int fmin_r = fmr ? atoi(fmr) : 10;
       const char* fmo = getenv("QTN_FCHAIN_MAX_OUT");
-      const int fmax_out = fmo ? atoi(fmo) : 15;
+      const int fmax_out = fmo ? atoi(fmo) : 17;
       const char* fno = getenv("QTN_FCHAIN_MIN_OUT");
       const int fmin_out = fno ? atoi(fno) : 1;
       for (int bi = 0; fchain && bi < nb; ++bi) {
