@@ -1236,6 +1236,8 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       const int fmax_out = fmo ? atoi(fmo) : 17;
       const char* fno = getenv("QTN_FCHAIN_MIN_OUT");
       const int fmin_out = fno ? atoi(fno) : 1;
+      const char* fso = getenv("QTN_FCHAIN_STREAM_MAX_OUT");
+      const int fstream_max_out = fso ? atoi(fso) : 13;
       for (int bi = 0; fchain && bi < nb; ++bi) {
         const auto& b = P->buckets[bi];
         if (b.ops.size() < 2 || chain_head[bi] >= 0 || b.rank + 1 < fmin_r) continue;
@@ -1252,6 +1254,14 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         {
           const int orank = P->tensors[P->buckets[members.back()].out].rank();
           if (orank > fmax_out || orank < fmin_out) continue;
+          // streaming chains (one operand holds all but <= 1 of the union's
+          // variables: each of its entries feeds one term) only up to
+          // QTN_FCHAIN_STREAM_MAX_OUT (13): the trace/reduce kernels stream
+          // them faster than the fused kernel's staged terms (config 4 in
+          // 2^3 slices 1.127 -> 0.998 ms, config 3 default unchanged)
+          int maxop = 0;
+          for (int32_t id : b.ops) maxop = std::max(maxop, P->tensors[id].rank());
+          if (maxop >= b.rank && orank > fstream_max_out) continue;
         }
         // geometry check with placeholder tags (tags do not change it)
         FChainSpec fs;

@@ -9,7 +9,7 @@ timeout 600 python bench.py > gpurun_out/r/bench_default.json 2> gpurun_out/r/be
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/r/bench_reference.json 2>&1; echo "ref rc=$?"
 timeout 300 python bench.py --workload config1 --angle-sets 1024 --steps 50 --warmup 10 --no-records --cpu-seconds 5 > gpurun_out/r/bench_config1.json 2>&1; echo "c1 rc=$?"
 timeout 300 python bench.py --workload config3 --angle-sets 256 --steps 5 --warmup 3 --no-records --cpu-seconds 5 > gpurun_out/r/bench_config3.json 2>&1; echo "c3 rc=$?"
-timeout 300 python bench.py --workload config3-default --angle-sets 1 --steps 5 --warmup 3 --no-records --cpu-seconds 10 > gpurun_out/r/bench_config3d.json 2>&1; echo "c3d rc=$?"
+timeout 300 python bench.py --workload config3-default --angle-sets 1 --steps 20 --warmup 5 --no-records --cpu-seconds 10 > gpurun_out/r/bench_config3d.json 2>&1; echo "c3d rc=$?"
 timeout 300 python bench.py --workload config4 --angle-sets 1 --steps 10 --warmup 3 --no-records --cpu-seconds 20 > gpurun_out/r/bench_config4.json 2>&1; echo "c4 rc=$?"
 timeout 300 python bench.py --workload config4 --angle-sets 1 --slices 3 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config4_k3.json 2>&1; echo "c4k3 rc=$?"
 timeout 600 python bench.py --workload config5 --steps 5 > gpurun_out/r/config5_sweep.json 2>&1; echo "c5 rc=$?"
@@ -30,3 +30,5 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 for w in config4 config3-default; do timeout 300 python tools/timeline.py $w --out gpurun_out/r/timeline_$w.json > gpurun_out/r/timeline_$w.txt 2>&1; done
 QTN_FUSE_CHAIN=1 timeout 300 python bench.py --workload config3-default --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config3d_fused.json 2>&1; echo "c3d fused rc=$?"
 QTN_FUSE_CHAIN=1 timeout 300 python bench.py --workload config4 --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config4_fused.json 2>&1; echo "c4 fused rc=$?"
+python bench.py --steps 1 --warmup 3 --workload config3-default --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/plain_c3d_f.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:fused_kernel -s 20 -c 1 -o gpurun_out/r/prof_fused_c3d python bench.py --steps 1 --warmup 3 --workload config3-default --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu7.log 2>&1; echo "ncu7 rc=$?"
