@@ -155,15 +155,14 @@ __host__ __device__ inline FLayout fused_layout(const FDesc& d) {
     w += 32u;
   }
   L.words = (w + 3u) & ~3u;
+  // the tables first (offset 0: the CTA copies them in before it has read
+  // its descriptor), then the stage buffers
+  L.tab = 0;
+  uint32_t off = 4u * L.words;
   L.bstride = (d.buf_bytes + 15u) & ~15u;
-  uint32_t off = 2u * L.bstride;
-  L.red = off;
-  off += 256u * 16u;
-  L.issue = off;
-  off += 16u * d.n_ops;
-  off = (off + 15u) & ~15u;
-  L.tab = off;
-  off += 4u * L.words;
+  L.red = off + 2u * L.bstride;
+  L.issue = L.red + 256u * 16u;
+  off = L.issue + 16u * d.n_ops;
   L.total = (off + 15u) & ~15u;
   return L;
 }
@@ -240,15 +239,14 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
   const uint32_t na = nto > nthr ? nto - nthr : 0u;        // in-thread output bits
   const uint32_t njs = 1u << (jn - na);
   const bool active = tid < (1u << nthr);
-  const uint32_t sbase = smem_u32(smem);
+  unsigned char* bufs = smem + 4u * Lo.words;             // stage buffers (after the tables)
+  const uint32_t sbase = smem_u32(bufs);                   // stage buffer 0
   const bool ltab_on = d.nl <= kFLTabBits;
   // ---- per-CTA tables: the host-built tables with the descriptor (one
   // 16-byte copy per thread), the copy records with resolved pointers
-  const uint32_t* tw = reinterpret_cast<const uint32_t*>(smem + Lo.tab);
+  const uint32_t* tw = reinterpret_cast<const uint32_t*>(smem + Lo.tab);  // copied in by the entry
+  (void)tabs;
   {
-    const uint4* src = reinterpret_cast<const uint4*>(tabs + d.tab_off / 4u);
-    uint4* dst = reinterpret_cast<uint4*>(smem + Lo.tab);
-    for (uint32_t i = tid; i < Lo.words / 4u; i += 256u) dst[i] = __ldg(src + i);
     if (tid < n) {
       const FOp& o = d.ops[tid];
       const FSide& S = d.sides[o.side];
@@ -335,7 +333,7 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
   auto store_pend = [&](uint32_t bufoff) {
     for (uint32_t t = 0; t < n; ++t) {
       const OpIssue r = iss[t];
-      if (r.mode == 3 && tid < r.n) reinterpret_cast<C*>(smem + bufoff + r.dst)[tid] = pend[t];
+      if (r.mode == 3 && tid < r.n) reinterpret_cast<C*>(bufs + bufoff + r.dst)[tid] = pend[t];
     }
   };
   // product sides: their math-type region from the operands' raw regions
@@ -343,7 +341,7 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
     for (uint32_t si = 0; si < ns; ++si) {
       const FSide& S = d.sides[si];
       if (S.kind != kFSideProd) continue;
-      C* dst = reinterpret_cast<C*>(smem + bufoff + S.st_off);
+      C* dst = reinterpret_cast<C*>(bufs + bufoff + S.st_off);
       for (uint32_t c = tid; c < (1u << S.nst); c += 256u) {
         C v = C{1, 0};
         for (uint32_t t = S.first_op; t < S.first_op + S.n_ops; ++t) {
@@ -351,10 +349,10 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
           const uint32_t j = (uint32_t)fgather(c, o.ocrun, o.n_ocrun);
           C x;
           if (o.c64) {
-            const float2 f = reinterpret_cast<const float2*>(smem + bufoff + o.raw_off)[j];
+            const float2 f = reinterpret_cast<const float2*>(bufs + bufoff + o.raw_off)[j];
             x = C{(E)f.x, (E)f.y};
           } else {
-            const double2 f = reinterpret_cast<const double2*>(smem + bufoff + o.raw_off)[j];
+            const double2 f = reinterpret_cast<const double2*>(bufs + bufoff + o.raw_off)[j];
             x = C{(E)f.x, (E)f.y};
           }
           v = t == S.first_op ? x : cm(v, x);
@@ -475,24 +473,26 @@ __global__ void __launch_bounds__(256, sizeof(C) == 8 ? 3 : 2) fused_kernel(cons
   __shared__ __align__(16) FDesc SD;
   pdl_trigger();
   pdl_wait();
-  const uint64_t cb = blockIdx.x;
-  uint32_t lo = 0, hi = L.n_items;  // last item whose first CTA <= cb
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (L.cta_prefix[mid] <= cb) lo = mid;
-    else hi = mid;
-  }
-  const FDesc* gd = &L.descs[L.item_desc[lo]];
+  // the CTA's record, then its descriptor and tables in one pass (both
+  // copies in flight together: the tables sit at offset 0 of the dynamic
+  // shared memory whatever the descriptor says)
+  const FCta rec = L.ctas[blockIdx.x];
   {
-    const uint32_t n16 = (kFHdrBytes + gd->n_ops * (uint32_t)sizeof(FOp)) / 16u;  // header + sides + used ops
-    for (uint32_t i = threadIdx.x; i < n16; i += 256u)
-      reinterpret_cast<uint4*>(&SD)[i] = __ldg(reinterpret_cast<const uint4*>(gd) + i);
+    const uint4* src = reinterpret_cast<const uint4*>(L.blob + rec.blob);
+    uint4* dsd = reinterpret_cast<uint4*>(&SD);
+    uint4* dtab = reinterpret_cast<uint4*>(fsm);
+    const uint32_t nd = rec.desc16, nt = rec.tab16;
+    for (uint32_t i = threadIdx.x; i < nd + nt; i += 256u) {
+      const uint4 v = __ldg(src + i);
+      if (i < nd) dsd[i] = v;
+      else dtab[i - nd] = v;
+    }
   }
   __syncthreads();
-  const uint32_t net = L.item_net[lo], set = blockIdx.y;
+  const uint32_t net = rec.net, set = blockIdx.y;
   const char* in = L.in_base + (int64_t)set * L.in_set_stride + L.net_in_off[net];
   char* ws = L.ws_base + (int64_t)set * L.ws_set_stride + L.net_ws_off[net];
-  const uint64_t c = cb - L.cta_prefix[lo];
+  const uint64_t c = rec.c;
   uint64_t u0, u1;
   uint32_t l0 = 0, l1 = 1u << SD.nl, split = 0;
   if (SD.sk) {  // split-K: CTA = (unit, split), a contiguous range of loop values

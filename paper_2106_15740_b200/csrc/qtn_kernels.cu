@@ -650,6 +650,8 @@ struct qtn_batch {
   // fused product chains per level (fused_kernel)
   qtn::FDesc* d_fdesc = nullptr;
   uint32_t* d_ftab = nullptr;
+  qtn::FCta* d_fctas = nullptr;
+  uint8_t* d_fblob = nullptr;
   uint32_t* d_fitem_desc = nullptr;
   uint32_t* d_fitem_net = nullptr;
   uint64_t* d_fprefix = nullptr;
@@ -659,6 +661,7 @@ struct qtn_batch {
   struct FGroup {
     uint32_t item0, n_items;
     uint64_t prefix0, ctas, cctas;
+    uint64_t cta0;                      // first per-CTA record (fused_kernel)
     uint32_t smem;
     uint8_t f64;
   };
@@ -718,6 +721,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix,
                   (void*)B->d_fdesc, (void*)B->d_fitem_desc, (void*)B->d_fitem_net,
                   (void*)B->d_fprefix, (void*)B->d_cprefix, (void*)B->d_ftab,
+                  (void*)B->d_fctas, (void*)B->d_fblob,
                   (void*)B->d_sub_items, (void*)B->d_sub_desc})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
@@ -807,12 +811,29 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     fdesc_base[h] = (uint32_t)fdescs.size();
     fdescs.insert(fdescs.end(), P->hbm_fdesc.begin(), P->hbm_fdesc.end());
   }
-  // host-built lookup tables of every fused descriptor (16-byte aligned each)
+  // host-built lookup tables of every fused descriptor (16-byte aligned each),
+  // and the per-descriptor blob [header, sides, used ops | tables] the
+  // fused kernel copies in one pass
   std::vector<uint32_t> ftabs;
-  for (auto& fd : fdescs) {
-    fd.tab_off = 4ull * ftabs.size();
+  std::vector<uint8_t> fblob;
+  std::vector<uint64_t> fblob_off(fdescs.size());
+  std::vector<uint32_t> fdesc16(fdescs.size()), ftab16(fdescs.size());
+  for (size_t i = 0; i < fdescs.size(); ++i) {
+    auto& fd = fdescs[i];
+    const size_t t0 = ftabs.size();
+    fd.tab_off = 4ull * t0;
     qtn::fused_build_tables(fd, ftabs);
     while (ftabs.size() & 3u) ftabs.push_back(0u);
+    const size_t dbytes = (offsetof(qtn::FDesc, ops) + fd.n_ops * sizeof(qtn::FOp) + 15) & ~(size_t)15;
+    const size_t tbytes = 4 * (ftabs.size() - t0);
+    fblob_off[i] = fblob.size();
+    fdesc16[i] = (uint32_t)(dbytes / 16);
+    ftab16[i] = (uint32_t)(tbytes / 16);
+    const uint8_t* dp = reinterpret_cast<const uint8_t*>(&fd);
+    fblob.insert(fblob.end(), dp, dp + std::min(dbytes, sizeof(qtn::FDesc)));
+    fblob.resize(fblob_off[i] + dbytes, 0);
+    const uint8_t* tp = reinterpret_cast<const uint8_t*>(ftabs.data() + t0);
+    fblob.insert(fblob.end(), tp, tp + tbytes);
   }
   // tiny subtrees, level-major over all HBM networks
   std::vector<qtn::SubItem> sub_items;
@@ -840,12 +861,14 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   // fused product chains, level-major over all HBM networks
   std::vector<uint32_t> fitem_desc, fitem_net;
   std::vector<uint64_t> fprefix, cprefix;
+  std::vector<qtn::FCta> fctas;
   for (int32_t lev = 0; lev < max_lev; ++lev) {
     B->level_fgroup0.push_back((uint32_t)B->fgroups.size());
     uint64_t lev_ctas = 0;
     for (int mt = 0; mt < 2; ++mt) {  // complex64 math, then complex128 math
       qtn_batch::FGroup g{};
       g.item0 = (uint32_t)fitem_desc.size();
+      g.cta0 = fctas.size();
       g.prefix0 = fprefix.size();
       g.f64 = (uint8_t)mt;
       uint64_t acc = 0, cacc = 0;
@@ -858,7 +881,18 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
           if (P->hbm_flevel[f] + hshift[h] != lev || (fd.math_f32 ? 0 : 1) != mt) continue;
           fitem_desc.push_back(fdesc_base[h] + (uint32_t)f);
           fitem_net.push_back((uint32_t)h);
-          acc += fd.sk ? (fd.n_units << fd.sk) : (fd.n_units + (1ull << fd.upc_log2) - 1) >> fd.upc_log2;
+          const uint64_t nc = fd.sk ? (fd.n_units << fd.sk) : (fd.n_units + (1ull << fd.upc_log2) - 1) >> fd.upc_log2;
+          const uint32_t di = fdesc_base[h] + (uint32_t)f;
+          for (uint64_t c = 0; c < nc; ++c) {
+            qtn::FCta r{};
+            r.blob = fblob_off[di];
+            r.desc16 = fdesc16[di];
+            r.tab16 = ftab16[di];
+            r.net = (uint32_t)h;
+            r.c = (uint32_t)c;
+            fctas.push_back(r);
+          }
+          acc += nc;
           fprefix.push_back(acc);
           cacc += fd.sk ? fd.n_units : 0;
           cprefix.push_back(cacc);
@@ -1080,7 +1114,8 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_level_sitem0, B->level_sitem0)) ||
       (rc = upload(&B->d_r1, r1items)) || (rc = upload(&B->d_r1prefix, r1prefix)) ||
       (rc = upload(&B->d_fdesc, fdescs)) || (rc = upload(&B->d_fitem_desc, fitem_desc)) ||
-      (rc = upload(&B->d_ftab, ftabs)) ||
+      (rc = upload(&B->d_ftab, ftabs)) || (rc = upload(&B->d_fctas, fctas)) ||
+      (rc = upload(&B->d_fblob, fblob)) ||
       (rc = upload(&B->d_sub_items, sub_items)) || (rc = upload(&B->d_sub_desc, sub_desc)) ||
       (rc = upload(&B->d_fitem_net, fitem_net)) || (rc = upload(&B->d_fprefix, fprefix)) ||
       (rc = upload(&B->d_cprefix, cprefix)) ||
@@ -1559,6 +1594,8 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
           std::memset(&F, 0, sizeof(F));
           F.descs = B->d_fdesc;
           F.tabs = B->d_ftab;
+          F.ctas = B->d_fctas + g.cta0;
+          F.blob = B->d_fblob;
           F.item_desc = B->d_fitem_desc + g.item0;
           F.item_net = B->d_fitem_net + g.item0;
           F.cta_prefix = B->d_fprefix + g.prefix0;

@@ -847,9 +847,20 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
   }
   d.upc_log2 = (uint8_t)upc;
   d.sk = (uint8_t)sk;
-  if (getenv("QTN_DEBUG_DESC") && R + K >= atoi(getenv("QTN_DEBUG_DESC")))
-    fprintf(stderr, "fdesc R=%d K=%d ops=%d sides=%d nq=%d nto=%d ng=%d nl=%d buf=%u upc=%d sk=%d fin=%d s0=%d\n", R,
-            K, n, (int)sides.size(), nq, nto, ng, nl, off, upc, sk, (int)d.has_finish, (int)d.sides[0].kind);
+  if (getenv("QTN_DEBUG_DESC") && R + K >= atoi(getenv("QTN_DEBUG_DESC"))) {
+    // per side: which in-thread slot bits (q bits [nthr, nto)) / summed in-thread bits it depends on
+    std::string sm;
+    for (size_t si = 0; si < sides.size(); ++si) {
+      const uint64_t sdep = dep[sides[si][0]] & tile;
+      int ms = 0, js = 0;
+      for (int i = nthr; i < nq; ++i)
+        if ((sdep >> qb[i]) & 1) (i < nto ? ms : js) |= 1 << (i - nthr);
+      sm += " s" + std::to_string(si) + "(n" + std::to_string(sides[si].size()) + ",a" + std::to_string(ms) +
+            ",j" + std::to_string(js) + ")";
+    }
+    fprintf(stderr, "fdesc R=%d K=%d ops=%d sides=%d nv=%d nq=%d nto=%d ng=%d nl=%d buf=%u upc=%d sk=%d fin=%d%s\n",
+            R, K, n, (int)sides.size(), n_var, nq, nto, ng, nl, off, upc, sk, (int)d.has_finish, sm.c_str());
+  }
   return true;
 }
 

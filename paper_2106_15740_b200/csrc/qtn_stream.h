@@ -355,9 +355,22 @@ struct FChainSpec {
   uint64_t out_tag;
 };
 bool encode_fused_desc(const FChainSpec& s, FDesc& d);
+// Per-CTA record of a fused launch (built with the batch): where the CTA's
+// descriptor + tables sit in the blob, its network and its index within the
+// item — one load instead of a search over the item prefix.
+struct FCta {
+  uint64_t blob;                      // byte offset of [descriptor | tables] in FLaunch::blob
+  uint32_t desc16, tab16;             // 16-byte words of the descriptor part / table part
+  uint32_t net;                       // network index (bases)
+  uint32_t c;                         // CTA index within its item
+  uint32_t pad[2];
+};
+static_assert(sizeof(FCta) == 32, "FCta");
 struct FLaunch {
   const FDesc* descs;                 // device
   const uint32_t* tabs;               // device: table blob (FDesc::tab_off)
+  const FCta* ctas;                   // device: per-CTA records (fused_kernel)
+  const uint8_t* blob;                // device: per descriptor [header, sides, used ops | tables]
   const uint32_t* item_desc;          // device: descriptor index per item
   const uint32_t* item_net;           // device: network index per item
   const uint64_t* cta_prefix;         // device: n_items + 1 (CTAs of one set)
