@@ -638,7 +638,8 @@ struct qtn_batch {
   qtn::R1Dev* d_r1 = nullptr;
   uint64_t* d_r1prefix = nullptr;
   std::vector<uint32_t> level_r1item0;  // first trace item of each level (+ end)
-  std::vector<uint64_t> level_r1prefix0, level_r1chunks;
+  std::vector<uint64_t> level_r1prefix0, level_r1chunks, level_r1chunk0;
+  uint32_t* d_r1chunk_item = nullptr;   // per trace chunk: its item within the level
   // expanding buckets of each level (expand_kernel)
   qtn::XDesc* d_xdesc = nullptr;
   uint32_t* d_xitem_desc = nullptr;
@@ -718,7 +719,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_hbm_rec, (void*)B->d_sitem_desc, (void*)B->d_sitem_net,
                   (void*)B->d_red, (void*)B->d_red_prefix, (void*)B->d_xdesc,
                   (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix,
-                  (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix,
+                  (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix, (void*)B->d_r1chunk_item,
                   (void*)B->d_fdesc, (void*)B->d_fitem_desc, (void*)B->d_fitem_net,
                   (void*)B->d_fprefix, (void*)B->d_cprefix, (void*)B->d_ftab,
                   (void*)B->d_fctas, (void*)B->d_fblob,
@@ -922,6 +923,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   const int trace_min_r = tmr ? atoi(tmr) : 8;
   std::vector<qtn::R1Dev> r1items;
   std::vector<uint64_t> r1prefix;
+  std::vector<uint32_t> r1chunk_item;
   for (int32_t lev = 0; lev < max_lev; ++lev) {
     B->level_item0.push_back((uint32_t)item_desc.size());
     B->level_prefix0.push_back(prefix.size());
@@ -930,6 +932,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     B->level_xprefix0.push_back(xprefix.size());
     B->level_r1item0.push_back((uint32_t)r1items.size());
     B->level_r1prefix0.push_back(r1prefix.size());
+    B->level_r1chunk0.push_back(r1chunk_item.size());
     uint64_t acc = 0, xacc = 0, r1acc = 0;
     uint32_t xstage = 0;
     prefix.push_back(0);
@@ -1003,7 +1006,10 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
           qtn::R1Dev r = P->hbm_r1[P->hbm_r1idx[bi]];
           r.net = (uint32_t)h;
           r1items.push_back(r);
-          r1acc += ((1ull << r.R) + qtn::kTraceChunk - 1) / qtn::kTraceChunk;
+          const uint64_t nck = ((1ull << r.R) + qtn::kTraceChunk - 1) / qtn::kTraceChunk;
+          for (uint64_t c = 0; c < nck; ++c)  // chunk -> item (level-relative): no search per CTA
+            r1chunk_item.push_back((uint32_t)(r1items.size() - 1 - B->level_r1item0.back()));
+          r1acc += nck;
           r1prefix.push_back(r1acc);
           continue;
         }
@@ -1113,6 +1119,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_xitem_net, xitem_net)) || (rc = upload(&B->d_xprefix, xprefix)) ||
       (rc = upload(&B->d_level_sitem0, B->level_sitem0)) ||
       (rc = upload(&B->d_r1, r1items)) || (rc = upload(&B->d_r1prefix, r1prefix)) ||
+      (rc = upload(&B->d_r1chunk_item, r1chunk_item)) ||
       (rc = upload(&B->d_fdesc, fdescs)) || (rc = upload(&B->d_fitem_desc, fitem_desc)) ||
       (rc = upload(&B->d_ftab, ftabs)) || (rc = upload(&B->d_fctas, fctas)) ||
       (rc = upload(&B->d_fblob, fblob)) ||
@@ -1642,7 +1649,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         if (!B->level_r1chunks[lev]) return QTN_OK;
         return qtn::launch_trace(L, B->d_r1 + B->level_r1item0[lev], B->d_r1prefix + B->level_r1prefix0[lev],
                                  B->level_r1item0[lev + 1] - B->level_r1item0[lev], B->level_r1chunks[lev],
-                                 next_stream());
+                                 next_stream(), B->d_r1chunk_item + B->level_r1chunk0[lev]);
       };
       auto l_expand = [&]() -> int {
         if (!B->level_xtiles[lev]) return QTN_OK;

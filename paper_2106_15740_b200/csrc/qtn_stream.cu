@@ -360,15 +360,21 @@ __device__ __forceinline__ void trace_staged(const R1Dev& r, const Bases& b, con
 __global__ void __launch_bounds__(256, 8) trace_kernel(const __grid_constant__ StreamLaunch L,
                                                     const R1Dev* __restrict__ items,
                                                     const uint64_t* __restrict__ prefix,
-                                                    uint32_t n_items) {
+                                                    uint32_t n_items,
+                                                    const uint32_t* __restrict__ chunk_item) {
   pdl_trigger();
   pdl_wait();
   const uint64_t cb = blockIdx.x;
-  uint32_t lo = 0, hi = n_items;  // last item whose first chunk <= cb
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (prefix[mid] <= cb) lo = mid;
-    else hi = mid;
+  uint32_t lo = 0;
+  if (chunk_item) {
+    lo = chunk_item[cb];
+  } else {
+    uint32_t hi = n_items;  // last item whose first chunk <= cb
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (prefix[mid] <= cb) lo = mid;
+      else hi = mid;
+    }
   }
   const R1Dev& r = items[lo];
   const uint32_t set = blockIdx.y;
@@ -461,14 +467,15 @@ __global__ void __launch_bounds__(256, 8) trace_kernel(const __grid_constant__ S
 }
 
 int launch_trace(const StreamLaunch& L, const R1Dev* items, const uint64_t* prefix,
-                 uint32_t n_items, uint64_t total_chunks, void* stream) {
+                 uint32_t n_items, uint64_t total_chunks, void* stream, const uint32_t* chunk_item) {
   if (!n_items || !total_chunks || !L.n_sets) return QTN_OK;
   if (total_chunks > 0x7fffffffull || L.n_sets > 65535) {
     set_error("trace_kernel: grid too large");
     return QTN_EINVAL;
   }
   cudaError_t e = launch_pdl<true>(trace_kernel, dim3((uint32_t)total_chunks, L.n_sets), dim3(256), 0,
-                                   reinterpret_cast<cudaStream_t>(stream), L, items, prefix, n_items);
+                                   reinterpret_cast<cudaStream_t>(stream), L, items, prefix, n_items,
+                                   chunk_item);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("trace_kernel launch: ") + cudaGetErrorString(e));

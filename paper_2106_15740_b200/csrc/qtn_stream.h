@@ -261,8 +261,10 @@ struct R1Dev {
   R1Stage st[kR1MaxS];
 };
 constexpr uint32_t kTraceChunk = 4096;
+// chunk_item (optional): the item of each chunk (no search over the prefix)
 int launch_trace(const StreamLaunch& L, const R1Dev* items, const uint64_t* prefix,
-                 uint32_t n_items, uint64_t total_chunks, void* stream);
+                 uint32_t n_items, uint64_t total_chunks, void* stream,
+                 const uint32_t* chunk_item = nullptr);
 
 // ---- fused product chains: a bucket of >= 2 operands whose result is then
 // reduced by k single-operand buckets (partial traces) is one contraction
