@@ -172,8 +172,9 @@ __host__ __device__ inline FLayout fused_layout(const FDesc& d) {
 // the product of one staged entry per varying side (32-bit shared addresses:
 // thread base + js part + slot part).
 // (side tables: sj[s * sstr + js] = summed part, sj[s * sstr + njs + a] = slot part)
-// G0: side 0 is streamed from global memory (element offsets, base g0)
-template <typename C, int NS, int NA, bool G0>
+// G0: side 0 is streamed from global memory (element offsets, base g0);
+// A0: side 0 does not depend on the in-thread output slots
+template <typename C, int NS, int NA, bool G0, bool A0 = false>
 __device__ __forceinline__ void stage_terms(const uint32_t* sj, uint32_t sstr, const uint32_t* cb,
                                             uint32_t njs, C (&ps)[kAcc], const C* g0) {
   uint32_t jta[NS][1 << NA];
@@ -187,9 +188,15 @@ __device__ __forceinline__ void stage_terms(const uint32_t* sj, uint32_t sstr, c
 #pragma unroll
     for (int s = 0; s < NS; ++s) off[s] = cb[s] + sj[s * sstr + js];
     C v0[1 << NA];
+    if (!G0 && A0) {  // side 0 does not depend on the slot bits: one load for every slot
+      const C v = lds_c(off[0], (C*)nullptr);
 #pragma unroll
-    for (int a = 0; a < (1 << NA); ++a)  // the streamed loads of all slots first
-      v0[a] = G0 ? __ldg(g0 + off[0] + jta[0][a]) : lds_c(off[0] + jta[0][a], (C*)nullptr);
+      for (int a = 0; a < (1 << NA); ++a) v0[a] = v;
+    } else {
+#pragma unroll
+      for (int a = 0; a < (1 << NA); ++a)  // the streamed loads of all slots first
+        v0[a] = G0 ? __ldg(g0 + off[0] + jta[0][a]) : lds_c(off[0] + jta[0][a], (C*)nullptr);
+    }
 #pragma unroll
     for (int a = 0; a < (1 << NA); ++a) {
       C p = v0[a];
@@ -202,7 +209,15 @@ __device__ __forceinline__ void stage_terms(const uint32_t* sj, uint32_t sstr, c
 template <typename C, int NS, bool G0>
 __device__ __forceinline__ void stage_terms_na(uint32_t na, const uint32_t* sj, uint32_t sstr,
                                                const uint32_t* cb, uint32_t njs, C (&ps)[kAcc],
-                                               const C* g0) {
+                                               const C* g0, bool a0 = false) {
+  if (!G0 && a0 && NS == 2) {  // the common GEMM shape: side 0 shared by every slot
+    switch (na) {
+      case 0: stage_terms<C, NS, 0, false, true>(sj, sstr, cb, njs, ps, g0); break;
+      case 1: stage_terms<C, NS, 1, false, true>(sj, sstr, cb, njs, ps, g0); break;
+      default: stage_terms<C, NS, 2, false, true>(sj, sstr, cb, njs, ps, g0); break;
+    }
+    return;
+  }
   switch (na) {
     case 0: stage_terms<C, NS, 0, G0>(sj, sstr, cb, njs, ps, g0); break;
     case 1: stage_terms<C, NS, 1, G0>(sj, sstr, cb, njs, ps, g0); break;
@@ -412,7 +427,7 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
         switch (nv) {
           case 0: ps[0] = C{1, 0}; break;
           case 1: stage_terms_na<C, 1, false>(na, sj, sstr, cb, njs, ps, nullptr); break;
-          case 2: stage_terms_na<C, 2, false>(na, sj, sstr, cb, njs, ps, nullptr); break;
+          case 2: stage_terms_na<C, 2, false>(na, sj, sstr, cb, njs, ps, nullptr, d.sides[0].aind != 0); break;
           case 3: stage_terms_na<C, 3, false>(na, sj, sstr, cb, njs, ps, nullptr); break;
           case 4: stage_terms_na<C, 4, false>(na, sj, sstr, cb, njs, ps, nullptr); break;
           default: stage_terms_any<C>(nv, na, sj, sstr, cb, njs, ps); break;

@@ -770,6 +770,11 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
     S.kind = side_kind(sides[si], tile);
     if (S.kind == kFSideStream && si != 0) S.kind = kFSideRaw;  // only side 0 streams
     S.tconst = (sdep & inthr) == 0 ? 1 : 0;
+    {
+      uint64_t slots = 0;  // in-thread output bits (q positions [nthr, nto))
+      for (int i = nthr; i < nto; ++i) slots |= 1ull << qb[i];
+      S.aind = (sdep & slots) == 0 ? 1 : 0;
+    }
     for (int t : sides[si]) {
       FOp& o = d.ops[slot[t]];
       o.ptr = s.optag[t];

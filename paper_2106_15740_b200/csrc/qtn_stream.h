@@ -316,7 +316,8 @@ struct FOp {
 // global memory (coalesced), so the stage holds only reused operands
 constexpr uint8_t kFSideRaw = 0, kFSideConv = 1, kFSideProd = 2, kFSideStream = 3;
 struct FSide {
-  uint8_t nst, n_qrun, kind, first_op, n_ops, tconst, pad[2];  // tconst: no in-thread bits
+  uint8_t nst, n_qrun, kind, first_op, n_ops, tconst, aind, pad;  // tconst: no in-thread bits;
+                                                                  // aind: independent of the slot bits
   uint32_t st_off;                    // byte offset of the side's region in a stage buffer
   uint32_t qrun[kFQRuns];             // tile index (q) bits -> side compact bits
   uint32_t pad2;
