@@ -478,8 +478,6 @@ __device__ __forceinline__ void fused_body(const FDesc& d, const uint32_t* tabs,
   }
 }
 
-constexpr uint32_t kFHdrBytes = offsetof(FDesc, ops);
-
 // 3 CTAs per SM (80 registers; the complex128-math variant spills ~260 bytes,
 // measured equal to 2 CTAs per SM without spills)
 template <typename C>

@@ -1537,6 +1537,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       const char* pv = getenv("QTN_PDL_SINGLE");
       pdl_single_env = (pv && pv[0] == '1') ? 1 : 0;
     }
+    qtn::g_pdl_next = false;         // a clean state even after an earlier failed call
     bool prev_single_small = false;  // the previous level was one small_kernel launch
     bool prev_single = false;        // the previous level was one launch
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
