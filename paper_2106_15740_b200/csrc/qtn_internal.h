@@ -237,6 +237,9 @@ struct qtn_plan {
   std::vector<uint64_t> hbm_sub_desc;    // member descriptor byte offsets (hbm_desc), in order
   std::vector<qtn::FDesc> hbm_fdesc;     // fused product chains (qtn_fused.cu)
   std::vector<int32_t> hbm_flevel;       // their levels
+  std::vector<uint8_t> hbm_wblob;        // warp-granular forms of the fused chains (qtn_fusedw.cu)
+  std::vector<int64_t> hbm_woff;         // per fused chain: its blob offset, or -1 (CTA kernel only)
+  std::vector<uint32_t> hbm_wwarps;      // per fused chain: warps of one set (0: none)
   int32_t n_levels = 0;
   // Set-major form of an SMEM-eligible network (qtn_setmajor.cu): angle
   // sets are the fastest-varying dimension of every tensor in HBM, one

@@ -665,8 +665,11 @@ struct qtn_batch {
     uint64_t cta0;                      // first per-CTA record (fused_kernel)
     uint32_t smem;
     uint8_t f64;
+    uint8_t warp;                       // warp-granular chains (fusedw_kernel): recs [cta0, cta0 + ctas)
   };
   std::vector<FGroup> fgroups;
+  uint8_t* d_wblob = nullptr;           // warp-granular chain blobs (qtn_fusedw.cu)
+  qtn::WRec* d_wrecs = nullptr;         // one record per warp of one set
   std::vector<uint32_t> level_fgroup0;  // first group of each level (+ end)
   std::vector<uint64_t> level_fctas;    // fused CTAs of one set per level (0: none)
   // tiny subtrees per level (subtree_kernel)
@@ -687,9 +690,18 @@ struct qtn_batch {
   // concurrent launches of one HBM level (independent buckets): side
   // streams forked from / joined into the caller's stream with events
   static constexpr int kSide = 7;  // up to 8 concurrent launches per level
-  cudaStream_t side[kSide] = {};
-  cudaEvent_t ev_fork = nullptr;
-  cudaEvent_t ev_join[kSide] = {};
+  // network groups (QTN_HBM_GROUPS): each an independent level sequence on
+  // its own stream lane (group 0: the caller's stream), with its own side
+  // streams for the concurrent launches of a level
+  static constexpr int kMaxGroups = 4;
+  int n_groups = 1;
+  int32_t lev_per_group = 0;
+  cudaStream_t gside[kMaxGroups][kSide] = {};
+  cudaEvent_t gfork[kMaxGroups] = {};
+  cudaEvent_t gjoin[kMaxGroups][kSide] = {};
+  cudaStream_t lane[kMaxGroups] = {};
+  cudaEvent_t ev_lanes = nullptr;
+  cudaEvent_t ev_lane_done[kMaxGroups] = {};
   // pinned staging of qtn_batch_energies_host
   double* pin = nullptr;
   size_t pin_doubles = 0;
@@ -705,11 +717,16 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
   for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
   for (auto& kv : B->egraphs) cudaGraphExecDestroy(kv.second);
   if (B->cap_stream) cudaStreamDestroy(B->cap_stream);
-  for (int k = 0; k < qtn_batch::kSide; ++k) {
-    if (B->side[k]) cudaStreamDestroy(B->side[k]);
-    if (B->ev_join[k]) cudaEventDestroy(B->ev_join[k]);
+  for (int g = 0; g < qtn_batch::kMaxGroups; ++g) {
+    for (int k = 0; k < qtn_batch::kSide; ++k) {
+      if (B->gside[g][k]) cudaStreamDestroy(B->gside[g][k]);
+      if (B->gjoin[g][k]) cudaEventDestroy(B->gjoin[g][k]);
+    }
+    if (B->gfork[g]) cudaEventDestroy(B->gfork[g]);
+    if (B->lane[g]) cudaStreamDestroy(B->lane[g]);
+    if (B->ev_lane_done[g]) cudaEventDestroy(B->ev_lane_done[g]);
   }
-  if (B->ev_fork) cudaEventDestroy(B->ev_fork);
+  if (B->ev_lanes) cudaEventDestroy(B->ev_lanes);
   if (B->pin) cudaFreeHost(B->pin);
   for (void* p : {(void*)B->d_prog, (void*)B->d_prog_off, (void*)B->d_in_off,
                   (void*)B->d_smem_index, (void*)B->d_desc, (void*)B->d_item_desc,
@@ -718,6 +735,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_fold_first, (void*)B->d_fold_pow2, (void*)B->d_hbm_index,
                   (void*)B->d_hbm_rec, (void*)B->d_sitem_desc, (void*)B->d_sitem_net,
                   (void*)B->d_red, (void*)B->d_red_prefix, (void*)B->d_xdesc,
+                  (void*)B->d_wblob, (void*)B->d_wrecs,
                   (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix,
                   (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix, (void*)B->d_r1chunk_item,
                   (void*)B->d_fdesc, (void*)B->d_fitem_desc, (void*)B->d_fitem_net,
@@ -794,6 +812,31 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     if (av && av[0] == '1')
       for (int h = 0; h < B->n_hbm; ++h) hshift[h] = max_lev - plans[hidx[h]]->n_levels;
   }
+  // QTN_HBM_GROUPS=G: the networks in G groups (LPT on algorithmic bytes),
+  // each group an independent sequence of levels on its own stream lane, so
+  // one group's latency-bound launches overlap another group's streaming
+  // ones instead of every level waiting for its slowest launch.  Virtual
+  // level = group * max_lev + level (the per-level lists below are built
+  // over virtual levels).
+  {
+    const char* gv = getenv("QTN_HBM_GROUPS");
+    int G = gv ? atoi(gv) : 1;
+    G = std::max(1, std::min(G, qtn_batch::kMaxGroups));
+    if (B->n_hbm < 2 * G) G = 1;
+    std::vector<int> ord(B->n_hbm);
+    for (int h = 0; h < B->n_hbm; ++h) ord[h] = h;
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](int a, int b) { return plans[hidx[a]]->alg_bytes > plans[hidx[b]]->alg_bytes; });
+    std::vector<double> load(G, 0.0);
+    for (int h : ord) {
+      const int g = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[g] += plans[hidx[h]]->alg_bytes;
+      hshift[h] += g * max_lev;
+    }
+    B->n_groups = G;
+    B->lev_per_group = max_lev;
+    max_lev *= G;
+  }
   // level-major item lists over all HBM networks
   std::vector<uint64_t> item_desc, prefix, sitem_desc;
   std::vector<uint32_t> item_net, sitem_net;
@@ -863,9 +906,44 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   std::vector<uint32_t> fitem_desc, fitem_net;
   std::vector<uint64_t> fprefix, cprefix;
   std::vector<qtn::FCta> fctas;
+  // warp-granular chains: the plans' blobs concatenated (16-byte aligned)
+  std::vector<uint8_t> wblob;
+  std::vector<uint64_t> wblob_base(B->n_hbm);
+  for (int h = 0; h < B->n_hbm; ++h) {
+    const qtn_plan* P = plans[hidx[h]];
+    while (wblob.size() & 15u) wblob.push_back(0);
+    wblob_base[h] = wblob.size();
+    wblob.insert(wblob.end(), P->hbm_wblob.begin(), P->hbm_wblob.end());
+  }
+  std::vector<qtn::WRec> wrecs;
   for (int32_t lev = 0; lev < max_lev; ++lev) {
     B->level_fgroup0.push_back((uint32_t)B->fgroups.size());
     uint64_t lev_ctas = 0;
+    for (int mt = 0; mt < 2; ++mt) {  // warp-granular chains of this math type
+      qtn_batch::FGroup g{};
+      g.warp = 1;
+      g.f64 = (uint8_t)mt;
+      g.cta0 = wrecs.size();
+      for (int h = 0; h < B->n_hbm; ++h) {
+        const qtn_plan* P = plans[hidx[h]];
+        for (size_t f = 0; f < P->hbm_fdesc.size(); ++f) {
+          const qtn::FDesc& fd = P->hbm_fdesc[f];
+          if (P->hbm_flevel[f] + hshift[h] != lev || (fd.math_f32 ? 0 : 1) != mt || P->hbm_woff[f] < 0) continue;
+          const uint64_t b16 = (wblob_base[h] + (uint64_t)P->hbm_woff[f]) / 16u;
+          for (uint32_t c = 0; c < P->hbm_wwarps[f]; ++c) {
+            qtn::WRec r{};
+            r.blob16 = (uint32_t)b16;
+            r.chunk = c;
+            r.net = (uint32_t)h;
+            wrecs.push_back(r);
+          }
+          g.n_items += 1;
+        }
+      }
+      g.ctas = wrecs.size() - g.cta0;
+      if (g.n_items) B->fgroups.push_back(g);
+      lev_ctas += (g.ctas + 7) / 8;
+    }
     for (int mt = 0; mt < 2; ++mt) {  // complex64 math, then complex128 math
       qtn_batch::FGroup g{};
       g.item0 = (uint32_t)fitem_desc.size();
@@ -879,7 +957,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
         const qtn_plan* P = plans[hidx[h]];
         for (size_t f = 0; f < P->hbm_fdesc.size(); ++f) {
           const qtn::FDesc& fd = P->hbm_fdesc[f];
-          if (P->hbm_flevel[f] + hshift[h] != lev || (fd.math_f32 ? 0 : 1) != mt) continue;
+          if (P->hbm_flevel[f] + hshift[h] != lev || (fd.math_f32 ? 0 : 1) != mt || P->hbm_woff[f] >= 0) continue;
           fitem_desc.push_back(fdesc_base[h] + (uint32_t)f);
           fitem_net.push_back((uint32_t)h);
           const uint64_t nc = fd.sk ? (fd.n_units << fd.sk) : (fd.n_units + (1ull << fd.upc_log2) - 1) >> fd.upc_log2;
@@ -1087,7 +1165,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     };
     for (size_t l = 0; chain_on && l < nl;) {
       size_t e = l;
-      while (e < nl && tiny_only(e)) ++e;
+      while (e < nl && tiny_only(e) && (!B->lev_per_group || e / B->lev_per_group == l / B->lev_per_group)) ++e;
       if (e - l >= 2) B->chain_len[l] = (uint32_t)(e - l);
       l = e > l ? e : l + 1;
     }
@@ -1122,7 +1200,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_r1chunk_item, r1chunk_item)) ||
       (rc = upload(&B->d_fdesc, fdescs)) || (rc = upload(&B->d_fitem_desc, fitem_desc)) ||
       (rc = upload(&B->d_ftab, ftabs)) || (rc = upload(&B->d_fctas, fctas)) ||
-      (rc = upload(&B->d_fblob, fblob)) ||
+      (rc = upload(&B->d_fblob, fblob)) || (rc = upload(&B->d_wblob, wblob)) || (rc = upload(&B->d_wrecs, wrecs)) ||
       (rc = upload(&B->d_sub_items, sub_items)) || (rc = upload(&B->d_sub_desc, sub_desc)) ||
       (rc = upload(&B->d_fitem_net, fitem_net)) || (rc = upload(&B->d_fprefix, fprefix)) ||
       (rc = upload(&B->d_cprefix, cprefix)) ||
@@ -1518,14 +1596,30 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     // back before the next level starts.
     const char* lsv = getenv("QTN_LEVEL_STREAMS");
     const bool level_streams = !(lsv && lsv[0] == '0');
-    if (level_streams && !B->ev_fork) {
-      cudaError_t e = cudaEventCreateWithFlags(&B->ev_fork, cudaEventDisableTiming);
-      for (int k = 0; k < qtn_batch::kSide && e == cudaSuccess; ++k) {
-        e = cudaStreamCreateWithFlags(&B->side[k], cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&B->ev_join[k], cudaEventDisableTiming);
+    const int G = B->n_groups;
+    for (int g = 0; g < G; ++g) {
+      if (level_streams && !B->gfork[g]) {
+        cudaError_t e = cudaEventCreateWithFlags(&B->gfork[g], cudaEventDisableTiming);
+        for (int k = 0; k < qtn_batch::kSide && e == cudaSuccess; ++k) {
+          e = cudaStreamCreateWithFlags(&B->gside[g][k], cudaStreamNonBlocking);
+          if (e == cudaSuccess) e = cudaEventCreateWithFlags(&B->gjoin[g][k], cudaEventDisableTiming);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "level streams");
       }
-      if (e != cudaSuccess) return cuda_fail(e, "level streams");
+      if (g > 0 && !B->lane[g]) {
+        cudaError_t e = cudaStreamCreateWithFlags(&B->lane[g], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&B->ev_lane_done[g], cudaEventDisableTiming);
+        if (e == cudaSuccess && !B->ev_lanes) e = cudaEventCreateWithFlags(&B->ev_lanes, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "group lanes");
+      }
     }
+    if (G > 1) {  // the lanes start after everything before the evaluation
+      cudaEventRecord(B->ev_lanes, st);
+      for (int g = 1; g < G; ++g) cudaStreamWaitEvent(B->lane[g], B->ev_lanes, 0);
+    }
+    int cur_g = -1;
+    cudaStream_t gst = st;       // the current group's lane
+    void* gstream = stream;
     static int pdl_tiny_env = -1;
     if (pdl_tiny_env < 0) {
       const char* pv = getenv("QTN_PDL_TINY");
@@ -1541,6 +1635,15 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
     bool prev_single_small = false;  // the previous level was one small_kernel launch
     bool prev_single = false;        // the previous level was one launch
     for (size_t lev = 0; lev < B->level_tiles.size(); ++lev) {
+      const int g = B->lev_per_group ? (int)(lev / (size_t)B->lev_per_group) : 0;
+      if (g != cur_g) {  // the next group: its own lane, a clean PDL state
+        cur_g = g;
+        gst = g ? B->lane[g] : st;
+        gstream = reinterpret_cast<void*>(gst);
+        prev_single_small = false;
+        prev_single = false;
+        qtn::g_pdl_next = false;
+      }
       // launches of this level, in issue order: reduce, small, trace, expand, stream
       const uint32_t nsub = B->level_sub0[lev + 1] - B->level_sub0[lev];
       const int n_launch = (int)(B->level_fgroup0[lev + 1] - B->level_fgroup0[lev]) + (nsub ? 1 : 0) +
@@ -1552,15 +1655,15 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       // one launch after one launch: PDL for it (QTN_PDL_SINGLE=1; tiny
       // small_kernel levels take it by default below)
       qtn::g_pdl_next = pdl_single_env == 1 && n_launch == 1 && prev_single;
-      int slot = 0;  // launch k of the level goes to stream k (0: the caller's)
+      int slot = 0;  // launch k of the level goes to stream k (0: the group's lane)
       auto next_stream = [&]() -> void* {
-        if (!fork) return stream;
-        const int k = slot++;
-        if (k == 0) return stream;
-        cudaStreamWaitEvent(B->side[k - 1], B->ev_fork, 0);
-        return reinterpret_cast<void*>(B->side[k - 1]);
+        if (!fork) return gstream;
+        const int k = std::min(slot++, (int)qtn_batch::kSide);  // more launches than side streams: share the last
+        if (k == 0) return gstream;
+        cudaStreamWaitEvent(B->gside[g][k - 1], B->gfork[g], 0);
+        return reinterpret_cast<void*>(B->gside[g][k - 1]);
       };
-      if (fork) cudaEventRecord(B->ev_fork, st);
+      if (fork) cudaEventRecord(B->gfork[g], gst);
       StreamLaunch L;
       std::memset(&L, 0, sizeof(L));
       L.descs = B->d_desc;
@@ -1576,7 +1679,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         Lc.item_desc = B->d_sitem_desc;
         Lc.item_net = B->d_sitem_net;
         Lc.n_items = B->level_sitem0.back();
-        if ((rc = qtn::launch_chain(Lc, B->d_level_sitem0 + lev, B->chain_len[lev], stream)))
+        if ((rc = qtn::launch_chain(Lc, B->d_level_sitem0 + lev, B->chain_len[lev], gstream)))
           return rc;
         lev += B->chain_len[lev] - 1;
         prev_single_small = false;
@@ -1598,6 +1701,24 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
       auto l_fused = [&]() -> int {
         for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi) {
           const qtn_batch::FGroup& g = B->fgroups[gi];
+          if (g.warp) {
+            qtn::WLaunch W;
+            std::memset(&W, 0, sizeof(W));
+            W.blob = B->d_wblob;
+            W.recs = B->d_wrecs + g.cta0;
+            W.n_warps = (uint32_t)g.ctas;
+            W.n_sets = (uint32_t)n_sets;
+            W.f64 = g.f64;
+            W.in_base = L.in_base;
+            W.in_set_stride = L.in_set_stride;
+            W.net_in_off = L.net_in_off;
+            W.ws_base = L.ws_base;
+            W.ws_set_stride = L.ws_set_stride;
+            W.net_ws_off = L.net_ws_off;
+            const int r2 = qtn::launch_fusedw(W, next_stream());
+            if (r2) return r2;
+            continue;
+          }
           qtn::FLaunch F;
           std::memset(&F, 0, sizeof(F));
           F.descs = B->d_fdesc;
@@ -1702,13 +1823,17 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
           return rc;
       }
       // join: the next level (or the fold) waits for every branch
-      for (int k = 1; k < slot; ++k) {
-        cudaEventRecord(B->ev_join[k - 1], B->side[k - 1]);
-        cudaStreamWaitEvent(st, B->ev_join[k - 1], 0);
+      for (int k = 1; k < std::min(slot, (int)qtn_batch::kSide + 1); ++k) {
+        cudaEventRecord(B->gjoin[g][k - 1], B->gside[g][k - 1]);
+        cudaStreamWaitEvent(gst, B->gjoin[g][k - 1], 0);
       }
       prev_single_small = n_launch == 1 && ns != 0;
       prev_single = n_launch == 1;
       qtn::g_pdl_next = false;
+    }
+    for (int g = 1; g < G; ++g) {  // join the lanes
+      cudaEventRecord(B->ev_lane_done[g], B->lane[g]);
+      cudaStreamWaitEvent(st, B->ev_lane_done[g], 0);
     }
     dim3 grid((B->n_hbm + 127) / 128, n_sets);
     cudaError_t e = launch_pdl<true>(

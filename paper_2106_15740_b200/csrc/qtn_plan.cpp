@@ -624,6 +624,8 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
   static const int fupc = getenv("QTN_FUPC") ? atoi(getenv("QTN_FUPC")) : 16;
   static const int fsplit = getenv("QTN_FSPLIT") ? atoi(getenv("QTN_FSPLIT")) : 16;
   static const int fmaxq = getenv("QTN_FMAXQ") ? atoi(getenv("QTN_FMAXQ")) : kFMaxQ;
+  // log2 of the CTAs an item keeps at least before units are packed per CTA
+  static const int fmin_units = getenv("QTN_FMIN_UNITS") ? atoi(getenv("QTN_FMIN_UNITS")) : 9;
   auto esz = [&](int t) { return s.opc64[t] ? 8u : 16u; };
   auto make_sides = [&](uint64_t tl) {
     std::vector<int> ord(n);
@@ -848,7 +850,7 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
   int upc = 0;
   if (!sk) {
     upc = std::max(0, fupc - (nq + nl));
-    upc = std::min(upc, std::max(0, ng - 9));
+    upc = std::min(upc, std::max(0, ng - fmin_units));
   }
   d.upc_log2 = (uint8_t)upc;
   d.sk = (uint8_t)sk;
@@ -867,6 +869,117 @@ bool encode_fused_desc(const FChainSpec& s, FDesc& d) {
             R, K, n, (int)sides.size(), n_var, nq, nto, ng, nl, off, upc, sk, (int)d.has_finish, sm.c_str());
   }
   return true;
+}
+
+// Warp-granular fused chain (qtn_stream.h WHdr, kernel in qtn_fusedw.cu):
+// lanes = output bits 0..4, NI = 8 in-lane slots over 3 output bits the
+// widest operand does not depend on (then the lowest others) when R >= 8,
+// the remaining output bits index the chain's warps (chunks).
+uint32_t encode_warp_chain(const FChainSpec& s, std::vector<uint8_t>& blob) {
+  const int R = (int)s.out_vars.size(), K = (int)s.summed.size(), n = (int)s.opvars.size();
+  if (n < 2 || n > kWMaxOps || R < 5 || K < 1 || K > kWMaxK) return 0;
+  const int ni_log2 = R >= 7 ? 2 : 0;
+  const int nc = R - 5 - ni_log2;  // chunk bits
+  if (nc > 24) return 0;
+  auto ubit = [&](int32_t u) -> int {
+    for (int i = 0; i < R; ++i)
+      if (s.out_vars[i] == u) return R - 1 - i;
+    for (int j = 0; j < K; ++j)
+      if (s.summed[j] == u) return R + j;
+    return -1;
+  };
+  std::vector<std::vector<int>> opbit(n, std::vector<int>(R + K, -1));  // U bit -> operand bit
+  int widest = 0;
+  for (int t = 0; t < n; ++t) {
+    const auto& vs = s.opvars[t];
+    const int rk = (int)vs.size();
+    if (rk > 32) return 0;
+    for (int j = 0; j < rk; ++j) {
+      const int b = ubit(vs[j]);
+      if (b < 0) return 0;
+      opbit[t][b] = rk - 1 - j;
+    }
+    if (vs.size() > s.opvars[widest].size()) widest = t;
+  }
+  std::vector<int> slot, chunkb;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int b = 5; b < R && (int)slot.size() < ni_log2; ++b) {
+      if (std::find(slot.begin(), slot.end(), b) != slot.end()) continue;
+      if (pass == 0 && opbit[widest][b] >= 0) continue;
+      slot.push_back(b);
+    }
+  for (int b = 5; b < R; ++b)
+    if (std::find(slot.begin(), slot.end(), b) == slot.end()) chunkb.push_back(b);
+  const int ni = 1 << ni_log2, nsv = 1 << K;
+  WHdr h;
+  std::memset(&h, 0, sizeof(h));
+  h.out = s.out_tag;
+  h.R = (uint8_t)R;
+  h.K = (uint8_t)K;
+  h.n_ops = (uint8_t)n;
+  h.out_c64 = s.out_c64 ? 1 : 0;
+  h.math_f32 = s.math_f32 ? 1 : 0;
+  h.ni_log2 = (uint8_t)ni_log2;
+  h.match = 1;
+  std::vector<uint32_t> runs;
+  {
+    std::vector<std::pair<int, int>> pr;
+    for (size_t j = 0; j < chunkb.size(); ++j) pr.push_back({(int)j, chunkb[j]});
+    make_runs(pr, runs);
+    if ((int)runs.size() > kWRuns) return 0;
+    std::copy(runs.begin(), runs.end(), h.ocrun);
+    h.n_ocrun = (uint8_t)runs.size();
+  }
+  for (int i = 0; i < ni; ++i) {
+    uint32_t o = 0;
+    for (int j = 0; j < ni_log2; ++j)
+      if ((i >> j) & 1) o |= 1u << slot[j];
+    h.slot_out[i] = o;
+  }
+  std::vector<WOpRec> recs(n);
+  std::vector<uint32_t> tabs;  // words after the header and op records
+  const uint32_t tab0 = (uint32_t)((sizeof(WHdr) + n * sizeof(WOpRec)) / 4);
+  for (int t = 0; t < n; ++t) {
+    WOpRec& o = recs[t];
+    std::memset(&o, 0, sizeof(o));
+    o.ptr = s.optag[t];
+    o.c64 = s.opc64[t];
+    if ((o.c64 != 0) != s.math_f32) h.match = 0;
+    std::vector<std::pair<int, int>> pr;
+    for (size_t j = 0; j < chunkb.size(); ++j)
+      if (opbit[t][chunkb[j]] >= 0) pr.push_back({(int)j, opbit[t][chunkb[j]]});
+    make_runs(pr, runs);
+    if ((int)runs.size() > kWRuns) return 0;
+    std::copy(runs.begin(), runs.end(), o.crun);
+    o.n_crun = (uint8_t)runs.size();
+    o.inv = 1;
+    for (int b : slot)
+      if (opbit[t][b] >= 0) o.inv = 0;
+    auto off = [&](uint64_t bits_u) {  // operand offset of a set of U bits
+      uint64_t x = 0;
+      for (int b = 0; b < R + K; ++b)
+        if (((bits_u >> b) & 1) && opbit[t][b] >= 0) x |= 1ull << opbit[t][b];
+      return (uint32_t)x;
+    };
+    o.lane_off = tab0 + (uint32_t)tabs.size();
+    for (uint32_t l = 0; l < 32; ++l) tabs.push_back(off(l));
+    o.slot_off = tab0 + (uint32_t)tabs.size();
+    for (int i = 0; i < ni; ++i) tabs.push_back(off(h.slot_out[i]));
+    o.hs_off = tab0 + (uint32_t)tabs.size();
+    for (int sv = 0; sv < nsv; ++sv) tabs.push_back(off((uint64_t)sv << R));
+  }
+  while (tabs.size() & 3u) tabs.push_back(0u);
+  const size_t at = (blob.size() + 15) & ~(size_t)15;
+  blob.resize(at, 0);
+  const uint8_t* hb = reinterpret_cast<const uint8_t*>(&h);
+  blob.insert(blob.end(), hb, hb + sizeof(h));
+  for (const auto& o : recs) {
+    const uint8_t* ob = reinterpret_cast<const uint8_t*>(&o);
+    blob.insert(blob.end(), ob, ob + sizeof(o));
+  }
+  const uint8_t* tb = reinterpret_cast<const uint8_t*>(tabs.data());
+  blob.insert(blob.end(), tb, tb + 4 * tabs.size());
+  return 1u << nc;
 }
 
 }  // namespace qtn
@@ -1488,6 +1601,10 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     };
     P->hbm_xidx.assign(nb, -1);
     P->hbm_r1idx.assign(nb, -1);
+    const char* fwv = getenv("QTN_FWARP");
+    const bool fwarp_on = !(fwv && fwv[0] == '0');
+    const char* fwt = getenv("QTN_FWARP_MAX_T");
+    const int fwarp_max_t = fwt ? atoi(fwt) : 12;
     for (int bi = 0; bi < nb; ++bi) {
       const auto& b = P->buckets[bi];
       P->hbm_desc_off.push_back(P->hbm_desc.size());
@@ -1520,6 +1637,18 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
           if (fd.sk) fd.part = tag_ws((uint64_t)fpart_off[bi]);
           P->hbm_fdesc.push_back(fd);
           P->hbm_flevel.push_back(P->hbm_level[bi]);
+          // warp-granular form (the executor picks one of the two at batch
+          // creation): chains of up to QTN_FWARP_MAX_T log2 terms
+          int64_t woff = -1;
+          uint32_t nw = 0;
+          if (fwarp_on && out.rank() + (int)fs.summed.size() <= fwarp_max_t) {
+            while (P->hbm_wblob.size() & 15u) P->hbm_wblob.push_back(0);
+            const size_t at = P->hbm_wblob.size();
+            nw = encode_warp_chain(fs, P->hbm_wblob);
+            if (nw) woff = (int64_t)at;
+          }
+          P->hbm_woff.push_back(woff);
+          P->hbm_wwarps.push_back(nw);
           continue;
         }
         const auto& src = P->tensors[b.ops[0]];

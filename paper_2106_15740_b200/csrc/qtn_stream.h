@@ -403,6 +403,64 @@ int launch_fused(const FLaunch& L, void* stream);
 // cta_prefix = the units of split items (0 for the others)
 int launch_fused_combine(const FLaunch& L, void* stream);
 
+// ---- warp-granular fused chains (qtn_fusedw.cu): the same contraction
+//   out[o] = sum_{s in 2^K} prod_t T_t[idx_t(o, s)]
+// for chains of 2-4 operands, output rank >= 5 and K <= kWMaxK, one warp per
+// 32 * NI outputs: lanes = output bits 0..4, NI in-lane slots over 3 more
+// output bits (NI = 8 when R >= 8, else 1), the rest a chunk index per warp.
+// No staging and no per-CTA tables: a warp reads its chain's blob (header,
+// op records, host-built lane / slot / summed-offset tables) and loads the
+// operand entries straight from L1/L2 (chain operands are small and were
+// just produced).  Index maps are OR-linear: idx_t = chunk_t + lane_t[l] +
+// slot_t[i] + hs_t[s].  The fused_kernel's per-CTA setup (descriptor and
+// tables copied to shared memory, cp.async stages) dominated these small
+// chains (config 3 default: ~60 % of its stall samples in code run once per
+// warp).
+constexpr int kWMaxOps = 4;
+constexpr int kWMaxK = 10;
+constexpr int kWRuns = 12;
+struct WHdr {
+  uint64_t out;                 // tagged
+  uint8_t R, K, n_ops, out_c64;
+  uint8_t math_f32, ni_log2, match, n_ocrun;  // match: every operand stored in the math type
+  uint32_t ocrun[kWRuns];       // chunk index bits -> output bits
+  uint32_t slot_out[8];         // output offset of in-lane slot i
+  uint32_t pad[4];
+};
+struct WOpRec {
+  uint64_t ptr;                 // tagged
+  uint8_t c64, inv, n_crun, pad;  // inv: independent of the slot bits (one load per s)
+  uint32_t crun[kWRuns];        // chunk index bits -> operand bits
+  uint32_t lane_off, slot_off, hs_off;  // word offsets of its tables (from the blob start)
+  uint32_t pad2[2];
+};
+static_assert(sizeof(WHdr) % 16 == 0, "WHdr");
+static_assert(sizeof(WOpRec) % 16 == 0, "WOpRec");
+// host encoder: appends the chain's blob (16-byte aligned) to `blob` and
+// returns its number of warps (chunks), or 0 when the chain does not fit
+uint32_t encode_warp_chain(const FChainSpec& s, std::vector<uint8_t>& blob);
+struct WRec {
+  uint32_t blob16;              // chain blob offset, 16-byte units
+  uint32_t chunk;               // chunk index within the chain
+  uint32_t net;                 // network index (bases)
+  uint32_t pad;
+};
+struct WLaunch {
+  const uint8_t* blob;          // device: chain blobs
+  const WRec* recs;             // device: one per warp
+  uint32_t n_warps;
+  uint32_t n_sets;
+  uint32_t f64;                 // complex128 math (one type per launch)
+  uint32_t pad;
+  const char* in_base;
+  int64_t in_set_stride;
+  const int64_t* net_in_off;
+  char* ws_base;
+  int64_t ws_set_stride;
+  const int64_t* net_ws_off;
+};
+int launch_fusedw(const WLaunch& L, void* stream);
+
 // ---- tiny subtrees: a connected set of small buckets (output rank <= 9)
 // of one elimination tree, evaluated by ONE CTA in elimination order with
 // its internal intermediates in shared memory (operand tags with selector

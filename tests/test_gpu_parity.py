@@ -675,15 +675,19 @@ def test_trace_kernel_every_eligible_bucket(golden, monkeypatch, dtype, tol):
         assert abs(out["1"][e] - out["0"][e]) <= tol * abs(w) + 1e-13
 
 
+@pytest.mark.parametrize("fwarp", ["1", "0"])
 @pytest.mark.parametrize("min_r", ["0", "10"])
-def test_fused_product_chains(golden, monkeypatch, min_r):
+def test_fused_product_chains(golden, monkeypatch, min_r, fwarp):
     """Product buckets followed by their partial traces as one contraction
-    (fused_kernel, qtn_fused.cu; every chain here, whatever the default
-    window): equal to the unfused bucket-by-bucket evaluation
-    (QTN_FUSE_CHAIN=0) and to the reference values, on config 3 default
-    (GEMM-shaped chains, dot-product chains into scalars) and config 4 edge
-    #16 (wide streaming chains), complex128 and complex64, at 1 and 3 angle
-    sets.  min_r 0 also fuses the tiny chains of the first levels."""
+    (every chain here, whatever the default window): equal to the unfused
+    bucket-by-bucket evaluation (QTN_FUSE_CHAIN=0) and to the reference
+    values, on config 3 default (GEMM-shaped chains, dot-product chains into
+    scalars) and config 4 edge #16 (wide streaming chains), complex128 and
+    complex64, at 1 and 3 angle sets.  min_r 0 also fuses the tiny chains of
+    the first levels.  fwarp 1: chains of output rank >= 5 on the
+    warp-granular kernel (fusedw_kernel, qtn_fusedw.cu), the rest on the CTA
+    kernel; 0: every chain on the CTA kernel (fused_kernel, qtn_fused.cu)."""
+    monkeypatch.setenv("QTN_FWARP", fwarp)
     monkeypatch.setenv("QTN_FCHAIN_MIN_R", min_r)
     monkeypatch.setenv("QTN_FCHAIN_MIN_OUT", "0")   # every chain: dot products,
     monkeypatch.setenv("QTN_FCHAIN_MAX_OUT", "64")  # wide streaming chains too
