@@ -227,6 +227,8 @@ struct qtn_plan {
   std::vector<uint64_t> hbm_tiles;
   std::vector<int32_t> hbm_xidx;         // expanding-bucket descriptor per bucket, or -1
   std::vector<qtn::XDesc> hbm_xdesc;
+  std::vector<qtn::YDesc> hbm_ydesc;     // expanding bucket + consumer pairs (qtn_xt.cu)
+  std::vector<int32_t> hbm_ylevel;       // their levels
   std::vector<int32_t> hbm_r1idx;        // single-operand (trace) record per bucket, or -1
   std::vector<qtn::R1Dev> hbm_r1;        // net = 0 here; set per batch
   struct SubRec {                        // tiny subtree (qtn_stream.h SubItem)

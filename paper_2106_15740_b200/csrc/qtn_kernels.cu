@@ -648,6 +648,14 @@ struct qtn_batch {
   std::vector<uint32_t> level_xitem0;   // first expand item of each level (+ end)
   std::vector<uint64_t> level_xprefix0, level_xtiles;
   std::vector<uint32_t> level_xstage;   // stage bytes (max over the level's items)
+  // expanding bucket + consumer pairs (xt_kernel), same shape as the expand lists
+  qtn::YDesc* d_ydesc = nullptr;
+  uint32_t* d_yitem_desc = nullptr;
+  uint32_t* d_yitem_net = nullptr;
+  uint64_t* d_yprefix = nullptr;
+  std::vector<uint32_t> level_yitem0;
+  std::vector<uint64_t> level_yprefix0, level_ytiles;
+  std::vector<uint32_t> level_ystage;
   // fused product chains per level (fused_kernel)
   qtn::FDesc* d_fdesc = nullptr;
   uint32_t* d_ftab = nullptr;
@@ -737,6 +745,7 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_red, (void*)B->d_red_prefix, (void*)B->d_xdesc,
                   (void*)B->d_wblob, (void*)B->d_wrecs,
                   (void*)B->d_xitem_desc, (void*)B->d_xitem_net, (void*)B->d_xprefix,
+                  (void*)B->d_ydesc, (void*)B->d_yitem_desc, (void*)B->d_yitem_net, (void*)B->d_yprefix,
                   (void*)B->d_level_sitem0, (void*)B->d_r1, (void*)B->d_r1prefix, (void*)B->d_r1chunk_item,
                   (void*)B->d_fdesc, (void*)B->d_fitem_desc, (void*)B->d_fitem_net,
                   (void*)B->d_fprefix, (void*)B->d_cprefix, (void*)B->d_ftab,
@@ -845,6 +854,8 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   std::vector<uint64_t> desc_base(B->n_hbm);
   std::vector<uint32_t> xdesc_base(B->n_hbm), fdesc_base(B->n_hbm);
   std::vector<qtn::XDesc> xdescs;
+  std::vector<qtn::YDesc> ydescs;
+  std::vector<uint32_t> ydesc_base(B->n_hbm);
   std::vector<qtn::FDesc> fdescs;
   for (int h = 0; h < B->n_hbm; ++h) {
     const qtn_plan* P = plans[hidx[h]];
@@ -854,7 +865,34 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     xdescs.insert(xdescs.end(), P->hbm_xdesc.begin(), P->hbm_xdesc.end());
     fdesc_base[h] = (uint32_t)fdescs.size();
     fdescs.insert(fdescs.end(), P->hbm_fdesc.begin(), P->hbm_fdesc.end());
+    ydesc_base[h] = (uint32_t)ydescs.size();
+    ydescs.insert(ydescs.end(), P->hbm_ydesc.begin(), P->hbm_ydesc.end());
   }
+  // expanding bucket + consumer pairs, level-major over all HBM networks
+  std::vector<uint32_t> yitem_desc, yitem_net;
+  std::vector<uint64_t> yprefix;
+  for (int32_t lev = 0; lev < max_lev; ++lev) {
+    B->level_yitem0.push_back((uint32_t)yitem_desc.size());
+    B->level_yprefix0.push_back(yprefix.size());
+    uint64_t yacc = 0;
+    uint32_t ystage = 0;
+    yprefix.push_back(0);
+    for (int h = 0; h < B->n_hbm; ++h) {
+      const qtn_plan* P = plans[hidx[h]];
+      for (size_t y = 0; y < P->hbm_ydesc.size(); ++y) {
+        if (P->hbm_ylevel[y] + hshift[h] != lev) continue;
+        const qtn::YDesc& yd = P->hbm_ydesc[y];
+        yitem_desc.push_back(ydesc_base[h] + (uint32_t)y);
+        yitem_net.push_back((uint32_t)h);
+        yacc += yd.n_tiles;
+        yprefix.push_back(yacc);
+        ystage = std::max(ystage, qtn::xt_stage_bytes(yd));
+      }
+    }
+    B->level_ytiles.push_back(yacc);
+    B->level_ystage.push_back(ystage);
+  }
+  B->level_yitem0.push_back((uint32_t)yitem_desc.size());
   // host-built lookup tables of every fused descriptor (16-byte aligned each),
   // and the per-descriptor blob [header, sides, used ops | tables] the
   // fused kernel copies in one pass
@@ -1159,7 +1197,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     const size_t nl = B->level_tiles.size();
     B->chain_len.assign(nl, 0);
     auto tiny_only = [&](size_t l) {
-      return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] && !B->level_r1chunks[l] &&
+      return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] && !B->level_ytiles[l] && !B->level_r1chunks[l] &&
              !B->level_fctas[l] && B->level_sub0[l + 1] == B->level_sub0[l] &&
              B->level_red0[l + 1] == B->level_red0[l] && B->level_sitem0[l + 1] > B->level_sitem0[l];
     };
@@ -1195,6 +1233,8 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_red, reds)) || (rc = upload(&B->d_red_prefix, rprefix)) ||
       (rc = upload(&B->d_xdesc, xdescs)) || (rc = upload(&B->d_xitem_desc, xitem_desc)) ||
       (rc = upload(&B->d_xitem_net, xitem_net)) || (rc = upload(&B->d_xprefix, xprefix)) ||
+      (rc = upload(&B->d_ydesc, ydescs)) || (rc = upload(&B->d_yitem_desc, yitem_desc)) ||
+      (rc = upload(&B->d_yitem_net, yitem_net)) || (rc = upload(&B->d_yprefix, yprefix)) ||
       (rc = upload(&B->d_level_sitem0, B->level_sitem0)) ||
       (rc = upload(&B->d_r1, r1items)) || (rc = upload(&B->d_r1prefix, r1prefix)) ||
       (rc = upload(&B->d_r1chunk_item, r1chunk_item)) ||
@@ -1259,7 +1299,7 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
       }
       c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
-           (B->level_r1chunks[lev] ? 1 : 0) + (B->level_sub0[lev + 1] > B->level_sub0[lev] ? 1 : 0);
+           (B->level_ytiles[lev] ? 1 : 0) + (B->level_r1chunks[lev] ? 1 : 0) + (B->level_sub0[lev + 1] > B->level_sub0[lev] ? 1 : 0);
       for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi)
         c += 1 + (B->fgroups[gi].cctas ? 1 : 0);
     }
@@ -1650,7 +1690,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
                            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) +
                            (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
                            (B->level_r1chunks[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
-                           (B->level_tiles[lev] ? 1 : 0);
+                           (B->level_ytiles[lev] ? 1 : 0) + (B->level_tiles[lev] ? 1 : 0);
       const bool fork = level_streams && n_launch >= 2 && !B->chain_len[lev];
       // one launch after one launch: PDL for it (QTN_PDL_SINGLE=1; tiny
       // small_kernel levels take it by default below)
@@ -1793,6 +1833,26 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         X.net_ws_off = L.net_ws_off;
         return qtn::launch_expand(X, next_stream());
       };
+      auto l_xt = [&]() -> int {
+        if (!B->level_ytiles[lev]) return QTN_OK;
+        qtn::YLaunch Y;
+        std::memset(&Y, 0, sizeof(Y));
+        Y.descs = B->d_ydesc;
+        Y.item_desc = B->d_yitem_desc + B->level_yitem0[lev];
+        Y.item_net = B->d_yitem_net + B->level_yitem0[lev];
+        Y.tile_prefix = B->d_yprefix + B->level_yprefix0[lev];
+        Y.n_items = B->level_yitem0[lev + 1] - B->level_yitem0[lev];
+        Y.n_sets = (uint32_t)n_sets;
+        Y.total_tiles = B->level_ytiles[lev];
+        Y.stage_bytes = B->level_ystage[lev];
+        Y.in_base = L.in_base;
+        Y.in_set_stride = L.in_set_stride;
+        Y.net_in_off = L.net_in_off;
+        Y.ws_base = L.ws_base;
+        Y.ws_set_stride = L.ws_set_stride;
+        Y.net_ws_off = L.net_ws_off;
+        return qtn::launch_xt(Y, next_stream());
+      };
       auto l_stream = [&]() -> int {
         if (!B->level_tiles[lev]) return QTN_OK;
         StreamLaunch Lt = L;
@@ -1814,12 +1874,12 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         lorder = ov ? atoi(ov) : 1;
       }
       if (lorder == 1) {
-        if ((rc = l_stream()) || (rc = l_expand()) || (rc = l_fused()) || (rc = l_trace()) || (rc = l_red()) ||
+        if ((rc = l_stream()) || (rc = l_xt()) || (rc = l_expand()) || (rc = l_fused()) || (rc = l_trace()) || (rc = l_red()) ||
             (rc = l_small()) || (rc = l_sub()))
           return rc;
       } else {
         if ((rc = l_sub()) || (rc = l_fused()) || (rc = l_red()) || (rc = l_small()) || (rc = l_trace()) ||
-            (rc = l_expand()) || (rc = l_stream()))
+            (rc = l_expand()) || (rc = l_xt()) || (rc = l_stream()))
           return rc;
       }
       // join: the next level (or the fold) waits for every branch

@@ -14,6 +14,7 @@
 // of the pairwise `_product` chain, with an output layout chosen so that the
 // largest operand streams contiguously.
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -570,6 +571,145 @@ bool encode_expand_desc(const BucketSpec& s, XDesc& d) {
   if (getenv("QTN_DEBUG_DESC") && R >= atoi(getenv("QTN_DEBUG_DESC")))
     fprintf(stderr, "xdesc R=%d h=%d c=%d nA=%d nB=%d tiles=%llu\n", R, h, c, (int)A.size(),
             (int)Bs.size(), (unsigned long long)d.n_tiles);
+  return true;
+}
+
+// Expanding bucket + consumer pair (qtn_stream.h YDesc, kernel in qtn_xt.cu).
+// Everything is expressed over O2's bits; v1 and v2 are the two summed bits.
+bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
+  const char* ev = getenv("QTN_XT_MIN_R");
+  const int min_r = ev ? atoi(ev) : 14;
+  const int R = (int)s.out_vars.size();
+  if (R < min_r || R > 40) return false;
+  std::memset(&d, 0, sizeof(d));
+  auto obit = [&](int32_t u) -> int {
+    for (int i = 0; i < R; ++i)
+      if (s.out_vars[i] == u) return R - 1 - i;
+    return -1;
+  };
+  const int n = (int)s.opvars.size();
+  std::vector<uint64_t> dep(n, 0);  // O2 bits each operand depends on
+  for (int t = 0; t < n; ++t)
+    for (int32_t u : s.opvars[t])
+      if (u != s.v1 && u != s.v2) {
+        const int b = obit(u);
+        if (b < 0) return false;  // the consumer must not add variables
+        dep[t] |= 1ull << b;
+      }
+  for (int t = s.n1; t < n; ++t)  // the consumer's operands never hold v1
+    if (std::find(s.opvars[t].begin(), s.opvars[t].end(), s.v1) != s.opvars[t].end()) return false;
+  const uint64_t pdep = dep[s.primary];
+  std::vector<int> A, Bs, Ws;
+  for (int t = 0; t < s.n1; ++t) ((dep[t] & ~pdep) == 0 ? A : Bs).push_back(t);
+  if (Bs.empty() || (int)Bs.size() > kYMaxG) return false;
+  uint64_t adep = 0, bdep = 0, wdep = 0;
+  for (int t : A) adep |= dep[t];
+  for (int t : Bs) bdep |= dep[t];
+  // consumer operands: on A-side bits only -> A-type (per-thread loads),
+  // otherwise staged with the B bits (W group)
+  for (int t = s.n1; t < n; ++t) {
+    if ((dep[t] & ~adep) == 0) A.push_back(t);
+    else {
+      Ws.push_back(t);
+      wdep |= dep[t];
+    }
+  }
+  if ((int)A.size() > kYMaxA || (int)Ws.size() > kYMaxG) return false;
+  std::vector<int> ta;
+  for (int b = 0; b < 6; ++b) {
+    if (!((adep >> b) & 1)) return false;
+    ta.push_back(b);
+  }
+  // 3 more A bits: first those neither staged group sees, then one, then any
+  for (int pass = 0; pass < 3 && (int)ta.size() < kXABits; ++pass)
+    for (int b = 6; b < R && (int)ta.size() < kXABits; ++b) {
+      if (!((adep >> b) & 1) || std::find(ta.begin(), ta.end(), b) != ta.end()) continue;
+      const int seen = (int)((bdep >> b) & 1) + (int)((wdep >> b) & 1);
+      if (seen > pass) continue;
+      ta.push_back(b);
+    }
+  if ((int)ta.size() < kXABits) return false;
+  std::sort(ta.begin(), ta.end());
+  std::vector<int> tc, tw;
+  for (int b : ta) {
+    if ((bdep >> b) & 1) tc.push_back(b);
+    if ((wdep >> b) & 1) tw.push_back(b);
+  }
+  const int c = (int)tc.size(), cw = (int)tw.size();
+  std::vector<int> nbits;  // B-bit candidates: no A-side dependence
+  for (int b = 0; b < R; ++b)
+    if (!((adep >> b) & 1)) nbits.push_back(b);
+  const char* hv = getenv("QTN_XT_MAX_H");
+  int h = std::min<int>((int)nbits.size(), hv ? atoi(hv) : kYMaxH);
+  h = std::min(h, kYMaxH);
+  while (h > 0 && ((4 << (h + c)) > kYStageB || (!Ws.empty() && (2 << (h + cw)) > kYStageW))) --h;
+  while (h > 2 && R - kXABits - h < 10) --h;  // >= ~1024 tiles when the pair allows it
+  if (h < 1) return false;
+  std::vector<int> tb(nbits.begin(), nbits.begin() + h);
+  std::vector<int> rest;
+  for (int b = 0; b < R; ++b)
+    if (std::find(ta.begin(), ta.end(), b) == ta.end() && std::find(tb.begin(), tb.end(), b) == tb.end())
+      rest.push_back(b);
+  auto put = [&](const std::vector<std::pair<int, int>>& pr, uint32_t* dst, uint8_t& cnt) {
+    std::vector<uint32_t> runs;
+    make_runs(pr, runs);
+    if ((int)runs.size() > kXRuns) return false;
+    std::copy(runs.begin(), runs.end(), dst);
+    cnt = (uint8_t)runs.size();
+    return true;
+  };
+  auto put_bits = [&](const std::vector<int>& bits, uint32_t* dst, uint8_t& cnt) {
+    std::vector<std::pair<int, int>> pr;
+    for (size_t i = 0; i < bits.size(); ++i) pr.push_back({(int)i, bits[i]});
+    return put(pr, dst, cnt);
+  };
+  auto put_sub = [&](const std::vector<int>& sub, uint32_t* dst, uint8_t& cnt) {  // ta element bits -> compact
+    std::vector<std::pair<int, int>> pr;
+    for (size_t i = 0; i < ta.size(); ++i) {
+      auto it = std::find(sub.begin(), sub.end(), ta[i]);
+      if (it != sub.end()) pr.push_back({(int)i, (int)(it - sub.begin())});
+    }
+    return put(pr, dst, cnt);
+  };
+  if (!put_bits(rest, d.trun, d.n_trun) || !put_bits(ta, d.arun, d.n_arun) ||
+      !put_bits(tb, d.brun, d.n_brun) || !put_bits(tc, d.crun, d.n_crun) ||
+      !put_bits(tw, d.wrun, d.n_wrun) || !put_sub(tc, d.acrun, d.n_acrun) ||
+      !put_sub(tw, d.awrun, d.n_awrun))
+    return false;
+  auto op_of = [&](int t, YOp& o) {
+    const auto& vs = s.opvars[t];
+    const int rk = (int)vs.size();
+    if (rk > 32) return false;  // 32-bit operand offsets in the kernel
+    std::vector<std::pair<int, int>> q;
+    o.vs1 = o.vs2 = 0xff;
+    for (int j = 0; j < rk; ++j) {
+      if (vs[j] == s.v1) o.vs1 = (uint8_t)(rk - 1 - j);
+      else if (vs[j] == s.v2) o.vs2 = (uint8_t)(rk - 1 - j);
+      else q.push_back({obit(vs[j]), rk - 1 - j});
+    }
+    o.ptr = s.optag[t];
+    o.c64 = s.opc64[t];
+    return put(q, o.runs, o.n_runs);
+  };
+  int k = 0;
+  for (int t : A)
+    if (!op_of(t, d.ops[k++])) return false;
+  for (int t : Bs)
+    if (!op_of(t, d.ops[k++])) return false;
+  for (int t : Ws)
+    if (!op_of(t, d.ops[k++])) return false;
+  d.out = s.out_tag;
+  d.R = (uint8_t)R;
+  d.h = (uint8_t)h;
+  d.c = (uint8_t)c;
+  d.cw = (uint8_t)cw;
+  d.nA = (uint8_t)A.size();
+  d.nB = (uint8_t)Bs.size();
+  d.nW = (uint8_t)Ws.size();
+  d.n_tiles = 1ull << (R - kXABits - h);
+  if (getenv("QTN_DEBUG_DESC") && R >= atoi(getenv("QTN_DEBUG_DESC")))
+    fprintf(stderr, "ydesc R=%d h=%d c=%d cw=%d nA=%d nB=%d nW=%d tiles=%llu\n", R, h, c, cw,
+            (int)A.size(), (int)Bs.size(), (int)Ws.size(), (unsigned long long)d.n_tiles);
   return true;
 }
 
@@ -1347,6 +1487,57 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     std::vector<int32_t> chain_head(nb, -1), chain_tail(nb, -1), chain_len(nb, 0);
     std::vector<char> is_fchain(nb, 0);
     std::map<int32_t, uint64_t> fpart_bytes;  // split fused chains: partial-sum block bytes
+    // Expanding bucket + consumer pairs (qtn_xt.cu): the consumer of an
+    // expanding bucket's result O1 eliminates one more variable without
+    // adding any; the pair runs as one pass and O1 is never stored.  Marked
+    // as a 2-bucket chain (head = the expanding bucket).  QTN_XT=0 disables.
+    std::vector<char> is_xt(nb, 0);
+    auto xt_spec = [&](int32_t bi, int32_t c, bool tags, YPairSpec& ys,
+                       const std::function<uint64_t(int32_t)>& tag) {
+      const auto& b = P->buckets[bi];
+      const auto& cb = P->buckets[c];
+      for (int32_t id : b.ops) {
+        ys.opvars.push_back(P->tensors[id].vars);
+        ys.opc64.push_back(P->tensors[id].c64 ? 1 : 0);
+        ys.optag.push_back(tags ? tag(id) : 0);
+      }
+      ys.n1 = (int32_t)b.ops.size();
+      ys.primary = b.primary;
+      for (int32_t id : cb.ops) {
+        if (id == b.out) continue;
+        ys.opvars.push_back(P->tensors[id].vars);
+        ys.opc64.push_back(P->tensors[id].c64 ? 1 : 0);
+        ys.optag.push_back(tags ? tag(id) : 0);
+      }
+      ys.v1 = b.v;
+      ys.v2 = cb.v;
+      ys.out_vars = P->tensors[cb.out].vars;
+      ys.out_tag = tags ? tag(cb.out) : 0;
+    };
+    {
+      const char* xv = getenv("QTN_XT");
+      const bool xt_on = !(xv && xv[0] == '0');
+      for (int bi = 0; xt_on && bi < nb; ++bi) {
+        const auto& b = P->buckets[bi];
+        if (b.ops.size() < 2 || !P->tensors[b.out].c64) continue;
+        int maxop = 0;
+        for (int32_t id : b.ops) maxop = std::max(maxop, P->tensors[id].rank());
+        if (maxop > b.rank) continue;  // not expanding: the primary alone holds every variable
+        const int32_t c = P->tensors[b.out].last_use;
+        if (c < 0 || c >= nb) continue;
+        const auto& cb = P->buckets[c];
+        if (cb.rank != b.rank - 1 || !P->tensors[cb.out].c64) continue;
+        YPairSpec ys;
+        xt_spec(bi, c, false, ys, nullptr);
+        YDesc probe;
+        if (!encode_xt_desc(ys, probe)) continue;
+        is_xt[bi] = 1;
+        chain_head[bi] = bi;
+        chain_head[c] = bi;
+        chain_tail[bi] = c;
+        chain_len[bi] = 2;
+      }
+    }
     // Product chains (qtn_fused.cu): a bucket of >= 2 operands whose result
     // is then reduced by single-operand buckets is one fused contraction; the
     // union-size product and the chain's intermediates are never written
@@ -1374,7 +1565,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         std::vector<int32_t> summed{b.v};
         for (int32_t cur = bi;;) {
           const int32_t c = P->tensors[P->buckets[cur].out].last_use;
-          if (c < 0 || c >= nb || P->buckets[c].ops.size() != 1) break;
+          if (c < 0 || c >= nb || P->buckets[c].ops.size() != 1 || chain_head[c] >= 0) break;
           members.push_back(c);
           summed.push_back(P->buckets[c].v);
           cur = c;
@@ -1423,6 +1614,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         const int32_t pb = src.input ? -1 : src.born;
         // extend the producer's chain (at most kRedMax eliminated variables)
         const bool extend = pb >= 0 && chain_head[pb] >= 0 && !is_fchain[chain_head[pb]] &&
+                            !is_xt[chain_head[pb]] &&
                             chain_len[chain_head[pb]] < kRedMax;
         chain_head[bi] = extend ? chain_head[pb] : bi;
         chain_len[chain_head[bi]] += 1;
@@ -1440,7 +1632,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       const char* mkv = getenv("QTN_FUSE_MAX_K");
       const int fuse_max_k = mkv ? atoi(mkv) : 4;
       for (int bi = 0; bi < nb; ++bi) {
-        if (chain_head[bi] != bi || is_fchain[bi]) continue;
+        if (chain_head[bi] != bi || is_fchain[bi] || is_xt[bi]) continue;
         const auto& src = P->tensors[P->buckets[bi].ops[0]];
         int lowest = 64;
         for (int32_t c = bi;; c = P->tensors[P->buckets[c].out].last_use) {
@@ -1555,6 +1747,9 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       }
       int32_t lv = 0;
       for (int32_t id : P->buckets[bi].ops) lv = std::max(lv, tlevel[id]);
+      if (is_xt[bi])  // the pair also waits for the consumer's other operands
+        for (int32_t id : P->buckets[chain_tail[bi]].ops)
+          if (id != P->buckets[bi].out) lv = std::max(lv, tlevel[id]);
       P->hbm_level[bi] = lv;  // 0-based level index
       const int32_t last = h >= 0 ? chain_tail[bi] : bi;
       tlevel[P->buckets[last].out] = lv + 1;
@@ -1611,6 +1806,19 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       if (chain_head[bi] >= 0) {  // fused chain (head) or absorbed member: no descriptor
         P->hbm_tiles.push_back(0);
         if (chain_head[bi] != bi) continue;
+        if (is_xt[bi]) {
+          YPairSpec ys;
+          xt_spec(bi, chain_tail[bi], true, ys, tag_of);
+          YDesc yd;
+          if (!encode_xt_desc(ys, yd)) {
+            delete P;
+            set_error("expand + consumer pair: descriptor no longer encodable");
+            return QTN_EINVAL;
+          }
+          P->hbm_ydesc.push_back(yd);
+          P->hbm_ylevel.push_back(P->hbm_level[bi]);
+          continue;
+        }
         if (is_fchain[bi]) {
           FChainSpec fs;
           for (int32_t id : b.ops) {
@@ -1819,6 +2027,9 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       for (int32_t id : b.ops)
         if (sm_off[id] < 0)  // subtree-internal operands never leave the SM
           eb += std::ldexp((double)elem_bytes(P->tensors[id].c64), P->tensors[id].rank());
+      if (h >= 0 && is_xt[bi])
+        for (int32_t id : P->buckets[chain_tail[bi]].ops)
+          if (id != b.out) eb += std::ldexp((double)elem_bytes(P->tensors[id].c64), P->tensors[id].rank());
       if (sm_off[b.out] >= 0) continue;
       const auto& o = P->tensors[P->buckets[h >= 0 ? chain_tail[bi] : bi].out];
       eb += std::ldexp((double)elem_bytes(o.c64), o.rank());

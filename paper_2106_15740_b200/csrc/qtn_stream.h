@@ -226,6 +226,82 @@ struct XLaunch {
 };
 int launch_expand(const XLaunch& L, void* stream);
 
+// ---- expanding bucket + its consumer as one pass (qtn_xt.cu).  The
+// union-size result O1 of an expanding bucket (eliminating v1) is read by
+// exactly one bucket, which eliminates v2 of it, often a (weighted) partial
+// trace: contraction.py:90-96 twice.  When that consumer adds no variables,
+//   O2[o] = sum_{v2} W_{v2}(o) * sum_{v1} A_{v1,v2}(o) * B_{v1,v2}(o)
+// is evaluated per O2 element and O1 (the largest tensor of the network) is
+// never written or read back.  Index space: the O2 bits plus (v2, v1).
+//   A-type operands: every operand that depends on no B bit (the expanding
+//     bucket's A side, plus the consumer's operands on A-side variables):
+//     loaded per thread for its 2 adjacent outputs x 4 (v2, v1) values;
+//   B group: the expanding bucket's B side, staged per tile as
+//     Bst[x_b][x_c][v2][v1] (x_c: tile-local A bits it depends on);
+//   W group: the consumer's operands that depend on B bits, staged as
+//     Wst[x_b][x_w][v2].
+// Tile = 9 tile-local A bits (256 threads x 2 outputs) x h B bits, as in the
+// expanding-bucket kernel.  complex64 intermediates only (float math).
+constexpr int kYMaxA = 6;        // A-type operands
+constexpr int kYMaxG = 2;        // operands per staged group
+constexpr int kYOps = kYMaxA + 2 * kYMaxG;
+constexpr int kYMaxH = 6;        // B bits per tile
+constexpr int kYStageB = 4096;   // staged B entries (x_b, x_c, v2, v1)
+constexpr int kYStageW = 2048;   // staged W entries (x_b, x_w, v2)
+struct YOp {
+  uint64_t ptr;                  // tagged
+  uint8_t vs1, vs2, c64, n_runs; // bit of v1 / v2 in the operand index (0xff: none)
+  uint32_t runs[kXRuns];         // O2 bits -> operand bits
+  uint32_t pad;
+};
+struct YDesc {
+  uint64_t out;                  // tagged
+  uint64_t n_tiles;
+  uint8_t R, h, c, cw, nA, nB, nW, n_trun, n_arun, n_brun, n_crun, n_wrun, n_acrun, n_awrun, pad[2];
+  uint32_t trun[kXRuns];         // tile index bits -> output bits
+  uint32_t arun[kXRuns];         // tile-local A element bits -> output bits
+  uint32_t brun[kXRuns];         // x_b bits -> output bits
+  uint32_t crun[kXRuns];         // x_c bits -> output bits
+  uint32_t wrun[kXRuns];         // x_w bits -> output bits
+  uint32_t acrun[kXRuns];        // tile-local A element bits -> x_c bits
+  uint32_t awrun[kXRuns];        // tile-local A element bits -> x_w bits
+  YOp ops[kYOps];                // A-type [0, nA), B group [nA, nA+nB), W group after
+};
+static_assert(sizeof(YOp) % 16 == 0, "YOp");
+static_assert(sizeof(YDesc) % 16 == 0, "YDesc");
+struct YPairSpec {
+  std::vector<std::vector<int32_t>> opvars;  // the expanding bucket's operands, then the consumer's others
+  std::vector<uint8_t> opc64;
+  std::vector<uint64_t> optag;
+  int32_t n1;                                // operands of the expanding bucket
+  int32_t primary;                           // its primary
+  int32_t v1, v2;
+  std::vector<int32_t> out_vars;             // O2's layout, MSB first
+  uint64_t out_tag;
+};
+// Host encoder: true when the pair takes xt_kernel.
+bool encode_xt_desc(const YPairSpec& s, YDesc& d);
+inline uint32_t xt_stage_bytes(const YDesc& d) {
+  return 8u * ((4u << (d.h + d.c)) + (d.nW ? (2u << (d.h + d.cw)) : 0u));
+}
+struct YLaunch {
+  const YDesc* descs;            // device
+  const uint32_t* item_desc;     // device: descriptor index per item
+  const uint32_t* item_net;      // device: network index per item
+  const uint64_t* tile_prefix;   // device: n_items + 1
+  uint32_t n_items;
+  uint32_t n_sets;
+  uint64_t total_tiles;          // tiles of one set
+  uint32_t stage_bytes;          // dynamic shared memory (max over items)
+  const char* in_base;
+  int64_t in_set_stride;
+  const int64_t* net_in_off;
+  char* ws_base;
+  int64_t ws_set_stride;
+  const int64_t* net_ws_off;
+};
+int launch_xt(const YLaunch& L, void* stream);
+
 // ---- single-operand buckets (partial traces, contraction.py:94-96 on a
 // bucket of one tensor): out[o] = P[o with 0 at bit pk] + P[o with 1 at pk],
 // the output layout being the primary's minus v.  A pure stream of 3 entries

@@ -1,0 +1,327 @@
+// Expanding bucket + its consumer in one pass (sm_100a).  An expanding
+// bucket writes the widest tensor of a network (O1, e.g. rank 26 in config
+// 4: 512 MB) and the next bucket reads it back once to eliminate one more
+// variable (contraction.py:90-96, twice in a row).  Here
+//   O2[o] = sum_{v2} W_{v2}(o) * sum_{v1} A_{v1,v2}(o) * B_{v1,v2}(o)
+// is evaluated per O2 element, so O1 never exists in memory: the pair moves
+// its small inputs and O2 only (qtn_stream.h YDesc for the index split).
+//
+// Persistent CTAs of 256 threads walk contiguous tile ranges; per tile
+// (2^9 A positions x 2^h B positions):
+//   1. B group -> shared memory Bst[x_b][x_c][v2][v1] (cp.async gather-copy
+//      when it is one complex64 operand), W group -> Wst[x_b][x_w][v2];
+//   2. per thread the A-type product for its 2 adjacent outputs x (v2, v1);
+//   3. for each x_b: 4 (+2) 16-byte shared loads, 32 (+16) FMAs, one 16-byte
+//      store (a warp writes 512 contiguous bytes).
+// complex64 intermediates: operand products are formed in float64 and
+// rounded once, the inner loop is float32 (the storage policy of the unfused
+// buckets, whose O1 would have been rounded to complex64 as well).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "qtn_internal.h"
+#include "qtn_stream.h"
+#include "qtn_pdl.cuh"
+
+namespace qtn {
+namespace {
+
+__device__ __forceinline__ double2 ycmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ uint64_t ygather(uint64_t o, const uint32_t* runs, uint32_t n) {
+  uint64_t idx = 0;
+  for (uint32_t r = 0; r < n; ++r) {
+    const uint32_t w = runs[r];
+    const uint32_t s = w & 0xff, d = (w >> 8) & 0xff, l = (w >> 16) & 0xff;
+    idx |= ((o >> s) & ((1ull << l) - 1)) << d;
+  }
+  return idx;
+}
+__device__ __forceinline__ const char* yresolve(uint64_t tag, const char* in, char* ws) {
+  const uint64_t sel = tag >> kSelShift, off = tag & kOffMask;
+  if (sel == 1) return in + off;
+  if (sel == 2) return ws + off;
+  return reinterpret_cast<const char*>(off);
+}
+__device__ __forceinline__ double2 yld(const char* p, uint32_t i, uint32_t c64) {
+  if (c64) {
+    const float2 f = __ldg(reinterpret_cast<const float2*>(p) + i);
+    return make_double2(f.x, f.y);
+  }
+  return __ldg(reinterpret_cast<const double2*>(p) + i);
+}
+// a0 * (b.x, b.y) + a1 * (b.z, b.w)
+__device__ __forceinline__ float2 mac2(float2 a0, float2 a1, float4 b) {
+  float2 r;
+  r.x = fmaf(a0.x, b.x, fmaf(-a0.y, b.y, fmaf(a1.x, b.z, -a1.y * b.w)));
+  r.y = fmaf(a0.x, b.y, fmaf(a0.y, b.x, fmaf(a1.x, b.w, a1.y * b.z)));
+  return r;
+}
+
+constexpr int kYG = 2 * kYMaxG;  // staged operands (B group, then W group)
+
+// Per-item state in shared memory (rebuilt when a CTA moves to a new item):
+// gathers are OR-linear over disjoint output bits, so a staged operand index
+// is base(tile) + tb[x_b] + tc[x_c or x_w] + v strides.
+struct YItemSmem {
+  const char* ptr[kYOps];
+  uint32_t base[kYOps];          // per tile
+  uint32_t s1[kYOps], s2[kYOps]; // element strides of v1 / v2 (0: independent)
+  uint32_t tb[kYG][1 << kYMaxH];
+  uint32_t tc[kYG][512];
+  uint8_t c64[kYOps];
+};
+
+template <bool HASW>
+__device__ __forceinline__ void xt_tile(const YDesc& d, YItemSmem& X, const uint32_t* ea,
+                                        const uint32_t* eb, uint32_t xc0, uint32_t xc1,
+                                        uint32_t xw0, uint32_t xw1, uint64_t obase, float2* out,
+                                        uint64_t bmask, unsigned char* smem) {
+  const uint32_t tid = threadIdx.x;
+  const uint32_t c = d.c, cw = d.cw, h = d.h, nA = d.nA, nB = d.nB, nW = d.nW;
+  const uint32_t nOps = nA + nB + nW;
+  if (tid < nOps) X.base[tid] = (uint32_t)ygather(obase, d.ops[tid].runs, d.ops[tid].n_runs);
+  __syncthreads();
+  // 1. stages: B entry ((x_b << c | x_c) << 2) | v2 << 1 | v1, W entry ((x_b << cw | x_w) << 1) | v2
+  const uint32_t nBst = 4u << (h + c);
+  float2* stB = reinterpret_cast<float2*>(smem);
+  float2* stW = stB + nBst;
+  bool async = false;
+  if (nB == 1 && X.c64[nA]) {
+    async = true;
+    const float2* src = reinterpret_cast<const float2*>(X.ptr[nA]) + X.base[nA];
+    const uint32_t s1 = X.s1[nA], s2 = X.s2[nA], cm = (1u << c) - 1u;
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stB));
+    for (uint32_t i = tid; i < nBst; i += 256)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * i),
+                   "l"(src + X.tb[0][i >> (c + 2)] + X.tc[0][(i >> 2) & cm] + (i & 1u) * s1 +
+                       ((i >> 1) & 1u) * s2)
+                   : "memory");
+  } else {
+    const uint32_t cm = (1u << c) - 1u;
+    for (uint32_t i = tid; i < nBst; i += 256) {
+      const uint32_t xc = (i >> 2) & cm, xb = i >> (c + 2);
+      double2 pr = make_double2(1.0, 0.0);
+      for (uint32_t q = 0; q < nB; ++q) {
+        const uint32_t k = nA + q;
+        pr = ycmul(pr, yld(X.ptr[k], X.base[k] + X.tb[q][xb] + X.tc[q][xc] + (i & 1u) * X.s1[k] +
+                                         ((i >> 1) & 1u) * X.s2[k], X.c64[k]));
+      }
+      stB[i] = make_float2((float)pr.x, (float)pr.y);
+    }
+  }
+  if (HASW) {
+    const uint32_t nWst = 2u << (h + cw), cm = (1u << cw) - 1u, kW = nA + nB;
+    if (nW == 1 && X.c64[kW]) {
+      async = true;
+      const float2* src = reinterpret_cast<const float2*>(X.ptr[kW]) + X.base[kW];
+      const uint32_t s2 = X.s2[kW];
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stW));
+      for (uint32_t i = tid; i < nWst; i += 256)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * i),
+                     "l"(src + X.tb[kYMaxG][i >> (cw + 1)] + X.tc[kYMaxG][(i >> 1) & cm] + (i & 1u) * s2)
+                     : "memory");
+    } else {
+      for (uint32_t i = tid; i < nWst; i += 256) {
+        const uint32_t xw = (i >> 1) & cm, xb = i >> (cw + 1);
+        double2 pr = make_double2(1.0, 0.0);
+        for (uint32_t q = 0; q < nW; ++q) {
+          const uint32_t k = kW + q;
+          pr = ycmul(pr, yld(X.ptr[k], X.base[k] + X.tb[kYMaxG + q][xb] + X.tc[kYMaxG + q][xw] +
+                                           (i & 1u) * X.s2[k], X.c64[k]));
+        }
+        stW[i] = make_float2((float)pr.x, (float)pr.y);
+      }
+    }
+  }
+  if (async) asm volatile("cp.async.commit_group;\n" ::: "memory");
+  // 2. A-type product of this thread's two adjacent outputs: a[j][v2][v1]
+  float2 a[2][2][2];
+  {
+    double2 p[2][2][2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v2 = 0; v2 < 2; ++v2)
+#pragma unroll
+        for (int v1 = 0; v1 < 2; ++v1) p[j][v2][v1] = make_double2(1.0, 0.0);
+#pragma unroll
+    for (uint32_t k = 0; k < kYMaxA; ++k) {
+      if (k < nA) {
+        const uint32_t i0 = X.base[k] + ea[k], s1 = X.s1[k], s2 = X.s2[k], c64 = X.c64[k];
+        const char* pk = X.ptr[k];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int v2 = 0; v2 < 2; ++v2)
+#pragma unroll
+            for (int v1 = 0; v1 < 2; ++v1)
+              p[j][v2][v1] = ycmul(p[j][v2][v1], yld(pk, i0 + j * eb[k] + v2 * s2 + v1 * s1, c64));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v2 = 0; v2 < 2; ++v2)
+#pragma unroll
+        for (int v1 = 0; v1 < 2; ++v1)
+          a[j][v2][v1] = make_float2((float)p[j][v2][v1].x, (float)p[j][v2][v1].y);
+  }
+  if (async) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  // 3. outputs: x_b -> output offset by a masked increment
+  const uint32_t nb = 1u << h;
+  const float4* sB = reinterpret_cast<const float4*>(stB);
+  const float4* sW = reinterpret_cast<const float4*>(stW);
+  uint64_t ob = 0;
+#pragma unroll 2
+  for (uint32_t xb = 0; xb < nb; ++xb) {
+    const uint32_t i0 = ((xb << c) | xc0) << 1, i1 = ((xb << c) | xc1) << 1;  // float4 units
+    const float4 b00 = sB[i0], b01 = sB[i0 + 1], b10 = sB[i1], b11 = sB[i1 + 1];
+    const float2 t00 = mac2(a[0][0][0], a[0][0][1], b00), t01 = mac2(a[0][1][0], a[0][1][1], b01);
+    const float2 t10 = mac2(a[1][0][0], a[1][0][1], b10), t11 = mac2(a[1][1][0], a[1][1][1], b11);
+    float2 r0, r1;
+    if (HASW) {
+      const float4 w0 = sW[(xb << cw) | xw0], w1 = sW[(xb << cw) | xw1];
+      r0 = mac2(t00, t01, w0);
+      r1 = mac2(t10, t11, w1);
+    } else {
+      r0 = make_float2(t00.x + t01.x, t00.y + t01.y);
+      r1 = make_float2(t10.x + t11.x, t10.y + t11.y);
+    }
+    __stcs(reinterpret_cast<float4*>(out + ob), make_float4(r0.x, r0.y, r1.x, r1.y));
+    ob = ((ob | ~bmask) + 1) & bmask;
+  }
+}
+
+__global__ void __launch_bounds__(256, 3) xt_kernel(const __grid_constant__ YLaunch L) {
+  extern __shared__ __align__(16) unsigned char ysmem[];
+  __shared__ YItemSmem X;
+  __shared__ __align__(16) YDesc SD;
+  pdl_trigger();
+  pdl_wait();
+  const uint64_t per = (L.total_tiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * per;
+  const uint64_t t1 = min(L.total_tiles, t0 + per);
+  const uint32_t set = blockIdx.y, tid = threadIdx.x;
+  uint64_t item_end = 0, first = 0, bmask = 0;
+  const YDesc* d = &SD;
+  const char* in = nullptr;
+  char* ws = nullptr;
+  uint32_t ea[kYMaxA], eb[kYMaxA];
+  uint32_t xc0 = 0, xc1 = 0, xw0 = 0, xw1 = 0;
+  uint64_t oa = 0;
+  for (uint64_t t = t0; t < t1; ++t) {
+    if (t >= item_end) {
+      uint32_t lo = 0, hi = L.n_items;  // last item whose first tile <= t
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (L.tile_prefix[mid] <= t) lo = mid;
+        else hi = mid;
+      }
+      first = L.tile_prefix[lo];
+      item_end = L.tile_prefix[lo + 1];
+      const YDesc* gd = &L.descs[L.item_desc[lo]];
+      const uint32_t net = L.item_net[lo];
+      in = L.in_base + (int64_t)set * L.in_set_stride + L.net_in_off[net];
+      ws = L.ws_base + (int64_t)set * L.ws_set_stride + L.net_ws_off[net];
+      __syncthreads();  // the previous item's tables and descriptor are no longer read
+      for (uint32_t i = tid; i < sizeof(YDesc) / 16; i += 256)
+        reinterpret_cast<uint4*>(&SD)[i] = __ldg(reinterpret_cast<const uint4*>(gd) + i);
+      __syncthreads();
+      const uint32_t nA = d->nA, nB = d->nB, nW = d->nW, nOps = nA + nB + nW;
+      if (tid < nOps) {
+        const YOp& op = d->ops[tid];
+        X.ptr[tid] = yresolve(op.ptr, in, ws);
+        X.s1[tid] = op.vs1 == 0xff ? 0u : 1u << op.vs1;
+        X.s2[tid] = op.vs2 == 0xff ? 0u : 1u << op.vs2;
+        X.c64[tid] = op.c64;
+      }
+      for (uint32_t q = 0; q < nB + nW; ++q) {
+        const bool isw = q >= nB;
+        const YOp& op = d->ops[nA + q];
+        const uint32_t slot = isw ? kYMaxG + (q - nB) : q;
+        for (uint32_t i = tid; i < (1u << d->h); i += 256)
+          X.tb[slot][i] = (uint32_t)ygather(ygather(i, d->brun, d->n_brun), op.runs, op.n_runs);
+        const uint32_t nc = 1u << (isw ? d->cw : d->c);
+        for (uint32_t i = tid; i < nc; i += 256)
+          X.tc[slot][i] = (uint32_t)ygather(
+              isw ? ygather(i, d->wrun, d->n_wrun) : ygather(i, d->crun, d->n_crun), op.runs, op.n_runs);
+      }
+      const uint32_t e0 = 2u * tid;
+      oa = ygather(e0, d->arun, d->n_arun);
+#pragma unroll
+      for (uint32_t k = 0; k < kYMaxA; ++k) {
+        ea[k] = 0;
+        eb[k] = 0;
+        if (k < nA) {
+          ea[k] = (uint32_t)ygather(oa, d->ops[k].runs, d->ops[k].n_runs);
+          eb[k] = (uint32_t)ygather(1u, d->ops[k].runs, d->ops[k].n_runs);  // output bit 0
+        }
+      }
+      xc0 = (uint32_t)ygather(e0, d->acrun, d->n_acrun);
+      xc1 = (uint32_t)ygather(e0 + 1u, d->acrun, d->n_acrun);
+      xw0 = (uint32_t)ygather(e0, d->awrun, d->n_awrun);
+      xw1 = (uint32_t)ygather(e0 + 1u, d->awrun, d->n_awrun);
+      bmask = 0;
+      for (uint32_t r = 0; r < d->n_brun; ++r) {
+        const uint32_t w = d->brun[r];
+        bmask |= ((1ull << ((w >> 16) & 0xff)) - 1) << ((w >> 8) & 0xff);
+      }
+    } else {
+      __syncthreads();  // stage reuse
+    }
+    const uint64_t obase = ygather(t - first, d->trun, d->n_trun);
+    float2* outp = reinterpret_cast<float2*>(const_cast<char*>(yresolve(d->out, in, ws))) + (obase | oa);
+    if (d->nW)
+      xt_tile<true>(*d, X, ea, eb, xc0, xc1, xw0, xw1, obase, outp, bmask, ysmem);
+    else
+      xt_tile<false>(*d, X, ea, eb, xc0, xc1, xw0, xw1, obase, outp, bmask, ysmem);
+  }
+}
+
+}  // namespace
+
+int launch_xt(const YLaunch& L, void* stream) {
+  if (!L.n_items || !L.n_sets || !L.total_tiles) return QTN_OK;
+  if (L.n_sets > 65535 || L.total_tiles > 0x7fffffffull) {
+    set_error("xt_kernel: grid too large");
+    return QTN_EINVAL;
+  }
+  static std::atomic<uint64_t> attr{0};
+  if (needs_setup(attr)) {
+    cudaError_t e = cudaFuncSetAttribute(xt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (kYStageB + kYStageW) * 8);
+    if (e != cudaSuccess) {
+      set_error(std::string("xt_kernel attribute: ") + cudaGetErrorString(e));
+      return QTN_ECUDA;
+    }
+    mark_setup(attr);
+  }
+  int n_sm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  if (n_sm <= 0) n_sm = 148;
+  int per_sm = 0;
+  const char* xc = getenv("QTN_XT_CTAS");
+  if (xc) per_sm = atoi(xc);
+  if (per_sm <= 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xt_kernel, 256, L.stage_bytes) != cudaSuccess)
+    per_sm = 3;
+  per_sm = std::max(1, per_sm);
+  const uint64_t ctas = std::min<uint64_t>(L.total_tiles, (uint64_t)n_sm * (uint64_t)per_sm);
+  dim3 grid((uint32_t)ctas, L.n_sets);
+  cudaError_t e = launch_pdl<true>(xt_kernel, grid, dim3(256), L.stage_bytes,
+                                   reinterpret_cast<cudaStream_t>(stream), L);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("xt_kernel launch: ") + cudaGetErrorString(e));
+    return QTN_ECUDA;
+  }
+  return QTN_OK;
+}
+
+}  // namespace qtn

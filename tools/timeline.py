@@ -8,6 +8,7 @@ Prints per kernel name: launches, summed duration, and the evaluation's
 wall span; writes the raw event list (name, ts_us, dur_us, stream) to --out.
 """
 import argparse
+import re
 import json
 import os
 import sys
@@ -48,7 +49,8 @@ def main():
     for e in prof.events():
         if e.device_type.name != "CUDA":
             continue
-        ev.append({"name": e.name.split("(")[0].split("<")[0].split("::")[-1],
+        m = re.search(r"(\w+_kernel\w*)", e.name)
+        ev.append({"name": m.group(1) if m else e.name[:40],
                    "ts": e.time_range.start, "dur": e.time_range.end - e.time_range.start})
     ev.sort(key=lambda x: x["ts"])
     # split into evaluations at gaps > 50 us
