@@ -83,6 +83,9 @@ typedef struct {
   int32_t n_fused_chains;    /* HBM executor: product chains run as one kernel   */
   double exec_bytes;         /* bytes the executor's kernels move (fused chains:  */
                              /* operands + final output only)                   */
+  int32_t n_pairs;           /* HBM executor: expanding bucket + consumer pairs  */
+  int32_t reserved;          /* run as one kernel (their union-size result is    */
+                             /* never stored)                                    */
 } qtn_plan_info_t;
 
 /* ---------------------------------------------------------------- ordering */

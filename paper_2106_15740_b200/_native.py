@@ -49,6 +49,8 @@ class PlanInfo(C.Structure):
         ("n_levels", C.c_int32),
         ("n_fused_chains", C.c_int32),
         ("exec_bytes", C.c_double),
+        ("n_pairs", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

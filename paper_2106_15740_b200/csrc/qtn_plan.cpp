@@ -2071,6 +2071,8 @@ extern "C" int qtn_plan_info(const qtn_plan* P, qtn_plan_info_t* info) {
   info->n_levels = P->n_levels;
   info->n_fused_chains = (int32_t)P->hbm_fdesc.size();
   info->exec_bytes = P->exec_bytes < 0.0 ? P->alg_bytes : P->exec_bytes;
+  info->n_pairs = (int32_t)P->hbm_ydesc.size();
+  info->reserved = 0;
   return QTN_OK;
 }
 

@@ -722,6 +722,49 @@ def test_fused_product_chains(golden, monkeypatch, min_r, fwarp):
         assert np.allclose(out["1", dt][2], out["0", dt][2], rtol=tol, atol=tol)
 
 
+@pytest.mark.parametrize("min_r", ["14", "10"])
+def test_expand_consumer_pairs(golden, monkeypatch, min_r):
+    """An expanding bucket and its consumer as one pass (xt_kernel,
+    qtn_xt.cu; contraction.py:90-96 twice without storing the union-size
+    result): equal to the bucket-by-bucket evaluation (QTN_XT=0) and to the
+    reference values, complex64 at 1e-5, on config 4 edges #16 and #1058 (the
+    rank-25/26 pairs, with and without a staged consumer operand) and on
+    config 3 default edges, at 1 and 3 angle sets.  min_r 10 also pairs the
+    small expanding buckets (few tiles, h = 1..2)."""
+    monkeypatch.setenv("QTN_XT_MIN_R", min_r)
+    monkeypatch.setenv("QTN_EXPAND_MIN_R", min_r)
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    recs = G["modes"]["default"][:12]
+    G4 = golden("config4.json")
+    rec4 = {r["edge_index"]: complex(*r["value"]) for r in G4["modes"]["zz+diagonal"]
+            if r["edge_index"] in (16, 1058)}
+    g4 = Q.random_regular_graph(G4["n"], 3, 0)
+    p4v = Q.QaoaParams(G4["gammas"], G4["betas"])
+    rng = np.random.default_rng(5)
+    sets3 = np.vstack([params.as_vector(), rng.uniform(0, math.pi, (2, 2 * G["p"]))])
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_XT", flag)
+        plan = Q.EnergyPlan(graph, G["p"], "default", dtype="complex64",
+                            edge_ids=[r["edge_index"] for r in recs])
+        p4 = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype="complex64", edge_ids=sorted(rec4))
+        npairs = sum(j.plan.n_pairs for j in plan.jobs), sum(j.plan.n_pairs for j in p4.jobs)
+        assert (npairs[0] > 0 and npairs[1] >= 4) if flag == "1" else npairs == (0, 0)
+        out[flag] = (plan.zz_values(params), p4.zz_values(p4v), plan.energies(sets3))
+        assert plan.launches == plan.launches_per_eval(1)
+    tol = 1e-5
+    for r in recs:
+        w = complex(*r["value"])
+        e = r["edge_index"]
+        assert abs(out["1"][0][e] - w) <= tol * abs(w) + 1e-12, e
+        assert abs(out["1"][0][e] - out["0"][0][e]) <= tol * abs(w) + 1e-12
+    for e, w in rec4.items():
+        assert abs(out["1"][1][e] - w) <= tol * abs(w), e
+        assert abs(out["1"][1][e] - out["0"][1][e]) <= tol * abs(w), e
+    assert np.allclose(out["1"][2], out["0"][2], rtol=tol, atol=tol)
+
 
 def test_device_memory_fit_check():
     """an evaluation whose buffers exceed the free device memory

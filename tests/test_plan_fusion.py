@@ -45,3 +45,32 @@ def test_fused_chains_config3_default_every_network(golden):
     assert sum(j.plan.n_fused_chains for j in jobs) > 100
     assert max(j.plan.n_levels for j in jobs) <= 55
     assert sum(j.plan.exec_bytes for j in jobs) < 0.8 * sum(j.plan.alg_bytes for j in jobs)
+
+
+def test_expand_consumer_pairs_config4(golden):
+    """Config 4 edge #1058: the three wide expanding buckets ([2,17,17]->25,
+    [2,16,19]->25, [1,22,21]->26) pair with their consumers (xt_kernel), so
+    the rank-25/26 results are never stored: executed bytes fall below half of
+    the reference's per-bucket bytes; QTN_XT=0 keeps every bucket on its own
+    kernel; complex128 plans have no pairs (float math only); step ranks and
+    the algorithmic bytes are those of the reference either way."""
+    import os
+
+    G4 = golden("config4.json")
+    g4 = Q.random_regular_graph(G4["n"], 3, 0)
+    j = Q.plan_edges(g4, G4["p"], "zz+diagonal", [1058], dtype="complex64")[0]
+    assert j.plan.n_pairs >= 3
+    assert j.plan.exec_bytes < 0.5 * j.plan.alg_bytes
+    assert max(j.plan.step_ranks) == j.report.width
+    os.environ["QTN_XT"] = "0"
+    try:
+        k = Q.plan_edges(g4, G4["p"], "zz+diagonal", [1058], dtype="complex64")[0]
+    finally:
+        del os.environ["QTN_XT"]
+    assert k.plan.n_pairs == 0
+    assert k.plan.n_levels > j.plan.n_levels
+    assert k.plan.exec_bytes > j.plan.exec_bytes
+    assert k.plan.alg_bytes == j.plan.alg_bytes
+    assert k.plan.step_ranks == j.plan.step_ranks
+    d = Q.plan_edges(g4, G4["p"], "zz+diagonal", [16], dtype="complex128")[0]
+    assert d.plan.n_pairs == 0
