@@ -720,6 +720,13 @@ struct qtn_batch {
   int32_t* d_hbm_index = nullptr;
 };
 
+// xt_kernel launches of one level (one per group count present)
+static int y_launches(const qtn_batch* B, size_t lev) {
+  int c = 0;
+  for (int gq = 0; gq <= qtn::kYMaxGB; ++gq) c += B->level_ytiles[lev * (qtn::kYMaxGB + 1) + gq] ? 1 : 0;
+  return c;
+}
+
 extern "C" int qtn_batch_destroy(qtn_batch* B) {
   if (!B) return QTN_OK;
   for (auto& kv : B->graphs) cudaGraphExecDestroy(kv.second);
@@ -871,7 +878,9 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
   // expanding bucket + consumer pairs, level-major over all HBM networks
   std::vector<uint32_t> yitem_desc, yitem_net;
   std::vector<uint64_t> yprefix;
-  for (int32_t lev = 0; lev < max_lev; ++lev) {
+  // (one list per level and group count g: a launch's items share g)
+  for (int32_t lev = 0; lev < max_lev; ++lev)
+   for (int gq = 0; gq <= qtn::kYMaxGB; ++gq) {
     B->level_yitem0.push_back((uint32_t)yitem_desc.size());
     B->level_yprefix0.push_back(yprefix.size());
     uint64_t yacc = 0;
@@ -880,7 +889,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     for (int h = 0; h < B->n_hbm; ++h) {
       const qtn_plan* P = plans[hidx[h]];
       for (size_t y = 0; y < P->hbm_ydesc.size(); ++y) {
-        if (P->hbm_ylevel[y] + hshift[h] != lev) continue;
+        if (P->hbm_ylevel[y] + hshift[h] != lev || P->hbm_ydesc[y].g != gq) continue;
         const qtn::YDesc& yd = P->hbm_ydesc[y];
         yitem_desc.push_back(ydesc_base[h] + (uint32_t)y);
         yitem_net.push_back((uint32_t)h);
@@ -1197,7 +1206,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     const size_t nl = B->level_tiles.size();
     B->chain_len.assign(nl, 0);
     auto tiny_only = [&](size_t l) {
-      return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] && !B->level_ytiles[l] && !B->level_r1chunks[l] &&
+      return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] && !y_launches(B, l) && !B->level_r1chunks[l] &&
              !B->level_fctas[l] && B->level_sub0[l + 1] == B->level_sub0[l] &&
              B->level_red0[l + 1] == B->level_red0[l] && B->level_sitem0[l + 1] > B->level_sitem0[l];
     };
@@ -1299,7 +1308,7 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
       }
       c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
-           (B->level_ytiles[lev] ? 1 : 0) + (B->level_r1chunks[lev] ? 1 : 0) + (B->level_sub0[lev + 1] > B->level_sub0[lev] ? 1 : 0);
+           y_launches(B, lev) + (B->level_r1chunks[lev] ? 1 : 0) + (B->level_sub0[lev + 1] > B->level_sub0[lev] ? 1 : 0);
       for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi)
         c += 1 + (B->fgroups[gi].cctas ? 1 : 0);
     }
@@ -1690,7 +1699,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
                            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) +
                            (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
                            (B->level_r1chunks[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
-                           (B->level_ytiles[lev] ? 1 : 0) + (B->level_tiles[lev] ? 1 : 0);
+                           y_launches(B, lev) + (B->level_tiles[lev] ? 1 : 0);
       const bool fork = level_streams && n_launch >= 2 && !B->chain_len[lev];
       // one launch after one launch: PDL for it (QTN_PDL_SINGLE=1; tiny
       // small_kernel levels take it by default below)
@@ -1834,24 +1843,30 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         return qtn::launch_expand(X, next_stream());
       };
       auto l_xt = [&]() -> int {
-        if (!B->level_ytiles[lev]) return QTN_OK;
-        qtn::YLaunch Y;
-        std::memset(&Y, 0, sizeof(Y));
-        Y.descs = B->d_ydesc;
-        Y.item_desc = B->d_yitem_desc + B->level_yitem0[lev];
-        Y.item_net = B->d_yitem_net + B->level_yitem0[lev];
-        Y.tile_prefix = B->d_yprefix + B->level_yprefix0[lev];
-        Y.n_items = B->level_yitem0[lev + 1] - B->level_yitem0[lev];
-        Y.n_sets = (uint32_t)n_sets;
-        Y.total_tiles = B->level_ytiles[lev];
-        Y.stage_bytes = B->level_ystage[lev];
-        Y.in_base = L.in_base;
-        Y.in_set_stride = L.in_set_stride;
-        Y.net_in_off = L.net_in_off;
-        Y.ws_base = L.ws_base;
-        Y.ws_set_stride = L.ws_set_stride;
-        Y.net_ws_off = L.net_ws_off;
-        return qtn::launch_xt(Y, next_stream());
+        for (int gq = qtn::kYMaxGB; gq >= 0; --gq) {  // the widest tiles first
+          const size_t yi = lev * (qtn::kYMaxGB + 1) + gq;
+          if (!B->level_ytiles[yi]) continue;
+          qtn::YLaunch Y;
+          std::memset(&Y, 0, sizeof(Y));
+          Y.descs = B->d_ydesc;
+          Y.item_desc = B->d_yitem_desc + B->level_yitem0[yi];
+          Y.item_net = B->d_yitem_net + B->level_yitem0[yi];
+          Y.tile_prefix = B->d_yprefix + B->level_yprefix0[yi];
+          Y.n_items = B->level_yitem0[yi + 1] - B->level_yitem0[yi];
+          Y.n_sets = (uint32_t)n_sets;
+          Y.total_tiles = B->level_ytiles[yi];
+          Y.stage_bytes = B->level_ystage[yi];
+          Y.g = (uint32_t)gq;
+          Y.in_base = L.in_base;
+          Y.in_set_stride = L.in_set_stride;
+          Y.net_in_off = L.net_in_off;
+          Y.ws_base = L.ws_base;
+          Y.ws_set_stride = L.ws_set_stride;
+          Y.net_ws_off = L.net_ws_off;
+          const int r2 = qtn::launch_xt(Y, next_stream());
+          if (r2) return r2;
+        }
+        return QTN_OK;
       };
       auto l_stream = [&]() -> int {
         if (!B->level_tiles[lev]) return QTN_OK;

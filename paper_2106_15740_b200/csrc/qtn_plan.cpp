@@ -580,7 +580,7 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
   const char* ev = getenv("QTN_XT_MIN_R");
   const int min_r = ev ? atoi(ev) : 14;
   const int R = (int)s.out_vars.size();
-  if (R < min_r || R > 40) return false;
+  if (R < min_r || R > 32) return false;
   std::memset(&d, 0, sizeof(d));
   auto obit = [&](int32_t u) -> int {
     for (int i = 0; i < R; ++i)
@@ -630,26 +630,67 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
     }
   if ((int)ta.size() < kXABits) return false;
   std::sort(ta.begin(), ta.end());
-  std::vector<int> tc, tw;
-  for (int b : ta) {
-    if ((bdep >> b) & 1) tc.push_back(b);
-    if ((wdep >> b) & 1) tw.push_back(b);
-  }
-  const int c = (int)tc.size(), cw = (int)tw.size();
+  // group bits: further A bits the B group does not see (one staged B row
+  // then serves every group of a thread); those the W group does not see first
+  const char* gv = getenv("QTN_XT_G");
+  const int gmax = std::min(kYMaxGB, gv ? atoi(gv) : 0);  // measured: config 4 0.654 / 0.670 / 0.713 ms at g = 0 / 1 / 2
+  int g = 0;
+  for (int pass = 0; pass < 2 && g < gmax; ++pass)
+    for (int b = 6; b < R && g < gmax; ++b) {
+      if (!((adep >> b) & 1) || ((bdep >> b) & 1) || std::find(ta.begin(), ta.end(), b) != ta.end()) continue;
+      if (pass == 0 && ((wdep >> b) & 1)) continue;
+      ta.push_back(b);
+      ++g;
+    }
   std::vector<int> nbits;  // B-bit candidates: no A-side dependence
   for (int b = 0; b < R; ++b)
     if (!((adep >> b) & 1)) nbits.push_back(b);
   const char* hv = getenv("QTN_XT_MAX_H");
-  int h = std::min<int>((int)nbits.size(), hv ? atoi(hv) : kYMaxH);
-  h = std::min(h, kYMaxH);
-  while (h > 0 && ((4 << (h + c)) > kYStageB || (!Ws.empty() && (2 << (h + cw)) > kYStageW))) --h;
-  while (h > 2 && R - kXABits - h < 10) --h;  // >= ~1024 tiles when the pair allows it
+  const int hmax = std::min<int>(std::min<int>((int)nbits.size(), hv ? atoi(hv) : kYMaxH), kYMaxH);
+  std::vector<int> tc, tw;
+  int c = 0, cw = 0, h = 0;
+  for (;; ta.pop_back(), --g) {  // small pairs: fewer groups, more tiles
+    tc.clear();
+    tw.clear();
+    for (int b : ta) {
+      if ((bdep >> b) & 1) tc.push_back(b);
+      if ((wdep >> b) & 1) tw.push_back(b);
+    }
+    c = (int)tc.size();
+    cw = (int)tw.size();
+    h = hmax;
+    while (h > 0 && ((4 << (h + c)) > kYStageB || (!Ws.empty() && (2 << (h + cw)) > kYStageW))) --h;
+    while (h > 2 && R - kXABits - g - h < 11) --h;  // >= ~2048 tiles when the pair allows it
+    if (g == 0 || R - kXABits - g - h >= 9) break;
+  }
   if (h < 1) return false;
   std::vector<int> tb(nbits.begin(), nbits.begin() + h);
   std::vector<int> rest;
   for (int b = 0; b < R; ++b)
     if (std::find(ta.begin(), ta.end(), b) == ta.end() && std::find(tb.begin(), tb.end(), b) == tb.end())
       rest.push_back(b);
+  {
+    // Tile order: consecutive tiles of a CTA differ first in the bits neither
+    // staged group depends on, then in the bits of the group whose stage
+    // costs less to keep (the kernel refills a stage only when its operands'
+    // bases change): the larger saving of staged entries per tile wins.
+    std::vector<int> f_both, f_b, f_w, others;
+    for (int b : rest) {
+      const bool sb = (bdep >> b) & 1, sw = !Ws.empty() && ((wdep >> b) & 1);
+      (!sb && !sw ? f_both : (!sb ? f_b : (!sw ? f_w : others))).push_back(b);
+    }
+    const double save_b = (double)(4 << (h + c)) * (1.0 - std::ldexp(1.0, -(int)f_b.size()));
+    const double save_w = Ws.empty() ? 0.0 : (double)(2 << (h + cw)) * (1.0 - std::ldexp(1.0, -(int)f_w.size()));
+    const char* ov = getenv("QTN_XT_ORDER");
+    if (!(ov && ov[0] == '0')) {
+    rest = f_both;
+    const auto& first = save_b >= save_w ? f_b : f_w;
+    const auto& second = save_b >= save_w ? f_w : f_b;
+    rest.insert(rest.end(), first.begin(), first.end());
+    rest.insert(rest.end(), second.begin(), second.end());
+    rest.insert(rest.end(), others.begin(), others.end());
+    }
+  }
   auto put = [&](const std::vector<std::pair<int, int>>& pr, uint32_t* dst, uint8_t& cnt) {
     std::vector<uint32_t> runs;
     make_runs(pr, runs);
@@ -706,10 +747,18 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
   d.nA = (uint8_t)A.size();
   d.nB = (uint8_t)Bs.size();
   d.nW = (uint8_t)Ws.size();
-  d.n_tiles = 1ull << (R - kXABits - h);
+  d.g = (uint8_t)g;
+  d.n_tiles = 1ull << (R - kXABits - g - h);
   if (getenv("QTN_DEBUG_DESC") && R >= atoi(getenv("QTN_DEBUG_DESC")))
-    fprintf(stderr, "ydesc R=%d h=%d c=%d cw=%d nA=%d nB=%d nW=%d tiles=%llu\n", R, h, c, cw,
+  {
+    fprintf(stderr, "ydesc R=%d h=%d g=%d c=%d cw=%d nA=%d nB=%d nW=%d tiles=%llu", R, h, g, c, cw,
             (int)A.size(), (int)Bs.size(), (int)Ws.size(), (unsigned long long)d.n_tiles);
+    for (int q = 0; q < d.nA + d.nB + d.nW; ++q)
+      fprintf(stderr, " %c(r%zu vs1=%d vs2=%d)", q < d.nA ? 'A' : (q < d.nA + d.nB ? 'B' : 'W'),
+              s.opvars[q < (int)A.size() ? A[q] : (q < (int)(A.size() + Bs.size()) ? Bs[q - A.size()] : Ws[q - A.size() - Bs.size()])].size(),
+              d.ops[q].vs1 == 0xff ? -1 : d.ops[q].vs1, d.ops[q].vs2 == 0xff ? -1 : d.ops[q].vs2);
+    fprintf(stderr, "\n");
+  }
   return true;
 }
 

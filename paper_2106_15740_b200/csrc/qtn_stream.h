@@ -246,6 +246,7 @@ constexpr int kYMaxA = 6;        // A-type operands
 constexpr int kYMaxG = 2;        // operands per staged group
 constexpr int kYOps = kYMaxA + 2 * kYMaxG;
 constexpr int kYMaxH = 6;        // B bits per tile
+constexpr int kYMaxGB = 2;       // group bits (2^g output pairs per thread)
 constexpr int kYStageB = 4096;   // staged B entries (x_b, x_c, v2, v1)
 constexpr int kYStageW = 2048;   // staged W entries (x_b, x_w, v2)
 struct YOp {
@@ -257,9 +258,11 @@ struct YOp {
 struct YDesc {
   uint64_t out;                  // tagged
   uint64_t n_tiles;
-  uint8_t R, h, c, cw, nA, nB, nW, n_trun, n_arun, n_brun, n_crun, n_wrun, n_acrun, n_awrun, pad[2];
+  uint8_t R, h, c, cw, nA, nB, nW, n_trun, n_arun, n_brun, n_crun, n_wrun, n_acrun, n_awrun, g, pad;
+  // g: a thread owns 2^g groups of 2 adjacent outputs (element bits 9..9+g:
+  // A bits the B group does not depend on, so one staged B row serves them all)
   uint32_t trun[kXRuns];         // tile index bits -> output bits
-  uint32_t arun[kXRuns];         // tile-local A element bits -> output bits
+  uint32_t arun[kXRuns];         // tile-local A element bits (9 + g) -> output bits
   uint32_t brun[kXRuns];         // x_b bits -> output bits
   uint32_t crun[kXRuns];         // x_c bits -> output bits
   uint32_t wrun[kXRuns];         // x_w bits -> output bits
@@ -293,6 +296,8 @@ struct YLaunch {
   uint32_t n_sets;
   uint64_t total_tiles;          // tiles of one set
   uint32_t stage_bytes;          // dynamic shared memory (max over items)
+  uint32_t g;                    // group bits of every item of this launch
+  uint32_t pad;
   const char* in_base;
   int64_t in_set_stride;
   const int64_t* net_in_off;

@@ -61,7 +61,12 @@ __device__ __forceinline__ float2 mac2(float2 a0, float2 a1, float4 b) {
   return r;
 }
 
+#ifndef XT_UNROLL
+#define XT_UNROLL 1
+#endif
+constexpr int kXtUnroll = XT_UNROLL;
 constexpr int kYG = 2 * kYMaxG;  // staged operands (B group, then W group)
+constexpr int kYMaxGroups = 1 << kYMaxGB;
 
 // Per-item state in shared memory (rebuilt when a CTA moves to a new item):
 // gathers are OR-linear over disjoint output bits, so a staged operand index
@@ -72,48 +77,78 @@ struct YItemSmem {
   uint32_t s1[kYOps], s2[kYOps]; // element strides of v1 / v2 (0: independent)
   uint32_t tb[kYG][1 << kYMaxH];
   uint32_t tc[kYG][512];
+  uint32_t goff[kYMaxA][kYMaxGroups];  // A-type operand offset of group gi
+  uint64_t og[kYMaxGroups];            // output offset of group gi
+  uint32_t gw[kYMaxGroups];            // x_w part of group gi
   uint8_t c64[kYOps];
 };
 
-template <bool HASW>
+// Stage layout: the B group as two planes of float4 (v2 = 0 / 1), each
+// [x_b][x_c] -> (v1 = 0, v1 = 1): a warp whose lanes differ in x_c reads
+// consecutive 16-byte words (no bank conflicts); the W group [x_b][x_w] ->
+// (v2 = 0, v2 = 1) after them.
+// prev[0..3]: the operand bases the stages were last filled for (B group,
+// W group); a tile whose bases are unchanged reuses them (the host orders the
+// tile index so that consecutive tiles differ in bits a group does not see)
+template <bool HASW, int G>
 __device__ __forceinline__ void xt_tile(const YDesc& d, YItemSmem& X, const uint32_t* ea,
                                         const uint32_t* eb, uint32_t xc0, uint32_t xc1,
                                         uint32_t xw0, uint32_t xw1, uint64_t obase, float2* out,
-                                        uint64_t bmask, unsigned char* smem) {
+                                        uint32_t bmask, unsigned char* smem, uint32_t* prev) {
   const uint32_t tid = threadIdx.x;
   const uint32_t c = d.c, cw = d.cw, h = d.h, nA = d.nA, nB = d.nB, nW = d.nW;
   const uint32_t nOps = nA + nB + nW;
   if (tid < nOps) X.base[tid] = (uint32_t)ygather(obase, d.ops[tid].runs, d.ops[tid].n_runs);
   __syncthreads();
-  // 1. stages: B entry ((x_b << c | x_c) << 2) | v2 << 1 | v1, W entry ((x_b << cw | x_w) << 1) | v2
+  // 1. stages.  B entry i = (row << 2) | v2 << 1 | v1, row = x_b << c | x_c
   const uint32_t nBst = 4u << (h + c);
   float2* stB = reinterpret_cast<float2*>(smem);
-  float2* stW = stB + nBst;
+  const uint32_t kYPlane = nBst * 4u, kYWOff = nBst * 8u;  // plane v2 = 1 and the W stage follow plane 0
+  float2* stW = reinterpret_cast<float2*>(smem + kYWOff);
   bool async = false;
-  if (nB == 1 && X.c64[nA]) {
+  bool fillB = false, fillW = false;
+#ifdef XT_NOPREV
+  fillB = fillW = true;
+#endif
+#pragma unroll
+  for (uint32_t q = 0; q < kYMaxG; ++q) {  // (unrolled: prev stays in registers)
+    if (q < nB) {
+      const uint32_t bq = X.base[nA + q];
+      fillB |= prev[q] != bq;
+      prev[q] = bq;
+    }
+    if (q < nW) {
+      const uint32_t bq = X.base[nA + nB + q];
+      fillW |= prev[kYMaxG + q] != bq;
+      prev[kYMaxG + q] = bq;
+    }
+  }
+  if (!fillB) {
+  } else if (nB == 1 && X.c64[nA]) {
     async = true;
     const float2* src = reinterpret_cast<const float2*>(X.ptr[nA]) + X.base[nA];
     const uint32_t s1 = X.s1[nA], s2 = X.s2[nA], cm = (1u << c) - 1u;
     const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stB));
-    for (uint32_t i = tid; i < nBst; i += 256)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * i),
-                   "l"(src + X.tb[0][i >> (c + 2)] + X.tc[0][(i >> 2) & cm] + (i & 1u) * s1 +
-                       ((i >> 1) & 1u) * s2)
+    for (uint32_t i = tid; i < nBst; i += 256) {
+      const uint32_t row = i >> 2, v2 = (i >> 1) & 1u, v1 = i & 1u;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + v2 * kYPlane + 8u * (2u * row + v1)),
+                   "l"(src + X.tb[0][row >> c] + X.tc[0][row & cm] + v1 * s1 + v2 * s2)
                    : "memory");
+    }
   } else {
     const uint32_t cm = (1u << c) - 1u;
     for (uint32_t i = tid; i < nBst; i += 256) {
-      const uint32_t xc = (i >> 2) & cm, xb = i >> (c + 2);
+      const uint32_t row = i >> 2, v2 = (i >> 1) & 1u, v1 = i & 1u;
       double2 pr = make_double2(1.0, 0.0);
       for (uint32_t q = 0; q < nB; ++q) {
         const uint32_t k = nA + q;
-        pr = ycmul(pr, yld(X.ptr[k], X.base[k] + X.tb[q][xb] + X.tc[q][xc] + (i & 1u) * X.s1[k] +
-                                         ((i >> 1) & 1u) * X.s2[k], X.c64[k]));
+        pr = ycmul(pr, yld(X.ptr[k], X.base[k] + X.tb[q][row >> c] + X.tc[q][row & cm] + v1 * X.s1[k] +
+                                         v2 * X.s2[k], X.c64[k]));
       }
-      stB[i] = make_float2((float)pr.x, (float)pr.y);
+      stB[v2 * (kYPlane / 8) + 2u * row + v1] = make_float2((float)pr.x, (float)pr.y);
     }
   }
-  if (HASW) {
+  if (HASW && fillW) {
     const uint32_t nWst = 2u << (h + cw), cm = (1u << cw) - 1u, kW = nA + nB;
     if (nW == 1 && X.c64[kW]) {
       async = true;
@@ -138,9 +173,10 @@ __device__ __forceinline__ void xt_tile(const YDesc& d, YItemSmem& X, const uint
     }
   }
   if (async) asm volatile("cp.async.commit_group;\n" ::: "memory");
-  // 2. A-type product of this thread's two adjacent outputs: a[j][v2][v1]
-  float2 a[2][2][2];
-  {
+  // 2. A-type product of this thread's outputs: a[group][j][v2][v1]
+  float2 a[G][2][2][2];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) {
     double2 p[2][2][2];
 #pragma unroll
     for (int j = 0; j < 2; ++j)
@@ -151,7 +187,7 @@ __device__ __forceinline__ void xt_tile(const YDesc& d, YItemSmem& X, const uint
 #pragma unroll
     for (uint32_t k = 0; k < kYMaxA; ++k) {
       if (k < nA) {
-        const uint32_t i0 = X.base[k] + ea[k], s1 = X.s1[k], s2 = X.s2[k], c64 = X.c64[k];
+        const uint32_t i0 = X.base[k] + ea[k] + X.goff[k][gi], s1 = X.s1[k], s2 = X.s2[k], c64 = X.c64[k];
         const char* pk = X.ptr[k];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
@@ -168,46 +204,70 @@ __device__ __forceinline__ void xt_tile(const YDesc& d, YItemSmem& X, const uint
       for (int v2 = 0; v2 < 2; ++v2)
 #pragma unroll
         for (int v1 = 0; v1 < 2; ++v1)
-          a[j][v2][v1] = make_float2((float)p[j][v2][v1].x, (float)p[j][v2][v1].y);
+          a[gi][j][v2][v1] = make_float2((float)p[j][v2][v1].x, (float)p[j][v2][v1].y);
   }
   if (async) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
-  // 3. outputs: x_b -> output offset by a masked increment
+  // 3. outputs: x_b -> output offset by a masked increment; shared-memory
+  // addresses advance by a stride per x_b (plane 1 and W at fixed offsets)
   const uint32_t nb = 1u << h;
-  const float4* sB = reinterpret_cast<const float4*>(stB);
-  const float4* sW = reinterpret_cast<const float4*>(stW);
-  uint64_t ob = 0;
-#pragma unroll 2
+  const bool pairb = xc0 == xc1;  // uniform per item: output bit 0 outside the B group
+  const float4* pb0 = reinterpret_cast<const float4*>(smem) + xc0;
+  const float4* pb1 = reinterpret_cast<const float4*>(smem) + xc1;
+  const float4* pq0 = pb0 + (nBst >> 2);  // plane v2 = 1
+  const float4* pq1 = pb1 + (nBst >> 2);
+  const uint32_t strideB = 1u << c, strideW = 1u << cw;
+  float2* og[G];
+  const float4 *pw0[G], *pw1[G];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) {
+    og[gi] = out + X.og[gi];
+    pw0[gi] = reinterpret_cast<const float4*>(stW) + (xw0 | X.gw[gi]);
+    pw1[gi] = reinterpret_cast<const float4*>(stW) + (xw1 | X.gw[gi]);
+  }
+  uint32_t ob = 0;
+#pragma unroll(G == 1 ? kXtUnroll : (G == 2 ? 2 : 1))
   for (uint32_t xb = 0; xb < nb; ++xb) {
-    const uint32_t i0 = ((xb << c) | xc0) << 1, i1 = ((xb << c) | xc1) << 1;  // float4 units
-    const float4 b00 = sB[i0], b01 = sB[i0 + 1], b10 = sB[i1], b11 = sB[i1 + 1];
-    const float2 t00 = mac2(a[0][0][0], a[0][0][1], b00), t01 = mac2(a[0][1][0], a[0][1][1], b01);
-    const float2 t10 = mac2(a[1][0][0], a[1][0][1], b10), t11 = mac2(a[1][1][0], a[1][1][1], b11);
-    float2 r0, r1;
-    if (HASW) {
-      const float4 w0 = sW[(xb << cw) | xw0], w1 = sW[(xb << cw) | xw1];
-      r0 = mac2(t00, t01, w0);
-      r1 = mac2(t10, t11, w1);
-    } else {
-      r0 = make_float2(t00.x + t01.x, t00.y + t01.y);
-      r1 = make_float2(t10.x + t11.x, t10.y + t11.y);
+    const float4 b00 = *pb0, b01 = *pq0;
+    float4 b10 = b00, b11 = b01;
+    if (!pairb) {
+      b10 = *pb1;
+      b11 = *pq1;
+      pb1 += strideB;
+      pq1 += strideB;
     }
-    __stcs(reinterpret_cast<float4*>(out + ob), make_float4(r0.x, r0.y, r1.x, r1.y));
-    ob = ((ob | ~bmask) + 1) & bmask;
+    pb0 += strideB;
+    pq0 += strideB;
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) {
+      const float2 t00 = mac2(a[gi][0][0][0], a[gi][0][0][1], b00), t01 = mac2(a[gi][0][1][0], a[gi][0][1][1], b01);
+      const float2 t10 = mac2(a[gi][1][0][0], a[gi][1][0][1], b10), t11 = mac2(a[gi][1][1][0], a[gi][1][1][1], b11);
+      float2 r0, r1;
+      if (HASW) {
+        const float4 w0 = *pw0[gi], w1 = *pw1[gi];
+        pw0[gi] += strideW;
+        pw1[gi] += strideW;
+        r0 = mac2(t00, t01, w0);
+        r1 = mac2(t10, t11, w1);
+      } else {
+        r0 = make_float2(t00.x + t01.x, t00.y + t01.y);
+        r1 = make_float2(t10.x + t11.x, t10.y + t11.y);
+      }
+      __stcs(reinterpret_cast<float4*>(og[gi] + ob), make_float4(r0.x, r0.y, r1.x, r1.y));
+    }
+    ob = ((ob | ~bmask) + 1u) & bmask;
   }
 }
 
-__global__ void __launch_bounds__(256, 3) xt_kernel(const __grid_constant__ YLaunch L) {
-  extern __shared__ __align__(16) unsigned char ysmem[];
-  __shared__ YItemSmem X;
-  __shared__ __align__(16) YDesc SD;
-  pdl_trigger();
-  pdl_wait();
+template <int G>
+__device__ __forceinline__ void xt_body(const YLaunch& L, unsigned char* ysmem, YItemSmem& X, YDesc& SD) {
   const uint64_t per = (L.total_tiles + gridDim.x - 1) / gridDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * per;
   const uint64_t t1 = min(L.total_tiles, t0 + per);
   const uint32_t set = blockIdx.y, tid = threadIdx.x;
-  uint64_t item_end = 0, first = 0, bmask = 0;
+  uint64_t item_end = 0, first = 0;
+  uint32_t bmask = 0;
+  uint32_t prev[kYG];
   const YDesc* d = &SD;
   const char* in = nullptr;
   char* ws = nullptr;
@@ -240,6 +300,14 @@ __global__ void __launch_bounds__(256, 3) xt_kernel(const __grid_constant__ YLau
         X.s2[tid] = op.vs2 == 0xff ? 0u : 1u << op.vs2;
         X.c64[tid] = op.c64;
       }
+      if (tid < kYMaxGroups) {  // group gi = element bits 9.. (0 beyond 2^g)
+        const uint32_t e = (tid < (1u << d->g)) ? tid << kXABits : 0u;
+        const uint64_t o = ygather(e, d->arun, d->n_arun);
+        X.og[tid] = o;
+        X.gw[tid] = (uint32_t)ygather(e, d->awrun, d->n_awrun);
+        for (uint32_t k = 0; k < nA; ++k)
+          X.goff[k][tid] = (uint32_t)ygather(o, d->ops[k].runs, d->ops[k].n_runs);
+      }
       for (uint32_t q = 0; q < nB + nW; ++q) {
         const bool isw = q >= nB;
         const YOp& op = d->ops[nA + q];
@@ -266,34 +334,43 @@ __global__ void __launch_bounds__(256, 3) xt_kernel(const __grid_constant__ YLau
       xc1 = (uint32_t)ygather(e0 + 1u, d->acrun, d->n_acrun);
       xw0 = (uint32_t)ygather(e0, d->awrun, d->n_awrun);
       xw1 = (uint32_t)ygather(e0 + 1u, d->awrun, d->n_awrun);
-      bmask = 0;
+      bmask = 0;  // output rank <= 32 (host check): 32-bit element offsets
       for (uint32_t r = 0; r < d->n_brun; ++r) {
         const uint32_t w = d->brun[r];
-        bmask |= ((1ull << ((w >> 16) & 0xff)) - 1) << ((w >> 8) & 0xff);
+        bmask |= (uint32_t)(((1ull << ((w >> 16) & 0xff)) - 1) << ((w >> 8) & 0xff));
       }
+#pragma unroll
+      for (int q = 0; q < kYG; ++q) prev[q] = 0xffffffffu;  // no stage of this item yet
     } else {
       __syncthreads();  // stage reuse
     }
     const uint64_t obase = ygather(t - first, d->trun, d->n_trun);
     float2* outp = reinterpret_cast<float2*>(const_cast<char*>(yresolve(d->out, in, ws))) + (obase | oa);
     if (d->nW)
-      xt_tile<true>(*d, X, ea, eb, xc0, xc1, xw0, xw1, obase, outp, bmask, ysmem);
+      xt_tile<true, G>(*d, X, ea, eb, xc0, xc1, xw0, xw1, obase, outp, bmask, ysmem, prev);
     else
-      xt_tile<false>(*d, X, ea, eb, xc0, xc1, xw0, xw1, obase, outp, bmask, ysmem);
+      xt_tile<false, G>(*d, X, ea, eb, xc0, xc1, xw0, xw1, obase, outp, bmask, ysmem, prev);
   }
+}
+
+// One launch holds items of one group count (the executor launches per g).
+template <int G, int MINB>
+__global__ void __launch_bounds__(256, MINB) xt_kernel(const __grid_constant__ YLaunch L) {
+  extern __shared__ __align__(16) unsigned char ysmem[];
+  __shared__ YItemSmem X;
+  __shared__ __align__(16) YDesc SD;
+  pdl_trigger();
+  pdl_wait();
+  xt_body<G>(L, ysmem, X, SD);
 }
 
 }  // namespace
 
-int launch_xt(const YLaunch& L, void* stream) {
-  if (!L.n_items || !L.n_sets || !L.total_tiles) return QTN_OK;
-  if (L.n_sets > 65535 || L.total_tiles > 0x7fffffffull) {
-    set_error("xt_kernel: grid too large");
-    return QTN_EINVAL;
-  }
+template <int G, int MINB>
+static int launch_xt_g(const YLaunch& L, void* stream) {
   static std::atomic<uint64_t> attr{0};
   if (needs_setup(attr)) {
-    cudaError_t e = cudaFuncSetAttribute(xt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(xt_kernel<G, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (kYStageB + kYStageW) * 8);
     if (e != cudaSuccess) {
       set_error(std::string("xt_kernel attribute: ") + cudaGetErrorString(e));
@@ -308,13 +385,13 @@ int launch_xt(const YLaunch& L, void* stream) {
   int per_sm = 0;
   const char* xc = getenv("QTN_XT_CTAS");
   if (xc) per_sm = atoi(xc);
-  if (per_sm <= 0 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xt_kernel, 256, L.stage_bytes) != cudaSuccess)
-    per_sm = 3;
+  if (per_sm <= 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xt_kernel<G, MINB>, 256,
+                                                                   L.stage_bytes) != cudaSuccess)
+    per_sm = MINB;
   per_sm = std::max(1, per_sm);
   const uint64_t ctas = std::min<uint64_t>(L.total_tiles, (uint64_t)n_sm * (uint64_t)per_sm);
   dim3 grid((uint32_t)ctas, L.n_sets);
-  cudaError_t e = launch_pdl<true>(xt_kernel, grid, dim3(256), L.stage_bytes,
+  cudaError_t e = launch_pdl<true>(xt_kernel<G, MINB>, grid, dim3(256), L.stage_bytes,
                                    reinterpret_cast<cudaStream_t>(stream), L);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -322,6 +399,20 @@ int launch_xt(const YLaunch& L, void* stream) {
     return QTN_ECUDA;
   }
   return QTN_OK;
+}
+
+int launch_xt(const YLaunch& L, void* stream) {
+  if (!L.n_items || !L.n_sets || !L.total_tiles) return QTN_OK;
+  if (L.n_sets > 65535 || L.total_tiles > 0x7fffffffull) {
+    set_error("xt_kernel: grid too large");
+    return QTN_EINVAL;
+  }
+  // the launch's items share one group count (level lists are built per g)
+  switch (L.g) {
+    case 0: return launch_xt_g<1, 3>(L, stream);
+    case 1: return launch_xt_g<2, 3>(L, stream);
+    default: return launch_xt_g<4, 2>(L, stream);
+  }
 }
 
 }  // namespace qtn
