@@ -574,29 +574,37 @@ bool encode_expand_desc(const BucketSpec& s, XDesc& d) {
   return true;
 }
 
-// Expanding bucket + consumer pair (qtn_stream.h YDesc, kernel in qtn_xt.cu).
-// Everything is expressed over O2's bits; v1 and v2 are the two summed bits.
+// Expanding bucket + consumers chain (qtn_stream.h YDesc, kernel in
+// qtn_xt.cu).  Extended bit space: F's bits [0, R), then the trailing summed
+// variables s_j at R + j; v1 and v2 are strides of their own.
 bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
   const char* ev = getenv("QTN_XT_MIN_R");
   const int min_r = ev ? atoi(ev) : 14;
-  const int R = (int)s.out_vars.size();
-  if (R < min_r || R > 32) return false;
+  const int R = (int)s.out_vars.size(), K = (int)s.trailing.size();
+  if (R + K + 1 < min_r || R < 10 || R > 32 || K > kYMaxK) return false;
+  // more than one trailing trace only into large results (measured: config 4
+  // 0.575 -> 0.506 ms with them, config 3 default 2.209 -> 2.247 ms: its
+  // small chains run slower with 4 groups per thread)
+  const char* krv = getenv("QTN_XT_K_MIN_R");
+  if (K > 1 && R < (krv ? atoi(krv) : 20)) return false;
   std::memset(&d, 0, sizeof(d));
-  auto obit = [&](int32_t u) -> int {
+  auto ebit = [&](int32_t u) -> int {
     for (int i = 0; i < R; ++i)
       if (s.out_vars[i] == u) return R - 1 - i;
+    for (int j = 0; j < K; ++j)
+      if (s.trailing[j] == u) return R + j;
     return -1;
   };
   const int n = (int)s.opvars.size();
-  std::vector<uint64_t> dep(n, 0);  // O2 bits each operand depends on
+  std::vector<uint64_t> dep(n, 0);  // extended bits each operand depends on
   for (int t = 0; t < n; ++t)
     for (int32_t u : s.opvars[t])
       if (u != s.v1 && u != s.v2) {
-        const int b = obit(u);
-        if (b < 0) return false;  // the consumer must not add variables
+        const int b = ebit(u);
+        if (b < 0) return false;  // the consumers must not add variables
         dep[t] |= 1ull << b;
       }
-  for (int t = s.n1; t < n; ++t)  // the consumer's operands never hold v1
+  for (int t = s.n1; t < n; ++t)  // the consumers' operands never hold v1
     if (std::find(s.opvars[t].begin(), s.opvars[t].end(), s.v1) != s.opvars[t].end()) return false;
   const uint64_t pdep = dep[s.primary];
   std::vector<int> A, Bs, Ws;
@@ -606,7 +614,7 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
   for (int t : A) adep |= dep[t];
   for (int t : Bs) bdep |= dep[t];
   // consumer operands: on A-side bits only -> A-type (per-thread loads),
-  // otherwise staged with the B bits (W group)
+  // otherwise staged with the loop bits (W group)
   for (int t = s.n1; t < n; ++t) {
     if ((dep[t] & ~adep) == 0) A.push_back(t);
     else {
@@ -615,6 +623,12 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
     }
   }
   if ((int)A.size() > kYMaxA || (int)Ws.size() > kYMaxG) return false;
+  // trailing summed variables: those the A side depends on are owned by the
+  // thread (group bits), the others are loop bits (innermost)
+  std::vector<int> gbits, sbits;
+  for (int j = 0; j < K; ++j) (((adep >> (R + j)) & 1) ? gbits : sbits).push_back(R + j);
+  const int g = (int)gbits.size(), hs = (int)sbits.size();
+  if (g > kYMaxGB) return false;
   std::vector<int> ta;
   for (int b = 0; b < 6; ++b) {
     if (!((adep >> b) & 1)) return false;
@@ -630,41 +644,26 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
     }
   if ((int)ta.size() < kXABits) return false;
   std::sort(ta.begin(), ta.end());
-  // group bits: further A bits the B group does not see (one staged B row
-  // then serves every group of a thread); those the W group does not see first
-  const char* gv = getenv("QTN_XT_G");
-  const int gmax = std::min(kYMaxGB, gv ? atoi(gv) : 0);  // measured: config 4 0.654 / 0.670 / 0.713 ms at g = 0 / 1 / 2
-  int g = 0;
-  for (int pass = 0; pass < 2 && g < gmax; ++pass)
-    for (int b = 6; b < R && g < gmax; ++b) {
-      if (!((adep >> b) & 1) || ((bdep >> b) & 1) || std::find(ta.begin(), ta.end(), b) != ta.end()) continue;
-      if (pass == 0 && ((wdep >> b) & 1)) continue;
-      ta.push_back(b);
-      ++g;
-    }
-  std::vector<int> nbits;  // B-bit candidates: no A-side dependence
+  ta.insert(ta.end(), gbits.begin(), gbits.end());  // element bits 9.. : the groups
+  std::vector<int> nbits;  // kept loop-bit candidates: F bits with no A-side dependence
   for (int b = 0; b < R; ++b)
     if (!((adep >> b) & 1)) nbits.push_back(b);
   const char* hv = getenv("QTN_XT_MAX_H");
-  const int hmax = std::min<int>(std::min<int>((int)nbits.size(), hv ? atoi(hv) : kYMaxH), kYMaxH);
+  const int hmax = std::min<int>(std::min<int>((int)nbits.size() + hs, hv ? atoi(hv) : kYMaxH), kYMaxH);
   std::vector<int> tc, tw;
-  int c = 0, cw = 0, h = 0;
-  for (;; ta.pop_back(), --g) {  // small pairs: fewer groups, more tiles
-    tc.clear();
-    tw.clear();
-    for (int b : ta) {
-      if ((bdep >> b) & 1) tc.push_back(b);
-      if ((wdep >> b) & 1) tw.push_back(b);
-    }
-    c = (int)tc.size();
-    cw = (int)tw.size();
-    h = hmax;
-    while (h > 0 && ((4 << (h + c)) > kYStageB || (!Ws.empty() && (2 << (h + cw)) > kYStageW))) --h;
-    while (h > 2 && R - kXABits - g - h < 11) --h;  // >= ~2048 tiles when the pair allows it
-    if (g == 0 || R - kXABits - g - h >= 9) break;
+  for (int b : ta) {
+    if ((bdep >> b) & 1) tc.push_back(b);
+    if ((wdep >> b) & 1) tw.push_back(b);
   }
-  if (h < 1) return false;
-  std::vector<int> tb(nbits.begin(), nbits.begin() + h);
+  const int c = (int)tc.size(), cw = (int)tw.size();
+  int h = hmax;
+  while (h > 0 && ((4 << (h + c)) > kYStageB || (!Ws.empty() && (2 << (h + cw)) > kYStageW))) --h;
+  const char* tlv = getenv("QTN_XT_TILES_LOG2");
+  const int tiles_log2 = tlv ? atoi(tlv) : 9;  // measured 8..11: config 4 0.504 / 0.506 / 0.562 / 0.646 ms
+  while (h - hs > 2 && R - kXABits - (h - hs) < tiles_log2) --h;  // >= ~512 tiles when the chain allows it
+  if (h < 1 || h < hs || cw > 9 || c > 9) return false;
+  std::vector<int> tb(sbits);  // x_b: summed loop bits lowest, then the kept ones
+  tb.insert(tb.end(), nbits.begin(), nbits.begin() + (h - hs));
   std::vector<int> rest;
   for (int b = 0; b < R; ++b)
     if (std::find(ta.begin(), ta.end(), b) == ta.end() && std::find(tb.begin(), tb.end(), b) == tb.end())
@@ -683,12 +682,12 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
     const double save_w = Ws.empty() ? 0.0 : (double)(2 << (h + cw)) * (1.0 - std::ldexp(1.0, -(int)f_w.size()));
     const char* ov = getenv("QTN_XT_ORDER");
     if (!(ov && ov[0] == '0')) {
-    rest = f_both;
-    const auto& first = save_b >= save_w ? f_b : f_w;
-    const auto& second = save_b >= save_w ? f_w : f_b;
-    rest.insert(rest.end(), first.begin(), first.end());
-    rest.insert(rest.end(), second.begin(), second.end());
-    rest.insert(rest.end(), others.begin(), others.end());
+      rest = f_both;
+      const auto& first = save_b >= save_w ? f_b : f_w;
+      const auto& second = save_b >= save_w ? f_w : f_b;
+      rest.insert(rest.end(), first.begin(), first.end());
+      rest.insert(rest.end(), second.begin(), second.end());
+      rest.insert(rest.end(), others.begin(), others.end());
     }
   }
   auto put = [&](const std::vector<std::pair<int, int>>& pr, uint32_t* dst, uint8_t& cnt) {
@@ -704,7 +703,7 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
     for (size_t i = 0; i < bits.size(); ++i) pr.push_back({(int)i, bits[i]});
     return put(pr, dst, cnt);
   };
-  auto put_sub = [&](const std::vector<int>& sub, uint32_t* dst, uint8_t& cnt) {  // ta element bits -> compact
+  auto put_sub = [&](const std::vector<int>& sub, uint32_t* dst, uint8_t& cnt) {  // element bits -> compact
     std::vector<std::pair<int, int>> pr;
     for (size_t i = 0; i < ta.size(); ++i) {
       auto it = std::find(sub.begin(), sub.end(), ta[i]);
@@ -726,7 +725,7 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
     for (int j = 0; j < rk; ++j) {
       if (vs[j] == s.v1) o.vs1 = (uint8_t)(rk - 1 - j);
       else if (vs[j] == s.v2) o.vs2 = (uint8_t)(rk - 1 - j);
-      else q.push_back({obit(vs[j]), rk - 1 - j});
+      else q.push_back({ebit(vs[j]), rk - 1 - j});
     }
     o.ptr = s.optag[t];
     o.c64 = s.opc64[t];
@@ -742,23 +741,17 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
   d.out = s.out_tag;
   d.R = (uint8_t)R;
   d.h = (uint8_t)h;
+  d.hs = (uint8_t)hs;
   d.c = (uint8_t)c;
   d.cw = (uint8_t)cw;
+  d.g = (uint8_t)g;
   d.nA = (uint8_t)A.size();
   d.nB = (uint8_t)Bs.size();
   d.nW = (uint8_t)Ws.size();
-  d.g = (uint8_t)g;
-  d.n_tiles = 1ull << (R - kXABits - g - h);
+  d.n_tiles = 1ull << (R - kXABits - (h - hs));
   if (getenv("QTN_DEBUG_DESC") && R >= atoi(getenv("QTN_DEBUG_DESC")))
-  {
-    fprintf(stderr, "ydesc R=%d h=%d g=%d c=%d cw=%d nA=%d nB=%d nW=%d tiles=%llu", R, h, g, c, cw,
-            (int)A.size(), (int)Bs.size(), (int)Ws.size(), (unsigned long long)d.n_tiles);
-    for (int q = 0; q < d.nA + d.nB + d.nW; ++q)
-      fprintf(stderr, " %c(r%zu vs1=%d vs2=%d)", q < d.nA ? 'A' : (q < d.nA + d.nB ? 'B' : 'W'),
-              s.opvars[q < (int)A.size() ? A[q] : (q < (int)(A.size() + Bs.size()) ? Bs[q - A.size()] : Ws[q - A.size() - Bs.size()])].size(),
-              d.ops[q].vs1 == 0xff ? -1 : d.ops[q].vs1, d.ops[q].vs2 == 0xff ? -1 : d.ops[q].vs2);
-    fprintf(stderr, "\n");
-  }
+    fprintf(stderr, "ydesc R=%d K=%d h=%d hs=%d g=%d c=%d cw=%d nA=%d nB=%d nW=%d tiles=%llu\n", R, K, h, hs, g,
+            c, cw, (int)A.size(), (int)Bs.size(), (int)Ws.size(), (unsigned long long)d.n_tiles);
   return true;
 }
 
@@ -1541,10 +1534,24 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
     // adding any; the pair runs as one pass and O1 is never stored.  Marked
     // as a 2-bucket chain (head = the expanding bucket).  QTN_XT=0 disables.
     std::vector<char> is_xt(nb, 0);
-    auto xt_spec = [&](int32_t bi, int32_t c, bool tags, YPairSpec& ys,
+    // members of the chain headed by bi: its consumer, then up to max_k
+    // trailing traces (buckets whose other operands add no variables)
+    auto xt_members = [&](int32_t bi, int max_k) {
+      std::vector<int32_t> m;
+      int32_t cur = bi;
+      while ((int)m.size() < 1 + max_k) {
+        const int32_t c = P->tensors[P->buckets[cur].out].last_use;
+        if (c < 0 || c >= nb || chain_head[c] >= 0) break;
+        const auto& cb = P->buckets[c];
+        if (cb.rank != P->buckets[cur].rank - 1 || !P->tensors[cb.out].c64) break;
+        m.push_back(c);
+        cur = c;
+      }
+      return m;
+    };
+    auto xt_spec = [&](int32_t bi, const std::vector<int32_t>& mem, bool tags, YPairSpec& ys,
                        const std::function<uint64_t(int32_t)>& tag) {
       const auto& b = P->buckets[bi];
-      const auto& cb = P->buckets[c];
       for (int32_t id : b.ops) {
         ys.opvars.push_back(P->tensors[id].vars);
         ys.opc64.push_back(P->tensors[id].c64 ? 1 : 0);
@@ -1552,39 +1559,47 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       }
       ys.n1 = (int32_t)b.ops.size();
       ys.primary = b.primary;
-      for (int32_t id : cb.ops) {
-        if (id == b.out) continue;
-        ys.opvars.push_back(P->tensors[id].vars);
-        ys.opc64.push_back(P->tensors[id].c64 ? 1 : 0);
-        ys.optag.push_back(tags ? tag(id) : 0);
+      int32_t running = b.out;
+      for (size_t q = 0; q < mem.size(); ++q) {
+        const auto& cb = P->buckets[mem[q]];
+        for (int32_t id : cb.ops) {
+          if (id == running) continue;
+          ys.opvars.push_back(P->tensors[id].vars);
+          ys.opc64.push_back(P->tensors[id].c64 ? 1 : 0);
+          ys.optag.push_back(tags ? tag(id) : 0);
+        }
+        if (q == 0) ys.v2 = cb.v;
+        else ys.trailing.push_back(cb.v);
+        running = cb.out;
       }
       ys.v1 = b.v;
-      ys.v2 = cb.v;
-      ys.out_vars = P->tensors[cb.out].vars;
-      ys.out_tag = tags ? tag(cb.out) : 0;
+      ys.out_vars = P->tensors[running].vars;
+      ys.out_tag = tags ? tag(running) : 0;
     };
     {
       const char* xv = getenv("QTN_XT");
       const bool xt_on = !(xv && xv[0] == '0');
+      const char* kv = getenv("QTN_XT_MAX_K");
+      const int max_k = std::min(kYMaxK, kv ? atoi(kv) : kYMaxK);
       for (int bi = 0; xt_on && bi < nb; ++bi) {
         const auto& b = P->buckets[bi];
-        if (b.ops.size() < 2 || !P->tensors[b.out].c64) continue;
+        if (b.ops.size() < 2 || !P->tensors[b.out].c64 || chain_head[bi] >= 0) continue;
         int maxop = 0;
         for (int32_t id : b.ops) maxop = std::max(maxop, P->tensors[id].rank());
         if (maxop > b.rank) continue;  // not expanding: the primary alone holds every variable
-        const int32_t c = P->tensors[b.out].last_use;
-        if (c < 0 || c >= nb) continue;
-        const auto& cb = P->buckets[c];
-        if (cb.rank != b.rank - 1 || !P->tensors[cb.out].c64) continue;
-        YPairSpec ys;
-        xt_spec(bi, c, false, ys, nullptr);
-        YDesc probe;
-        if (!encode_xt_desc(ys, probe)) continue;
+        std::vector<int32_t> mem = xt_members(bi, max_k);
+        for (; !mem.empty(); mem.pop_back()) {  // the longest chain that encodes
+          YPairSpec ys;
+          xt_spec(bi, mem, false, ys, nullptr);
+          YDesc probe;
+          if (encode_xt_desc(ys, probe)) break;
+        }
+        if (mem.empty()) continue;
         is_xt[bi] = 1;
         chain_head[bi] = bi;
-        chain_head[c] = bi;
-        chain_tail[bi] = c;
-        chain_len[bi] = 2;
+        for (int32_t c : mem) chain_head[c] = bi;
+        chain_tail[bi] = mem.back();
+        chain_len[bi] = 1 + (int)mem.size();
       }
     }
     // Product chains (qtn_fused.cu): a bucket of >= 2 operands whose result
@@ -1796,9 +1811,12 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       }
       int32_t lv = 0;
       for (int32_t id : P->buckets[bi].ops) lv = std::max(lv, tlevel[id]);
-      if (is_xt[bi])  // the pair also waits for the consumer's other operands
-        for (int32_t id : P->buckets[chain_tail[bi]].ops)
-          if (id != P->buckets[bi].out) lv = std::max(lv, tlevel[id]);
+      if (is_xt[bi])  // the chain also waits for its consumers' other operands
+        for (int32_t c = P->tensors[P->buckets[bi].out].last_use;; c = P->tensors[P->buckets[c].out].last_use) {
+          for (int32_t id : P->buckets[c].ops)
+            if (P->tensors[id].input || chain_head[P->tensors[id].born] != bi) lv = std::max(lv, tlevel[id]);
+          if (c == chain_tail[bi]) break;
+        }
       P->hbm_level[bi] = lv;  // 0-based level index
       const int32_t last = h >= 0 ? chain_tail[bi] : bi;
       tlevel[P->buckets[last].out] = lv + 1;
@@ -1857,7 +1875,12 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         if (chain_head[bi] != bi) continue;
         if (is_xt[bi]) {
           YPairSpec ys;
-          xt_spec(bi, chain_tail[bi], true, ys, tag_of);
+          std::vector<int32_t> mem;
+          for (int32_t c = P->tensors[b.out].last_use;; c = P->tensors[P->buckets[c].out].last_use) {
+            mem.push_back(c);
+            if (c == chain_tail[bi]) break;
+          }
+          xt_spec(bi, mem, true, ys, tag_of);
           YDesc yd;
           if (!encode_xt_desc(ys, yd)) {
             delete P;
@@ -2077,8 +2100,12 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         if (sm_off[id] < 0)  // subtree-internal operands never leave the SM
           eb += std::ldexp((double)elem_bytes(P->tensors[id].c64), P->tensors[id].rank());
       if (h >= 0 && is_xt[bi])
-        for (int32_t id : P->buckets[chain_tail[bi]].ops)
-          if (id != b.out) eb += std::ldexp((double)elem_bytes(P->tensors[id].c64), P->tensors[id].rank());
+        for (int32_t c = P->tensors[b.out].last_use;; c = P->tensors[P->buckets[c].out].last_use) {
+          for (int32_t id : P->buckets[c].ops)
+            if (P->tensors[id].input || chain_head[P->tensors[id].born] != bi)
+              eb += std::ldexp((double)elem_bytes(P->tensors[id].c64), P->tensors[id].rank());
+          if (c == chain_tail[bi]) break;
+        }
       if (sm_off[b.out] >= 0) continue;
       const auto& o = P->tensors[P->buckets[h >= 0 ? chain_tail[bi] : bi].out];
       eb += std::ldexp((double)elem_bytes(o.c64), o.rank());

@@ -226,63 +226,71 @@ struct XLaunch {
 };
 int launch_expand(const XLaunch& L, void* stream);
 
-// ---- expanding bucket + its consumer as one pass (qtn_xt.cu).  The
+// ---- expanding bucket + its consumers as one pass (qtn_xt.cu).  The
 // union-size result O1 of an expanding bucket (eliminating v1) is read by
 // exactly one bucket, which eliminates v2 of it, often a (weighted) partial
-// trace: contraction.py:90-96 twice.  When that consumer adds no variables,
-//   O2[o] = sum_{v2} W_{v2}(o) * sum_{v1} A_{v1,v2}(o) * B_{v1,v2}(o)
-// is evaluated per O2 element and O1 (the largest tensor of the network) is
-// never written or read back.  Index space: the O2 bits plus (v2, v1).
-//   A-type operands: every operand that depends on no B bit (the expanding
-//     bucket's A side, plus the consumer's operands on A-side variables):
-//     loaded per thread for its 2 adjacent outputs x 4 (v2, v1) values;
+// trace, and that result by further partial traces (s_1 .. s_K):
+// contraction.py:90-96 K + 2 times in a row.  When the consumers add no
+// variables,
+//   F[o] = sum_{s_1..s_K} sum_{v2} W_{v2}(o,s) * sum_{v1} A_{v1,v2}(o,s) * B_{v1,v2}(o,s)
+// is evaluated per element of the last result F, and O1 (the largest tensor
+// of the network) and the chain's intermediates are never written or read
+// back.  Index space: F's bits [0, R), then the trailing summed variables
+// s_j as extended bits R + j; v2 and v1 are strides of their own.
+//   A-type operands: every operand that depends on no loop bit (the
+//     expanding bucket's A side, the consumers' operands on A-side
+//     variables): loaded per thread for its 2 adjacent outputs x 2^g groups
+//     x 4 (v2, v1) values;
 //   B group: the expanding bucket's B side, staged per tile as
-//     Bst[x_b][x_c][v2][v1] (x_c: tile-local A bits it depends on);
-//   W group: the consumer's operands that depend on B bits, staged as
+//     Bst[v2][x_b][x_c][v1] (x_c: thread-owned bits it depends on);
+//   W group: the consumers' operands that depend on loop bits, staged as
 //     Wst[x_b][x_w][v2].
-// Tile = 9 tile-local A bits (256 threads x 2 outputs) x h B bits, as in the
-// expanding-bucket kernel.  complex64 intermediates only (float math).
+// Tile = 9 tile-local A bits of F (256 threads x 2 adjacent outputs) x 2^g
+// groups (the trailing summed variables the A side depends on: a thread sums
+// over them in registers) x h loop bits (hs of them trailing summed
+// variables, innermost; the other h - hs are F bits no A-side operand depends
+// on).  complex64 intermediates only (float math).
 constexpr int kYMaxA = 6;        // A-type operands
 constexpr int kYMaxG = 2;        // operands per staged group
 constexpr int kYOps = kYMaxA + 2 * kYMaxG;
-constexpr int kYMaxH = 6;        // B bits per tile
-constexpr int kYMaxGB = 2;       // group bits (2^g output pairs per thread)
-constexpr int kYStageB = 4096;   // staged B entries (x_b, x_c, v2, v1)
+constexpr int kYMaxH = 6;        // loop bits per tile
+constexpr int kYMaxGB = 2;       // group bits (2^g summed positions per thread)
+constexpr int kYMaxK = 3;        // trailing traces
+constexpr int kYStageB = 4096;   // staged B entries (v2, x_b, x_c, v1)
 constexpr int kYStageW = 2048;   // staged W entries (x_b, x_w, v2)
 struct YOp {
   uint64_t ptr;                  // tagged
   uint8_t vs1, vs2, c64, n_runs; // bit of v1 / v2 in the operand index (0xff: none)
-  uint32_t runs[kXRuns];         // O2 bits -> operand bits
+  uint32_t runs[kXRuns];         // extended bits (F bits, then s_j at R + j) -> operand bits
   uint32_t pad;
 };
 struct YDesc {
   uint64_t out;                  // tagged
   uint64_t n_tiles;
-  uint8_t R, h, c, cw, nA, nB, nW, n_trun, n_arun, n_brun, n_crun, n_wrun, n_acrun, n_awrun, g, pad;
-  // g: a thread owns 2^g groups of 2 adjacent outputs (element bits 9..9+g:
-  // A bits the B group does not depend on, so one staged B row serves them all)
-  uint32_t trun[kXRuns];         // tile index bits -> output bits
-  uint32_t arun[kXRuns];         // tile-local A element bits (9 + g) -> output bits
-  uint32_t brun[kXRuns];         // x_b bits -> output bits
-  uint32_t crun[kXRuns];         // x_c bits -> output bits
-  uint32_t wrun[kXRuns];         // x_w bits -> output bits
-  uint32_t acrun[kXRuns];        // tile-local A element bits -> x_c bits
-  uint32_t awrun[kXRuns];        // tile-local A element bits -> x_w bits
+  uint8_t R, h, c, cw, nA, nB, nW, n_trun, n_arun, n_brun, n_crun, n_wrun, n_acrun, n_awrun, g, hs;
+  uint32_t trun[kXRuns];         // tile index bits -> F bits
+  uint32_t arun[kXRuns];         // element bits (9 tile-local A bits, then g group bits) -> extended bits
+  uint32_t brun[kXRuns];         // x_b bits (hs summed, then h - hs kept) -> extended bits
+  uint32_t crun[kXRuns];         // x_c bits -> extended bits
+  uint32_t wrun[kXRuns];         // x_w bits -> extended bits
+  uint32_t acrun[kXRuns];        // element bits -> x_c bits
+  uint32_t awrun[kXRuns];        // element bits -> x_w bits
   YOp ops[kYOps];                // A-type [0, nA), B group [nA, nA+nB), W group after
 };
 static_assert(sizeof(YOp) % 16 == 0, "YOp");
 static_assert(sizeof(YDesc) % 16 == 0, "YDesc");
 struct YPairSpec {
-  std::vector<std::vector<int32_t>> opvars;  // the expanding bucket's operands, then the consumer's others
+  std::vector<std::vector<int32_t>> opvars;  // the expanding bucket's operands, then the consumers' others
   std::vector<uint8_t> opc64;
   std::vector<uint64_t> optag;
   int32_t n1;                                // operands of the expanding bucket
   int32_t primary;                           // its primary
   int32_t v1, v2;
-  std::vector<int32_t> out_vars;             // O2's layout, MSB first
+  std::vector<int32_t> trailing;             // s_1 .. s_K, in elimination order
+  std::vector<int32_t> out_vars;             // F's layout, MSB first
   uint64_t out_tag;
 };
-// Host encoder: true when the pair takes xt_kernel.
+// Host encoder: true when the chain takes xt_kernel.
 bool encode_xt_desc(const YPairSpec& s, YDesc& d);
 inline uint32_t xt_stage_bytes(const YDesc& d) {
   return 8u * ((4u << (d.h + d.c)) + (d.nW ? (2u << (d.h + d.cw)) : 0u));

@@ -78,7 +78,7 @@ struct YItemSmem {
   uint32_t tb[kYG][1 << kYMaxH];
   uint32_t tc[kYG][512];
   uint32_t goff[kYMaxA][kYMaxGroups];  // A-type operand offset of group gi
-  uint64_t og[kYMaxGroups];            // output offset of group gi
+  uint32_t gb[kYMaxGroups];            // x_c part of group gi
   uint32_t gw[kYMaxGroups];            // x_w part of group gi
   uint8_t c64[kYOps];
 };
@@ -208,53 +208,69 @@ __device__ __forceinline__ void xt_tile(const YDesc& d, YItemSmem& X, const uint
   }
   if (async) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
-  // 3. outputs: x_b -> output offset by a masked increment; shared-memory
-  // addresses advance by a stride per x_b (plane 1 and W at fixed offsets)
-  const uint32_t nb = 1u << h;
+  // 3. outputs.  x_b = kept << hs | summed: the shared-memory rows advance by
+  // one stride per x_b; the hs summed loop bits and the 2^g groups accumulate
+  // in registers, one 16-byte store per kept value (masked increment of the
+  // output offset)
+  const uint32_t nk = 1u << (h - d.hs), ns = 1u << d.hs;
   const bool pairb = xc0 == xc1;  // uniform per item: output bit 0 outside the B group
   const float4* pb0 = reinterpret_cast<const float4*>(smem) + xc0;
   const float4* pb1 = reinterpret_cast<const float4*>(smem) + xc1;
-  const float4* pq0 = pb0 + (nBst >> 2);  // plane v2 = 1
-  const float4* pq1 = pb1 + (nBst >> 2);
+  const uint32_t plane = nBst >> 2;  // float4 words to plane v2 = 1
   const uint32_t strideB = 1u << c, strideW = 1u << cw;
-  float2* og[G];
-  const float4 *pw0[G], *pw1[G];
+  const float4* pw0 = reinterpret_cast<const float4*>(stW) + xw0;
+  const float4* pw1 = reinterpret_cast<const float4*>(stW) + xw1;
+  uint32_t gb[G], gw[G];
+  bool gdepb = false;
 #pragma unroll
   for (int gi = 0; gi < G; ++gi) {
-    og[gi] = out + X.og[gi];
-    pw0[gi] = reinterpret_cast<const float4*>(stW) + (xw0 | X.gw[gi]);
-    pw1[gi] = reinterpret_cast<const float4*>(stW) + (xw1 | X.gw[gi]);
+    gb[gi] = X.gb[gi];
+    gw[gi] = X.gw[gi];
+    gdepb |= gb[gi] != 0u;
   }
   uint32_t ob = 0;
-#pragma unroll(G == 1 ? kXtUnroll : (G == 2 ? 2 : 1))
-  for (uint32_t xb = 0; xb < nb; ++xb) {
-    const float4 b00 = *pb0, b01 = *pq0;
-    float4 b10 = b00, b11 = b01;
-    if (!pairb) {
-      b10 = *pb1;
-      b11 = *pq1;
-      pb1 += strideB;
-      pq1 += strideB;
-    }
-    pb0 += strideB;
-    pq0 += strideB;
+#pragma unroll 1
+  for (uint32_t kept = 0; kept < nk; ++kept) {
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll 1
+    for (uint32_t sv = 0; sv < ns; ++sv) {
+      float4 b00, b01, b10, b11;
 #pragma unroll
-    for (int gi = 0; gi < G; ++gi) {
-      const float2 t00 = mac2(a[gi][0][0][0], a[gi][0][0][1], b00), t01 = mac2(a[gi][0][1][0], a[gi][0][1][1], b01);
-      const float2 t10 = mac2(a[gi][1][0][0], a[gi][1][0][1], b10), t11 = mac2(a[gi][1][1][0], a[gi][1][1][1], b11);
-      float2 r0, r1;
-      if (HASW) {
-        const float4 w0 = *pw0[gi], w1 = *pw1[gi];
-        pw0[gi] += strideW;
-        pw1[gi] += strideW;
-        r0 = mac2(t00, t01, w0);
-        r1 = mac2(t10, t11, w1);
-      } else {
-        r0 = make_float2(t00.x + t01.x, t00.y + t01.y);
-        r1 = make_float2(t10.x + t11.x, t10.y + t11.y);
+      for (int gi = 0; gi < G; ++gi) {
+        if (gi == 0 || gdepb) {
+          b00 = pb0[gb[gi]];
+          b01 = pb0[gb[gi] + plane];
+          b10 = b00;
+          b11 = b01;
+          if (!pairb) {
+            b10 = pb1[gb[gi]];
+            b11 = pb1[gb[gi] + plane];
+          }
+        }
+        const float2 t00 = mac2(a[gi][0][0][0], a[gi][0][0][1], b00), t01 = mac2(a[gi][0][1][0], a[gi][0][1][1], b01);
+        const float2 t10 = mac2(a[gi][1][0][0], a[gi][1][0][1], b10), t11 = mac2(a[gi][1][1][0], a[gi][1][1][1], b11);
+        if (HASW) {
+          const float4 w0 = pw0[gw[gi]], w1 = pw1[gw[gi]];
+          const float2 r0 = mac2(t00, t01, w0), r1 = mac2(t10, t11, w1);
+          acc0.x += r0.x;
+          acc0.y += r0.y;
+          acc1.x += r1.x;
+          acc1.y += r1.y;
+        } else {
+          acc0.x += t00.x + t01.x;
+          acc0.y += t00.y + t01.y;
+          acc1.x += t10.x + t11.x;
+          acc1.y += t10.y + t11.y;
+        }
       }
-      __stcs(reinterpret_cast<float4*>(og[gi] + ob), make_float4(r0.x, r0.y, r1.x, r1.y));
+      pb0 += strideB;
+      pb1 += strideB;
+      if (HASW) {
+        pw0 += strideW;
+        pw1 += strideW;
+      }
     }
+    __stcs(reinterpret_cast<float4*>(out + ob), make_float4(acc0.x, acc0.y, acc1.x, acc1.y));
     ob = ((ob | ~bmask) + 1u) & bmask;
   }
 }
@@ -302,8 +318,8 @@ __device__ __forceinline__ void xt_body(const YLaunch& L, unsigned char* ysmem, 
       }
       if (tid < kYMaxGroups) {  // group gi = element bits 9.. (0 beyond 2^g)
         const uint32_t e = (tid < (1u << d->g)) ? tid << kXABits : 0u;
-        const uint64_t o = ygather(e, d->arun, d->n_arun);
-        X.og[tid] = o;
+        const uint64_t o = ygather(e, d->arun, d->n_arun);  // extended bits of the group's summed variables
+        X.gb[tid] = (uint32_t)ygather(e, d->acrun, d->n_acrun);
         X.gw[tid] = (uint32_t)ygather(e, d->awrun, d->n_awrun);
         for (uint32_t k = 0; k < nA; ++k)
           X.goff[k][tid] = (uint32_t)ygather(o, d->ops[k].runs, d->ops[k].n_runs);
@@ -334,11 +350,8 @@ __device__ __forceinline__ void xt_body(const YLaunch& L, unsigned char* ysmem, 
       xc1 = (uint32_t)ygather(e0 + 1u, d->acrun, d->n_acrun);
       xw0 = (uint32_t)ygather(e0, d->awrun, d->n_awrun);
       xw1 = (uint32_t)ygather(e0 + 1u, d->awrun, d->n_awrun);
-      bmask = 0;  // output rank <= 32 (host check): 32-bit element offsets
-      for (uint32_t r = 0; r < d->n_brun; ++r) {
-        const uint32_t w = d->brun[r];
-        bmask |= (uint32_t)(((1ull << ((w >> 16) & 0xff)) - 1) << ((w >> 8) & 0xff));
-      }
+      // output bits of the kept loop bits (output rank <= 32, host check: 32-bit element offsets)
+      bmask = (uint32_t)ygather(((1u << d->h) - 1u) ^ ((1u << d->hs) - 1u), d->brun, d->n_brun);
 #pragma unroll
       for (int q = 0; q < kYG; ++q) prev[q] = 0xffffffffu;  // no stage of this item yet
     } else {
