@@ -173,38 +173,54 @@ __device__ __forceinline__ void xt_tile(const YDesc& d, YItemSmem& X, const uint
     }
   }
   if (async) asm volatile("cp.async.commit_group;\n" ::: "memory");
-  // 2. A-type product of this thread's outputs: a[group][j][v2][v1]
+  // 2. A-type product of this thread's outputs: a[group][j][v2][v1], formed
+  // in float (complex128 gate entries rounded once); the 8 loads of an
+  // operand issue together
   float2 a[G][2][2][2];
 #pragma unroll
   for (int gi = 0; gi < G; ++gi) {
-    double2 p[2][2][2];
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int v2 = 0; v2 < 2; ++v2)
 #pragma unroll
-        for (int v1 = 0; v1 < 2; ++v1) p[j][v2][v1] = make_double2(1.0, 0.0);
+        for (int v1 = 0; v1 < 2; ++v1) a[gi][j][v2][v1] = make_float2(1.f, 0.f);
 #pragma unroll
     for (uint32_t k = 0; k < kYMaxA; ++k) {
       if (k < nA) {
-        const uint32_t i0 = X.base[k] + ea[k] + X.goff[k][gi], s1 = X.s1[k], s2 = X.s2[k], c64 = X.c64[k];
-        const char* pk = X.ptr[k];
+        const uint32_t i0 = X.base[k] + ea[k] + X.goff[k][gi], s1 = X.s1[k], s2 = X.s2[k];
+        float2 v[2][2][2];
+        if (X.c64[k]) {
+          const float2* pk = reinterpret_cast<const float2*>(X.ptr[k]) + i0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v2 = 0; v2 < 2; ++v2)
+#pragma unroll
+              for (int v1 = 0; v1 < 2; ++v1) v[j][v2][v1] = __ldg(pk + (j * eb[k] + v2 * s2 + v1 * s1));
+        } else {
+          const double2* pk = reinterpret_cast<const double2*>(X.ptr[k]) + i0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v2 = 0; v2 < 2; ++v2)
+#pragma unroll
+              for (int v1 = 0; v1 < 2; ++v1) {
+                const double2 t = __ldg(pk + (j * eb[k] + v2 * s2 + v1 * s1));
+                v[j][v2][v1] = make_float2((float)t.x, (float)t.y);
+              }
+        }
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int v2 = 0; v2 < 2; ++v2)
 #pragma unroll
-            for (int v1 = 0; v1 < 2; ++v1)
-              p[j][v2][v1] = ycmul(p[j][v2][v1], yld(pk, i0 + j * eb[k] + v2 * s2 + v1 * s1, c64));
+            for (int v1 = 0; v1 < 2; ++v1) {
+              const float2 x = a[gi][j][v2][v1], y = v[j][v2][v1];
+              a[gi][j][v2][v1] = make_float2(fmaf(x.x, y.x, -x.y * y.y), fmaf(x.x, y.y, x.y * y.x));
+            }
       }
     }
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int v2 = 0; v2 < 2; ++v2)
-#pragma unroll
-        for (int v1 = 0; v1 < 2; ++v1)
-          a[gi][j][v2][v1] = make_float2((float)p[j][v2][v1].x, (float)p[j][v2][v1].y);
   }
   if (async) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
