@@ -61,6 +61,9 @@ __device__ __forceinline__ float2 mac2(float2 a0, float2 a1, float4 b) {
   return r;
 }
 
+#ifndef XT_MINB1
+#define XT_MINB1 4
+#endif
 #ifndef XT_UNROLL
 #define XT_UNROLL 1
 #endif
@@ -438,7 +441,7 @@ int launch_xt(const YLaunch& L, void* stream) {
   }
   // the launch's items share one group count (level lists are built per g)
   switch (L.g) {
-    case 0: return launch_xt_g<1, 3>(L, stream);
+    case 0: return launch_xt_g<1, XT_MINB1>(L, stream);
     case 1: return launch_xt_g<2, 3>(L, stream);
     default: return launch_xt_g<4, 2>(L, stream);
   }

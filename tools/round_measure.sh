@@ -23,12 +23,12 @@ python bench.py --workload config5 --steps 2 --c5-ws 30 --c5-ms 16 > gpurun_out/
 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 2 -c 1 -o gpurun_out/r/prof_stream_c5 python bench.py --workload config5 --steps 2 --c5-ws 30 --c5-ms 16 > gpurun_out/r/ncu3.log 2>&1; echo "ncu3 rc=$?"
 python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/plain_c4.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 --csv --log-file gpurun_out/r/launches_config4.csv python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu4.log 2>&1; echo "ncu4 rc=$?"
-# the largest expanding bucket of config 4 ([1,22,21]->26, 8th expand launch)
-ncu --set full --clock-control none --import-source on -k regex:expand_kernel -s 7 -c 1 -o gpurun_out/r/prof_expand_c4 python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu5.log 2>&1; echo "ncu5 rc=$?"
+# the largest chain of config 4 ([1,22,21] -> 26, its consumer [2,16,26] -> 25 and three traces -> 22: the 6th xt launch)
+ncu --set full --clock-control none --import-source on -k regex:xt_kernel -s 5 -c 1 -o gpurun_out/r/prof_xt_c4 python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu5.log 2>&1; echo "ncu5 rc=$?"
 python tools/micro/write_bw.py > gpurun_out/r/write_bw.txt 2>&1; echo "wbw rc=$?"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 320 --csv --log-file gpurun_out/r/launches_config3d.csv python bench.py --steps 1 --warmup 3 --workload config3-default --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu6.log 2>&1; echo "ncu6 rc=$?"
 for w in config4 config3-default; do timeout 300 python tools/timeline.py $w --out gpurun_out/r/timeline_$w.json > gpurun_out/r/timeline_$w.txt 2>&1; done
-QTN_FUSE_CHAIN=1 timeout 300 python bench.py --workload config3-default --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config3d_fused.json 2>&1; echo "c3d fused rc=$?"
-QTN_FUSE_CHAIN=1 timeout 300 python bench.py --workload config4 --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config4_fused.json 2>&1; echo "c4 fused rc=$?"
+QTN_XT=0 timeout 300 python bench.py --workload config3-default --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config3d_noxt.json 2>&1; echo "c3d noxt rc=$?"
+QTN_XT=0 timeout 300 python bench.py --workload config4 --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config4_noxt.json 2>&1; echo "c4 noxt rc=$?"
 python bench.py --steps 1 --warmup 3 --workload config3-default --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/plain_c3d_f.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:fused_kernel -s 20 -c 1 -o gpurun_out/r/prof_fused_c3d python bench.py --steps 1 --warmup 3 --workload config3-default --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu7.log 2>&1; echo "ncu7 rc=$?"

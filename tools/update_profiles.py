@@ -73,7 +73,13 @@ def main():
     sm = summary(os.path.join(R, "prof_setmajor.ncu-rep"))
     smem = summary(os.path.join(R, "prof_smem.ncu-rep"))
     c5 = summary(os.path.join(R, "prof_stream_c5.ncu-rep"))
-    s4 = agg["stream_kernel"]
+    s4 = agg.get("stream_kernel", {"launches": 0, "time_s": 0.0, "dram_bytes": 0.0})
+    for src, dst in [("bench_config3d_noxt", "config3d_noxt"), ("bench_config4_noxt", "config4_noxt")]:
+        line = last_json(os.path.join(R, src + ".json")) if os.path.exists(os.path.join(R, src + ".json")) else None
+        if line:
+            open(os.path.join(P, f"bench_{TAG}_{dst}.json"), "w").write(line)
+    f7 = os.path.join(R, "prof_fused_c3d.ncu-rep")
+    y4 = agg.get("xt_kernel")
     x4 = agg.get("expand_kernel")
     out = {"note": "dram_bytes_per_launch: DRAM bytes (read+write) of the kernel for one "
                    "evaluation of the workload; for multi-launch executors (set-major levels, "
@@ -82,9 +88,9 @@ def main():
                "sm_level_kernel_c64@config2": dict(sm, workload="config2: 150 edges x 1024 angle "
                                                               "sets, complex64 rows, one evaluation "
                                                               "= 15 level launches"),
-               "expand_kernel@config4": dict(summary(os.path.join(R, "prof_expand_c4.ncu-rep")),
-                                             workload="config4 edge #1058: the [1,22,21]->26 "
-                                                      "expanding bucket, one launch"),
+               "xt_kernel@config4": dict(summary(os.path.join(R, "prof_xt_c4.ncu-rep")),
+                                         workload="config4 edge #1058: the chain [1,22,21]->26, "
+                                                  "[2,16,26]->25, three traces ->22 as one launch"),
                "smem_net_kernel@config2-16sets": dict(smem, workload="config2, 16 angle sets "
                                                                      "(warp-resident executor)"),
                "stream_kernel@config5": dict(c5, workload="config5 w=30 m=16, one launch"),
@@ -115,6 +121,13 @@ def main():
             "time_sum_s": sum(v["time_s"] for v in agg3.values()),
             "dram_bytes_per_launch": sum(v["dram_bytes"] for v in agg3.values()),
             "by_kernel": agg3, "source": f"launches_{TAG}_config3d.json"}
+    if os.path.exists(f7):
+        out["kernels"]["fused_kernel@config3-default"] = dict(summary(f7), workload="config3 default: one fused_kernel launch")
+    if y4:
+        out["kernels"]["xt_kernel@config4-all"] = {
+            "kernel": "xt_kernel", "workload": "config4 edge #1058, one contraction: its xt_kernel launches",
+            "launches_summed": y4["launches"], "time_sum_s": y4["time_s"],
+            "dram_bytes_per_launch": y4["dram_bytes"], "source": f"launches_{TAG}_config4.json"}
     if x4:
         out["kernels"]["expand_kernel@config4-all"] = {
             "kernel": "expand_kernel", "workload": "config4 edge #1058, one contraction: its "
