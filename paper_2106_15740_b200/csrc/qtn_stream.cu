@@ -64,10 +64,7 @@ __device__ __forceinline__ double2 ld_op(const void* p, uint64_t i, uint32_t c64
   }
   return __ldcg(reinterpret_cast<const double2*>(p) + i);
 }
-// E elements per thread and pass: the E loads of an operand are independent
-// and issue together (a bucket of n operands is a chain of n load latencies
-// per pass whatever E is; small_kernel uses 4).
-template <int CG, int E = 1>
+template <int CG>
 __device__ __forceinline__ void small_eval(const uint8_t* dsc, const Bases& b, uint64_t o_begin,
                                            uint64_t o_end, uint64_t o_step) {
   const SHdr& h = *reinterpret_cast<const SHdr*>(dsc);
@@ -78,69 +75,34 @@ __device__ __forceinline__ void small_eval(const uint8_t* dsc, const Bases& b, u
   const char* P = resolve(h.p, b);
   char* out = const_cast<char*>(resolve(h.out, b));
   const uint32_t r1 = h.p_rank - 1u, pk = h.p_k;
-  for (uint64_t o = o_begin; o < o_end; o += E * o_step) {
-    uint64_t oo[E];
-    double2 a0[E], a1[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      oo[e] = o + e * o_step;
-      if (oo[e] >= o_end) oo[e] = o;  // past the end: recompute element o, no store
-      const uint64_t op = oo[e] & ((1ull << r1) - 1);
-      const uint64_t p0 = (op & ((1ull << pk) - 1)) | ((op >> pk) << (pk + 1));
-      a0[e] = ld_op<CG>(P, p0, h.p_c64);
-      a1[e] = ld_op<CG>(P, p0 | (1ull << pk), h.p_c64);
-    }
+  for (uint64_t o = o_begin; o < o_end; o += o_step) {
+    const uint64_t op = o & ((1ull << r1) - 1);
+    const uint64_t p0 = (op & ((1ull << pk) - 1)) | ((op >> pk) << (pk + 1));
+    double2 a0 = ld_op<CG>(P, p0, h.p_c64), a1 = ld_op<CG>(P, p0 | (1ull << pk), h.p_c64);
     for (uint32_t q = 0; q < h.nt; ++q) {
-      uint64_t bits[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) bits[e] = gather(oo[e], tr[q].runs, tr[q].n_runs);
+      const uint64_t bits = gather(o, tr[q].runs, tr[q].n_runs);
       for (uint32_t k = 0; k < tr[q].n_ops; ++k) {
         const SORec& O = orr[tr[q].first_op + k];
         const char* op_p = resolve(O.ptr, b);
-        double2 x0[E], x1[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const uint64_t idx = gather(bits[e], O.runs, O.n_runs);
-          x0[e] = ld_op<CG>(op_p, idx, O.c64);
-          x1[e] = ld_op<CG>(op_p, idx | (1ull << O.vshift), O.c64);
-        }
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          a0[e] = cmul(a0[e], x0[e]);
-          a1[e] = cmul(a1[e], x1[e]);
-        }
+        const uint64_t idx = gather(bits, O.runs, O.n_runs);
+        a0 = cmul(a0, ld_op<CG>(op_p, idx, O.c64));
+        a1 = cmul(a1, ld_op<CG>(op_p, idx | (1ull << O.vshift), O.c64));
       }
     }
     for (uint32_t g = 0; g < h.ng; ++g) {
       const char* gp = resolve(gr[g].ptr, b);
-      double2 x0[E], x1[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const uint64_t idx = gather(oo[e], gr[g].runs, gr[g].n_runs);
-        x0[e] = ld_op<CG>(gp, idx, gr[g].c64);
-        x1[e] = ld_op<CG>(gp, idx | (1ull << gr[g].vshift), gr[g].c64);
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        a0[e] = cmul(a0[e], x0[e]);
-        a1[e] = cmul(a1[e], x1[e]);
-      }
+      const uint64_t idx = gather(o, gr[g].runs, gr[g].n_runs);
+      a0 = cmul(a0, ld_op<CG>(gp, idx, gr[g].c64));
+      a1 = cmul(a1, ld_op<CG>(gp, idx | (1ull << gr[g].vshift), gr[g].c64));
     }
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      if (e > 0 && o + e * o_step >= o_end) continue;
-      const double2 r = make_double2(a0[e].x + a1[e].x, a0[e].y + a1[e].y);
-      if (h.out_c64)
-        reinterpret_cast<float2*>(out)[oo[e]] = make_float2((float)r.x, (float)r.y);
-      else
-        reinterpret_cast<double2*>(out)[oo[e]] = r;
-    }
+    const double2 r = make_double2(a0.x + a1.x, a0.y + a1.y);
+    if (h.out_c64)
+      reinterpret_cast<float2*>(out)[o] = make_float2((float)r.x, (float)r.y);
+    else
+      reinterpret_cast<double2*>(out)[o] = r;
   }
 }
 
-#ifndef QTN_SMALL_E
-#define QTN_SMALL_E 4
-#endif
 constexpr uint32_t kSmallChunk = 1024;
 __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ StreamLaunch L,
                                                     uint32_t tpi_log2) {
@@ -173,7 +135,7 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
   const uint64_t o0 = tpi == 256 ? (uint64_t)blockIdx.y * kSmallChunk : 0;
   if (o0 >= n_all) return;
   const uint64_t n_out = tpi == 256 ? min(n_all, o0 + kSmallChunk) : n_all;
-  small_eval<0, QTN_SMALL_E>(dsc, b, o0 + lane, n_out, tpi);
+  small_eval<0>(dsc, b, o0 + lane, n_out, tpi);
 }
 
 // ---- tiny subtrees (qtn_stream.h SubItem): one CTA per (subtree, set)
