@@ -586,7 +586,7 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
   // 0.575 -> 0.506 ms with them, config 3 default 2.209 -> 2.247 ms: its
   // small chains run slower with 4 groups per thread)
   const char* krv = getenv("QTN_XT_K_MIN_R");
-  if (K > 1 && R < (krv ? atoi(krv) : 20)) return false;
+  if (K > 1 && R < (krv ? atoi(krv) : 18)) return false;  // 18..21: config 4 0.508/0.511/0.520/0.520 ms
   std::memset(&d, 0, sizeof(d));
   auto ebit = [&](int32_t u) -> int {
     for (int i = 0; i < R; ++i)
@@ -750,8 +750,12 @@ bool encode_xt_desc(const YPairSpec& s, YDesc& d) {
   d.nW = (uint8_t)Ws.size();
   d.n_tiles = 1ull << (R - kXABits - (h - hs));
   if (getenv("QTN_DEBUG_DESC") && R >= atoi(getenv("QTN_DEBUG_DESC")))
-    fprintf(stderr, "ydesc R=%d K=%d h=%d hs=%d g=%d c=%d cw=%d nA=%d nB=%d nW=%d tiles=%llu\n", R, K, h, hs, g,
-            c, cw, (int)A.size(), (int)Bs.size(), (int)Ws.size(), (unsigned long long)d.n_tiles);
+  {
+    int afree = 0;
+    for (int b : rest) afree += !((adep >> b) & 1);
+    fprintf(stderr, "ydesc R=%d K=%d h=%d hs=%d g=%d c=%d cw=%d nA=%d nB=%d nW=%d tiles=%llu afree=%d nbits=%zu\n", R, K, h, hs, g,
+            c, cw, (int)A.size(), (int)Bs.size(), (int)Ws.size(), (unsigned long long)d.n_tiles, afree, nbits.size());
+  }
   return true;
 }
 
