@@ -511,6 +511,10 @@ def roofline(plan, A, kt, key):
         # fused chains skip the union-size products: the bytes the kernels move
         r["exec_bytes_per_launch"] = ex
         r["exec_frac"] = ex / kt / 1e9 / peak
+        r["note"] = ("achieved/frac count the reference's per-bucket bytes (SURVEY 8d); fused chains "
+                     "(fused_kernel, xt_kernel) never write or re-read the union-size intermediates, so "
+                     "frac may exceed 1: exec_frac counts the bytes the kernels move, dram_frac the "
+                     "ncu DRAM bytes of the same evaluation")
     if traffic:
         # DRAM bytes of the committed ncu capture of the same evaluation over
         # the live executor time: the fraction of HBM actually moving
