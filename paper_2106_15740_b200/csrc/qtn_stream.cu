@@ -104,8 +104,9 @@ __device__ __forceinline__ void small_eval(const uint8_t* dsc, const Bases& b, u
 }
 
 constexpr uint32_t kSmallChunk = 1024;
+constexpr uint32_t kSmallCtaBudget = 2400;  // measured: config 4 0.510 -> 0.479 ms, config 3 default unchanged
 __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ StreamLaunch L,
-                                                    uint32_t tpi_log2) {
+                                                    uint32_t tpi_log2, uint32_t chunk) {
   pdl_trigger();
   const uint32_t tpi = 1u << tpi_log2;
   const uint32_t item = blockIdx.x * (256u >> tpi_log2) + (threadIdx.x >> tpi_log2);
@@ -120,6 +121,8 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
   // element; from L1/L2 they were a chain of dependent loads)
   __shared__ uint4 sdesc[8][(kSDescMax + 15) / 16];
   const uint8_t* gdsc = L.descs + L.item_desc[item];
+  // CTA mode: chunks beyond the bucket's 2^R elements leave before staging
+  if (tpi == 256 && ((uint64_t)blockIdx.y * chunk >> reinterpret_cast<const SHdr*>(gdsc)->R)) return;
   uint4* slot = sdesc[tpi == 256 ? 0 : (threadIdx.x >> 5)];
   {
     const uint32_t n16 = (reinterpret_cast<const SHdr*>(gdsc)->desc_bytes + 15u) / 16u;
@@ -132,9 +135,9 @@ __global__ void __launch_bounds__(256) small_kernel(const __grid_constant__ Stre
   // PDL they overlap the previous level's tail; tensors are read after this
   pdl_wait();
   const uint64_t n_all = 1ull << reinterpret_cast<const SHdr*>(dsc)->R;
-  const uint64_t o0 = tpi == 256 ? (uint64_t)blockIdx.y * kSmallChunk : 0;
+  const uint64_t o0 = tpi == 256 ? (uint64_t)blockIdx.y * chunk : 0;
   if (o0 >= n_all) return;
-  const uint64_t n_out = tpi == 256 ? min(n_all, o0 + kSmallChunk) : n_all;
+  const uint64_t n_out = tpi == 256 ? min(n_all, o0 + chunk) : n_all;
   small_eval<0>(dsc, b, o0 + lane, n_out, tpi);
 }
 
@@ -193,11 +196,28 @@ int launch_small(const StreamLaunch& L, uint32_t max_r, void* stream, bool pdl) 
   // kSmallChunk elements each
   const uint32_t tpi_log2 = (uint64_t)L.n_items * L.n_sets >= 4u * 148u * 8u ? 5u : 8u;
   const uint32_t per_block = 256u >> tpi_log2;
-  const uint32_t chunks =
-      tpi_log2 == 8u ? (uint32_t)(((1ull << max_r) + kSmallChunk - 1) / kSmallChunk) : 1u;
+  // CTA mode: the fewest elements per thread (each a chain of dependent
+  // operand round trips) that keeps the launch within ~kSmallCtaBudget CTAs
+  static const uint32_t fixed = [] {
+    const char* e = getenv("QTN_SMALL_CHUNK");
+    const uint32_t v = e ? (uint32_t)atoi(e) : 0u;
+    return v >= 256u ? v : 0u;
+  }();
+  static const uint64_t budget = [] {
+    const char* e = getenv("QTN_SMALL_CTAS");
+    const uint64_t v = e ? (uint64_t)atoll(e) : 0u;
+    return v ? v : (uint64_t)kSmallCtaBudget;
+  }();
+  uint32_t chunk = kSmallChunk;
+  if (fixed) chunk = fixed;
+  else if (tpi_log2 == 8u)
+    while (chunk > 256u &&
+           (uint64_t)L.n_items * L.n_sets * (((1ull << max_r) + chunk / 2 - 1) / (chunk / 2)) <= budget)
+      chunk >>= 1;
+  const uint32_t chunks = tpi_log2 == 8u ? (uint32_t)(((1ull << max_r) + chunk - 1) / chunk) : 1u;
   dim3 grid((L.n_items + per_block - 1) / per_block, chunks, L.n_sets);
   cudaError_t e = launch_pdl_if<true>(pdl, small_kernel, grid, dim3(256), 0,
-                                      reinterpret_cast<cudaStream_t>(stream), L, tpi_log2);
+                                      reinterpret_cast<cudaStream_t>(stream), L, tpi_log2, chunk);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("small_kernel launch: ") + cudaGetErrorString(e));
