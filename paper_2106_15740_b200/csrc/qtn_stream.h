@@ -256,8 +256,8 @@ constexpr int kYOps = kYMaxA + 2 * kYMaxG;
 constexpr int kYMaxH = 6;        // loop bits per tile
 constexpr int kYMaxGB = 2;       // group bits (2^g summed positions per thread)
 constexpr int kYMaxK = 3;        // trailing traces
-constexpr int kYStageB = 4096;   // staged B entries (v2, x_b, x_c, v1)
-constexpr int kYStageW = 2048;   // staged W entries (x_b, x_w, v2)
+constexpr int kYStageB = 8192;   // staged B entries (v2, x_b, x_c, v1)
+constexpr int kYStageW = 4096;   // staged W entries (x_b, x_w, v2)
 struct YOp {
   uint64_t ptr;                  // tagged
   uint8_t vs1, vs2, c64, n_runs; // bit of v1 / v2 in the operand index (0xff: none)
