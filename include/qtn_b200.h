@@ -84,8 +84,10 @@ typedef struct {
   double exec_bytes;         /* bytes the executor's kernels move (fused chains:  */
                              /* operands + final output only)                   */
   int32_t n_pairs;           /* HBM executor: expanding bucket + consumer pairs  */
-  int32_t reserved;          /* run as one kernel (their union-size result is    */
+                             /* run as one kernel (their union-size result is    */
                              /* never stored)                                    */
+  int32_t n_tails;           /* HBM executor: tail chains run as one weighted    */
+                             /* sum over their first operand (qtn_wsum.cu)       */
 } qtn_plan_info_t;
 
 /* ---------------------------------------------------------------- ordering */

@@ -50,7 +50,7 @@ class PlanInfo(C.Structure):
         ("n_fused_chains", C.c_int32),
         ("exec_bytes", C.c_double),
         ("n_pairs", C.c_int32),
-        ("reserved", C.c_int32),
+        ("n_tails", C.c_int32),
     ]
 
 

@@ -118,6 +118,7 @@ class ContractionPlan:
         self.n_fused_chains = int(info.n_fused_chains)
         self.exec_bytes = float(info.exec_bytes)
         self.n_pairs = int(info.n_pairs)
+        self.n_tails = int(info.n_tails)
         sr = np.zeros(max(len(sequence), 1), dtype=np.int32)
         N.check(N.lib.qtn_plan_step_ranks(h, N.i32(sr)))
         self.step_ranks = tuple(int(x) for x in sr[: len(sequence)])

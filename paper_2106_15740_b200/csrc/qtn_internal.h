@@ -229,6 +229,8 @@ struct qtn_plan {
   std::vector<qtn::XDesc> hbm_xdesc;
   std::vector<qtn::YDesc> hbm_ydesc;     // expanding bucket + consumer pairs (qtn_xt.cu)
   std::vector<int32_t> hbm_ylevel;       // their levels
+  std::vector<qtn::WsDesc> hbm_wsdesc;   // weighted full sums: the tail chains (qtn_wsum.cu)
+  std::vector<int32_t> hbm_wslevel;      // their levels
   std::vector<int32_t> hbm_r1idx;        // single-operand (trace) record per bucket, or -1
   std::vector<qtn::R1Dev> hbm_r1;        // net = 0 here; set per batch
   struct SubRec {                        // tiny subtree (qtn_stream.h SubItem)

@@ -656,6 +656,13 @@ struct qtn_batch {
   std::vector<uint32_t> level_yitem0;
   std::vector<uint64_t> level_yprefix0, level_ytiles;
   std::vector<uint32_t> level_ystage;
+  // weighted full sums: the tail chains (wsum_kernel)
+  qtn::WsDesc* d_wsdesc = nullptr;
+  uint32_t* d_wsitem_desc = nullptr;
+  uint32_t* d_wsitem_net = nullptr;
+  uint32_t* d_wsprefix = nullptr;
+  std::vector<uint32_t> level_ws0;      // first tail item of each level (+ end)
+  std::vector<uint32_t> level_wsprefix0, level_wsctas;
   // fused product chains per level (fused_kernel)
   qtn::FDesc* d_fdesc = nullptr;
   uint32_t* d_ftab = nullptr;
@@ -757,7 +764,8 @@ extern "C" int qtn_batch_destroy(qtn_batch* B) {
                   (void*)B->d_fdesc, (void*)B->d_fitem_desc, (void*)B->d_fitem_net,
                   (void*)B->d_fprefix, (void*)B->d_cprefix, (void*)B->d_ftab,
                   (void*)B->d_fctas, (void*)B->d_fblob,
-                  (void*)B->d_sub_items, (void*)B->d_sub_desc})
+                  (void*)B->d_sub_items, (void*)B->d_sub_desc, (void*)B->d_wsdesc,
+                  (void*)B->d_wsitem_desc, (void*)B->d_wsitem_net, (void*)B->d_wsprefix})
     device_free(p);
   qtn::setmajor_destroy(B->sm);
   delete B;
@@ -902,6 +910,28 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     B->level_ystage.push_back(ystage);
   }
   B->level_yitem0.push_back((uint32_t)yitem_desc.size());
+  // tail chains (weighted full sums), level-major over all HBM networks
+  std::vector<qtn::WsDesc> wsdescs;
+  std::vector<uint32_t> wsitem_desc, wsitem_net, wsprefix;
+  for (int32_t lev = 0; lev < max_lev; ++lev) {
+    B->level_ws0.push_back((uint32_t)wsitem_desc.size());
+    B->level_wsprefix0.push_back((uint32_t)wsprefix.size());
+    uint32_t acc = 0;
+    wsprefix.push_back(0);
+    for (int h = 0; h < B->n_hbm; ++h) {
+      const qtn_plan* P = plans[hidx[h]];
+      for (size_t w = 0; w < P->hbm_wsdesc.size(); ++w) {
+        if (P->hbm_wslevel[w] + hshift[h] != lev) continue;
+        wsitem_desc.push_back((uint32_t)wsdescs.size());
+        wsitem_net.push_back((uint32_t)h);
+        wsdescs.push_back(P->hbm_wsdesc[w]);
+        acc += P->hbm_wsdesc[w].n_ctas;
+        wsprefix.push_back(acc);
+      }
+    }
+    B->level_wsctas.push_back(acc);
+  }
+  B->level_ws0.push_back((uint32_t)wsitem_desc.size());
   // host-built lookup tables of every fused descriptor (16-byte aligned each),
   // and the per-descriptor blob [header, sides, used ops | tables] the
   // fused kernel copies in one pass
@@ -1207,7 +1237,7 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
     B->chain_len.assign(nl, 0);
     auto tiny_only = [&](size_t l) {
       return B->level_tiny[l] && !B->level_tiles[l] && !B->level_xtiles[l] && !y_launches(B, l) && !B->level_r1chunks[l] &&
-             !B->level_fctas[l] && B->level_sub0[l + 1] == B->level_sub0[l] &&
+             !B->level_wsctas[l] && !B->level_fctas[l] && B->level_sub0[l + 1] == B->level_sub0[l] &&
              B->level_red0[l + 1] == B->level_red0[l] && B->level_sitem0[l + 1] > B->level_sitem0[l];
     };
     for (size_t l = 0; chain_on && l < nl;) {
@@ -1244,6 +1274,8 @@ extern "C" int qtn_batch_create(qtn_plan* const* plans, int32_t n, qtn_batch** o
       (rc = upload(&B->d_xitem_net, xitem_net)) || (rc = upload(&B->d_xprefix, xprefix)) ||
       (rc = upload(&B->d_ydesc, ydescs)) || (rc = upload(&B->d_yitem_desc, yitem_desc)) ||
       (rc = upload(&B->d_yitem_net, yitem_net)) || (rc = upload(&B->d_yprefix, yprefix)) ||
+      (rc = upload(&B->d_wsdesc, wsdescs)) || (rc = upload(&B->d_wsitem_desc, wsitem_desc)) ||
+      (rc = upload(&B->d_wsitem_net, wsitem_net)) || (rc = upload(&B->d_wsprefix, wsprefix)) ||
       (rc = upload(&B->d_level_sitem0, B->level_sitem0)) ||
       (rc = upload(&B->d_r1, r1items)) || (rc = upload(&B->d_r1prefix, r1prefix)) ||
       (rc = upload(&B->d_r1chunk_item, r1chunk_item)) ||
@@ -1308,7 +1340,8 @@ extern "C" int qtn_batch_launches(const qtn_batch* B, int32_t n_sets, int32_t* o
       }
       c += (B->level_tiles[lev] ? 1 : 0) + (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
-           y_launches(B, lev) + (B->level_r1chunks[lev] ? 1 : 0) + (B->level_sub0[lev + 1] > B->level_sub0[lev] ? 1 : 0);
+           y_launches(B, lev) + (B->level_r1chunks[lev] ? 1 : 0) + (B->level_sub0[lev + 1] > B->level_sub0[lev] ? 1 : 0) +
+           (B->level_wsctas[lev] ? 2 : 0);
       for (uint32_t gi = B->level_fgroup0[lev]; gi < B->level_fgroup0[lev + 1]; ++gi)
         c += 1 + (B->fgroups[gi].cctas ? 1 : 0);
     }
@@ -1699,7 +1732,7 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
                            (B->level_red0[lev + 1] > B->level_red0[lev] ? 1 : 0) +
                            (B->level_sitem0[lev + 1] > B->level_sitem0[lev] ? 1 : 0) +
                            (B->level_r1chunks[lev] ? 1 : 0) + (B->level_xtiles[lev] ? 1 : 0) +
-                           y_launches(B, lev) + (B->level_tiles[lev] ? 1 : 0);
+                           y_launches(B, lev) + (B->level_tiles[lev] ? 1 : 0) + (B->level_wsctas[lev] ? 1 : 0);
       const bool fork = level_streams && n_launch >= 2 && !B->chain_len[lev];
       // one launch after one launch: PDL for it (QTN_PDL_SINGLE=1; tiny
       // small_kernel levels take it by default below)
@@ -1868,6 +1901,25 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         }
         return QTN_OK;
       };
+      auto l_ws = [&]() -> int {
+        if (!B->level_wsctas[lev]) return QTN_OK;
+        qtn::WsLaunch W;
+        std::memset(&W, 0, sizeof(W));
+        W.descs = B->d_wsdesc;
+        W.item_desc = B->d_wsitem_desc + B->level_ws0[lev];
+        W.item_net = B->d_wsitem_net + B->level_ws0[lev];
+        W.cta_prefix = B->d_wsprefix + B->level_wsprefix0[lev];
+        W.n_items = B->level_ws0[lev + 1] - B->level_ws0[lev];
+        W.n_sets = (uint32_t)n_sets;
+        W.total_ctas = B->level_wsctas[lev];
+        W.in_base = L.in_base;
+        W.in_set_stride = L.in_set_stride;
+        W.net_in_off = L.net_in_off;
+        W.ws_base = L.ws_base;
+        W.ws_set_stride = L.ws_set_stride;
+        W.net_ws_off = L.net_ws_off;
+        return qtn::launch_wsum(W, next_stream());
+      };
       auto l_stream = [&]() -> int {
         if (!B->level_tiles[lev]) return QTN_OK;
         StreamLaunch Lt = L;
@@ -1889,12 +1941,12 @@ static int run_batch(qtn_batch* B, const void* inputs, int64_t set_stride, const
         lorder = ov ? atoi(ov) : 1;
       }
       if (lorder == 1) {
-        if ((rc = l_stream()) || (rc = l_xt()) || (rc = l_expand()) || (rc = l_fused()) || (rc = l_trace()) || (rc = l_red()) ||
+        if ((rc = l_stream()) || (rc = l_xt()) || (rc = l_ws()) || (rc = l_expand()) || (rc = l_fused()) || (rc = l_trace()) || (rc = l_red()) ||
             (rc = l_small()) || (rc = l_sub()))
           return rc;
       } else {
         if ((rc = l_sub()) || (rc = l_fused()) || (rc = l_red()) || (rc = l_small()) || (rc = l_trace()) ||
-            (rc = l_expand()) || (rc = l_xt()) || (rc = l_stream()))
+            (rc = l_expand()) || (rc = l_xt()) || (rc = l_ws()) || (rc = l_stream()))
           return rc;
       }
       // join: the next level (or the fold) waits for every branch

@@ -1606,6 +1606,100 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         chain_len[bi] = 1 + (int)mem.size();
       }
     }
+    // Tail chains (qtn_wsum.cu): from a complex64 intermediate T of rank >=
+    // QTN_WSUM_MIN_R (12) on, every bucket down to the scalar has the previous
+    // result as its only intermediate operand and rank-1/2 gates on T's
+    // variables otherwise: one weighted sum over T (head = the first bucket,
+    // the others absorbed, no intermediate stored).  QTN_WSUM=0 disables.
+    std::vector<char> is_ws(nb, 0);
+    // main operand of a tail bucket: its latest-produced intermediate operand
+    // (the previous result of the chain); every other operand a rank-1/2
+    // tensor (a gate, or a small product of gates) on the main operand's
+    // variables; -1 otherwise
+    auto ws_main = [&](int32_t bi) -> int32_t {
+      const auto& b = P->buckets[bi];
+      int32_t m = -1;
+      for (int32_t id : b.ops)
+        if (!P->tensors[id].input && (m < 0 || P->tensors[id].born > P->tensors[m].born)) m = id;
+      if (m < 0) return -1;
+      const auto& mv = P->tensors[m].vars;
+      if (b.rank != (int)mv.size() - 1) return -1;
+      for (int32_t id : b.ops) {
+        if (id == m) continue;
+        const auto& t = P->tensors[id];
+        if (t.rank() < 1 || t.rank() > 2) return -1;
+        for (int32_t u : t.vars)
+          if (std::find(mv.begin(), mv.end(), u) == mv.end()) return -1;
+      }
+      return m;
+    };
+    {
+      const char* wv = getenv("QTN_WSUM");
+      const bool ws_on = !(wv && wv[0] == '0');
+      const char* wr = getenv("QTN_WSUM_MIN_R");
+      const int ws_min_r = std::max(kWsL + 1, wr ? atoi(wr) : 12);
+      for (int bi = 0; ws_on && bi < nb; ++bi) {
+        // a tail ends at a bucket whose result is a scalar
+        if (P->buckets[bi].rank != 0 || chain_head[bi] >= 0) continue;
+        std::vector<int32_t> mem;  // from the scalar's bucket backwards
+        int32_t head_main = -1;
+        size_t n_gates = 0;
+        for (int32_t c = bi; c >= 0 && chain_head[c] < 0;) {
+          const int32_t m = ws_main(c);
+          if (getenv("QTN_DEBUG_WS")) {
+            fprintf(stderr, "  bucket %d rank %d main %d ops:", c, P->buckets[c].rank, m);
+            for (int32_t id : P->buckets[c].ops)
+              fprintf(stderr, " %d(r%d%s b%d lu%d)", id, P->tensors[id].rank(), P->tensors[id].input ? "i" : "", P->tensors[id].born, P->tensors[id].last_use);
+            fprintf(stderr, "\n");
+          }
+          if (m < 0) break;
+          n_gates += P->buckets[c].ops.size() - 1;
+          if (n_gates > (size_t)kWsMaxGates) break;
+          mem.push_back(c);
+          head_main = m;
+          if (P->tensors[m].born < 0 || P->tensors[m].last_use != c) break;
+          c = P->tensors[m].born;
+        }
+        // the head's main operand must be a complex64 intermediate of rank >= min_r:
+        // drop members from the head side until it is
+        while (!mem.empty()) {
+          const auto& t = P->tensors[head_main];
+          if (t.c64 && t.rank() >= ws_min_r) break;
+          mem.pop_back();
+          if (!mem.empty()) head_main = ws_main(mem.back());
+        }
+        if (getenv("QTN_DEBUG_WS"))
+          fprintf(stderr, "ws tail: end bucket %d, members %zu, head main rank %d c64 %d gates %zu\n", bi, mem.size(),
+                  head_main >= 0 ? P->tensors[head_main].rank() : -1,
+                  head_main >= 0 ? (int)P->tensors[head_main].c64 : -1, n_gates);
+        if (mem.size() < 3) continue;
+        std::reverse(mem.begin(), mem.end());  // head first
+        // geometry check (tags do not change it)
+        WsSpec wsp;
+        wsp.src_vars = P->tensors[head_main].vars;
+        wsp.src_tag = wsp.out_tag = 0;
+        wsp.out_c64 = P->tensors[P->buckets[mem.back()].out].c64;
+        for (int32_t c : mem) {
+          const int32_t cm = ws_main(c);
+          for (int32_t id : P->buckets[c].ops)
+            if (id != cm) {
+              wsp.gate_vars.push_back(P->tensors[id].vars);
+              wsp.gate_tag.push_back(0);
+              wsp.gate_c64.push_back(P->tensors[id].c64 ? 1 : 0);
+            }
+        }
+        WsDesc probe;
+        if (!encode_wsum_desc(wsp, probe)) continue;
+        if (getenv("QTN_DEBUG_WS"))
+          fprintf(stderr, "ws desc: R %d lo %d hi %d st %d ctas %u\n", probe.R, probe.n_lo, probe.n_hi, probe.n_st, probe.n_ctas);
+        const int32_t hb = mem.front();
+        is_ws[hb] = 1;
+        for (int32_t c : mem) chain_head[c] = hb;
+        chain_tail[hb] = mem.back();
+        chain_len[hb] = (int)mem.size();
+        fpart_bytes[hb] = 16ull * probe.n_ctas;
+      }
+    }
     // Product chains (qtn_fused.cu): a bucket of >= 2 operands whose result
     // is then reduced by single-operand buckets is one fused contraction; the
     // union-size product and the chain's intermediates are never written
@@ -1682,7 +1776,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
         const int32_t pb = src.input ? -1 : src.born;
         // extend the producer's chain (at most kRedMax eliminated variables)
         const bool extend = pb >= 0 && chain_head[pb] >= 0 && !is_fchain[chain_head[pb]] &&
-                            !is_xt[chain_head[pb]] &&
+                            !is_xt[chain_head[pb]] && !is_ws[chain_head[pb]] &&
                             chain_len[chain_head[pb]] < kRedMax;
         chain_head[bi] = extend ? chain_head[pb] : bi;
         chain_len[chain_head[bi]] += 1;
@@ -1700,7 +1794,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       const char* mkv = getenv("QTN_FUSE_MAX_K");
       const int fuse_max_k = mkv ? atoi(mkv) : 4;
       for (int bi = 0; bi < nb; ++bi) {
-        if (chain_head[bi] != bi || is_fchain[bi] || is_xt[bi]) continue;
+        if (chain_head[bi] != bi || is_fchain[bi] || is_xt[bi] || is_ws[bi]) continue;
         const auto& src = P->tensors[P->buckets[bi].ops[0]];
         int lowest = 64;
         for (int32_t c = bi;; c = P->tensors[P->buckets[c].out].last_use) {
@@ -1815,7 +1909,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       }
       int32_t lv = 0;
       for (int32_t id : P->buckets[bi].ops) lv = std::max(lv, tlevel[id]);
-      if (is_xt[bi])  // the chain also waits for its consumers' other operands
+      if (is_xt[bi] || is_ws[bi])  // the chain also waits for its consumers' other operands
         for (int32_t c = P->tensors[P->buckets[bi].out].last_use;; c = P->tensors[P->buckets[c].out].last_use) {
           for (int32_t id : P->buckets[c].ops)
             if (P->tensors[id].input || chain_head[P->tensors[id].born] != bi) lv = std::max(lv, tlevel[id]);
@@ -1893,6 +1987,34 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
           }
           P->hbm_ydesc.push_back(yd);
           P->hbm_ylevel.push_back(P->hbm_level[bi]);
+          continue;
+        }
+        if (is_ws[bi]) {
+          WsSpec wsp;
+          const int32_t main_id = ws_main(bi);
+          wsp.src_vars = P->tensors[main_id].vars;
+          wsp.src_tag = tag_of(main_id);
+          wsp.out_tag = tag_of(P->buckets[chain_tail[bi]].out);
+          wsp.out_c64 = P->tensors[P->buckets[chain_tail[bi]].out].c64;
+          for (int32_t c = bi;; c = P->tensors[P->buckets[c].out].last_use) {
+            const int32_t cm = ws_main(c);
+            for (int32_t id : P->buckets[c].ops)
+              if (id != cm) {
+                wsp.gate_vars.push_back(P->tensors[id].vars);
+                wsp.gate_tag.push_back(tag_of(id));
+                wsp.gate_c64.push_back(P->tensors[id].c64 ? 1 : 0);
+              }
+            if (c == chain_tail[bi]) break;
+          }
+          WsDesc wd;
+          if (!encode_wsum_desc(wsp, wd) || !fpart_off.count(bi)) {
+            delete P;
+            set_error("tail chain: descriptor no longer encodable");
+            return QTN_EINVAL;
+          }
+          wd.part = tag_ws((uint64_t)fpart_off[bi]);
+          P->hbm_wsdesc.push_back(wd);
+          P->hbm_wslevel.push_back(P->hbm_level[bi]);
           continue;
         }
         if (is_fchain[bi]) {
@@ -2103,7 +2225,7 @@ extern "C" int qtn_plan_create(const qtn_network_desc* net, const int32_t* order
       for (int32_t id : b.ops)
         if (sm_off[id] < 0)  // subtree-internal operands never leave the SM
           eb += std::ldexp((double)elem_bytes(P->tensors[id].c64), P->tensors[id].rank());
-      if (h >= 0 && is_xt[bi])
+      if (h >= 0 && (is_xt[bi] || is_ws[bi]))
         for (int32_t c = P->tensors[b.out].last_use;; c = P->tensors[P->buckets[c].out].last_use) {
           for (int32_t id : P->buckets[c].ops)
             if (P->tensors[id].input || chain_head[P->tensors[id].born] != bi)
@@ -2152,7 +2274,7 @@ extern "C" int qtn_plan_info(const qtn_plan* P, qtn_plan_info_t* info) {
   info->n_fused_chains = (int32_t)P->hbm_fdesc.size();
   info->exec_bytes = P->exec_bytes < 0.0 ? P->alg_bytes : P->exec_bytes;
   info->n_pairs = (int32_t)P->hbm_ydesc.size();
-  info->reserved = 0;
+  info->n_tails = (int32_t)P->hbm_wsdesc.size();
   return QTN_OK;
 }
 

@@ -565,6 +565,66 @@ struct SubItem {
 int launch_subtree(const StreamLaunch& L, const SubItem* items, uint32_t n_items,
                    const uint64_t* sub_desc, uint32_t smem_bytes, void* stream);
 
+// ---- weighted full sums (qtn_wsum.cu): the tail of an elimination order is
+// a linear chain of buckets that each eliminate one more variable of the
+// previous result T with rank-1/2 gates as the only other operands, down to
+// the scalar (contraction.py:90-96 repeated R times).  The chain is one sum
+//   Z = sum_x T[x] * prod_k g_k(x[vars_k])
+// over T's 2^R entries: T is read once, no intermediate of the chain exists.
+// Tile = the low kWsL bits of x: gates on tile bits only form a lookup table
+// (built per CTA), gates on high bits a per-tile factor, gates across both
+// are multiplied per element.
+constexpr int kWsL = 11;          // tile bits (a warp sums one tile)
+constexpr int kWsMaxGates = 64;
+constexpr int kWsMaxSt = 4;       // gates across the tile boundary
+constexpr int kWsMaxCtas = 296;   // CTAs (partial sums) per item
+struct WsGate {
+  uint64_t ptr;                   // tagged (inputs: complex128 entries)
+  uint8_t rank;                   // 1 or 2
+  uint8_t b0, b1;                 // T index bits of the gate's variables (entry index = x[b0] << 1 | x[b1]; rank 1: x[b0])
+  uint8_t c64;
+  uint32_t pad;
+};
+struct WsDesc {
+  uint64_t src, part, out;        // tagged: T (complex64), the CTA partial sums (complex128), the scalar
+  uint64_t n_tiles;               // 2^(R - kWsL)
+  uint32_t n_ctas;
+  uint8_t R, out_c64, n_lo, n_hi, n_st, pad[3];
+  uint8_t lo_first[kWsL + 1];     // lo gates sorted by highest bit: those with highest bit b are [lo_first[b], lo_first[b+1])
+  uint8_t pad2[16 - (kWsL + 1) % 16];
+  WsGate g[kWsMaxGates];          // lo gates, then hi gates, then the gates across
+};
+static_assert(sizeof(WsGate) == 16, "WsGate");
+static_assert(sizeof(WsDesc) % 16 == 0, "WsDesc");
+struct WsSpec {
+  std::vector<int32_t> src_vars;                  // T's layout, MSB first
+  uint64_t src_tag, out_tag;
+  bool out_c64;
+  std::vector<std::vector<int32_t>> gate_vars;    // rank-1/2 gates, in bucket order
+  std::vector<uint64_t> gate_tag;
+  std::vector<uint8_t> gate_c64;
+};
+// Host encoder: false when the chain does not fit (gate counts).  part is set by the caller.
+bool encode_wsum_desc(const WsSpec& s, WsDesc& d);
+struct WsLaunch {
+  const WsDesc* descs;           // device
+  const uint32_t* item_desc;     // device: descriptor index per item
+  const uint32_t* item_net;      // device: network index per item
+  const uint32_t* cta_prefix;    // device: n_items + 1
+  uint32_t n_items;
+  uint32_t n_sets;
+  uint32_t total_ctas;
+  uint32_t pad;
+  const char* in_base;
+  int64_t in_set_stride;
+  const int64_t* net_in_off;
+  char* ws_base;
+  int64_t ws_set_stride;
+  const int64_t* net_ws_off;
+};
+// stage 1 (partial sums per CTA) and stage 2 (their sum -> the scalar) on one stream
+int launch_wsum(const WsLaunch& L, void* stream);
+
 // single descriptor with absolute pointers, descriptor passed by value
 int launch_stream_single(const std::vector<uint8_t>& desc, void* stream);
 

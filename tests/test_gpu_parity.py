@@ -841,3 +841,53 @@ def test_tiny_subtrees(golden, monkeypatch, sub_r):
             assert abs(out["1", dt][0][e] - w) <= tol * abs(w) + 1e-12, (dt, e)
             assert abs(out["1", dt][0][e] - out["0", dt][0][e]) <= tol * abs(w) + 1e-12
         assert abs(out["1", dt][1] - rec4) <= tol * abs(rec4)
+
+
+def test_tail_chains(golden, monkeypatch):
+    """Tail chains (wsum_kernel, DESIGN 3.9): the linear chain from the last
+    wide intermediate to the scalar (contraction.py:90-96 once per remaining
+    variable) as one weighted full sum.  Equal to the bucket-by-bucket
+    evaluation (QTN_WSUM=0) and to the reference values at 1e-5 on config 4
+    edges #16 / #1058 (unsliced and in 2^3 slices) and on config 3 default
+    networks, for several angle sets; repeated evaluations are bitwise equal
+    (fixed summation order)."""
+    G = golden("config3.json")
+    graph = Q.random_regular_graph(G["n"], 3, 0)
+    params = Q.QaoaParams(G["gammas"], G["betas"])
+    recs = G["modes"]["default"][:12]
+    G4 = golden("config4.json")
+    rec4 = {r["edge_index"]: complex(*r["value"]) for r in G4["modes"]["zz+diagonal"]
+            if r["edge_index"] in (16, 1058)}
+    g4 = Q.random_regular_graph(G4["n"], 3, 0)
+    p4v = Q.QaoaParams(G4["gammas"], G4["betas"])
+    rng = np.random.default_rng(7)
+    sets3 = np.vstack([params.as_vector(), rng.uniform(0, math.pi, (2, 2 * G["p"]))])
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QTN_WSUM", flag)
+        plan = Q.EnergyPlan(graph, G["p"], "default", dtype="complex64",
+                            edge_ids=[r["edge_index"] for r in recs])
+        p4 = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype="complex64", edge_ids=sorted(rec4))
+        p4s = Q.EnergyPlan(g4, G4["p"], "zz+diagonal", dtype="complex64", edge_ids=[1058], slice_k=3)
+        nt = sum(j.plan.n_tails for j in plan.jobs), sum(j.plan.n_tails for j in p4.jobs), \
+            sum(j.plan.n_tails for j in p4s.jobs)
+        assert (nt[0] > 0 and nt[1] >= 1 and nt[2] >= 1) if flag == "1" else nt == (0, 0, 0)
+        out[flag] = (plan.zz_values(params), p4.zz_values(p4v), plan.energies(sets3), p4s.zz_values(p4v))
+        assert plan.launches == plan.launches_per_eval(1)
+        again = p4.zz_values(p4v)
+        assert all(again[e] == out[flag][1][e] for e in rec4)
+    tol = 1e-5
+    for r in recs:
+        w = complex(*r["value"])
+        e = r["edge_index"]
+        assert abs(out["1"][0][e] - w) <= tol * abs(w) + 1e-12, e
+        assert abs(out["1"][0][e] - out["0"][0][e]) <= tol * abs(w) + 1e-12
+    for e, w in rec4.items():
+        assert abs(out["1"][1][e] - w) <= tol * abs(w), e
+        assert abs(out["1"][1][e] - out["0"][1][e]) <= tol * abs(w), e
+    w = rec4[1058]
+    assert abs(out["1"][3][1058] - w) <= tol * abs(w)
+    assert np.allclose(out["1"][2], out["0"][2], rtol=tol, atol=tol)
+
+
+

@@ -15,18 +15,22 @@ def test_fused_chain_census_and_levels(golden):
     G4 = golden("config4.json")
     g4 = Q.random_regular_graph(G4["n"], 3, 0)
     os.environ["QTN_FCHAIN_MAX_OUT"] = "64"  # every chain, wide streaming ones too
+    os.environ["QTN_WSUM"] = "0"             # (the tail chain would take the last product chains)
     try:
         j = Q.plan_edges(g4, G4["p"], "zz+diagonal", [1058], dtype="complex64")[0]
     finally:
         del os.environ["QTN_FCHAIN_MAX_OUT"]
+        del os.environ["QTN_WSUM"]
     assert j.plan.n_fused_chains >= 5
     assert j.plan.exec_bytes < 0.8 * j.plan.alg_bytes
     assert max(j.plan.step_ranks) == j.report.width
     os.environ["QTN_FUSE_CHAIN"] = "0"
+    os.environ["QTN_WSUM"] = "0"
     try:
         k = Q.plan_edges(g4, G4["p"], "zz+diagonal", [1058], dtype="complex64")[0]
     finally:
         del os.environ["QTN_FUSE_CHAIN"]
+        del os.environ["QTN_WSUM"]
     assert k.plan.n_fused_chains == 0
     assert k.plan.n_levels > j.plan.n_levels
     assert k.plan.alg_bytes == j.plan.alg_bytes
@@ -74,3 +78,31 @@ def test_expand_consumer_pairs_config4(golden):
     assert k.plan.step_ranks == j.plan.step_ranks
     d = Q.plan_edges(g4, G4["p"], "zz+diagonal", [16], dtype="complex128")[0]
     assert d.plan.n_pairs == 0
+
+
+def test_tail_chain_config4(golden):
+    """Config 4 edge #1058: after the last wide chain the elimination order is
+    a linear chain from a rank-22 intermediate to the scalar (22 buckets whose
+    other operands are rank-1/2 gates): one weighted full sum (wsum_kernel),
+    so the tail's levels and intermediates disappear; QTN_WSUM=0 keeps them;
+    complex128 plans have no tail chain (their intermediates are complex128);
+    step ranks and algorithmic bytes are the reference's either way."""
+    import os
+
+    G4 = golden("config4.json")
+    g4 = Q.random_regular_graph(G4["n"], 3, 0)
+    j = Q.plan_edges(g4, G4["p"], "zz+diagonal", [1058], dtype="complex64")[0]
+    assert j.plan.n_tails == 1
+    assert max(j.plan.step_ranks) == j.report.width
+    os.environ["QTN_WSUM"] = "0"
+    try:
+        k = Q.plan_edges(g4, G4["p"], "zz+diagonal", [1058], dtype="complex64")[0]
+    finally:
+        del os.environ["QTN_WSUM"]
+    assert k.plan.n_tails == 0
+    assert k.plan.n_levels >= j.plan.n_levels + 10
+    assert k.plan.exec_bytes > j.plan.exec_bytes
+    assert k.plan.alg_bytes == j.plan.alg_bytes
+    assert k.plan.step_ranks == j.plan.step_ranks
+    d = Q.plan_edges(g4, G4["p"], "zz+diagonal", [16], dtype="complex128")[0]
+    assert d.plan.n_tails == 0
