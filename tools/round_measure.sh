@@ -25,10 +25,14 @@ python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 --csv --log-file gpurun_out/r/launches_config4.csv python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu4.log 2>&1; echo "ncu4 rc=$?"
 # the largest chain of config 4 ([1,22,21] -> 26, its consumer [2,16,26] -> 25 and three traces -> 22: the 6th xt launch)
 ncu --set full --clock-control none --import-source on -k regex:xt_kernel -s 5 -c 1 -o gpurun_out/r/prof_xt_c4 python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu5.log 2>&1; echo "ncu5 rc=$?"
+# the tail chain of config 4 (rank-22 intermediate -> scalar as one weighted sum)
+ncu --set full --clock-control none --import-source on -k regex:wsum_kernel -s 3 -c 1 -f -o gpurun_out/r/prof_wsum_c4 python bench.py --steps 2 --warmup 3 --workload config4 --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu5b.log 2>&1; echo "ncu5b rc=$?"
 python tools/micro/write_bw.py > gpurun_out/r/write_bw.txt 2>&1; echo "wbw rc=$?"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 320 --csv --log-file gpurun_out/r/launches_config3d.csv python bench.py --steps 1 --warmup 3 --workload config3-default --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu6.log 2>&1; echo "ncu6 rc=$?"
 for w in config4 config3-default; do timeout 300 python tools/timeline.py $w --out gpurun_out/r/timeline_$w.json > gpurun_out/r/timeline_$w.txt 2>&1; done
 QTN_XT=0 timeout 300 python bench.py --workload config3-default --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config3d_noxt.json 2>&1; echo "c3d noxt rc=$?"
 QTN_XT=0 timeout 300 python bench.py --workload config4 --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config4_noxt.json 2>&1; echo "c4 noxt rc=$?"
+QTN_WSUM=0 timeout 300 python bench.py --workload config4 --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config4_nowsum.json 2>&1; echo "c4 nowsum rc=$?"
+QTN_WSUM=0 timeout 300 python bench.py --workload config3-default --angle-sets 1 --steps 10 --warmup 3 --no-records --no-cpu-baseline > gpurun_out/r/bench_config3d_nowsum.json 2>&1; echo "c3d nowsum rc=$?"
 python bench.py --steps 1 --warmup 3 --workload config3-default --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/plain_c3d_f.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:fused_kernel -s 20 -c 1 -o gpurun_out/r/prof_fused_c3d python bench.py --steps 1 --warmup 3 --workload config3-default --angle-sets 1 --no-cpu-baseline --no-records > gpurun_out/r/ncu7.log 2>&1; echo "ncu7 rc=$?"

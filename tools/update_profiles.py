@@ -74,7 +74,8 @@ def main():
     smem = summary(os.path.join(R, "prof_smem.ncu-rep"))
     c5 = summary(os.path.join(R, "prof_stream_c5.ncu-rep"))
     s4 = agg.get("stream_kernel", {"launches": 0, "time_s": 0.0, "dram_bytes": 0.0})
-    for src, dst in [("bench_config3d_noxt", "config3d_noxt"), ("bench_config4_noxt", "config4_noxt")]:
+    for src, dst in [("bench_config3d_noxt", "config3d_noxt"), ("bench_config4_noxt", "config4_noxt"),
+                     ("bench_config3d_nowsum", "config3d_nowsum"), ("bench_config4_nowsum", "config4_nowsum")]:
         line = last_json(os.path.join(R, src + ".json")) if os.path.exists(os.path.join(R, src + ".json")) else None
         if line:
             open(os.path.join(P, f"bench_{TAG}_{dst}.json"), "w").write(line)
@@ -121,6 +122,10 @@ def main():
             "time_sum_s": sum(v["time_s"] for v in agg3.values()),
             "dram_bytes_per_launch": sum(v["dram_bytes"] for v in agg3.values()),
             "by_kernel": agg3, "source": f"launches_{TAG}_config3d.json"}
+    w4 = os.path.join(R, "prof_wsum_c4.ncu-rep")
+    if os.path.exists(w4):
+        out["kernels"]["wsum_kernel@config4"] = dict(summary(w4), workload="config4 edge #1058: the tail chain (rank-22 "
+                                                     "intermediate, 22 buckets down to the scalar) as one weighted sum")
     if os.path.exists(f7):
         out["kernels"]["fused_kernel@config3-default"] = dict(summary(f7), workload="config3 default: one fused_kernel launch")
     if y4:
