@@ -399,6 +399,15 @@ __global__ void __launch_bounds__(256, MINB) xt_kernel(const __grid_constant__ Y
 }  // namespace
 
 template <int G, int MINB>
+static int xt_ctas_per_sm(uint32_t stage_bytes) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xt_kernel<G, MINB>, 256, stage_bytes) !=
+      cudaSuccess)
+    per_sm = MINB;
+  return std::max(1, per_sm);
+}
+
+template <int G, int MINB>
 static int launch_xt_g(const YLaunch& L, void* stream) {
   static std::atomic<uint64_t> attr{0};
   if (needs_setup(attr)) {
@@ -417,10 +426,7 @@ static int launch_xt_g(const YLaunch& L, void* stream) {
   int per_sm = 0;
   const char* xc = getenv("QTN_XT_CTAS");
   if (xc) per_sm = atoi(xc);
-  if (per_sm <= 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xt_kernel<G, MINB>, 256,
-                                                                   L.stage_bytes) != cudaSuccess)
-    per_sm = MINB;
-  per_sm = std::max(1, per_sm);
+  if (per_sm <= 0) per_sm = xt_ctas_per_sm<G, MINB>(L.stage_bytes);
   const uint64_t ctas = std::min<uint64_t>(L.total_tiles, (uint64_t)n_sm * (uint64_t)per_sm);
   dim3 grid((uint32_t)ctas, L.n_sets);
   cudaError_t e = launch_pdl<true>(xt_kernel<G, MINB>, grid, dim3(256), L.stage_bytes,
@@ -433,6 +439,21 @@ static int launch_xt_g(const YLaunch& L, void* stream) {
   return QTN_OK;
 }
 
+// The register bound follows the shared-memory bound: a launch whose stages
+// leave room for fewer CTAs per SM than the default build's register budget
+// targets runs the build compiled for that CTA count (more registers, no
+// spills).  QTN_XT_REGS=0: always the default builds.
+template <int G, int MINB>
+static int launch_xt_fit(const YLaunch& L, void* stream) {
+  static const bool fit = [] {
+    const char* e = getenv("QTN_XT_REGS");
+    return !e || atoi(e) != 0;
+  }();
+  if (fit && MINB > 2 && xt_ctas_per_sm<G, MINB>(L.stage_bytes) < MINB)
+    return launch_xt_g<G, MINB - 1>(L, stream);
+  return launch_xt_g<G, MINB>(L, stream);
+}
+
 int launch_xt(const YLaunch& L, void* stream) {
   if (!L.n_items || !L.n_sets || !L.total_tiles) return QTN_OK;
   if (L.n_sets > 65535 || L.total_tiles > 0x7fffffffull) {
@@ -441,8 +462,8 @@ int launch_xt(const YLaunch& L, void* stream) {
   }
   // the launch's items share one group count (level lists are built per g)
   switch (L.g) {
-    case 0: return launch_xt_g<1, XT_MINB1>(L, stream);
-    case 1: return launch_xt_g<2, 3>(L, stream);
+    case 0: return launch_xt_fit<1, XT_MINB1>(L, stream);
+    case 1: return launch_xt_fit<2, 3>(L, stream);
     default: return launch_xt_g<4, 2>(L, stream);
   }
 }
