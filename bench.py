@@ -740,6 +740,46 @@ def sub_records(rig, args, main_cpu):
         return r
 
     guard("config5", c5)
+
+    # the drop-in call itself: contract(network, order) on one network, host
+    # network in, host scalar out (what the reference's own callers see:
+    # bench.py:247, cli.py:108), beside qtnsim.contract on the same network
+    def call_latency():
+        import paper_2106_15740_b200 as Q
+
+        out = {"unit": "ms per contract() call (median of 20 after one warm call)",
+               "api": "contract(network, order): host TensorNetwork -> host complex"}
+        for key, name in (("config2_edge0", "config2"), ("config3_default_edge0", "config3")):
+            wl = dict(WORKLOADS[name], mode="default") if name == "config3" else WORKLOADS[name]
+            g = Q.random_regular_graph(wl["n"], 3, 0)
+            ang = angle_sets(wl["p"], 1)[0]
+            net = Q.build_energy_network(g, g.edges[0], Q.seeded_angles(wl["p"], 0), wl["mode"])
+            order, _ = Q.rgreedy_order(Q.line_graph(net))
+            v = Q.contract(net, order)
+            ts = []
+            for _ in range(20):
+                t0 = time.perf_counter()
+                v = Q.contract(net, order)
+                ts.append(time.perf_counter() - t0)
+            ts.sort()
+            rec = {"ms": ts[len(ts) // 2] * 1e3, "ms_min": ts[0] * 1e3,
+                   "value": [v.real, v.imag]}
+            w = R.prepare(wl["n"], wl["p"], wl["mode"], [0], ang)
+            cv = w.zz(0, ang[:wl["p"]], ang[wl["p"]:])
+            cs = []
+            for _ in range(5):
+                t0 = time.perf_counter()
+                cv = w.zz(0, ang[:wl["p"]], ang[wl["p"]:])
+                cs.append(time.perf_counter() - t0)
+            cs.sort()
+            rec["cpu_baseline"] = {"ms": cs[len(cs) // 2] * 1e3, "cores": 1, "kind": w.kind,
+                                   "sample": "circuit_to_network + contract on the same edge "
+                                             "network, median of 5", "value": [cv.real, cv.imag]}
+            rec["rel_err_vs_cpu"] = abs(v - cv) / max(abs(cv), 1e-300)
+            out[key] = rec
+        return out
+
+    guard("contract_call", call_latency)
     recs["wall_s"] = time.perf_counter() - t_all
     return recs
 

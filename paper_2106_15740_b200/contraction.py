@@ -125,6 +125,11 @@ class ContractionPlan:
         io = np.zeros(max(len(structure), 1), dtype=np.int64)
         N.check(N.lib.qtn_plan_input_offsets(h, N.i64(io)))
         self.input_offsets = io[: len(structure)].copy()
+        sizes = np.array([1 << len(v) for v in structure], dtype=np.int64)
+        ends = self.input_offsets + sizes
+        self._dense = bool(len(structure) and self.input_offsets[0] == 0
+                           and np.array_equal(self.input_offsets[1:], ends[:-1]))
+        self._dense_end = int(ends[-1]) if len(structure) else 0
         self.n_inputs = len(structure)
 
     @classmethod
@@ -141,6 +146,14 @@ class ContractionPlan:
     def pack(self, datas, out: np.ndarray | None = None) -> np.ndarray:
         """Pack sliced tensor data (network order) into the input layout."""
         buf = out if out is not None else np.empty(self.input_elems, dtype=np.complex128)
+        if self._dense and len(datas) == len(self.input_offsets):
+            # tensors lie back to back in network order: one concatenate call
+            try:
+                np.concatenate([np.asarray(d, dtype=np.complex128).reshape(-1) for d in datas],
+                               out=buf[: self._dense_end])
+                return buf
+            except ValueError:  # sizes differ from the structure: per-tensor placement below
+                pass
         for off, d in zip(self.input_offsets, datas):
             flat = np.asarray(d, dtype=np.complex128).reshape(-1)
             buf[off: off + flat.size] = flat
@@ -320,27 +333,37 @@ def _contract_with_ranks(network: TensorNetwork, order: ContractionOrder, rank_c
     unfixed = network.unfixed_variables()
     if sorted(order.sequence) != list(unfixed):
         raise ValueError("order is not a permutation of the network's unfixed variables")
-    sl = sliced_tensors(network)
     import torch
 
-    key = (tuple(t.variables for t in sl), network.variable_count, frozenset(network.fixed),
+    # the unsliced structure and the set of fixed variables determine the
+    # sliced structure (the fixed values only pick the data, network.py:153-165)
+    fx = network.fixed
+    key = (tuple(t.variables for t in network.tensors), network.variable_count, frozenset(fx),
            tuple(order.sequence), int(rank_cap), _dtype_code(dtype), tuple(sorted(kw.items())),
            torch.cuda.current_device() if torch.cuda.is_available() else -1)
     with _RUNS_LOCK:
         run = _RUNS.get(key)
         if run is not None:
             _RUNS.move_to_end(key)
-    if run is None:
-        # RankCapExceeded / ValueError surface here, before any device work
-        plan = ContractionPlan([t.variables for t in sl], network.variable_count, network.fixed,
-                               order.sequence, rank_cap=rank_cap, dtype=dtype, **kw)
-        run = _CachedRun(plan)  # raises without a CUDA device (no CPU fallback)
-        with _RUNS_LOCK:
-            _RUNS[key] = run
-            total = sum(r.device_bytes for r in _RUNS.values())
-            while len(_RUNS) > 1 and (len(_RUNS) > _RUNS_MAX or total > _RUNS_MAX_BYTES):
-                _, old = _RUNS.popitem(last=False)
-                total -= old.device_bytes
+    if run is not None:
+        # known structure: pin the fixed variables on the data only (no Tensor objects)
+        datas = [t.data for t in network.tensors]
+        for k in run.touched:
+            t = network.tensors[k]
+            datas[k] = t.data[tuple(fx[v] if v in fx else slice(None) for v in t.variables)]
+        return run.run(datas), list(run.plan.step_ranks)
+    sl = sliced_tensors(network)
+    # RankCapExceeded / ValueError surface here, before any device work
+    plan = ContractionPlan([t.variables for t in sl], network.variable_count, network.fixed,
+                           order.sequence, rank_cap=rank_cap, dtype=dtype, **kw)
+    run = _CachedRun(plan)  # raises without a CUDA device (no CPU fallback)
+    run.touched = [k for k, t in enumerate(network.tensors) if any(v in fx for v in t.variables)]
+    with _RUNS_LOCK:
+        _RUNS[key] = run
+        total = sum(r.device_bytes for r in _RUNS.values())
+        while len(_RUNS) > 1 and (len(_RUNS) > _RUNS_MAX or total > _RUNS_MAX_BYTES):
+            _, old = _RUNS.popitem(last=False)
+            total -= old.device_bytes
     return run.run([t.data for t in sl]), list(run.plan.step_ranks)
 
 

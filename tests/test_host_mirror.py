@@ -330,3 +330,19 @@ def test_threaded_planning_matches_serial():
         assert x.plan.step_ranks == y.plan.step_ranks
         assert x.plan.program_bytes == y.plan.program_bytes
         assert x.plan.alg_bytes == y.plan.alg_bytes
+
+
+def test_plan_pack_layout_matches_input_offsets():
+    """ContractionPlan.pack (one concatenate when the inputs lie back to back)
+    places tensor k at input_offsets[k], sliced data included
+    (network.py:153-165 slicing, contraction.py:66-73 input list)."""
+    g = Q.random_regular_graph(20, 3, 0)
+    net = Q.build_energy_network(g, g.edges[0], Q.seeded_angles(1, 0), "zz+diagonal")
+    order, _ = Q.rgreedy_order(Q.line_graph(net))
+    plan, sl = Q.ContractionPlan.from_network(net, order)
+    datas = [t.data for t in sl]
+    buf = plan.pack(datas)
+    assert buf.shape == (plan.input_elems,)
+    for off, d in zip(plan.input_offsets, datas):
+        flat = np.asarray(d, dtype=np.complex128).reshape(-1)
+        assert np.array_equal(buf[off: off + flat.size], flat)
