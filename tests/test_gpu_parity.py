@@ -346,6 +346,40 @@ def test_random_circuits_vs_statevector():
                     assert abs(v - want) < 1e-12, (trial, mode, budget)
 
 
+def test_contract_cached_structure_other_outputs_and_data():
+    """One structure, many calls: contract() keeps the compiled plan of a
+    structure and pins the fixed variables on the data only
+    (network.py:153-165).  Every output bitstring of one circuit (same
+    structure, other fixed values) and other gate angles (same structure,
+    other data) against the oracle statevector."""
+    from paper_2106_15740_b200 import contraction as CT
+
+    rng = np.random.default_rng(11)
+    n = 4
+    for rep in range(2):
+        gates, ogates = [], []
+        for k, qs in (("H", (0,)), ("H", (1,)), ("H", (2,)), ("H", (3,)), ("ZZ", (0, 1)), ("ZZ", (1, 2)),
+                      ("CNOT", (2, 3)), ("XPOW", (0,)), ("ZPOW", (3,)), ("ZZ", (0, 3)), ("XPOW", (2,))):
+            t = float(rng.uniform(-3, 3)) if k in ("ZPOW", "XPOW", "ZZ") else None
+            gates.append(Q.Gate(Q.GateKind[k], qs, t))
+            ogates.append((k, qs, t))
+        circ = Q.Circuit(n, tuple(gates), 1.0 + 0.0j)
+        psi = O.statevector(n, ogates, circ.phase)
+        for mode in (Q.NetworkMode.FULL, Q.NetworkMode.DIAGONAL):
+            order = None
+            n_runs = None
+            for b in range(1 << n):
+                bits = format(b, f"0{n}b")
+                net = Q.circuit_to_network(circ, mode, bits)
+                if order is None:
+                    order = Q.greedy_order(Q.line_graph(net))
+                v = Q.contract(net, order)
+                assert abs(v - complex(psi[tuple(int(c) for c in bits)])) < 1e-12, (rep, mode, bits)
+                if n_runs is None:
+                    n_runs = set(CT._RUNS)
+            assert set(CT._RUNS) == n_runs  # the 16 outputs share one compiled plan
+
+
 def test_degenerate_networks():
     """Empty buckets (factor 2), scalar-only networks, a single variable."""
     t0 = Q.Tensor(0, (0,), np.array([1.0, 2.0 + 1j]))
