@@ -224,6 +224,16 @@ int qtn_batch_execute_angles(qtn_batch* batch, const double* angles_dev, int32_t
 int qtn_energy_reduce(const void* values_dev, const double* weights_dev, int32_t n,
                       int32_t n_sets, double* energies_dev, void* zz_sum_dev, void* stream);
 
+/* Host-to-host contraction of one set of packed inputs, the drop-in
+ * `contract` call (contraction.py:114-123) on a kept batch: copy input_bytes
+ * from inputs_pinned (page-locked host memory, the packed layout of
+ * qtn_batch_input_offsets) to inputs_dev, run qtn_batch_execute for one set
+ * on `stream`, copy the batch's n complex128 results to results_pinned and
+ * wait for the stream. */
+int qtn_batch_execute_host(qtn_batch* batch, const void* inputs_pinned, int64_t input_bytes,
+                           void* inputs_dev, void* workspace, void* results_dev,
+                           void* results_pinned, void* stream);
+
 /* Host-to-host energy evaluation, the QAOA optimiser's call: copy n_sets
  * angle vectors from host memory (any host pointer; staged through pinned
  * memory owned by the batch) to angles_dev, run qtn_batch_execute_angles and

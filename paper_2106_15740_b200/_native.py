@@ -97,6 +97,7 @@ _SIGNATURES = {
     "qtn_batch_launches": [_p, C.c_int32, _i32p],
     "qtn_batch_uses_setmajor": [_p, C.c_int32, _i32p],
     "qtn_batch_setmajor_elem_bytes": [_p, C.c_int32, _i32p],
+    "qtn_batch_execute_host": [_p, _p, C.c_int64, _p, _p, _p, _p, _p],
     "qtn_batch_energies_host": [_p, _p, C.c_int32, C.c_int32, _p, _p, _p, _p, _p, _p, _p, _p],
     "qtn_batch_execute": [_p, _p, C.c_int64, C.c_int32, _p, _p, _p],
     "qtn_batch_destroy": [_p],

@@ -1372,6 +1372,28 @@ extern "C" int qtn_batch_execute(qtn_batch* B, const void* inputs, int64_t set_s
   return run_batch(B, inputs, set_stride, nullptr, 0, n_sets, workspace, results, stream);
 }
 
+// Host-to-host contraction of one set of packed inputs (the drop-in
+// contract() call): H2D from the caller's pinned buffer, the evaluation, D2H
+// of the n results and the stream wait in one native call.
+extern "C" int qtn_batch_execute_host(qtn_batch* B, const void* inputs_pinned, int64_t input_bytes,
+                                      void* inputs_dev, void* workspace, void* results_dev,
+                                      void* results_pinned, void* stream) {
+  if (!B || !inputs_pinned || !inputs_dev || !results_dev || !results_pinned || input_bytes < 0) {
+    set_error("qtn_batch_execute_host: bad arguments");
+    return QTN_EINVAL;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(inputs_dev, inputs_pinned, (size_t)input_bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "inputs H2D");
+  const int rc = run_batch(B, inputs_dev, 0, nullptr, 0, 1, workspace, results_dev, stream);
+  if (rc) return rc;
+  e = cudaMemcpyAsync(results_pinned, results_dev, (size_t)B->n * sizeof(double2), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(e, "results D2H");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "execute_host sync");
+  return QTN_OK;
+}
+
 extern "C" int qtn_batch_set_recipes(qtn_batch* B, const qtn_tensor_recipe* rec,
                                      const int64_t* offsets) {
   if (!B || !rec || !offsets) {
