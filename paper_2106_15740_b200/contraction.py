@@ -149,11 +149,11 @@ class ContractionPlan:
         if self._dense and len(datas) == len(self.input_offsets):
             # tensors lie back to back in network order: one concatenate call
             try:
-                np.concatenate([np.asarray(d, dtype=np.complex128).reshape(-1) for d in datas],
-                               out=buf[: self._dense_end])
+                # (Tensor.data is always an ndarray; concatenate casts other dtypes into buf)
+                np.concatenate([d.ravel() for d in datas], out=buf[: self._dense_end])
                 return buf
-            except ValueError:  # sizes differ from the structure: per-tensor placement below
-                pass
+            except (ValueError, AttributeError, TypeError):
+                pass  # not arrays, or sizes differ from the structure: per-tensor placement below
         for off, d in zip(self.input_offsets, datas):
             flat = np.asarray(d, dtype=np.complex128).reshape(-1)
             buf[off: off + flat.size] = flat
